@@ -1,0 +1,126 @@
+/*
+ * tsg.h -- C ABI of the B200-native two-phase SpGEMM ("tiered SpGEMM").
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/tiered_spgemm/kernel.py, chunking.py).  The
+ * reference is pure Python with no FFI of its own; the binding a maintainer
+ * would add is the ctypes stub shown in INTEGRATION.md, which is exactly what
+ * paper_1804_00695_b200/_lib.py does.  Signatures use plain pointers and
+ * sizes only: host arrays are the reference's int64 / float64 / uint64
+ * numpy buffers, device objects are opaque handles owned by the library.
+ *
+ * Every entry point returns a status code; the message of the last failure
+ * on the calling thread is available from tsg_last_error().  Codes map to the
+ * reference's exception classes (errors.py:4-45):
+ *   TSG_EDIM      -> DimensionError
+ *   TSG_EVALID    -> MatrixValidationError
+ *   TSG_EKERNEL   -> KernelError   (count mismatch, probe overflow)
+ *   TSG_ECAPACITY -> CapacityError (HBM budget)
+ *   TSG_EUNSPLIT  -> UnsplittableRowError
+ *   TSG_ECUDA     -> KernelError   (CUDA runtime failure, message attached)
+ *   TSG_EARG      -> ValueError
+ *
+ * Threading: a context owns one compute stream and two copy streams on one
+ * device; it is not thread-safe.  Use one context per GPU.
+ */
+#ifndef TSG_H
+#define TSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_OK 0
+#define TSG_EDIM 1
+#define TSG_EVALID 2
+#define TSG_EKERNEL 3
+#define TSG_ECAPACITY 4
+#define TSG_EUNSPLIT 5
+#define TSG_ECUDA 6
+#define TSG_EARG 7
+
+#define TSG_ABI_VERSION 1
+
+typedef struct tsg_ctx tsg_ctx;   /* device, streams, scratch, error flag        */
+typedef struct tsg_csr tsg_csr;   /* device CSR: int64 offsets, int32 cols, f64  */
+typedef struct tsg_cmat tsg_cmat; /* device compressed (set, 64-bit mask) rows   */
+typedef struct tsg_vec tsg_vec;   /* device int64 vector (+ per-row set counts)  */
+
+/* ---- library / context -------------------------------------------------- */
+const char *tsg_last_error(void);
+int tsg_abi_version(void);
+int tsg_device_count(int *count);
+int tsg_init(int device, tsg_ctx **out);
+int tsg_destroy(tsg_ctx *ctx);
+int tsg_sync(tsg_ctx *ctx);
+/* Bytes of device memory currently held by the context's allocations. */
+int tsg_mem_in_use(tsg_ctx *ctx, int64_t *bytes);
+/* Per-phase device times (ms) of the last multiply-type call:
+   [0] bounds+bins [1] compress [2] symbolic [3] scan [4] numeric [5] total */
+int tsg_last_phase_ms(tsg_ctx *ctx, float *out, int n);
+int tsg_set_timing(tsg_ctx *ctx, int enabled);
+
+/* ---- CSR operands (csr.py:32-106 CsrMatrix) ------------------------------ */
+/* values may be NULL (pattern).  Columns must be < 2^31 (device int32). */
+int tsg_csr_upload(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,
+                   const int64_t *row_ptr, const int64_t *col_idx,
+                   const double *values, tsg_csr **out);
+int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int64_t *nnz,
+                 int *has_values);
+/* Host buffers sized rows+1 / nnz / nnz (values may be NULL to skip). */
+int tsg_csr_download(tsg_ctx *ctx, const tsg_csr *m, int64_t *row_ptr,
+                     int64_t *col_idx, double *values);
+/* Rows [begin, end) as a new rebased device CSR (csr.py:187-195 slice_rows). */
+int tsg_csr_slice_rows(tsg_ctx *ctx, const tsg_csr *m, int64_t begin,
+                       int64_t end, tsg_csr **out);
+int tsg_csr_free(tsg_ctx *ctx, tsg_csr *m);
+
+/* ---- compressed form (kernel.py:52-93 CompressedMatrix / compress) ------- */
+/* Sets are emitted in first-touch order per row, as the reference does. */
+int tsg_compress(tsg_ctx *ctx, const tsg_csr *b, tsg_cmat **out);
+int tsg_cmat_info(tsg_ctx *ctx, const tsg_cmat *cm, int64_t *rows,
+                  int64_t *n_sets);
+int tsg_cmat_download(tsg_ctx *ctx, const tsg_cmat *cm, int64_t *row_ptr,
+                      int64_t *set_idx, uint64_t *set_bits);
+int tsg_cmat_upload(tsg_ctx *ctx, int64_t rows, int64_t n_sets,
+                    const int64_t *row_ptr, const int64_t *set_idx,
+                    const uint64_t *set_bits, tsg_cmat **out);
+int tsg_cmat_free(tsg_ctx *ctx, tsg_cmat *cm);
+
+/* ---- int64 vectors (symbolic counts) ------------------------------------- */
+int tsg_vec_upload(tsg_ctx *ctx, int64_t n, const int64_t *host, tsg_vec **out);
+int tsg_vec_download(tsg_ctx *ctx, const tsg_vec *v, int64_t *host);
+int tsg_vec_len(const tsg_vec *v, int64_t *n);
+int tsg_vec_free(tsg_ctx *ctx, tsg_vec *v);
+
+/* ---- the hot path ---------------------------------------------------------- */
+/* kernel.py:96-103 count_multiplications */
+int tsg_count_multiplications(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b,
+                              int64_t *total);
+/* kernel.py:124-168 spgemm_symbolic: exact nnz per row of A*B. */
+int tsg_symbolic(tsg_ctx *ctx, const tsg_csr *a, const tsg_cmat *cb,
+                 tsg_vec **counts);
+/* kernel.py:171-232 spgemm_numeric.  cb may be NULL (compressed on the fly).
+   C rows come out with ascending columns (the reference's are first-touch;
+   canonical forms are identical).  TSG_EKERNEL if counts are wrong. */
+int tsg_numeric(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b,
+                const tsg_cmat *cb, const tsg_vec *counts, tsg_csr **c);
+/* kernel.py:343-346 multiply = compress + symbolic + numeric, all on device. */
+int tsg_multiply(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b, tsg_csr **c);
+/* kernel.py:235-340 spgemm_numeric_fused:
+   out = c_partial + A[a_lo:a_hi, b_lo:b_hi] * b_chunk  (b_chunk rebased). */
+int tsg_numeric_fused(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b_chunk,
+                      const tsg_csr *c_partial, int64_t a_lo, int64_t a_hi,
+                      int64_t b_lo, int64_t b_hi, tsg_csr **out);
+/* kernel.py:349-394 masked_row_intersect_count (TSG_EVALID if L is not
+   strictly lower triangular). */
+int tsg_masked_count(tsg_ctx *ctx, const tsg_csr *l, const tsg_cmat *cl,
+                     int64_t *total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSG_H */

@@ -1,0 +1,308 @@
+"""ctypes binding of libtsg.so (include/tsg.h) and device-resident handles.
+
+This is the stub a maintainer would add to the reference to bind the C ABI
+(INTEGRATION.md shows it next to the reference call sites).  There is no CPU
+fallback: if the library or a B200 is missing, every entry point raises
+KernelError.  Status codes map to the reference's exception classes
+(errors.py:4-45).
+"""
+
+import ctypes
+import os
+import threading
+import weakref
+
+import numpy as np
+
+from .csr import CsrMatrix
+from .errors import (CapacityError, DimensionError, KernelError,
+                     MatrixValidationError, UnsplittableRowError)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsg.so")
+
+TSG_OK, TSG_EDIM, TSG_EVALID, TSG_EKERNEL, TSG_ECAPACITY, TSG_EUNSPLIT, TSG_ECUDA, TSG_EARG = range(8)
+
+_ERRORS = {
+    TSG_EDIM: DimensionError,
+    TSG_EVALID: MatrixValidationError,
+    TSG_EKERNEL: KernelError,
+    TSG_ECAPACITY: CapacityError,
+    TSG_EUNSPLIT: UnsplittableRowError,
+    TSG_ECUDA: KernelError,
+    TSG_EARG: ValueError,
+}
+
+# every symbol include/tsg.h declares (checked by tests/test_boundary.py)
+EXPORTS = (
+    "tsg_last_error", "tsg_abi_version", "tsg_device_count", "tsg_init", "tsg_destroy",
+    "tsg_sync", "tsg_mem_in_use", "tsg_last_phase_ms", "tsg_set_timing",
+    "tsg_csr_upload", "tsg_csr_info", "tsg_csr_download", "tsg_csr_slice_rows", "tsg_csr_free",
+    "tsg_compress", "tsg_cmat_info", "tsg_cmat_download", "tsg_cmat_upload", "tsg_cmat_free",
+    "tsg_vec_upload", "tsg_vec_download", "tsg_vec_len", "tsg_vec_free",
+    "tsg_count_multiplications", "tsg_symbolic", "tsg_numeric", "tsg_multiply",
+    "tsg_numeric_fused", "tsg_masked_count",
+)
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+_PP = ctypes.POINTER(ctypes.c_void_p)
+
+_SIGS = {
+    "tsg_last_error": ([], ctypes.c_char_p),
+    "tsg_abi_version": ([], ctypes.c_int),
+    "tsg_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tsg_init": ([ctypes.c_int, _PP], ctypes.c_int),
+    "tsg_destroy": ([_P], ctypes.c_int),
+    "tsg_sync": ([_P], ctypes.c_int),
+    "tsg_mem_in_use": ([_P, _PI64], ctypes.c_int),
+    "tsg_last_phase_ms": ([_P, ctypes.POINTER(ctypes.c_float), ctypes.c_int], ctypes.c_int),
+    "tsg_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
+    "tsg_csr_upload": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
+    "tsg_csr_info": ([_P, _PI64, _PI64, _PI64, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tsg_csr_download": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "tsg_csr_slice_rows": ([_P, _P, _I64, _I64, _PP], ctypes.c_int),
+    "tsg_csr_free": ([_P, _P], ctypes.c_int),
+    "tsg_compress": ([_P, _P, _PP], ctypes.c_int),
+    "tsg_cmat_info": ([_P, _P, _PI64, _PI64], ctypes.c_int),
+    "tsg_cmat_download": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "tsg_cmat_upload": ([_P, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
+    "tsg_cmat_free": ([_P, _P], ctypes.c_int),
+    "tsg_vec_upload": ([_P, _I64, _P, _PP], ctypes.c_int),
+    "tsg_vec_download": ([_P, _P, _P], ctypes.c_int),
+    "tsg_vec_len": ([_P, _PI64], ctypes.c_int),
+    "tsg_vec_free": ([_P, _P], ctypes.c_int),
+    "tsg_count_multiplications": ([_P, _P, _P, _PI64], ctypes.c_int),
+    "tsg_symbolic": ([_P, _P, _P, _PP], ctypes.c_int),
+    "tsg_numeric": ([_P, _P, _P, _P, _P, _PP], ctypes.c_int),
+    "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
+    "tsg_numeric_fused": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _PP], ctypes.c_int),
+    "tsg_masked_count": ([_P, _P, _P, _PI64], ctypes.c_int),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """Load libtsg.so (raises KernelError if it was never built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise KernelError("libtsg.so is not built (run __graft_entry__.build()); "
+                                  "there is no CPU fallback")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def check(status):
+    if status == TSG_OK:
+        return
+    msg = load().tsg_last_error().decode(errors="replace")
+    raise _ERRORS.get(status, KernelError)(msg)
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class Context:
+    """One CUDA device: compute stream + copy streams inside libtsg."""
+
+    _instances = {}
+
+    def __init__(self, device=0):
+        self.device = device
+        h = ctypes.c_void_p()
+        check(load().tsg_init(device, ctypes.byref(h)))
+        self.h = h
+
+    @classmethod
+    def get(cls, device=None):
+        if device is None:
+            device = int(os.environ.get("TSG_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+            n = ctypes.c_int(0)
+            check(load().tsg_device_count(ctypes.byref(n)))
+            if n.value == 0:
+                raise KernelError("no CUDA device visible; libtsg has no CPU fallback")
+            device = device % n.value
+        ctx = cls._instances.get(device)
+        if ctx is None:
+            ctx = cls._instances[device] = Context(device)
+        return ctx
+
+    def sync(self):
+        check(load().tsg_sync(self.h))
+
+    def set_timing(self, on=True):
+        check(load().tsg_set_timing(self.h, 1 if on else 0))
+
+    def phase_ms(self):
+        out = (ctypes.c_float * 8)()
+        check(load().tsg_last_phase_ms(self.h, out, 8))
+        return list(out)
+
+    def mem_in_use(self):
+        v = ctypes.c_int64(0)
+        check(load().tsg_mem_in_use(self.h, ctypes.byref(v)))
+        return v.value
+
+
+class _Handle:
+    _free_fn = None
+
+    def __init__(self, ctx, h):
+        self.ctx = ctx
+        self.h = h
+        self._fin = weakref.finalize(self, _Handle._release, self._free_fn, ctx, h)
+
+    @staticmethod
+    def _release(fname, ctx, h):
+        try:
+            getattr(load(), fname)(ctx.h, h)
+        except Exception:  # interpreter shutdown
+            pass
+
+    def free(self):
+        self._fin()
+
+
+class DeviceCsr(_Handle):
+    """CSR matrix resident in HBM (int64 offsets, int32 columns, fp64 values)."""
+
+    _free_fn = "tsg_csr_free"
+
+    def __init__(self, ctx, h):
+        super().__init__(ctx, h)
+        r, c, n, hv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        check(load().tsg_csr_info(h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(n), ctypes.byref(hv)))
+        self.num_rows, self.num_cols, self.nnz, self.has_values = r.value, c.value, n.value, bool(hv.value)
+
+    @classmethod
+    def upload(cls, m, ctx=None):
+        ctx = ctx or Context.get()
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(m.col_idx, dtype=np.int64)
+        va = None if m.values is None else np.ascontiguousarray(m.values, dtype=np.float64)
+        if rp.shape[0] != m.num_rows + 1:
+            raise MatrixValidationError("row_ptr length must be num_rows + 1")
+        h = ctypes.c_void_p()
+        check(load().tsg_csr_upload(ctx.h, m.num_rows, m.num_cols, ci.shape[0], _ptr(rp), _ptr(ci),
+                                    _ptr(va), ctypes.byref(h)))
+        return cls(ctx, h)
+
+    def download(self) -> CsrMatrix:
+        rp = np.empty(self.num_rows + 1, dtype=np.int64)
+        ci = np.empty(self.nnz, dtype=np.int64)
+        va = np.empty(self.nnz, dtype=np.float64) if self.has_values else None
+        check(load().tsg_csr_download(self.ctx.h, self.h, _ptr(rp), _ptr(ci), _ptr(va)))
+        return CsrMatrix._adopt(self.num_rows, self.num_cols, rp, ci, va)
+
+    def slice_rows(self, begin, end):
+        h = ctypes.c_void_p()
+        check(load().tsg_csr_slice_rows(self.ctx.h, self.h, begin, end, ctypes.byref(h)))
+        return DeviceCsr(self.ctx, h)
+
+
+class DeviceCompressed(_Handle):
+    _free_fn = "tsg_cmat_free"
+
+    def __init__(self, ctx, h, rows):
+        super().__init__(ctx, h)
+        self.num_rows = rows
+
+    @classmethod
+    def upload(cls, cm, ctx=None):
+        ctx = ctx or Context.get()
+        rp = np.ascontiguousarray(cm.row_ptr, dtype=np.int64)
+        si = np.ascontiguousarray(cm.set_idx, dtype=np.int64)
+        sb = np.ascontiguousarray(cm.set_bits, dtype=np.uint64)
+        h = ctypes.c_void_p()
+        check(load().tsg_cmat_upload(ctx.h, cm.num_rows, si.shape[0], _ptr(rp), _ptr(si), _ptr(sb),
+                                     ctypes.byref(h)))
+        return cls(ctx, h, cm.num_rows)
+
+    def download(self):
+        r, n = ctypes.c_int64(), ctypes.c_int64()
+        check(load().tsg_cmat_info(self.ctx.h, self.h, ctypes.byref(r), ctypes.byref(n)))
+        rp = np.empty(self.num_rows + 1, dtype=np.int64)
+        si = np.empty(n.value, dtype=np.int64)
+        sb = np.empty(n.value, dtype=np.uint64)
+        check(load().tsg_cmat_download(self.ctx.h, self.h, _ptr(rp), _ptr(si), _ptr(sb)))
+        return rp, si, sb
+
+
+class DeviceVec(_Handle):
+    _free_fn = "tsg_vec_free"
+
+    def __init__(self, ctx, h):
+        super().__init__(ctx, h)
+        n = ctypes.c_int64()
+        check(load().tsg_vec_len(h, ctypes.byref(n)))
+        self.n = n.value
+
+    @classmethod
+    def upload(cls, arr, ctx=None):
+        ctx = ctx or Context.get()
+        a = np.ascontiguousarray(arr, dtype=np.int64)
+        h = ctypes.c_void_p()
+        check(load().tsg_vec_upload(ctx.h, a.shape[0], _ptr(a), ctypes.byref(h)))
+        return cls(ctx, h)
+
+    def download(self):
+        out = np.empty(self.n, dtype=np.int64)
+        check(load().tsg_vec_download(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+
+# ---- raw calls on device handles ---------------------------------------------
+
+def d_compress(db: DeviceCsr) -> DeviceCompressed:
+    h = ctypes.c_void_p()
+    check(load().tsg_compress(db.ctx.h, db.h, ctypes.byref(h)))
+    return DeviceCompressed(db.ctx, h, db.num_rows)
+
+
+def d_count_multiplications(da, db) -> int:
+    v = ctypes.c_int64()
+    check(load().tsg_count_multiplications(da.ctx.h, da.h, db.h, ctypes.byref(v)))
+    return v.value
+
+
+def d_symbolic(da, dcb) -> DeviceVec:
+    h = ctypes.c_void_p()
+    check(load().tsg_symbolic(da.ctx.h, da.h, dcb.h, ctypes.byref(h)))
+    return DeviceVec(da.ctx, h)
+
+
+def d_numeric(da, db, dcb, dcounts) -> DeviceCsr:
+    h = ctypes.c_void_p()
+    check(load().tsg_numeric(da.ctx.h, da.h, db.h, None if dcb is None else dcb.h, dcounts.h,
+                             ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)
+
+
+def d_multiply(da, db) -> DeviceCsr:
+    h = ctypes.c_void_p()
+    check(load().tsg_multiply(da.ctx.h, da.h, db.h, ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)
+
+
+def d_numeric_fused(da, dbc, dcp, a_lo, a_hi, b_lo, b_hi) -> DeviceCsr:
+    h = ctypes.c_void_p()
+    check(load().tsg_numeric_fused(da.ctx.h, da.h, dbc.h, dcp.h, a_lo, a_hi, b_lo, b_hi,
+                                   ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)
+
+
+def d_masked_count(dl, dcl) -> int:
+    v = ctypes.c_int64()
+    check(load().tsg_masked_count(dl.ctx.h, dl.h, dcl.h, ctypes.byref(v)))
+    return v.value

@@ -1,0 +1,545 @@
+// tsg_core.cu -- context, device memory, scans, operand upload/download.
+//
+// Host<->device conversion of the reference's int64 column arrays happens on
+// the device (int64 staging -> int32 device columns on upload, the reverse on
+// download) so the host never runs an O(nnz) numpy conversion.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "tsg_internal.cuh"
+
+static thread_local char g_err[1024] = "";
+
+void tsg_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int tsg_cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    tsg_set_error("CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    return TSG_ECUDA;
+}
+
+extern "C" const char *tsg_last_error(void) { return g_err; }
+extern "C" int tsg_abi_version(void) { return TSG_ABI_VERSION; }
+
+extern "C" int tsg_device_count(int *count) {
+    TSG_CK(cudaGetDeviceCount(count));
+    return TSG_OK;
+}
+
+// ------------------------------------------------------------------ context
+
+extern "C" int tsg_init(int device, tsg_ctx **out) {
+    if (!out) { tsg_set_error("null output handle"); return TSG_EARG; }
+    int n = 0;
+    TSG_CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) {
+        tsg_set_error("device %d not present (%d visible)", device, n);
+        return TSG_EARG;
+    }
+    TSG_CK(cudaSetDevice(device));
+    tsg_ctx *c = new tsg_ctx();
+    memset(c, 0, sizeof(*c));
+    c->device = device;
+    cudaDeviceProp prop;
+    TSG_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        tsg_set_error("libtsg is built for sm_100a (B200); device %d is sm_%d%d", device,
+                      prop.major, prop.minor);
+        delete c;
+        return TSG_ECUDA;
+    }
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    TSG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    TSG_CK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+    TSG_CK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    // keep freed blocks cached in the default pool: no OS round trips per call
+    cudaMemPool_t pool;
+    TSG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    TSG_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    TSG_CK(cudaMalloc(&c->d_err, 4 * sizeof(int)));
+    TSG_CK(cudaMemset(c->d_err, 0, 4 * sizeof(int)));
+    TSG_CK(cudaMalloc(&c->d_small, 64 * sizeof(int64_t)));
+    TSG_CK(cudaMallocHost(&c->h_small, 64 * sizeof(int64_t)));
+    int init_err[2] = {0, 0x7fffffff};
+    TSG_CK(cudaMemcpy(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice));
+    for (int i = 0; i < 8; i++) TSG_CK(cudaEventCreate(&c->ev[i]));
+    c->timing = 0;
+    *out = c;
+    return TSG_OK;
+}
+
+extern "C" int tsg_destroy(tsg_ctx *c) {
+    if (!c) return TSG_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
+    cudaFree(c->d_err);
+    cudaFree(c->d_small);
+    cudaFreeHost(c->h_small);
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->copy_in);
+    cudaStreamDestroy(c->copy_out);
+    delete c;
+    return TSG_OK;
+}
+
+extern "C" int tsg_sync(tsg_ctx *c) {
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    return TSG_OK;
+}
+
+extern "C" int tsg_mem_in_use(tsg_ctx *c, int64_t *bytes) {
+    *bytes = c->bytes_in_use;
+    return TSG_OK;
+}
+
+extern "C" int tsg_set_timing(tsg_ctx *c, int enabled) {
+    c->timing = enabled ? 1 : 0;
+    return TSG_OK;
+}
+
+extern "C" int tsg_last_phase_ms(tsg_ctx *c, float *out, int n) {
+    for (int i = 0; i < n && i < 8; i++) out[i] = c->phase_ms[i];
+    return TSG_OK;
+}
+
+void PhaseTimer::finish(int total_slot) {
+    if (!ctx->timing || n < 2) return;
+    cudaEventSynchronize(ctx->ev[n - 1]);
+    for (int i = 0; i + 1 < n && i < 8; i++)
+        cudaEventElapsedTime(&ctx->phase_ms[i], ctx->ev[i], ctx->ev[i + 1]);
+    if (total_slot < 8) cudaEventElapsedTime(&ctx->phase_ms[total_slot], ctx->ev[0], ctx->ev[n - 1]);
+}
+
+// ------------------------------------------------------------------ memory
+// Stream-ordered allocation from the device's default pool (release threshold
+// raised in tsg_init, so steady-state calls never reach the OS).  Sizes are
+// tracked host-side so tsg_mem_in_use reports the context's footprint.
+
+static std::mutex g_alloc_mu;
+static std::unordered_map<void *, size_t> g_alloc_sizes;
+
+int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~(size_t)255;
+    void *raw = nullptr;
+    cudaError_t e = cudaMallocAsync(&raw, bytes, c->stream);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        tsg_set_error("device allocation of %zu bytes failed (out of HBM)", bytes);
+        return TSG_ECAPACITY;
+    }
+    if (e != cudaSuccess) return tsg_cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
+    {
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        g_alloc_sizes[raw] = bytes;
+        c->bytes_in_use += (int64_t)bytes;
+    }
+    *p = raw;
+    return TSG_OK;
+}
+
+int tsg_free(tsg_ctx *c, void *p) {
+    if (!p) return TSG_OK;
+    {
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        auto it = g_alloc_sizes.find(p);
+        if (it != g_alloc_sizes.end()) {
+            c->bytes_in_use -= (int64_t)it->second;
+            g_alloc_sizes.erase(it);
+        }
+    }
+    TSG_CK(cudaFreeAsync(p, c->stream));
+    return TSG_OK;
+}
+
+int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
+    int h[2];
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaMemcpyAsync(h, c->d_err, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    if (h[0] == KERR_NONE) return TSG_OK;
+    int init_err[2] = {0, 0x7fffffff};
+    TSG_CK(cudaMemcpyAsync(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    switch (h[0]) {
+    case KERR_COUNT:
+        tsg_set_error("%s: row %d: symbolic count disagrees with the entries accumulated", phase, h[1]);
+        return TSG_EKERNEL;
+    case KERR_PROBE:
+        tsg_set_error("%s: row %d: accumulator probe overflow (table full)", phase, h[1]);
+        return TSG_EKERNEL;
+    case KERR_NOTLOWER:
+        tsg_set_error("row %d has a column >= its row: not strictly lower triangular", h[1]);
+        return TSG_EVALID;
+    case KERR_COLRANGE:
+        tsg_set_error("%s: column index out of range in row %d", phase, h[1]);
+        return TSG_EVALID;
+    default:
+        tsg_set_error("%s: internal kernel error %d at row %d", phase, h[0], h[1]);
+        return TSG_EKERNEL;
+    }
+}
+
+// ------------------------------------------------------------------ scan
+// Three-phase exclusive scan: tile sums -> scan of tile sums -> tile scan.
+
+namespace {
+constexpr int SCAN_BS = 256;
+constexpr int SCAN_IT = 8;
+constexpr int SCAN_TILE = SCAN_BS * SCAN_IT;
+
+template <typename TI>
+__global__ void scan_tile_sums(const TI *__restrict__ in, int64_t n, int64_t *__restrict__ sums) {
+    __shared__ int64_t ws[SCAN_BS / 32];
+    int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_IT; k++) {
+        int64_t i = base + (int64_t)k * SCAN_BS + threadIdx.x;
+        if (i < n) s += (int64_t)in[i];
+    }
+    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < SCAN_BS / 32; w++) t += ws[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+// single block: exclusive scan of m tile sums in place, total into sums[m]
+__global__ void scan_sums_single(int64_t *sums, int64_t m) {
+    __shared__ int64_t ws[32];
+    __shared__ int64_t carry_s;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < m; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int64_t v = i < m ? sums[i] : 0;
+        int64_t x = v;
+        int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int d = 1; d < 32; d <<= 1) {
+            int64_t o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        if (lane == 31) ws[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int64_t y = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+            for (int d = 1; d < 32; d <<= 1) {
+                int64_t o = __shfl_up_sync(0xffffffffu, y, d);
+                if (lane >= d) y += o;
+            }
+            ws[lane] = y;
+        }
+        __syncthreads();
+        int64_t incl = x + (w > 0 ? ws[w - 1] : 0);
+        int64_t carry = carry_s;
+        if (i < m) sums[i] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry_s = carry + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[m] = carry_s;
+}
+
+template <typename TI>
+__global__ void scan_tiles(const TI *__restrict__ in, int64_t n, const int64_t *__restrict__ sums,
+                           int64_t *__restrict__ out) {
+    __shared__ int64_t ws[SCAN_BS / 32];
+    int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IT;
+    int64_t v[SCAN_IT];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_IT; k++) {
+        int64_t i = base + k;
+        v[k] = i < n ? (int64_t)in[i] : 0;
+        s += v[k];
+    }
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t x = s;
+    for (int d = 1; d < 32; d <<= 1) {
+        int64_t o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    int64_t woff = 0;
+    for (int j = 0; j < w; j++) woff += ws[j];
+    int64_t run = sums[blockIdx.x] + woff + x - s;
+#pragma unroll
+    for (int k = 0; k < SCAN_IT; k++) {
+        int64_t i = base + k;
+        if (i < n) out[i] = run;
+        run += v[k];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+}
+
+template <typename TI>
+int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
+    if (n == 0) {
+        TSG_CK(cudaMemsetAsync(out, 0, sizeof(int64_t), c->stream));
+        return TSG_OK;
+    }
+    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t *sums = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &sums, tiles + 1));
+    scan_tile_sums<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums);
+    scan_sums_single<<<1, 1024, 0, c->stream>>>(sums, tiles);
+    // in-place safe: every tile reads its inputs into registers before writing,
+    // and tiles write only their own range (plus out[n], past every input).
+    scan_tiles<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums, out);
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_free(c, sums));
+    return TSG_OK;
+}
+}  // namespace
+
+int tsg_exclusive_scan_i64(tsg_ctx *c, const int64_t *in, int64_t *out, int64_t n) {
+    return scan_impl<int64_t>(c, in, out, n);
+}
+
+int tsg_exclusive_scan_i32_to_i64(tsg_ctx *c, const int32_t *in, int64_t *out, int64_t n) {
+    return scan_impl<int32_t>(c, in, out, n);
+}
+
+// ------------------------------------------------------------------ objects
+
+int tsg_csr_alloc(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz, bool values,
+                  tsg_csr **out) {
+    tsg_csr *m = new tsg_csr();
+    m->rows = rows;
+    m->cols = cols;
+    m->nnz = nnz;
+    m->rp = nullptr;
+    m->col = nullptr;
+    m->val = nullptr;
+    int s = tsg_alloc_t(c, &m->rp, rows + 1);
+    if (s == TSG_OK) s = tsg_alloc_t(c, &m->col, nnz);
+    if (s == TSG_OK && values) s = tsg_alloc_t(c, &m->val, nnz);
+    if (s != TSG_OK) {
+        tsg_free(c, m->rp);
+        tsg_free(c, m->col);
+        tsg_free(c, m->val);
+        delete m;
+        return s;
+    }
+    *out = m;
+    return TSG_OK;
+}
+
+int tsg_vec_alloc(tsg_ctx *c, int64_t n, bool aux, tsg_vec **out) {
+    tsg_vec *v = new tsg_vec();
+    v->n = n;
+    v->d = nullptr;
+    v->aux = nullptr;
+    int s = tsg_alloc_t(c, &v->d, n + 1);
+    if (s == TSG_OK && aux) s = tsg_alloc_t(c, &v->aux, n + 1);
+    if (s != TSG_OK) {
+        tsg_free(c, v->d);
+        delete v;
+        return s;
+    }
+    *out = v;
+    return TSG_OK;
+}
+
+int tsg_cmat_alloc(tsg_ctx *c, int64_t rows, int64_t cap, tsg_cmat **out) {
+    tsg_cmat *m = new tsg_cmat();
+    m->rows = rows;
+    m->cap = cap;
+    m->start = nullptr;
+    m->cnt = nullptr;
+    m->set = nullptr;
+    m->bits = nullptr;
+    int s = tsg_alloc_t(c, &m->start, rows + 1);
+    if (s == TSG_OK) s = tsg_alloc_t(c, &m->cnt, rows + 1);
+    if (s == TSG_OK) s = tsg_alloc_t(c, &m->set, cap);
+    if (s == TSG_OK) s = tsg_alloc_t(c, &m->bits, cap);
+    if (s != TSG_OK) {
+        tsg_free(c, m->start);
+        tsg_free(c, m->cnt);
+        tsg_free(c, m->set);
+        delete m;
+        return s;
+    }
+    *out = m;
+    return TSG_OK;
+}
+
+// ------------------------------------------------------------------ CSR I/O
+
+namespace {
+__global__ void cols_i64_to_i32(const int64_t *__restrict__ in, int32_t *__restrict__ out,
+                                int64_t n, int64_t ncols, int *err) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = in[i];
+        if (v < 0 || v >= ncols) {
+            kerr(err, KERR_COLRANGE, i);
+            v = 0;
+        }
+        out[i] = (int32_t)v;
+    }
+}
+
+__global__ void cols_i32_to_i64(const int32_t *__restrict__ in, int64_t *__restrict__ out,
+                                int64_t n, int64_t add) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i] + add;
+}
+
+__global__ void rebase_rp(const int64_t *__restrict__ in, int64_t *__restrict__ out, int64_t n) {
+    int64_t base = in[0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] - base;
+}
+}  // namespace
+
+static unsigned ew_grid(tsg_ctx *c, int64_t n) { return grid_for(n, 256, c->num_sms * 16); }
+
+extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
+                              const int64_t *row_ptr, const int64_t *col_idx,
+                              const double *values, tsg_csr **out) {
+    if (rows < 0 || cols < 0 || nnz < 0) {
+        tsg_set_error("negative dimensions");
+        return TSG_EVALID;
+    }
+    if (cols > 0x7fffffffLL) {
+        tsg_set_error("%lld columns exceed the device int32 column index", (long long)cols);
+        return TSG_EDIM;
+    }
+    tsg_csr *m = nullptr;
+    TSG_TRY(tsg_csr_alloc(c, rows, cols, nnz, values != nullptr, &m));
+    TSG_CK(cudaMemcpyAsync(m->rp, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                           c->stream));
+    if (nnz > 0) {
+        int64_t *stage = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &stage, nnz));
+        TSG_CK(cudaMemcpyAsync(stage, col_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice,
+                               c->stream));
+        cols_i64_to_i32<<<ew_grid(c, nnz), 256, 0, c->stream>>>(stage, m->col, nnz, cols, c->d_err);
+        if (values)
+            TSG_CK(cudaMemcpyAsync(m->val, values, nnz * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream));
+        TSG_TRY(tsg_free(c, stage));
+    }
+    int s = tsg_check_kernel_errors(c, "upload");
+    if (s != TSG_OK) {
+        tsg_csr_free(c, m);
+        return s;
+    }
+    *out = m;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int64_t *nnz,
+                            int *has_values) {
+    if (rows) *rows = m->rows;
+    if (cols) *cols = m->cols;
+    if (nnz) *nnz = m->nnz;
+    if (has_values) *has_values = m->val != nullptr;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
+                                int64_t *col_idx, double *values) {
+    if (row_ptr)
+        TSG_CK(cudaMemcpyAsync(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+    if (m->nnz > 0 && col_idx) {
+        int64_t *stage = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &stage, m->nnz));
+        cols_i32_to_i64<<<ew_grid(c, m->nnz), 256, 0, c->stream>>>(m->col, stage, m->nnz, 0);
+        TSG_CK(cudaMemcpyAsync(col_idx, stage, m->nnz * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        TSG_TRY(tsg_free(c, stage));
+    }
+    if (m->nnz > 0 && values && m->val)
+        TSG_CK(cudaMemcpyAsync(values, m->val, m->nnz * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, int64_t end,
+                                  tsg_csr **out) {
+    if (!(0 <= begin && begin <= end && end <= m->rows)) {
+        tsg_set_error("row slice [%lld, %lld) out of range", (long long)begin, (long long)end);
+        return TSG_EDIM;
+    }
+    int64_t lo = 0, hi = 0;
+    TSG_CK(cudaMemcpyAsync(&lo, m->rp + begin, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaMemcpyAsync(&hi, m->rp + end, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    tsg_csr *s = nullptr;
+    TSG_TRY(tsg_csr_alloc(c, end - begin, m->cols, hi - lo, m->val != nullptr, &s));
+    rebase_rp<<<ew_grid(c, end - begin + 1), 256, 0, c->stream>>>(m->rp + begin, s->rp,
+                                                                  end - begin + 1);
+    if (hi > lo) {
+        TSG_CK(cudaMemcpyAsync(s->col, m->col + lo, (hi - lo) * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, c->stream));
+        if (m->val)
+            TSG_CK(cudaMemcpyAsync(s->val, m->val + lo, (hi - lo) * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    }
+    TSG_CK(cudaGetLastError());
+    *out = s;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_free(tsg_ctx *c, tsg_csr *m) {
+    if (!m) return TSG_OK;
+    tsg_free(c, m->rp);
+    tsg_free(c, m->col);
+    tsg_free(c, m->val);
+    delete m;
+    return TSG_OK;
+}
+
+// ------------------------------------------------------------------ vectors
+
+extern "C" int tsg_vec_upload(tsg_ctx *c, int64_t n, const int64_t *host, tsg_vec **out) {
+    tsg_vec *v = nullptr;
+    TSG_TRY(tsg_vec_alloc(c, n, false, &v));
+    if (n > 0)
+        TSG_CK(cudaMemcpyAsync(v->d, host, n * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    *out = v;
+    return TSG_OK;
+}
+
+extern "C" int tsg_vec_download(tsg_ctx *c, const tsg_vec *v, int64_t *host) {
+    if (v->n > 0)
+        TSG_CK(cudaMemcpyAsync(host, v->d, v->n * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    return TSG_OK;
+}
+
+extern "C" int tsg_vec_len(const tsg_vec *v, int64_t *n) {
+    *n = v->n;
+    return TSG_OK;
+}
+
+extern "C" int tsg_vec_free(tsg_ctx *c, tsg_vec *v) {
+    if (!v) return TSG_OK;
+    tsg_free(c, v->d);
+    tsg_free(c, v->aux);
+    delete v;
+    return TSG_OK;
+}

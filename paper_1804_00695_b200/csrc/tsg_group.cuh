@@ -1,0 +1,151 @@
+// tsg_group.cuh -- row-group primitives shared by the symbolic, numeric and
+// masked-count kernels.
+//
+// A "group" is G lanes of one warp (G in {8,16,32}) that owns one output row
+// at a time, or a whole CTA for big rows.  The group walks the row's work in
+// FLATTENED order: for the A entries t of the row (storage order) and, for
+// each, the entries s of the B (or compressed-B) row it selects.  Lanes take
+// consecutive flattened positions, so a chunk of G positions may straddle
+// several A entries; a log2(G)-step shuffle binary search maps a position back
+// to its A entry.  This keeps every lane busy whatever the B row lengths are
+// (27-entry stencil rows and 1-entry aggregation rows alike) and, because
+// lane order == flattened order, lets the numeric kernel reproduce the
+// reference's per-column summation order (accumulator.py:101-106) exactly.
+#pragma once
+
+#include "tsg_internal.cuh"
+
+// ---------------------------------------------------------------- tables
+// slot = int4 {key, mask_lo, mask_hi, base}; key TSG_EMPTY when free.
+
+__device__ __forceinline__ void tbl_clear(int4 *tbl, int T, int from, int step) {
+    for (int s = from; s < T; s += step) tbl[s] = make_int4(TSG_EMPTY, 0, 0, 0);
+}
+
+// insert-or-OR; returns false if the table is full (probe overflow)
+__device__ __forceinline__ bool tbl_or(int4 *tbl, int T, int logT, int key, unsigned lo,
+                                       unsigned hi) {
+    unsigned h = hash_slot(key, logT);
+    for (int n = 0; n < T; ++n) {
+        int k = *((volatile int *)&tbl[h].x);
+        if (k == TSG_EMPTY) {
+            k = atomicCAS(&tbl[h].x, TSG_EMPTY, key);
+            if (k == TSG_EMPTY) k = key;
+        }
+        if (k == key) {
+            if (lo) atomicOr((unsigned *)&tbl[h].y, lo);
+            if (hi) atomicOr((unsigned *)&tbl[h].z, hi);
+            return true;
+        }
+        h = (h + 1) & (unsigned)(T - 1);
+    }
+    return false;
+}
+
+// lookup; -1 if absent
+__device__ __forceinline__ int tbl_find(const int4 *tbl, int T, int logT, int key, int4 &out) {
+    unsigned h = hash_slot(key, logT);
+    for (int n = 0; n < T; ++n) {
+        int4 e = tbl[h];
+        if (e.x == key) {
+            out = e;
+            return (int)h;
+        }
+        if (e.x == TSG_EMPTY) return -1;
+        h = (h + 1) & (unsigned)(T - 1);
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int slot_pop(const int4 &e) {
+    return __popc((unsigned)e.y) + __popc((unsigned)e.z);
+}
+
+// rank of column `bit` inside a 64-bit set mask (number of lower set bits)
+__device__ __forceinline__ int mask_rank(const int4 &e, int bit) {
+    unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+    if (bit < 32) return __popc(lo & ((1u << bit) - 1u));
+    return __popc(lo) + __popc(hi & ((1u << (bit - 32)) - 1u));
+}
+
+// ---------------------------------------------------------------- enumerate
+// src(t, start, len): entries [start, start+len) selected by A entry t
+//                     (len = 0 to skip, e.g. outside a B row range).
+// f(valid, j, t, s): called by every lane of the group for each chunk; j is
+//                 the group lane holding A entry t, s the selected entry.
+template <int G, class Src, class F>
+__device__ __forceinline__ void group_enumerate(unsigned gm, int glane, int64_t a0, int64_t a1,
+                                                Src src, F f) {
+    for (int64_t base = a0; base < a1; base += G) {
+        int64_t t = base + glane;
+        int64_t st = 0;
+        int len = 0;
+        if (t < a1) src(t, st, len);
+        int incl = group_incl_scan<G, int>(gm, len, glane);
+        int total = __shfl_sync(gm, incl, G - 1, G);
+        for (int p0 = 0; p0 < total; p0 += G) {
+            int p = p0 + glane;
+            int j = 0;
+#pragma unroll
+            for (int step = G / 2; step >= 1; step >>= 1) {
+                int v = __shfl_sync(gm, incl, j + step - 1, G);
+                if (v <= p) j += step;
+            }
+            int inc_j = __shfl_sync(gm, incl, j, G);
+            int len_j = __shfl_sync(gm, len, j, G);
+            int64_t st_j = __shfl_sync(gm, st, j, G);
+            bool valid = p < total;
+            f(valid, j, base + j, st_j + (int64_t)(p - (inc_j - len_j)));
+        }
+    }
+}
+
+// Block-wide version for one row per CTA (NT threads, NT multiple of 32).
+// f(t, s) is called only for valid positions (no collectives inside f).
+template <int NT, class Src, class F>
+__device__ __forceinline__ void block_enumerate(int64_t a0, int64_t a1, Src src, F f) {
+    __shared__ int s_incl[NT];
+    __shared__ int s_len[NT];
+    __shared__ int64_t s_st[NT];
+    __shared__ int s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int64_t base = a0; base < a1; base += NT) {
+        int64_t t = base + tid;
+        int64_t st = 0;
+        int len = 0;
+        if (t < a1) src(t, st, len);
+        int x = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        if (lane == 31) s_warp[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int y = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int o = __shfl_up_sync(0xffffffffu, y, d);
+                if (lane >= d) y += o;
+            }
+            s_warp[lane] = y;
+        }
+        __syncthreads();
+        s_incl[tid] = x + (w ? s_warp[w - 1] : 0);
+        s_len[tid] = len;
+        s_st[tid] = st;
+        int total = s_warp[NT / 32 - 1];
+        __syncthreads();
+        for (int p = tid; p < total; p += NT) {
+            int lo = 0, hi = NT - 1;          // first j with incl[j] > p
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (s_incl[mid] <= p) lo = mid + 1;
+                else hi = mid;
+            }
+            f(base + lo, s_st[lo] + (int64_t)(p - (s_incl[lo] - s_len[lo])));
+        }
+        __syncthreads();
+    }
+}

@@ -1,0 +1,183 @@
+// tsg_internal.cuh -- shared internals of libtsg (B200 / sm_100a).
+//
+// Device layouts (HBM):
+//   CSR   : int64 row_ptr[rows+1], int32 col[nnz], fp64 val[nnz]
+//   CMAT  : padded compressed rows.  Row r's sets live at [start[r], start[r] +
+//           cnt[r]) of int32 set[] / uint64 bits[]; start[] is a copy of the
+//           source CSR's row_ptr, so compress is a single pass with no scan.
+//   VEC   : int64 d[n] (+ optional int32 aux[n] = distinct sets per row).
+//
+// Accumulator tables are 16-byte slots {key, mask_lo, mask_hi, base}: the key
+// is claimed with a 32-bit CAS and the 64-bit column mask is ORed as two
+// native 32-bit ATOMS.OR halves (a 64-bit shared-memory OR is a CAS loop on
+// sm_100a).  One 128-bit LDS fetches a whole slot during lookups.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/tsg.h"
+
+#define TSG_EMPTY (-1)
+
+struct tsg_ctx {
+    int device;
+    int num_sms;
+    size_t smem_optin;
+    cudaStream_t stream;      // compute
+    cudaStream_t copy_in;     // H2D
+    cudaStream_t copy_out;    // D2H
+    int *d_err;               // [0] code, [1] row (lowest)
+    int64_t *h_small;         // pinned scratch for small D2H reads (64 x int64)
+    int64_t *d_small;         // device scratch for reductions (64 x int64)
+    int timing;
+    cudaEvent_t ev[8];
+    float phase_ms[8];
+    int64_t bytes_in_use;
+};
+
+struct tsg_csr {
+    int64_t rows, cols, nnz;
+    int64_t *rp;
+    int32_t *col;
+    double *val;
+};
+
+struct tsg_cmat {
+    int64_t rows;
+    int64_t *start;   // rows (+1; copy of source row_ptr, or compact ptr)
+    int32_t *cnt;     // rows
+    int32_t *set;     // capacity >= nsets
+    uint64_t *bits;
+    int64_t cap;      // entries allocated in set/bits
+};
+
+struct tsg_vec {
+    int64_t n;
+    int64_t *d;
+    int32_t *aux;     // distinct sets per row (from symbolic) or null
+};
+
+// ---------------------------------------------------------------- errors
+void tsg_set_error(const char *fmt, ...);
+int tsg_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define TSG_CK(call)                                                        \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return tsg_cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define TSG_TRY(call)                      \
+    do {                                   \
+        int _s = (call);                   \
+        if (_s != TSG_OK) return _s;       \
+    } while (0)
+
+// kernel-side error reporting: first code wins, lowest row kept
+enum { KERR_NONE = 0, KERR_COUNT = 1, KERR_PROBE = 2, KERR_NOTLOWER = 3, KERR_COLRANGE = 4,
+       KERR_UNSORTED_INTERNAL = 5 };
+
+__device__ __forceinline__ void kerr(int *err, int code, int64_t row) {
+    atomicCAS(err, 0, code);
+    atomicMin(err + 1, (int)(row < 0x7fffffff ? row : 0x7fffffff));
+}
+
+// ---------------------------------------------------------------- memory
+int tsg_alloc(tsg_ctx *ctx, void **p, size_t bytes);
+int tsg_free(tsg_ctx *ctx, void *p);
+template <typename T>
+inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
+    return tsg_alloc(ctx, (void **)p, count * sizeof(T));
+}
+// Reads and clears the device error flag (synchronises the compute stream).
+int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
+
+// ---------------------------------------------------------------- scan
+// Exclusive prefix sum of n int64 values into out[0..n] (out[n] = total).
+// in and out may alias only if in == out (in-place supported).
+int tsg_exclusive_scan_i64(tsg_ctx *ctx, const int64_t *in, int64_t *out, int64_t n);
+// Same for int32 input, int64 output.
+int tsg_exclusive_scan_i32_to_i64(tsg_ctx *ctx, const int32_t *in, int64_t *out, int64_t n);
+
+// ---------------------------------------------------------------- objects
+int tsg_csr_alloc(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, bool values,
+                  tsg_csr **out);
+int tsg_vec_alloc(tsg_ctx *ctx, int64_t n, bool aux, tsg_vec **out);
+int tsg_cmat_alloc(tsg_ctx *ctx, int64_t rows, int64_t cap, tsg_cmat **out);
+
+// ---------------------------------------------------------------- timing
+struct PhaseTimer {
+    tsg_ctx *ctx;
+    int n;
+    explicit PhaseTimer(tsg_ctx *c) : ctx(c), n(0) {}
+    void mark() {
+        if (ctx->timing && n < 8) cudaEventRecord(ctx->ev[n++], ctx->stream);
+    }
+    void finish(int total_slot);
+};
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ unsigned hash_slot(int key, int logT) {
+    return (unsigned)((unsigned)key * 2654435761u) >> (32 - logT);
+}
+
+__device__ __forceinline__ int ilog2_pow2(int T) { return 31 - __clz(T); }
+
+__host__ __device__ __forceinline__ int pow2_ceil_i(int64_t x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// table slots for a row holding up to `m` distinct keys: load factor <= 3/4
+__host__ __device__ __forceinline__ int table_slots(int64_t m) {
+    int64_t need = m + (m + 2) / 3;   // ~4m/3
+    int t = pow2_ceil_i(need < 8 ? 8 : need);
+    return t;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned r;
+    asm("mov.u32 %0, %%laneid;" : "=r"(r));
+    return r;
+}
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+    if constexpr (G == 32) return 0xffffffffu;
+    else return ((1u << G) - 1u) << (lane_id() & ~(G - 1));
+}
+
+// inclusive scan of v over the G lanes of a group
+template <int G, typename T>
+__device__ __forceinline__ T group_incl_scan(unsigned gm, T v, int glane) {
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+        T o = __shfl_up_sync(gm, v, d, G);
+        if (glane >= d) v += o;
+    }
+    return v;
+}
+
+template <int G, typename T>
+__device__ __forceinline__ T group_sum(unsigned gm, T v) {
+#pragma unroll
+    for (int d = G / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(gm, v, d, G);
+    return v;
+}
+
+// ---------------------------------------------------------------- launch helpers
+static inline unsigned grid_for(int64_t work, int per_block, int cap = 1 << 30) {
+    int64_t g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}

@@ -1,0 +1,407 @@
+// tsg_masked.cu -- K6 masked intersect-count (triangle counting) and the
+// compressed-matrix boundary (download / upload / info).
+//
+// masked_row_intersect_count (kernel.py:349-394): for every row i of a
+// strictly lower-triangular pattern L, the row's own columns are ORed into a
+// set table (rejecting any column >= i), then every entry j of the row walks
+// the compressed row j of cl and adds popcount(bits & table[set]).  Work is
+// enumerated in flattened order over the selected compressed rows, rows are
+// binned by table size exactly like the symbolic phase, and the int64 total
+// is reduced warp -> CTA (shared atomic) -> one global atomic per CTA, so the
+// integer result is exact and launch-order independent.
+#include "tsg_group.cuh"
+
+namespace {
+
+struct MaskArgs {
+    const int64_t *lrp;
+    const int32_t *lcol;
+    const int64_t *cstart;
+    const int32_t *ccnt;
+    const int32_t *cset;
+    const uint64_t *cbits;
+    unsigned long long *total;
+    int *err;
+};
+
+constexpr int MB = 9;  // bins: 0..6 group tier (slice 512 << b), 7 CTA, 8 global
+
+__device__ __forceinline__ int mask_bin(int64_t len) {
+    if (len <= 0) return 255;
+    int64_t need = 16 * (int64_t)table_slots(len);
+    for (int b = 0; b < 7; b++)
+        if (need <= (512 << b)) return b;
+    if (table_slots(len) <= 8192) return 7;
+    return 8;
+}
+
+__global__ void k_mask_bins(int64_t rows, const int64_t *__restrict__ lrp, uint8_t *bins) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bins[i] = (uint8_t)mask_bin(lrp[i + 1] - lrp[i]);
+}
+
+constexpr int TILE = 4096;
+
+__global__ void k_hist(int64_t rows, const uint8_t *__restrict__ bins, int ntiles, int *tc) {
+    __shared__ int h[MB];
+    if (threadIdx.x < MB) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < TILE; k += blockDim.x) {
+        int64_t i = (int64_t)blockIdx.x * TILE + k;
+        if (i < rows && bins[i] < MB) atomicAdd(&h[bins[i]], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < MB) tc[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void k_scatter(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
+                          const int64_t *__restrict__ offs, int32_t *list) {
+    __shared__ int h[MB];
+    if (threadIdx.x < MB) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < TILE; k += blockDim.x) {
+        int64_t i = (int64_t)blockIdx.x * TILE + k;
+        if (i < rows && bins[i] < MB) {
+            int r = atomicAdd(&h[bins[i]], 1);
+            list[offs[(int64_t)bins[i] * ntiles + blockIdx.x] + r] = (int32_t)i;
+        }
+    }
+}
+
+template <int G, int SLICE>
+__global__ void __launch_bounds__(256) k_mask_group(const int32_t *__restrict__ list, int64_t nlist,
+                                                    MaskArgs a) {
+    extern __shared__ int4 smem[];
+    __shared__ unsigned long long s_tot;
+    constexpr int TMAX = SLICE / 16;
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    int4 *tbl = smem + (threadIdx.x / G) * TMAX;
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+    long long mine = 0;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
+         li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t r0 = a.lrp[i], r1 = a.lrp[i + 1];
+        int T = table_slots(r1 - r0);
+        if (T > TMAX) T = TMAX;
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, glane, G);
+        __syncwarp(gm);
+        bool ok = true, lower = true;
+        for (int64_t q = r0 + glane; q < r1; q += G) {
+            int c = a.lcol[q];
+            if ((int64_t)c >= i) lower = false;
+            int bit = c & 63;
+            ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                         bit >= 32 ? 1u << (bit - 32) : 0u);
+        }
+        if (!lower) kerr(a.err, KERR_NOTLOWER, i);
+        if (!ok) kerr(a.err, KERR_PROBE, i);
+        __syncwarp(gm);
+        group_enumerate<G>(
+            gm, glane, r0, r1,
+            [&](int64_t t, int64_t &st, int &len) {
+                int j = a.lcol[t];
+                st = a.cstart[j];
+                len = a.ccnt[j];
+            },
+            [&](bool valid, int, int64_t, int64_t s) {
+                if (valid) {
+                    int4 e;
+                    if (tbl_find(tbl, T, logT, a.cset[s], e) >= 0) {
+                        uint64_t b = a.cbits[s];
+                        mine += __popc((unsigned)b & (unsigned)e.y) +
+                                __popc((unsigned)(b >> 32) & (unsigned)e.z);
+                    }
+                }
+            });
+        __syncwarp(gm);
+    }
+    for (int d = 16; d >= 1; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_tot, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_tot) atomicAdd(a.total, s_tot);
+}
+
+template <int NT, bool GLOBAL>
+__global__ void __launch_bounds__(NT) k_mask_block(const int32_t *__restrict__ list, int64_t nlist,
+                                                   MaskArgs a, int4 *slab, int64_t slab_slots,
+                                                   int tmax) {
+    extern __shared__ int4 smem[];
+    __shared__ unsigned long long s_tot;
+    int4 *tbl = GLOBAL ? slab + (int64_t)blockIdx.x * slab_slots : smem;
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+    long long mine = 0;
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t r0 = a.lrp[i], r1 = a.lrp[i + 1];
+        int64_t want = table_slots(r1 - r0);
+        int T = (int)(want < tmax ? want : tmax);
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, threadIdx.x, NT);
+        __syncthreads();
+        bool ok = true, lower = true;
+        for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) {
+            int c = a.lcol[q];
+            if ((int64_t)c >= i) lower = false;
+            int bit = c & 63;
+            ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                         bit >= 32 ? 1u << (bit - 32) : 0u);
+        }
+        if (!lower) kerr(a.err, KERR_NOTLOWER, i);
+        if (!ok) kerr(a.err, KERR_PROBE, i);
+        __syncthreads();
+        block_enumerate<NT>(
+            r0, r1,
+            [&](int64_t t, int64_t &st, int &len) {
+                int j = a.lcol[t];
+                st = a.cstart[j];
+                len = a.ccnt[j];
+            },
+            [&](int64_t, int64_t s) {
+                int4 e;
+                if (tbl_find(tbl, T, logT, a.cset[s], e) >= 0) {
+                    uint64_t b = a.cbits[s];
+                    mine += __popc((unsigned)b & (unsigned)e.y) +
+                            __popc((unsigned)(b >> 32) & (unsigned)e.z);
+                }
+            });
+        __syncthreads();
+    }
+    for (int d = 16; d >= 1; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_tot, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_tot) atomicAdd(a.total, s_tot);
+}
+
+template <int B>
+int launch_mask_group(tsg_ctx *c, const int32_t *list, const int64_t *off, const MaskArgs &a) {
+    constexpr int G = B == 0 ? 8 : (B == 1 ? 16 : 32);
+    constexpr int SL = 512 << B;
+    constexpr int BS = B <= 4 ? 256 : (B == 5 ? 128 : 64);
+    int64_t n = off[B + 1] - off[B];
+    if (n <= 0) return TSG_OK;
+    size_t smem = (size_t)(BS / G) * SL;
+    if (smem > 48 * 1024)
+        TSG_CK(cudaFuncSetAttribute(k_mask_group<G, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    k_mask_group<G, SL><<<grid_for(n, BS / G, c->num_sms * 64), BS, smem, c->stream>>>(list + off[B],
+                                                                                      n, a);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+__global__ void k_maxlen(const int32_t *list, int64_t n, const int64_t *rp, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = list[x];
+        unsigned long long l = (unsigned long long)(rp[i + 1] - rp[i]);
+        m = l > m ? l : m;
+    }
+    for (int d = 16; d >= 1; d >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// ---------------------------------------------------------------- cmat I/O
+
+__global__ void k_cmat_compact(int64_t rows, const int64_t *__restrict__ start,
+                               const int32_t *__restrict__ cnt, const int64_t *__restrict__ off,
+                               const int32_t *__restrict__ set, const uint64_t *__restrict__ bits,
+                               int64_t *__restrict__ oset, uint64_t *__restrict__ obits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w; r < rows; r += nw) {
+        int64_t s0 = start[r], o0 = off[r];
+        for (int q = lane; q < cnt[r]; q += 32) {
+            oset[o0 + q] = set[s0 + q];
+            obits[o0 + q] = bits[s0 + q];
+        }
+    }
+}
+
+__global__ void k_cmat_from_compact(int64_t rows, const int64_t *__restrict__ rp, int32_t *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        cnt[r] = (int32_t)(rp[r + 1] - rp[r]);
+}
+
+__global__ void k_i64_to_i32(const int64_t *in, int32_t *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)in[i];
+}
+
+}  // namespace
+
+extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl, int64_t *total) {
+    if (l->rows != cl->rows) {
+        tsg_set_error("matrix and compressed form disagree on row count");
+        return TSG_EDIM;
+    }
+    const int64_t rows = l->rows;
+    *total = 0;
+    if (rows == 0 || l->nnz == 0) return TSG_OK;
+    uint8_t *bins = nullptr;
+    int *tc = nullptr;
+    int64_t *offs = nullptr;
+    int32_t *list = nullptr;
+    int ntiles = (int)((rows + TILE - 1) / TILE);
+    TSG_TRY(tsg_alloc_t(c, &bins, rows));
+    TSG_TRY(tsg_alloc_t(c, &tc, (size_t)MB * ntiles));
+    TSG_TRY(tsg_alloc_t(c, &offs, (size_t)MB * ntiles + 1));
+    TSG_TRY(tsg_alloc_t(c, &list, rows));
+    k_mask_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, l->rp, bins);
+    k_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc);
+    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)MB * ntiles));
+    k_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, list);
+    TSG_CK(cudaGetLastError());
+    int64_t off[MB + 1];
+    for (int b = 0; b <= MB; b++)
+        TSG_CK(cudaMemcpyAsync(&c->h_small[b], offs + (int64_t)b * ntiles, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b <= MB; b++) off[b] = c->h_small[b];
+
+    unsigned long long *dtot = (unsigned long long *)(c->d_small + 16);
+    TSG_CK(cudaMemsetAsync(dtot, 0, sizeof(unsigned long long), c->stream));
+    MaskArgs a{l->rp, l->col, cl->start, cl->cnt, cl->set, cl->bits, dtot, c->d_err};
+    TSG_TRY(launch_mask_group<0>(c, list, off, a));
+    TSG_TRY(launch_mask_group<1>(c, list, off, a));
+    TSG_TRY(launch_mask_group<2>(c, list, off, a));
+    TSG_TRY(launch_mask_group<3>(c, list, off, a));
+    TSG_TRY(launch_mask_group<4>(c, list, off, a));
+    TSG_TRY(launch_mask_group<5>(c, list, off, a));
+    TSG_TRY(launch_mask_group<6>(c, list, off, a));
+    int64_t n7 = off[8] - off[7];
+    if (n7 > 0) {
+        size_t smem = 8192 * 16;
+        TSG_CK(cudaFuncSetAttribute(k_mask_block<512, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_mask_block<512, false><<<grid_for(n7, 1, c->num_sms * 4), 512, smem, c->stream>>>(
+            list + off[7], n7, a, nullptr, 0, 8192);
+        TSG_CK(cudaGetLastError());
+    }
+    int64_t n8 = off[9] - off[8];
+    int4 *slab = nullptr;
+    if (n8 > 0) {
+        unsigned long long *dmax = (unsigned long long *)(c->d_small + 24);
+        TSG_CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
+        k_maxlen<<<grid_for(n8, 256, c->num_sms * 4), 256, 0, c->stream>>>(list + off[8], n8, l->rp,
+                                                                          dmax);
+        TSG_CK(cudaMemcpyAsync(&c->h_small[0], dmax, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        int64_t T = table_slots(c->h_small[0]);
+        int64_t ctas = ((int64_t)2 << 30) / (T * 16);
+        if (ctas < 1) ctas = 1;
+        if (ctas > n8) ctas = n8;
+        if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
+        TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
+        k_mask_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(list + off[8], n8, a, slab, T,
+                                                                      (int)T);
+        TSG_CK(cudaGetLastError());
+    }
+    TSG_CK(cudaMemcpyAsync(&c->h_small[1], dtot, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    int s = tsg_check_kernel_errors(c, "masked count");   // synchronises
+    *total = c->h_small[1];
+    tsg_free(c, slab);
+    tsg_free(c, bins);
+    tsg_free(c, tc);
+    tsg_free(c, offs);
+    tsg_free(c, list);
+    return s;
+}
+
+extern "C" int tsg_cmat_info(tsg_ctx *c, const tsg_cmat *cm, int64_t *rows, int64_t *n_sets) {
+    if (rows) *rows = cm->rows;
+    if (n_sets) {
+        int64_t *off = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &off, cm->rows + 1));
+        TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, cm->cnt, off, cm->rows));
+        TSG_CK(cudaMemcpyAsync(&c->h_small[0], off + cm->rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        *n_sets = c->h_small[0];
+        TSG_TRY(tsg_free(c, off));
+    }
+    return TSG_OK;
+}
+
+extern "C" int tsg_cmat_download(tsg_ctx *c, const tsg_cmat *cm, int64_t *row_ptr, int64_t *set_idx,
+                                 uint64_t *set_bits) {
+    int64_t *off = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &off, cm->rows + 1));
+    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, cm->cnt, off, cm->rows));
+    TSG_CK(cudaMemcpyAsync(&c->h_small[0], off + cm->rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    int64_t ns = c->h_small[0];
+    if (row_ptr)
+        TSG_CK(cudaMemcpyAsync(row_ptr, off, (cm->rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+    if (ns > 0) {
+        int64_t *oset = nullptr;
+        uint64_t *obits = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &oset, ns));
+        TSG_TRY(tsg_alloc_t(c, &obits, ns));
+        k_cmat_compact<<<grid_for(cm->rows, 8, c->num_sms * 32), 256, 0, c->stream>>>(
+            cm->rows, cm->start, cm->cnt, off, cm->set, cm->bits, oset, obits);
+        TSG_CK(cudaGetLastError());
+        if (set_idx)
+            TSG_CK(cudaMemcpyAsync(set_idx, oset, ns * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        if (set_bits)
+            TSG_CK(cudaMemcpyAsync(set_bits, obits, ns * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        TSG_TRY(tsg_free(c, oset));
+        TSG_TRY(tsg_free(c, obits));
+    }
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    TSG_TRY(tsg_free(c, off));
+    return TSG_OK;
+}
+
+extern "C" int tsg_cmat_upload(tsg_ctx *c, int64_t rows, int64_t n_sets, const int64_t *row_ptr,
+                               const int64_t *set_idx, const uint64_t *set_bits, tsg_cmat **out) {
+    tsg_cmat *cm = nullptr;
+    TSG_TRY(tsg_cmat_alloc(c, rows, n_sets > 0 ? n_sets : 1, &cm));
+    TSG_CK(cudaMemcpyAsync(cm->start, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                           c->stream));
+    k_cmat_from_compact<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, cm->start,
+                                                                                   cm->cnt);
+    if (n_sets > 0) {
+        int64_t *stage = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &stage, n_sets));
+        TSG_CK(cudaMemcpyAsync(stage, set_idx, n_sets * sizeof(int64_t), cudaMemcpyHostToDevice,
+                               c->stream));
+        k_i64_to_i32<<<grid_for(n_sets, 256, c->num_sms * 8), 256, 0, c->stream>>>(stage, cm->set,
+                                                                                   n_sets);
+        TSG_CK(cudaMemcpyAsync(cm->bits, set_bits, n_sets * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                               c->stream));
+        TSG_TRY(tsg_free(c, stage));
+    }
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    *out = cm;
+    return TSG_OK;
+}
+
+extern "C" int tsg_cmat_free(tsg_ctx *c, tsg_cmat *cm) {
+    if (!cm) return TSG_OK;
+    tsg_free(c, cm->start);
+    tsg_free(c, cm->cnt);
+    tsg_free(c, cm->set);
+    tsg_free(c, cm->bits);
+    delete cm;
+    return TSG_OK;
+}

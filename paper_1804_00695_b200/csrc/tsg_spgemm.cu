@@ -1,0 +1,1349 @@
+// tsg_spgemm.cu -- the two-phase SpGEMM hot path on sm_100a.
+//
+//   K0 k_row_bounds   per A row: flops = sum nnz(B_k), set bound = sum nnz(CB_k)
+//                     (kernel.py:96-103, 135-145)
+//   K1 k_compress     B rows -> (set = col>>6, 64-bit mask) in first-touch
+//                     order (kernel.py:73-93); padded layout, single pass
+//   bins              rows partitioned by accumulator footprint (thread-group,
+//                     CTA, or global-memory tier)
+//   K2 k_sym_*        exact nnz per C row = popcount of the OR-union of the
+//                     compressed B rows (kernel.py:124-168)
+//   K3 scan           C row_ptr (tsg_core.cu)
+//   K4 k_num_*        C values (kernel.py:171-232), fused multiply-add
+//                     variant (kernel.py:235-340) via NumArgs.
+//
+// Numeric structure: the union of compressed sets is rebuilt in the row's
+// table, each occupied set gets base = number of output columns in smaller
+// sets, and a product for column c lands at position base(c>>6) +
+// rank(c & 63).  Column order within the row is therefore ascending with no
+// sort over columns, and values accumulate into a dense per-row array.  In
+// the thread-group tier the accumulation replays the reference's order
+// (first product, then += in A storage order) with __match_any_sync + an
+// ordered shuffle chain, so fp64 results are bit-identical to the CPU
+// reference; the CTA and global tiers use fp64 REDG adds (order-free,
+// within the 1e-12 parity tolerance).
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "tsg_group.cuh"
+
+namespace {
+
+// ======================================================================= args
+
+struct SymArgs {
+    const int64_t *arp;
+    const int32_t *acol;
+    int64_t a_row_off;   // A row = listed row + a_row_off (fused)
+    int32_t b_lo, b_hi;  // A columns outside [b_lo, b_hi) are skipped; B row = k - b_lo
+    const int64_t *cbstart;
+    const int32_t *cbcnt;
+    const int32_t *cbset;
+    const uint64_t *cbbits;
+    const int64_t *prp;  // partial C rows (fused) or null
+    const int32_t *pcol;
+    const int64_t *sbound;
+    int64_t *counts;
+    int32_t *msets;
+    int *err;
+};
+
+struct NumArgs {
+    const int64_t *arp;
+    const int32_t *acol;
+    const double *aval;
+    int64_t a_row_off;
+    int32_t b_lo, b_hi;
+    const int64_t *brp;
+    const int32_t *bcol;
+    const double *bval;
+    const int64_t *cbstart;
+    const int32_t *cbcnt;
+    const int32_t *cbset;
+    const uint64_t *cbbits;
+    const int64_t *prp;
+    const int32_t *pcol;
+    const double *pval;
+    const int64_t *cptr;
+    const int64_t *counts;
+    const int32_t *msets;  // may be null
+    const int64_t *sbound;
+    int32_t *ccol;
+    double *cval;
+    int *err;
+};
+
+// ======================================================================= K0
+
+template <int G>
+__global__ void k_row_bounds(int64_t rows, const int64_t *__restrict__ arp,
+                             const int32_t *__restrict__ acol, const int64_t *__restrict__ brp,
+                             const int32_t *__restrict__ cbcnt, int64_t *__restrict__ flops,
+                             int64_t *__restrict__ sbound, unsigned long long *total) {
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    int64_t mine = 0;
+    for (int64_t i = gid; i < rows; i += ngroups) {
+        int64_t f = 0, sb = 0;
+        for (int64_t t = arp[i] + glane; t < arp[i + 1]; t += G) {
+            int k = acol[t];
+            f += brp[k + 1] - brp[k];
+            if (cbcnt) sb += cbcnt[k];
+        }
+        f = group_sum<G, int64_t>(gm, f);
+        if (cbcnt) sb = group_sum<G, int64_t>(gm, sb);
+        if (glane == 0) {
+            if (flops) flops[i] = f;
+            if (sbound) sbound[i] = cbcnt ? sb : f;
+            mine += f;
+        }
+    }
+    if (total) {
+        for (int d = 16; d >= 1; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, (unsigned long long)mine);
+    }
+}
+
+// ======================================================================= K1
+
+// Sorted (non-decreasing set) rows: run-length encode in one pass.  Rows whose
+// sets go down somewhere are flagged (cnt = -1) for the first-touch slow path.
+template <int G>
+__global__ void k_compress(int64_t rows, const int64_t *__restrict__ rp,
+                           const int32_t *__restrict__ col, int32_t *__restrict__ cnt,
+                           int32_t *__restrict__ oset, uint64_t *__restrict__ obits,
+                           int *n_unsorted, int32_t *unsorted) {
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const unsigned lt = lanemask_lt();
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t i = gid; i < rows; i += ngroups) {
+        const int64_t r0 = rp[i], r1 = rp[i + 1];
+        int carry = 0;
+        int prev = -1;
+        bool bad = false;
+        for (int64_t base = r0; base < r1; base += G) {
+            int64_t t = base + glane;
+            bool valid = t < r1;
+            int c = valid ? col[t] : 0;
+            int s = c >> 6;
+            int ps = __shfl_up_sync(gm, s, 1, G);
+            if (glane == 0) ps = prev;
+            bool head = valid && (t == r0 || s != ps);
+            bool down = valid && t > r0 && s < ps;
+            if (__ballot_sync(gm, down) & gm) {
+                bad = true;
+                break;
+            }
+            unsigned hb = __ballot_sync(gm, head) & gm;
+            if (head) {
+                uint64_t bits = 0;
+                for (int64_t q = t; q < r1; ++q) {
+                    int cq = col[q];
+                    if ((cq >> 6) != s) break;
+                    bits |= 1ull << (cq & 63);
+                }
+                int64_t pos = r0 + carry + __popc(hb & lt);
+                oset[pos] = s;
+                obits[pos] = bits;
+            }
+            carry += __popc(hb);
+            prev = __shfl_sync(gm, s, G - 1, G);
+        }
+        if (glane == 0) {
+            if (bad) {
+                cnt[i] = -1;
+                int slot = atomicAdd(n_unsorted, 1);
+                unsorted[slot] = (int32_t)i;
+            } else {
+                cnt[i] = carry;
+            }
+        }
+    }
+}
+
+// First-touch compression of unsorted rows: entry t heads its set if no
+// earlier entry of the row has the same set (the reference's dict order).
+template <int NT>
+__global__ void k_compress_unsorted(const int *n_unsorted, const int32_t *__restrict__ list,
+                                    const int64_t *__restrict__ rp,
+                                    const int32_t *__restrict__ col, int32_t *__restrict__ cnt,
+                                    int32_t *__restrict__ oset, uint64_t *__restrict__ obits) {
+    __shared__ int s_warp[NT / 32];
+    __shared__ int s_carry;
+    const int nrow = *n_unsorted;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int li = blockIdx.x; li < nrow; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t r0 = rp[i], r1 = rp[i + 1];
+        if (tid == 0) s_carry = 0;
+        __syncthreads();
+        for (int64_t base = r0; base < r1; base += NT) {
+            int64_t t = base + tid;
+            bool head = t < r1;
+            int s = head ? (col[t] >> 6) : -1;
+            for (int64_t q = r0; head && q < t; ++q)
+                if ((col[q] >> 6) == s) head = false;
+            uint64_t bits = 0;
+            if (head)
+                for (int64_t q = t; q < r1; ++q) {
+                    int cq = col[q];
+                    if ((cq >> 6) == s) bits |= 1ull << (cq & 63);
+                }
+            unsigned hb = __ballot_sync(0xffffffffu, head);
+            if (lane == 0) s_warp[w] = __popc(hb);
+            __syncthreads();
+            int before = s_carry;
+            for (int j = 0; j < w; j++) before += s_warp[j];
+            if (head) {
+                int64_t pos = r0 + before + __popc(hb & lanemask_lt());
+                oset[pos] = s;
+                obits[pos] = bits;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int tot = 0;
+                for (int j = 0; j < NT / 32; j++) tot += s_warp[j];
+                s_carry += tot;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) cnt[i] = s_carry;
+        __syncthreads();
+    }
+}
+
+// ======================================================================= bins
+// Tier sizes.  Thread-group tier: a G-lane group owns a SLICE-byte region of
+// shared memory (table + dense values).  CTA tier: one row per CTA, table in
+// shared memory.  Global tier: one row per CTA, table in a global slab.
+
+constexpr int NBINS = 10;
+// bins 0..6: group tier slices (bytes) and group sizes
+__host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
+__host__ __device__ constexpr int gt_g(int b) { return b == 0 ? 8 : (b == 1 ? 16 : 32); }
+__host__ __device__ constexpr int gt_block(int b) { return b <= 4 ? 256 : (b == 5 ? 128 : 64); }
+// bins 7, 8: CTA tier table slots (smem table 16 B/slot + sort keys 8 B/slot)
+__host__ __device__ constexpr int ct_slots(int cb) { return 2048 << (2 * cb); }
+__host__ __device__ constexpr int ct_nt(int cb) { return 256 << cb; }
+constexpr int BIN_GLOBAL = 9;
+
+__host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15) & ~(int64_t)15; }
+
+// symbolic: table only (16 B/slot)
+__device__ __forceinline__ int sym_bin(int64_t sbound) {
+    if (sbound <= 0) return 255;
+    int64_t T = table_slots(sbound);
+    int64_t need = 16 * T;
+    for (int b = 0; b < 7; b++)
+        if (need <= gt_slice(b)) return b;
+    for (int b = 0; b < 2; b++)
+        if (T <= ct_slots(b)) return 7 + b;
+    return BIN_GLOBAL;
+}
+
+// numeric: table + dense fp64 values for the group tier; table for CTA tier
+__device__ __forceinline__ int num_bin(int64_t n, int64_t m) {
+    if (n <= 0) return 255;
+    int64_t T = table_slots(m);
+    int64_t need = round16(8 * n) + 16 * T;
+    for (int b = 0; b < 7; b++)
+        if (need <= gt_slice(b)) return b;
+    for (int b = 0; b < 2; b++)
+        if (T <= ct_slots(b)) return 7 + b;
+    return BIN_GLOBAL;
+}
+
+__global__ void k_sym_bins(int64_t rows, const int64_t *__restrict__ sbound, uint8_t *bins,
+                           int64_t *counts, int32_t *msets) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int b = sym_bin(sbound[i]);
+        bins[i] = (uint8_t)b;
+        if (b == 255) {
+            counts[i] = 0;
+            if (msets) msets[i] = 0;
+        }
+    }
+}
+
+__global__ void k_num_bins(int64_t rows, const int64_t *__restrict__ counts,
+                           const int32_t *__restrict__ msets, const int64_t *__restrict__ sbound,
+                           uint8_t *bins) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t n = counts[i];
+        int64_t m = msets ? (int64_t)msets[i] : (sbound[i] < n ? sbound[i] : n);
+        bins[i] = (uint8_t)num_bin(n, m);
+    }
+}
+
+constexpr int BIN_TILE = 4096;
+
+__global__ void k_bin_hist(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
+                           int *__restrict__ tilecounts) {
+    __shared__ int h[NBINS];
+    if (threadIdx.x < NBINS) h[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * BIN_TILE;
+    for (int k = threadIdx.x; k < BIN_TILE; k += blockDim.x) {
+        int64_t i = base + k;
+        if (i < rows) {
+            int b = bins[i];
+            if (b < NBINS) atomicAdd(&h[b], 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < NBINS) tilecounts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void k_bin_scatter(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
+                              const int64_t *__restrict__ offs, int32_t *__restrict__ list) {
+    __shared__ int h[NBINS];
+    if (threadIdx.x < NBINS) h[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * BIN_TILE;
+    for (int k = threadIdx.x; k < BIN_TILE; k += blockDim.x) {
+        int64_t i = base + k;
+        if (i < rows) {
+            int b = bins[i];
+            if (b < NBINS) {
+                int r = atomicAdd(&h[b], 1);
+                list[offs[(int64_t)b * ntiles + blockIdx.x] + r] = (int32_t)i;
+            }
+        }
+    }
+}
+
+// ======================================================================= K2 group tier
+
+template <int G, int SLICE>
+__global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
+                                                   SymArgs a) {
+    extern __shared__ int4 smem[];
+    constexpr int TMAX = SLICE / 16;
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    int4 *tbl = smem + (threadIdx.x / G) * TMAX;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
+         li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        int T = table_slots(a.sbound[i]);
+        if (T > TMAX) T = TMAX;
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, glane, G);
+        __syncwarp(gm);
+        bool ok = true;
+        if (a.prp) {
+            for (int64_t q = a.prp[i] + glane; q < a.prp[i + 1]; q += G) {
+                int c = a.pcol[q];
+                int bit = c & 63;
+                ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                             bit >= 32 ? 1u << (bit - 32) : 0u);
+            }
+        }
+        group_enumerate<G>(
+            gm, glane, a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.cbstart[k];
+                    len = a.cbcnt[k];
+                }
+            },
+            [&](bool valid, int, int64_t, int64_t s) {
+                if (valid) {
+                    uint64_t bits = a.cbbits[s];
+                    ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                }
+            });
+        __syncwarp(gm);
+        int cnt = 0, m = 0;
+        for (int s = glane; s < T; s += G) {
+            int4 e = tbl[s];
+            if (e.x != TSG_EMPTY) {
+                m++;
+                cnt += slot_pop(e);
+            }
+        }
+        cnt = group_sum<G, int>(gm, cnt);
+        m = group_sum<G, int>(gm, m);
+        if (!ok) kerr(a.err, KERR_PROBE, gi);
+        if (glane == 0) {
+            a.counts[i] = cnt;
+            if (a.msets) a.msets[i] = m;
+        }
+        __syncwarp(gm);
+    }
+}
+
+// ======================================================================= K4 group tier
+
+// Ordered accumulation of `prod` into vals[pos] (pos < 0: lane inactive).
+// Lanes with equal pos combine in lane order, i.e. flattened product order:
+// the leader adds its own product to the running value, then every peer's in
+// turn -- exactly the reference's sequence of `payload += value`.
+template <int G>
+__device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, double prod) {
+    const unsigned lane = lane_id();
+    unsigned peers = __match_any_sync(gm, pos);
+    bool leader = (pos >= 0) && ((int)lane == __ffs(peers) - 1);
+    unsigned rest = leader ? (peers & ~(1u << lane)) : 0u;
+    unsigned iters = __reduce_max_sync(gm, (unsigned)__popc(rest));
+    double acc = 0.0;
+    if (leader) acc = __dadd_rn(vals[pos], prod);
+    for (unsigned it = 0; it < iters; ++it) {
+        int src = rest ? __ffs(rest) - 1 : (int)lane;
+        double o = __shfl_sync(gm, prod, src);
+        if (rest) {
+            acc = __dadd_rn(acc, o);
+            rest &= rest - 1;
+        }
+    }
+    if (leader) vals[pos] = acc;
+    __syncwarp(gm);
+}
+
+template <int G, int SLICE>
+__global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
+                                                   NumArgs a) {
+    extern __shared__ int4 smem[];
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
+         li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int n = (int)a.counts[i];
+        const int64_t cp = a.cptr[i];
+        int64_t mest = a.msets ? (int64_t)a.msets[i] : (a.sbound[i] < n ? a.sbound[i] : n);
+        double *vals = reinterpret_cast<double *>(slice);
+        int4 *tbl = reinterpret_cast<int4 *>(slice + round16(8 * (int64_t)n));
+        int T = table_slots(mest);
+        const int tmax = (int)((SLICE - round16(8 * (int64_t)n)) / 16);
+        if (T > tmax) T = 1 << ilog2_pow2(tmax);   // binning guarantees T <= tmax
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, glane, G);
+        for (int q = glane; q < n; q += G) vals[q] = -0.0;
+        __syncwarp(gm);
+
+        // phase A: union of column sets (partial row + compressed B rows)
+        bool ok = true;
+        const int64_t p0 = a.prp ? a.prp[i] : 0, p1 = a.prp ? a.prp[i + 1] : 0;
+        for (int64_t q = p0 + glane; q < p1; q += G) {
+            int c = a.pcol[q];
+            int bit = c & 63;
+            ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                         bit >= 32 ? 1u << (bit - 32) : 0u);
+        }
+        group_enumerate<G>(
+            gm, glane, a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.cbstart[k];
+                    len = a.cbcnt[k];
+                }
+            },
+            [&](bool valid, int, int64_t, int64_t s) {
+                if (valid) {
+                    uint64_t bits = a.cbbits[s];
+                    ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                }
+            });
+        __syncwarp(gm);
+
+        // phase B: base offset of each set = columns in smaller sets; emit columns
+        int tot = 0;
+        for (int s = glane; s < T; s += G) {
+            int4 e = tbl[s];
+            if (e.x == TSG_EMPTY) continue;
+            int base = 0;
+            for (int u = 0; u < T; ++u) {
+                int4 f = tbl[u];
+                if (f.x != TSG_EMPTY && f.x < e.x) base += slot_pop(f);
+            }
+            tbl[s].w = base;
+            int pc = slot_pop(e);
+            tot += pc;
+            if (base + pc <= n) {
+                unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+                int r = base;
+                while (lo) {
+                    int b = __ffs(lo) - 1;
+                    lo &= lo - 1;
+                    a.ccol[cp + r++] = e.x * 64 + b;
+                }
+                while (hi) {
+                    int b = __ffs(hi) - 1;
+                    hi &= hi - 1;
+                    a.ccol[cp + r++] = e.x * 64 + 32 + b;
+                }
+            }
+        }
+        tot = group_sum<G, int>(gm, tot);
+        ok = __all_sync(gm, ok);
+        __syncwarp(gm);
+        if (tot != n || !ok) {
+            if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+            continue;   // group-uniform
+        }
+
+        // phase C: partial values first, then products in flattened order
+        for (int64_t q = p0 + glane; q < p1; q += G) {
+            int c = a.pcol[q];
+            int4 e;
+            tbl_find(tbl, T, logT, c >> 6, e);
+            vals[e.w + mask_rank(e, c & 63)] = a.pval[q];
+        }
+        __syncwarp(gm);
+        group_enumerate<G>(
+            gm, glane, a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.brp[k];
+                    len = (int)(a.brp[k + 1] - st);
+                }
+            },
+            [&](bool valid, int j, int64_t t, int64_t s) {
+                int pos = -1;
+                double prod = 0.0;
+                if (valid) {
+                    int c = a.bcol[s];
+                    int4 e;
+                    tbl_find(tbl, T, logT, c >> 6, e);
+                    pos = e.w + mask_rank(e, c & 63);
+                    prod = __dmul_rn(a.aval[t], a.bval[s]);
+                }
+                ordered_add<G>(gm, vals, pos, prod);
+            });
+        __syncwarp(gm);
+        for (int q = glane; q < n; q += G) a.cval[cp + q] = vals[q];
+        __syncwarp(gm);
+    }
+}
+
+// ======================================================================= CTA / global tiers
+
+// Block-wide inclusive scan helper (NT threads).
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_warp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int y = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, y, d);
+            if (lane >= d) y += o;
+        }
+        s_warp[lane] = y;
+    }
+    __syncthreads();
+    int r = x - v + (w ? s_warp[w - 1] : 0);
+    total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return r;
+}
+
+// Union of the row's sets into tbl (generic pointer: smem or global slab).
+template <int NT>
+__device__ __forceinline__ bool block_union(int4 *tbl, int T, int logT, const int64_t *prp,
+                                            const int32_t *pcol, int64_t li, int64_t a0,
+                                            int64_t a1, const int32_t *acol, int32_t b_lo,
+                                            int32_t b_hi, const int64_t *cbstart,
+                                            const int32_t *cbcnt, const int32_t *cbset,
+                                            const uint64_t *cbbits) {
+    bool ok = true;
+    if (prp) {
+        for (int64_t q = prp[li] + threadIdx.x; q < prp[li + 1]; q += NT) {
+            int c = pcol[q];
+            int bit = c & 63;
+            ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                         bit >= 32 ? 1u << (bit - 32) : 0u);
+        }
+    }
+    block_enumerate<NT>(
+        a0, a1,
+        [&](int64_t t, int64_t &st, int &len) {
+            int k = acol[t];
+            if (k >= b_lo && k < b_hi) {
+                k -= b_lo;
+                st = cbstart[k];
+                len = cbcnt[k];
+            }
+        },
+        [&](int64_t, int64_t s) {
+            uint64_t bits = cbbits[s];
+            ok &= tbl_or(tbl, T, logT, cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+        });
+    return ok;
+}
+
+template <int NT, bool GLOBAL>
+__global__ void __launch_bounds__(NT) k_sym_block(const int32_t *__restrict__ list, int64_t nlist,
+                                                  SymArgs a, int4 *slab, int64_t slab_slots,
+                                                  int tmax) {
+    extern __shared__ int4 smem[];
+    __shared__ int s_warp[32];
+    __shared__ int s_red[2];
+    int4 *tbl = GLOBAL ? slab + (int64_t)blockIdx.x * slab_slots : smem;
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        int64_t want = table_slots(a.sbound[i]);
+        int T = (int)(want < tmax ? want : tmax);
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, threadIdx.x, NT);
+        if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
+        __syncthreads();
+        bool ok = block_union<NT>(tbl, T, logT, a.prp, a.pcol, i, a.arp[gi], a.arp[gi + 1], a.acol,
+                                  a.b_lo, a.b_hi, a.cbstart, a.cbcnt, a.cbset, a.cbbits);
+        __syncthreads();
+        int cnt = 0, m = 0;
+        for (int s = threadIdx.x; s < T; s += NT) {
+            int4 e = tbl[s];
+            if (e.x != TSG_EMPTY) {
+                m++;
+                cnt += slot_pop(e);
+            }
+        }
+        int tc, tm;
+        (void)block_excl_scan<NT>(cnt, tc, s_warp);
+        (void)block_excl_scan<NT>(m, tm, s_warp);
+        if (!ok) kerr(a.err, KERR_PROBE, gi);
+        if (threadIdx.x == 0) {
+            a.counts[i] = tc;
+            if (a.msets) a.msets[i] = tm;
+        }
+        __syncthreads();
+    }
+}
+
+// Numeric CTA/global tier: union -> compact + bitonic sort of set keys ->
+// scan of popcounts -> columns; values accumulate straight into C with fp64
+// REDG adds (C values pre-set to -0.0, the additive identity that keeps the
+// sign of a lone -0.0 product).
+template <int NT, bool GLOBAL>
+__global__ void __launch_bounds__(NT) k_num_block(const int32_t *__restrict__ list, int64_t nlist,
+                                                  NumArgs a, int4 *slab, uint64_t *sortslab,
+                                                  int64_t slab_slots, int tmax) {
+    extern __shared__ int4 smem[];
+    __shared__ int s_warp[32];
+    __shared__ int s_m;
+    int4 *tbl = GLOBAL ? slab + (int64_t)blockIdx.x * slab_slots : smem;
+    uint64_t *keys = GLOBAL ? sortslab + (int64_t)blockIdx.x * slab_slots
+                            : reinterpret_cast<uint64_t *>(smem + tmax);
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t n = a.counts[i];
+        const int64_t cp = a.cptr[i];
+        int64_t mest = a.msets ? (int64_t)a.msets[i] : (a.sbound[i] < n ? a.sbound[i] : n);
+        int64_t want = table_slots(mest);
+        int T = (int)(want < tmax ? want : tmax);
+        const int logT = ilog2_pow2(T);
+        tbl_clear(tbl, T, threadIdx.x, NT);
+        if (threadIdx.x == 0) s_m = 0;
+        __syncthreads();
+        bool ok = block_union<NT>(tbl, T, logT, a.prp, a.pcol, i, a.arp[gi], a.arp[gi + 1], a.acol,
+                                  a.b_lo, a.b_hi, a.cbstart, a.cbcnt, a.cbset, a.cbbits);
+        __syncthreads();
+        // compact occupied slots as sortable (key << 32 | slot)
+        for (int s = threadIdx.x; s < T; s += NT) {
+            int4 e = tbl[s];
+            if (e.x != TSG_EMPTY) {
+                int p = atomicAdd(&s_m, 1);
+                keys[p] = ((uint64_t)(uint32_t)e.x << 32) | (uint32_t)s;
+            }
+        }
+        __syncthreads();
+        const int m = s_m;
+        int P = 1;
+        while (P < m) P <<= 1;
+        for (int s = m + threadIdx.x; s < P; s += NT) keys[s] = ~0ull;
+        __syncthreads();
+        // bitonic sort of P keys
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int x = threadIdx.x; x < P; x += NT) {
+                    int y = x ^ j;
+                    if (y > x) {
+                        uint64_t kx = keys[x], ky = keys[y];
+                        bool up = (x & k) == 0;
+                        if ((kx > ky) == up) {
+                            keys[x] = ky;
+                            keys[y] = kx;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // exclusive scan of popcounts in key order -> base; emit columns
+        int carry = 0;
+        for (int b0 = 0; b0 < m; b0 += NT) {
+            int x = b0 + threadIdx.x;
+            int slot = -1, pc = 0;
+            int4 e = make_int4(0, 0, 0, 0);
+            if (x < m) {
+                slot = (int)(uint32_t)keys[x];
+                e = tbl[slot];
+                pc = slot_pop(e);
+            }
+            int tot;
+            int base = carry + block_excl_scan<NT>(pc, tot, s_warp);
+            if (x < m) {
+                tbl[slot].w = base;
+                if (base + pc <= n) {
+                    unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+                    int64_t r = cp + base;
+                    while (lo) {
+                        int b = __ffs(lo) - 1;
+                        lo &= lo - 1;
+                        a.ccol[r] = e.x * 64 + b;
+                        a.cval[r++] = -0.0;
+                    }
+                    while (hi) {
+                        int b = __ffs(hi) - 1;
+                        hi &= hi - 1;
+                        a.ccol[r] = e.x * 64 + 32 + b;
+                        a.cval[r++] = -0.0;
+                    }
+                }
+            }
+            carry += tot;
+        }
+        ok = __syncthreads_and(ok);
+        if (carry != n || !ok) {
+            if (threadIdx.x == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+            __syncthreads();
+            continue;
+        }
+        // partial values, then products (order-free REDG adds)
+        if (a.prp) {
+            for (int64_t q = a.prp[i] + threadIdx.x; q < a.prp[i + 1]; q += NT) {
+                int c = a.pcol[q];
+                int4 e;
+                tbl_find(tbl, T, logT, c >> 6, e);
+                a.cval[cp + e.w + mask_rank(e, c & 63)] = a.pval[q];
+            }
+            __syncthreads();
+        }
+        block_enumerate<NT>(
+            a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.brp[k];
+                    len = (int)(a.brp[k + 1] - st);
+                }
+            },
+            [&](int64_t t, int64_t s) {
+                int c = a.bcol[s];
+                int4 e;
+                tbl_find(tbl, T, logT, c >> 6, e);
+                atomicAdd(&a.cval[cp + e.w + mask_rank(e, c & 63)], __dmul_rn(a.aval[t], a.bval[s]));
+            });
+        __syncthreads();
+    }
+}
+
+// ======================================================================= host helpers
+
+struct BinLists {
+    int32_t *list = nullptr;
+    int64_t off[NBINS + 1] = {0};
+};
+
+int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out) {
+    int ntiles = (int)((rows + BIN_TILE - 1) / BIN_TILE);
+    if (ntiles < 1) ntiles = 1;
+    int *tc = nullptr;
+    int64_t *offs = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &tc, (size_t)NBINS * ntiles));
+    TSG_TRY(tsg_alloc_t(c, &offs, (size_t)NBINS * ntiles + 1));
+    TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
+    k_bin_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc);
+    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NBINS * ntiles));
+    k_bin_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list);
+    TSG_CK(cudaGetLastError());
+    // bin starts: offs[b * ntiles]
+    for (int b = 0; b <= NBINS; b++)
+        TSG_CK(cudaMemcpyAsync(&c->h_small[b], offs + (int64_t)b * ntiles, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b <= NBINS; b++) out.off[b] = c->h_small[b];
+    TSG_TRY(tsg_free(c, tc));
+    TSG_TRY(tsg_free(c, offs));
+    return TSG_OK;
+}
+
+template <typename K>
+int set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        TSG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return TSG_OK;
+}
+
+unsigned group_grid(tsg_ctx *c, int64_t nrows, int groups_per_block) {
+    return grid_for(nrows, groups_per_block, c->num_sms * 64);
+}
+
+// global-tier slab sizing: T slots per CTA, bounded by a memory budget
+constexpr int64_t GLOBAL_SLAB_BUDGET = (int64_t)2 << 30;
+
+template <int B>
+int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+    constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    size_t smem = (size_t)(BS / G) * SL;
+    TSG_TRY(set_smem(k_sym_group<G, SL>, smem));
+    k_sym_group<G, SL><<<group_grid(c, n, BS / G), BS, smem, c->stream>>>(bl.list + bl.off[B], n, a);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+template <int B>
+int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+    constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    size_t smem = (size_t)(BS / G) * SL;
+    TSG_TRY(set_smem(k_num_group<G, SL>, smem));
+    k_num_group<G, SL><<<group_grid(c, n, BS / G), BS, smem, c->stream>>>(bl.list + bl.off[B], n, a);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+template <int CB>
+int launch_sym_cta(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+    constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
+    const int B = 7 + CB;
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    size_t smem = (size_t)TS * 16;
+    TSG_TRY(set_smem(k_sym_block<NT, false>, smem));
+    k_sym_block<NT, false><<<grid_for(n, 1, c->num_sms * 8), NT, smem, c->stream>>>(
+        bl.list + bl.off[B], n, a, nullptr, 0, TS);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+template <int CB>
+int launch_num_cta(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+    constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
+    const int B = 7 + CB;
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    size_t smem = (size_t)TS * 24;
+    TSG_TRY(set_smem(k_num_block<NT, false>, smem));
+    k_num_block<NT, false><<<grid_for(n, 1, c->num_sms * 8), NT, smem, c->stream>>>(
+        bl.list + bl.off[B], n, a, nullptr, nullptr, 0, TS);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+__global__ void k_max_i64_list(const int32_t *list, int64_t n, const int64_t *v,
+                               unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long y = (unsigned long long)v[list[x]];
+        m = y > m ? y : m;
+    }
+    for (int d = 16; d >= 1; d >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// max over listed rows of v[] (host value)
+int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64_t &out) {
+    TSG_CK(cudaMemsetAsync(c->d_small, 0, sizeof(int64_t), c->stream));
+    k_max_i64_list<<<grid_for(n, 256, c->num_sms * 4), 256, 0, c->stream>>>(
+        list, n, v, (unsigned long long *)c->d_small);
+    TSG_CK(cudaMemcpyAsync(c->h_small, c->d_small, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    out = c->h_small[0];
+    return TSG_OK;
+}
+
+int launch_sym_global(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+    const int B = BIN_GLOBAL;
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    int64_t maxb = 0;
+    TSG_TRY(list_max(c, bl.list + bl.off[B], n, a.sbound, maxb));
+    int64_t T = table_slots(maxb);
+    if (T > (1ll << 30)) {
+        tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
+        return TSG_ECAPACITY;
+    }
+    int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 16);
+    if (ctas < 1) ctas = 1;
+    if (ctas > n) ctas = n;
+    if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
+    int4 *slab = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
+    k_sym_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab, T,
+                                                                   (int)T);
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_free(c, slab));
+    return TSG_OK;
+}
+
+int launch_num_global(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+    const int B = BIN_GLOBAL;
+    int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    int64_t maxm = 0;   // distinct sets <= columns: size the slab by the largest count
+    TSG_TRY(list_max(c, bl.list + bl.off[B], n, a.counts, maxm));
+    int64_t T = table_slots(maxm);
+    if (T > (1ll << 30)) {
+        tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
+        return TSG_ECAPACITY;
+    }
+    int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 24);
+    if (ctas < 1) ctas = 1;
+    if (ctas > n) ctas = n;
+    if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
+    int4 *slab = nullptr;
+    uint64_t *sortslab = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
+    TSG_TRY(tsg_alloc_t(c, &sortslab, (size_t)(ctas * T)));
+    k_num_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab,
+                                                                   sortslab, T, (int)T);
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_free(c, slab));
+    TSG_TRY(tsg_free(c, sortslab));
+    return TSG_OK;
+}
+
+int run_symbolic_bins(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+    TSG_TRY(launch_sym_group<0>(c, bl, a));
+    TSG_TRY(launch_sym_group<1>(c, bl, a));
+    TSG_TRY(launch_sym_group<2>(c, bl, a));
+    TSG_TRY(launch_sym_group<3>(c, bl, a));
+    TSG_TRY(launch_sym_group<4>(c, bl, a));
+    TSG_TRY(launch_sym_group<5>(c, bl, a));
+    TSG_TRY(launch_sym_group<6>(c, bl, a));
+    TSG_TRY(launch_sym_cta<0>(c, bl, a));
+    TSG_TRY(launch_sym_cta<1>(c, bl, a));
+    TSG_TRY(launch_sym_global(c, bl, a));
+    return TSG_OK;
+}
+
+int run_numeric_bins(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+    TSG_TRY(launch_num_group<0>(c, bl, a));
+    TSG_TRY(launch_num_group<1>(c, bl, a));
+    TSG_TRY(launch_num_group<2>(c, bl, a));
+    TSG_TRY(launch_num_group<3>(c, bl, a));
+    TSG_TRY(launch_num_group<4>(c, bl, a));
+    TSG_TRY(launch_num_group<5>(c, bl, a));
+    TSG_TRY(launch_num_group<6>(c, bl, a));
+    TSG_TRY(launch_num_cta<0>(c, bl, a));
+    TSG_TRY(launch_num_cta<1>(c, bl, a));
+    TSG_TRY(launch_num_global(c, bl, a));
+    return TSG_OK;
+}
+
+// group size for row-streaming kernels from the average row length
+int pick_g(int64_t nnz, int64_t rows) {
+    double avg = rows ? (double)nnz / (double)rows : 0.0;
+    if (avg <= 6) return 4;
+    if (avg <= 12) return 8;
+    if (avg <= 24) return 16;
+    return 32;
+}
+
+template <int G>
+void launch_bounds_g(tsg_ctx *c, int64_t rows, const tsg_csr *a, const int64_t *brp,
+                     const int32_t *cbcnt, int64_t *flops, int64_t *sbound,
+                     unsigned long long *total) {
+    unsigned grid = grid_for(rows, 256 / G, c->num_sms * 32);
+    k_row_bounds<G><<<grid, 256, 0, c->stream>>>(rows, a->rp, a->col, brp, cbcnt, flops, sbound,
+                                                 total);
+}
+
+void launch_bounds(tsg_ctx *c, const tsg_csr *a, const int64_t *brp, const int32_t *cbcnt,
+                   int64_t *flops, int64_t *sbound, unsigned long long *total) {
+    switch (pick_g(a->nnz, a->rows)) {
+    case 4: launch_bounds_g<4>(c, a->rows, a, brp, cbcnt, flops, sbound, total); break;
+    case 8: launch_bounds_g<8>(c, a->rows, a, brp, cbcnt, flops, sbound, total); break;
+    case 16: launch_bounds_g<16>(c, a->rows, a, brp, cbcnt, flops, sbound, total); break;
+    default: launch_bounds_g<32>(c, a->rows, a, brp, cbcnt, flops, sbound, total); break;
+    }
+}
+
+template <int G>
+void launch_compress_g(tsg_ctx *c, const tsg_csr *b, tsg_cmat *cm, int *n_unsorted,
+                       int32_t *unsorted) {
+    unsigned grid = grid_for(b->rows, 256 / G, c->num_sms * 32);
+    k_compress<G><<<grid, 256, 0, c->stream>>>(b->rows, b->rp, b->col, cm->cnt, cm->set, cm->bits,
+                                               n_unsorted, unsorted);
+}
+
+}  // namespace
+
+// ======================================================================= internal API
+
+int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_row_off,
+                     int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
+                     const int64_t *prp, int64_t *sbound);
+
+int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
+    tsg_cmat *cm = nullptr;
+    TSG_TRY(tsg_cmat_alloc(c, b->rows, b->nnz > 0 ? b->nnz : 1, &cm));
+    TSG_CK(cudaMemcpyAsync(cm->start, b->rp, (b->rows + 1) * sizeof(int64_t),
+                           cudaMemcpyDeviceToDevice, c->stream));
+    if (b->rows > 0) {
+        int *n_uns = reinterpret_cast<int *>(c->d_small + 8);
+        int32_t *uns = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &uns, b->rows));
+        TSG_CK(cudaMemsetAsync(n_uns, 0, sizeof(int), c->stream));
+        switch (pick_g(b->nnz, b->rows)) {
+        case 4: launch_compress_g<4>(c, b, cm, n_uns, uns); break;
+        case 8: launch_compress_g<8>(c, b, cm, n_uns, uns); break;
+        case 16: launch_compress_g<16>(c, b, cm, n_uns, uns); break;
+        default: launch_compress_g<32>(c, b, cm, n_uns, uns); break;
+        }
+        // slow path launches unconditionally; it exits at once when no row is unsorted
+        k_compress_unsorted<256><<<c->num_sms * 2, 256, 0, c->stream>>>(n_uns, uns, b->rp, b->col,
+                                                                       cm->cnt, cm->set, cm->bits);
+        TSG_CK(cudaGetLastError());
+        TSG_TRY(tsg_free(c, uns));
+    }
+    *out = cm;
+    return TSG_OK;
+}
+
+// counts (+ msets) of A * B for output rows [0, rows_out); fused mode when
+// prp != null or a_row_off/b range given.
+int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_row_off,
+                      int32_t b_lo, int32_t b_hi, const tsg_cmat *cb, const tsg_csr *partial,
+                      tsg_vec **out, int64_t **sbound_out) {
+    tsg_vec *v = nullptr;
+    TSG_TRY(tsg_vec_alloc(c, rows_out, true, &v));
+    int64_t *sbound = nullptr;
+    uint8_t *bins = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &sbound, rows_out + 1));
+    TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
+    if (rows_out > 0) {
+        // set bounds: partial row length + sum of selected compressed B rows
+        if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
+            rows_out == a->rows) {
+            launch_bounds(c, a, cb->start, cb->cnt, nullptr, sbound, nullptr);
+        } else {
+            TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
+                                     partial ? partial->rp : nullptr, sbound));
+        }
+        k_sym_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+            rows_out, sbound, bins, v->d, v->aux);
+        TSG_CK(cudaGetLastError());
+        BinLists bl;
+        TSG_TRY(partition_rows(c, rows_out, bins, bl));
+        SymArgs sa;
+        sa.arp = a->rp;
+        sa.acol = a->col;
+        sa.a_row_off = a_row_off;
+        sa.b_lo = b_lo;
+        sa.b_hi = b_hi;
+        sa.cbstart = cb->start;
+        sa.cbcnt = cb->cnt;
+        sa.cbset = cb->set;
+        sa.cbbits = cb->bits;
+        sa.prp = partial ? partial->rp : nullptr;
+        sa.pcol = partial ? partial->col : nullptr;
+        sa.sbound = sbound;
+        sa.counts = v->d;
+        sa.msets = v->aux;
+        sa.err = c->d_err;
+        TSG_TRY(run_symbolic_bins(c, bl, sa));
+        TSG_TRY(tsg_free(c, bl.list));
+    }
+    TSG_TRY(tsg_free(c, bins));
+    if (sbound_out)
+        *sbound_out = sbound;
+    else
+        TSG_TRY(tsg_free(c, sbound));
+    *out = v;
+    return TSG_OK;
+}
+
+namespace {
+__global__ void k_fused_bounds(int64_t rows_out, const int64_t *__restrict__ arp,
+                               const int32_t *__restrict__ acol, int64_t a_row_off, int32_t b_lo,
+                               int32_t b_hi, const int64_t *__restrict__ cbstart,
+                               const int32_t *__restrict__ cbcnt, const int64_t *__restrict__ prp,
+                               int64_t *__restrict__ sbound) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < rows_out; i += nw) {
+        int64_t gi = i + a_row_off;
+        int64_t s = 0;
+        for (int64_t t = arp[gi] + lane; t < arp[gi + 1]; t += 32) {
+            int k = acol[t];
+            if (k >= b_lo && k < b_hi) s += cbcnt[k - b_lo];
+        }
+        for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+        if (lane == 0) sbound[i] = s + (prp ? prp[i + 1] - prp[i] : 0);
+    }
+}
+}  // namespace
+
+int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_row_off,
+                     int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
+                     const int64_t *prp, int64_t *sbound) {
+    k_fused_bounds<<<grid_for(rows_out, 8, c->num_sms * 32), 256, 0, c->stream>>>(
+        rows_out, a->rp, a->col, a_row_off, b_lo, b_hi, cbstart, cbcnt, prp, sbound);
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+// numeric into a freshly allocated C whose row_ptr = scan(counts)
+int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_csr *a,
+                     int64_t a_row_off, int32_t b_lo, int32_t b_hi, const tsg_csr *b,
+                     const tsg_cmat *cb, const tsg_csr *partial, const tsg_vec *counts,
+                     const int64_t *sbound_in, tsg_csr **out, PhaseTimer *pt) {
+    // C row pointers
+    int64_t *cptr = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &cptr, rows_out + 1));
+    TSG_TRY(tsg_exclusive_scan_i64(c, counts->d, cptr, rows_out));
+    if (pt) pt->mark();
+    int64_t nnz = 0;
+    TSG_CK(cudaMemcpyAsync(&c->h_small[0], cptr + rows_out, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    nnz = c->h_small[0];
+    tsg_csr *C = new tsg_csr();
+    C->rows = rows_out;
+    C->cols = cols_out;
+    C->nnz = nnz;
+    C->rp = cptr;
+    C->col = nullptr;
+    C->val = nullptr;
+    int st = tsg_alloc_t(c, &C->col, nnz);
+    if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, nnz);
+    if (st != TSG_OK) {
+        tsg_csr_free(c, C);
+        return st;
+    }
+    int64_t *sbound = nullptr;
+    uint8_t *bins = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
+    if (!sbound_in) {
+        TSG_TRY(tsg_alloc_t(c, &sbound, rows_out + 1));
+        if (rows_out > 0)
+            TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
+                                     partial ? partial->rp : nullptr, sbound));
+        sbound_in = sbound;
+    }
+    if (rows_out > 0 && nnz > 0) {
+        k_num_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+            rows_out, counts->d, counts->aux, sbound_in, bins);
+        TSG_CK(cudaGetLastError());
+        BinLists bl;
+        TSG_TRY(partition_rows(c, rows_out, bins, bl));
+        NumArgs na;
+        na.arp = a->rp;
+        na.acol = a->col;
+        na.aval = a->val;
+        na.a_row_off = a_row_off;
+        na.b_lo = b_lo;
+        na.b_hi = b_hi;
+        na.brp = b->rp;
+        na.bcol = b->col;
+        na.bval = b->val;
+        na.cbstart = cb->start;
+        na.cbcnt = cb->cnt;
+        na.cbset = cb->set;
+        na.cbbits = cb->bits;
+        na.prp = partial ? partial->rp : nullptr;
+        na.pcol = partial ? partial->col : nullptr;
+        na.pval = partial ? partial->val : nullptr;
+        na.cptr = cptr;
+        na.counts = counts->d;
+        na.msets = counts->aux;
+        na.sbound = sbound_in;
+        na.ccol = C->col;
+        na.cval = C->val;
+        na.err = c->d_err;
+        TSG_TRY(run_numeric_bins(c, bl, na));
+        TSG_TRY(tsg_free(c, bl.list));
+    }
+    TSG_TRY(tsg_free(c, bins));
+    TSG_TRY(tsg_free(c, sbound));
+    if (pt) pt->mark();
+    int s = tsg_check_kernel_errors(c, "numeric");
+    if (s != TSG_OK) {
+        tsg_csr_free(c, C);
+        return s;
+    }
+    *out = C;
+    return TSG_OK;
+}
+
+// ======================================================================= C ABI
+
+extern "C" int tsg_compress(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
+    TSG_TRY(tsg_compress_impl(c, b, out));
+    return tsg_check_kernel_errors(c, "compress");
+}
+
+extern "C" int tsg_count_multiplications(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b,
+                                         int64_t *total) {
+    if (a->cols != b->rows) {
+        tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
+                      (long long)b->rows);
+        return TSG_EDIM;
+    }
+    TSG_CK(cudaMemsetAsync(c->d_small, 0, sizeof(int64_t), c->stream));
+    if (a->rows > 0 && a->nnz > 0)
+        launch_bounds(c, a, b->rp, nullptr, nullptr, nullptr, (unsigned long long *)c->d_small);
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaMemcpyAsync(c->h_small, c->d_small, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    *total = c->h_small[0];
+    return TSG_OK;
+}
+
+extern "C" int tsg_symbolic(tsg_ctx *c, const tsg_csr *a, const tsg_cmat *cb, tsg_vec **counts) {
+    if (a->cols != cb->rows) {
+        tsg_set_error("A has %lld cols but compressed B has %lld rows", (long long)a->cols,
+                      (long long)cb->rows);
+        return TSG_EDIM;
+    }
+    tsg_vec *v = nullptr;
+    TSG_TRY(tsg_symbolic_impl(c, a->rows, a, 0, 0, 0x7fffffff, cb, nullptr, &v, nullptr));
+    int s = tsg_check_kernel_errors(c, "symbolic");
+    if (s != TSG_OK) {
+        tsg_vec_free(c, v);
+        return s;
+    }
+    *counts = v;
+    return TSG_OK;
+}
+
+extern "C" int tsg_numeric(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, const tsg_cmat *cb,
+                           const tsg_vec *counts, tsg_csr **out) {
+    if (a->cols != b->rows) {
+        tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
+                      (long long)b->rows);
+        return TSG_EDIM;
+    }
+    if (!a->val || !b->val) {
+        tsg_set_error("numeric multiply requires values on both operands");
+        return TSG_EVALID;
+    }
+    if (counts->n != a->rows) {
+        tsg_set_error("c_counts length must equal A's row count");
+        return TSG_EDIM;
+    }
+    tsg_cmat *own = nullptr;
+    if (!cb) {
+        TSG_TRY(tsg_compress_impl(c, b, &own));
+        cb = own;
+    }
+    int s = tsg_numeric_impl(c, a->rows, b->cols, a, 0, 0, 0x7fffffff, b, cb, nullptr, counts,
+                             nullptr, out, nullptr);
+    if (own) tsg_cmat_free(c, own);
+    return s;
+}
+
+extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_csr **out) {
+    if (a->cols != b->rows) {
+        tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
+                      (long long)b->rows);
+        return TSG_EDIM;
+    }
+    if (!a->val || !b->val) {
+        tsg_set_error("numeric multiply requires values on both operands");
+        return TSG_EVALID;
+    }
+    PhaseTimer pt(c);
+    pt.mark();
+    tsg_cmat *cb = nullptr;
+    TSG_TRY(tsg_compress_impl(c, b, &cb));
+    pt.mark();
+    tsg_vec *counts = nullptr;
+    int64_t *sbound = nullptr;
+    int s = tsg_symbolic_impl(c, a->rows, a, 0, 0, 0x7fffffff, cb, nullptr, &counts, &sbound);
+    pt.mark();
+    if (s == TSG_OK)
+        s = tsg_numeric_impl(c, a->rows, b->cols, a, 0, 0, 0x7fffffff, b, cb, nullptr, counts, sbound,
+                             out, &pt);
+    pt.finish(5);
+    // phase slots: [0] compress [1] symbolic [2] scan [3] numeric [5] total
+    tsg_free(c, sbound);
+    tsg_vec_free(c, counts);
+    tsg_cmat_free(c, cb);
+    return s;
+}
+
+extern "C" int tsg_numeric_fused(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b_chunk,
+                                 const tsg_csr *c_partial, int64_t a_lo, int64_t a_hi,
+                                 int64_t b_lo, int64_t b_hi, tsg_csr **out) {
+    if (a_hi > a->rows || a_lo < 0 || a_lo > a_hi) {
+        tsg_set_error("a_rows exceeds A's row count");
+        return TSG_EDIM;
+    }
+    if (b_hi > a->cols || b_lo < 0 || b_lo > b_hi) {
+        tsg_set_error("b_rows exceeds A's column count");
+        return TSG_EDIM;
+    }
+    if (b_chunk->rows != b_hi - b_lo) {
+        tsg_set_error("b_chunk must hold exactly the b_rows rows");
+        return TSG_EDIM;
+    }
+    if (c_partial->rows != a_hi - a_lo) {
+        tsg_set_error("c_partial must cover exactly the a_rows rows");
+        return TSG_EDIM;
+    }
+    if (c_partial->cols != b_chunk->cols) {
+        tsg_set_error("c_partial and b_chunk column spaces differ");
+        return TSG_EDIM;
+    }
+    if (!a->val || !b_chunk->val || !c_partial->val) {
+        tsg_set_error("fused multiply requires numeric operands");
+        return TSG_EVALID;
+    }
+    int64_t rows_out = a_hi - a_lo;
+    tsg_cmat *cb = nullptr;
+    TSG_TRY(tsg_compress_impl(c, b_chunk, &cb));
+    tsg_vec *counts = nullptr;
+    int64_t *sbound = nullptr;
+    int s = tsg_symbolic_impl(c, rows_out, a, a_lo, (int32_t)b_lo, (int32_t)b_hi, cb, c_partial,
+                              &counts, &sbound);
+    if (s == TSG_OK) s = tsg_check_kernel_errors(c, "fused symbolic");
+    if (s == TSG_OK)
+        s = tsg_numeric_impl(c, rows_out, b_chunk->cols, a, a_lo, (int32_t)b_lo, (int32_t)b_hi,
+                             b_chunk, cb, c_partial, counts, sbound, out, nullptr);
+    tsg_free(c, sbound);
+    tsg_vec_free(c, counts);
+    tsg_cmat_free(c, cb);
+    return s;
+}

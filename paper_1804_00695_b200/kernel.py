@@ -1,0 +1,240 @@
+"""Drop-in replacement for the reference's hot path, tiered_spgemm.kernel.
+
+Same names, signatures, defaults, argument checks and exceptions as
+/root/reference/pkg/src/tiered_spgemm/kernel.py:37-394; every numeric call
+runs hand-written sm_100a kernels through the C ABI (include/tsg.h, bound in
+_lib.py).  There is no CPU fallback.
+
+Differences a caller can observe, all inside the reference's contract:
+
+* ``spgemm_numeric`` / ``multiply`` / ``spgemm_numeric_fused`` emit each C row
+  with ascending columns instead of the accumulator's first-touch order.
+  ``canonicalize`` (csr.py:145-150) of either is identical, which is what
+  ``products_match`` compares.  Values are bit-identical to the reference for
+  rows handled by the thread-group tier (every row of the five benchmark
+  configurations) and within 1e-12 relative elsewhere.
+* ``workers`` is accepted and ignored: one launch covers every row, results
+  never depend on it (the reference guarantees the same, kernel.py:11-14).
+* Operands stay cached in HBM while the host object is alive, so
+  compress -> symbolic -> numeric on the same objects uploads each once.
+"""
+
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .csr import CsrMatrix, as_csr
+from .errors import DimensionError, MatrixValidationError
+
+COMPRESSION_WORD_BITS = 64
+
+
+def set_debug_checks(enabled: bool) -> None:
+    """Accepted for compatibility (kernel.py:31-34).  Device tables are rebuilt
+    per row and probe overflow always raises KernelError, so there is no
+    separate debug scan to enable."""
+    return None
+
+
+@dataclass(frozen=True)
+class RowRange:
+    """Half-open row interval [begin, end) (kernel.py:37-49)."""
+
+    begin: int
+    end: int
+
+    def __post_init__(self):
+        if not (0 <= self.begin <= self.end):
+            raise DimensionError("invalid row range [%d, %d)" % (self.begin, self.end))
+
+    def __len__(self):
+        return self.end - self.begin
+
+
+class CompressedMatrix:
+    """Per-row (set index, 64-bit mask) pairs (kernel.py:52-70).
+
+    Produced on the device by ``compress``; the host arrays are fetched lazily
+    on first access, and the device copy is reused by ``spgemm_symbolic``.
+    """
+
+    def __init__(self, num_rows, row_ptr=None, set_idx=None, set_bits=None, _device=None):
+        self.num_rows = int(num_rows)
+        self._dev = _device
+        self._host = None
+        if row_ptr is not None:
+            arrs = (np.array(row_ptr, dtype=np.int64), np.array(set_idx, dtype=np.int64),
+                    np.array(set_bits, dtype=np.uint64))
+            for a in arrs:
+                a.flags.writeable = False
+            self._host = arrs
+
+    def _fetch(self):
+        if self._host is None:
+            arrs = self._dev.download()
+            for a in arrs:
+                a.flags.writeable = False
+            self._host = arrs
+        return self._host
+
+    @property
+    def row_ptr(self):
+        return self._fetch()[0]
+
+    @property
+    def set_idx(self):
+        return self._fetch()[1]
+
+    @property
+    def set_bits(self):
+        return self._fetch()[2]
+
+    @property
+    def n_sets(self) -> int:
+        return int(self.set_idx.shape[0])
+
+    def device(self, ctx=None):
+        if self._dev is None:
+            self._dev = _lib.DeviceCompressed.upload(self, ctx)
+        return self._dev
+
+
+# ---- device residency cache ---------------------------------------------------
+
+_resident = {}
+
+
+def _key(m):
+    vals = None if m.values is None else m.values.__array_interface__["data"][0]
+    return (id(m), m.row_ptr.__array_interface__["data"][0],
+            m.col_idx.__array_interface__["data"][0], vals, m.num_rows, m.num_cols)
+
+
+def _on_device(m) -> "_lib.DeviceCsr":
+    """Device copy of a host CSR (cached while the host object lives)."""
+    if isinstance(m, _lib.DeviceCsr):
+        return m
+    k = _key(m)
+    hit = _resident.get(id(m))
+    if hit is not None and hit[0] == k:
+        return hit[1]
+    d = _lib.DeviceCsr.upload(m)
+    try:
+        weakref.finalize(m, _resident.pop, id(m), None)
+        _resident[id(m)] = (k, d)
+    except TypeError:  # not weak-referenceable: do not cache
+        pass
+    return d
+
+
+def _counts_on_device(counts: np.ndarray) -> "_lib.DeviceVec":
+    dv = getattr(counts, "_tsg_dev", None)
+    snap = getattr(counts, "_tsg_snap", None)
+    if dv is not None and snap is not None and np.array_equal(snap, counts):
+        return dv
+    return _lib.DeviceVec.upload(np.asarray(counts, dtype=np.int64))
+
+
+class _Counts(np.ndarray):
+    """int64 symbolic counts that remember their device copy (which also
+    carries the per-row distinct-set counts the numeric phase sizes its
+    tables with)."""
+
+
+def _wrap_counts(host: np.ndarray, dev) -> np.ndarray:
+    out = host.view(_Counts)
+    out._tsg_dev = dev
+    out._tsg_snap = host.copy()
+    return out
+
+
+# ---- the hot path ---------------------------------------------------------------
+
+def compress(b) -> CompressedMatrix:
+    """Bitmask-compress B's rows on the device (kernel.py:73-93)."""
+    db = _on_device(b)
+    return CompressedMatrix(b.num_rows, _device=_lib.d_compress(db))
+
+
+def count_multiplications(a, b) -> int:
+    """Scalar multiplications of A * B (kernel.py:96-103); flops are twice this."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A is %dx%d but B has %d rows" % (a.num_rows, a.num_cols, b.num_rows))
+    if a.col_idx.shape[0] == 0:
+        return 0
+    return _lib.d_count_multiplications(_on_device(a), _on_device(b))
+
+
+def spgemm_symbolic(a, cb, workers: int = 1) -> np.ndarray:
+    """Exact per-row nonzero counts of A * B (kernel.py:124-168)."""
+    if a.num_cols != cb.num_rows:
+        raise DimensionError("A has %d cols but compressed B has %d rows" % (a.num_cols, cb.num_rows))
+    dcb = cb.device() if isinstance(cb, CompressedMatrix) else _lib.DeviceCompressed.upload(cb)
+    dv = _lib.d_symbolic(_on_device(a), dcb)
+    return _wrap_counts(dv.download(), dv)
+
+
+def spgemm_numeric(a, b, c_counts, workers: int = 1) -> CsrMatrix:
+    """C = A * B with exactly c_counts entries per row (kernel.py:171-232)."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A is %dx%d but B has %d rows" % (a.num_rows, a.num_cols, b.num_rows))
+    if b.values is None or a.values is None:
+        raise MatrixValidationError("numeric multiply requires values on both operands")
+    counts = np.asarray(c_counts)
+    if counts.ndim != 1 or counts.shape[0] != a.num_rows:
+        raise DimensionError("c_counts length must equal A's row count")
+    dv = _counts_on_device(c_counts if isinstance(c_counts, _Counts) else counts)
+    return _lib.d_numeric(_on_device(a), _on_device(b), None, dv).download()
+
+
+def spgemm_numeric_fused(a, b_chunk, c_partial, a_rows: RowRange, b_rows: RowRange,
+                         workers: int = 1) -> CsrMatrix:
+    """result = c_partial + A[a_rows, b_rows] * B[b_rows, :] (kernel.py:235-340)."""
+    if a_rows.end > a.num_rows:
+        raise DimensionError("a_rows exceeds A's row count")
+    if b_rows.end > a.num_cols:
+        raise DimensionError("b_rows exceeds A's column count")
+    if b_chunk.num_rows != len(b_rows):
+        raise DimensionError("b_chunk must hold exactly the b_rows rows")
+    if c_partial.num_rows != len(a_rows):
+        raise DimensionError("c_partial must cover exactly the a_rows rows")
+    if c_partial.num_cols != b_chunk.num_cols:
+        raise DimensionError("c_partial and b_chunk column spaces differ")
+    if len(a_rows) == 0:
+        return c_partial
+    if a.values is None or b_chunk.values is None or c_partial.values is None:
+        raise MatrixValidationError("fused multiply requires numeric operands")
+    out = _lib.d_numeric_fused(_on_device(a), _on_device(b_chunk), _on_device(c_partial),
+                               a_rows.begin, a_rows.end, b_rows.begin, b_rows.end)
+    return out.download()
+
+
+def multiply(a, b, workers: int = 1) -> CsrMatrix:
+    """compress -> symbolic -> numeric, entirely on the device (kernel.py:343-346)."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A has %d cols but compressed B has %d rows" % (a.num_cols, b.num_rows))
+    if b.values is None or a.values is None:
+        raise MatrixValidationError("numeric multiply requires values on both operands")
+    return _lib.d_multiply(_on_device(a), _on_device(b)).download()
+
+
+def masked_row_intersect_count(l, cl, workers: int = 1) -> int:
+    """Sum over L's entries (i, j) of |cols(L_j) & cols(L_i)|; L strictly
+    lower triangular (kernel.py:349-394)."""
+    if l.num_rows != cl.num_rows:
+        raise DimensionError("matrix and compressed form disagree on row count")
+    dcl = cl.device() if isinstance(cl, CompressedMatrix) else _lib.DeviceCompressed.upload(cl)
+    return _lib.d_masked_count(_on_device(l), dcl)
+
+
+# ---- device-resident entry points (no host round trips) ------------------------
+
+def multiply_device(da, db):
+    """A * B for operands already in HBM; returns a DeviceCsr."""
+    return _lib.d_multiply(da, db)
+
+
+def upload(m):
+    return _lib.DeviceCsr.upload(as_csr(m))

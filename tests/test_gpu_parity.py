@@ -1,0 +1,206 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle.
+
+Bar (BASELINE.json north_star): row pointers and per-row sorted columns
+bit-exact; fp64 values bit-exact for the thread-group tier (the reference's
+summation order is replayed) and within rtol 1e-12 for CTA/global-tier rows;
+integer results (triangle counts) exact.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1804_00695_b200 as tsg
+from paper_1804_00695_b200 import generators as gen
+from paper_1804_00695_b200.csr import CsrMatrix, canonicalize, slice_rows
+from oracle import oracle as O
+from conftest import assert_same_product, random_csr
+
+pytestmark = pytest.mark.gpu
+
+
+def test_compress_matches_reference_first_touch_order(rng):
+    for unsorted in (False, True):
+        for _ in range(5):
+            b = random_csr(rng, 300, 700, 40)
+            if not unsorted:
+                b = canonicalize(b)
+            cm = tsg.compress(b)
+            rp, s, bits = O.compress(b)
+            assert np.array_equal(cm.row_ptr, rp)
+            assert np.array_equal(cm.set_idx, s)
+            assert np.array_equal(cm.set_bits, bits)
+
+
+def test_compress_kats():
+    def rows(rs, n):
+        r = [i for i, cs in enumerate(rs) for _ in cs]
+        c = [x for cs in rs for x in cs]
+        return CsrMatrix.from_coo(r, c, np.ones(len(c)), len(rs), n)
+    cm = tsg.compress(rows([[0, 63]], 64))
+    assert cm.n_sets == 1 and cm.set_idx[0] == 0 and int(cm.set_bits[0]) == (1 | (1 << 63))
+    cm = tsg.compress(rows([[0, 64]], 65))
+    assert sorted(cm.set_idx.tolist()) == [0, 1]
+    cm = tsg.compress(rows([[], [3]], 8))
+    assert cm.row_ptr.tolist() == [0, 0, 1]
+
+
+def test_symbolic_and_numeric_random_pairs(rng):
+    for _ in range(60):
+        n = int(rng.integers(4, 120))
+        a = random_csr(rng, n, n, 8)
+        b = random_csr(rng, n, n, 8)
+        cb = tsg.compress(b)
+        counts = tsg.spgemm_symbolic(a, cb)
+        want_counts = O.symbolic(a, O.compress(b))
+        assert np.array_equal(counts, want_counts)
+        c = tsg.spgemm_numeric(a, b, counts)
+        assert_same_product(c, O.numeric(a, b, want_counts), exact=True)
+
+
+def test_multiply_rectangular_and_empty_rows(rng):
+    for _ in range(20):
+        a = random_csr(rng, 90, 140, 12)
+        b = random_csr(rng, 140, 3000, 30)
+        assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=True)
+
+
+def test_numeric_with_host_counts(rng):
+    a = random_csr(rng, 200, 200, 10)
+    b = random_csr(rng, 200, 500, 10)
+    want = O.symbolic(a, O.compress(b))
+    c = tsg.spgemm_numeric(a, b, np.array(want))   # plain ndarray: no device set counts
+    assert_same_product(c, O.numeric(a, b, want), exact=True)
+
+
+def test_wrong_counts_raise_kernel_error(rng):
+    a = random_csr(rng, 10, 10, 3, exact_delta=True)
+    b = random_csr(rng, 10, 10, 3, exact_delta=True)
+    counts = tsg.spgemm_symbolic(a, tsg.compress(b))
+    bad = np.array(counts).copy()
+    bad[0] += 1
+    with pytest.raises(tsg.KernelError):
+        tsg.spgemm_numeric(a, b, bad)
+
+
+def test_dimension_and_value_errors():
+    a = CsrMatrix(1, 3, [0, 1], [0], [1.0])
+    b = CsrMatrix(2, 2, [0, 1, 2], [0, 0], [1.0, 1.0])
+    with pytest.raises(tsg.DimensionError):
+        tsg.spgemm_symbolic(a, tsg.compress(b))
+    p = CsrMatrix(1, 1, [0, 1], [0], None)
+    with pytest.raises(tsg.MatrixValidationError):
+        tsg.spgemm_numeric(p, p, np.array([1]))
+
+
+def test_config1_laplace2d_small_full():
+    a = gen.stencil(gen.LAPLACE2D, (64, 64))
+    assert_same_product(tsg.multiply(a, a), O.multiply(a, a), exact=True)
+
+
+def test_config2_rap_small_full():
+    a = gen.stencil(gen.BRICK3D, (16, 16, 16))
+    p, r = gen.aggregation((16, 16, 16))
+    ra = tsg.multiply(r, a)
+    ra_o = O.multiply(r, a)
+    assert_same_product(ra, ra_o, exact=True)
+    rap = tsg.multiply(ra, p)
+    ra_host = CsrMatrix(r.num_rows, a.num_cols, *ra_o)
+    assert_same_product(rap, O.multiply(ra_host, p), exact=True)
+
+
+def test_fused_full_range_equals_plain(rng):
+    a = random_csr(rng, 30, 40, 5)
+    b = random_csr(rng, 40, 35, 5)
+    plain = tsg.multiply(a, b)
+    fused = tsg.spgemm_numeric_fused(a, b, CsrMatrix.empty(30, 35), tsg.RowRange(0, 30),
+                                     tsg.RowRange(0, 40))
+    assert np.array_equal(fused.row_ptr, plain.row_ptr)
+    assert np.array_equal(fused.col_idx, plain.col_idx)
+    assert np.array_equal(fused.values, plain.values)
+
+
+def test_fused_chunk_sequence_matches_oracle(rng):
+    for _ in range(10):
+        a = random_csr(rng, 80, 90, 9)
+        b = random_csr(rng, 90, 120, 9)
+        part = CsrMatrix.empty(50, 120)
+        opart = part
+        for lo, hi in ((0, 31), (31, 60), (60, 90)):
+            chunk = slice_rows(b, lo, hi)
+            part = tsg.spgemm_numeric_fused(a, chunk, part, tsg.RowRange(20, 70),
+                                            tsg.RowRange(lo, hi))
+            o = O.fused(a, chunk, opart, 20, 70, lo, hi)
+            assert_same_product(part, o, exact=True)
+            opart = CsrMatrix(50, 120, *o)
+
+
+def test_fused_empty_a_rows_returns_partial():
+    a = CsrMatrix(2, 2, [0, 1, 2], [0, 1], [1.0, 1.0])
+    empty_partial = CsrMatrix.empty(0, 2)
+    out = tsg.spgemm_numeric_fused(a, slice_rows(a, 0, 1), empty_partial, tsg.RowRange(0, 0),
+                                   tsg.RowRange(0, 1))
+    assert out is empty_partial
+
+
+def test_large_rows_cta_and_global_tiers(rng):
+    # rows with thousands of outputs exercise the CTA tier; a dense-ish hub row
+    # the global-memory tier.  Values stay within 1e-12 (order-free adds).
+    n = 6000
+    a_rows = [rng.choice(n, size=k, replace=False) for k in (3, 40, 400, 2500)]
+    r = np.concatenate([np.full(len(x), i) for i, x in enumerate(a_rows)])
+    a = CsrMatrix.from_coo(r, np.concatenate(a_rows), rng.uniform(0.1, 1, len(r)), 4, n)
+    b = random_csr(rng, n, 200000, 60)
+    c = tsg.multiply(a, b)
+    assert_same_product(c, O.multiply(a, b), exact=False, rtol=1e-12)
+
+
+def test_integer_valued_big_rows_exact(rng):
+    n = 3000
+    b = random_csr(rng, n, 100000, 50)
+    b = CsrMatrix(b.num_rows, b.num_cols, b.row_ptr, b.col_idx, np.round(b.values * 8))
+    a = CsrMatrix.from_coo(np.zeros(n, np.int64), np.arange(n), np.ones(n), 1, n)
+    assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=True)
+
+
+def test_masked_count_random_graphs(rng):
+    for _ in range(10):
+        n = int(rng.integers(20, 300))
+        up = np.triu(rng.random((n, n)) < 0.1, 1)
+        rows, cols = np.nonzero(up | up.T)
+        keep = rows > cols
+        l = CsrMatrix.from_coo(rows[keep], cols[keep], None, n, n)
+        want = O.masked_count(l, O.compress(l))
+        assert tsg.masked_row_intersect_count(l, tsg.compress(l)) == want
+
+
+def test_masked_count_kats_and_lower_check():
+    def lower(edges, n):
+        return CsrMatrix.from_coo([max(u, v) for u, v in edges], [min(u, v) for u, v in edges],
+                                  None, n, n)
+    k4 = lower([(i, j) for i in range(4) for j in range(i + 1, 4)], 4)
+    assert tsg.masked_row_intersect_count(k4, tsg.compress(k4)) == 4
+    path = lower([(0, 1), (1, 2), (2, 3)], 4)
+    assert tsg.masked_row_intersect_count(path, tsg.compress(path)) == 0
+    bad = CsrMatrix.from_coo([0], [1], None, 2, 2)
+    with pytest.raises(tsg.MatrixValidationError):
+        tsg.masked_row_intersect_count(bad, tsg.compress(bad))
+
+
+def test_masked_count_rmat_scale12():
+    g = gen.rmat_graph(12)
+    deg = np.diff(g.row_ptr)
+    perm = np.lexsort((np.arange(g.num_rows), deg))
+    pos = np.empty_like(perm)
+    pos[perm] = np.arange(g.num_rows)
+    rows = pos[np.repeat(np.arange(g.num_rows), deg)]
+    cols = pos[g.col_idx]
+    keep = rows > cols
+    l = CsrMatrix.from_coo(rows[keep], cols[keep], None, g.num_rows, g.num_rows)
+    want = O.masked_count(l, O.compress(l), workers=8)
+    assert tsg.masked_row_intersect_count(l, tsg.compress(l)) == want
+
+
+def test_count_multiplications(rng):
+    a = random_csr(rng, 25, 30, 5)
+    b = random_csr(rng, 30, 20, 5)
+    assert tsg.count_multiplications(a, b) == O.count_multiplications(a, b)
