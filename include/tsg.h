@@ -58,10 +58,31 @@ int tsg_destroy(tsg_ctx *ctx);
 int tsg_sync(tsg_ctx *ctx);
 /* Bytes of device memory currently held by the context's allocations. */
 int tsg_mem_in_use(tsg_ctx *ctx, int64_t *bytes);
-/* Per-phase device times (ms) of the last multiply-type call:
-   [0] bounds+bins [1] compress [2] symbolic [3] scan [4] numeric [5] total */
+/* Per-phase device times (ms) of the last tsg_multiply (timing enabled):
+   [0] compress [1] symbolic [2] row-pointer scan [3] numeric [5] total */
 int tsg_last_phase_ms(tsg_ctx *ctx, float *out, int n);
 int tsg_set_timing(tsg_ctx *ctx, int enabled);
+/* Cumulative kernel launches of the context, and (timing enabled) the device
+   time of the symbolic and numeric kernels of the last multiply-type call,
+   measured with CUDA events on the context's compute stream. */
+typedef struct {
+    int64_t launches;
+    float symbolic_ms;
+    float numeric_ms;
+} tsg_stats;
+int tsg_get_stats(tsg_ctx *ctx, tsg_stats *out);
+/* User timing events on the compute stream (slot 0..7): record, then the
+   elapsed device time between two recorded slots (synchronises on `to`). */
+int tsg_event_record(tsg_ctx *ctx, int slot);
+int tsg_event_elapsed(tsg_ctx *ctx, int from, int to, float *ms);
+/* Device-to-device import of a CSR whose arrays already live on this device
+   (e.g. gathered by NCCL): int64 row_ptr, int32 columns, fp64 values. */
+int tsg_csr_from_device(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,
+                        const int64_t *d_row_ptr, const int32_t *d_col,
+                        const double *d_values, tsg_csr **out);
+/* Device pointers of a CSR (borrowed; valid until tsg_csr_free). */
+int tsg_csr_device_ptrs(const tsg_csr *m, int64_t **d_row_ptr, int32_t **d_col,
+                        double **d_values);
 
 /* ---- CSR operands (csr.py:32-106 CsrMatrix) ------------------------------ */
 /* values may be NULL (pattern).  Columns must be < 2^31 (device int32). */

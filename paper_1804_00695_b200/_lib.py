@@ -36,12 +36,13 @@ _ERRORS = {
 # every symbol include/tsg.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "tsg_last_error", "tsg_abi_version", "tsg_device_count", "tsg_init", "tsg_destroy",
-    "tsg_sync", "tsg_mem_in_use", "tsg_last_phase_ms", "tsg_set_timing",
+    "tsg_sync", "tsg_mem_in_use", "tsg_last_phase_ms", "tsg_set_timing", "tsg_get_stats",
     "tsg_csr_upload", "tsg_csr_info", "tsg_csr_download", "tsg_csr_slice_rows", "tsg_csr_free",
     "tsg_compress", "tsg_cmat_info", "tsg_cmat_download", "tsg_cmat_upload", "tsg_cmat_free",
     "tsg_vec_upload", "tsg_vec_download", "tsg_vec_len", "tsg_vec_free",
     "tsg_count_multiplications", "tsg_symbolic", "tsg_numeric", "tsg_multiply",
-    "tsg_numeric_fused", "tsg_masked_count",
+    "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
+    "tsg_csr_from_device", "tsg_csr_device_ptrs",
 )
 
 _P = ctypes.c_void_p
@@ -59,6 +60,7 @@ _SIGS = {
     "tsg_mem_in_use": ([_P, _PI64], ctypes.c_int),
     "tsg_last_phase_ms": ([_P, ctypes.POINTER(ctypes.c_float), ctypes.c_int], ctypes.c_int),
     "tsg_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
+    "tsg_get_stats": ([_P, _P], ctypes.c_int),
     "tsg_csr_upload": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_csr_info": ([_P, _PI64, _PI64, _PI64, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tsg_csr_download": ([_P, _P, _P, _P, _P], ctypes.c_int),
@@ -79,6 +81,11 @@ _SIGS = {
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric_fused": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _PP], ctypes.c_int),
     "tsg_masked_count": ([_P, _P, _P, _PI64], ctypes.c_int),
+    "tsg_event_record": ([_P, ctypes.c_int], ctypes.c_int),
+    "tsg_event_elapsed": ([_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)],
+                          ctypes.c_int),
+    "tsg_csr_from_device": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
+    "tsg_csr_device_ptrs": ([_P, _PP, _PP, _PP], ctypes.c_int),
 }
 
 _lib = None
@@ -111,6 +118,11 @@ def check(status):
 
 def _ptr(a):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("symbolic_ms", ctypes.c_float),
+                ("numeric_ms", ctypes.c_float)]
 
 
 class Context:
@@ -148,6 +160,20 @@ class Context:
         out = (ctypes.c_float * 8)()
         check(load().tsg_last_phase_ms(self.h, out, 8))
         return list(out)
+
+    def stats(self):
+        """(launches so far, symbolic ms, numeric ms of the last multiply)."""
+        st = _Stats()
+        check(load().tsg_get_stats(self.h, ctypes.byref(st)))
+        return st.launches, st.symbolic_ms, st.numeric_ms
+
+    def record(self, slot):
+        check(load().tsg_event_record(self.h, slot))
+
+    def elapsed_ms(self, a, b):
+        v = ctypes.c_float()
+        check(load().tsg_event_elapsed(self.h, a, b, ctypes.byref(v)))
+        return v.value
 
     def mem_in_use(self):
         v = ctypes.c_int64(0)
@@ -204,6 +230,21 @@ class DeviceCsr(_Handle):
         va = np.empty(self.nnz, dtype=np.float64) if self.has_values else None
         check(load().tsg_csr_download(self.ctx.h, self.h, _ptr(rp), _ptr(ci), _ptr(va)))
         return CsrMatrix._adopt(self.num_rows, self.num_cols, rp, ci, va)
+
+    @classmethod
+    def from_device(cls, ctx, rows, cols, nnz, rp_ptr, col_ptr, val_ptr):
+        """D2D import of CSR arrays already on this device (int64/int32/fp64)."""
+        h = ctypes.c_void_p()
+        check(load().tsg_csr_from_device(ctx.h, rows, cols, nnz, ctypes.c_void_p(rp_ptr),
+                                         ctypes.c_void_p(col_ptr),
+                                         None if val_ptr is None else ctypes.c_void_p(val_ptr),
+                                         ctypes.byref(h)))
+        return cls(ctx, h)
+
+    def device_ptrs(self):
+        rp, ci, va = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        check(load().tsg_csr_device_ptrs(self.h, ctypes.byref(rp), ctypes.byref(ci), ctypes.byref(va)))
+        return rp.value, ci.value, va.value
 
     def slice_rows(self, begin, end):
         h = ctypes.c_void_p()

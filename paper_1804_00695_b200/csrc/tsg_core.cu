@@ -73,6 +73,11 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     int init_err[2] = {0, 0x7fffffff};
     TSG_CK(cudaMemcpy(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice));
     for (int i = 0; i < 8; i++) TSG_CK(cudaEventCreate(&c->ev[i]));
+    for (int i = 0; i < 8; i++) TSG_CK(cudaEventCreate(&c->ev_user[i]));
+    for (int i = 0; i < 2; i++) {
+        TSG_CK(cudaEventCreate(&c->ev_num[i]));
+        TSG_CK(cudaEventCreate(&c->ev_sym[i]));
+    }
     c->timing = 0;
     *out = c;
     return TSG_OK;
@@ -105,6 +110,43 @@ extern "C" int tsg_mem_in_use(tsg_ctx *c, int64_t *bytes) {
 
 extern "C" int tsg_set_timing(tsg_ctx *c, int enabled) {
     c->timing = enabled ? 1 : 0;
+    return TSG_OK;
+}
+
+extern "C" int tsg_event_record(tsg_ctx *c, int slot) {
+    if (slot < 0 || slot >= 8) {
+        tsg_set_error("event slot %d out of range", slot);
+        return TSG_EARG;
+    }
+    TSG_CK(cudaEventRecord(c->ev_user[slot], c->stream));
+    return TSG_OK;
+}
+
+extern "C" int tsg_event_elapsed(tsg_ctx *c, int from, int to, float *ms) {
+    if (from < 0 || from >= 8 || to < 0 || to >= 8) {
+        tsg_set_error("event slot out of range");
+        return TSG_EARG;
+    }
+    TSG_CK(cudaEventSynchronize(c->ev_user[to]));
+    TSG_CK(cudaEventElapsedTime(ms, c->ev_user[from], c->ev_user[to]));
+    return TSG_OK;
+}
+
+extern "C" int tsg_get_stats(tsg_ctx *c, tsg_stats *st) {
+    st->launches = c->launches;
+    st->symbolic_ms = 0.f;
+    st->numeric_ms = 0.f;
+    if (c->timing) {
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        if (cudaEventElapsedTime(&st->symbolic_ms, c->ev_sym[0], c->ev_sym[1]) != cudaSuccess) {
+            cudaGetLastError();
+            st->symbolic_ms = -1.f;
+        }
+        if (cudaEventElapsedTime(&st->numeric_ms, c->ev_num[0], c->ev_num[1]) != cudaSuccess) {
+            cudaGetLastError();
+            st->numeric_ms = -1.f;
+        }
+    }
     return TSG_OK;
 }
 
@@ -162,6 +204,14 @@ int tsg_free(tsg_ctx *c, void *p) {
     }
     TSG_CK(cudaFreeAsync(p, c->stream));
     return TSG_OK;
+}
+
+int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size_t smem) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return TSG_OK;
+    tsg_set_error("launch of %s (bin %d, grid %u, block %d, dynamic smem %zu) failed: %s", kernel,
+                  bin, grid, block, smem, cudaGetErrorString(e));
+    return TSG_ECUDA;
 }
 
 int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
@@ -298,11 +348,11 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     int64_t *sums = nullptr;
     TSG_TRY(tsg_alloc_t(c, &sums, tiles + 1));
-    scan_tile_sums<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums);
-    scan_sums_single<<<1, 1024, 0, c->stream>>>(sums, tiles);
+    scan_tile_sums<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums); ++c->launches;
+    scan_sums_single<<<1, 1024, 0, c->stream>>>(sums, tiles); ++c->launches;
     // in-place safe: every tile reads its inputs into registers before writing,
     // and tiles write only their own range (plus out[n], past every input).
-    scan_tiles<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums, out);
+    scan_tiles<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums, out); ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, sums));
     return TSG_OK;
@@ -434,7 +484,7 @@ extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nn
         TSG_TRY(tsg_alloc_t(c, &stage, nnz));
         TSG_CK(cudaMemcpyAsync(stage, col_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice,
                                c->stream));
-        cols_i64_to_i32<<<ew_grid(c, nnz), 256, 0, c->stream>>>(stage, m->col, nnz, cols, c->d_err);
+        cols_i64_to_i32<<<ew_grid(c, nnz), 256, 0, c->stream>>>(stage, m->col, nnz, cols, c->d_err); ++c->launches;
         if (values)
             TSG_CK(cudaMemcpyAsync(m->val, values, nnz * sizeof(double), cudaMemcpyHostToDevice,
                                    c->stream));
@@ -466,7 +516,7 @@ extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
     if (m->nnz > 0 && col_idx) {
         int64_t *stage = nullptr;
         TSG_TRY(tsg_alloc_t(c, &stage, m->nnz));
-        cols_i32_to_i64<<<ew_grid(c, m->nnz), 256, 0, c->stream>>>(m->col, stage, m->nnz, 0);
+        cols_i32_to_i64<<<ew_grid(c, m->nnz), 256, 0, c->stream>>>(m->col, stage, m->nnz, 0); ++c->launches;
         TSG_CK(cudaMemcpyAsync(col_idx, stage, m->nnz * sizeof(int64_t), cudaMemcpyDeviceToHost,
                                c->stream));
         TSG_TRY(tsg_free(c, stage));
@@ -491,7 +541,7 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
     tsg_csr *s = nullptr;
     TSG_TRY(tsg_csr_alloc(c, end - begin, m->cols, hi - lo, m->val != nullptr, &s));
     rebase_rp<<<ew_grid(c, end - begin + 1), 256, 0, c->stream>>>(m->rp + begin, s->rp,
-                                                                  end - begin + 1);
+                                                                  end - begin + 1); ++c->launches;
     if (hi > lo) {
         TSG_CK(cudaMemcpyAsync(s->col, m->col + lo, (hi - lo) * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice, c->stream));
@@ -501,6 +551,32 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
     }
     TSG_CK(cudaGetLastError());
     *out = s;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_from_device(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
+                                   const int64_t *d_rp, const int32_t *d_col, const double *d_val,
+                                   tsg_csr **out) {
+    tsg_csr *m = nullptr;
+    TSG_TRY(tsg_csr_alloc(c, rows, cols, nnz, d_val != nullptr, &m));
+    TSG_CK(cudaMemcpyAsync(m->rp, d_rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                           c->stream));
+    if (nnz > 0) {
+        TSG_CK(cudaMemcpyAsync(m->col, d_col, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                               c->stream));
+        if (d_val)
+            TSG_CK(cudaMemcpyAsync(m->val, d_val, nnz * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+    }
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    *out = m;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_device_ptrs(const tsg_csr *m, int64_t **rp, int32_t **col, double **val) {
+    if (rp) *rp = m->rp;
+    if (col) *col = m->col;
+    if (val) *val = m->val;
     return TSG_OK;
 }
 

@@ -35,6 +35,10 @@ struct tsg_ctx {
     cudaEvent_t ev[8];
     float phase_ms[8];
     int64_t bytes_in_use;
+    int64_t launches;         // kernels launched by this context (all entry points)
+    cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
+    cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
+    cudaEvent_t ev_user[8];   // tsg_event_record slots
 };
 
 struct tsg_csr {
@@ -93,6 +97,9 @@ inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
 }
 // Reads and clears the device error flag (synchronises the compute stream).
 int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
+
+// cudaGetLastError after a launch, with the launch shape in the message
+int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size_t smem);
 
 // ---------------------------------------------------------------- scan
 // Exclusive prefix sum of n int64 values into out[0..n] (out[n] = total).

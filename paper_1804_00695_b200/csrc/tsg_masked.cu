@@ -187,11 +187,10 @@ int launch_mask_group(tsg_ctx *c, const int32_t *list, const int64_t *off, const
     int64_t n = off[B + 1] - off[B];
     if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
-    if (smem > 48 * 1024)
-        TSG_CK(cudaFuncSetAttribute(k_mask_group<G, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+    TSG_CK(cudaFuncSetAttribute(k_mask_group<G, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
     k_mask_group<G, SL><<<grid_for(n, BS / G, c->num_sms * 64), BS, smem, c->stream>>>(list + off[B],
-                                                                                      n, a);
+                                                                                      n, a); ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -260,10 +259,10 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     TSG_TRY(tsg_alloc_t(c, &tc, (size_t)MB * ntiles));
     TSG_TRY(tsg_alloc_t(c, &offs, (size_t)MB * ntiles + 1));
     TSG_TRY(tsg_alloc_t(c, &list, rows));
-    k_mask_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, l->rp, bins);
-    k_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc);
+    k_mask_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, l->rp, bins); ++c->launches;
+    k_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)MB * ntiles));
-    k_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, list);
+    k_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, list); ++c->launches;
     TSG_CK(cudaGetLastError());
     int64_t off[MB + 1];
     for (int b = 0; b <= MB; b++)
@@ -288,7 +287,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
         TSG_CK(cudaFuncSetAttribute(k_mask_block<512, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_mask_block<512, false><<<grid_for(n7, 1, c->num_sms * 4), 512, smem, c->stream>>>(
-            list + off[7], n7, a, nullptr, 0, 8192);
+            list + off[7], n7, a, nullptr, 0, 8192); ++c->launches;
         TSG_CK(cudaGetLastError());
     }
     int64_t n8 = off[9] - off[8];
@@ -297,7 +296,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
         unsigned long long *dmax = (unsigned long long *)(c->d_small + 24);
         TSG_CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
         k_maxlen<<<grid_for(n8, 256, c->num_sms * 4), 256, 0, c->stream>>>(list + off[8], n8, l->rp,
-                                                                          dmax);
+                                                                          dmax); ++c->launches;
         TSG_CK(cudaMemcpyAsync(&c->h_small[0], dmax, sizeof(int64_t), cudaMemcpyDeviceToHost,
                                c->stream));
         TSG_CK(cudaStreamSynchronize(c->stream));
@@ -308,7 +307,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
         if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
         TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
         k_mask_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(list + off[8], n8, a, slab, T,
-                                                                      (int)T);
+                                                                      (int)T); ++c->launches;
         TSG_CK(cudaGetLastError());
     }
     TSG_CK(cudaMemcpyAsync(&c->h_small[1], dtot, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -355,7 +354,7 @@ extern "C" int tsg_cmat_download(tsg_ctx *c, const tsg_cmat *cm, int64_t *row_pt
         TSG_TRY(tsg_alloc_t(c, &oset, ns));
         TSG_TRY(tsg_alloc_t(c, &obits, ns));
         k_cmat_compact<<<grid_for(cm->rows, 8, c->num_sms * 32), 256, 0, c->stream>>>(
-            cm->rows, cm->start, cm->cnt, off, cm->set, cm->bits, oset, obits);
+            cm->rows, cm->start, cm->cnt, off, cm->set, cm->bits, oset, obits); ++c->launches;
         TSG_CK(cudaGetLastError());
         if (set_idx)
             TSG_CK(cudaMemcpyAsync(set_idx, oset, ns * sizeof(int64_t), cudaMemcpyDeviceToHost,
@@ -378,14 +377,14 @@ extern "C" int tsg_cmat_upload(tsg_ctx *c, int64_t rows, int64_t n_sets, const i
     TSG_CK(cudaMemcpyAsync(cm->start, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                            c->stream));
     k_cmat_from_compact<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, cm->start,
-                                                                                   cm->cnt);
+                                                                                   cm->cnt); ++c->launches;
     if (n_sets > 0) {
         int64_t *stage = nullptr;
         TSG_TRY(tsg_alloc_t(c, &stage, n_sets));
         TSG_CK(cudaMemcpyAsync(stage, set_idx, n_sets * sizeof(int64_t), cudaMemcpyHostToDevice,
                                c->stream));
         k_i64_to_i32<<<grid_for(n_sets, 256, c->num_sms * 8), 256, 0, c->stream>>>(stage, cm->set,
-                                                                                   n_sets);
+                                                                                   n_sets); ++c->launches;
         TSG_CK(cudaMemcpyAsync(cm->bits, set_bits, n_sets * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                c->stream));
         TSG_TRY(tsg_free(c, stage));

@@ -784,9 +784,9 @@ int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out)
     TSG_TRY(tsg_alloc_t(c, &tc, (size_t)NBINS * ntiles));
     TSG_TRY(tsg_alloc_t(c, &offs, (size_t)NBINS * ntiles + 1));
     TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
-    k_bin_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc);
+    k_bin_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NBINS * ntiles));
-    k_bin_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list);
+    k_bin_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list); ++c->launches;
     TSG_CK(cudaGetLastError());
     // bin starts: offs[b * ntiles]
     for (int b = 0; b <= NBINS; b++)
@@ -799,10 +799,16 @@ int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out)
     return TSG_OK;
 }
 
+// Opt in to the dynamic shared memory a launch needs (static + dynamic must fit
+// 227 KB; the default dynamic cap is 48 KB minus the static part).  Raised
+// monotonically per kernel, so steady-state launches skip the call.
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
+    static size_t granted = 0;   // one per template instantiation (per kernel)
+    if (bytes > granted) {
         TSG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        granted = bytes;
+    }
     return TSG_OK;
 }
 
@@ -820,8 +826,9 @@ int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_sym_group<G, SL>, smem));
-    k_sym_group<G, SL><<<group_grid(c, n, BS / G), BS, smem, c->stream>>>(bl.list + bl.off[B], n, a);
-    TSG_CK(cudaGetLastError());
+    unsigned grid = group_grid(c, n, BS / G);
+    k_sym_group<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_group", B, grid, BS, smem));
     return TSG_OK;
 }
 
@@ -832,8 +839,9 @@ int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
     if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_num_group<G, SL>, smem));
-    k_num_group<G, SL><<<group_grid(c, n, BS / G), BS, smem, c->stream>>>(bl.list + bl.off[B], n, a);
-    TSG_CK(cudaGetLastError());
+    unsigned grid = group_grid(c, n, BS / G);
+    k_num_group<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_num_group", B, grid, BS, smem));
     return TSG_OK;
 }
 
@@ -846,7 +854,7 @@ int launch_sym_cta(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     size_t smem = (size_t)TS * 16;
     TSG_TRY(set_smem(k_sym_block<NT, false>, smem));
     k_sym_block<NT, false><<<grid_for(n, 1, c->num_sms * 8), NT, smem, c->stream>>>(
-        bl.list + bl.off[B], n, a, nullptr, 0, TS);
+        bl.list + bl.off[B], n, a, nullptr, 0, TS); ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -860,7 +868,7 @@ int launch_num_cta(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
     size_t smem = (size_t)TS * 24;
     TSG_TRY(set_smem(k_num_block<NT, false>, smem));
     k_num_block<NT, false><<<grid_for(n, 1, c->num_sms * 8), NT, smem, c->stream>>>(
-        bl.list + bl.off[B], n, a, nullptr, nullptr, 0, TS);
+        bl.list + bl.off[B], n, a, nullptr, nullptr, 0, TS); ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -884,7 +892,7 @@ __global__ void k_max_i64_list(const int32_t *list, int64_t n, const int64_t *v,
 int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64_t &out) {
     TSG_CK(cudaMemsetAsync(c->d_small, 0, sizeof(int64_t), c->stream));
     k_max_i64_list<<<grid_for(n, 256, c->num_sms * 4), 256, 0, c->stream>>>(
-        list, n, v, (unsigned long long *)c->d_small);
+        list, n, v, (unsigned long long *)c->d_small); ++c->launches;
     TSG_CK(cudaMemcpyAsync(c->h_small, c->d_small, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
     out = c->h_small[0];
@@ -909,7 +917,7 @@ int launch_sym_global(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     int4 *slab = nullptr;
     TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
     k_sym_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab, T,
-                                                                   (int)T);
+                                                                   (int)T); ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, slab));
     return TSG_OK;
@@ -935,7 +943,7 @@ int launch_num_global(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
     TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
     TSG_TRY(tsg_alloc_t(c, &sortslab, (size_t)(ctas * T)));
     k_num_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab,
-                                                                   sortslab, T, (int)T);
+                                                                   sortslab, T, (int)T); ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, slab));
     TSG_TRY(tsg_free(c, sortslab));
@@ -985,7 +993,7 @@ void launch_bounds_g(tsg_ctx *c, int64_t rows, const tsg_csr *a, const int64_t *
                      unsigned long long *total) {
     unsigned grid = grid_for(rows, 256 / G, c->num_sms * 32);
     k_row_bounds<G><<<grid, 256, 0, c->stream>>>(rows, a->rp, a->col, brp, cbcnt, flops, sbound,
-                                                 total);
+                                                 total); ++c->launches;
 }
 
 void launch_bounds(tsg_ctx *c, const tsg_csr *a, const int64_t *brp, const int32_t *cbcnt,
@@ -1003,7 +1011,7 @@ void launch_compress_g(tsg_ctx *c, const tsg_csr *b, tsg_cmat *cm, int *n_unsort
                        int32_t *unsorted) {
     unsigned grid = grid_for(b->rows, 256 / G, c->num_sms * 32);
     k_compress<G><<<grid, 256, 0, c->stream>>>(b->rows, b->rp, b->col, cm->cnt, cm->set, cm->bits,
-                                               n_unsorted, unsorted);
+                                               n_unsorted, unsorted); ++c->launches;
 }
 
 }  // namespace
@@ -1032,7 +1040,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         }
         // slow path launches unconditionally; it exits at once when no row is unsorted
         k_compress_unsorted<256><<<c->num_sms * 2, 256, 0, c->stream>>>(n_uns, uns, b->rp, b->col,
-                                                                       cm->cnt, cm->set, cm->bits);
+                                                                       cm->cnt, cm->set, cm->bits); ++c->launches;
         TSG_CK(cudaGetLastError());
         TSG_TRY(tsg_free(c, uns));
     }
@@ -1061,7 +1069,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
                                      partial ? partial->rp : nullptr, sbound));
         }
         k_sym_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, sbound, bins, v->d, v->aux);
+            rows_out, sbound, bins, v->d, v->aux); ++c->launches;
         TSG_CK(cudaGetLastError());
         BinLists bl;
         TSG_TRY(partition_rows(c, rows_out, bins, bl));
@@ -1081,7 +1089,9 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.counts = v->d;
         sa.msets = v->aux;
         sa.err = c->d_err;
+        if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
+        if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
         TSG_TRY(tsg_free(c, bl.list));
     }
     TSG_TRY(tsg_free(c, bins));
@@ -1119,7 +1129,7 @@ int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_r
                      int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
                      const int64_t *prp, int64_t *sbound) {
     k_fused_bounds<<<grid_for(rows_out, 8, c->num_sms * 32), 256, 0, c->stream>>>(
-        rows_out, a->rp, a->col, a_row_off, b_lo, b_hi, cbstart, cbcnt, prp, sbound);
+        rows_out, a->rp, a->col, a_row_off, b_lo, b_hi, cbstart, cbcnt, prp, sbound); ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -1164,7 +1174,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     }
     if (rows_out > 0 && nnz > 0) {
         k_num_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, counts->d, counts->aux, sbound_in, bins);
+            rows_out, counts->d, counts->aux, sbound_in, bins); ++c->launches;
         TSG_CK(cudaGetLastError());
         BinLists bl;
         TSG_TRY(partition_rows(c, rows_out, bins, bl));
@@ -1192,7 +1202,9 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.ccol = C->col;
         na.cval = C->val;
         na.err = c->d_err;
+        if (c->timing) cudaEventRecord(c->ev_num[0], c->stream);
         TSG_TRY(run_numeric_bins(c, bl, na));
+        if (c->timing) cudaEventRecord(c->ev_num[1], c->stream);
         TSG_TRY(tsg_free(c, bl.list));
     }
     TSG_TRY(tsg_free(c, bins));

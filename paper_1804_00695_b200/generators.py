@@ -50,26 +50,19 @@ def _offsets(kind):
     raise GridError("unknown stencil kind %r" % (kind,))
 
 
-def stencil(kind: str, dims) -> CsrMatrix:
-    """Grid operator with row-sorted columns (first axis fastest)."""
-    dims = tuple(int(d) for d in dims)
-    want = 2 if kind in (LAPLACE2D, BIGSTAR2D) else 3
-    if len(dims) != want:
-        raise GridError("%s needs %d grid dims" % (kind, want))
-    if any(d <= 0 for d in dims):
-        raise GridError("grid dims must be positive")
+def _scalar_rows(kind, dims, lo, hi):
+    """(row_len, cols, vals) of scalar stencil rows [lo, hi), row-sorted."""
     offs = _offsets(kind)
     strides = [1]
     for d in dims[:-1]:
         strides.append(strides[-1] * d)
     # ascending linear shift == ascending column within every row
     offs.sort(key=lambda o: sum(s * st for s, st in zip(o[0], strides)))
-    n = int(np.prod(dims))
-    idx = np.arange(n, dtype=np.int64)
+    idx = np.arange(lo, hi, dtype=np.int64)
     coord = [(idx // st) % d for st, d in zip(strides, dims)]
     k = len(offs)
-    keep = np.ones((n, k), dtype=bool)
-    cand = np.empty((n, k), dtype=np.int64)
+    keep = np.ones((hi - lo, k), dtype=bool)
+    cand = np.empty((hi - lo, k), dtype=np.int64)
     vals = np.empty(k, dtype=np.float64)
     for j, (shift, w) in enumerate(offs):
         ok = keep[:, j]
@@ -78,9 +71,35 @@ def stencil(kind: str, dims) -> CsrMatrix:
                 ok &= (coord[ax] + s >= 0) & (coord[ax] + s < dims[ax])
         cand[:, j] = idx + sum(s * st for s, st in zip(shift, strides))
         vals[j] = w
-    row_len = keep.sum(axis=1)
-    cols = cand[keep]
-    v = np.broadcast_to(vals, (n, k))[keep]
+    return keep.sum(axis=1), cand[keep], np.ascontiguousarray(np.broadcast_to(vals, keep.shape)[keep])
+
+
+def _check_dims(kind, dims):
+    dims = tuple(int(d) for d in dims)
+    want = 2 if kind in (LAPLACE2D, BIGSTAR2D) else 3
+    if len(dims) != want:
+        raise GridError("%s needs %d grid dims" % (kind, want))
+    if any(d <= 0 for d in dims):
+        raise GridError("grid dims must be positive")
+    return dims
+
+
+def stencil_rows(kind: str, dims, lo: int, hi: int) -> CsrMatrix:
+    """Rows [lo, hi) of a scalar stencil operator (a row shard, full column
+    space) -- what one rank of the row partition builds."""
+    dims = _check_dims(kind, dims)
+    n = int(np.prod(dims))
+    row_len, cols, v = _scalar_rows(kind, dims, lo, hi)
+    ptr = np.zeros(hi - lo + 1, dtype=np.int64)
+    np.cumsum(row_len, out=ptr[1:])
+    return CsrMatrix._adopt(hi - lo, n, ptr, cols, v)
+
+
+def stencil(kind: str, dims) -> CsrMatrix:
+    """Grid operator with row-sorted columns (first axis fastest)."""
+    dims = _check_dims(kind, dims)
+    n = int(np.prod(dims))
+    row_len, cols, v = _scalar_rows(kind, dims, 0, n)
     ptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(row_len, out=ptr[1:])
     if kind != ELASTICITY3D:
