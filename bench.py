@@ -241,14 +241,19 @@ def main():
     for _ in range(args.warmup):
         dra, drap, _ = step()
     if args.phases:
-        for _ in range(3):
+        for _ in range(4):
             ctx.record(0)
+            h0 = time.perf_counter()
+            res0 = ctx.pool_reserved()
             dra = kernel.multiply_device(dr, da)
+            h1 = time.perf_counter()
             ph1, st1 = ctx.phase_ms(), ctx.stats()
             drap = kernel.multiply_device(dra, dp)
             ph2, st2 = ctx.phase_ms(), ctx.stats()
             ctx.record(1)
-            print(json.dumps({"step_ms": ctx.elapsed_ms(0, 1),
+            h2 = time.perf_counter()
+            print(json.dumps({"step_ms": ctx.elapsed_ms(0, 1), "host_ms": [1e3 * (h1 - h0), 1e3 * (h2 - h1)],
+                              "pool_reserved_mb": [res0 >> 20, ctx.pool_reserved() >> 20],
                               "RA": {"compress": ph1[0], "symbolic": ph1[1], "scan": ph1[2],
                                      "numeric": ph1[3], "total": ph1[5],
                                      "sym_kernels": st1[1], "num_kernels": st1[2]},

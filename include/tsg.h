@@ -58,6 +58,8 @@ int tsg_destroy(tsg_ctx *ctx);
 int tsg_sync(tsg_ctx *ctx);
 /* Bytes of device memory currently held by the context's allocations. */
 int tsg_mem_in_use(tsg_ctx *ctx, int64_t *bytes);
+/* Bytes the device's stream-ordered pool has reserved from the driver. */
+int tsg_pool_reserved(tsg_ctx *ctx, int64_t *bytes);
 /* Per-phase device times (ms) of the last tsg_multiply (timing enabled):
    [0] compress [1] symbolic [2] row-pointer scan [3] numeric [5] total */
 int tsg_last_phase_ms(tsg_ctx *ctx, float *out, int n);

@@ -36,7 +36,7 @@ _ERRORS = {
 # every symbol include/tsg.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "tsg_last_error", "tsg_abi_version", "tsg_device_count", "tsg_init", "tsg_destroy",
-    "tsg_sync", "tsg_mem_in_use", "tsg_last_phase_ms", "tsg_set_timing", "tsg_get_stats",
+    "tsg_sync", "tsg_mem_in_use", "tsg_pool_reserved", "tsg_last_phase_ms", "tsg_set_timing", "tsg_get_stats",
     "tsg_csr_upload", "tsg_csr_info", "tsg_csr_download", "tsg_csr_slice_rows", "tsg_csr_free",
     "tsg_compress", "tsg_cmat_info", "tsg_cmat_download", "tsg_cmat_upload", "tsg_cmat_free",
     "tsg_vec_upload", "tsg_vec_download", "tsg_vec_len", "tsg_vec_free",
@@ -58,6 +58,7 @@ _SIGS = {
     "tsg_destroy": ([_P], ctypes.c_int),
     "tsg_sync": ([_P], ctypes.c_int),
     "tsg_mem_in_use": ([_P, _PI64], ctypes.c_int),
+    "tsg_pool_reserved": ([_P, _PI64], ctypes.c_int),
     "tsg_last_phase_ms": ([_P, ctypes.POINTER(ctypes.c_float), ctypes.c_int], ctypes.c_int),
     "tsg_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
     "tsg_get_stats": ([_P, _P], ctypes.c_int),
@@ -173,6 +174,11 @@ class Context:
     def elapsed_ms(self, a, b):
         v = ctypes.c_float()
         check(load().tsg_event_elapsed(self.h, a, b, ctypes.byref(v)))
+        return v.value
+
+    def pool_reserved(self):
+        v = ctypes.c_int64(0)
+        check(load().tsg_pool_reserved(self.h, ctypes.byref(v)))
         return v.value
 
     def mem_in_use(self):

@@ -6,6 +6,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -45,8 +47,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
         return TSG_EARG;
     }
     TSG_CK(cudaSetDevice(device));
-    tsg_ctx *c = new tsg_ctx();
-    memset(c, 0, sizeof(*c));
+    tsg_ctx *c = new tsg_ctx();   // value-initialised (all zero)
     c->device = device;
     cudaDeviceProp prop;
     TSG_CK(cudaGetDeviceProperties(&prop, device));
@@ -87,6 +88,7 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
     if (!c) return TSG_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    tsg_arena_trim(c);
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
     cudaFree(c->d_err);
     cudaFree(c->d_small);
@@ -105,6 +107,15 @@ extern "C" int tsg_sync(tsg_ctx *c) {
 
 extern "C" int tsg_mem_in_use(tsg_ctx *c, int64_t *bytes) {
     *bytes = c->bytes_in_use;
+    return TSG_OK;
+}
+
+extern "C" int tsg_pool_reserved(tsg_ctx *c, int64_t *bytes) {
+    cudaMemPool_t pool;
+    TSG_CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    uint64_t v = 0;
+    TSG_CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v));
+    *bytes = (int64_t)v;
     return TSG_OK;
 }
 
@@ -164,45 +175,148 @@ void PhaseTimer::finish(int total_slot) {
 }
 
 // ------------------------------------------------------------------ memory
-// Stream-ordered allocation from the device's default pool (release threshold
-// raised in tsg_init, so steady-state calls never reach the OS).  Sizes are
-// tracked host-side so tsg_mem_in_use reports the context's footprint.
 
-static std::mutex g_alloc_mu;
-static std::unordered_map<void *, size_t> g_alloc_sizes;
+
+static double now_us() {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+}
+
+int tsg_trace_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("TSG_TRACE");
+        on = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return on;
+}
+
+void tsg_trace(tsg_ctx *c, const char *what, int64_t arg) {
+    if (!tsg_trace_enabled()) return;
+    double t0 = now_us();
+    cudaStreamSynchronize(c->stream);
+    double t1 = now_us();
+    fprintf(stderr, "[tsg %12.1f us] %-28s %14lld  (gpu drain %.1f us)\n", t0, what, (long long)arg,
+            t1 - t0);
+}
+
+// Caching layer over cudaMallocAsync.  Per-call temporaries (compressed B,
+// bins, row lists, bounds) and outputs are recycled through a best-fit free
+// list instead of going back to the driver pool: measured on B200, a 445 MB
+// cudaMallocAsync right after a same-size cudaFreeAsync can block the host
+// for 0.4-100 ms.  Blocks are only reused in the context's compute-stream
+// order (every libtsg kernel and copy runs on that stream or is joined to it
+// by an event before the memory is released).
+struct Arena {
+    std::mutex mu;
+    std::multimap<size_t, void *> free_blocks;   // size class -> block
+    std::unordered_map<void *, size_t> live;     // block -> size class
+    size_t cached = 0;
+};
+
+static std::mutex g_arena_mu;
+static std::unordered_map<const tsg_ctx *, Arena *> g_arenas;
+
+static Arena *arena_of(tsg_ctx *c) {
+    std::lock_guard<std::mutex> g(g_arena_mu);
+    Arena *&a = g_arenas[c];
+    if (!a) a = new Arena();
+    return a;
+}
+
+static size_t size_class(size_t bytes) {
+    if (bytes <= 4096) return 4096;
+    if (bytes <= (1u << 20)) {
+        size_t p = 4096;
+        while (p < bytes) p <<= 1;
+        return p;
+    }
+    return (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);   // 1 MiB granules
+}
+
+static const size_t ARENA_CACHE_LIMIT = (size_t)48 << 30;
 
 int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
     *p = nullptr;
-    if (bytes == 0) bytes = 16;
-    bytes = (bytes + 255) & ~(size_t)255;
+    tsg_trace(c, "alloc", (int64_t)bytes);
+    Arena *A = arena_of(c);
+    size_t cls = size_class(bytes);
+    {
+        std::lock_guard<std::mutex> g(A->mu);
+        auto it = A->free_blocks.lower_bound(cls);
+        if (it != A->free_blocks.end() && it->first <= cls + cls / 4) {   // best fit, <= 25% slack
+            *p = it->second;
+            size_t got = it->first;
+            A->free_blocks.erase(it);
+            A->cached -= got;
+            A->live[*p] = got;
+            c->bytes_in_use += (int64_t)got;
+            return TSG_OK;
+        }
+    }
     void *raw = nullptr;
-    cudaError_t e = cudaMallocAsync(&raw, bytes, c->stream);
+    cudaError_t e = cudaMallocAsync(&raw, cls, c->stream);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
-        tsg_set_error("device allocation of %zu bytes failed (out of HBM)", bytes);
-        return TSG_ECAPACITY;
+        tsg_arena_trim(c);   // give the cache back to the driver and retry once
+        e = cudaMallocAsync(&raw, cls, c->stream);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            tsg_set_error("device allocation of %zu bytes failed (out of HBM)", bytes);
+            return TSG_ECAPACITY;
+        }
     }
     if (e != cudaSuccess) return tsg_cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
-    {
-        std::lock_guard<std::mutex> g(g_alloc_mu);
-        g_alloc_sizes[raw] = bytes;
-        c->bytes_in_use += (int64_t)bytes;
-    }
+    std::lock_guard<std::mutex> g(A->mu);
+    A->live[raw] = cls;
+    c->bytes_in_use += (int64_t)cls;
     *p = raw;
     return TSG_OK;
 }
 
 int tsg_free(tsg_ctx *c, void *p) {
     if (!p) return TSG_OK;
-    {
-        std::lock_guard<std::mutex> g(g_alloc_mu);
-        auto it = g_alloc_sizes.find(p);
-        if (it != g_alloc_sizes.end()) {
-            c->bytes_in_use -= (int64_t)it->second;
-            g_alloc_sizes.erase(it);
-        }
+    Arena *A = arena_of(c);
+    std::lock_guard<std::mutex> g(A->mu);
+    auto it = A->live.find(p);
+    if (it == A->live.end()) {
+        TSG_CK(cudaFreeAsync(p, c->stream));
+        return TSG_OK;
     }
-    TSG_CK(cudaFreeAsync(p, c->stream));
+    size_t cls = it->second;
+    A->live.erase(it);
+    c->bytes_in_use -= (int64_t)cls;
+    if (A->cached + cls > ARENA_CACHE_LIMIT) {
+        TSG_CK(cudaFreeAsync(p, c->stream));
+        return TSG_OK;
+    }
+    A->free_blocks.emplace(cls, p);
+    A->cached += cls;
+    return TSG_OK;
+}
+
+int tsg_arena_trim(tsg_ctx *c) {
+    Arena *A = arena_of(c);
+    std::lock_guard<std::mutex> g(A->mu);
+    for (auto &kv : A->free_blocks) cudaFreeAsync(kv.second, c->stream);
+    A->free_blocks.clear();
+    A->cached = 0;
+    cudaStreamSynchronize(c->stream);
+    return TSG_OK;
+}
+
+int tsg_func_smem(const void *kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> granted[64];
+    int dev = 0;
+    TSG_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    size_t &have = granted[dev & 63][kernel];
+    if (bytes > have) {
+        TSG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        have = bytes;
+    }
     return TSG_OK;
 }
 

@@ -91,6 +91,8 @@ __device__ __forceinline__ void kerr(int *err, int code, int64_t row) {
 // ---------------------------------------------------------------- memory
 int tsg_alloc(tsg_ctx *ctx, void **p, size_t bytes);
 int tsg_free(tsg_ctx *ctx, void *p);
+// return every cached block to the driver pool
+int tsg_arena_trim(tsg_ctx *ctx);
 template <typename T>
 inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
     return tsg_alloc(ctx, (void **)p, count * sizeof(T));
@@ -98,8 +100,17 @@ inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
 // Reads and clears the device error flag (synchronises the compute stream).
 int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
 
+int tsg_trace_enabled();
+// TSG_TRACE=1: host timestamps + GPU drain per traced step (debug only)
+void tsg_trace(tsg_ctx *c, const char *what, int64_t arg);
+
 // cudaGetLastError after a launch, with the launch shape in the message
 int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size_t smem);
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device
+// (static + dynamic must fit 227 KB; the default dynamic cap is 48 KB minus
+// the static part).  Cached per (device, kernel): steady state makes no call.
+int tsg_func_smem(const void *kernel, size_t bytes);
 
 // ---------------------------------------------------------------- scan
 // Exclusive prefix sum of n int64 values into out[0..n] (out[n] = total).

@@ -187,8 +187,7 @@ int launch_mask_group(tsg_ctx *c, const int32_t *list, const int64_t *off, const
     int64_t n = off[B + 1] - off[B];
     if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
-    TSG_CK(cudaFuncSetAttribute(k_mask_group<G, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+    TSG_TRY(tsg_func_smem((const void *)k_mask_group<G, SL>, smem));
     k_mask_group<G, SL><<<grid_for(n, BS / G, c->num_sms * 64), BS, smem, c->stream>>>(list + off[B],
                                                                                       n, a); ++c->launches;
     TSG_CK(cudaGetLastError());
@@ -284,8 +283,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     int64_t n7 = off[8] - off[7];
     if (n7 > 0) {
         size_t smem = 8192 * 16;
-        TSG_CK(cudaFuncSetAttribute(k_mask_block<512, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TSG_TRY(tsg_func_smem((const void *)k_mask_block<512, false>, smem));
         k_mask_block<512, false><<<grid_for(n7, 1, c->num_sms * 4), 512, smem, c->stream>>>(
             list + off[7], n7, a, nullptr, 0, 8192); ++c->launches;
         TSG_CK(cudaGetLastError());

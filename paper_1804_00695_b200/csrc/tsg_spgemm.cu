@@ -72,6 +72,7 @@ struct NumArgs {
     int32_t *ccol;
     double *cval;
     int *err;
+    int seq;   // host-chosen product mode: B rows long enough for lane-per-entry
 };
 
 // ======================================================================= K0
@@ -411,12 +412,54 @@ __device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, 
     __syncwarp(gm);
 }
 
-template <int G, int SLICE>
+// Product phase, sequential mode (B rows at least ~G/2 long): A entries are
+// taken one at a time in storage order and the G lanes split that entry's B
+// row.  A B row has distinct columns, so lanes never collide within a step
+// and a plain read-add-write replays the reference's order exactly; a
+// __syncwarp separates consecutive A entries.  No search, no match.
+template <int G>
+__device__ __forceinline__ void products_seq(unsigned gm, int glane, const NumArgs &a, int64_t a0,
+                                             int64_t a1, const int4 *tbl, int T, int logT,
+                                             double *vals) {
+    for (int64_t base = a0; base < a1; base += G) {
+        int64_t t = base + glane;
+        int64_t st = 0;
+        int len = 0;
+        double av = 0.0;
+        if (t < a1) {
+            int k = a.acol[t];
+            if (k >= a.b_lo && k < a.b_hi) {
+                k -= a.b_lo;
+                st = a.brp[k];
+                len = (int)(a.brp[k + 1] - st);
+                av = a.aval[t];
+            }
+        }
+        const int cnt = (int)((a1 - base) < G ? (a1 - base) : G);
+        for (int j = 0; j < cnt; ++j) {
+            int64_t sj = __shfl_sync(gm, st, j, G);
+            int lj = __shfl_sync(gm, len, j, G);
+            double aj = __shfl_sync(gm, av, j, G);
+            for (int q = glane; q < lj; q += G) {
+                int c = a.bcol[sj + q];
+                double prod = __dmul_rn(aj, a.bval[sj + q]);
+                int4 e;
+                tbl_find(tbl, T, logT, c >> 6, e);
+                int pos = e.w + mask_rank(e, c & 63);
+                vals[pos] = __dadd_rn(vals[pos], prod);
+            }
+            __syncwarp(gm);
+        }
+    }
+}
+
+template <int G, int SLICE, bool SEQ>
 __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
     extern __shared__ int4 smem[];
     const unsigned gm = group_mask<G>();
     const int glane = threadIdx.x & (G - 1);
+    const unsigned lt = lanemask_lt();
     const int gpb = blockDim.x / G;
     char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE;
     for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
@@ -425,15 +468,16 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         const int64_t gi = i + a.a_row_off;
         const int n = (int)a.counts[i];
         const int64_t cp = a.cptr[i];
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
         int64_t mest = a.msets ? (int64_t)a.msets[i] : (a.sbound[i] < n ? a.sbound[i] : n);
         double *vals = reinterpret_cast<double *>(slice);
+        int2 *cbuf = reinterpret_cast<int2 *>(slice);   // phase-B scratch, aliases vals
         int4 *tbl = reinterpret_cast<int4 *>(slice + round16(8 * (int64_t)n));
         int T = table_slots(mest);
         const int tmax = (int)((SLICE - round16(8 * (int64_t)n)) / 16);
         if (T > tmax) T = 1 << ilog2_pow2(tmax);   // binning guarantees T <= tmax
         const int logT = ilog2_pow2(T);
         tbl_clear(tbl, T, glane, G);
-        for (int q = glane; q < n; q += G) vals[q] = -0.0;
         __syncwarp(gm);
 
         // phase A: union of column sets (partial row + compressed B rows)
@@ -446,7 +490,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
                          bit >= 32 ? 1u << (bit - 32) : 0u);
         }
         group_enumerate<G>(
-            gm, glane, a.arp[gi], a.arp[gi + 1],
+            gm, glane, a0, a1,
             [&](int64_t t, int64_t &st, int &len) {
                 int k = a.acol[t];
                 if (k >= a.b_lo && k < a.b_hi) {
@@ -463,43 +507,56 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
             });
         __syncwarp(gm);
 
-        // phase B: base offset of each set = columns in smaller sets; emit columns
-        int tot = 0;
-        for (int s = glane; s < T; s += G) {
-            int4 e = tbl[s];
-            if (e.x == TSG_EMPTY) continue;
-            int base = 0;
-            for (int u = 0; u < T; ++u) {
-                int4 f = tbl[u];
-                if (f.x != TSG_EMPTY && f.x < e.x) base += slot_pop(f);
-            }
-            tbl[s].w = base;
+        // phase B: compact the occupied sets (key, slot<<8 | popcount) into the
+        // value area (m <= n entries of 8 B), rank each against the compacted
+        // list -> base = columns in smaller sets; emit the row's columns.
+        int m = 0, tot = 0;
+        for (int r0 = 0; r0 < T; r0 += G) {
+            int s = r0 + glane;
+            int4 e = s < T ? tbl[s] : make_int4(TSG_EMPTY, 0, 0, 0);
+            bool occ = e.x != TSG_EMPTY;
+            unsigned bal = __ballot_sync(gm, occ) & gm;
             int pc = slot_pop(e);
-            tot += pc;
-            if (base + pc <= n) {
-                unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
-                int r = base;
-                while (lo) {
-                    int b = __ffs(lo) - 1;
-                    lo &= lo - 1;
-                    a.ccol[cp + r++] = e.x * 64 + b;
-                }
-                while (hi) {
-                    int b = __ffs(hi) - 1;
-                    hi &= hi - 1;
-                    a.ccol[cp + r++] = e.x * 64 + 32 + b;
-                }
-            }
+            if (occ && m + __popc(bal & lt) < n) cbuf[m + __popc(bal & lt)] = make_int2(e.x, (s << 8) | pc);
+            if (occ) tot += pc;
+            m += __popc(bal);
         }
         tot = group_sum<G, int>(gm, tot);
         ok = __all_sync(gm, ok);
-        __syncwarp(gm);
-        if (tot != n || !ok) {
+        if (tot != n || !ok || m > n) {
             if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+            __syncwarp(gm);
             continue;   // group-uniform
         }
+        __syncwarp(gm);
+        for (int q = glane; q < m; q += G) {
+            int2 me = cbuf[q];
+            int base = 0;
+            for (int u = 0; u < m; ++u) {
+                int2 o = cbuf[u];
+                if (o.x < me.x) base += o.y & 0xff;
+            }
+            int slot = me.y >> 8;
+            tbl[slot].w = base;
+            int4 e = tbl[slot];
+            unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+            int r = base;
+            while (lo) {
+                int b = __ffs(lo) - 1;
+                lo &= lo - 1;
+                a.ccol[cp + r++] = me.x * 64 + b;
+            }
+            while (hi) {
+                int b = __ffs(hi) - 1;
+                hi &= hi - 1;
+                a.ccol[cp + r++] = me.x * 64 + 32 + b;
+            }
+        }
+        __syncwarp(gm);
+        for (int q = glane; q < n; q += G) vals[q] = -0.0;
+        __syncwarp(gm);
 
-        // phase C: partial values first, then products in flattened order
+        // phase C: partial values first, then products in A storage order
         for (int64_t q = p0 + glane; q < p1; q += G) {
             int c = a.pcol[q];
             int4 e;
@@ -507,28 +564,32 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
             vals[e.w + mask_rank(e, c & 63)] = a.pval[q];
         }
         __syncwarp(gm);
-        group_enumerate<G>(
-            gm, glane, a.arp[gi], a.arp[gi + 1],
-            [&](int64_t t, int64_t &st, int &len) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    st = a.brp[k];
-                    len = (int)(a.brp[k + 1] - st);
-                }
-            },
-            [&](bool valid, int j, int64_t t, int64_t s) {
-                int pos = -1;
-                double prod = 0.0;
-                if (valid) {
-                    int c = a.bcol[s];
-                    int4 e;
-                    tbl_find(tbl, T, logT, c >> 6, e);
-                    pos = e.w + mask_rank(e, c & 63);
-                    prod = __dmul_rn(a.aval[t], a.bval[s]);
-                }
-                ordered_add<G>(gm, vals, pos, prod);
-            });
+        if constexpr (SEQ) {
+            products_seq<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
+        } else {
+            group_enumerate<G>(
+                gm, glane, a0, a1,
+                [&](int64_t t, int64_t &st, int &len) {
+                    int k = a.acol[t];
+                    if (k >= a.b_lo && k < a.b_hi) {
+                        k -= a.b_lo;
+                        st = a.brp[k];
+                        len = (int)(a.brp[k + 1] - st);
+                    }
+                },
+                [&](bool valid, int j, int64_t t, int64_t s) {
+                    int pos = -1;
+                    double prod = 0.0;
+                    if (valid) {
+                        int c = a.bcol[s];
+                        int4 e;
+                        tbl_find(tbl, T, logT, c >> 6, e);
+                        pos = e.w + mask_rank(e, c & 63);
+                        prod = __dmul_rn(a.aval[t], a.bval[s]);
+                    }
+                    ordered_add<G>(gm, vals, pos, prod);
+                });
+        }
         __syncwarp(gm);
         for (int q = glane; q < n; q += G) a.cval[cp + q] = vals[q];
         __syncwarp(gm);
@@ -776,7 +837,18 @@ struct BinLists {
     int64_t off[NBINS + 1] = {0};
 };
 
-int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out) {
+__global__ void k_gather_offsets(const int64_t *__restrict__ offs, int ntiles, int nb,
+                                 const int64_t *__restrict__ extra, int64_t *__restrict__ out) {
+    int b = threadIdx.x;
+    if (b <= nb) out[b] = offs[(int64_t)b * ntiles];
+    if (b == 0) out[nb + 1] = extra ? *extra : 0;
+}
+
+// Stable-per-tile partition of rows by bin id.  Bin starts (and, if `extra`
+// is given, one more device int64 such as nnz(C)) come back in ONE D2H copy
+// and one stream sync.
+int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out,
+                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr) {
     int ntiles = (int)((rows + BIN_TILE - 1) / BIN_TILE);
     if (ntiles < 1) ntiles = 1;
     int *tc = nullptr;
@@ -787,29 +859,21 @@ int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out)
     k_bin_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NBINS * ntiles));
     k_bin_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list); ++c->launches;
+    k_gather_offsets<<<1, 32, 0, c->stream>>>(offs, ntiles, NBINS, extra, c->d_small + 32); ++c->launches;
     TSG_CK(cudaGetLastError());
-    // bin starts: offs[b * ntiles]
-    for (int b = 0; b <= NBINS; b++)
-        TSG_CK(cudaMemcpyAsync(&c->h_small[b], offs + (int64_t)b * ntiles, sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, c->stream));
-    TSG_CK(cudaStreamSynchronize(c->stream));
-    for (int b = 0; b <= NBINS; b++) out.off[b] = c->h_small[b];
+    TSG_CK(cudaMemcpyAsync(c->h_small + 32, c->d_small + 32, (NBINS + 2) * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, c->stream));
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b <= NBINS; b++) out.off[b] = c->h_small[32 + b];
+    if (extra_out) *extra_out = c->h_small[32 + NBINS + 1];
     return TSG_OK;
 }
 
-// Opt in to the dynamic shared memory a launch needs (static + dynamic must fit
-// 227 KB; the default dynamic cap is 48 KB minus the static part).  Raised
-// monotonically per kernel, so steady-state launches skip the call.
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
-    static size_t granted = 0;   // one per template instantiation (per kernel)
-    if (bytes > granted) {
-        TSG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        granted = bytes;
-    }
-    return TSG_OK;
+    return tsg_func_smem((const void *)kernel, bytes);
 }
 
 unsigned group_grid(tsg_ctx *c, int64_t nrows, int groups_per_block) {
@@ -832,17 +896,24 @@ int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
-template <int B>
-int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+template <int B, bool SEQ>
+int launch_num_group_m(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
     constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
-    if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
-    TSG_TRY(set_smem(k_num_group<G, SL>, smem));
+    TSG_TRY(set_smem(k_num_group<G, SL, SEQ>, smem));
     unsigned grid = group_grid(c, n, BS / G);
-    k_num_group<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    k_num_group<G, SL, SEQ><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_num_group", B, grid, BS, smem));
     return TSG_OK;
+}
+
+template <int B>
+int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+    if (bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
+    // lane-per-B-entry mode pays off once B rows fill at least half a group
+    if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, true>(c, bl, a);
+    return launch_num_group_m<B, false>(c, bl, a);
 }
 
 template <int CB>
@@ -1039,6 +1110,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         default: launch_compress_g<32>(c, b, cm, n_uns, uns); break;
         }
         // slow path launches unconditionally; it exits at once when no row is unsorted
+        tsg_trace(c, "compress:kernel", b->rows);
         k_compress_unsorted<256><<<c->num_sms * 2, 256, 0, c->stream>>>(n_uns, uns, b->rp, b->col,
                                                                        cm->cnt, cm->set, cm->bits); ++c->launches;
         TSG_CK(cudaGetLastError());
@@ -1139,16 +1211,29 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
                      int64_t a_row_off, int32_t b_lo, int32_t b_hi, const tsg_csr *b,
                      const tsg_cmat *cb, const tsg_csr *partial, const tsg_vec *counts,
                      const int64_t *sbound_in, tsg_csr **out, PhaseTimer *pt) {
-    // C row pointers
+    // C row pointers, numeric bins and nnz(C): one sync for all of them
     int64_t *cptr = nullptr;
     TSG_TRY(tsg_alloc_t(c, &cptr, rows_out + 1));
     TSG_TRY(tsg_exclusive_scan_i64(c, counts->d, cptr, rows_out));
     if (pt) pt->mark();
+    int64_t *sbound = nullptr;
+    uint8_t *bins = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
+    if (!sbound_in) {
+        TSG_TRY(tsg_alloc_t(c, &sbound, rows_out + 1));
+        if (rows_out > 0)
+            TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
+                                     partial ? partial->rp : nullptr, sbound));
+        sbound_in = sbound;
+    }
+    BinLists bl;
     int64_t nnz = 0;
-    TSG_CK(cudaMemcpyAsync(&c->h_small[0], cptr + rows_out, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                           c->stream));
-    TSG_CK(cudaStreamSynchronize(c->stream));
-    nnz = c->h_small[0];
+    if (rows_out > 0) {
+        k_num_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+            rows_out, counts->d, counts->aux, sbound_in, bins); ++c->launches;
+        TSG_CK(cudaGetLastError());
+        TSG_TRY(partition_rows(c, rows_out, bins, bl, cptr + rows_out, &nnz));
+    }
     tsg_csr *C = new tsg_csr();
     C->rows = rows_out;
     C->cols = cols_out;
@@ -1162,22 +1247,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         tsg_csr_free(c, C);
         return st;
     }
-    int64_t *sbound = nullptr;
-    uint8_t *bins = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
-    if (!sbound_in) {
-        TSG_TRY(tsg_alloc_t(c, &sbound, rows_out + 1));
-        if (rows_out > 0)
-            TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
-                                     partial ? partial->rp : nullptr, sbound));
-        sbound_in = sbound;
-    }
     if (rows_out > 0 && nnz > 0) {
-        k_num_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, counts->d, counts->aux, sbound_in, bins); ++c->launches;
-        TSG_CK(cudaGetLastError());
-        BinLists bl;
-        TSG_TRY(partition_rows(c, rows_out, bins, bl));
         NumArgs na;
         na.arp = a->rp;
         na.acol = a->col;
@@ -1202,11 +1272,12 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.ccol = C->col;
         na.cval = C->val;
         na.err = c->d_err;
+        na.seq = b->rows > 0 ? (int)(b->nnz / b->rows) : 0;
         if (c->timing) cudaEventRecord(c->ev_num[0], c->stream);
         TSG_TRY(run_numeric_bins(c, bl, na));
         if (c->timing) cudaEventRecord(c->ev_num[1], c->stream);
-        TSG_TRY(tsg_free(c, bl.list));
     }
+    if (bl.list) TSG_TRY(tsg_free(c, bl.list));
     TSG_TRY(tsg_free(c, bins));
     TSG_TRY(tsg_free(c, sbound));
     if (pt) pt->mark();
@@ -1298,12 +1369,15 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
     }
     PhaseTimer pt(c);
     pt.mark();
+    tsg_trace(c, "multiply:start", a->rows);
     tsg_cmat *cb = nullptr;
     TSG_TRY(tsg_compress_impl(c, b, &cb));
+    tsg_trace(c, "multiply:compressed", b->nnz);
     pt.mark();
     tsg_vec *counts = nullptr;
     int64_t *sbound = nullptr;
     int s = tsg_symbolic_impl(c, a->rows, a, 0, 0, 0x7fffffff, cb, nullptr, &counts, &sbound);
+    tsg_trace(c, "multiply:symbolic", 0);
     pt.mark();
     if (s == TSG_OK)
         s = tsg_numeric_impl(c, a->rows, b->cols, a, 0, 0, 0x7fffffff, b, cb, nullptr, counts, sbound,
