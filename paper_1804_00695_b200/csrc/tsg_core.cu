@@ -511,6 +511,9 @@ int tsg_vec_alloc(tsg_ctx *c, int64_t n, bool aux, tsg_vec **out) {
     v->n = n;
     v->d = nullptr;
     v->aux = nullptr;
+    v->sptr = nullptr;
+    v->sset = nullptr;
+    v->sbits = nullptr;
     int s = tsg_alloc_t(c, &v->d, n + 1);
     if (s == TSG_OK && aux) s = tsg_alloc_t(c, &v->aux, n + 1);
     if (s != TSG_OK) {
@@ -730,6 +733,9 @@ extern "C" int tsg_vec_free(tsg_ctx *c, tsg_vec *v) {
     if (!v) return TSG_OK;
     tsg_free(c, v->d);
     tsg_free(c, v->aux);
+    tsg_free(c, v->sptr);
+    tsg_free(c, v->sset);
+    tsg_free(c, v->sbits);
     delete v;
     return TSG_OK;
 }

@@ -42,6 +42,16 @@ __device__ __forceinline__ bool tbl_or(int4 *tbl, int T, int logT, int key, unsi
     return false;
 }
 
+// claim a slot for a key known to be absent (distinct keys); -1 if full
+__device__ __forceinline__ int tbl_claim(int4 *tbl, int T, int logT, int key) {
+    unsigned h = hash_slot(key, logT);
+    for (int n = 0; n < T; ++n) {
+        if (atomicCAS(&tbl[h].x, TSG_EMPTY, key) == TSG_EMPTY) return (int)h;
+        h = (h + 1) & (unsigned)(T - 1);
+    }
+    return -1;
+}
+
 // lookup; -1 if absent
 __device__ __forceinline__ int tbl_find(const int4 *tbl, int T, int logT, int key, int4 &out) {
     unsigned h = hash_slot(key, logT);

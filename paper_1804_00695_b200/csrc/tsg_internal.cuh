@@ -60,7 +60,10 @@ struct tsg_cmat {
 struct tsg_vec {
     int64_t n;
     int64_t *d;
-    int32_t *aux;     // distinct sets per row (from symbolic) or null
+    int32_t *aux;     // distinct sets per row (from symbolic) or null; bit 30 = sets emitted
+    int64_t *sptr;    // symbolic's sorted (set, mask) lists per row, or null
+    int32_t *sset;
+    uint64_t *sbits;
 };
 
 // ---------------------------------------------------------------- errors

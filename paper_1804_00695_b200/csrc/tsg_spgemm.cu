@@ -47,7 +47,14 @@ struct SymArgs {
     int64_t *counts;
     int32_t *msets;
     int *err;
+    // optional sorted-set output (group tier): row i's sets go to
+    // [sptr[i], sptr[i] + m) of oset / obits, msets[i] gets SETS_WRITTEN
+    const int64_t *sptr;
+    int32_t *oset;
+    uint64_t *obits;
 };
+
+constexpr int SETS_WRITTEN = 1 << 30;
 
 struct NumArgs {
     const int64_t *arp;
@@ -73,6 +80,9 @@ struct NumArgs {
     double *cval;
     int *err;
     int seq;   // host-chosen product mode: B rows long enough for lane-per-entry
+    const int64_t *sptr;   // sorted sets from the symbolic phase (rows flagged SETS_WRITTEN)
+    const int32_t *sset;
+    const uint64_t *sbits;
 };
 
 // ======================================================================= K0
@@ -239,7 +249,7 @@ __host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15)
 __device__ __forceinline__ int sym_bin(int64_t sbound) {
     if (sbound <= 0) return 255;
     int64_t T = table_slots(sbound);
-    int64_t need = 16 * T;
+    int64_t need = 24 * T;
     for (int b = 0; b < 7; b++)
         if (need <= gt_slice(b)) return b;
     for (int b = 0; b < 2; b++)
@@ -260,11 +270,12 @@ __device__ __forceinline__ int num_bin(int64_t n, int64_t m) {
 }
 
 __global__ void k_sym_bins(int64_t rows, const int64_t *__restrict__ sbound, uint8_t *bins,
-                           int64_t *counts, int32_t *msets) {
+                           int64_t *counts, int32_t *msets, int64_t *scap) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         int b = sym_bin(sbound[i]);
         bins[i] = (uint8_t)b;
+        if (scap) scap[i] = b < 7 ? sbound[i] : 0;   // sorted sets are emitted by the group tier
         if (b == 255) {
             counts[i] = 0;
             if (msets) msets[i] = 0;
@@ -278,7 +289,7 @@ __global__ void k_num_bins(int64_t rows, const int64_t *__restrict__ counts,
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t n = counts[i];
-        int64_t m = msets ? (int64_t)msets[i] : (sbound[i] < n ? sbound[i] : n);
+        int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
         bins[i] = (uint8_t)num_bin(n, m);
     }
 }
@@ -326,17 +337,17 @@ template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
     extern __shared__ int4 smem[];
-    constexpr int TMAX = SLICE / 16;
+    constexpr int TMAX = SLICE / 24;   // 16 B table slot + 8 B sort key per slot
     const unsigned gm = group_mask<G>();
     const int glane = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
-    int4 *tbl = smem + (threadIdx.x / G) * TMAX;
+    int4 *tbl = reinterpret_cast<int4 *>(reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE);
     for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
          li += (int64_t)gridDim.x * gpb) {
         const int64_t i = list[li];
         const int64_t gi = i + a.a_row_off;
         int T = table_slots(a.sbound[i]);
-        if (T > TMAX) T = TMAX;
+        if (T > TMAX) T = 1 << ilog2_pow2(TMAX);
         const int logT = ilog2_pow2(T);
         tbl_clear(tbl, T, glane, G);
         __syncwarp(gm);
@@ -366,20 +377,69 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                 }
             });
         __syncwarp(gm);
+        // compact occupied slots as sortable (key << 32 | slot) into the scratch
+        // area behind the table; count columns on the way
+        uint64_t *ck = reinterpret_cast<uint64_t *>(tbl + T);
+        const unsigned lt = lanemask_lt();
         int cnt = 0, m = 0;
-        for (int s = glane; s < T; s += G) {
-            int4 e = tbl[s];
-            if (e.x != TSG_EMPTY) {
-                m++;
+        for (int r0 = 0; r0 < T; r0 += G) {
+            int s = r0 + glane;
+            int4 e = s < T ? tbl[s] : make_int4(TSG_EMPTY, 0, 0, 0);
+            bool occ = e.x != TSG_EMPTY;
+            unsigned bal = __ballot_sync(gm, occ) & gm;
+            if (occ) {
                 cnt += slot_pop(e);
+                ck[m + __popc(bal & lt)] = ((uint64_t)(uint32_t)e.x << 32) | (uint32_t)s;
             }
+            m += __popc(bal);
         }
         cnt = group_sum<G, int>(gm, cnt);
-        m = group_sum<G, int>(gm, m);
         if (!ok) kerr(a.err, KERR_PROBE, gi);
+        bool emit = a.oset != nullptr && ok && m <= a.sbound[i];
+        if (emit) {
+            __syncwarp(gm);
+            const int64_t sp = a.sptr[i];
+            if (m <= 64) {
+                // rank sort: entry q goes to #keys smaller than it
+                for (int q = glane; q < m; q += G) {
+                    uint64_t me = ck[q];
+                    int r = 0;
+                    for (int u = 0; u < m; ++u) r += (ck[u] < me);
+                    int slot = (int)(uint32_t)me;
+                    int4 e = tbl[slot];
+                    a.oset[sp + r] = e.x;
+                    a.obits[sp + r] = ((uint64_t)(uint32_t)e.z << 32) | (uint32_t)e.y;
+                }
+            } else {
+                int P = 1;
+                while (P < m) P <<= 1;
+                for (int q = m + glane; q < P; q += G) ck[q] = ~0ull;
+                __syncwarp(gm);
+                for (int k = 2; k <= P; k <<= 1) {
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        for (int x = glane; x < P; x += G) {
+                            int y = x ^ j;
+                            if (y > x) {
+                                uint64_t kx = ck[x], ky = ck[y];
+                                if ((kx > ky) == ((x & k) == 0)) {
+                                    ck[x] = ky;
+                                    ck[y] = kx;
+                                }
+                            }
+                        }
+                        __syncwarp(gm);
+                    }
+                }
+                for (int q = glane; q < m; q += G) {
+                    int4 e = tbl[(int)(uint32_t)ck[q]];
+                    a.oset[sp + q] = e.x;
+                    a.obits[sp + q] = ((uint64_t)(uint32_t)e.z << 32) | (uint32_t)e.y;
+                }
+            }
+        }
         if (glane == 0) {
             a.counts[i] = cnt;
-            if (a.msets) a.msets[i] = m;
+            if (a.msets) a.msets[i] = m | (emit ? SETS_WRITTEN : 0);
         }
         __syncwarp(gm);
     }
@@ -469,7 +529,10 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         const int n = (int)a.counts[i];
         const int64_t cp = a.cptr[i];
         const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
-        int64_t mest = a.msets ? (int64_t)a.msets[i] : (a.sbound[i] < n ? a.sbound[i] : n);
+        const int mflag = a.msets ? a.msets[i] : 0;
+        const bool have_sets = a.sptr != nullptr && (mflag & SETS_WRITTEN);
+        int64_t mest = a.msets ? (int64_t)(mflag & (SETS_WRITTEN - 1))
+                               : (a.sbound[i] < n ? a.sbound[i] : n);
         double *vals = reinterpret_cast<double *>(slice);
         int2 *cbuf = reinterpret_cast<int2 *>(slice);   // phase-B scratch, aliases vals
         int4 *tbl = reinterpret_cast<int4 *>(slice + round16(8 * (int64_t)n));
@@ -479,78 +542,120 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         const int logT = ilog2_pow2(T);
         tbl_clear(tbl, T, glane, G);
         __syncwarp(gm);
-
-        // phase A: union of column sets (partial row + compressed B rows)
-        bool ok = true;
         const int64_t p0 = a.prp ? a.prp[i] : 0, p1 = a.prp ? a.prp[i + 1] : 0;
-        for (int64_t q = p0 + glane; q < p1; q += G) {
-            int c = a.pcol[q];
-            int bit = c & 63;
-            ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
-                         bit >= 32 ? 1u << (bit - 32) : 0u);
-        }
-        group_enumerate<G>(
-            gm, glane, a0, a1,
-            [&](int64_t t, int64_t &st, int &len) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    st = a.cbstart[k];
-                    len = a.cbcnt[k];
-                }
-            },
-            [&](bool valid, int, int64_t, int64_t s) {
-                if (valid) {
-                    uint64_t bits = a.cbbits[s];
-                    ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
-                }
-            });
-        __syncwarp(gm);
+        bool ok = true;
 
-        // phase B: compact the occupied sets (key, slot<<8 | popcount) into the
-        // value area (m <= n entries of 8 B), rank each against the compacted
-        // list -> base = columns in smaller sets; emit the row's columns.
-        int m = 0, tot = 0;
-        for (int r0 = 0; r0 < T; r0 += G) {
-            int s = r0 + glane;
-            int4 e = s < T ? tbl[s] : make_int4(TSG_EMPTY, 0, 0, 0);
-            bool occ = e.x != TSG_EMPTY;
-            unsigned bal = __ballot_sync(gm, occ) & gm;
-            int pc = slot_pop(e);
-            if (occ && m + __popc(bal & lt) < n) cbuf[m + __popc(bal & lt)] = make_int2(e.x, (s << 8) | pc);
-            if (occ) tot += pc;
-            m += __popc(bal);
-        }
-        tot = group_sum<G, int>(gm, tot);
-        ok = __all_sync(gm, ok);
-        if (tot != n || !ok || m > n) {
-            if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+        if (have_sets) {
+            // sorted sets from the symbolic phase: base = running popcount
+            const int m = (int)mest;
+            const int64_t sp = a.sptr[i];
+            int carry = 0;
+            for (int q0 = 0; q0 < m; q0 += G) {
+                int q = q0 + glane;
+                bool valid = q < m;
+                int key = valid ? a.sset[sp + q] : 0;
+                uint64_t bits = valid ? a.sbits[sp + q] : 0ull;
+                int pc = __popcll(bits);
+                int incl = group_incl_scan<G, int>(gm, pc, glane);
+                int base = carry + incl - pc;
+                carry += __shfl_sync(gm, incl, G - 1, G);
+                if (valid) {
+                    int slot = tbl_claim(tbl, T, logT, key);
+                    if (slot < 0) {
+                        ok = false;
+                    } else {
+                        tbl[slot].y = (int)(uint32_t)bits;
+                        tbl[slot].z = (int)(uint32_t)(bits >> 32);
+                        tbl[slot].w = base;
+                    }
+                    if (base + pc <= n) {
+                        uint64_t b = bits;
+                        int r = base;
+                        while (b) {
+                            a.ccol[cp + r++] = key * 64 + (__ffsll((long long)b) - 1);
+                            b &= b - 1;
+                        }
+                    }
+                }
+            }
+            ok = __all_sync(gm, ok);
+            if (carry != n || !ok) {
+                if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+                __syncwarp(gm);
+                continue;   // group-uniform
+            }
+        } else {
+            // phase A: union of column sets (partial row + compressed B rows)
+            for (int64_t q = p0 + glane; q < p1; q += G) {
+                int c = a.pcol[q];
+                int bit = c & 63;
+                ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
+                             bit >= 32 ? 1u << (bit - 32) : 0u);
+            }
+            group_enumerate<G>(
+                gm, glane, a0, a1,
+                [&](int64_t t, int64_t &st, int &len) {
+                    int k = a.acol[t];
+                    if (k >= a.b_lo && k < a.b_hi) {
+                        k -= a.b_lo;
+                        st = a.cbstart[k];
+                        len = a.cbcnt[k];
+                    }
+                },
+                [&](bool valid, int, int64_t, int64_t s) {
+                    if (valid) {
+                        uint64_t bits = a.cbbits[s];
+                        ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                    }
+                });
             __syncwarp(gm);
-            continue;   // group-uniform
-        }
-        __syncwarp(gm);
-        for (int q = glane; q < m; q += G) {
-            int2 me = cbuf[q];
-            int base = 0;
-            for (int u = 0; u < m; ++u) {
-                int2 o = cbuf[u];
-                if (o.x < me.x) base += o.y & 0xff;
+
+            // phase B: compact the occupied sets (key, slot<<8 | popcount) into the
+            // value area (m <= n entries of 8 B), rank each against the compacted
+            // list -> base = columns in smaller sets; emit the row's columns.
+            int m = 0, tot = 0;
+            for (int r0 = 0; r0 < T; r0 += G) {
+                int s = r0 + glane;
+                int4 e = s < T ? tbl[s] : make_int4(TSG_EMPTY, 0, 0, 0);
+                bool occ = e.x != TSG_EMPTY;
+                unsigned bal = __ballot_sync(gm, occ) & gm;
+                int pc = slot_pop(e);
+                if (occ && m + __popc(bal & lt) < n) cbuf[m + __popc(bal & lt)] = make_int2(e.x, (s << 8) | pc);
+                if (occ) tot += pc;
+                m += __popc(bal);
             }
-            int slot = me.y >> 8;
-            tbl[slot].w = base;
-            int4 e = tbl[slot];
-            unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
-            int r = base;
-            while (lo) {
-                int b = __ffs(lo) - 1;
-                lo &= lo - 1;
-                a.ccol[cp + r++] = me.x * 64 + b;
+            tot = group_sum<G, int>(gm, tot);
+            ok = __all_sync(gm, ok);
+            if (tot != n || !ok || m > n) {
+                if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
+                __syncwarp(gm);
+                continue;   // group-uniform
             }
-            while (hi) {
-                int b = __ffs(hi) - 1;
-                hi &= hi - 1;
-                a.ccol[cp + r++] = me.x * 64 + 32 + b;
+            __syncwarp(gm);
+            for (int q = glane; q < m; q += G) {
+                int2 me = cbuf[q];
+                int base = 0;
+                for (int u = 0; u < m; ++u) {
+                    int2 o = cbuf[u];
+                    if (o.x < me.x) base += o.y & 0xff;
+                }
+                int slot = me.y >> 8;
+                tbl[slot].w = base;
+                int4 e = tbl[slot];
+                unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+                int r = base;
+                while (lo) {
+                    int b = __ffs(lo) - 1;
+                    lo &= lo - 1;
+                    a.ccol[cp + r++] = me.x * 64 + b;
+                }
+                while (hi) {
+                    int b = __ffs(hi) - 1;
+                    hi &= hi - 1;
+                    a.ccol[cp + r++] = me.x * 64 + 32 + b;
+                }
             }
+
         }
         __syncwarp(gm);
         for (int q = glane; q < n; q += G) vals[q] = -0.0;
@@ -719,7 +824,7 @@ __global__ void __launch_bounds__(NT) k_num_block(const int32_t *__restrict__ li
         const int64_t gi = i + a.a_row_off;
         const int64_t n = a.counts[i];
         const int64_t cp = a.cptr[i];
-        int64_t mest = a.msets ? (int64_t)a.msets[i] : (a.sbound[i] < n ? a.sbound[i] : n);
+        int64_t mest = a.msets ? (int64_t)(a.msets[i] & (SETS_WRITTEN - 1)) : (a.sbound[i] < n ? a.sbound[i] : n);
         int64_t want = table_slots(mest);
         int T = (int)(want < tmax ? want : tmax);
         const int logT = ilog2_pow2(T);
@@ -1140,11 +1245,19 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
             TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
                                      partial ? partial->rp : nullptr, sbound));
         }
+        int64_t *scap = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &scap, rows_out + 1));
+        TSG_TRY(tsg_alloc_t(c, &v->sptr, rows_out + 1));
         k_sym_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, sbound, bins, v->d, v->aux); ++c->launches;
+            rows_out, sbound, bins, v->d, v->aux, scap); ++c->launches;
         TSG_CK(cudaGetLastError());
+        TSG_TRY(tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out));
         BinLists bl;
-        TSG_TRY(partition_rows(c, rows_out, bins, bl));
+        int64_t set_cap = 0;
+        TSG_TRY(partition_rows(c, rows_out, bins, bl, v->sptr + rows_out, &set_cap));
+        TSG_TRY(tsg_free(c, scap));
+        TSG_TRY(tsg_alloc_t(c, &v->sset, set_cap > 0 ? set_cap : 1));
+        TSG_TRY(tsg_alloc_t(c, &v->sbits, set_cap > 0 ? set_cap : 1));
         SymArgs sa;
         sa.arp = a->rp;
         sa.acol = a->col;
@@ -1161,6 +1274,9 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.counts = v->d;
         sa.msets = v->aux;
         sa.err = c->d_err;
+        sa.sptr = v->sptr;
+        sa.oset = v->sset;
+        sa.obits = v->sbits;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
@@ -1273,6 +1389,9 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.cval = C->val;
         na.err = c->d_err;
         na.seq = b->rows > 0 ? (int)(b->nnz / b->rows) : 0;
+        na.sptr = counts->sptr;
+        na.sset = counts->sset;
+        na.sbits = counts->sbits;
         if (c->timing) cudaEventRecord(c->ev_num[0], c->stream);
         TSG_TRY(run_numeric_bins(c, bl, na));
         if (c->timing) cudaEventRecord(c->ev_num[1], c->stream);
