@@ -86,6 +86,11 @@ int tsg_csr_from_device(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,
 int tsg_csr_device_ptrs(const tsg_csr *m, int64_t **d_row_ptr, int32_t **d_col,
                         double **d_values);
 
+/* Pinned host memory from a caching pool (falls back to pageable memory if
+   pinning is refused).  Used for result arrays returned to the caller. */
+int tsg_host_alloc(size_t bytes, void **out);
+int tsg_host_free(void *p);
+
 /* ---- CSR operands (csr.py:32-106 CsrMatrix) ------------------------------ */
 /* values may be NULL (pattern).  Columns must be < 2^31 (device int32). */
 int tsg_csr_upload(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,

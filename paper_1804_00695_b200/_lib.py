@@ -42,7 +42,7 @@ EXPORTS = (
     "tsg_vec_upload", "tsg_vec_download", "tsg_vec_len", "tsg_vec_free",
     "tsg_count_multiplications", "tsg_symbolic", "tsg_numeric", "tsg_multiply",
     "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
-    "tsg_csr_from_device", "tsg_csr_device_ptrs",
+    "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
 )
 
 _P = ctypes.c_void_p
@@ -87,6 +87,8 @@ _SIGS = {
                           ctypes.c_int),
     "tsg_csr_from_device": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_csr_device_ptrs": ([_P, _PP, _PP, _PP], ctypes.c_int),
+    "tsg_host_alloc": ([ctypes.c_size_t, _PP], ctypes.c_int),
+    "tsg_host_free": ([_P], ctypes.c_int),
 }
 
 _lib = None
@@ -119,6 +121,36 @@ def check(status):
 
 def _ptr(a):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class _PinnedBlock:
+    """Owner of one pinned host block; returns it to libtsg's pool when the
+    last numpy view goes away."""
+
+    __slots__ = ("addr", "__weakref__")
+
+    def __init__(self, nbytes):
+        p = ctypes.c_void_p()
+        check(load().tsg_host_alloc(max(int(nbytes), 1), ctypes.byref(p)))
+        self.addr = p.value
+        weakref.finalize(self, _host_free, p.value)
+
+
+def _host_free(addr):
+    try:
+        load().tsg_host_free(ctypes.c_void_p(addr))
+    except Exception:  # interpreter shutdown
+        pass
+
+
+def pinned_empty(n, dtype):
+    """numpy array of n elements in pinned host memory (pooled)."""
+    dtype = np.dtype(dtype)
+    nbytes = int(n) * dtype.itemsize
+    blk = _PinnedBlock(nbytes)
+    raw = (ctypes.c_char * max(nbytes, 1)).from_address(blk.addr)
+    raw._owner = blk
+    return np.frombuffer(raw, dtype=dtype, count=int(n))
 
 
 class _Stats(ctypes.Structure):
@@ -231,9 +263,9 @@ class DeviceCsr(_Handle):
         return cls(ctx, h)
 
     def download(self) -> CsrMatrix:
-        rp = np.empty(self.num_rows + 1, dtype=np.int64)
-        ci = np.empty(self.nnz, dtype=np.int64)
-        va = np.empty(self.nnz, dtype=np.float64) if self.has_values else None
+        rp = pinned_empty(self.num_rows + 1, np.int64)
+        ci = pinned_empty(self.nnz, np.int64)
+        va = pinned_empty(self.nnz, np.float64) if self.has_values else None
         check(load().tsg_csr_download(self.ctx.h, self.h, _ptr(rp), _ptr(ci), _ptr(va)))
         return CsrMatrix._adopt(self.num_rows, self.num_cols, rp, ci, va)
 

@@ -296,6 +296,67 @@ int tsg_free(tsg_ctx *c, void *p) {
     return TSG_OK;
 }
 
+// ---- pinned host pool: result arrays handed to the caller live here, so the
+// D2H of a product (and its re-upload as the next operand) runs at full
+// PCIe rate instead of the driver's pageable staging rate.
+static std::mutex g_host_mu;
+static std::multimap<size_t, void *> g_host_free;
+static std::unordered_map<void *, size_t> g_host_live;
+static size_t g_host_cached = 0;
+static const size_t HOST_CACHE_LIMIT = (size_t)16 << 30;
+
+extern "C" int tsg_host_alloc(size_t bytes, void **out) {
+    *out = nullptr;
+    size_t cls = size_class(bytes ? bytes : 1);
+    {
+        std::lock_guard<std::mutex> g(g_host_mu);
+        auto it = g_host_free.lower_bound(cls);
+        if (it != g_host_free.end() && it->first <= cls + cls / 4) {
+            *out = it->second;
+            g_host_live[*out] = it->first;
+            g_host_cached -= it->first;
+            g_host_free.erase(it);
+            return TSG_OK;
+        }
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, cls, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        // pinning can fail under memlock limits: fall back to pageable memory
+        p = malloc(cls);
+        if (!p) {
+            tsg_set_error("host allocation of %zu bytes failed", bytes);
+            return TSG_ECAPACITY;
+        }
+        cls |= 1;   // tag: not pinned
+    }
+    std::lock_guard<std::mutex> g(g_host_mu);
+    g_host_live[p] = cls;
+    *out = p;
+    return TSG_OK;
+}
+
+extern "C" int tsg_host_free(void *p) {
+    if (!p) return TSG_OK;
+    std::lock_guard<std::mutex> g(g_host_mu);
+    auto it = g_host_live.find(p);
+    if (it == g_host_live.end()) return TSG_OK;
+    size_t cls = it->second;
+    g_host_live.erase(it);
+    if (cls & 1) {
+        free(p);
+        return TSG_OK;
+    }
+    if (g_host_cached + cls > HOST_CACHE_LIMIT) {
+        cudaFreeHost(p);
+        return TSG_OK;
+    }
+    g_host_free.emplace(cls, p);
+    g_host_cached += cls;
+    return TSG_OK;
+}
+
 int tsg_arena_trim(tsg_ctx *c) {
     Arena *A = arena_of(c);
     std::lock_guard<std::mutex> g(A->mu);

@@ -91,8 +91,65 @@ __device__ __forceinline__ void group_enumerate(unsigned gm, int glane, int64_t 
         int64_t st = 0;
         int len = 0;
         if (t < a1) src(t, st, len);
+        if (__all_sync(gm, len == 1 || t >= a1)) {
+            // unit rows (aggregation operators): position p is lane p itself
+            f(t < a1, glane, t, st);
+            continue;
+        }
         int incl = group_incl_scan<G, int>(gm, len, glane);
         int total = __shfl_sync(gm, incl, G - 1, G);
+        for (int p0 = 0; p0 < total; p0 += G) {
+            int p = p0 + glane;
+            int j = 0;
+#pragma unroll
+            for (int step = G / 2; step >= 1; step >>= 1) {
+                int v = __shfl_sync(gm, incl, j + step - 1, G);
+                if (v <= p) j += step;
+            }
+            int inc_j = __shfl_sync(gm, incl, j, G);
+            int len_j = __shfl_sync(gm, len, j, G);
+            int64_t st_j = __shfl_sync(gm, st, j, G);
+            bool valid = p < total;
+            f(valid, j, base + j, st_j + (int64_t)(p - (inc_j - len_j)));
+        }
+    }
+}
+
+// Order-free variant (symbolic union, masked count): per chunk of A entries
+// it picks the cheaper of the flattened mapping above and a fixed mapping in
+// which each A entry gets L = G / pow2(entries) lanes that stride through its
+// row -- no search, no shuffles per position.  For uniform rows (stencils:
+// 8 A entries x ~11 compressed sets) the fixed mapping needs ~3 steps and no
+// binary search; skewed rows (power-law graphs) stay flattened.
+template <int G, class Src, class F>
+__device__ __forceinline__ void group_enumerate_any(unsigned gm, int glane, int64_t a0, int64_t a1,
+                                                    Src src, F f) {
+    for (int64_t base = a0; base < a1; base += G) {
+        int64_t t = base + glane;
+        int64_t st = 0;
+        int len = 0;
+        if (t < a1) src(t, st, len);
+        int incl = group_incl_scan<G, int>(gm, len, glane);
+        int total = __shfl_sync(gm, incl, G - 1, G);
+        int maxlen = len;
+#pragma unroll
+        for (int d = G / 2; d >= 1; d >>= 1) maxlen = max(maxlen, __shfl_xor_sync(gm, maxlen, d, G));
+        const int ne = (int)((a1 - base) < G ? (a1 - base) : G);
+        const int lg_pe = ne <= 1 ? 0 : 32 - __clz(ne - 1);        // log2(pow2 >= ne)
+        const int lg_l = ilog2_pow2(G) - lg_pe;                      // lanes per entry = 2^lg_l
+        const int steps_fixed = (maxlen + (1 << lg_l) - 1) >> lg_l;
+        const int steps_flat = (total + G - 1) / G;
+        if (steps_fixed <= 2 * steps_flat) {
+            const int j = glane >> lg_l, sub = glane & ((1 << lg_l) - 1);
+            int64_t st_j = __shfl_sync(gm, st, j, G);
+            int len_j = __shfl_sync(gm, len, j, G);
+            if (j >= ne) len_j = 0;
+            for (int q = sub; q < (steps_fixed << lg_l); q += (1 << lg_l)) {
+                bool valid = q < len_j;
+                f(valid, j, base + j, st_j + q);
+            }
+            continue;
+        }
         for (int p0 = 0; p0 < total; p0 += G) {
             int p = p0 + glane;
             int j = 0;

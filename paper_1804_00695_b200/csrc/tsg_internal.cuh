@@ -147,9 +147,12 @@ __device__ __forceinline__ unsigned hash_slot(int key, int logT) {
 __device__ __forceinline__ int ilog2_pow2(int T) { return 31 - __clz(T); }
 
 __host__ __device__ __forceinline__ int pow2_ceil_i(int64_t x) {
-    int p = 1;
-    while (p < x) p <<= 1;
-    return p;
+    if (x <= 1) return 1;
+#ifdef __CUDA_ARCH__
+    return (int)(1ull << (64 - __clzll((unsigned long long)(x - 1))));
+#else
+    return (int)(1ull << (64 - __builtin_clzll((unsigned long long)(x - 1))));
+#endif
 }
 
 // table slots for a row holding up to `m` distinct keys: load factor <= 3/4

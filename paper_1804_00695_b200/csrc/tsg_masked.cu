@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) k_mask_group(const int32_t *__restrict__ 
         if (!lower) kerr(a.err, KERR_NOTLOWER, i);
         if (!ok) kerr(a.err, KERR_PROBE, i);
         __syncwarp(gm);
-        group_enumerate<G>(
+        group_enumerate_any<G>(
             gm, glane, r0, r1,
             [&](int64_t t, int64_t &st, int &len) {
                 int j = a.lcol[t];

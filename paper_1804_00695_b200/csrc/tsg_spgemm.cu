@@ -177,6 +177,65 @@ __global__ void k_compress(int64_t rows, const int64_t *__restrict__ rp,
     }
 }
 
+// Tiled compression for short rows: a CTA stages the column indices of CT_ROWS
+// consecutive rows (one contiguous range of B) in shared memory with
+// coalesced loads, each thread run-length encodes one row from shared memory
+// (stride = row length, conflict-free for odd lengths), and the tile's output
+// range [rp[r0], rp[r0 + CT_ROWS]) of the padded layout is written back
+// coalesced (holes included; they are never read).  Tiles whose entries
+// exceed the staging buffer fall back to per-thread global reads.
+constexpr int CT_ROWS = 128;
+constexpr int CT_CAP = 6144;   // staged column indices per tile (24 KB)
+
+__global__ void __launch_bounds__(CT_ROWS) k_compress_tiled(
+    int64_t rows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+    int32_t *__restrict__ cnt, int32_t *__restrict__ oset, uint64_t *__restrict__ obits,
+    int *n_unsorted, int32_t *unsorted) {
+    __shared__ int32_t s_col[CT_CAP];
+    for (int64_t r0 = (int64_t)blockIdx.x * CT_ROWS; r0 < rows; r0 += (int64_t)gridDim.x * CT_ROWS) {
+        const int64_t r1 = r0 + CT_ROWS < rows ? r0 + CT_ROWS : rows;
+        const int64_t e0 = rp[r0], e1 = rp[r1];
+        const bool staged = (e1 - e0) <= CT_CAP;
+        if (staged)
+            for (int64_t q = e0 + threadIdx.x; q < e1; q += CT_ROWS) s_col[q - e0] = col[q];
+        __syncthreads();
+        const int64_t i = r0 + threadIdx.x;
+        if (i < r1) {
+            const int64_t lo = rp[i], hi = rp[i + 1];
+            int prev = -1, k = 0;
+            uint64_t bits = 0;
+            bool bad = false;
+            for (int64_t q = lo; q < hi; ++q) {
+                int c = staged ? s_col[q - e0] : col[q];
+                int sv = c >> 6;
+                if (sv != prev) {
+                    if (sv < prev) bad = true;
+                    if (prev >= 0) {
+                        oset[lo + k] = prev;
+                        obits[lo + k] = bits;
+                        ++k;
+                    }
+                    prev = sv;
+                    bits = 0;
+                }
+                bits |= 1ull << (c & 63);
+            }
+            if (prev >= 0) {
+                oset[lo + k] = prev;
+                obits[lo + k] = bits;
+                ++k;
+            }
+            if (bad) {
+                cnt[i] = -1;
+                unsorted[atomicAdd(n_unsorted, 1)] = (int32_t)i;
+            } else {
+                cnt[i] = k;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // First-touch compression of unsorted rows: entry t heads its set if no
 // earlier entry of the row has the same set (the reference's dict order).
 template <int NT>
@@ -236,7 +295,9 @@ __global__ void k_compress_unsorted(const int *n_unsorted, const int32_t *__rest
 constexpr int NBINS = 10;
 // bins 0..6: group tier slices (bytes) and group sizes
 __host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
-__host__ __device__ constexpr int gt_g(int b) { return b == 0 ? 8 : (b == 1 ? 16 : 32); }
+__host__ __device__ constexpr int gt_g(int b) { return b <= 1 ? 8 : (b == 2 ? 16 : 32); }
+// symbolic tables are larger (bounded by compressed entries, not exact sets)
+__host__ __device__ constexpr int gt_g_sym(int b) { return b == 0 ? 8 : (b == 1 ? 16 : 32); }
 __host__ __device__ constexpr int gt_block(int b) { return b <= 4 ? 256 : (b == 5 ? 128 : 64); }
 // bins 7, 8: CTA tier table slots (smem table 16 B/slot + sort keys 8 B/slot)
 __host__ __device__ constexpr int ct_slots(int cb) { return 2048 << (2 * cb); }
@@ -360,7 +421,7 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                              bit >= 32 ? 1u << (bit - 32) : 0u);
             }
         }
-        group_enumerate<G>(
+        group_enumerate_any<G>(
             gm, glane, a.arp[gi], a.arp[gi + 1],
             [&](int64_t t, int64_t &st, int &len) {
                 int k = a.acol[t];
@@ -457,10 +518,9 @@ __device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, 
     unsigned peers = __match_any_sync(gm, pos);
     bool leader = (pos >= 0) && ((int)lane == __ffs(peers) - 1);
     unsigned rest = leader ? (peers & ~(1u << lane)) : 0u;
-    unsigned iters = __reduce_max_sync(gm, (unsigned)__popc(rest));
     double acc = 0.0;
     if (leader) acc = __dadd_rn(vals[pos], prod);
-    for (unsigned it = 0; it < iters; ++it) {
+    while (__any_sync(gm, rest != 0)) {
         int src = rest ? __ffs(rest) - 1 : (int)lane;
         double o = __shfl_sync(gm, prod, src);
         if (rest) {
@@ -592,7 +652,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
                 ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
                              bit >= 32 ? 1u << (bit - 32) : 0u);
             }
-            group_enumerate<G>(
+            group_enumerate_any<G>(
                 gm, glane, a0, a1,
                 [&](int64_t t, int64_t &st, int &len) {
                     int k = a.acol[t];
@@ -990,7 +1050,7 @@ constexpr int64_t GLOBAL_SLAB_BUDGET = (int64_t)2 << 30;
 
 template <int B>
 int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
-    constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
+    constexpr int G = gt_g_sym(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
@@ -1208,11 +1268,19 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         int32_t *uns = nullptr;
         TSG_TRY(tsg_alloc_t(c, &uns, b->rows));
         TSG_CK(cudaMemsetAsync(n_uns, 0, sizeof(int), c->stream));
-        switch (pick_g(b->nnz, b->rows)) {
-        case 4: launch_compress_g<4>(c, b, cm, n_uns, uns); break;
-        case 8: launch_compress_g<8>(c, b, cm, n_uns, uns); break;
-        case 16: launch_compress_g<16>(c, b, cm, n_uns, uns); break;
-        default: launch_compress_g<32>(c, b, cm, n_uns, uns); break;
+        double avg = (double)b->nnz / (double)b->rows;
+        if (avg <= 40.0) {
+            unsigned grid = grid_for(b->rows, CT_ROWS, c->num_sms * 16);
+            k_compress_tiled<<<grid, CT_ROWS, 0, c->stream>>>(b->rows, b->rp, b->col, cm->cnt,
+                                                              cm->set, cm->bits, n_uns, uns); ++c->launches;
+            TSG_TRY(tsg_launch_check("k_compress_tiled", -1, grid, CT_ROWS, 0));
+        } else {
+            switch (pick_g(b->nnz, b->rows)) {
+            case 4: launch_compress_g<4>(c, b, cm, n_uns, uns); break;
+            case 8: launch_compress_g<8>(c, b, cm, n_uns, uns); break;
+            case 16: launch_compress_g<16>(c, b, cm, n_uns, uns); break;
+            default: launch_compress_g<32>(c, b, cm, n_uns, uns); break;
+            }
         }
         // slow path launches unconditionally; it exits at once when no row is unsorted
         tsg_trace(c, "compress:kernel", b->rows);

@@ -1,5 +1,15 @@
-"""Per-source-line instruction / stall-sample hotspots of one launch in an ncu report."""
-import csv, subprocess, sys
+"""Per-source-line instruction / stall-sample hotspots of one launch in an ncu report.
+usage: python tools_ncu_source.py REPORT LAUNCH_INDEX [TOP]"""
+import csv, os, subprocess, sys
+
+SRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), 'paper_1804_00695_b200', 'csrc')
+
+
+def num(x):
+    try:
+        return int(x)
+    except ValueError:
+        return 0
 
 
 def main(rep, skip, top=30):
@@ -7,29 +17,33 @@ def main(rep, skip, top=30):
                           '--launch-skip', str(skip), '--launch-count', '1'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    cur, hdr, res = None, None, []
+    cur, hdr, res, smp = None, None, {}, {}
     for r in rows:
         if r and r[0] == 'File Path':
             cur = r[1].split('/')[-1]
             continue
         if r and r[0] == 'Function Name':
-            print(r[1][:100])
+            fn = r[1]
             continue
         if r and r[0] == 'Line No':
             hdr = r
             continue
         if hdr and len(r) >= 8 and r[0].isdigit():
-            try:
-                ie = int(r[hdr.index('Instructions Executed')] or 0)
-                smp = int(r[hdr.index('Warp Stall Sampling (All Samples)')] or 0)
-            except ValueError:
-                continue
-            res.append((ie, smp, cur, int(r[0]), r[1].strip()[:90]))
-    tot = sum(o[0] for o in res) or 1
-    ts = sum(o[1] for o in res) or 1
+            k = (cur, int(r[0]))
+            res[k] = res.get(k, 0) + num(r[hdr.index('Instructions Executed')])
+            smp[k] = smp.get(k, 0) + num(r[hdr.index('Warp Stall Sampling (All Samples)')])
+    tot = sum(res.values()) or 1
+    ts = sum(smp.values()) or 1
+    print(fn[:110])
     print("total warp-instructions %d, stall samples %d" % (tot, ts))
-    for o in sorted(res, key=lambda x: -x[1])[:top]:
-        print("%10d %5.1f%%  smp %5.1f%%  %s:%d  %s" % (o[0], 100 * o[0] / tot, 100 * o[1] / ts, o[2], o[3], o[4]))
+    cache = {}
+    for k, v in sorted(res.items(), key=lambda x: -x[1])[:top]:
+        path = os.path.join(SRC, k[0])
+        if k[0] not in cache:
+            cache[k[0]] = open(path).read().split('\n') if os.path.exists(path) else []
+        line = cache[k[0]][k[1] - 1].strip()[:72] if len(cache[k[0]]) >= k[1] else ''
+        print("%10d %5.1f%% smp %5.1f%%  %s:%d  %s" % (v, 100 * v / tot, 100 * smp.get(k, 0) / ts,
+                                                     k[0], k[1], line))
 
 
 if __name__ == '__main__':
