@@ -65,3 +65,33 @@ def gpu_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+# ---- golden fixtures (tests/golden/make_golden.py ran the reference) --------------
+_GOLD = None
+
+
+def golden():
+    """(arrays, meta) of tests/golden/golden.{npz,json}."""
+    global _GOLD
+    if _GOLD is None:
+        import json
+        d = os.path.join(ROOT, "tests", "golden")
+        arrs = dict(np.load(os.path.join(d, "golden.npz")))
+        with open(os.path.join(d, "golden.json")) as fh:
+            meta = json.load(fh)
+        _GOLD = (arrs, meta)
+    return _GOLD
+
+
+def gcsr(name):
+    from paper_1804_00695_b200.csr import CsrMatrix
+    arrs, meta = golden()
+    rows, cols, has_v = meta[name]
+    return CsrMatrix(rows, cols, arrs[name + "/rp"], arrs[name + "/ci"],
+                     arrs[name + "/va"] if has_v else None)
+
+
+def gcm(name):
+    arrs, _ = golden()
+    return arrs[name + "/rp"], arrs[name + "/set"], arrs[name + "/bits"]
