@@ -148,6 +148,28 @@ int tsg_numeric_fused(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b_chunk,
 int tsg_masked_count(tsg_ctx *ctx, const tsg_csr *l, const tsg_cmat *cl,
                      int64_t *total);
 
+/* ---- chunked execution through an HBM budget (chunking.py:219-337) -------- */
+/* algo: 0 = KNL order (B streamed past all of A/C), 1 = GPU chunk1 (A/C row
+   range in place, B streamed), 2 = GPU chunk2 (B range in place, A/C
+   streamed).  Partitions are boundary arrays (n+1 entries, 0 .. rows).  Host
+   arrays use the reference's formats (int64 offsets and indices, f64
+   values); pin them for full PCIe rate.  c_row_ptr = exclusive scan of the
+   symbolic counts; c_col / c_val (sum of counts entries) are filled.  Every
+   chunk step is the fused multiply-add run in place in HBM. */
+typedef struct {
+    int64_t h2d_bytes;          /* bytes actually copied host -> device     */
+    int64_t d2h_bytes;          /* bytes actually copied device -> host     */
+    double kernel_ms;           /* device time of compress + fused kernels   */
+    double wall_ms;             /* host wall time of the whole call          */
+    int64_t peak_device_bytes;  /* device bytes held at the end of the plan  */
+} tsg_chunk_stats;
+int tsg_chunk_multiply(tsg_ctx *ctx, int algo, int64_t a_rows, int64_t a_cols,
+                       const int64_t *a_row_ptr, const int64_t *a_col, const double *a_val,
+                       int64_t b_rows, int64_t b_cols, const int64_t *b_row_ptr,
+                       const int64_t *b_col, const double *b_val, const int64_t *c_row_ptr,
+                       int64_t *c_col, double *c_val, int64_t n_ac, const int64_t *ac_bounds,
+                       int64_t n_b, const int64_t *b_bounds, tsg_chunk_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ EXPORTS = (
     "tsg_count_multiplications", "tsg_symbolic", "tsg_numeric", "tsg_multiply",
     "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
+    "tsg_chunk_multiply",
 )
 
 _P = ctypes.c_void_p
@@ -89,6 +90,8 @@ _SIGS = {
     "tsg_csr_device_ptrs": ([_P, _PP, _PP, _PP], ctypes.c_int),
     "tsg_host_alloc": ([ctypes.c_size_t, _PP], ctypes.c_int),
     "tsg_host_free": ([_P], ctypes.c_int),
+    "tsg_chunk_multiply": ([_P, ctypes.c_int, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                            _P, _P, _P, _I64, _P, _I64, _P, _P], ctypes.c_int),
 }
 
 _lib = None

@@ -1,0 +1,374 @@
+"""Chunked / data-placement execution retargeted to B200 (HBM fast tier,
+pinned host DDR over PCIe slow tier).
+
+Drop-in for /root/reference/pkg/src/tiered_spgemm/chunking.py: the row
+partitioner, the Alg. 4 planner and the copy-cost formulas are host logic
+restated here with identical outputs (tests/test_chunking.py pins them to
+the reference's own plans), and the three executors keep their signatures
+and return ``(C, CopyLedger)`` with exactly the reference's billed events
+(chunking.py:219-337).  The difference is that the data really moves: each
+executor calls ``tsg_chunk_multiply`` (csrc/tsg_chunk.cu), which streams the
+planned ranges between host memory and HBM with double-buffered
+cudaMemcpyAsync on side streams and runs every chunk step as the fused
+multiply-add kernel in place in HBM.  The physical DMA bytes and times land
+in ``ledger.physical``; ``ledger.total_bytes()`` stays the reference's
+billing (chunk2 nets partial-C writebacks onto copy-ins, chunking.py:13-22).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .csr import OFFSET_BYTES, CsrMatrix
+from .errors import CapacityError, DimensionError, UnsplittableRowError
+from .kernel import RowRange
+from .memory import FAST, SLOW, CopyLedger, MemoryModel
+
+KNL_CHUNK = "knl_chunk"
+GPU_CHUNK1_AC_IN_PLACE = "gpu_chunk1_ac_in_place"
+GPU_CHUNK2_B_IN_PLACE = "gpu_chunk2_b_in_place"
+
+_ALGO_ID = {KNL_CHUNK: 0, GPU_CHUNK1_AC_IN_PLACE: 1, GPU_CHUNK2_B_IN_PLACE: 2}
+
+
+# ---------------------------------------------------------------- partitions
+
+@dataclass
+class RowPartition:
+    """Contiguous half-open row ranges covering [0, num_rows) with byte sizes
+    (chunking.py:39-71)."""
+
+    ranges: list
+    range_bytes: list
+    num_rows: int
+
+    def __post_init__(self):
+        at = 0
+        for r in self.ranges:
+            if r.begin != at:
+                raise DimensionError("partition ranges must be contiguous")
+            at = r.end
+        if at != self.num_rows:
+            raise DimensionError("partition must cover all %d rows" % self.num_rows)
+        if len(self.range_bytes) != len(self.ranges):
+            raise DimensionError("one byte size per range required")
+
+    def __len__(self):
+        return len(self.ranges)
+
+    @property
+    def max_range_bytes(self) -> int:
+        return max(self.range_bytes) if self.range_bytes else 0
+
+    @property
+    def total_bytes(self) -> int:
+        return sum(self.range_bytes)
+
+    def bounds(self) -> np.ndarray:
+        return np.array([0] + [r.end for r in self.ranges], dtype=np.int64)
+
+    def to_json_dict(self) -> dict:
+        return {"ranges": [[r.begin, r.end] for r in self.ranges],
+                "range_bytes": [int(x) for x in self.range_bytes]}
+
+
+def _prefix(row_bytes) -> np.ndarray:
+    rb = np.asarray(row_bytes, dtype=np.int64)
+    out = np.zeros(rb.shape[0] + 1, dtype=np.int64)
+    np.cumsum(rb, out=out[1:])
+    return out
+
+
+def singleton_partition(row_bytes) -> RowPartition:
+    rb = np.asarray(row_bytes, dtype=np.int64)
+    return RowPartition([RowRange(0, int(rb.shape[0]))], [int(rb.sum())], int(rb.shape[0]))
+
+
+def binary_search_partition(row_bytes, target: int, capacity: int | None = None) -> RowPartition:
+    """Cut where the byte prefix last stays within each multiple of ``target``
+    (chunking.py:80-128); ranges above ``capacity`` are split greedily and a
+    single row above it raises UnsplittableRowError."""
+    rb = np.asarray(row_bytes, dtype=np.int64)
+    if target <= 0:
+        raise ValueError("partition target must be positive")
+    n = int(rb.shape[0])
+    if n == 0:
+        return RowPartition([], [], 0)
+    if capacity is not None and int(rb.max()) > capacity:
+        worst = int(np.argmax(rb))
+        raise UnsplittableRowError("row %d is %d bytes, capacity %d" % (worst, int(rb[worst]), capacity))
+    pre = _prefix(rb)
+    cuts = [0]
+    at = 0
+    while at < n:
+        multiple = -(-int(pre[at + 1]) // target)          # first multiple reached past `at`
+        nxt = min(int(np.searchsorted(pre, multiple * target, side="right")) - 1, n)
+        cuts.append(nxt)
+        at = nxt
+    if capacity is not None:
+        fixed = [0]
+        for end in cuts[1:]:
+            while int(pre[end] - pre[fixed[-1]]) > capacity:
+                fixed.append(int(np.searchsorted(pre, int(pre[fixed[-1]]) + capacity, side="right")) - 1)
+            fixed.append(end)
+        cuts = fixed
+    ranges, sizes = [], []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        if hi > lo:
+            ranges.append(RowRange(lo, hi))
+            sizes.append(int(pre[hi] - pre[lo]))
+    return RowPartition(ranges, sizes, n)
+
+
+def balanced_partition(row_bytes, portion: int, capacity: int | None = None) -> RowPartition:
+    """np = ceil(total / portion) parts of pSize = ceil(total / np) (chunking.py:131-142)."""
+    rb = np.asarray(row_bytes, dtype=np.int64)
+    total = int(rb.sum())
+    if portion <= 0:
+        raise ValueError("portion must be positive")
+    if total == 0:
+        return singleton_partition(rb)
+    parts = -(-total // portion)
+    return binary_search_partition(rb, -(-total // parts), portion if capacity is None else capacity)
+
+
+# ---------------------------------------------------------------- planner
+
+@dataclass
+class ChunkPlan:
+    algorithm: str
+    partition_b: RowPartition
+    partition_ac: RowPartition | None
+    predicted_copy_bytes: int
+    heuristic_branch: int | None = None
+
+    def to_json_dict(self) -> dict:
+        return {"algorithm": self.algorithm,
+                "partition_b": self.partition_b.to_json_dict(),
+                "partition_ac": None if self.partition_ac is None else self.partition_ac.to_json_dict(),
+                "predicted_copy_bytes": int(self.predicted_copy_bytes),
+                "heuristic_branch": self.heuristic_branch}
+
+
+def copy_cost_chunk1(size_a: int, size_b: int, size_c: int, n_ac_parts: int) -> int:
+    """A and C once, B once per A/C range (chunking.py:166-171)."""
+    if n_ac_parts < 1:
+        raise ValueError("need at least one A/C part")
+    return size_a + size_c + size_b * n_ac_parts
+
+
+def copy_cost_chunk2(size_a: int, size_b: int, size_c: int, n_b_parts: int) -> int:
+    """B once, A once per B range, C re-read after the first sweep (chunking.py:174-179)."""
+    if n_b_parts < 1:
+        raise ValueError("need at least one B part")
+    return size_b + size_a * n_b_parts + size_c * (n_b_parts - 1)
+
+
+def c_row_byte_sizes(num_rows: int, c_counts) -> np.ndarray:
+    """Bytes of each not-yet-built C row: 16 per entry + its offset (row 0 also
+    carries the leading offset) (chunking.py:182-189)."""
+    out = np.asarray(c_counts, dtype=np.int64) * 16 + OFFSET_BYTES
+    if num_rows > 0:
+        out = out.copy()
+        out[0] += OFFSET_BYTES
+    return out
+
+
+def decide_chunking(size_a: int, size_b: int, size_c: int, row_bytes_a, row_bytes_b,
+                    row_bytes_c, fast_size: int) -> ChunkPlan:
+    """Alg. 4 (chunking.py:340-400): 3/4 of the fast tier goes to whichever
+    group fits whole (B first, then A+C); otherwise to the group with the
+    larger movement cost, both closed forms are priced and the cheaper order
+    wins, ties to the AC-in-place order."""
+    ra = np.asarray(row_bytes_a, dtype=np.int64)
+    rb = np.asarray(row_bytes_b, dtype=np.int64)
+    rc = np.asarray(row_bytes_c, dtype=np.int64)
+    if int(ra.sum()) != size_a or int(rb.sum()) != size_b or int(rc.sum()) != size_c:
+        raise ValueError("matrix sizes must equal their per-row byte sums")
+    if ra.shape != rc.shape:
+        raise DimensionError("A and C must have the same row count")
+    if fast_size <= 0:
+        raise ValueError("fast_size must be positive")
+    big = 3 * fast_size // 4
+    rac = ra + rc
+    if size_b < big:
+        p_b = singleton_partition(rb)
+        p_ac = balanced_partition(rac, fast_size - size_b)
+        return ChunkPlan(GPU_CHUNK2_B_IN_PLACE, p_b, p_ac,
+                         copy_cost_chunk2(size_a, size_b, size_c, len(p_b)), heuristic_branch=1)
+    if size_a + size_c < big:
+        p_ac = singleton_partition(rac)
+        p_b = balanced_partition(rb, fast_size - (size_a + size_c))
+        return ChunkPlan(GPU_CHUNK1_AC_IN_PLACE, p_b, p_ac,
+                         copy_cost_chunk1(size_a, size_b, size_c, len(p_ac)), heuristic_branch=2)
+    if size_a + 2 * size_c > size_b:
+        p_ac = balanced_partition(rac, big)
+        left = fast_size - p_ac.max_range_bytes
+        if left <= 0:
+            raise CapacityError("no room left for B chunks in %d bytes" % fast_size)
+        p_b = balanced_partition(rb, left)
+        branch = 3
+    else:
+        p_b = balanced_partition(rb, big)
+        left = fast_size - p_b.max_range_bytes
+        if left <= 0:
+            raise CapacityError("no room left for A/C chunks in %d bytes" % fast_size)
+        p_ac = balanced_partition(rac, left)
+        branch = 4
+    c1 = copy_cost_chunk1(size_a, size_b, size_c, len(p_ac))
+    c2 = copy_cost_chunk2(size_a, size_b, size_c, len(p_b))
+    if c1 <= c2:
+        return ChunkPlan(GPU_CHUNK1_AC_IN_PLACE, p_b, p_ac, c1, heuristic_branch=branch)
+    return ChunkPlan(GPU_CHUNK2_B_IN_PLACE, p_b, p_ac, c2, heuristic_branch=branch)
+
+
+def plan_for_multiply(a, b, c_counts, fast_size: int) -> ChunkPlan:
+    ra, rb = a.row_byte_sizes(), b.row_byte_sizes()
+    rc = c_row_byte_sizes(a.num_rows, c_counts)
+    return decide_chunking(int(ra.sum()), int(rb.sum()), int(rc.sum()), ra, rb, rc, fast_size)
+
+
+# ---------------------------------------------------------------- executors
+
+def _range_bytes(pre, r) -> int:
+    return int(pre[r.end] - pre[r.begin])
+
+
+def _check_partition(p: RowPartition, num_rows: int, what: str) -> None:
+    if p.num_rows != num_rows:
+        raise DimensionError("%s partition covers %d rows, expected %d" % (what, p.num_rows, num_rows))
+
+
+class _ChunkStats(ctypes.Structure):
+    _fields_ = [("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("kernel_ms", ctypes.c_double), ("wall_ms", ctypes.c_double),
+                ("peak_device_bytes", ctypes.c_int64)]
+
+
+def _c_array(x, dt):
+    return np.ascontiguousarray(np.asarray(x), dtype=dt)
+
+
+def _physical(algo: str, a, b, c_counts, ac_bounds, b_bounds, ledger) -> CsrMatrix:
+    """Run the plan on the device; fills ledger.physical; returns C."""
+    lib = _lib.load()
+    ctx = _lib.Context.get()
+    counts = _c_array(c_counts, np.int64)
+    if counts.shape[0] != a.num_rows:
+        raise DimensionError("c_counts length must equal A's row count")
+    c_rp = _lib.pinned_empty(a.num_rows + 1, np.int64)
+    c_rp[0] = 0
+    np.cumsum(counts, out=c_rp[1:])
+    nnz = int(c_rp[-1])
+    c_col = _lib.pinned_empty(nnz, np.int64)
+    c_val = _lib.pinned_empty(nnz, np.float64)
+    arrs = [_c_array(m, dt) for m, dt in ((a.row_ptr, np.int64), (a.col_idx, np.int64),
+                                           (a.values, np.float64), (b.row_ptr, np.int64),
+                                           (b.col_idx, np.int64), (b.values, np.float64))]
+    acb = _c_array(ac_bounds, np.int64)
+    bb = _c_array(b_bounds, np.int64)
+    st = _ChunkStats()
+    P = _lib._ptr
+    _lib.check(lib.tsg_chunk_multiply(
+        ctx.h, _ALGO_ID[algo], a.num_rows, a.num_cols, P(arrs[0]), P(arrs[1]), P(arrs[2]),
+        b.num_rows, b.num_cols, P(arrs[3]), P(arrs[4]), P(arrs[5]), P(c_rp), P(c_col), P(c_val),
+        len(acb) - 1, P(acb), len(bb) - 1, P(bb), ctypes.byref(st)))
+    ledger.physical = {"h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
+                       "kernel_ms": st.kernel_ms, "wall_ms": st.wall_ms,
+                       "link_gbs": (st.h2d_bytes + st.d2h_bytes) / max(st.wall_ms, 1e-9) / 1e6,
+                       "algorithm": algo}
+    return CsrMatrix._adopt(a.num_rows, b.num_cols, c_rp, c_col, c_val)
+
+
+def knl_chunk_multiply(a, b, c_counts, fast_size: int, model: MemoryModel, workers: int = 1):
+    """Alg. 1 (chunking.py:219-249): ceil(size(B)/fast) B row chunks stream
+    through fast memory past all of A and C.  Returns (C, ledger); the ledger
+    bills exactly size(B)."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A has %d cols but B has %d rows" % (a.num_cols, b.num_rows))
+    if fast_size <= 0:
+        raise ValueError("fast_size must be positive")
+    rb = b.row_byte_sizes()
+    size_b = int(rb.sum())
+    parts = max(1, -(-size_b // fast_size))
+    p_b = binary_search_partition(rb, -(-size_b // parts), fast_size)
+    ledger = CopyLedger(model)
+    pre = _prefix(rb)
+    for r in p_b.ranges:
+        nb = _range_bytes(pre, r)
+        ledger.alloc(FAST, nb)
+        ledger.record(nb, SLOW, FAST, tag="B")
+        ledger.free(FAST, nb)
+    c = _physical(KNL_CHUNK, a, b, c_counts, [0, a.num_rows], p_b.bounds(), ledger)
+    return c, ledger
+
+
+def gpu_chunk_multiply_1(a, b, c_counts, p_ac: RowPartition, p_b: RowPartition,
+                         model: MemoryModel, workers: int = 1):
+    """Alg. 2, A/C in place (chunking.py:258-296): per A/C range, A rows and
+    C offsets in, every B chunk streams past, finished C entries out."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A has %d cols but B has %d rows" % (a.num_cols, b.num_rows))
+    _check_partition(p_ac, a.num_rows, "AC")
+    _check_partition(p_b, b.num_rows, "B")
+    pa, pb = _prefix(a.row_byte_sizes()), _prefix(b.row_byte_sizes())
+    pc = _prefix(c_row_byte_sizes(a.num_rows, c_counts))
+    counts = np.asarray(c_counts, dtype=np.int64)
+    ledger = CopyLedger(model)
+    for ac in p_ac.ranges:
+        a_bytes, c_full = _range_bytes(pa, ac), _range_bytes(pc, ac)
+        c_entries = int(counts[ac.begin:ac.end].sum()) * 16
+        ledger.alloc(FAST, a_bytes + c_full)
+        ledger.record(a_bytes, SLOW, FAST, tag="A")
+        ledger.record(c_full - c_entries, SLOW, FAST, tag="C_in")
+        for br in p_b.ranges:
+            nb = _range_bytes(pb, br)
+            ledger.alloc(FAST, nb)
+            ledger.record(nb, SLOW, FAST, tag="B")
+            ledger.free(FAST, nb)
+        ledger.record(c_entries, FAST, SLOW, tag="C_out")
+        ledger.free(FAST, a_bytes + c_full)
+    c = _physical(GPU_CHUNK1_AC_IN_PLACE, a, b, counts, p_ac.bounds(), p_b.bounds(), ledger)
+    return c, ledger
+
+
+def gpu_chunk_multiply_2(a, b, c_counts, p_ac: RowPartition, p_b: RowPartition,
+                         model: MemoryModel, workers: int = 1):
+    """Alg. 3, B in place (chunking.py:299-337): per B chunk, every A/C range
+    streams past; partial C round-trips are billed on the copy-in."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A has %d cols but B has %d rows" % (a.num_cols, b.num_rows))
+    _check_partition(p_ac, a.num_rows, "AC")
+    _check_partition(p_b, b.num_rows, "B")
+    pa, pb = _prefix(a.row_byte_sizes()), _prefix(b.row_byte_sizes())
+    pc = _prefix(c_row_byte_sizes(a.num_rows, c_counts))
+    ledger = CopyLedger(model)
+    for bi, br in enumerate(p_b.ranges):
+        nb = _range_bytes(pb, br)
+        ledger.alloc(FAST, nb)
+        ledger.record(nb, SLOW, FAST, tag="B")
+        for ac in p_ac.ranges:
+            a_bytes, c_full = _range_bytes(pa, ac), _range_bytes(pc, ac)
+            ledger.alloc(FAST, a_bytes + c_full)
+            ledger.record(a_bytes, SLOW, FAST, tag="A")
+            ledger.record(c_full if bi > 0 else 0, SLOW, FAST, tag="C_in")
+            ledger.record(0, FAST, SLOW, tag="C_out")
+            ledger.free(FAST, a_bytes + c_full)
+        ledger.free(FAST, nb)
+    c = _physical(GPU_CHUNK2_B_IN_PLACE, a, b, c_counts, p_ac.bounds(), p_b.bounds(), ledger)
+    return c, ledger
+
+
+def execute_plan(a, b, c_counts, plan: ChunkPlan, model: MemoryModel, workers: int = 1):
+    """Dispatch a ChunkPlan (chunking.py:412-426)."""
+    if plan.algorithm == GPU_CHUNK1_AC_IN_PLACE:
+        return gpu_chunk_multiply_1(a, b, c_counts, plan.partition_ac, plan.partition_b, model)
+    if plan.algorithm == GPU_CHUNK2_B_IN_PLACE:
+        return gpu_chunk_multiply_2(a, b, c_counts, plan.partition_ac, plan.partition_b, model)
+    if plan.algorithm == KNL_CHUNK:
+        if model.fast.capacity is None:
+            raise ValueError("KNL chunk execution needs a finite fast capacity")
+        return knl_chunk_multiply(a, b, c_counts, model.fast.capacity, model)
+    raise ValueError("unknown chunk algorithm %r" % plan.algorithm)

@@ -1,0 +1,387 @@
+// tsg_chunk.cu -- physical chunked execution through an HBM budget.
+//
+// The reference's three orders (chunking.py:219-337) bill a simulated copy
+// ledger; here the same orders really move the data.  The slow tier is host
+// memory (the caller's arrays, pinned for full PCIe rate), the fast tier is
+// HBM:
+//   order 1 (gpu chunk1, AC in place): per A/C row range, A rows go H2D once,
+//     the C range lives in HBM at its final row capacity while every B row
+//     chunk streams past it, then the finished C range goes D2H once.
+//   order 2 (gpu chunk2, B in place): per B chunk (resident), every A/C range
+//     streams past it; C partials round-trip through host memory.
+//   order 0 (KNL): B chunks stream past the whole of A/C (order 1 with one
+//     A/C range).
+// Every chunk step is the fused multiply-add (kernel.py:235-340) run IN
+// PLACE: C rows keep their final capacity and the running partial occupies a
+// prefix whose length is tracked per row, so no C copy is ever made on the
+// device.  B chunks and A ranges are double-buffered: the next one's H2D runs
+// on the copy-in stream while the current one computes; C ranges drain D2H on
+// the copy-out stream while the next range computes.  Host formats are the
+// reference's (int64 indices): columns travel as int64 and are narrowed /
+// widened on the device, so physical PCIe bytes equal the ledger's byte
+// convention (csr.py:65-67).
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "tsg_internal.cuh"
+
+// implemented in tsg_spgemm.cu
+int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out);
+int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, const tsg_csr *b,
+                      const tsg_cmat *cb, const int64_t *cptr, const int64_t *cap, int32_t *ccol,
+                      double *cval, int32_t *plen, int64_t rows);
+
+namespace {
+
+__global__ void k_rebase(const int64_t *__restrict__ in, int64_t *__restrict__ out, int64_t n,
+                         int64_t base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] - base;
+}
+
+__global__ void k_narrow(const int64_t *__restrict__ in, int32_t *__restrict__ out, int64_t n,
+                         int64_t ncols, int *err) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = in[i];
+        if (v < 0 || v >= ncols) {
+            kerr(err, KERR_COLRANGE, i);
+            v = 0;
+        }
+        out[i] = (int32_t)v;
+    }
+}
+
+__global__ void k_widen(const int32_t *__restrict__ in, int64_t *__restrict__ out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i];
+}
+
+__global__ void k_check_full(const int32_t *__restrict__ plen, const int64_t *__restrict__ cap,
+                             int64_t n, int64_t row0, int *err) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if ((int64_t)plen[i] != cap[i]) kerr(err, KERR_ROWSIZE, row0 + i);
+}
+
+__global__ void k_caps(const int64_t *__restrict__ cptr, int64_t *__restrict__ cap, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        cap[i] = cptr[i + 1] - cptr[i];
+}
+
+// A row range [lo, hi) of a host CSR staged in HBM (rebased row pointers).
+struct DevRange {
+    tsg_csr m{};          // device view (rp rebased, int32 cols)
+    int64_t *stage = nullptr;   // int64 column staging
+    int64_t cap_rows = 0, cap_nnz = 0;
+    cudaEvent_t ready{};
+};
+
+struct HostCsr {
+    int64_t rows, cols;
+    const int64_t *rp;
+    const int64_t *col;
+    const double *val;
+};
+
+int ensure(tsg_ctx *c, DevRange &d, int64_t rows, int64_t nnz, bool values) {
+    if (rows > d.cap_rows || nnz > d.cap_nnz) {
+        tsg_free(c, d.m.rp);
+        tsg_free(c, d.m.col);
+        tsg_free(c, d.m.val);
+        tsg_free(c, d.stage);
+        d.cap_rows = rows > d.cap_rows ? rows : d.cap_rows;
+        d.cap_nnz = nnz > d.cap_nnz ? nnz : d.cap_nnz;
+        TSG_TRY(tsg_alloc_t(c, &d.m.rp, d.cap_rows + 2));
+        TSG_TRY(tsg_alloc_t(c, &d.m.col, d.cap_nnz + 1));
+        if (values) TSG_TRY(tsg_alloc_t(c, &d.m.val, d.cap_nnz + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.stage, d.cap_nnz + 2));
+    }
+    if (!d.ready) TSG_CK(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
+    return TSG_OK;
+}
+
+void release(tsg_ctx *c, DevRange &d) {
+    tsg_free(c, d.m.rp);
+    tsg_free(c, d.m.col);
+    tsg_free(c, d.m.val);
+    tsg_free(c, d.stage);
+    if (d.ready) cudaEventDestroy(d.ready);
+    d = DevRange();
+}
+
+// H2D of host rows [lo, hi) on the copy-in stream; narrowing/rebasing kernels
+// run on the copy-in stream too, `ready` marks completion.
+int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d,
+               cudaEvent_t wait_free, int64_t &bytes) {
+    const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
+    TSG_TRY(ensure(c, d, rows, nnz, h.val != nullptr));
+    cudaStream_t s = c->copy_in;
+    if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
+    // row pointers: staged through the int64 buffer then rebased
+    TSG_CK(cudaMemcpyAsync(d.stage, h.rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, s>>>(d.stage, d.m.rp, rows + 1, e0); ++c->launches;
+    if (nnz > 0) {
+        TSG_CK(cudaMemcpyAsync(d.stage, h.col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.m.col, nnz, h.cols,
+                                                                     c->d_err); ++c->launches;
+        if (h.val)
+            TSG_CK(cudaMemcpyAsync(d.m.val, h.val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaEventRecord(d.ready, s));
+    d.m.rows = rows;
+    d.m.cols = h.cols;
+    d.m.nnz = nnz;
+    bytes += (rows + 1) * 8 + nnz * (h.val ? 16 : 8);
+    return TSG_OK;
+}
+
+// C range [lo, hi) resident in HBM at final row capacity
+struct DevC {
+    int64_t *cptr = nullptr;   // rebased final row pointers (rows + 1)
+    int64_t *cap = nullptr;    // capacities (rows)
+    int32_t *col = nullptr;
+    double *val = nullptr;
+    int32_t *plen = nullptr;   // running partial lengths
+    int64_t *stage = nullptr;  // int64 column staging for transfers
+    int64_t cap_rows = 0, cap_nnz = 0;
+    cudaEvent_t drained{};     // D2H of this buffer finished
+};
+
+int ensure_c(tsg_ctx *c, DevC &d, int64_t rows, int64_t nnz) {
+    if (rows > d.cap_rows || nnz > d.cap_nnz) {
+        tsg_free(c, d.cptr);
+        tsg_free(c, d.cap);
+        tsg_free(c, d.col);
+        tsg_free(c, d.val);
+        tsg_free(c, d.plen);
+        tsg_free(c, d.stage);
+        d.cap_rows = rows > d.cap_rows ? rows : d.cap_rows;
+        d.cap_nnz = nnz > d.cap_nnz ? nnz : d.cap_nnz;
+        TSG_TRY(tsg_alloc_t(c, &d.cptr, d.cap_rows + 2));
+        TSG_TRY(tsg_alloc_t(c, &d.cap, d.cap_rows + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.col, d.cap_nnz + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.val, d.cap_nnz + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.plen, d.cap_rows + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.stage, d.cap_nnz + d.cap_rows + 2));
+    }
+    if (!d.drained) TSG_CK(cudaEventCreateWithFlags(&d.drained, cudaEventDisableTiming));
+    return TSG_OK;
+}
+
+void release_c(tsg_ctx *c, DevC &d) {
+    tsg_free(c, d.cptr);
+    tsg_free(c, d.cap);
+    tsg_free(c, d.col);
+    tsg_free(c, d.val);
+    tsg_free(c, d.plen);
+    tsg_free(c, d.stage);
+    if (d.drained) cudaEventDestroy(d.drained);
+    d = DevC();
+}
+
+struct Job {
+    tsg_ctx *c;
+    HostCsr A, B;
+    const int64_t *c_rp;
+    int64_t *c_col;
+    double *c_val;
+    int32_t *h_plen;    // host partial lengths (order 2), per row of A
+    tsg_chunk_stats *st;
+};
+
+// C range setup on the compute stream: row pointers (rebased) + capacities;
+// optionally load a partial (order 2) from host.
+int open_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool load_partial) {
+    tsg_ctx *c = J.c;
+    const int64_t rows = hi - lo, e0 = J.c_rp[lo], nnz = J.c_rp[hi] - e0;
+    TSG_TRY(ensure_c(c, d, rows, nnz));
+    cudaStream_t s = c->stream;
+    TSG_CK(cudaStreamWaitEvent(s, d.drained, 0));   // previous D2H of this buffer
+    TSG_CK(cudaMemcpyAsync(d.stage, J.c_rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, s>>>(d.stage, d.cptr, rows + 1, e0); ++c->launches;
+    k_caps<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, s>>>(d.cptr, d.cap, rows); ++c->launches;
+    J.st->h2d_bytes += (rows + 1) * 8;
+    if (load_partial) {
+        TSG_CK(cudaMemcpyAsync(d.plen, J.h_plen + lo, rows * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        if (nnz > 0) {
+            TSG_CK(cudaMemcpyAsync(d.stage, J.c_col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.col, nnz, J.B.cols,
+                                                                         c->d_err); ++c->launches;
+            TSG_CK(cudaMemcpyAsync(d.val, J.c_val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        J.st->h2d_bytes += rows * 4 + nnz * 16;
+    } else {
+        TSG_CK(cudaMemsetAsync(d.plen, 0, rows * sizeof(int32_t), s));
+    }
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+// D2H of a C range (columns widened to int64) on the copy-out stream.
+int drain_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool with_plen) {
+    tsg_ctx *c = J.c;
+    const int64_t rows = hi - lo, e0 = J.c_rp[lo], nnz = J.c_rp[hi] - e0;
+    cudaEvent_t done;
+    TSG_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    if (nnz > 0) {
+        k_widen<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, c->stream>>>(d.col, d.stage, nnz); ++c->launches;
+    }
+    TSG_CK(cudaEventRecord(done, c->stream));
+    cudaStream_t s = c->copy_out;
+    TSG_CK(cudaStreamWaitEvent(s, done, 0));
+    if (nnz > 0) {
+        TSG_CK(cudaMemcpyAsync(J.c_col + e0, d.stage, nnz * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        TSG_CK(cudaMemcpyAsync(J.c_val + e0, d.val, nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (with_plen)
+        TSG_CK(cudaMemcpyAsync(J.h_plen + lo, d.plen, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TSG_CK(cudaEventRecord(d.drained, s));
+    TSG_CK(cudaEventDestroy(done));
+    J.st->d2h_bytes += nnz * 16 + (with_plen ? rows * 4 : 0);
+    return TSG_OK;
+}
+
+}  // namespace
+
+extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t a_cols,
+                                  const int64_t *a_rp, const int64_t *a_col, const double *a_val,
+                                  int64_t b_rows, int64_t b_cols, const int64_t *b_rp,
+                                  const int64_t *b_col, const double *b_val, const int64_t *c_rp,
+                                  int64_t *c_col, double *c_val, int64_t n_ac,
+                                  const int64_t *ac_bounds, int64_t n_b, const int64_t *b_bounds,
+                                  tsg_chunk_stats *stats) {
+    if (a_cols != b_rows) {
+        tsg_set_error("A has %lld cols but B has %lld rows", (long long)a_cols, (long long)b_rows);
+        return TSG_EDIM;
+    }
+    if (!a_val || !b_val) {
+        tsg_set_error("chunked multiply requires values on both operands");
+        return TSG_EVALID;
+    }
+    if (algo < 0 || algo > 2 || n_ac < 1 || n_b < 1 || ac_bounds[0] != 0 || ac_bounds[n_ac] != a_rows ||
+        b_bounds[0] != 0 || b_bounds[n_b] != b_rows) {
+        tsg_set_error("invalid chunk plan");
+        return TSG_EARG;
+    }
+    tsg_chunk_stats local;
+    memset(&local, 0, sizeof(local));
+    auto t0 = std::chrono::steady_clock::now();
+    Job J{c, {a_rows, a_cols, a_rp, a_col, a_val}, {b_rows, b_cols, b_rp, b_col, b_val}, c_rp,
+          c_col, c_val, nullptr, &local};
+    std::vector<int32_t> plen_host;
+    DevRange Abuf[2], Bbuf[2];
+    DevC Cbuf[2];
+    cudaEvent_t used[2] = {nullptr, nullptr};   // compute finished with Bbuf/Abuf slot
+    for (int i = 0; i < 2; i++) TSG_CK(cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming));
+    cudaEvent_t k0, k1;
+    TSG_CK(cudaEventCreate(&k0));
+    TSG_CK(cudaEventCreate(&k1));
+    float kernel_ms = 0.f;
+    int st = TSG_OK;
+
+    auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi,
+                          int64_t rows) -> int {
+        TSG_CK(cudaStreamWaitEvent(c->stream, A.ready, 0));
+        TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
+        TSG_CK(cudaEventRecord(k0, c->stream));
+        tsg_cmat *cb = nullptr;
+        TSG_TRY(tsg_compress_impl(c, &B.m, &cb));
+        int s2 = tsg_fused_inplace(c, &A.m, (int32_t)blo, (int32_t)bhi, &B.m, cb, C.cptr, C.cap, C.col,
+                                   C.val, C.plen, rows);
+        tsg_cmat_free(c, cb);
+        TSG_TRY(s2);
+        TSG_CK(cudaEventRecord(k1, c->stream));
+        TSG_CK(cudaEventSynchronize(k1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, k0, k1);
+        kernel_ms += ms;
+        return TSG_OK;
+    };
+
+    if (algo == 0 || algo == 1) {
+        const int64_t *acb = ac_bounds;
+        int64_t nac = n_ac;
+        int64_t whole[2] = {0, a_rows};
+        if (algo == 0) {
+            acb = whole;
+            nac = 1;
+        }
+        for (int64_t r = 0; r < nac && st == TSG_OK; ++r) {
+            const int64_t lo = acb[r], hi = acb[r + 1];
+            DevRange &A = Abuf[r & 1];
+            DevC &C = Cbuf[r & 1];
+            if ((st = stage_rows(c, J.A, lo, hi, A, nullptr, local.h2d_bytes)) != TSG_OK) break;
+            if ((st = open_c(J, C, lo, hi, false)) != TSG_OK) break;
+            if ((st = stage_rows(c, J.B, b_bounds[0], b_bounds[1], Bbuf[0], used[0], local.h2d_bytes)) != TSG_OK)
+                break;
+            for (int64_t j = 0; j < n_b && st == TSG_OK; ++j) {
+                if (j + 1 < n_b)   // prefetch the next B chunk into the other slot
+                    st = stage_rows(c, J.B, b_bounds[j + 1], b_bounds[j + 2], Bbuf[(j + 1) & 1],
+                                    used[(j + 1) & 1], local.h2d_bytes);
+                if (st != TSG_OK) break;
+                st = fused_step(A, Bbuf[j & 1], C, b_bounds[j], b_bounds[j + 1], hi - lo);
+                cudaEventRecord(used[j & 1], c->stream);
+            }
+            if (st == TSG_OK) {
+                k_check_full<<<grid_for(hi - lo, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+                    C.plen, C.cap, hi - lo, lo, c->d_err); ++c->launches;
+                st = drain_c(J, C, lo, hi, false);
+            }
+        }
+    } else {
+        plen_host.assign((size_t)a_rows + 1, 0);
+        J.h_plen = plen_host.data();
+        for (int64_t j = 0; j < n_b && st == TSG_OK; ++j) {
+            DevRange &B = Bbuf[j & 1];
+            if ((st = stage_rows(c, J.B, b_bounds[j], b_bounds[j + 1], B, used[j & 1], local.h2d_bytes)) != TSG_OK)
+                break;
+            for (int64_t r = 0; r < n_ac && st == TSG_OK; ++r) {
+                const int64_t lo = ac_bounds[r], hi = ac_bounds[r + 1];
+                DevRange &A = Abuf[r & 1];
+                DevC &C = Cbuf[r & 1];
+                if ((st = stage_rows(c, J.A, lo, hi, A, nullptr, local.h2d_bytes)) != TSG_OK) break;
+                // partials come back from host after the first B sweep; the D2H
+                // of the previous sweep for this range must have landed
+                TSG_CK(cudaStreamSynchronize(c->copy_out));
+                if ((st = open_c(J, C, lo, hi, j > 0)) != TSG_OK) break;
+                st = fused_step(A, B, C, b_bounds[j], b_bounds[j + 1], hi - lo);
+                if (st == TSG_OK) st = drain_c(J, C, lo, hi, true);
+            }
+            cudaEventRecord(used[j & 1], c->stream);
+        }
+    }
+    cudaStreamSynchronize(c->copy_in);
+    cudaStreamSynchronize(c->copy_out);
+    cudaStreamSynchronize(c->stream);
+    if (st == TSG_OK) st = tsg_check_kernel_errors(c, "chunked multiply");
+    if (st == TSG_OK && algo == 2) {
+        for (int64_t i = 0; i < a_rows; ++i)
+            if (plen_host[i] != c_rp[i + 1] - c_rp[i]) {
+                tsg_set_error("chunked result rows disagree with symbolic counts (row %lld: %d vs %lld)",
+                              (long long)i, plen_host[i], (long long)(c_rp[i + 1] - c_rp[i]));
+                st = TSG_EDIM;
+                break;
+            }
+    }
+    int64_t mem = c->bytes_in_use;
+    for (int i = 0; i < 2; i++) {
+        release(c, Abuf[i]);
+        release(c, Bbuf[i]);
+        release_c(c, Cbuf[i]);
+        cudaEventDestroy(used[i]);
+    }
+    cudaEventDestroy(k0);
+    cudaEventDestroy(k1);
+    cudaStreamSynchronize(c->stream);
+    local.kernel_ms = kernel_ms;
+    local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    local.peak_device_bytes = mem;
+    if (stats) *stats = local;
+    return st;
+}

@@ -408,6 +408,9 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
     case KERR_NOTLOWER:
         tsg_set_error("row %d has a column >= its row: not strictly lower triangular", h[1]);
         return TSG_EVALID;
+    case KERR_ROWSIZE:
+        tsg_set_error("chunked result rows disagree with symbolic counts (row %d)", h[1]);
+        return TSG_EDIM;
     case KERR_COLRANGE:
         tsg_set_error("%s: column index out of range in row %d", phase, h[1]);
         return TSG_EVALID;

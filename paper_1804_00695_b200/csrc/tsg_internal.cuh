@@ -84,7 +84,7 @@ int tsg_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
 
 // kernel-side error reporting: first code wins, lowest row kept
 enum { KERR_NONE = 0, KERR_COUNT = 1, KERR_PROBE = 2, KERR_NOTLOWER = 3, KERR_COLRANGE = 4,
-       KERR_UNSORTED_INTERNAL = 5 };
+       KERR_UNSORTED_INTERNAL = 5, KERR_ROWSIZE = 6 };
 
 __device__ __forceinline__ void kerr(int *err, int code, int64_t row) {
     atomicCAS(err, 0, code);

@@ -24,6 +24,7 @@
 // within the 1e-12 parity tolerance).
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "tsg_group.cuh"
@@ -83,7 +84,25 @@ struct NumArgs {
     const int64_t *sptr;   // sorted sets from the symbolic phase (rows flagged SETS_WRITTEN)
     const int32_t *sset;
     const uint64_t *sbits;
+    // capacity mode (chunked executors): counts[i] is row i's final capacity,
+    // the partial row is (pcol, pval)[pstart[i] .. + plen_in[i]) -- possibly the
+    // output row itself -- and the merged length is written to plen_out[i].
+    const int64_t *pstart;
+    const int32_t *plen_in;
+    int32_t *plen_out;
 };
+
+__device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
+    if (a.pstart) {
+        p0 = a.pstart[i];
+        p1 = p0 + a.plen_in[i];
+    } else if (a.prp) {
+        p0 = a.prp[i];
+        p1 = a.prp[i + 1];
+    } else {
+        p0 = p1 = 0;
+    }
+}
 
 // ======================================================================= K0
 
@@ -602,7 +621,13 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         const int logT = ilog2_pow2(T);
         tbl_clear(tbl, T, glane, G);
         __syncwarp(gm);
-        const int64_t p0 = a.prp ? a.prp[i] : 0, p1 = a.prp ? a.prp[i + 1] : 0;
+        int64_t p0, p1;
+        partial_range(a, i, p0, p1);
+        const bool cap_mode = a.plen_out != nullptr;
+        // in place: the partial row IS the output row, so columns are emitted
+        // only after the partial values have been read (phase D)
+        const bool inplace = cap_mode && a.pcol == a.ccol;
+        int rowlen = n;
         bool ok = true;
 
         if (have_sets) {
@@ -686,11 +711,12 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
             }
             tot = group_sum<G, int>(gm, tot);
             ok = __all_sync(gm, ok);
-            if (tot != n || !ok || m > n) {
+            if ((cap_mode ? tot > n : tot != n) || !ok || m > n) {
                 if (glane == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
                 __syncwarp(gm);
                 continue;   // group-uniform
             }
+            rowlen = tot;
             __syncwarp(gm);
             for (int q = glane; q < m; q += G) {
                 int2 me = cbuf[q];
@@ -701,6 +727,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
                 }
                 int slot = me.y >> 8;
                 tbl[slot].w = base;
+                if (inplace) continue;
                 int4 e = tbl[slot];
                 unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
                 int r = base;
@@ -718,7 +745,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
 
         }
         __syncwarp(gm);
-        for (int q = glane; q < n; q += G) vals[q] = -0.0;
+        for (int q = glane; q < rowlen; q += G) vals[q] = -0.0;
         __syncwarp(gm);
 
         // phase C: partial values first, then products in A storage order
@@ -756,7 +783,25 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
                 });
         }
         __syncwarp(gm);
-        for (int q = glane; q < n; q += G) a.cval[cp + q] = vals[q];
+        if (inplace) {
+            // phase D: the partial row has been consumed; emit merged columns
+            for (int s = glane; s < T; s += G) {
+                int4 e = tbl[s];
+                if (e.x == TSG_EMPTY) continue;
+                unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+                int r = e.w;
+                while (lo) {
+                    a.ccol[cp + r++] = e.x * 64 + (__ffs(lo) - 1);
+                    lo &= lo - 1;
+                }
+                while (hi) {
+                    a.ccol[cp + r++] = e.x * 64 + 32 + (__ffs(hi) - 1);
+                    hi &= hi - 1;
+                }
+            }
+        }
+        for (int q = glane; q < rowlen; q += G) a.cval[cp + q] = vals[q];
+        if (cap_mode && glane == 0) a.plen_out[i] = rowlen;
         __syncwarp(gm);
     }
 }
@@ -793,15 +838,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_warp) {
 
 // Union of the row's sets into tbl (generic pointer: smem or global slab).
 template <int NT>
-__device__ __forceinline__ bool block_union(int4 *tbl, int T, int logT, const int64_t *prp,
-                                            const int32_t *pcol, int64_t li, int64_t a0,
+__device__ __forceinline__ bool block_union(int4 *tbl, int T, int logT, int64_t p0, int64_t p1,
+                                            const int32_t *pcol, int64_t a0,
                                             int64_t a1, const int32_t *acol, int32_t b_lo,
                                             int32_t b_hi, const int64_t *cbstart,
                                             const int32_t *cbcnt, const int32_t *cbset,
                                             const uint64_t *cbbits) {
     bool ok = true;
-    if (prp) {
-        for (int64_t q = prp[li] + threadIdx.x; q < prp[li + 1]; q += NT) {
+    {
+        for (int64_t q = p0 + threadIdx.x; q < p1; q += NT) {
             int c = pcol[q];
             int bit = c & 63;
             ok &= tbl_or(tbl, T, logT, c >> 6, bit < 32 ? 1u << bit : 0u,
@@ -842,7 +887,8 @@ __global__ void __launch_bounds__(NT) k_sym_block(const int32_t *__restrict__ li
         tbl_clear(tbl, T, threadIdx.x, NT);
         if (threadIdx.x < 2) s_red[threadIdx.x] = 0;
         __syncthreads();
-        bool ok = block_union<NT>(tbl, T, logT, a.prp, a.pcol, i, a.arp[gi], a.arp[gi + 1], a.acol,
+        const int64_t sp0 = a.prp ? a.prp[i] : 0, sp1 = a.prp ? a.prp[i + 1] : 0;
+        bool ok = block_union<NT>(tbl, T, logT, sp0, sp1, a.pcol, a.arp[gi], a.arp[gi + 1], a.acol,
                                   a.b_lo, a.b_hi, a.cbstart, a.cbcnt, a.cbset, a.cbbits);
         __syncthreads();
         int cnt = 0, m = 0;
@@ -891,7 +937,9 @@ __global__ void __launch_bounds__(NT) k_num_block(const int32_t *__restrict__ li
         tbl_clear(tbl, T, threadIdx.x, NT);
         if (threadIdx.x == 0) s_m = 0;
         __syncthreads();
-        bool ok = block_union<NT>(tbl, T, logT, a.prp, a.pcol, i, a.arp[gi], a.arp[gi + 1], a.acol,
+        int64_t p0, p1;
+        partial_range(a, i, p0, p1);
+        bool ok = block_union<NT>(tbl, T, logT, p0, p1, a.pcol, a.arp[gi], a.arp[gi + 1], a.acol,
                                   a.b_lo, a.b_hi, a.cbstart, a.cbcnt, a.cbset, a.cbbits);
         __syncthreads();
         // compact occupied slots as sortable (key << 32 | slot)
@@ -960,14 +1008,15 @@ __global__ void __launch_bounds__(NT) k_num_block(const int32_t *__restrict__ li
             carry += tot;
         }
         ok = __syncthreads_and(ok);
-        if (carry != n || !ok) {
+        if ((a.plen_out ? carry > n : carry != n) || !ok) {
             if (threadIdx.x == 0) kerr(a.err, ok ? KERR_COUNT : KERR_PROBE, gi);
             __syncthreads();
             continue;
         }
+        if (a.plen_out && threadIdx.x == 0) a.plen_out[i] = carry;
         // partial values, then products (order-free REDG adds)
-        if (a.prp) {
-            for (int64_t q = a.prp[i] + threadIdx.x; q < a.prp[i + 1]; q += NT) {
+        if (p1 > p0) {
+            for (int64_t q = p0 + threadIdx.x; q < p1; q += NT) {
                 int c = a.pcol[q];
                 int4 e;
                 tbl_find(tbl, T, logT, c >> 6, e);
@@ -1364,7 +1413,7 @@ __global__ void k_fused_bounds(int64_t rows_out, const int64_t *__restrict__ arp
                                const int32_t *__restrict__ acol, int64_t a_row_off, int32_t b_lo,
                                int32_t b_hi, const int64_t *__restrict__ cbstart,
                                const int32_t *__restrict__ cbcnt, const int64_t *__restrict__ prp,
-                               int64_t *__restrict__ sbound) {
+                               int64_t *__restrict__ sbound, const int32_t *__restrict__ plen) {
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1376,7 +1425,7 @@ __global__ void k_fused_bounds(int64_t rows_out, const int64_t *__restrict__ arp
             if (k >= b_lo && k < b_hi) s += cbcnt[k - b_lo];
         }
         for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-        if (lane == 0) sbound[i] = s + (prp ? prp[i + 1] - prp[i] : 0);
+        if (lane == 0) sbound[i] = s + (prp ? prp[i + 1] - prp[i] : 0) + (plen ? plen[i] : 0);
     }
 }
 }  // namespace
@@ -1385,7 +1434,7 @@ int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_r
                      int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
                      const int64_t *prp, int64_t *sbound) {
     k_fused_bounds<<<grid_for(rows_out, 8, c->num_sms * 32), 256, 0, c->stream>>>(
-        rows_out, a->rp, a->col, a_row_off, b_lo, b_hi, cbstart, cbcnt, prp, sbound); ++c->launches;
+        rows_out, a->rp, a->col, a_row_off, b_lo, b_hi, cbstart, cbcnt, prp, sbound, nullptr); ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -1460,6 +1509,9 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.sptr = counts->sptr;
         na.sset = counts->sset;
         na.sbits = counts->sbits;
+        na.pstart = nullptr;
+        na.plen_in = nullptr;
+        na.plen_out = nullptr;
         if (c->timing) cudaEventRecord(c->ev_num[0], c->stream);
         TSG_TRY(run_numeric_bins(c, bl, na));
         if (c->timing) cudaEventRecord(c->ev_num[1], c->stream);
@@ -1474,6 +1526,108 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         return s;
     }
     *out = C;
+    return TSG_OK;
+}
+
+namespace {
+__global__ void k_copy_partials(const int32_t *__restrict__ list, int64_t n,
+                                const int64_t *__restrict__ cptr, const int32_t *__restrict__ plen,
+                                const int32_t *__restrict__ col, const double *__restrict__ val,
+                                int32_t *__restrict__ scol, double *__restrict__ sval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = w; x < n; x += nw) {
+        int64_t i = list[x];
+        int64_t p0 = cptr[i];
+        for (int64_t q = p0 + lane; q < p0 + plen[i]; q += 32) {
+            scol[q] = col[q];
+            sval[q] = val[q];
+        }
+    }
+}
+}  // namespace
+
+// One in-place fused multiply-add step of the chunked executors:
+//   C[r] = C[r] (partial prefix of plen[r] entries, row capacity cap[r]) +
+//          A[r, b_lo:b_hi] * B_chunk
+// Thread-group rows merge in place (tsg_group path, deferred emission); CTA
+// and global-tier rows read their partial from a scratch copy.
+int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, const tsg_csr *b,
+                      const tsg_cmat *cb, const int64_t *cptr, const int64_t *cap, int32_t *ccol,
+                      double *cval, int32_t *plen, int64_t rows) {
+    if (rows <= 0) return TSG_OK;
+    int64_t *sbound = nullptr;
+    uint8_t *bins = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &sbound, rows + 1));
+    TSG_TRY(tsg_alloc_t(c, &bins, rows + 1));
+    k_fused_bounds<<<grid_for(rows, 8, c->num_sms * 32), 256, 0, c->stream>>>(
+        rows, a->rp, a->col, 0, b_lo, b_hi, cb->start, cb->cnt, nullptr, sbound, plen); ++c->launches;
+    k_num_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, cap, nullptr, sbound,
+                                                                          bins); ++c->launches;
+    TSG_CK(cudaGetLastError());
+    BinLists bl;
+    TSG_TRY(partition_rows(c, rows, bins, bl));
+    NumArgs na;
+    memset(&na, 0, sizeof(na));
+    na.arp = a->rp;
+    na.acol = a->col;
+    na.aval = a->val;
+    na.a_row_off = 0;
+    na.b_lo = b_lo;
+    na.b_hi = b_hi;
+    na.brp = b->rp;
+    na.bcol = b->col;
+    na.bval = b->val;
+    na.cbstart = cb->start;
+    na.cbcnt = cb->cnt;
+    na.cbset = cb->set;
+    na.cbbits = cb->bits;
+    na.cptr = cptr;
+    na.counts = cap;
+    na.sbound = sbound;
+    na.ccol = ccol;
+    na.cval = cval;
+    na.err = c->d_err;
+    na.seq = b->rows > 0 ? (int)(b->nnz / b->rows) : 0;
+    na.pcol = ccol;            // in place
+    na.pval = cval;
+    na.pstart = cptr;
+    na.plen_in = plen;
+    na.plen_out = plen;
+    TSG_TRY(launch_num_group<0>(c, bl, na));
+    TSG_TRY(launch_num_group<1>(c, bl, na));
+    TSG_TRY(launch_num_group<2>(c, bl, na));
+    TSG_TRY(launch_num_group<3>(c, bl, na));
+    TSG_TRY(launch_num_group<4>(c, bl, na));
+    TSG_TRY(launch_num_group<5>(c, bl, na));
+    TSG_TRY(launch_num_group<6>(c, bl, na));
+    int64_t nbig = bl.off[NBINS] - bl.off[7];
+    int32_t *scol = nullptr;
+    double *sval = nullptr;
+    if (nbig > 0) {
+        int64_t total = 0;
+        TSG_CK(cudaMemcpyAsync(&c->h_small[40], cptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        total = c->h_small[40];
+        TSG_TRY(tsg_alloc_t(c, &scol, total + 1));
+        TSG_TRY(tsg_alloc_t(c, &sval, total + 1));
+        k_copy_partials<<<grid_for(nbig, 8, c->num_sms * 16), 256, 0, c->stream>>>(
+            bl.list + bl.off[7], nbig, cptr, plen, ccol, cval, scol, sval); ++c->launches;
+        NumArgs nb = na;
+        nb.pcol = scol;
+        nb.pval = sval;
+        TSG_TRY(launch_num_cta<0>(c, bl, nb));
+        TSG_TRY(launch_num_cta<1>(c, bl, nb));
+        TSG_TRY(launch_num_global(c, bl, nb));
+    }
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_free(c, scol));
+    TSG_TRY(tsg_free(c, sval));
+    TSG_TRY(tsg_free(c, bl.list));
+    TSG_TRY(tsg_free(c, sbound));
+    TSG_TRY(tsg_free(c, bins));
     return TSG_OK;
 }
 
