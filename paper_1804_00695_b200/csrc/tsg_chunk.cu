@@ -21,6 +21,7 @@
 // widened on the device, so physical PCIe bytes equal the ledger's byte
 // convention (csr.py:65-67).
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -46,7 +47,7 @@ __global__ void k_narrow(const int64_t *__restrict__ in, int32_t *__restrict__ o
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t v = in[i];
-        if (v < 0 || v >= ncols) {
+        if (ncols >= 0 && (v < 0 || v >= ncols)) {   // ncols < 0: unchecked (stale tails)
             kerr(err, KERR_COLRANGE, i);
             v = 0;
         }
@@ -99,7 +100,8 @@ int ensure(tsg_ctx *c, DevRange &d, int64_t rows, int64_t nnz, bool values) {
         TSG_TRY(tsg_alloc_t(c, &d.m.rp, d.cap_rows + 2));
         TSG_TRY(tsg_alloc_t(c, &d.m.col, d.cap_nnz + 1));
         if (values) TSG_TRY(tsg_alloc_t(c, &d.m.val, d.cap_nnz + 1));
-        TSG_TRY(tsg_alloc_t(c, &d.stage, d.cap_nnz + 2));
+        // staging carries the row pointers (rows + 1) or the int64 columns
+        TSG_TRY(tsg_alloc_t(c, &d.stage, (d.cap_nnz > d.cap_rows ? d.cap_nnz : d.cap_rows) + 2));
     }
     if (!d.ready) TSG_CK(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
     return TSG_OK;
@@ -121,6 +123,9 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
     TSG_TRY(ensure(c, d, rows, nnz, h.val != nullptr));
     cudaStream_t s = c->copy_in;
+    // buffers come from the compute-stream-ordered arena: order the copy stream after it
+    TSG_CK(cudaEventRecord(d.ready, c->stream));
+    TSG_CK(cudaStreamWaitEvent(s, d.ready, 0));
     if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
     // row pointers: staged through the int64 buffer then rebased
     TSG_CK(cudaMemcpyAsync(d.stage, h.rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -134,6 +139,13 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     }
     TSG_CK(cudaGetLastError());
     TSG_CK(cudaEventRecord(d.ready, s));
+    if (tsg_trace_enabled()) {
+        cudaStreamSynchronize(s);
+        int eh[2];
+        cudaMemcpy(eh, c->d_err, sizeof(eh), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[tsg chunk] staged rows [%lld,%lld) nnz %lld ncols %lld err %d/%d\n",
+                (long long)lo, (long long)hi, (long long)nnz, (long long)h.cols, eh[0], eh[1]);
+    }
     d.m.rows = rows;
     d.m.cols = h.cols;
     d.m.nnz = nnz;
@@ -211,7 +223,9 @@ int open_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool load_partial) {
         TSG_CK(cudaMemcpyAsync(d.plen, J.h_plen + lo, rows * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         if (nnz > 0) {
             TSG_CK(cudaMemcpyAsync(d.stage, J.c_col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-            k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.col, nnz, J.B.cols,
+            // only each row's partial prefix (plen) is meaningful; the capacity
+            // tail is stale host memory and is never read, so no range check
+            k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.col, nnz, -1,
                                                                          c->d_err); ++c->launches;
             TSG_CK(cudaMemcpyAsync(d.val, J.c_val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
         }
