@@ -190,6 +190,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--phases", action="store_true", help="print per-phase device times and exit")
+    ap.add_argument("--config", type=int, default=2,
+                    help="BASELINE.json config (2 = the driver's bench line; 1, 3, 4 = secondary)")
+    ap.add_argument("--scale", type=int, default=22, help="R-MAT scale for --config 3")
+    ap.add_argument("--grid", type=int, default=256, help="brick grid edge for --config 4")
+    ap.add_argument("--hbm-cap-gib", type=float, default=8.0, help="HBM budget for --config 4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -207,6 +212,10 @@ def main():
         run_reference(args, world, rank)
         if dist:
             dist.destroy_process_group()
+        return
+    if args.config != 2:
+        import bench_configs
+        print(json.dumps(bench_configs.run(args)), flush=True)
         return
 
     import torch
