@@ -363,44 +363,24 @@ def main():
 
 def exchange_offsets(local_nnz, torch, dist, world):
     """Row-pointer offset exchange: all-gather of per-rank nnz(C slice)."""
-    t = torch.tensor([local_nnz], dtype=torch.int64, device="cuda")
-    out = torch.empty(world, dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(out, t)
-    return torch.cumsum(out, 0) - out
+    from paper_1804_00695_b200 import distributed as D
+    return D.exchange_offsets(local_nnz, dist, "cuda")
 
 
 def replicate_b(ctx, a_loc, dims, world, rank, torch, dist):
     """NCCL all-gather of the fine operator's row shards into a full device B."""
     from paper_1804_00695_b200 import _lib
+    from paper_1804_00695_b200 import distributed as D
     t0 = time.perf_counter()
-    rows = a_loc.num_rows
-    nnz = torch.tensor([a_loc.nnz], dtype=torch.int64, device="cuda")
-    all_nnz = torch.empty(world, dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(all_nnz, nnz)
-    nn = all_nnz.cpu().numpy()
-    cap = int(nn.max())
-    col = torch.zeros(cap, dtype=torch.int32, device="cuda")
-    val = torch.zeros(cap, dtype=torch.float64, device="cuda")
-    col[:a_loc.nnz] = torch.from_numpy(a_loc.col_idx.astype(np.int32)).cuda()
-    val[:a_loc.nnz] = torch.from_numpy(np.asarray(a_loc.values)).cuda()
-    cnt = torch.from_numpy(np.diff(a_loc.row_ptr)).cuda()
-    g_col = torch.empty(world * cap, dtype=torch.int32, device="cuda")
-    g_val = torch.empty(world * cap, dtype=torch.float64, device="cuda")
-    g_cnt = torch.empty(world * rows, dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(g_col, col)
-    dist.all_gather_into_tensor(g_val, val)
-    dist.all_gather_into_tensor(g_cnt, cnt)
-    keep = torch.cat([torch.arange(k * cap, k * cap + int(nn[k]), device="cuda") for k in range(world)])
-    f_col = g_col[keep].contiguous()
-    f_val = g_val[keep].contiguous()
-    f_rp = torch.zeros(world * rows + 1, dtype=torch.int64, device="cuda")
-    f_rp[1:] = torch.cumsum(g_cnt, 0)
+    rp, col, val = D.allgather_csr(torch.from_numpy(np.diff(a_loc.row_ptr)).cuda(),
+                                   torch.from_numpy(a_loc.col_idx.astype(np.int32)).cuda(),
+                                   torch.from_numpy(np.asarray(a_loc.values)).cuda(), dist, "cuda")
     torch.cuda.synchronize()
-    n_full = world * rows
-    da = _lib.DeviceCsr.from_device(ctx, n_full, n_full, int(f_col.numel()), f_rp.data_ptr(),
-                                    f_col.data_ptr(), f_val.data_ptr())
+    n_full = rp.numel() - 1
+    da = _lib.DeviceCsr.from_device(ctx, n_full, a_loc.num_cols, int(col.numel()), rp.data_ptr(),
+                                    col.data_ptr(), val.data_ptr())
     return da, {"b_allgather_s": time.perf_counter() - t0,
-                "b_bytes_per_rank": int(8 * (rows + 1) + 12 * a_loc.nnz)}
+                "b_bytes_per_rank": int(8 * (a_loc.num_rows + 1) + 12 * a_loc.nnz)}
 
 
 def run_e2e(ctx, r, a, p, args):
