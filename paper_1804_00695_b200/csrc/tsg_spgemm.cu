@@ -137,175 +137,6 @@ __global__ void k_row_bounds(int64_t rows, const int64_t *__restrict__ arp,
     }
 }
 
-// ======================================================================= K1
-
-// Sorted (non-decreasing set) rows: run-length encode in one pass.  Rows whose
-// sets go down somewhere are flagged (cnt = -1) for the first-touch slow path.
-template <int G>
-__global__ void k_compress(int64_t rows, const int64_t *__restrict__ rp,
-                           const int32_t *__restrict__ col, int32_t *__restrict__ cnt,
-                           int32_t *__restrict__ oset, uint64_t *__restrict__ obits,
-                           int *n_unsorted, int32_t *unsorted) {
-    const unsigned gm = group_mask<G>();
-    const int glane = threadIdx.x & (G - 1);
-    const unsigned lt = lanemask_lt();
-    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
-    for (int64_t i = gid; i < rows; i += ngroups) {
-        const int64_t r0 = rp[i], r1 = rp[i + 1];
-        int carry = 0;
-        int prev = -1;
-        bool bad = false;
-        for (int64_t base = r0; base < r1; base += G) {
-            int64_t t = base + glane;
-            bool valid = t < r1;
-            int c = valid ? col[t] : 0;
-            int s = c >> 6;
-            int ps = __shfl_up_sync(gm, s, 1, G);
-            if (glane == 0) ps = prev;
-            bool head = valid && (t == r0 || s != ps);
-            bool down = valid && t > r0 && s < ps;
-            if (__ballot_sync(gm, down) & gm) {
-                bad = true;
-                break;
-            }
-            unsigned hb = __ballot_sync(gm, head) & gm;
-            if (head) {
-                uint64_t bits = 0;
-                for (int64_t q = t; q < r1; ++q) {
-                    int cq = col[q];
-                    if ((cq >> 6) != s) break;
-                    bits |= 1ull << (cq & 63);
-                }
-                int64_t pos = r0 + carry + __popc(hb & lt);
-                oset[pos] = s;
-                obits[pos] = bits;
-            }
-            carry += __popc(hb);
-            prev = __shfl_sync(gm, s, G - 1, G);
-        }
-        if (glane == 0) {
-            if (bad) {
-                cnt[i] = -1;
-                int slot = atomicAdd(n_unsorted, 1);
-                unsorted[slot] = (int32_t)i;
-            } else {
-                cnt[i] = carry;
-            }
-        }
-    }
-}
-
-// Tiled compression for short rows: a CTA stages the column indices of CT_ROWS
-// consecutive rows (one contiguous range of B) in shared memory with
-// coalesced loads, each thread run-length encodes one row from shared memory
-// (stride = row length, conflict-free for odd lengths), and the tile's output
-// range [rp[r0], rp[r0 + CT_ROWS]) of the padded layout is written back
-// coalesced (holes included; they are never read).  Tiles whose entries
-// exceed the staging buffer fall back to per-thread global reads.
-constexpr int CT_ROWS = 128;
-constexpr int CT_CAP = 6144;   // staged column indices per tile (24 KB)
-
-__global__ void __launch_bounds__(CT_ROWS) k_compress_tiled(
-    int64_t rows, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-    int32_t *__restrict__ cnt, int32_t *__restrict__ oset, uint64_t *__restrict__ obits,
-    int *n_unsorted, int32_t *unsorted) {
-    __shared__ int32_t s_col[CT_CAP];
-    for (int64_t r0 = (int64_t)blockIdx.x * CT_ROWS; r0 < rows; r0 += (int64_t)gridDim.x * CT_ROWS) {
-        const int64_t r1 = r0 + CT_ROWS < rows ? r0 + CT_ROWS : rows;
-        const int64_t e0 = rp[r0], e1 = rp[r1];
-        const bool staged = (e1 - e0) <= CT_CAP;
-        if (staged)
-            for (int64_t q = e0 + threadIdx.x; q < e1; q += CT_ROWS) s_col[q - e0] = col[q];
-        __syncthreads();
-        const int64_t i = r0 + threadIdx.x;
-        if (i < r1) {
-            const int64_t lo = rp[i], hi = rp[i + 1];
-            int prev = -1, k = 0;
-            uint64_t bits = 0;
-            bool bad = false;
-            for (int64_t q = lo; q < hi; ++q) {
-                int c = staged ? s_col[q - e0] : col[q];
-                int sv = c >> 6;
-                if (sv != prev) {
-                    if (sv < prev) bad = true;
-                    if (prev >= 0) {
-                        oset[lo + k] = prev;
-                        obits[lo + k] = bits;
-                        ++k;
-                    }
-                    prev = sv;
-                    bits = 0;
-                }
-                bits |= 1ull << (c & 63);
-            }
-            if (prev >= 0) {
-                oset[lo + k] = prev;
-                obits[lo + k] = bits;
-                ++k;
-            }
-            if (bad) {
-                cnt[i] = -1;
-                unsorted[atomicAdd(n_unsorted, 1)] = (int32_t)i;
-            } else {
-                cnt[i] = k;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// First-touch compression of unsorted rows: entry t heads its set if no
-// earlier entry of the row has the same set (the reference's dict order).
-template <int NT>
-__global__ void k_compress_unsorted(const int *n_unsorted, const int32_t *__restrict__ list,
-                                    const int64_t *__restrict__ rp,
-                                    const int32_t *__restrict__ col, int32_t *__restrict__ cnt,
-                                    int32_t *__restrict__ oset, uint64_t *__restrict__ obits) {
-    __shared__ int s_warp[NT / 32];
-    __shared__ int s_carry;
-    const int nrow = *n_unsorted;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    for (int li = blockIdx.x; li < nrow; li += gridDim.x) {
-        const int64_t i = list[li];
-        const int64_t r0 = rp[i], r1 = rp[i + 1];
-        if (tid == 0) s_carry = 0;
-        __syncthreads();
-        for (int64_t base = r0; base < r1; base += NT) {
-            int64_t t = base + tid;
-            bool head = t < r1;
-            int s = head ? (col[t] >> 6) : -1;
-            for (int64_t q = r0; head && q < t; ++q)
-                if ((col[q] >> 6) == s) head = false;
-            uint64_t bits = 0;
-            if (head)
-                for (int64_t q = t; q < r1; ++q) {
-                    int cq = col[q];
-                    if ((cq >> 6) == s) bits |= 1ull << (cq & 63);
-                }
-            unsigned hb = __ballot_sync(0xffffffffu, head);
-            if (lane == 0) s_warp[w] = __popc(hb);
-            __syncthreads();
-            int before = s_carry;
-            for (int j = 0; j < w; j++) before += s_warp[j];
-            if (head) {
-                int64_t pos = r0 + before + __popc(hb & lanemask_lt());
-                oset[pos] = s;
-                obits[pos] = bits;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                int tot = 0;
-                for (int j = 0; j < NT / 32; j++) tot += s_warp[j];
-                s_carry += tot;
-            }
-            __syncthreads();
-        }
-        if (tid == 0) cnt[i] = s_carry;
-        __syncthreads();
-    }
-}
-
 // ======================================================================= bins
 // Tier sizes.  Thread-group tier: a G-lane group owns a SLICE-byte region of
 // shared memory (table + dense values).  CTA tier: one row per CTA, table in
@@ -1291,13 +1122,6 @@ void launch_bounds(tsg_ctx *c, const tsg_csr *a, const int64_t *brp, const int32
     }
 }
 
-template <int G>
-void launch_compress_g(tsg_ctx *c, const tsg_csr *b, tsg_cmat *cm, int *n_unsorted,
-                       int32_t *unsorted) {
-    unsigned grid = grid_for(b->rows, 256 / G, c->num_sms * 32);
-    k_compress<G><<<grid, 256, 0, c->stream>>>(b->rows, b->rp, b->col, cm->cnt, cm->set, cm->bits,
-                                               n_unsorted, unsorted); ++c->launches;
-}
 
 }  // namespace
 
@@ -1307,40 +1131,7 @@ int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_r
                      int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
                      const int64_t *prp, int64_t *sbound);
 
-int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
-    tsg_cmat *cm = nullptr;
-    TSG_TRY(tsg_cmat_alloc(c, b->rows, b->nnz > 0 ? b->nnz : 1, &cm));
-    TSG_CK(cudaMemcpyAsync(cm->start, b->rp, (b->rows + 1) * sizeof(int64_t),
-                           cudaMemcpyDeviceToDevice, c->stream));
-    if (b->rows > 0) {
-        int *n_uns = reinterpret_cast<int *>(c->d_small + 8);
-        int32_t *uns = nullptr;
-        TSG_TRY(tsg_alloc_t(c, &uns, b->rows));
-        TSG_CK(cudaMemsetAsync(n_uns, 0, sizeof(int), c->stream));
-        double avg = (double)b->nnz / (double)b->rows;
-        if (avg <= 40.0) {
-            unsigned grid = grid_for(b->rows, CT_ROWS, c->num_sms * 16);
-            k_compress_tiled<<<grid, CT_ROWS, 0, c->stream>>>(b->rows, b->rp, b->col, cm->cnt,
-                                                              cm->set, cm->bits, n_uns, uns); ++c->launches;
-            TSG_TRY(tsg_launch_check("k_compress_tiled", -1, grid, CT_ROWS, 0));
-        } else {
-            switch (pick_g(b->nnz, b->rows)) {
-            case 4: launch_compress_g<4>(c, b, cm, n_uns, uns); break;
-            case 8: launch_compress_g<8>(c, b, cm, n_uns, uns); break;
-            case 16: launch_compress_g<16>(c, b, cm, n_uns, uns); break;
-            default: launch_compress_g<32>(c, b, cm, n_uns, uns); break;
-            }
-        }
-        // slow path launches unconditionally; it exits at once when no row is unsorted
-        tsg_trace(c, "compress:kernel", b->rows);
-        k_compress_unsorted<256><<<c->num_sms * 2, 256, 0, c->stream>>>(n_uns, uns, b->rp, b->col,
-                                                                       cm->cnt, cm->set, cm->bits); ++c->launches;
-        TSG_CK(cudaGetLastError());
-        TSG_TRY(tsg_free(c, uns));
-    }
-    *out = cm;
-    return TSG_OK;
-}
+int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out);   // tsg_compress.cu
 
 // counts (+ msets) of A * B for output rows [0, rows_out); fused mode when
 // prp != null or a_row_off/b range given.
