@@ -322,12 +322,19 @@ def main():
         (8 * (ra_rows + 1) + 12 * ra_nnz)
     num_ms = statistics.median(num_times)
     achieved = alg_bytes / (num_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            traffic = int(json.load(fh)["traffic_bytes_per_launch"])
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None,
+            "frac": achieved / hbm, "traffic": traffic,
             "kernel": "k_num_group (numeric phase of R*A, all bins)",
             "peak_kind": peak_kind, "algorithmic_bytes": alg_bytes,
             "device_layout_bytes": dev_bytes, "kernel_ms": num_ms,
-            "note": "traffic: see profiles/ (ncu dram__bytes per launch)"}
+            "note": "traffic = dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch "
+                    "from one ncu --set full capture (profiles/r01_traffic.json)"}
     whole_bytes_ms = tot_ms / args.steps
 
     line = {
@@ -419,7 +426,9 @@ def run_e2e(ctx, r, a, p, args):
         times.append(ms)
     fl = 2 * (kernel.count_multiplications(r, a) + ra.nnz)
     ms = statistics.median(times)
-    h2d = sum(8 * (m.num_rows + 1) + 16 * m.nnz for m in (r, a, ra, p))
+    # RA comes back from the first multiply with its device copy kept, so the
+    # second multiply does not upload it again
+    h2d = sum(8 * (m.num_rows + 1) + 16 * m.nnz for m in (r, a, p))
     d2h = sum(8 * (m.num_rows + 1) + 16 * m.nnz for m in (ra, rap))
     return {"value": fl / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,

@@ -382,6 +382,59 @@ __device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, 
     __syncwarp(gm);
 }
 
+// One A entry's B-row batch for products_seq: the first BB_UF*G entries of
+// the row, loaded together so their DRAM latencies overlap.
+constexpr int BB_UF = 4;
+struct BBatch {
+    int c[BB_UF];
+    double v[BB_UF];
+};
+
+template <int G>
+__device__ __forceinline__ BBatch bbatch_issue(unsigned gm, int glane, const NumArgs &a, int64_t st,
+                                               int len, int j, int cnt) {
+    BBatch b;
+    const int jj = j < cnt ? j : 0;
+    const int64_t sj = __shfl_sync(gm, st, jj, G);
+    const int lj = j < cnt ? __shfl_sync(gm, len, jj, G) : 0;
+#pragma unroll
+    for (int u = 0; u < BB_UF; ++u) {
+        const int q = u * G + glane;
+        b.c[u] = q < lj ? a.bcol[sj + q] : 0;
+        b.v[u] = q < lj ? a.bval[sj + q] : 0.0;
+    }
+    return b;
+}
+
+template <int G>
+__device__ __forceinline__ void bbatch_accumulate(unsigned gm, int glane, const NumArgs &a, int64_t st,
+                                                  int len, double av, int j, const BBatch &b,
+                                                  const int4 *tbl, int T, int logT, double *vals) {
+    const int64_t sj = __shfl_sync(gm, st, j, G);
+    const int lj = __shfl_sync(gm, len, j, G);
+    const double aj = __shfl_sync(gm, av, j, G);
+#pragma unroll
+    for (int u = 0; u < BB_UF; ++u) {
+        if (u * G + glane < lj) {
+            const int c = b.c[u];
+            const double prod = __dmul_rn(aj, b.v[u]);
+            int4 e;
+            tbl_find(tbl, T, logT, c >> 6, e);
+            const int pos = e.w + mask_rank(e, c & 63);
+            vals[pos] = __dadd_rn(vals[pos], prod);
+        }
+    }
+    for (int q = BB_UF * G + glane; q < lj; q += G) {   // long B rows: remainder
+        const int c = a.bcol[sj + q];
+        const double prod = __dmul_rn(aj, a.bval[sj + q]);
+        int4 e;
+        tbl_find(tbl, T, logT, c >> 6, e);
+        const int pos = e.w + mask_rank(e, c & 63);
+        vals[pos] = __dadd_rn(vals[pos], prod);
+    }
+    __syncwarp(gm);
+}
+
 // Product phase, sequential mode (B rows at least ~G/2 long): A entries are
 // taken one at a time in storage order and the G lanes split that entry's B
 // row.  A B row has distinct columns, so lanes never collide within a step
@@ -406,19 +459,16 @@ __device__ __forceinline__ void products_seq(unsigned gm, int glane, const NumAr
             }
         }
         const int cnt = (int)((a1 - base) < G ? (a1 - base) : G);
-        for (int j = 0; j < cnt; ++j) {
-            int64_t sj = __shfl_sync(gm, st, j, G);
-            int lj = __shfl_sync(gm, len, j, G);
-            double aj = __shfl_sync(gm, av, j, G);
-            for (int q = glane; q < lj; q += G) {
-                int c = a.bcol[sj + q];
-                double prod = __dmul_rn(aj, a.bval[sj + q]);
-                int4 e;
-                tbl_find(tbl, T, logT, c >> 6, e);
-                int pos = e.w + mask_rank(e, c & 63);
-                vals[pos] = __dadd_rn(vals[pos], prod);
-            }
-            __syncwarp(gm);
+        // Memory-level parallelism: the first UF*G entries of A entry j's B row
+        // are loaded in one batch, and entry j+1's batch is issued before entry
+        // j is accumulated, so a row costs ~1 DRAM round trip per A chunk
+        // instead of one per (entry, G-slice).
+        BBatch bx = bbatch_issue<G>(gm, glane, a, st, len, 0, cnt);
+        for (int j = 0; j < cnt; j += 2) {
+            BBatch by = bbatch_issue<G>(gm, glane, a, st, len, j + 1, cnt);
+            bbatch_accumulate<G>(gm, glane, a, st, len, av, j, bx, tbl, T, logT, vals);
+            bx = bbatch_issue<G>(gm, glane, a, st, len, j + 2, cnt);
+            if (j + 1 < cnt) bbatch_accumulate<G>(gm, glane, a, st, len, av, j + 1, by, tbl, T, logT, vals);
         }
     }
 }

@@ -129,6 +129,30 @@ def _on_device(m) -> "_lib.DeviceCsr":
     return d
 
 
+# results keep their device copy (bounded), so a product fed straight back as
+# an operand -- RA in R*A*P -- is not uploaded again
+_RESULT_CACHE_BYTES = 32 << 30
+_result_bytes = [0]
+
+
+def _keep_result(host, dev):
+    nbytes = 8 * (dev.num_rows + 1) + 12 * dev.nnz
+    if _result_bytes[0] + nbytes > _RESULT_CACHE_BYTES:
+        return host
+    try:
+        k = _key(host)
+        _resident[id(host)] = (k, dev)
+        _result_bytes[0] += nbytes
+
+        def _drop(i=id(host), n=nbytes):
+            _resident.pop(i, None)
+            _result_bytes[0] -= n
+        weakref.finalize(host, _drop)
+    except TypeError:
+        pass
+    return host
+
+
 def _counts_on_device(counts: np.ndarray) -> "_lib.DeviceVec":
     dv = getattr(counts, "_tsg_dev", None)
     snap = getattr(counts, "_tsg_snap", None)
@@ -186,7 +210,8 @@ def spgemm_numeric(a, b, c_counts, workers: int = 1) -> CsrMatrix:
     if counts.ndim != 1 or counts.shape[0] != a.num_rows:
         raise DimensionError("c_counts length must equal A's row count")
     dv = _counts_on_device(c_counts if isinstance(c_counts, _Counts) else counts)
-    return _lib.d_numeric(_on_device(a), _on_device(b), None, dv).download()
+    dc = _lib.d_numeric(_on_device(a), _on_device(b), None, dv)
+    return _keep_result(dc.download(), dc)
 
 
 def spgemm_numeric_fused(a, b_chunk, c_partial, a_rows: RowRange, b_rows: RowRange,
@@ -208,7 +233,7 @@ def spgemm_numeric_fused(a, b_chunk, c_partial, a_rows: RowRange, b_rows: RowRan
         raise MatrixValidationError("fused multiply requires numeric operands")
     out = _lib.d_numeric_fused(_on_device(a), _on_device(b_chunk), _on_device(c_partial),
                                a_rows.begin, a_rows.end, b_rows.begin, b_rows.end)
-    return out.download()
+    return _keep_result(out.download(), out)
 
 
 def multiply(a, b, workers: int = 1) -> CsrMatrix:
@@ -217,7 +242,8 @@ def multiply(a, b, workers: int = 1) -> CsrMatrix:
         raise DimensionError("A has %d cols but compressed B has %d rows" % (a.num_cols, b.num_rows))
     if b.values is None or a.values is None:
         raise MatrixValidationError("numeric multiply requires values on both operands")
-    return _lib.d_multiply(_on_device(a), _on_device(b)).download()
+    dc = _lib.d_multiply(_on_device(a), _on_device(b))
+    return _keep_result(dc.download(), dc)
 
 
 def masked_row_intersect_count(l, cl, workers: int = 1) -> int:
