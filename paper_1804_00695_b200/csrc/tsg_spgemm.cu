@@ -53,9 +53,11 @@ struct SymArgs {
     const int64_t *sptr;
     int32_t *oset;
     uint64_t *obits;
+    const int *unit_b;   // device flag: every compressed B row has <= 1 set
 };
 
 constexpr int SETS_WRITTEN = 1 << 30;
+constexpr int UB = 4;   // A chunks whose loads are batched on the unit-row paths
 
 struct NumArgs {
     const int64_t *arp;
@@ -90,6 +92,7 @@ struct NumArgs {
     const int64_t *pstart;
     const int32_t *plen_in;
     int32_t *plen_out;
+    const int *unit_b;   // device flag: every B row has <= 1 entry
 };
 
 __device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
@@ -178,6 +181,19 @@ __device__ __forceinline__ int num_bin(int64_t n, int64_t m) {
     for (int b = 0; b < 2; b++)
         if (T <= ct_slots(b)) return 7 + b;
     return BIN_GLOBAL;
+}
+
+// flag = 1 iff every row of the (row_ptr or count) array holds <= 1 entry
+__global__ void k_unit_rows(int64_t rows, const int64_t *__restrict__ rp, const int32_t *__restrict__ cnt,
+                            int *flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = rp ? rp[i + 1] - rp[i] : cnt[i];
+        if (len > 1) {
+            *flag = 0;
+            return;
+        }
+    }
 }
 
 __global__ void k_sym_bins(int64_t rows, const int64_t *__restrict__ sbound, uint8_t *bins,
@@ -271,22 +287,51 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                              bit >= 32 ? 1u << (bit - 32) : 0u);
             }
         }
-        group_enumerate_any<G>(
-            gm, glane, a.arp[gi], a.arp[gi + 1],
-            [&](int64_t t, int64_t &st, int &len) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    st = a.cbstart[k];
-                    len = a.cbcnt[k];
+        if (a.unit_b && *a.unit_b) {
+            // unit compressed rows: batch the three dependent load rounds of UB chunks
+            const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+            for (int64_t base = a0; base < a1; base += UB * G) {
+                int kk[UB];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int64_t t = base + u * G + glane;
+                    const int k = t < a1 ? a.acol[t] : -1;
+                    kk[u] = (k >= a.b_lo && k < a.b_hi) ? k - a.b_lo : -1;
                 }
-            },
-            [&](bool valid, int, int64_t, int64_t s) {
-                if (valid) {
-                    uint64_t bits = a.cbbits[s];
-                    ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                int64_t ss[UB];
+                bool has[UB];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    ss[u] = kk[u] >= 0 ? a.cbstart[kk[u]] : 0;
+                    has[u] = kk[u] >= 0 && a.cbcnt[kk[u]] > 0;
                 }
-            });
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    if (has[u]) {
+                        const uint64_t bits = a.cbbits[ss[u]];
+                        ok &= tbl_or(tbl, T, logT, a.cbset[ss[u]], (unsigned)bits,
+                                     (unsigned)(bits >> 32));
+                    }
+                }
+            }
+        } else {
+            group_enumerate_any<G>(
+                gm, glane, a.arp[gi], a.arp[gi + 1],
+                [&](int64_t t, int64_t &st, int &len) {
+                    int k = a.acol[t];
+                    if (k >= a.b_lo && k < a.b_hi) {
+                        k -= a.b_lo;
+                        st = a.cbstart[k];
+                        len = a.cbcnt[k];
+                    }
+                },
+                [&](bool valid, int, int64_t, int64_t s) {
+                    if (valid) {
+                        uint64_t bits = a.cbbits[s];
+                        ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                    }
+                });
+        }
         __syncwarp(gm);
         // compact occupied slots as sortable (key << 32 | slot) into the scratch
         // area behind the table; count columns on the way
@@ -473,6 +518,53 @@ __device__ __forceinline__ void products_seq(unsigned gm, int glane, const NumAr
     }
 }
 
+// Product phase for unit B rows (every B row has <= 1 entry, e.g. the
+// aggregation prolongator): lane j of a chunk owns A entry t = base + j and its
+// single product.  UB chunks are loaded together -- the three dependent
+// rounds (A column -> B row pointer -> B entry) are paid once per UB*G A
+// entries -- then accumulated chunk by chunk in order with the ordered add.
+template <int G>
+__device__ __forceinline__ void products_unit(unsigned gm, int glane, const NumArgs &a, int64_t a0,
+                                              int64_t a1, const int4 *tbl, int T, int logT,
+                                              double *vals) {
+    for (int64_t base = a0; base < a1; base += UB * G) {
+        int kk[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int64_t t = base + u * G + glane;
+            kk[u] = t < a1 ? a.acol[t] : -1;
+        }
+        int64_t ss[UB];
+        bool has[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int k = kk[u];
+            const bool in = k >= a.b_lo && k < a.b_hi;
+            ss[u] = in ? a.brp[k - a.b_lo] : 0;
+            has[u] = in && a.brp[k - a.b_lo + 1] > ss[u];
+        }
+        int cc[UB];
+        double pp[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int64_t t = base + u * G + glane;
+            cc[u] = has[u] ? a.bcol[ss[u]] : 0;
+            pp[u] = has[u] ? __dmul_rn(a.aval[t], a.bval[ss[u]]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            if (base + u * G >= a1) break;   // group-uniform
+            int pos = -1;
+            if (has[u]) {
+                int4 e;
+                tbl_find(tbl, T, logT, cc[u] >> 6, e);
+                pos = e.w + mask_rank(e, cc[u] & 63);
+            }
+            ordered_add<G>(gm, vals, pos, pp[u]);
+        }
+    }
+}
+
 template <int G, int SLICE, bool SEQ>
 __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
@@ -639,6 +731,8 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         __syncwarp(gm);
         if constexpr (SEQ) {
             products_seq<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
+        } else if (a.unit_b && *a.unit_b) {
+            products_unit<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
         } else {
             group_enumerate<G>(
                 gm, glane, a0, a1,
@@ -1235,6 +1329,11 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.sptr = v->sptr;
         sa.oset = v->sset;
         sa.obits = v->sbits;
+        int *uflag = reinterpret_cast<int *>(c->d_small + 48);
+        TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));   // nonzero = unit until disproved
+        k_unit_rows<<<grid_for(cb->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(cb->rows, nullptr,
+                                                                                  cb->cnt, uflag); ++c->launches;
+        sa.unit_b = uflag;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
@@ -1350,6 +1449,11 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.sptr = counts->sptr;
         na.sset = counts->sset;
         na.sbits = counts->sbits;
+        int *uflag = reinterpret_cast<int *>(c->d_small + 49);
+        TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));
+        k_unit_rows<<<grid_for(b->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(b->rows, b->rp, nullptr,
+                                                                                 uflag); ++c->launches;
+        na.unit_b = uflag;
         na.pstart = nullptr;
         na.plen_in = nullptr;
         na.plen_out = nullptr;
