@@ -260,6 +260,93 @@ __global__ void k_bin_scatter(int64_t rows, const uint8_t *__restrict__ bins, in
 
 // ======================================================================= K2 group tier
 
+// Union of the row's compressed B rows into the table, order-free.  Per
+// chunk of A entries it takes the cheaper of (a) a fixed mapping -- each A
+// entry gets L = G / pow2(entries) lanes striding its compressed row, with
+// up to SF strides of (set, mask) loads issued together before any insert
+// -- and (b) the flattened mapping of group_enumerate (skewed rows).
+constexpr int SF = 4;
+
+template <int G>
+__device__ __forceinline__ bool union_rows(unsigned gm, int glane, int64_t a0, int64_t a1,
+                                           const int32_t *__restrict__ acol, int32_t b_lo,
+                                           int32_t b_hi, const int64_t *__restrict__ cbstart,
+                                           const int32_t *__restrict__ cbcnt,
+                                           const int32_t *__restrict__ cbset,
+                                           const uint64_t *__restrict__ cbbits, int4 *tbl, int T,
+                                           int logT) {
+    bool ok = true;
+    for (int64_t base = a0; base < a1; base += G) {
+        const int64_t t = base + glane;
+        int64_t st = 0;
+        int len = 0;
+        if (t < a1) {
+            int k = acol[t];
+            if (k >= b_lo && k < b_hi) {
+                st = cbstart[k - b_lo];
+                len = cbcnt[k - b_lo];
+            }
+        }
+        int maxlen = len, total = len;
+#pragma unroll
+        for (int d = G / 2; d >= 1; d >>= 1) {
+            maxlen = max(maxlen, __shfl_xor_sync(gm, maxlen, d, G));
+            total += __shfl_xor_sync(gm, total, d, G);
+        }
+        const int ne = (int)((a1 - base) < G ? (a1 - base) : G);
+        const int lg_pe = ne <= 1 ? 0 : 32 - __clz(ne - 1);
+        const int lg_l = ilog2_pow2(G) - lg_pe;
+        const int steps = (maxlen + (1 << lg_l) - 1) >> lg_l;
+        if (steps <= 2 * ((total + G - 1) / G)) {
+            const int j = glane >> lg_l, sub = glane & ((1 << lg_l) - 1);
+            const int64_t sj = __shfl_sync(gm, st, j, G);
+            int lj = __shfl_sync(gm, len, j, G);
+            if (j >= ne) lj = 0;
+            // neighbouring A entries select near-identical B rows (stencils), so
+            // entry j starts its walk at offset j: lanes of one step then hit
+            // different sets instead of contending for the same slot
+            const int rot = lj > 0 ? j % lj : 0;
+            for (int s0 = 0; s0 < steps; s0 += SF) {
+                int key[SF];
+                uint64_t bits[SF];
+#pragma unroll
+                for (int u = 0; u < SF; ++u) {
+                    const int q = ((s0 + u) << lg_l) + sub;
+                    const bool v = q < lj;
+                    int qq = q + rot;
+                    if (qq >= lj) qq -= lj;
+                    key[u] = v ? cbset[sj + qq] : TSG_EMPTY;
+                    bits[u] = v ? cbbits[sj + qq] : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < SF; ++u)
+                    if (key[u] != TSG_EMPTY)
+                        ok &= tbl_or(tbl, T, logT, key[u], (unsigned)bits[u], (unsigned)(bits[u] >> 32));
+            }
+        } else {
+            const int incl = group_incl_scan<G, int>(gm, len, glane);
+            for (int p0 = 0; p0 < total; p0 += G) {
+                const int p = p0 + glane;
+                int j = 0;
+#pragma unroll
+                for (int step = G / 2; step >= 1; step >>= 1) {
+                    const int v = __shfl_sync(gm, incl, j + step - 1, G);
+                    if (v <= p) j += step;
+                }
+                const int inc_j = __shfl_sync(gm, incl, j, G);
+                const int len_j = __shfl_sync(gm, len, j, G);
+                const int64_t st_j = __shfl_sync(gm, st, j, G);
+                if (p < total) {
+                    const int64_t q = st_j + (p - (inc_j - len_j));
+                    const uint64_t b = cbbits[q];
+                    ok &= tbl_or(tbl, T, logT, cbset[q], (unsigned)b, (unsigned)(b >> 32));
+                }
+            }
+        }
+    }
+    return ok;
+}
+
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
@@ -315,22 +402,8 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                 }
             }
         } else {
-            group_enumerate_any<G>(
-                gm, glane, a.arp[gi], a.arp[gi + 1],
-                [&](int64_t t, int64_t &st, int &len) {
-                    int k = a.acol[t];
-                    if (k >= a.b_lo && k < a.b_hi) {
-                        k -= a.b_lo;
-                        st = a.cbstart[k];
-                        len = a.cbcnt[k];
-                    }
-                },
-                [&](bool valid, int, int64_t, int64_t s) {
-                    if (valid) {
-                        uint64_t bits = a.cbbits[s];
-                        ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
-                    }
-                });
+            ok &= union_rows<G>(gm, glane, a.arp[gi], a.arp[gi + 1], a.acol, a.b_lo, a.b_hi, a.cbstart,
+                                a.cbcnt, a.cbset, a.cbbits, tbl, T, logT);
         }
         __syncwarp(gm);
         // compact occupied slots as sortable (key << 32 | slot) into the scratch
