@@ -154,5 +154,34 @@ def config4(args):
                              "sample": "first 65536 rows of A times A (extrapolated rate)"}}
 
 
+def placement(args):
+    """The paper's data-placement table (Laplace R x A:
+    HBM / A_Pin / B_Pin / C_Pin / HostPin) on B200: config 2's R*A with each
+    operand either in HBM or in pinned, device-mapped host memory that the
+    kernels read/write in place over PCIe."""
+    import paper_1804_00695_b200 as tsg
+    from paper_1804_00695_b200 import _lib, generators as gen
+    from paper_1804_00695_b200.memory import PlacementPolicy
+    n = args.grid if args.grid != 256 else 128
+    a = gen.stencil(gen.BRICK3D, (n, n, n))
+    _, r = gen.aggregation((n, n, n))
+    mults = a.nnz   # R has one entry per column of A
+    out = {}
+    for name, spaces in (("HBM", "fff"), ("A_Pin", "sff"), ("B_Pin", "fsf"), ("C_Pin", "ffs"),
+                         ("HostPin", "sss")):
+        pol = PlacementPolicy(name, {k: ("fast" if v == "f" else "slow") for k, v in zip("ABC", spaces)})
+        tsg.multiply(r, a, placement=pol)          # warm-up (and operand placement)
+        times = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            tsg.multiply(r, a, placement=pol)
+            times.append(time.perf_counter() - t0)
+        out[name] = 2 * mults / statistics.median(times) / 1e9
+    return {"metric": "R*A GFLOP/s by operand placement (paper Table, PAPER.md:819)",
+            "unit": UNIT, "values": out, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "brick3d %d^3 R*A (2x2x2 aggregation), host wall time per call "
+                                   "incl. placement of slow operands and download of C" % n}}
+
+
 def run(args):
-    return {1: config1, 3: config3, 4: config4}[args.config](args)
+    return {1: config1, 3: config3, 4: config4, 6: placement}[args.config](args)

@@ -148,6 +148,18 @@ int tsg_numeric_fused(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b_chunk,
 int tsg_masked_count(tsg_ctx *ctx, const tsg_csr *l, const tsg_cmat *cl,
                      int64_t *total);
 
+/* ---- data placement (memory.py:193-223 PlacementPolicy; PAPER.md:600-625,
+   810-829).  A CSR whose arrays live in pinned, device-mapped HOST memory:
+   kernels read it in place over PCIe (the paper's "pinned" columns).  Columns
+   are narrowed to int32 on the host at mapping time. */
+int tsg_csr_map_host(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t *row_ptr, const int64_t *col_idx, const double *values,
+                     tsg_csr **out);
+/* multiply with C built in mapped host memory when c_in_host != 0 (operands
+   may be device or mapped-host CSRs: any placement of A, B and C). */
+int tsg_multiply_placed(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b, int c_in_host,
+                        tsg_csr **c);
+
 /* ---- chunked execution through an HBM budget (chunking.py:219-337) -------- */
 /* algo: 0 = KNL order (B streamed past all of A/C), 1 = GPU chunk1 (A/C row
    range in place, B streamed), 2 = GPU chunk2 (B range in place, A/C

@@ -43,7 +43,7 @@ EXPORTS = (
     "tsg_count_multiplications", "tsg_symbolic", "tsg_numeric", "tsg_multiply",
     "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
-    "tsg_chunk_multiply",
+    "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
 )
 
 _P = ctypes.c_void_p
@@ -90,6 +90,8 @@ _SIGS = {
     "tsg_csr_device_ptrs": ([_P, _PP, _PP, _PP], ctypes.c_int),
     "tsg_host_alloc": ([ctypes.c_size_t, _PP], ctypes.c_int),
     "tsg_host_free": ([_P], ctypes.c_int),
+    "tsg_csr_map_host": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
+    "tsg_multiply_placed": ([_P, _P, _P, ctypes.c_int, _PP], ctypes.c_int),
     "tsg_chunk_multiply": ([_P, ctypes.c_int, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
                             _P, _P, _P, _I64, _P, _I64, _P, _P], ctypes.c_int),
 }
@@ -265,6 +267,18 @@ class DeviceCsr(_Handle):
                                     _ptr(va), ctypes.byref(h)))
         return cls(ctx, h)
 
+    @classmethod
+    def map_host(cls, m, ctx=None):
+        """A CSR kept in pinned, device-mapped HOST memory (placement slow tier)."""
+        ctx = ctx or Context.get()
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(m.col_idx, dtype=np.int64)
+        va = None if m.values is None else np.ascontiguousarray(m.values, dtype=np.float64)
+        h = ctypes.c_void_p()
+        check(load().tsg_csr_map_host(ctx.h, m.num_rows, m.num_cols, ci.shape[0], _ptr(rp), _ptr(ci),
+                                      _ptr(va), ctypes.byref(h)))
+        return cls(ctx, h)
+
     def download(self) -> CsrMatrix:
         rp = pinned_empty(self.num_rows + 1, np.int64)
         ci = pinned_empty(self.nnz, np.int64)
@@ -374,6 +388,12 @@ def d_numeric(da, db, dcb, dcounts) -> DeviceCsr:
 def d_multiply(da, db) -> DeviceCsr:
     h = ctypes.c_void_p()
     check(load().tsg_multiply(da.ctx.h, da.h, db.h, ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)
+
+
+def d_multiply_placed(da, db, c_in_host: bool) -> DeviceCsr:
+    h = ctypes.c_void_p()
+    check(load().tsg_multiply_placed(da.ctx.h, da.h, db.h, 1 if c_in_host else 0, ctypes.byref(h)))
     return DeviceCsr(da.ctx, h)
 
 

@@ -691,6 +691,14 @@ extern "C" int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int6
 
 extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
                                 int64_t *col_idx, double *values) {
+    if (m->host_mapped) {   // already in host memory: widen on the host
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        if (row_ptr) memcpy(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t));
+        if (col_idx)
+            for (int64_t i = 0; i < m->nnz; ++i) col_idx[i] = m->col[i];
+        if (values && m->val) memcpy(values, m->val, m->nnz * sizeof(double));
+        return TSG_OK;
+    }
     if (row_ptr)
         TSG_CK(cudaMemcpyAsync(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, c->stream));
@@ -735,6 +743,57 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
     return TSG_OK;
 }
 
+// ---- placement: operands in pinned, device-mapped host memory -------------
+
+int tsg_csr_alloc_mapped(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz, bool values,
+                         tsg_csr **out) {
+    (void)c;
+    tsg_csr *m = new tsg_csr();
+    m->rows = rows;
+    m->cols = cols;
+    m->nnz = nnz;
+    m->host_mapped = 1;
+    const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+    cudaError_t e = cudaHostAlloc((void **)&m->rp, (rows + 1) * sizeof(int64_t), fl);
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&m->col, (nnz > 0 ? nnz : 1) * sizeof(int32_t), fl);
+    if (e == cudaSuccess && values) e = cudaHostAlloc((void **)&m->val, (nnz > 0 ? nnz : 1) * sizeof(double), fl);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeHost(m->rp);
+        cudaFreeHost(m->col);
+        cudaFreeHost(m->val);
+        delete m;
+        tsg_set_error("pinned mapped host allocation failed: %s", cudaGetErrorString(e));
+        return TSG_ECAPACITY;
+    }
+    *out = m;
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_map_host(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
+                                const int64_t *row_ptr, const int64_t *col_idx,
+                                const double *values, tsg_csr **out) {
+    if (cols > 0x7fffffffLL) {
+        tsg_set_error("%lld columns exceed the device int32 column index", (long long)cols);
+        return TSG_EDIM;
+    }
+    tsg_csr *m = nullptr;
+    TSG_TRY(tsg_csr_alloc_mapped(c, rows, cols, nnz, values != nullptr, &m));
+    memcpy(m->rp, row_ptr, (rows + 1) * sizeof(int64_t));
+    for (int64_t i = 0; i < nnz; ++i) {
+        int64_t v = col_idx[i];
+        if (v < 0 || v >= cols) {
+            tsg_csr_free(c, m);
+            tsg_set_error("column index out of range at entry %lld", (long long)i);
+            return TSG_EVALID;
+        }
+        m->col[i] = (int32_t)v;
+    }
+    if (values) memcpy(m->val, values, nnz * sizeof(double));
+    *out = m;
+    return TSG_OK;
+}
+
 extern "C" int tsg_csr_from_device(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
                                    const int64_t *d_rp, const int32_t *d_col, const double *d_val,
                                    tsg_csr **out) {
@@ -763,6 +822,14 @@ extern "C" int tsg_csr_device_ptrs(const tsg_csr *m, int64_t **rp, int32_t **col
 
 extern "C" int tsg_csr_free(tsg_ctx *c, tsg_csr *m) {
     if (!m) return TSG_OK;
+    if (m->host_mapped) {
+        cudaStreamSynchronize(c->stream);
+        cudaFreeHost(m->rp);
+        cudaFreeHost(m->col);
+        cudaFreeHost(m->val);
+        delete m;
+        return TSG_OK;
+    }
     tsg_free(c, m->rp);
     tsg_free(c, m->col);
     tsg_free(c, m->val);

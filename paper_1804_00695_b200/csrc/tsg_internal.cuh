@@ -39,6 +39,7 @@ struct tsg_ctx {
     cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
     cudaEvent_t ev_user[8];   // tsg_event_record slots
+    int c_host_out;           // tsg_multiply_placed: build C in mapped host memory
 };
 
 struct tsg_csr {
@@ -46,6 +47,7 @@ struct tsg_csr {
     int64_t *rp;
     int32_t *col;
     double *val;
+    int host_mapped;   // arrays live in pinned, device-mapped host memory (placement)
 };
 
 struct tsg_cmat {
@@ -123,6 +125,8 @@ int tsg_exclusive_scan_i64(tsg_ctx *ctx, const int64_t *in, int64_t *out, int64_
 int tsg_exclusive_scan_i32_to_i64(tsg_ctx *ctx, const int32_t *in, int64_t *out, int64_t n);
 
 // ---------------------------------------------------------------- objects
+int tsg_csr_alloc_mapped(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, bool values,
+                         tsg_csr **out);
 int tsg_csr_alloc(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, bool values,
                   tsg_csr **out);
 int tsg_vec_alloc(tsg_ctx *ctx, int64_t n, bool aux, tsg_vec **out);

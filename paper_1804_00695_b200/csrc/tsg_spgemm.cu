@@ -140,6 +140,44 @@ __global__ void k_row_bounds(int64_t rows, const int64_t *__restrict__ arp,
     }
 }
 
+__global__ void k_max_i32(int64_t n, const int32_t *__restrict__ v, int *out) {
+    int m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, v[i]);
+    for (int d = 16; d >= 1; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Symbolic set bound per A row.  When every compressed B row is short
+// (max <= CHEAP_CB) the bound len(A_i) * max needs no gather at all (exact
+// for aggregation operators, within ~10 % for stencils); skewed B falls back
+// to the exact sum of the selected compressed rows.
+constexpr int CHEAP_CB = 16;
+
+template <int G>
+__global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
+                             const int32_t *__restrict__ acol, const int32_t *__restrict__ cbcnt,
+                             const int *maxcb, int64_t *__restrict__ sbound) {
+    const int mcb = *maxcb;
+    if (mcb <= CHEAP_CB) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+             i += (int64_t)gridDim.x * blockDim.x)
+            sbound[i] = (arp[i + 1] - arp[i]) * (int64_t)mcb;
+        return;
+    }
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t i = gid; i < rows; i += ngroups) {
+        int64_t sb = 0;
+        for (int64_t t = arp[i] + glane; t < arp[i + 1]; t += G) sb += cbcnt[acol[t]];
+        sb = group_sum<G, int64_t>(gm, sb);
+        if (glane == 0) sbound[i] = sb;
+    }
+}
+
 // ======================================================================= bins
 // Tier sizes.  Thread-group tier: a G-lane group owns a SLICE-byte region of
 // shared memory (table + dense values).  CTA tier: one row per CTA, table in
@@ -260,93 +298,6 @@ __global__ void k_bin_scatter(int64_t rows, const uint8_t *__restrict__ bins, in
 
 // ======================================================================= K2 group tier
 
-// Union of the row's compressed B rows into the table, order-free.  Per
-// chunk of A entries it takes the cheaper of (a) a fixed mapping -- each A
-// entry gets L = G / pow2(entries) lanes striding its compressed row, with
-// up to SF strides of (set, mask) loads issued together before any insert
-// -- and (b) the flattened mapping of group_enumerate (skewed rows).
-constexpr int SF = 4;
-
-template <int G>
-__device__ __forceinline__ bool union_rows(unsigned gm, int glane, int64_t a0, int64_t a1,
-                                           const int32_t *__restrict__ acol, int32_t b_lo,
-                                           int32_t b_hi, const int64_t *__restrict__ cbstart,
-                                           const int32_t *__restrict__ cbcnt,
-                                           const int32_t *__restrict__ cbset,
-                                           const uint64_t *__restrict__ cbbits, int4 *tbl, int T,
-                                           int logT) {
-    bool ok = true;
-    for (int64_t base = a0; base < a1; base += G) {
-        const int64_t t = base + glane;
-        int64_t st = 0;
-        int len = 0;
-        if (t < a1) {
-            int k = acol[t];
-            if (k >= b_lo && k < b_hi) {
-                st = cbstart[k - b_lo];
-                len = cbcnt[k - b_lo];
-            }
-        }
-        int maxlen = len, total = len;
-#pragma unroll
-        for (int d = G / 2; d >= 1; d >>= 1) {
-            maxlen = max(maxlen, __shfl_xor_sync(gm, maxlen, d, G));
-            total += __shfl_xor_sync(gm, total, d, G);
-        }
-        const int ne = (int)((a1 - base) < G ? (a1 - base) : G);
-        const int lg_pe = ne <= 1 ? 0 : 32 - __clz(ne - 1);
-        const int lg_l = ilog2_pow2(G) - lg_pe;
-        const int steps = (maxlen + (1 << lg_l) - 1) >> lg_l;
-        if (steps <= 2 * ((total + G - 1) / G)) {
-            const int j = glane >> lg_l, sub = glane & ((1 << lg_l) - 1);
-            const int64_t sj = __shfl_sync(gm, st, j, G);
-            int lj = __shfl_sync(gm, len, j, G);
-            if (j >= ne) lj = 0;
-            // neighbouring A entries select near-identical B rows (stencils), so
-            // entry j starts its walk at offset j: lanes of one step then hit
-            // different sets instead of contending for the same slot
-            const int rot = lj > 0 ? j % lj : 0;
-            for (int s0 = 0; s0 < steps; s0 += SF) {
-                int key[SF];
-                uint64_t bits[SF];
-#pragma unroll
-                for (int u = 0; u < SF; ++u) {
-                    const int q = ((s0 + u) << lg_l) + sub;
-                    const bool v = q < lj;
-                    int qq = q + rot;
-                    if (qq >= lj) qq -= lj;
-                    key[u] = v ? cbset[sj + qq] : TSG_EMPTY;
-                    bits[u] = v ? cbbits[sj + qq] : 0ull;
-                }
-#pragma unroll
-                for (int u = 0; u < SF; ++u)
-                    if (key[u] != TSG_EMPTY)
-                        ok &= tbl_or(tbl, T, logT, key[u], (unsigned)bits[u], (unsigned)(bits[u] >> 32));
-            }
-        } else {
-            const int incl = group_incl_scan<G, int>(gm, len, glane);
-            for (int p0 = 0; p0 < total; p0 += G) {
-                const int p = p0 + glane;
-                int j = 0;
-#pragma unroll
-                for (int step = G / 2; step >= 1; step >>= 1) {
-                    const int v = __shfl_sync(gm, incl, j + step - 1, G);
-                    if (v <= p) j += step;
-                }
-                const int inc_j = __shfl_sync(gm, incl, j, G);
-                const int len_j = __shfl_sync(gm, len, j, G);
-                const int64_t st_j = __shfl_sync(gm, st, j, G);
-                if (p < total) {
-                    const int64_t q = st_j + (p - (inc_j - len_j));
-                    const uint64_t b = cbbits[q];
-                    ok &= tbl_or(tbl, T, logT, cbset[q], (unsigned)b, (unsigned)(b >> 32));
-                }
-            }
-        }
-    }
-    return ok;
-}
-
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
@@ -402,8 +353,22 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                 }
             }
         } else {
-            ok &= union_rows<G>(gm, glane, a.arp[gi], a.arp[gi + 1], a.acol, a.b_lo, a.b_hi, a.cbstart,
-                                a.cbcnt, a.cbset, a.cbbits, tbl, T, logT);
+            group_enumerate_any<G>(
+                gm, glane, a.arp[gi], a.arp[gi + 1],
+                [&](int64_t t, int64_t &st, int &len) {
+                    int k = a.acol[t];
+                    if (k >= a.b_lo && k < a.b_hi) {
+                        k -= a.b_lo;
+                        st = a.cbstart[k];
+                        len = a.cbcnt[k];
+                    }
+                },
+                [&](bool valid, int, int64_t, int64_t s) {
+                    if (valid) {
+                        uint64_t bits = a.cbbits[s];
+                        ok &= tbl_or(tbl, T, logT, a.cbset[s], (unsigned)bits, (unsigned)(bits >> 32));
+                    }
+                });
         }
         __syncwarp(gm);
         // compact occupied slots as sortable (key << 32 | slot) into the scratch
@@ -638,6 +603,25 @@ __device__ __forceinline__ void products_unit(unsigned gm, int glane, const NumA
     }
 }
 
+struct NumRowHdr {
+    int64_t i = 0, cp = 0, a0 = 0, a1 = 0, sp = 0, sb = 0;
+    int n = 0, mflag = 0;
+};
+
+__device__ __forceinline__ NumRowHdr num_row_hdr(const NumArgs &a, int64_t i) {
+    NumRowHdr h;
+    h.i = i;
+    const int64_t gi = i + a.a_row_off;
+    h.n = (int)a.counts[i];
+    h.cp = a.cptr[i];
+    h.a0 = a.arp[gi];
+    h.a1 = a.arp[gi + 1];
+    h.mflag = a.msets ? a.msets[i] : 0;
+    h.sp = a.sptr ? a.sptr[i] : 0;
+    h.sb = a.msets ? 0 : a.sbound[i];
+    return h;
+}
+
 template <int G, int SLICE, bool SEQ>
 __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
@@ -649,15 +633,15 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
     char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE;
     for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
          li += (int64_t)gridDim.x * gpb) {
-        const int64_t i = list[li];
+        const NumRowHdr h = num_row_hdr(a, list[li]);
+        const int64_t i = h.i;
         const int64_t gi = i + a.a_row_off;
-        const int n = (int)a.counts[i];
-        const int64_t cp = a.cptr[i];
-        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
-        const int mflag = a.msets ? a.msets[i] : 0;
+        const int n = h.n;
+        const int64_t cp = h.cp;
+        const int64_t a0 = h.a0, a1 = h.a1;
+        const int mflag = h.mflag;
         const bool have_sets = a.sptr != nullptr && (mflag & SETS_WRITTEN);
-        int64_t mest = a.msets ? (int64_t)(mflag & (SETS_WRITTEN - 1))
-                               : (a.sbound[i] < n ? a.sbound[i] : n);
+        int64_t mest = a.msets ? (int64_t)(mflag & (SETS_WRITTEN - 1)) : (h.sb < n ? h.sb : n);
         double *vals = reinterpret_cast<double *>(slice);
         int2 *cbuf = reinterpret_cast<int2 *>(slice);   // phase-B scratch, aliases vals
         int4 *tbl = reinterpret_cast<int4 *>(slice + round16(8 * (int64_t)n));
@@ -679,7 +663,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         if (have_sets) {
             // sorted sets from the symbolic phase: base = running popcount
             const int m = (int)mest;
-            const int64_t sp = a.sptr[i];
+            const int64_t sp = h.sp;
             int carry = 0;
             for (int q0 = 0; q0 < m; q0 += G) {
                 int q = q0 + glane;
@@ -1365,7 +1349,18 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         // set bounds: partial row length + sum of selected compressed B rows
         if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
             rows_out == a->rows) {
-            launch_bounds(c, a, cb->start, cb->cnt, nullptr, sbound, nullptr);
+            int *maxcb = reinterpret_cast<int *>(c->d_small + 50);
+            TSG_CK(cudaMemsetAsync(maxcb, 0, sizeof(int), c->stream));
+            k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
+                                                                                    maxcb); ++c->launches;
+            const unsigned g = grid_for(a->rows, 256, c->num_sms * 16);
+            switch (pick_g(a->nnz, a->rows)) {
+            case 4: k_sym_bounds<4><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+            case 8: k_sym_bounds<8><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+            case 16: k_sym_bounds<16><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+            default: k_sym_bounds<32><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+            }
+            ++c->launches;
         } else {
             TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
                                      partial ? partial->rp : nullptr, sbound));
@@ -1480,18 +1475,27 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         TSG_CK(cudaGetLastError());
         TSG_TRY(partition_rows(c, rows_out, bins, bl, cptr + rows_out, &nnz));
     }
-    tsg_csr *C = new tsg_csr();
-    C->rows = rows_out;
-    C->cols = cols_out;
-    C->nnz = nnz;
-    C->rp = cptr;
-    C->col = nullptr;
-    C->val = nullptr;
-    int st = tsg_alloc_t(c, &C->col, nnz);
-    if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, nnz);
-    if (st != TSG_OK) {
-        tsg_csr_free(c, C);
-        return st;
+    tsg_csr *C = nullptr;
+    if (c->c_host_out) {
+        // placement with C in the slow tier: the numeric kernels write C over
+        // PCIe into pinned, mapped host memory
+        TSG_TRY(tsg_csr_alloc_mapped(c, rows_out, cols_out, nnz, true, &C));
+        TSG_CK(cudaMemcpyAsync(C->rp, cptr, (rows_out + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+    } else {
+        C = new tsg_csr();
+        C->rows = rows_out;
+        C->cols = cols_out;
+        C->nnz = nnz;
+        C->rp = cptr;
+        C->col = nullptr;
+        C->val = nullptr;
+        int st = tsg_alloc_t(c, &C->col, nnz);
+        if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, nnz);
+        if (st != TSG_OK) {
+            tsg_csr_free(c, C);
+            return st;
+        }
     }
     if (rows_out > 0 && nnz > 0) {
         NumArgs na;
@@ -1539,6 +1543,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     TSG_TRY(tsg_free(c, sbound));
     if (pt) pt->mark();
     int s = tsg_check_kernel_errors(c, "numeric");
+    if (C->host_mapped) tsg_free(c, cptr);
     if (s != TSG_OK) {
         tsg_csr_free(c, C);
         return s;
@@ -1746,6 +1751,14 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
     tsg_free(c, sbound);
     tsg_vec_free(c, counts);
     tsg_cmat_free(c, cb);
+    return s;
+}
+
+extern "C" int tsg_multiply_placed(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int c_in_host,
+                                   tsg_csr **out) {
+    c->c_host_out = c_in_host ? 1 : 0;
+    int s = tsg_multiply(c, a, b, out);
+    c->c_host_out = 0;
     return s;
 }
 

@@ -236,14 +236,29 @@ def spgemm_numeric_fused(a, b_chunk, c_partial, a_rows: RowRange, b_rows: RowRan
     return _keep_result(out.download(), out)
 
 
-def multiply(a, b, workers: int = 1) -> CsrMatrix:
-    """compress -> symbolic -> numeric, entirely on the device (kernel.py:343-346)."""
+def multiply(a, b, workers: int = 1, placement="all_fast") -> CsrMatrix:
+    """compress -> symbolic -> numeric on the device (kernel.py:343-346).
+
+    ``placement`` (a memory.PlacementPolicy or its name, memory.py:193-223)
+    places each operand in HBM ("fast") or in pinned, device-mapped host
+    memory ("slow") that the kernels read and write in place over PCIe --
+    the paper's data-placement experiment:
+    "all_fast" (default), "b_in_fast" (A and C slow), "all_slow", or any
+    PlacementPolicy with per-operand spaces.  "chunked" is the executors'
+    job (chunking.execute_plan)."""
     if a.num_cols != b.num_rows:
         raise DimensionError("A has %d cols but compressed B has %d rows" % (a.num_cols, b.num_rows))
     if b.values is None or a.values is None:
         raise MatrixValidationError("numeric multiply requires values on both operands")
-    dc = _lib.d_multiply(_on_device(a), _on_device(b))
-    return _keep_result(dc.download(), dc)
+    from .memory import ALL_FAST, CHUNKED, FAST, PlacementPolicy
+    pol = placement if isinstance(placement, PlacementPolicy) else PlacementPolicy.from_name(placement)
+    if pol.name in (ALL_FAST, CHUNKED) or all(v == FAST for v in pol.spaces.values()):
+        dc = _lib.d_multiply(_on_device(a), _on_device(b))
+        return _keep_result(dc.download(), dc)
+    da = _on_device(a) if pol.space_of("A") == FAST else _lib.DeviceCsr.map_host(a)
+    db = _on_device(b) if pol.space_of("B") == FAST else _lib.DeviceCsr.map_host(b)
+    dc = _lib.d_multiply_placed(da, db, pol.space_of("C") != FAST)
+    return dc.download()
 
 
 def masked_row_intersect_count(l, cl, workers: int = 1) -> int:

@@ -204,3 +204,16 @@ def test_count_multiplications(rng):
     a = random_csr(rng, 25, 30, 5)
     b = random_csr(rng, 30, 20, 5)
     assert tsg.count_multiplications(a, b) == O.count_multiplications(a, b)
+
+
+def test_placement_policies_same_product(rng):
+    """Data placement (memory.py:193-223): every operand placement gives the
+    same product; slow-tier operands are read/written in mapped host memory."""
+    from paper_1804_00695_b200.memory import PlacementPolicy
+    a = random_csr(rng, 300, 400, 12)
+    b = random_csr(rng, 400, 500, 12)
+    want = O.multiply(a, b)
+    for name in ("all_fast", "b_in_fast", "all_slow"):
+        assert_same_product(tsg.multiply(a, b, placement=name), want, exact=True)
+    pol = PlacementPolicy("c_pin", {"A": "fast", "B": "fast", "C": "slow"})
+    assert_same_product(tsg.multiply(a, b, placement=pol), want, exact=True)
