@@ -23,9 +23,12 @@
 
 namespace {
 
-constexpr int CT = 256;             // threads per block
-constexpr int PB = 1024;            // entries per block (4 per thread, strided by CT)
-constexpr int WPBLK = PB / 32;      // 32-entry words per block
+// Thread-per-word layout: one thread owns a 32-entry word of B's column
+// array (8 x 16-byte loads, its own cache line), so head detection and run
+// ORs are straight-line register code (~8 instructions per entry instead of
+// warp shuffles per entry).  A block covers CT words = 32*CT entries.
+constexpr int CT = 256;                 // threads (= words) per block
+constexpr int PB = CT * 32;             // entries per block
 
 __global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint32_t *rsbits) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
@@ -35,67 +38,81 @@ __global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint3
     }
 }
 
-// stage the block's PB columns (+ the one before) in shared memory
-__device__ __forceinline__ void stage_cols(int64_t nnz, int64_t base, const int32_t *__restrict__ col,
-                                           int *s_c) {
+__device__ __forceinline__ void load_word(const int32_t *__restrict__ col, int64_t nnz, int64_t t0,
+                                          int (&c)[32]) {
+    if (t0 + 32 <= nnz && (((uintptr_t)(col + t0)) & 15) == 0) {
+        const int4 *p = reinterpret_cast<const int4 *>(col + t0);
 #pragma unroll
-    for (int k = 0; k < PB / CT; ++k) {
-        const int e = k * CT + threadIdx.x;
-        const int64_t t = base + e;
-        s_c[e + 1] = t < nnz ? col[t] : 0;
+        for (int k = 0; k < 8; ++k) {
+            int4 v = __ldg(p + k);
+            c[4 * k] = v.x;
+            c[4 * k + 1] = v.y;
+            c[4 * k + 2] = v.z;
+            c[4 * k + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) c[q] = t0 + q < nnz ? __ldg(col + t0 + q) : 0;
     }
-    if (threadIdx.x == 0) s_c[0] = base > 0 ? col[base - 1] : 0;
 }
 
-// P1: head words (one ballot per 32 consecutive entries), block-relative
-// per-word prefixes and per-block totals.
+// P1: head mask of each word (an entry opens a set if its row starts there or
+// its set differs from the previous entry's), block-relative word prefixes,
+// block totals; a set that goes down inside a row flags the matrix unsorted.
 __global__ void __launch_bounds__(CT) k_heads(int64_t nnz, const int32_t *__restrict__ col,
                                              const uint32_t *__restrict__ rsbits,
                                              uint32_t *__restrict__ hbits,
                                              uint16_t *__restrict__ wpre,
                                              int64_t *__restrict__ bcnt, int *unsorted) {
-    __shared__ int s_c[PB + 1];
-    __shared__ int s_n[WPBLK];
+    __shared__ int s_w[CT / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * PB;
-    stage_cols(nnz, base, col, s_c);
-    __syncthreads();
+    const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const int64_t t0 = word * 32;
+    int n = 0;
+    uint32_t hw = 0;
     bool bad = false;
+    if (t0 < nnz) {
+        int c[32];
+        load_word(col, nnz, t0, c);
+        const uint32_t rs = rsbits[word];
+        int prev = t0 > 0 ? (__ldg(col + t0 - 1) >> 6) : -1;
 #pragma unroll
-    for (int k = 0; k < PB / CT; ++k) {
-        const int e = k * CT + threadIdx.x;
-        const int64_t t = base + e;
-        const bool valid = t < nnz;
-        const int sv = s_c[e + 1] >> 6, sp = s_c[e] >> 6;
-        const bool rs = valid && ((rsbits[t >> 5] >> (t & 31)) & 1u);
-        const bool head = valid && (rs || t == 0 || sv != sp);
-        bad |= valid && !rs && t > 0 && sv < sp;
-        const uint32_t hw = __ballot_sync(0xffffffffu, head);
-        const int word = k * (CT / 32) + w;
-        if (lane == 0) {
-            if (base + word * 32 < nnz) hbits[(base >> 5) + word] = hw;
-            s_n[word] = __popc(hw);
+        for (int q = 0; q < 32; ++q) {
+            const int sv = c[q] >> 6;
+            const bool valid = t0 + q < nnz;
+            const bool start = (rs >> q) & 1u;
+            const bool head = valid && (start || t0 + q == 0 || sv != prev);
+            bad |= valid && !start && t0 + q > 0 && sv < prev;
+            hw |= (uint32_t)head << q;
+            prev = sv;
         }
+        hbits[word] = hw;
+        n = __popc(hw);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
-    __syncthreads();
-    if (w == 0) {
-        int v = s_n[lane];   // WPBLK == 32
-        int x = v;
+    // block-relative exclusive prefix of the words' head counts
+    int x = n;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += o;
-        }
-        if (base + lane * 32 < nnz) wpre[(base >> 5) + lane] = (uint16_t)(x - v);
-        if (lane == 31) bcnt[blockIdx.x] = x;
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
     }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    int woff = 0;
+    for (int j = 0; j < w; ++j) woff += s_w[j];
+    if (t0 < nnz) wpre[word] = (uint16_t)(woff + x - n);
+    if (threadIdx.x == CT - 1) bcnt[blockIdx.x] = woff + x;
 }
 
-// P3: every head ORs the bits of its run (a forward scan in shared memory;
-// a run crossing the block end continues in global memory) and writes its
-// (set, mask) at its global rank.  Consecutive heads of a warp write
-// consecutive addresses.
+// P3: each thread walks its word's runs in registers and emits every run it
+// owns; a run that started in an earlier word belongs to that word's thread,
+// which reads ahead until the next head.  The block's runs form one
+// contiguous output range, so they are staged in shared memory and written
+// back with coalesced 16-byte stores (per-thread stores of 4/8-byte runs
+// would scatter across sectors).
+constexpr int EMIT_CAP = 4096;   // staged runs per block (48 KB); more -> direct stores
+
 __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__restrict__ col,
                                                  const uint32_t *__restrict__ hbits,
                                                  const uint16_t *__restrict__ wpre,
@@ -104,41 +121,59 @@ __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__
                                                  uint64_t *__restrict__ obits,
                                                  const int *unsorted) {
     if (*unsorted) return;
-    __shared__ int s_c[PB + 1];
-    __shared__ uint32_t s_h[WPBLK];
-    const int lane = threadIdx.x & 31;
-    const int64_t base = (int64_t)blockIdx.x * PB;
-    const int lim = nnz - base < PB ? (int)(nnz - base) : PB;
-    stage_cols(nnz, base, col, s_c);
-    if (threadIdx.x < WPBLK)
-        s_h[threadIdx.x] = base + threadIdx.x * 32 < nnz ? hbits[(base >> 5) + threadIdx.x] : 0u;
-    __syncthreads();
-    const int64_t bb = boff[blockIdx.x];
+    extern __shared__ int4 esm[];
+    uint64_t *s_bits = reinterpret_cast<uint64_t *>(esm);
+    int32_t *s_set = reinterpret_cast<int32_t *>(s_bits + EMIT_CAP);
+    const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const int64_t t0 = word * 32;
+    const int64_t b0 = boff[blockIdx.x];
+    const int nrun = (int)(boff[blockIdx.x + 1] - b0);
+    const bool staged = nrun <= EMIT_CAP;
+    const uint32_t hw = t0 < nnz ? hbits[word] : 0u;
+    if (hw) {
+        int c[32];
+        load_word(col, nnz, t0, c);
+        int r = wpre[word];   // block-relative rank of this word's first head
+        int set = -1;
+        uint64_t bits = 0;
 #pragma unroll
-    for (int k = 0; k < PB / CT; ++k) {
-        const int e = k * CT + threadIdx.x;
-        const int word = e >> 5;
-        const uint32_t hw = s_h[word];
-        if (!((hw >> lane) & 1u)) continue;
-        const int c0 = s_c[e + 1];
-        unsigned lo = 0, hi = 0;
-        int q = e;
-        do {   // run = entries up to the next head
-            const int b = s_c[q + 1] & 63;
-            if (b < 32) lo |= 1u << b;
-            else hi |= 1u << (b - 32);
-            ++q;
-        } while (q < lim && !((s_h[q >> 5] >> (q & 31)) & 1u));
-        uint64_t bits = ((uint64_t)hi << 32) | lo;
-        if (q == PB) {
-            for (int64_t g = base + PB; g < nnz; ++g) {
-                if ((hbits[g >> 5] >> (g & 31)) & 1u) break;
-                bits |= 1ull << (col[g] & 63);
+        for (int q = 0; q < 32; ++q) {
+            const bool valid = t0 + q < nnz;
+            const uint64_t b = 1ull << (c[q] & 63);
+            if (valid && ((hw >> q) & 1u)) {
+                if (set >= 0) {
+                    if (staged) {
+                        s_set[r] = set;
+                        s_bits[r] = bits;
+                    } else {
+                        oset[b0 + r] = set;
+                        obits[b0 + r] = bits;
+                    }
+                    ++r;
+                }
+                set = c[q] >> 6;
+                bits = b;
+            } else if (valid && set >= 0) {
+                bits |= b;
             }
         }
-        const int64_t pos = bb + wpre[(base >> 5) + word] + __popc(hw & ((1u << lane) - 1u));
-        oset[pos] = c0 >> 6;
-        obits[pos] = bits;
+        for (int64_t g = t0 + 32; g < nnz; ++g) {   // the last run may continue
+            if ((hbits[g >> 5] >> (g & 31)) & 1u) break;
+            bits |= 1ull << (__ldg(col + g) & 63);
+        }
+        if (staged) {
+            s_set[r] = set;
+            s_bits[r] = bits;
+        } else {
+            oset[b0 + r] = set;
+            obits[b0 + r] = bits;
+        }
+    }
+    if (!staged) return;   // block-uniform
+    __syncthreads();
+    for (int x = threadIdx.x; x < nrun; x += CT) {
+        oset[b0 + x] = s_set[x];
+        obits[b0 + x] = s_bits[x];
     }
 }
 
@@ -152,7 +187,7 @@ __global__ void k_set_starts(int64_t rows, int64_t nnz, const int64_t *__restric
     auto rank_at = [&](int64_t e) -> int64_t {
         if (e >= nnz) return boff[nblocks];
         return boff[e / PB] + wpre[e >> 5] + __popc(hbits[e >> 5] & ((1u << (e & 31)) - 1u));
-    };
+    };   // PB entries per block, wpre block-relative
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t s0 = rank_at(rp[i]);
@@ -235,7 +270,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         *out = cm;
         return TSG_OK;
     }
-    const int64_t nwords = (nnz + 31) / 32, nblocks = (nnz + PB - 1) / PB;   // PB = 1024 entries
+    const int64_t nwords = (nnz + 31) / 32, nblocks = (nnz + PB - 1) / PB;   // PB = 8192 entries
     uint32_t *rsbits = nullptr, *hbits = nullptr;
     uint16_t *wpre = nullptr;
     int64_t *bcnt = nullptr, *fstart = nullptr;
@@ -254,8 +289,10 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits); ++c->launches;
     k_heads<<<(unsigned)nblocks, CT, 0, s>>>(nnz, b->col, rsbits, hbits, wpre, bcnt, unsorted); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i64(c, bcnt, bcnt, nblocks));
-    k_emit_sets<<<(unsigned)nblocks, CT, 0, s>>>(nnz, b->col, hbits, wpre, bcnt, cm->set, cm->bits,
-                                                 unsorted); ++c->launches;
+    const size_t esmem = (size_t)EMIT_CAP * 12;
+    TSG_TRY(tsg_func_smem((const void *)k_emit_sets, esmem));
+    k_emit_sets<<<(unsigned)nblocks, CT, esmem, s>>>(nnz, b->col, hbits, wpre, bcnt, cm->set, cm->bits,
+                                                     unsorted); ++c->launches;
     k_set_starts<<<rgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
                                        unsorted); ++c->launches;
     // first-occurrence fallback: every kernel returns at once on sorted input
