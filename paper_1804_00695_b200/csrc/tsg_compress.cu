@@ -295,12 +295,15 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
                                                      unsorted); ++c->launches;
     k_set_starts<<<rgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
                                        unsorted); ++c->launches;
-    // first-occurrence fallback: every kernel returns at once on sorted input
-    const unsigned wgrid = (unsigned)(c->num_sms * 4);   // grid-stride; exits at once when sorted
-    k_first_count<<<wgrid, 256, 0, s>>>(rows, b->rp, b->col, fcnt, unsorted); ++c->launches;
-    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, fcnt, fstart, rows));
-    k_first_emit<<<wgrid, 256, 0, s>>>(rows, b->rp, b->col, fcnt, fstart, cm->start, cm->cnt, cm->set,
-                                       cm->bits, unsorted); ++c->launches;
+    // first-occurrence fallback for input not known to be row-sorted: every
+    // kernel returns at once if P1 found the rows sorted after all
+    if (!b->sorted) {
+        const unsigned wgrid = (unsigned)(c->num_sms * 4);   // grid-stride
+        k_first_count<<<wgrid, 256, 0, s>>>(rows, b->rp, b->col, fcnt, unsorted); ++c->launches;
+        TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, fcnt, fstart, rows));
+        k_first_emit<<<wgrid, 256, 0, s>>>(rows, b->rp, b->col, fcnt, fstart, cm->start, cm->cnt,
+                                           cm->set, cm->bits, unsorted); ++c->launches;
+    }
     TSG_CK(cudaGetLastError());
     tsg_free(c, rsbits);
     tsg_free(c, hbits);

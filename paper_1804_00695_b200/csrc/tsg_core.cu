@@ -517,10 +517,58 @@ __global__ void scan_tiles(const TI *__restrict__ in, int64_t n, const int64_t *
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
 }
 
+// Inputs up to SMALL_SCAN elements: one 1024-thread block, one launch.
+constexpr int64_t SMALL_SCAN = 1024 * 16;
+
+template <typename TI>
+__global__ void __launch_bounds__(1024) scan_one_block(const TI *__restrict__ in, int64_t n,
+                                                       int64_t *__restrict__ out) {
+    __shared__ int64_t ws[32];
+    constexpr int IT = 16;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)threadIdx.x * IT;
+    int64_t v[IT];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+        v[k] = base + k < n ? (int64_t)in[base + k] : 0;
+        s += v[k];
+    }
+    int64_t x = s;
+    for (int d = 1; d < 32; d <<= 1) {
+        int64_t o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int64_t y = ws[lane];
+        for (int d = 1; d < 32; d <<= 1) {
+            int64_t o = __shfl_up_sync(0xffffffffu, y, d);
+            if (lane >= d) y += o;
+        }
+        ws[lane] = y;
+    }
+    __syncthreads();
+    int64_t run = x - s + (w ? ws[w - 1] : 0);
+    __syncthreads();   // in place: every thread has read its inputs
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+    if (threadIdx.x == 1023) out[n] = run;
+}
+
 template <typename TI>
 int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     if (n == 0) {
         TSG_CK(cudaMemsetAsync(out, 0, sizeof(int64_t), c->stream));
+        return TSG_OK;
+    }
+    if (n <= SMALL_SCAN) {
+        scan_one_block<TI><<<1, 1024, 0, c->stream>>>(in, n, out); ++c->launches;
+        TSG_CK(cudaGetLastError());
         return TSG_OK;
     }
     int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -643,6 +691,38 @@ __global__ void rebase_rp(const int64_t *__restrict__ in, int64_t *__restrict__ 
 }
 }  // namespace
 
+namespace {
+// flag <- 1 if some row has a column smaller than its predecessor
+__global__ void k_rows_unsorted(int64_t rows, const int64_t *__restrict__ rp,
+                                const int32_t *__restrict__ col, int *flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < rows; i += nw) {
+        bool bad = false;
+        for (int64_t t = rp[i] + 1 + lane; t < rp[i + 1]; t += 32) bad |= col[t] < col[t - 1];
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) *flag = 1;
+            return;
+        }
+    }
+}
+}  // namespace
+
+int tsg_csr_check_sorted(tsg_ctx *c, tsg_csr *m) {
+    int *flag = reinterpret_cast<int *>(c->d_small + 52);
+    TSG_CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    if (m->nnz > 0 && m->rows > 0) {
+        k_rows_unsorted<<<grid_for(m->rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(m->rows, m->rp,
+                                                                                  m->col, flag); ++c->launches;
+    }
+    int h = 0;
+    TSG_CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    m->sorted = h ? 0 : 1;
+    return TSG_OK;
+}
+
 static unsigned ew_grid(tsg_ctx *c, int64_t n) { return grid_for(n, 256, c->num_sms * 16); }
 
 extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
@@ -672,6 +752,7 @@ extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nn
         TSG_TRY(tsg_free(c, stage));
     }
     int s = tsg_check_kernel_errors(c, "upload");
+    if (s == TSG_OK) s = tsg_csr_check_sorted(c, m);
     if (s != TSG_OK) {
         tsg_csr_free(c, m);
         return s;
@@ -739,6 +820,7 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
                                    cudaMemcpyDeviceToDevice, c->stream));
     }
     TSG_CK(cudaGetLastError());
+    s->sorted = m->sorted;
     *out = s;
     return TSG_OK;
 }
@@ -809,6 +891,7 @@ extern "C" int tsg_csr_from_device(tsg_ctx *c, int64_t rows, int64_t cols, int64
                                    c->stream));
     }
     TSG_CK(cudaStreamSynchronize(c->stream));
+    TSG_TRY(tsg_csr_check_sorted(c, m));
     *out = m;
     return TSG_OK;
 }

@@ -48,6 +48,7 @@ struct tsg_csr {
     int32_t *col;
     double *val;
     int host_mapped;   // arrays live in pinned, device-mapped host memory (placement)
+    int sorted;        // 1: every row's columns are non-decreasing (compress needs no fallback)
 };
 
 struct tsg_cmat {
@@ -130,6 +131,8 @@ int tsg_csr_alloc_mapped(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, 
 int tsg_csr_alloc(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, bool values,
                   tsg_csr **out);
 int tsg_vec_alloc(tsg_ctx *ctx, int64_t n, bool aux, tsg_vec **out);
+// sets m->sorted from the device data (synchronises)
+int tsg_csr_check_sorted(tsg_ctx *ctx, tsg_csr *m);
 int tsg_cmat_alloc(tsg_ctx *ctx, int64_t rows, int64_t cap, tsg_cmat **out);
 
 // ---------------------------------------------------------------- timing

@@ -1544,6 +1544,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     if (pt) pt->mark();
     int s = tsg_check_kernel_errors(c, "numeric");
     if (C->host_mapped) tsg_free(c, cptr);
+    C->sorted = 1;   // every emitted row lists its columns in ascending order
     if (s != TSG_OK) {
         tsg_csr_free(c, C);
         return s;
