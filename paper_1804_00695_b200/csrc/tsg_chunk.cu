@@ -122,6 +122,8 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
                cudaEvent_t wait_free, int64_t &bytes) {
     const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
     TSG_TRY(ensure(c, d, rows, nnz, h.val != nullptr));
+    d.m.sorted = 0;      // host rows are not inspected: compress keeps its fallback
+    d.m.max_row = -1;
     cudaStream_t s = c->copy_in;
     // buffers come from the compute-stream-ordered arena: order the copy stream after it
     TSG_CK(cudaEventRecord(d.ready, c->stream));

@@ -260,10 +260,39 @@ __global__ void k_first_emit(int64_t rows, const int64_t *__restrict__ rp,
 
 }  // namespace
 
+namespace {
+// rows of at most one entry (aggregation operators): each entry is its own set
+__global__ void k_compress_unit(int64_t rows, int64_t nnz, const int64_t *__restrict__ rp,
+                                const int32_t *__restrict__ col, int64_t *__restrict__ start,
+                                int32_t *__restrict__ cnt, int32_t *__restrict__ oset,
+                                uint64_t *__restrict__ obits) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = rp[i];
+        start[i] = e;
+        if (i < rows) {
+            cnt[i] = (int32_t)(rp[i + 1] - e);
+            if (rp[i + 1] > e) {
+                const int cv = col[e];
+                oset[e] = cv >> 6;
+                obits[e] = 1ull << (cv & 63);
+            }
+        }
+    }
+}
+}  // namespace
+
 int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_cmat *cm = nullptr;
     const int64_t rows = b->rows, nnz = b->nnz;
     TSG_TRY(tsg_cmat_alloc(c, rows, nnz > 0 ? nnz : 1, &cm));
+    if (b->max_row >= 0 && b->max_row <= 1 && nnz > 0) {
+        k_compress_unit<<<grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+            rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;
+        TSG_CK(cudaGetLastError());
+        *out = cm;
+        return TSG_OK;
+    }
     if (nnz == 0) {
         TSG_CK(cudaMemsetAsync(cm->start, 0, (rows + 1) * sizeof(int64_t), c->stream));
         TSG_CK(cudaMemsetAsync(cm->cnt, 0, (rows + 1) * sizeof(int32_t), c->stream));

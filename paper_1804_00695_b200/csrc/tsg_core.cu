@@ -598,6 +598,7 @@ int tsg_exclusive_scan_i32_to_i64(tsg_ctx *c, const int32_t *in, int64_t *out, i
 int tsg_csr_alloc(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz, bool values,
                   tsg_csr **out) {
     tsg_csr *m = new tsg_csr();
+    m->max_row = -1;
     m->rows = rows;
     m->cols = cols;
     m->nnz = nnz;
@@ -694,32 +695,36 @@ __global__ void rebase_rp(const int64_t *__restrict__ in, int64_t *__restrict__ 
 namespace {
 // flag <- 1 if some row has a column smaller than its predecessor
 __global__ void k_rows_unsorted(int64_t rows, const int64_t *__restrict__ rp,
-                                const int32_t *__restrict__ col, int *flag) {
+                                const int32_t *__restrict__ col, int *flag,
+                                unsigned long long *maxlen) {
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long ml = 0;
+    bool bad = false;
     for (int64_t i = w; i < rows; i += nw) {
-        bool bad = false;
-        for (int64_t t = rp[i] + 1 + lane; t < rp[i + 1]; t += 32) bad |= col[t] < col[t - 1];
-        if (__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) *flag = 1;
-            return;
-        }
+        const int64_t r0 = rp[i], r1 = rp[i + 1];
+        if ((unsigned long long)(r1 - r0) > ml) ml = (unsigned long long)(r1 - r0);
+        for (int64_t t = r0 + 1 + lane; t < r1; t += 32) bad |= col[t] < col[t - 1];
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *flag = 1;
+    if (lane == 0 && ml) atomicMax(maxlen, ml);
 }
 }  // namespace
 
 int tsg_csr_check_sorted(tsg_ctx *c, tsg_csr *m) {
     int *flag = reinterpret_cast<int *>(c->d_small + 52);
-    TSG_CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    unsigned long long *ml = reinterpret_cast<unsigned long long *>(c->d_small + 53);
+    TSG_CK(cudaMemsetAsync(c->d_small + 52, 0, 2 * sizeof(int64_t), c->stream));
     if (m->nnz > 0 && m->rows > 0) {
-        k_rows_unsorted<<<grid_for(m->rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(m->rows, m->rp,
-                                                                                  m->col, flag); ++c->launches;
+        k_rows_unsorted<<<grid_for(m->rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(
+            m->rows, m->rp, m->col, flag, ml); ++c->launches;
     }
-    int h = 0;
-    TSG_CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int64_t h[2] = {0, 0};
+    TSG_CK(cudaMemcpyAsync(h, c->d_small + 52, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
-    m->sorted = h ? 0 : 1;
+    m->sorted = ((int)h[0]) ? 0 : 1;
+    m->max_row = h[1];
     return TSG_OK;
 }
 
@@ -821,6 +826,7 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
     }
     TSG_CK(cudaGetLastError());
     s->sorted = m->sorted;
+    s->max_row = m->max_row;
     *out = s;
     return TSG_OK;
 }
@@ -835,6 +841,7 @@ int tsg_csr_alloc_mapped(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz, bo
     m->cols = cols;
     m->nnz = nnz;
     m->host_mapped = 1;
+    m->max_row = -1;
     const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
     cudaError_t e = cudaHostAlloc((void **)&m->rp, (rows + 1) * sizeof(int64_t), fl);
     if (e == cudaSuccess) e = cudaHostAlloc((void **)&m->col, (nnz > 0 ? nnz : 1) * sizeof(int32_t), fl);

@@ -1484,6 +1484,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
                                c->stream));
     } else {
         C = new tsg_csr();
+        C->max_row = -1;
         C->rows = rows_out;
         C->cols = cols_out;
         C->nnz = nnz;
