@@ -190,6 +190,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--phases", action="store_true", help="print per-phase device times and exit")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
+                         "(for ncu --profile-from-start off)")
     ap.add_argument("--config", type=int, default=2,
                     help="BASELINE.json config (2 = the driver's bench line; 1, 3, 4 = secondary)")
     ap.add_argument("--scale", type=int, default=22, help="R-MAT scale for --config 3")
@@ -249,6 +252,14 @@ def main():
 
     for _ in range(args.warmup):
         dra, drap, _ = step()
+    if args.profile_step:
+        ctx.sync()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        dra, drap, _ = step()
+        ctx.sync()
+        torch.cuda.profiler.stop()
+        return
     if args.phases:
         for _ in range(4):
             ctx.record(0)

@@ -38,21 +38,42 @@ __global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint3
     }
 }
 
-__device__ __forceinline__ void load_word(const int32_t *__restrict__ col, int64_t nnz, int64_t t0,
-                                          int (&c)[32]) {
-    if (t0 + 32 <= nnz && (((uintptr_t)(col + t0)) & 15) == 0) {
-        const int4 *p = reinterpret_cast<const int4 *>(col + t0);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            int4 v = __ldg(p + k);
-            c[4 * k] = v.x;
-            c[4 * k + 1] = v.y;
-            c[4 * k + 2] = v.z;
-            c[4 * k + 3] = v.w;
+// The block's PB column entries are staged in shared memory with coalesced
+// 16-byte loads, then each thread reads its own 32-entry word back into
+// registers.  Thread-owned 128-byte lines read straight from global would
+// cost 32 L1 wavefronts per warp load (one per line); the 16-byte chunks are
+// XOR-swizzled by line (chunk k of word w at w*8 + (k ^ (w & 7))) so both
+// the staging stores and the per-thread reads are bank-conflict free.
+__device__ __forceinline__ void stage_cols(const int32_t *__restrict__ col, int64_t nnz, int64_t e0,
+                                           int4 *__restrict__ sm) {
+    const bool vec = e0 + PB <= nnz && (((uintptr_t)(col + e0)) & 15) == 0;
+    const int4 *src = reinterpret_cast<const int4 *>(col + e0);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < PB / 4; i += CT) {
+        int4 v;
+        if (vec) {
+            v = __ldg(src + i);
+        } else {
+            const int64_t b = e0 + 4 * (int64_t)i;
+            v.x = b < nnz ? __ldg(col + b) : 0;
+            v.y = b + 1 < nnz ? __ldg(col + b + 1) : 0;
+            v.z = b + 2 < nnz ? __ldg(col + b + 2) : 0;
+            v.w = b + 3 < nnz ? __ldg(col + b + 3) : 0;
         }
-    } else {
+        const int w = i >> 3, k = i & 7;
+        sm[w * 8 + (k ^ (w & 7))] = v;
+    }
+}
+
+__device__ __forceinline__ void word_from_smem(const int4 *__restrict__ sm, int (&c)[32]) {
+    const int w = threadIdx.x;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) c[q] = t0 + q < nnz ? __ldg(col + t0 + q) : 0;
+    for (int k = 0; k < 8; ++k) {
+        const int4 v = sm[w * 8 + (k ^ (w & 7))];
+        c[4 * k] = v.x;
+        c[4 * k + 1] = v.y;
+        c[4 * k + 2] = v.z;
+        c[4 * k + 3] = v.w;
     }
 }
 
@@ -64,18 +85,27 @@ __global__ void __launch_bounds__(CT) k_heads(int64_t nnz, const int32_t *__rest
                                              uint32_t *__restrict__ hbits,
                                              uint16_t *__restrict__ wpre,
                                              int64_t *__restrict__ bcnt, int *unsorted) {
+    __shared__ int4 s_col[PB / 4];
     __shared__ int s_w[CT / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
     const int64_t t0 = word * 32;
+    stage_cols(col, nnz, (int64_t)blockIdx.x * PB, s_col);
+    __syncthreads();
     int n = 0;
     uint32_t hw = 0;
     bool bad = false;
     if (t0 < nnz) {
         int c[32];
-        load_word(col, nnz, t0, c);
+        word_from_smem(s_col, c);
         const uint32_t rs = rsbits[word];
-        int prev = t0 > 0 ? (__ldg(col + t0 - 1) >> 6) : -1;
+        int prev;
+        if (threadIdx.x > 0) {
+            const int pw = threadIdx.x - 1;
+            prev = reinterpret_cast<const int *>(s_col)[(pw * 8 + (7 ^ (pw & 7))) * 4 + 3] >> 6;
+        } else {
+            prev = t0 > 0 ? (__ldg(col + t0 - 1) >> 6) : -1;
+        }
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
             const int sv = c[q] >> 6;
@@ -108,10 +138,16 @@ __global__ void __launch_bounds__(CT) k_heads(int64_t nnz, const int32_t *__rest
 // P3: each thread walks its word's runs in registers and emits every run it
 // owns; a run that started in an earlier word belongs to that word's thread,
 // which reads ahead until the next head.  The block's runs form one
-// contiguous output range, so they are staged in shared memory and written
-// back with coalesced 16-byte stores (per-thread stores of 4/8-byte runs
-// would scatter across sectors).
-constexpr int EMIT_CAP = 4096;   // staged runs per block (48 KB); more -> direct stores
+// contiguous output range, so they are staged in shared memory (aliasing the
+// column stage once every thread holds its word) and written back with
+// coalesced stores.  Set masks are staged as two 32-bit halves and every
+// staged array is padded one word per 32: regular matrices give the threads
+// that open a run in the same iteration ranks exactly 32 apart (a 27-point
+// stencil row has 9 runs of 3 -> a head every third entry, ranks 32k + c),
+// which unpadded would put all of them on one bank.
+constexpr int EMIT_CAP = 4096;   // staged runs per block (~50 KB); more -> direct stores
+constexpr int EMIT_PAD = EMIT_CAP + EMIT_CAP / 32;
+constexpr size_t EMIT_SMEM = (size_t)EMIT_PAD * 12 > (size_t)PB * 4 ? (size_t)EMIT_PAD * 12 : (size_t)PB * 4;
 
 __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__restrict__ col,
                                                  const uint32_t *__restrict__ hbits,
@@ -122,33 +158,42 @@ __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__
                                                  const int *unsorted) {
     if (*unsorted) return;
     extern __shared__ int4 esm[];
-    uint64_t *s_bits = reinterpret_cast<uint64_t *>(esm);
-    int32_t *s_set = reinterpret_cast<int32_t *>(s_bits + EMIT_CAP);
+    uint32_t *s_lo = reinterpret_cast<uint32_t *>(esm);
+    uint32_t *s_hi = s_lo + EMIT_PAD;
+    int32_t *s_set = reinterpret_cast<int32_t *>(s_hi + EMIT_PAD);
     const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
     const int64_t t0 = word * 32;
     const int64_t b0 = boff[blockIdx.x];
     const int nrun = (int)(boff[blockIdx.x + 1] - b0);
     const bool staged = nrun <= EMIT_CAP;
     const uint32_t hw = t0 < nnz ? hbits[word] : 0u;
+    stage_cols(col, nnz, (int64_t)blockIdx.x * PB, esm);
+    __syncthreads();
+    int c[32];
+    word_from_smem(esm, c);
+    __syncthreads();   // the column stage is reused for the output below
     if (hw) {
-        int c[32];
-        load_word(col, nnz, t0, c);
         int r = wpre[word];   // block-relative rank of this word's first head
         int set = -1;
         uint64_t bits = 0;
+        auto put = [&](int rr, int st, uint64_t bb) {
+            if (staged) {
+                const int pr = rr + (rr >> 5);
+                s_set[pr] = st;
+                s_lo[pr] = (uint32_t)bb;
+                s_hi[pr] = (uint32_t)(bb >> 32);
+            } else {
+                oset[b0 + rr] = st;
+                obits[b0 + rr] = bb;
+            }
+        };
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
             const bool valid = t0 + q < nnz;
             const uint64_t b = 1ull << (c[q] & 63);
             if (valid && ((hw >> q) & 1u)) {
                 if (set >= 0) {
-                    if (staged) {
-                        s_set[r] = set;
-                        s_bits[r] = bits;
-                    } else {
-                        oset[b0 + r] = set;
-                        obits[b0 + r] = bits;
-                    }
+                    put(r, set, bits);
                     ++r;
                 }
                 set = c[q] >> 6;
@@ -161,19 +206,14 @@ __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__
             if ((hbits[g >> 5] >> (g & 31)) & 1u) break;
             bits |= 1ull << (__ldg(col + g) & 63);
         }
-        if (staged) {
-            s_set[r] = set;
-            s_bits[r] = bits;
-        } else {
-            oset[b0 + r] = set;
-            obits[b0 + r] = bits;
-        }
+        put(r, set, bits);
     }
     if (!staged) return;   // block-uniform
     __syncthreads();
     for (int x = threadIdx.x; x < nrun; x += CT) {
-        oset[b0 + x] = s_set[x];
-        obits[b0 + x] = s_bits[x];
+        const int px = x + (x >> 5);
+        oset[b0 + x] = s_set[px];
+        obits[b0 + x] = (uint64_t)s_lo[px] | ((uint64_t)s_hi[px] << 32);
     }
 }
 
@@ -318,7 +358,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits); ++c->launches;
     k_heads<<<(unsigned)nblocks, CT, 0, s>>>(nnz, b->col, rsbits, hbits, wpre, bcnt, unsorted); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i64(c, bcnt, bcnt, nblocks));
-    const size_t esmem = (size_t)EMIT_CAP * 12;
+    const size_t esmem = EMIT_SMEM;
     TSG_TRY(tsg_func_smem((const void *)k_emit_sets, esmem));
     k_emit_sets<<<(unsigned)nblocks, CT, esmem, s>>>(nnz, b->col, hbits, wpre, bcnt, cm->set, cm->bits,
                                                      unsorted); ++c->launches;

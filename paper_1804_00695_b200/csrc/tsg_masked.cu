@@ -10,6 +10,7 @@
 // is reduced warp -> CTA (shared atomic) -> one global atomic per CTA, so the
 // integer result is exact and launch-order independent.
 #include "tsg_group.cuh"
+#include "tsg_partition.cuh"
 
 namespace {
 
@@ -35,39 +36,10 @@ __device__ __forceinline__ int mask_bin(int64_t len) {
     return 8;
 }
 
-__global__ void k_mask_bins(int64_t rows, const int64_t *__restrict__ lrp, uint8_t *bins) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
-         i += (int64_t)gridDim.x * blockDim.x)
-        bins[i] = (uint8_t)mask_bin(lrp[i + 1] - lrp[i]);
-}
-
-constexpr int TILE = 4096;
-
-__global__ void k_hist(int64_t rows, const uint8_t *__restrict__ bins, int ntiles, int *tc) {
-    __shared__ int h[MB];
-    if (threadIdx.x < MB) h[threadIdx.x] = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < TILE; k += blockDim.x) {
-        int64_t i = (int64_t)blockIdx.x * TILE + k;
-        if (i < rows && bins[i] < MB) atomicAdd(&h[bins[i]], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x < MB) tc[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-__global__ void k_scatter(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
-                          const int64_t *__restrict__ offs, int32_t *list) {
-    __shared__ int h[MB];
-    if (threadIdx.x < MB) h[threadIdx.x] = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < TILE; k += blockDim.x) {
-        int64_t i = (int64_t)blockIdx.x * TILE + k;
-        if (i < rows && bins[i] < MB) {
-            int r = atomicAdd(&h[bins[i]], 1);
-            list[offs[(int64_t)bins[i] * ntiles + blockIdx.x] + r] = (int32_t)i;
-        }
-    }
-}
+struct MaskBinF {
+    const int64_t *lrp;
+    __device__ __forceinline__ int operator()(int64_t i) const { return mask_bin(lrp[i + 1] - lrp[i]); }
+};
 
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_mask_group(const int32_t *__restrict__ list, int64_t nlist,
@@ -250,25 +222,12 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     *total = 0;
     if (rows == 0 || l->nnz == 0) return TSG_OK;
     uint8_t *bins = nullptr;
-    int *tc = nullptr;
-    int64_t *offs = nullptr;
-    int32_t *list = nullptr;
-    int ntiles = (int)((rows + TILE - 1) / TILE);
     TSG_TRY(tsg_alloc_t(c, &bins, rows));
-    TSG_TRY(tsg_alloc_t(c, &tc, (size_t)MB * ntiles));
-    TSG_TRY(tsg_alloc_t(c, &offs, (size_t)MB * ntiles + 1));
-    TSG_TRY(tsg_alloc_t(c, &list, rows));
-    k_mask_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, l->rp, bins); ++c->launches;
-    k_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc); ++c->launches;
-    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)MB * ntiles));
-    k_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, list); ++c->launches;
-    TSG_CK(cudaGetLastError());
+    BinLists<MB> bl;
+    TSG_TRY(tsg_partition<MB>(c, rows, MaskBinF{l->rp}, bins, bl));
+    int32_t *list = bl.list;
     int64_t off[MB + 1];
-    for (int b = 0; b <= MB; b++)
-        TSG_CK(cudaMemcpyAsync(&c->h_small[b], offs + (int64_t)b * ntiles, sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, c->stream));
-    TSG_CK(cudaStreamSynchronize(c->stream));
-    for (int b = 0; b <= MB; b++) off[b] = c->h_small[b];
+    for (int b = 0; b <= MB; b++) off[b] = bl.off[b];
 
     unsigned long long *dtot = (unsigned long long *)(c->d_small + 16);
     TSG_CK(cudaMemsetAsync(dtot, 0, sizeof(unsigned long long), c->stream));
@@ -313,8 +272,6 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     *total = c->h_small[1];
     tsg_free(c, slab);
     tsg_free(c, bins);
-    tsg_free(c, tc);
-    tsg_free(c, offs);
     tsg_free(c, list);
     return s;
 }

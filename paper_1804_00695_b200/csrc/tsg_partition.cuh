@@ -1,0 +1,111 @@
+// tsg_partition.cuh -- row partition by tier ("bin"), shared by the symbolic,
+// numeric, fused and masked-count phases.
+//
+// Three launches and one D2H copy + stream sync per partition:
+//   k_part_bins     the phase's bin functor per row (it may also write
+//                   per-row side outputs), warp-aggregated tile histogram
+//   scan            exclusive scan of the NB x ntiles tile counts
+//   k_part_scatter  row ids into per-bin lists (tile order kept, order inside
+//                   a tile not), block 0 also gathers the bin starts and one
+//                   optional extra device value (e.g. nnz(C)) for the D2H
+// Rows are ranked with __match_any_sync peers so a block does one shared
+// atomic per distinct bin per warp, not one per row (a single dominant bin
+// otherwise serialises 1024 atomics on one address).
+#pragma once
+#include "tsg_internal.cuh"
+
+constexpr int PART_TILE = 1024;   // rows per tile = one 256-thread block
+
+template <int NB>
+struct BinLists {
+    int32_t *list = nullptr;
+    int64_t off[NB + 1] = {0};
+};
+
+template <int NB, class F>
+__global__ void __launch_bounds__(256) k_part_bins(int64_t rows, F f, uint8_t *__restrict__ bins,
+                                                   int ntiles, int *__restrict__ tc) {
+    __shared__ int h[NB];
+    if (threadIdx.x < NB) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * PART_TILE;
+#pragma unroll
+    for (int k = threadIdx.x; k < PART_TILE; k += 256) {
+        const int64_t i = base + k;
+        int b = 255;
+        if (i < rows) {
+            b = f(i);
+            bins[i] = (uint8_t)b;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b < NB && lane == __ffs(peers) - 1) atomicAdd(&h[b], __popc(peers));
+    }
+    __syncthreads();
+    if (threadIdx.x < NB) tc[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_t *__restrict__ bins,
+                                                      int ntiles, const int64_t *__restrict__ offs,
+                                                      int32_t *__restrict__ list,
+                                                      const int64_t *__restrict__ extra,
+                                                      int64_t *__restrict__ out) {
+    __shared__ int h[NB];
+    if (threadIdx.x < NB) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * PART_TILE;
+#pragma unroll
+    for (int k = threadIdx.x; k < PART_TILE; k += 256) {
+        const int64_t i = base + k;
+        const int b = i < rows ? bins[i] : 255;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        int r0 = 0;
+        if (b < NB && lane == leader) r0 = atomicAdd(&h[b], __popc(peers));
+        r0 = __shfl_sync(0xffffffffu, r0, leader);
+        if (b < NB) list[offs[(int64_t)b * ntiles + blockIdx.x] + r0 + __popc(peers & lt)] = (int32_t)i;
+    }
+    if (blockIdx.x == 0) {
+        if (threadIdx.x <= NB) out[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
+        if (threadIdx.x == NB + 1) out[NB + 1] = extra ? *extra : 0;
+    }
+}
+
+// Partition rows [0, rows) by f(i) (values >= NB: row skipped).  `bins` is
+// caller scratch of `rows` bytes; `out.list` is allocated here (caller frees).
+// Bin starts and *extra come back in c->h_small[32 ..].  `mid()` is enqueued
+// between the bin and scatter kernels (e.g. a scan of a side output of f whose
+// total is `extra`).
+struct NoMid {
+    int operator()() const { return TSG_OK; }
+};
+
+template <int NB, class F, class Mid = NoMid>
+int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
+                  const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid()) {
+    static_assert(32 + NB + 2 <= 48, "partition results overlap the d_small flags");
+    int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
+    if (ntiles < 1) ntiles = 1;
+    int *tc = nullptr;
+    int64_t *offs = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &tc, (size_t)NB * ntiles));
+    TSG_TRY(tsg_alloc_t(c, &offs, (size_t)NB * ntiles + 1));
+    TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
+    k_part_bins<NB, F><<<ntiles, 256, 0, c->stream>>>(rows, f, bins, ntiles, tc); ++c->launches;
+    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NB * ntiles));
+    TSG_TRY(mid());
+    k_part_scatter<NB><<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list, extra,
+                                                      c->d_small + 32); ++c->launches;
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaMemcpyAsync(c->h_small + 32, c->d_small + 32, (NB + 2) * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, c->stream));
+    TSG_TRY(tsg_free(c, tc));
+    TSG_TRY(tsg_free(c, offs));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b <= NB; b++) out.off[b] = c->h_small[32 + b];
+    if (extra_out) *extra_out = c->h_small[32 + NB + 1];
+    return TSG_OK;
+}

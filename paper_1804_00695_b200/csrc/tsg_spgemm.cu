@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "tsg_group.cuh"
+#include "tsg_partition.cuh"
 
 namespace {
 
@@ -234,67 +235,34 @@ __global__ void k_unit_rows(int64_t rows, const int64_t *__restrict__ rp, const 
     }
 }
 
-__global__ void k_sym_bins(int64_t rows, const int64_t *__restrict__ sbound, uint8_t *bins,
-                           int64_t *counts, int32_t *msets, int64_t *scap) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int b = sym_bin(sbound[i]);
-        bins[i] = (uint8_t)b;
-        if (scap) scap[i] = b < 7 ? sbound[i] : 0;   // sorted sets are emitted by the group tier
+// per-row bin functors for tsg_partition (tsg_partition.cuh)
+struct SymBinF {
+    const int64_t *sbound;
+    int64_t *counts;
+    int32_t *msets;
+    int64_t *scap;
+    __device__ __forceinline__ int operator()(int64_t i) const {
+        const int64_t sb = sbound[i];
+        const int b = sym_bin(sb);
+        scap[i] = b < 7 ? sb : 0;   // sorted sets are emitted by the group tier
         if (b == 255) {
             counts[i] = 0;
             if (msets) msets[i] = 0;
         }
+        return b;
     }
-}
+};
 
-__global__ void k_num_bins(int64_t rows, const int64_t *__restrict__ counts,
-                           const int32_t *__restrict__ msets, const int64_t *__restrict__ sbound,
-                           uint8_t *bins) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t n = counts[i];
-        int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
-        bins[i] = (uint8_t)num_bin(n, m);
+struct NumBinF {
+    const int64_t *counts;
+    const int32_t *msets;
+    const int64_t *sbound;
+    __device__ __forceinline__ int operator()(int64_t i) const {
+        const int64_t n = counts[i];
+        const int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
+        return num_bin(n, m);
     }
-}
-
-constexpr int BIN_TILE = 4096;
-
-__global__ void k_bin_hist(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
-                           int *__restrict__ tilecounts) {
-    __shared__ int h[NBINS];
-    if (threadIdx.x < NBINS) h[threadIdx.x] = 0;
-    __syncthreads();
-    int64_t base = (int64_t)blockIdx.x * BIN_TILE;
-    for (int k = threadIdx.x; k < BIN_TILE; k += blockDim.x) {
-        int64_t i = base + k;
-        if (i < rows) {
-            int b = bins[i];
-            if (b < NBINS) atomicAdd(&h[b], 1);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < NBINS) tilecounts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-__global__ void k_bin_scatter(int64_t rows, const uint8_t *__restrict__ bins, int ntiles,
-                              const int64_t *__restrict__ offs, int32_t *__restrict__ list) {
-    __shared__ int h[NBINS];
-    if (threadIdx.x < NBINS) h[threadIdx.x] = 0;
-    __syncthreads();
-    int64_t base = (int64_t)blockIdx.x * BIN_TILE;
-    for (int k = threadIdx.x; k < BIN_TILE; k += blockDim.x) {
-        int64_t i = base + k;
-        if (i < rows) {
-            int b = bins[i];
-            if (b < NBINS) {
-                int r = atomicAdd(&h[b], 1);
-                list[offs[(int64_t)b * ntiles + blockIdx.x] + r] = (int32_t)i;
-            }
-        }
-    }
-}
+};
 
 // ======================================================================= K2 group tier
 
@@ -1078,44 +1046,7 @@ __global__ void __launch_bounds__(NT) k_num_block(const int32_t *__restrict__ li
 
 // ======================================================================= host helpers
 
-struct BinLists {
-    int32_t *list = nullptr;
-    int64_t off[NBINS + 1] = {0};
-};
-
-__global__ void k_gather_offsets(const int64_t *__restrict__ offs, int ntiles, int nb,
-                                 const int64_t *__restrict__ extra, int64_t *__restrict__ out) {
-    int b = threadIdx.x;
-    if (b <= nb) out[b] = offs[(int64_t)b * ntiles];
-    if (b == 0) out[nb + 1] = extra ? *extra : 0;
-}
-
-// Stable-per-tile partition of rows by bin id.  Bin starts (and, if `extra`
-// is given, one more device int64 such as nnz(C)) come back in ONE D2H copy
-// and one stream sync.
-int partition_rows(tsg_ctx *c, int64_t rows, const uint8_t *bins, BinLists &out,
-                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr) {
-    int ntiles = (int)((rows + BIN_TILE - 1) / BIN_TILE);
-    if (ntiles < 1) ntiles = 1;
-    int *tc = nullptr;
-    int64_t *offs = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &tc, (size_t)NBINS * ntiles));
-    TSG_TRY(tsg_alloc_t(c, &offs, (size_t)NBINS * ntiles + 1));
-    TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
-    k_bin_hist<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, tc); ++c->launches;
-    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NBINS * ntiles));
-    k_bin_scatter<<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list); ++c->launches;
-    k_gather_offsets<<<1, 32, 0, c->stream>>>(offs, ntiles, NBINS, extra, c->d_small + 32); ++c->launches;
-    TSG_CK(cudaGetLastError());
-    TSG_CK(cudaMemcpyAsync(c->h_small + 32, c->d_small + 32, (NBINS + 2) * sizeof(int64_t),
-                           cudaMemcpyDeviceToHost, c->stream));
-    TSG_TRY(tsg_free(c, tc));
-    TSG_TRY(tsg_free(c, offs));
-    TSG_CK(cudaStreamSynchronize(c->stream));
-    for (int b = 0; b <= NBINS; b++) out.off[b] = c->h_small[32 + b];
-    if (extra_out) *extra_out = c->h_small[32 + NBINS + 1];
-    return TSG_OK;
-}
+using Bins = ::BinLists<NBINS>;
 
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
@@ -1130,7 +1061,7 @@ unsigned group_grid(tsg_ctx *c, int64_t nrows, int groups_per_block) {
 constexpr int64_t GLOBAL_SLAB_BUDGET = (int64_t)2 << 30;
 
 template <int B>
-int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+int launch_sym_group(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     constexpr int G = gt_g_sym(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
@@ -1143,7 +1074,7 @@ int launch_sym_group(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
 }
 
 template <int B, bool SEQ>
-int launch_num_group_m(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
     size_t smem = (size_t)(BS / G) * SL;
@@ -1155,7 +1086,7 @@ int launch_num_group_m(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
 }
 
 template <int B>
-int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+int launch_num_group(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     if (bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
     // lane-per-B-entry mode pays off once B rows fill at least half a group
     if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, true>(c, bl, a);
@@ -1163,7 +1094,7 @@ int launch_num_group(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
 }
 
 template <int CB>
-int launch_sym_cta(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+int launch_sym_cta(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
     const int B = 7 + CB;
     int64_t n = bl.off[B + 1] - bl.off[B];
@@ -1177,7 +1108,7 @@ int launch_sym_cta(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
 }
 
 template <int CB>
-int launch_num_cta(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+int launch_num_cta(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
     const int B = 7 + CB;
     int64_t n = bl.off[B + 1] - bl.off[B];
@@ -1216,7 +1147,7 @@ int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64
     return TSG_OK;
 }
 
-int launch_sym_global(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
@@ -1240,7 +1171,7 @@ int launch_sym_global(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
-int launch_num_global(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
@@ -1267,7 +1198,7 @@ int launch_num_global(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
     return TSG_OK;
 }
 
-int run_symbolic_bins(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
+int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     TSG_TRY(launch_sym_group<0>(c, bl, a));
     TSG_TRY(launch_sym_group<1>(c, bl, a));
     TSG_TRY(launch_sym_group<2>(c, bl, a));
@@ -1281,7 +1212,7 @@ int run_symbolic_bins(tsg_ctx *c, const BinLists &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
-int run_numeric_bins(tsg_ctx *c, const BinLists &bl, const NumArgs &a) {
+int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     TSG_TRY(launch_num_group<0>(c, bl, a));
     TSG_TRY(launch_num_group<1>(c, bl, a));
     TSG_TRY(launch_num_group<2>(c, bl, a));
@@ -1368,13 +1299,11 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         int64_t *scap = nullptr;
         TSG_TRY(tsg_alloc_t(c, &scap, rows_out + 1));
         TSG_TRY(tsg_alloc_t(c, &v->sptr, rows_out + 1));
-        k_sym_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, sbound, bins, v->d, v->aux, scap); ++c->launches;
-        TSG_CK(cudaGetLastError());
-        TSG_TRY(tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out));
-        BinLists bl;
+        Bins bl;
         int64_t set_cap = 0;
-        TSG_TRY(partition_rows(c, rows_out, bins, bl, v->sptr + rows_out, &set_cap));
+        TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap}, bins, bl,
+                                     v->sptr + rows_out, &set_cap,
+                                     [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
         TSG_TRY(tsg_free(c, scap));
         TSG_TRY(tsg_alloc_t(c, &v->sset, set_cap > 0 ? set_cap : 1));
         TSG_TRY(tsg_alloc_t(c, &v->sbits, set_cap > 0 ? set_cap : 1));
@@ -1467,13 +1396,11 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
                                      partial ? partial->rp : nullptr, sbound));
         sbound_in = sbound;
     }
-    BinLists bl;
+    Bins bl;
     int64_t nnz = 0;
     if (rows_out > 0) {
-        k_num_bins<<<grid_for(rows_out, 256, c->num_sms * 8), 256, 0, c->stream>>>(
-            rows_out, counts->d, counts->aux, sbound_in, bins); ++c->launches;
-        TSG_CK(cudaGetLastError());
-        TSG_TRY(partition_rows(c, rows_out, bins, bl, cptr + rows_out, &nnz));
+        TSG_TRY(tsg_partition<NBINS>(c, rows_out, NumBinF{counts->d, counts->aux, sbound_in}, bins, bl,
+                                     cptr + rows_out, &nnz));
     }
     tsg_csr *C = nullptr;
     if (c->c_host_out) {
@@ -1588,11 +1515,9 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
     TSG_TRY(tsg_alloc_t(c, &bins, rows + 1));
     k_fused_bounds<<<grid_for(rows, 8, c->num_sms * 32), 256, 0, c->stream>>>(
         rows, a->rp, a->col, 0, b_lo, b_hi, cb->start, cb->cnt, nullptr, sbound, plen); ++c->launches;
-    k_num_bins<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(rows, cap, nullptr, sbound,
-                                                                          bins); ++c->launches;
     TSG_CK(cudaGetLastError());
-    BinLists bl;
-    TSG_TRY(partition_rows(c, rows, bins, bl));
+    Bins bl;
+    TSG_TRY(tsg_partition<NBINS>(c, rows, NumBinF{cap, nullptr, sbound}, bins, bl));
     NumArgs na;
     memset(&na, 0, sizeof(na));
     na.arp = a->rp;

@@ -31,6 +31,22 @@ def test_compress_matches_reference_first_touch_order(rng):
             assert np.array_equal(cm.set_bits, bits)
 
 
+def test_compress_many_blocks_and_long_runs(rng):
+    # > 8192 entries per compression block: runs crossing word and block
+    # boundaries, a dense row spanning many blocks, empty rows between
+    for dense in (False, True):
+        b = canonicalize(random_csr(rng, 20000, 5000, 30))
+        if dense:
+            rows = np.concatenate([np.full(4000, 7), np.full(3000, 9)])
+            cols = np.concatenate([np.arange(4000), rng.choice(5000, 3000, replace=False)])
+            b = canonicalize(CsrMatrix.from_coo(rows, cols, np.ones(7000), 20, 5000))
+        cm = tsg.compress(b)
+        rp, s, bits = O.compress(b)
+        assert np.array_equal(cm.row_ptr, rp)
+        assert np.array_equal(cm.set_idx, s)
+        assert np.array_equal(cm.set_bits, bits)
+
+
 def test_compress_kats():
     def rows(rs, n):
         r = [i for i, cs in enumerate(rs) for _ in cs]
