@@ -54,7 +54,7 @@ struct SymArgs {
     const int64_t *sptr;
     int32_t *oset;
     uint64_t *obits;
-    const int *unit_b;   // device flag: every compressed B row has <= 1 set
+    const int *maxcb;    // device max sets per compressed B row (<= 1: unit path)
 };
 
 constexpr int SETS_WRITTEN = 1 << 30;
@@ -93,7 +93,8 @@ struct NumArgs {
     const int64_t *pstart;
     const int32_t *plen_in;
     int32_t *plen_out;
-    const int *unit_b;   // device flag: every B row has <= 1 entry
+    const int *unit_b;   // device flag: every B row has <= 1 entry (read if unit_known < 0)
+    int unit_known;      // 1 / 0: known on the host (uploaded B), -1: read *unit_b
 };
 
 __device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                              bit >= 32 ? 1u << (bit - 32) : 0u);
             }
         }
-        if (a.unit_b && *a.unit_b) {
+        if (a.maxcb && *a.maxcb <= 1) {
             // unit compressed rows: batch the three dependent load rounds of UB chunks
             const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
             for (int64_t base = a0; base < a1; base += UB * G) {
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
         __syncwarp(gm);
         if constexpr (SEQ) {
             products_seq<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
-        } else if (a.unit_b && *a.unit_b) {
+        } else if (a.unit_known > 0 || (a.unit_known < 0 && *a.unit_b)) {
             products_unit<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
         } else {
             group_enumerate<G>(
@@ -1278,12 +1279,12 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
     TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
     if (rows_out > 0) {
         // set bounds: partial row length + sum of selected compressed B rows
+        int *maxcb = reinterpret_cast<int *>(c->d_small + 50);
+        TSG_CK(cudaMemsetAsync(maxcb, 0, sizeof(int), c->stream));
+        k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
+                                                                                maxcb); ++c->launches;
         if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
             rows_out == a->rows) {
-            int *maxcb = reinterpret_cast<int *>(c->d_small + 50);
-            TSG_CK(cudaMemsetAsync(maxcb, 0, sizeof(int), c->stream));
-            k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
-                                                                                    maxcb); ++c->launches;
             const unsigned g = grid_for(a->rows, 256, c->num_sms * 16);
             switch (pick_g(a->nnz, a->rows)) {
             case 4: k_sym_bounds<4><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
@@ -1326,11 +1327,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.sptr = v->sptr;
         sa.oset = v->sset;
         sa.obits = v->sbits;
-        int *uflag = reinterpret_cast<int *>(c->d_small + 48);
-        TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));   // nonzero = unit until disproved
-        k_unit_rows<<<grid_for(cb->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(cb->rows, nullptr,
-                                                                                  cb->cnt, uflag); ++c->launches;
-        sa.unit_b = uflag;
+        sa.maxcb = maxcb;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
@@ -1454,11 +1451,17 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.sptr = counts->sptr;
         na.sset = counts->sset;
         na.sbits = counts->sbits;
-        int *uflag = reinterpret_cast<int *>(c->d_small + 49);
-        TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));
-        k_unit_rows<<<grid_for(b->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(b->rows, b->rp, nullptr,
-                                                                                 uflag); ++c->launches;
-        na.unit_b = uflag;
+        if (b->max_row >= 0) {   // known since upload: no device check
+            na.unit_known = b->max_row <= 1 ? 1 : 0;
+            na.unit_b = nullptr;
+        } else {
+            int *uflag = reinterpret_cast<int *>(c->d_small + 49);
+            TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));
+            k_unit_rows<<<grid_for(b->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(b->rows, b->rp, nullptr,
+                                                                                     uflag); ++c->launches;
+            na.unit_known = -1;
+            na.unit_b = uflag;
+        }
         na.pstart = nullptr;
         na.plen_in = nullptr;
         na.plen_out = nullptr;
