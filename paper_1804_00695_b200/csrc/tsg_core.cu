@@ -421,100 +421,104 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
 }
 
 // ------------------------------------------------------------------ scan
-// Three-phase exclusive scan: tile sums -> scan of tile sums -> tile scan.
+// Exclusive scans of non-negative counts (row lengths, set counts), result
+// total in out[n].  Up to SMALL_SCAN elements: one 1024-thread block.  Above:
+// ONE single-pass launch with decoupled look-back -- tiles take their index
+// from an atomic counter (so a tile only ever waits on tiles that are already
+// running), publish their aggregate, and warp 0 walks back over a 32-tile
+// window until it meets a published inclusive prefix.  State words pack
+// (value << 2 | flag) into one 64-bit store, so value and flag are observed
+// together; flag 1 = aggregate, 2 = inclusive prefix.
 
 namespace {
-constexpr int SCAN_BS = 256;
-constexpr int SCAN_IT = 8;
-constexpr int SCAN_TILE = SCAN_BS * SCAN_IT;
+constexpr int LB_BS = 256;
+constexpr int LB_IT = 16;
+constexpr int LB_TILE = LB_BS * LB_IT;
 
-template <typename TI>
-__global__ void scan_tile_sums(const TI *__restrict__ in, int64_t n, int64_t *__restrict__ sums) {
-    __shared__ int64_t ws[SCAN_BS / 32];
-    int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-    int64_t s = 0;
-#pragma unroll
-    for (int k = 0; k < SCAN_IT; k++) {
-        int64_t i = base + (int64_t)k * SCAN_BS + threadIdx.x;
-        if (i < n) s += (int64_t)in[i];
-    }
-    for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t t = 0;
-        for (int w = 0; w < SCAN_BS / 32; w++) t += ws[w];
-        sums[blockIdx.x] = t;
-    }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
-// single block: exclusive scan of m tile sums in place, total into sums[m]
-__global__ void scan_sums_single(int64_t *sums, int64_t m) {
-    __shared__ int64_t ws[32];
-    __shared__ int64_t carry_s;
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < m; base += blockDim.x) {
-        int64_t i = base + threadIdx.x;
-        int64_t v = i < m ? sums[i] : 0;
-        int64_t x = v;
-        int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int d = 1; d < 32; d <<= 1) {
-            int64_t o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += o;
-        }
-        if (lane == 31) ws[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int64_t y = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
-            for (int d = 1; d < 32; d <<= 1) {
-                int64_t o = __shfl_up_sync(0xffffffffu, y, d);
-                if (lane >= d) y += o;
-            }
-            ws[lane] = y;
-        }
-        __syncthreads();
-        int64_t incl = x + (w > 0 ? ws[w - 1] : 0);
-        int64_t carry = carry_s;
-        if (i < m) sums[i] = carry + incl - v;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry_s = carry + incl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) sums[m] = carry_s;
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <typename TI>
-__global__ void scan_tiles(const TI *__restrict__ in, int64_t n, const int64_t *__restrict__ sums,
-                           int64_t *__restrict__ out) {
-    __shared__ int64_t ws[SCAN_BS / 32];
-    int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IT;
-    int64_t v[SCAN_IT];
+__global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in, int64_t n,
+                                                      int64_t *__restrict__ out,
+                                                      unsigned long long *state, unsigned *counter,
+                                                      unsigned ntiles) {
+    __shared__ int64_t ws[LB_BS / 32];
+    __shared__ int64_t s_excl;
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)tile * LB_TILE + (int64_t)threadIdx.x * LB_IT;
+    int64_t v[LB_IT];
     int64_t s = 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_IT; k++) {
-        int64_t i = base + k;
-        v[k] = i < n ? (int64_t)in[i] : 0;
+    for (int k = 0; k < LB_IT; k++) {
+        v[k] = base + k < n ? (int64_t)in[base + k] : 0;
         s += v[k];
     }
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t x = s;
+#pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         int64_t o = __shfl_up_sync(0xffffffffu, x, d);
         if (lane >= d) x += o;
     }
     if (lane == 31) ws[w] = x;
     __syncthreads();
-    int64_t woff = 0;
-    for (int j = 0; j < w; j++) woff += ws[j];
-    int64_t run = sums[blockIdx.x] + woff + x - s;
+    int64_t woff = 0, agg = 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_IT; k++) {
-        int64_t i = base + k;
-        if (i < n) out[i] = run;
+    for (int j = 0; j < LB_BS / 32; j++) {
+        woff += j < w ? ws[j] : 0;
+        agg += ws[j];
+    }
+    if (w == 0) {
+        if (tile == 0) {
+            if (lane == 0) {
+                st_relaxed_gpu(&state[0], ((unsigned long long)agg << 2) | 2ull);
+                s_excl = 0;
+            }
+        } else {
+            if (lane == 0) st_relaxed_gpu(&state[tile], ((unsigned long long)agg << 2) | 1ull);
+            int64_t excl = 0;
+            int64_t pred = (int64_t)tile - 1 - lane;
+            for (;;) {
+                const unsigned long long sv = pred >= 0 ? ld_relaxed_gpu(&state[pred]) : 2ull;
+                const unsigned flag = (unsigned)(sv & 3ull);
+                if (__any_sync(0xffffffffu, flag == 0)) continue;   // a predecessor not published yet
+                const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+                int64_t val = (int64_t)(sv >> 2);
+                if (incl) {
+                    const int k = __ffs(incl) - 1;   // nearest inclusive prefix
+                    if (lane > k) val = 0;
+                }
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+                excl += val;
+                if (incl) break;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                st_relaxed_gpu(&state[tile], ((unsigned long long)(excl + agg) << 2) | 2ull);
+                s_excl = excl;
+            }
+        }
+    }
+    __syncthreads();
+    int64_t run = s_excl + woff + x - s;
+#pragma unroll
+    for (int k = 0; k < LB_IT; k++) {
+        if (base + k < n) out[base + k] = run;
         run += v[k];
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+    if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_excl + agg;
 }
 
 // Inputs up to SMALL_SCAN elements: one 1024-thread block, one launch.
@@ -571,16 +575,16 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
         TSG_CK(cudaGetLastError());
         return TSG_OK;
     }
-    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    int64_t *sums = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &sums, tiles + 1));
-    scan_tile_sums<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums); ++c->launches;
-    scan_sums_single<<<1, 1024, 0, c->stream>>>(sums, tiles); ++c->launches;
-    // in-place safe: every tile reads its inputs into registers before writing,
-    // and tiles write only their own range (plus out[n], past every input).
-    scan_tiles<TI><<<(unsigned)tiles, SCAN_BS, 0, c->stream>>>(in, n, sums, out); ++c->launches;
+    const int64_t tiles = (n + LB_TILE - 1) / LB_TILE;
+    unsigned long long *state = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &state, tiles + 1));   // + the tile counter
+    TSG_CK(cudaMemsetAsync(state, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
+    // in-place safe: a tile reads its inputs before writing, and writes only
+    // its own range (plus out[n], past every input)
+    scan_lookback<TI><<<(unsigned)tiles, LB_BS, 0, c->stream>>>(
+        in, n, out, state, reinterpret_cast<unsigned *>(state + tiles), (unsigned)tiles); ++c->launches;
     TSG_CK(cudaGetLastError());
-    TSG_TRY(tsg_free(c, sums));
+    TSG_TRY(tsg_free(c, state));
     return TSG_OK;
 }
 }  // namespace

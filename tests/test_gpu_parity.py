@@ -80,6 +80,13 @@ def test_multiply_rectangular_and_empty_rows(rng):
         assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=True)
 
 
+def test_multiply_many_rows_multi_tile_scans(rng):
+    # > 16 K rows: the single-pass look-back scans run over many tiles
+    a = random_csr(rng, 150000, 3000, 4)
+    b = random_csr(rng, 3000, 4000, 6)
+    assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=True)
+
+
 def test_numeric_with_host_counts(rng):
     a = random_csr(rng, 200, 200, 10)
     b = random_csr(rng, 200, 500, 10)
