@@ -210,3 +210,129 @@ def random_rhs(num_rows: int, num_cols: int, delta: int, seed: int) -> CsrMatrix
             p += 1
     return CsrMatrix._adopt(num_rows, num_cols, np.arange(num_rows + 1, dtype=np.int64) * delta,
                             cols, vals)
+
+
+# ---------------------------------------------------------------- reference problems
+# The reference's problem builders for its benchmark CLI (generators.py:51-246):
+# a stencil spec, exact nnz / byte sizes, target-byte grid search and the
+# geometric (bi/tri)linear interpolation pair.  Input builders, not hot path.
+
+from dataclasses import dataclass as _dataclass
+
+
+@_dataclass(frozen=True)
+class StencilSpec:
+    """Stencil family + per-axis grid point counts (generators.py:51-83)."""
+
+    kind: str
+    grid_dims: tuple
+
+    def __post_init__(self):
+        if self.kind not in STENCIL_KINDS:
+            raise GridError("unknown stencil kind %r" % (self.kind,))
+        dims = tuple(int(d) for d in self.grid_dims)
+        object.__setattr__(self, "grid_dims", dims)
+        if any(d <= 0 for d in dims):
+            raise GridError("grid dims must be positive")
+        want = 2 if self.kind in (BIGSTAR2D, LAPLACE2D) else 3
+        if len(dims) != want:
+            raise GridError("%s needs %d grid dims, got %d" % (self.kind, want, len(dims)))
+
+    @property
+    def rank(self) -> int:
+        return len(self.grid_dims)
+
+    @property
+    def dofs_per_point(self) -> int:
+        return 3 if self.kind == ELASTICITY3D else 1
+
+    @property
+    def num_points(self) -> int:
+        return int(np.prod(self.grid_dims))
+
+    @property
+    def matrix_rows(self) -> int:
+        return self.num_points * self.dofs_per_point
+
+
+def generate_stencil(spec: StencilSpec) -> CsrMatrix:
+    """The reference's entry point (generators.py:115-142): dims >= 5."""
+    if any(d < 5 for d in spec.grid_dims):
+        raise GridError("stencil grids need every dim >= 5")
+    return stencil(spec.kind, spec.grid_dims)
+
+
+def stencil_nnz(kind: str, grid_dims) -> int:
+    """Exact nnz without building: each offset keeps the points whose shifted
+    neighbour stays in the grid (generators.py:145-160)."""
+    spec = StencilSpec(kind, tuple(grid_dims))
+    total = 0
+    for shift, _ in _offsets(kind):
+        k = 1
+        for ax, s in enumerate(shift):
+            k *= max(spec.grid_dims[ax] - abs(s), 0)
+        total += k
+    return total * spec.dofs_per_point ** 2
+
+
+def stencil_byte_size(kind: str, grid_dims) -> int:
+    spec = StencilSpec(kind, tuple(grid_dims))
+    return 8 * (spec.matrix_rows + 1) + 16 * stencil_nnz(kind, grid_dims)
+
+
+def grid_for_target_bytes(kind: str, target_bytes: int, max_dim: int = 513):
+    """Smallest odd cubic (square in 2D) grid reaching target_bytes
+    (generators.py:168-179)."""
+    rank = 2 if kind in (BIGSTAR2D, LAPLACE2D) else 3
+    for n in range(5, max_dim + 1, 2):
+        dims = (n,) * rank
+        if stencil_byte_size(kind, dims) >= target_bytes:
+            return dims
+    raise GridError("no grid up to %d^%d reaches %d bytes" % (max_dim, rank, target_bytes))
+
+
+def generate_interpolation(spec: StencilSpec):
+    """(P, R = P^T) coarsening by two on every axis (generators.py:182-245):
+    coarse points on even coordinates, odd points average their two coarse
+    neighbours, per-axis weights multiplied (all powers of two, so exact).
+    Vectorised: one pass per choice pattern of the 2^rank neighbour combos."""
+    dims = spec.grid_dims
+    for d in dims:
+        if d < 3 or d % 2 == 0:
+            raise GridError("interpolation needs odd grid dims >= 3, got %r" % (dims,))
+    coarse = [(d + 1) // 2 for d in dims]
+    n = spec.num_points
+    idx = np.arange(n, dtype=np.int64)
+    coords, div = [], 1
+    for d in dims:
+        coords.append((idx // div) % d)
+        div *= d
+    cstride = np.cumprod([1] + coarse[:-1]).astype(np.int64)
+    rows, cols, vals = [], [], []
+    for combo in range(1 << len(dims)):
+        ok = np.ones(n, dtype=bool)
+        col = np.zeros(n, dtype=np.int64)
+        w = np.ones(n, dtype=np.float64)
+        for ax in range(len(dims)):
+            x = coords[ax]
+            odd = (x & 1) == 1
+            up = (combo >> ax) & 1
+            if up:
+                ok &= odd
+            col += cstride[ax] * (x // 2 + up)
+            w *= np.where(odd, 0.5, 1.0)
+        rows.append(idx[ok])
+        cols.append(col[ok])
+        vals.append(w[ok])
+    rows, cols, vals = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    dofs = spec.dofs_per_point
+    if dofs > 1:
+        d = np.arange(dofs)
+        rows = (dofs * rows[:, None] + d[None, :]).ravel()
+        cols = (dofs * cols[:, None] + d[None, :]).ravel()
+        vals = np.repeat(vals, dofs)
+    p = CsrMatrix.from_coo(rows, cols, vals, n * dofs, int(np.prod(coarse)) * dofs)
+    return p, transpose(p)
+
+
+generate_random_rhs = random_rhs
