@@ -148,6 +148,22 @@ int tsg_numeric_fused(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b_chunk,
 int tsg_masked_count(tsg_ctx *ctx, const tsg_csr *l, const tsg_cmat *cl,
                      int64_t *total);
 
+/* ---- graph preparation on the device ----------- */
+/* triangles.py:18-46 validate_graph (check != 0: square, loop-free, symmetric
+   pattern -> TSG_EVALID) + degree_sort_permutation (stable by degree, ties by
+   index) + lower_triangle: L = strict lower triangle of the relabelled graph,
+   rows sorted, pattern only.  perm_host (optional, n int64): the permutation
+   (position -> original vertex) as degree_sort_permutation returns it. */
+int tsg_graph_lower(tsg_ctx *ctx, const tsg_csr *g, int check, tsg_csr **L,
+                    int64_t *perm_host);
+/* generators.rmat_graph of this package on the device: Graph500 R-MAT with
+   2^scale vertices and edge_factor * 2^scale directed draws from the
+   SplitMix64 counter stream of `seed`, vertices relabelled by the ranks of a
+   second stream (seed ^ GAMMA), symmetrised, de-duplicated, loop-free pattern
+   CSR -- equal to the host builder entry for entry. */
+int tsg_rmat_graph(tsg_ctx *ctx, int scale, int edge_factor, uint64_t seed, double a, double b,
+                   double c, tsg_csr **out);
+
 /* ---- data placement (memory.py:193-223 PlacementPolicy; PAPER.md:600-625,
    810-829).  A CSR whose arrays live in pinned, device-mapped HOST memory:
    kernels read it in place over PCIe (the paper's "pinned" columns).  Columns

@@ -44,6 +44,7 @@ EXPORTS = (
     "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
+    "tsg_graph_lower", "tsg_rmat_graph",
 )
 
 _P = ctypes.c_void_p
@@ -83,6 +84,9 @@ _SIGS = {
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric_fused": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _PP], ctypes.c_int),
     "tsg_masked_count": ([_P, _P, _P, _PI64], ctypes.c_int),
+    "tsg_graph_lower": ([_P, _P, ctypes.c_int, _PP, _P], ctypes.c_int),
+    "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                        ctypes.c_double, ctypes.c_double, _PP], ctypes.c_int),
     "tsg_event_record": ([_P, ctypes.c_int], ctypes.c_int),
     "tsg_event_elapsed": ([_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)],
                           ctypes.c_int),
@@ -408,3 +412,24 @@ def d_masked_count(dl, dcl) -> int:
     v = ctypes.c_int64()
     check(load().tsg_masked_count(dl.ctx.h, dl.h, dcl.h, ctypes.byref(v)))
     return v.value
+
+
+check_ = check
+
+
+def d_graph_lower(dg, check: bool = True, want_perm: bool = False):
+    """(L, perm or None): degree-ordered strict lower triangle on the device."""
+    h = ctypes.c_void_p()
+    perm = np.empty(dg.num_rows, dtype=np.int64) if want_perm else None
+    check_(load().tsg_graph_lower(dg.ctx.h, dg.h, 1 if check else 0, ctypes.byref(h),
+                                  _ptr(perm) if want_perm else None))
+    return DeviceCsr(dg.ctx, h), perm
+
+
+def d_rmat_graph(scale: int, edge_factor: int, seed: int, a: float, b: float, c: float,
+                 ctx=None) -> DeviceCsr:
+    ctx = ctx or Context.get()
+    h = ctypes.c_void_p()
+    check_(load().tsg_rmat_graph(ctx.h, int(scale), int(edge_factor), int(seed) & ((1 << 64) - 1),
+                                 float(a), float(b), float(c), ctypes.byref(h)))
+    return DeviceCsr(ctx, h)

@@ -189,6 +189,15 @@ def rmat_graph(scale: int, edge_factor: int = 16, seed: int = 22) -> CsrMatrix:
     return undirected_pattern(u, v, 1 << scale)
 
 
+def rmat_graph_device(scale: int, edge_factor: int = 16, seed: int = 22,
+                      a: float = 0.57, b: float = 0.19, c: float = 0.19):
+    """``rmat_graph`` built in HBM (csrc/tsg_graph.cu):
+    same SplitMix64 draws, relabelling and de-duplication, so the DeviceCsr
+    equals the host builder's matrix entry for entry."""
+    from . import _lib
+    return _lib.d_rmat_graph(scale, edge_factor, seed, a, b, c)
+
+
 def with_unit_values(g: CsrMatrix) -> CsrMatrix:
     return CsrMatrix._adopt(g.num_rows, g.num_cols, g.row_ptr, g.col_idx, np.ones(g.nnz))
 
