@@ -591,6 +591,8 @@ __device__ __forceinline__ NumRowHdr num_row_hdr(const NumArgs &a, int64_t i) {
     return h;
 }
 
+constexpr int NUM_SKEW = 64;
+
 template <int G, int SLICE, bool SEQ>
 __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
@@ -599,7 +601,12 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
     const int glane = threadIdx.x & (G - 1);
     const unsigned lt = lanemask_lt();
     const int gpb = blockDim.x / G;
-    char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE;
+    // 8-lane groups: a half-warp 64-bit shared access spans two groups, whose
+    // equally aligned slices would put equal value positions on one bank;
+    // each odd group starts 64 B (16 banks) later than its even partner
+    // (cumulative, so slices never overlap)
+    char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE +
+                  (G == 8 ? (size_t)(((threadIdx.x / G) + 1) >> 1) * NUM_SKEW : 0);
     for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
          li += (int64_t)gridDim.x * gpb) {
         const NumRowHdr h = num_row_hdr(a, list[li]);
@@ -1078,7 +1085,7 @@ template <int B, bool SEQ>
 int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
-    size_t smem = (size_t)(BS / G) * SL;
+    size_t smem = (size_t)(BS / G) * SL + (G == 8 ? (size_t)(BS / G / 2) * NUM_SKEW : 0);
     TSG_TRY(set_smem(k_num_group<G, SL, SEQ>, smem));
     unsigned grid = group_grid(c, n, BS / G);
     k_num_group<G, SL, SEQ><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
