@@ -75,6 +75,11 @@ typedef struct {
 int tsg_get_stats(tsg_ctx *ctx, tsg_stats *out);
 /* User timing events on the compute stream (slot 0..7): record, then the
    elapsed device time between two recorded slots (synchronises on `to`). */
+/* Numeric-kernel timing ring (timing on): tsg_numeric_calls = numeric phases
+   run so far; tsg_numeric_ms = device time of the numeric kernels of call k
+   (one of the last 32), read without synchronising the calls after it. */
+int tsg_numeric_calls(tsg_ctx *ctx, int64_t *n);
+int tsg_numeric_ms(tsg_ctx *ctx, int64_t call, float *ms);
 int tsg_event_record(tsg_ctx *ctx, int slot);
 int tsg_event_elapsed(tsg_ctx *ctx, int from, int to, float *ms);
 /* Device-to-device import of a CSR whose arrays already live on this device

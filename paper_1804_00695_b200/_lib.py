@@ -44,7 +44,7 @@ EXPORTS = (
     "tsg_numeric_fused", "tsg_masked_count", "tsg_event_record", "tsg_event_elapsed",
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
-    "tsg_graph_lower", "tsg_rmat_graph",
+    "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
 )
 
 _P = ctypes.c_void_p
@@ -85,6 +85,8 @@ _SIGS = {
     "tsg_numeric_fused": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _PP], ctypes.c_int),
     "tsg_masked_count": ([_P, _P, _P, _PI64], ctypes.c_int),
     "tsg_graph_lower": ([_P, _P, ctypes.c_int, _PP, _P], ctypes.c_int),
+    "tsg_numeric_calls": ([_P, _PI64], ctypes.c_int),
+    "tsg_numeric_ms": ([_P, _I64, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                         ctypes.c_double, ctypes.c_double, _PP], ctypes.c_int),
     "tsg_event_record": ([_P, ctypes.c_int], ctypes.c_int),
@@ -211,6 +213,16 @@ class Context:
 
     def record(self, slot):
         check(load().tsg_event_record(self.h, slot))
+
+    def numeric_calls(self) -> int:
+        v = ctypes.c_int64(0)
+        check(load().tsg_numeric_calls(self.h, ctypes.byref(v)))
+        return v.value
+
+    def numeric_ms(self, call: int) -> float:
+        v = ctypes.c_float()
+        check(load().tsg_numeric_ms(self.h, int(call), ctypes.byref(v)))
+        return v.value
 
     def elapsed_ms(self, a, b):
         v = ctypes.c_float()

@@ -79,6 +79,11 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
         TSG_CK(cudaEventCreate(&c->ev_num[i]));
         TSG_CK(cudaEventCreate(&c->ev_sym[i]));
     }
+    for (int i = 0; i < 2 * tsg_ctx::NRING; i++) TSG_CK(cudaEventCreate(&c->ev_ring[i]));
+    for (int i = 0; i < tsg_ctx::NRING; i++) c->ring_timed[i] = -1;
+    c->num_calls = 0;
+    c->pending = nullptr;
+    c->phase_n = c->phase_total = c->phase_dirty = 0;
     c->timing = 0;
     *out = c;
     return TSG_OK;
@@ -102,6 +107,25 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
 
 extern "C" int tsg_sync(tsg_ctx *c) {
     TSG_CK(cudaStreamSynchronize(c->stream));
+    if (c->pending) return tsg_check_kernel_errors(c, c->pending);
+    return TSG_OK;
+}
+
+extern "C" int tsg_numeric_calls(tsg_ctx *c, int64_t *n) {
+    *n = c->num_calls;
+    return TSG_OK;
+}
+
+extern "C" int tsg_numeric_ms(tsg_ctx *c, int64_t call, float *ms) {
+    if (call < 0 || call >= c->num_calls || c->num_calls - call > tsg_ctx::NRING ||
+        c->ring_timed[call % tsg_ctx::NRING] != call) {
+        tsg_set_error("numeric call %lld is not in the timing ring (timing off or too old)",
+                      (long long)call);
+        return TSG_EARG;
+    }
+    const int k = (int)(call % tsg_ctx::NRING);
+    TSG_CK(cudaEventSynchronize(c->ev_ring[2 * k + 1]));
+    TSG_CK(cudaEventElapsedTime(ms, c->ev_ring[2 * k], c->ev_ring[2 * k + 1]));
     return TSG_OK;
 }
 
@@ -162,16 +186,24 @@ extern "C" int tsg_get_stats(tsg_ctx *c, tsg_stats *st) {
 }
 
 extern "C" int tsg_last_phase_ms(tsg_ctx *c, float *out, int n) {
+    if (c->phase_dirty) {   // evaluated on demand: multiplies never wait for their timers
+        const int m = c->phase_n;
+        TSG_CK(cudaEventSynchronize(c->ev[m - 1]));
+        for (int i = 0; i + 1 < m && i < 8; i++)
+            TSG_CK(cudaEventElapsedTime(&c->phase_ms[i], c->ev[i], c->ev[i + 1]));
+        if (c->phase_total < 8)
+            TSG_CK(cudaEventElapsedTime(&c->phase_ms[c->phase_total], c->ev[0], c->ev[m - 1]));
+        c->phase_dirty = 0;
+    }
     for (int i = 0; i < n && i < 8; i++) out[i] = c->phase_ms[i];
     return TSG_OK;
 }
 
 void PhaseTimer::finish(int total_slot) {
     if (!ctx->timing || n < 2) return;
-    cudaEventSynchronize(ctx->ev[n - 1]);
-    for (int i = 0; i + 1 < n && i < 8; i++)
-        cudaEventElapsedTime(&ctx->phase_ms[i], ctx->ev[i], ctx->ev[i + 1]);
-    if (total_slot < 8) cudaEventElapsedTime(&ctx->phase_ms[total_slot], ctx->ev[0], ctx->ev[n - 1]);
+    ctx->phase_n = n;
+    ctx->phase_total = total_slot;
+    ctx->phase_dirty = 1;
 }
 
 // ------------------------------------------------------------------ memory
@@ -389,8 +421,15 @@ int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size
     return TSG_ECUDA;
 }
 
+int tsg_pending_errors(tsg_ctx *c) {
+    const int *h = reinterpret_cast<const int *>(c->h_small + 46);
+    if (h[0] == KERR_NONE) return TSG_OK;
+    return tsg_check_kernel_errors(c, c->pending ? c->pending : "kernel");
+}
+
 int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
     int h[2];
+    c->pending = nullptr;
     TSG_CK(cudaGetLastError());
     TSG_CK(cudaMemcpyAsync(h, c->d_err, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
@@ -783,6 +822,7 @@ extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
                                 int64_t *col_idx, double *values) {
     if (m->host_mapped) {   // already in host memory: widen on the host
         TSG_CK(cudaStreamSynchronize(c->stream));
+        if (c->pending) TSG_TRY(tsg_check_kernel_errors(c, c->pending));
         if (row_ptr) memcpy(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t));
         if (col_idx)
             for (int64_t i = 0; i < m->nnz; ++i) col_idx[i] = m->col[i];
@@ -804,6 +844,7 @@ extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
         TSG_CK(cudaMemcpyAsync(values, m->val, m->nnz * sizeof(double), cudaMemcpyDeviceToHost,
                                c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
+    if (c->pending) return tsg_check_kernel_errors(c, c->pending);   // the producer's errors
     return TSG_OK;
 }
 

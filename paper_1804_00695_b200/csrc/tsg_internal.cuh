@@ -40,6 +40,16 @@ struct tsg_ctx {
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
     cudaEvent_t ev_user[8];   // tsg_event_record slots
     int c_host_out;           // tsg_multiply_placed: build C in mapped host memory
+    // lazily evaluated PhaseTimer (no sync at the end of a multiply)
+    int phase_n, phase_total, phase_dirty;
+    // kernel-error check deferred to the next synchronising call (download,
+    // partition read-back, tsg_sync): the phase it belongs to
+    const char *pending;
+    // numeric-kernel event ring: call k's events are ev_ring[2 (k % NRING)] .. +1
+    static constexpr int NRING = 32;
+    cudaEvent_t ev_ring[2 * NRING];
+    int64_t num_calls;
+    int64_t ring_timed[NRING];   // call id recorded in each ring slot (-1: none)
 };
 
 struct tsg_csr {
@@ -106,6 +116,9 @@ inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
 }
 // Reads and clears the device error flag (synchronises the compute stream).
 int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
+// after a stream sync that also copied d_err into h_small[46]: report a
+// pending (deferred) kernel error, if any
+int tsg_pending_errors(tsg_ctx *ctx);
 
 int tsg_trace_enabled();
 // TSG_TRACE=1: host timestamps + GPU drain per traced step (debug only)

@@ -1472,15 +1472,30 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.pstart = nullptr;
         na.plen_in = nullptr;
         na.plen_out = nullptr;
-        if (c->timing) cudaEventRecord(c->ev_num[0], c->stream);
+        const int rk = (int)(c->num_calls % tsg_ctx::NRING);
+        if (c->timing) {
+            cudaEventRecord(c->ev_num[0], c->stream);
+            cudaEventRecord(c->ev_ring[2 * rk], c->stream);
+        }
         TSG_TRY(run_numeric_bins(c, bl, na));
-        if (c->timing) cudaEventRecord(c->ev_num[1], c->stream);
+        if (c->timing) {
+            cudaEventRecord(c->ev_num[1], c->stream);
+            cudaEventRecord(c->ev_ring[2 * rk + 1], c->stream);
+            c->ring_timed[rk] = c->num_calls;
+        } else {
+            c->ring_timed[rk] = -1;
+        }
     }
     if (bl.list) TSG_TRY(tsg_free(c, bl.list));
     TSG_TRY(tsg_free(c, bins));
     TSG_TRY(tsg_free(c, sbound));
     if (pt) pt->mark();
-    int s = tsg_check_kernel_errors(c, "numeric");
+    ++c->num_calls;
+    // kernel errors (count mismatch, probe overflow) are checked at the next
+    // synchronising call -- the download of C, the next partition read-back
+    // or tsg_sync -- so the host can queue the next multiply while these run
+    c->pending = "numeric";
+    int s = TSG_OK;
     if (C->host_mapped) tsg_free(c, cptr);
     C->sorted = 1;   // every emitted row lists its columns in ascending order
     if (s != TSG_OK) {
