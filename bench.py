@@ -91,16 +91,22 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.monotonic()   # nvidia-smi takes a moment to print its first line
+            while not self.lines and time.monotonic() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
+    def mark(self, which):
+        setattr(self, which, time.monotonic())
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
     def stop(self):
         if not self.proc:
@@ -112,7 +118,11 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples taken inside the timed region (else the ones around it)
+        lo, hi = getattr(self, "t_begin", None), getattr(self, "t_end", None)
+        inside = [ln for t, ln in self.lines if lo is not None and hi is not None and lo <= t <= hi + 0.01]
+        chosen = inside or [ln for _, ln in self.lines[-3:]]
+        for ln in chosen:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -126,7 +136,8 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "samples_in_timed_region": len(inside)}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -184,7 +195,7 @@ def run_reference(args, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -295,6 +306,7 @@ def main():
     torch.cuda.synchronize()
     ctx.sync()
     sampler.start()
+    sampler.mark("t_begin")
     l0 = ctx.stats()[0]
     times, num_times = [], []
     offs = None
@@ -310,6 +322,7 @@ def main():
     l1 = ctx.stats()[0]
     ctx.sync()
     torch.cuda.synchronize()
+    sampler.mark("t_end")
     if dist:
         dist.barrier()
     clocks = sampler.stop()
