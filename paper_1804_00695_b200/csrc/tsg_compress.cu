@@ -330,12 +330,14 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         k_compress_unit<<<grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream>>>(
             rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;
         TSG_CK(cudaGetLastError());
+        cm->sorted_sets = 1;   // one set per row
         *out = cm;
         return TSG_OK;
     }
     if (nnz == 0) {
         TSG_CK(cudaMemsetAsync(cm->start, 0, (rows + 1) * sizeof(int64_t), c->stream));
         TSG_CK(cudaMemsetAsync(cm->cnt, 0, (rows + 1) * sizeof(int32_t), c->stream));
+        cm->sorted_sets = 1;
         *out = cm;
         return TSG_OK;
     }
@@ -380,6 +382,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_free(c, bcnt);
     tsg_free(c, fcnt);
     tsg_free(c, fstart);
+    cm->sorted_sets = b->sorted;   // first-touch order of a row-sorted B ascends
     *out = cm;
     return TSG_OK;
 }

@@ -422,7 +422,7 @@ int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size
 }
 
 int tsg_pending_errors(tsg_ctx *c) {
-    const int *h = reinterpret_cast<const int *>(c->h_small + 46);
+    const int *h = reinterpret_cast<const int *>(c->h_small + 62);
     if (h[0] == KERR_NONE) return TSG_OK;
     return tsg_check_kernel_errors(c, c->pending ? c->pending : "kernel");
 }
@@ -684,6 +684,7 @@ int tsg_vec_alloc(tsg_ctx *c, int64_t n, bool aux, tsg_vec **out) {
 int tsg_cmat_alloc(tsg_ctx *c, int64_t rows, int64_t cap, tsg_cmat **out) {
     tsg_cmat *m = new tsg_cmat();
     m->rows = rows;
+    m->sorted_sets = 0;
     m->cap = cap;
     m->start = nullptr;
     m->cnt = nullptr;

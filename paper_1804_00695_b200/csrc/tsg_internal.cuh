@@ -69,6 +69,7 @@ struct tsg_cmat {
     int32_t *set;     // capacity >= nsets
     uint64_t *bits;
     int64_t cap;      // entries allocated in set/bits
+    int sorted_sets;  // 1: every row's sets ascend (compact compression of a row-sorted B)
 };
 
 struct tsg_vec {
@@ -116,7 +117,7 @@ inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
 }
 // Reads and clears the device error flag (synchronises the compute stream).
 int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
-// after a stream sync that also copied d_err into h_small[46]: report a
+// after a stream sync that also copied d_err into h_small[62]: report a
 // pending (deferred) kernel error, if any
 int tsg_pending_errors(tsg_ctx *ctx);
 

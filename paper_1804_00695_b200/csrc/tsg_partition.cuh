@@ -86,7 +86,7 @@ struct NoMid {
 template <int NB, class F, class Mid = NoMid>
 int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid()) {
-    static_assert(32 + NB + 2 <= 46, "partition results overlap the error copy / d_small flags");
+    static_assert(32 + NB + 2 <= 48, "partition results overlap the d_small flags");
     int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
     if (ntiles < 1) ntiles = 1;
     int *tc = nullptr;
@@ -103,7 +103,7 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_CK(cudaMemcpyAsync(c->h_small + 32, c->d_small + 32, (NB + 2) * sizeof(int64_t),
                            cudaMemcpyDeviceToHost, c->stream));
     // deferred kernel errors of earlier work ride along with the same sync
-    TSG_CK(cudaMemcpyAsync(c->h_small + 46, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+    TSG_CK(cudaMemcpyAsync(c->h_small + 62, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                            c->stream));
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));

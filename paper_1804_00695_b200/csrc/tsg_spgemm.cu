@@ -185,7 +185,7 @@ __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
 // shared memory (table + dense values).  CTA tier: one row per CTA, table in
 // shared memory.  Global tier: one row per CTA, table in a global slab.
 
-constexpr int NBINS = 10;
+constexpr int NBINS = 13;   // 0-6 group, 7-8 CTA, 9 global, 10-12 symbolic merge tier
 // bins 0..6: group tier slices (bytes) and group sizes
 __host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
 __host__ __device__ constexpr int gt_g(int b) { return b <= 1 ? 8 : (b == 2 ? 16 : 32); }
@@ -196,6 +196,12 @@ __host__ __device__ constexpr int gt_block(int b) { return b <= 4 ? 256 : (b == 
 __host__ __device__ constexpr int ct_slots(int cb) { return 2048 << (2 * cb); }
 __host__ __device__ constexpr int ct_nt(int cb) { return 256 << cb; }
 constexpr int BIN_GLOBAL = 9;
+// bins 10..12 (symbolic only): k-way merge of the row's sorted compressed B
+// rows, one list per lane -- G = 8/16/32 lanes, lists staged in SLICE bytes
+__host__ __device__ constexpr int mt_g(int m) { return 8 << m; }
+__host__ __device__ constexpr int mt_slice(int m) { return 1024 << m; }
+__host__ __device__ constexpr int mt_cap(int m) { return mt_slice(m) / 12; }   // staged (set, mask) pairs
+constexpr int BIN_MERGE = 10;
 
 __host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
@@ -242,10 +248,21 @@ struct SymBinF {
     int64_t *counts;
     int32_t *msets;
     int64_t *scap;
+    const int64_t *arp;   // non-null: merge tier allowed (row-sorted B, no partial rows)
+    int64_t a_row_off;
     __device__ __forceinline__ int operator()(int64_t i) const {
         const int64_t sb = sbound[i];
-        const int b = sym_bin(sb);
-        scap[i] = b < 7 ? sb : 0;   // sorted sets are emitted by the group tier
+        int b = sym_bin(sb);
+        if (arp && b != 255) {
+            // few A entries, bounded staging: merge the sorted lists instead of hashing
+            const int64_t alen = arp[i + a_row_off + 1] - arp[i + a_row_off];
+            for (int m = 0; m < 3; ++m)
+                if (alen <= mt_g(m) && sb <= mt_cap(m)) {
+                    b = BIN_MERGE + m;
+                    break;
+                }
+        }
+        scap[i] = (b < 7 || b >= BIN_MERGE) ? sb : 0;   // these tiers emit sorted sets
         if (b == 255) {
             counts[i] = 0;
             if (msets) msets[i] = 0;
@@ -407,6 +424,107 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
         __syncwarp(gm);
     }
 }
+
+// Merge tier: a row with at most G A entries whose compressed B rows are
+// sorted by set (compact compression of a row-sorted B).  Lane j stages list j
+// (its A entry's compressed row) in shared memory, then the group repeatedly
+// takes the minimum head set (shuffle min), ORs the masks of the lanes holding
+// it (shuffle OR) and advances them: the union comes out already sorted and
+// de-duplicated -- no table, no atomics, no sort.
+template <int G, int SLICE>
+__global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ list, int64_t nlist,
+                                                   SymArgs a) {
+    extern __shared__ int4 smem[];
+    constexpr int CAP = SLICE / 12;
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    const int g = threadIdx.x / G;
+    uint64_t *lbits = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + (size_t)g * SLICE);
+    int32_t *lset = reinterpret_cast<int32_t *>(lbits + CAP);
+    for (int64_t li = (int64_t)blockIdx.x * gpb + g; li < nlist; li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+        int64_t st = 0;
+        int cnt = 0;
+        if (a0 + glane < a1) {
+            int k = a.acol[a0 + glane];
+            if (k >= a.b_lo && k < a.b_hi) {
+                k -= a.b_lo;
+                st = a.cbstart[k];
+                cnt = a.cbcnt[k];
+            }
+        }
+        const int incl = group_incl_scan<G, int>(gm, cnt, glane);
+        const int off = incl - cnt;
+        // stage the list (independent loads, four in flight per lane)
+        for (int q0 = 0; q0 < cnt; q0 += 4) {
+            int sv[4];
+            uint64_t bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u < cnt ? q0 + u : cnt - 1;
+                sv[u] = a.cbset[st + q];
+                bv[u] = a.cbbits[st + q];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q0 + u < cnt) {
+                    lset[off + q0 + u] = sv[u];
+                    lbits[off + q0 + u] = bv[u];
+                }
+        }
+        __syncwarp(gm);
+        int p = off;
+        const int e = off + cnt;
+        int hs = p < e ? lset[p] : INT32_MAX;
+        uint64_t hb = p < e ? lbits[p] : 0ull;
+        const int64_t sp = a.sptr[i];
+        int m = 0, total = 0;
+        for (;;) {
+            // one butterfly carries (head, mask): the smaller head wins, equal
+            // heads OR their masks -> every lane ends with (min, OR of its holders)
+            int mn = hs;
+            unsigned lo = (unsigned)hb, hi = (unsigned)(hb >> 32);
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) {
+                const int ok = __shfl_xor_sync(gm, mn, d, G);
+                const unsigned olo = __shfl_xor_sync(gm, lo, d, G);
+                const unsigned ohi = __shfl_xor_sync(gm, hi, d, G);
+                if (ok < mn) {
+                    mn = ok;
+                    lo = olo;
+                    hi = ohi;
+                } else if (ok == mn) {
+                    lo |= olo;
+                    hi |= ohi;
+                }
+            }
+            if (mn == INT32_MAX) break;
+            const bool mine = hs == mn;
+            if (glane == 0) {
+                a.oset[sp + m] = mn;
+                a.obits[sp + m] = ((uint64_t)hi << 32) | lo;
+            }
+            total += __popc(lo) + __popc(hi);
+            ++m;
+            if (mine) {
+                ++p;
+                hs = p < e ? lset[p] : INT32_MAX;
+                hb = p < e ? lbits[p] : 0ull;
+            }
+        }
+        if (glane == 0) {
+            a.counts[i] = total;
+            if (a.msets) a.msets[i] = m | SETS_WRITTEN;
+        }
+        __syncwarp(gm);
+    }
+}
+
+template <int M>
+int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 
 // ======================================================================= K4 group tier
 
@@ -1206,7 +1324,24 @@ int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     return TSG_OK;
 }
 
+template <int M>
+int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+    constexpr int G = mt_g(M), SL = mt_slice(M), BS = 256;
+    const int B = BIN_MERGE + M;
+    const int64_t n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return TSG_OK;
+    const size_t smem = (size_t)(BS / G) * SL;
+    TSG_TRY(set_smem(k_sym_merge<G, SL>, smem));
+    const unsigned grid = group_grid(c, n, BS / G);
+    k_sym_merge<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_merge", B, grid, BS, smem));
+    return TSG_OK;
+}
+
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+    TSG_TRY(launch_sym_merge<0>(c, bl, a));
+    TSG_TRY(launch_sym_merge<1>(c, bl, a));
+    TSG_TRY(launch_sym_merge<2>(c, bl, a));
     TSG_TRY(launch_sym_group<0>(c, bl, a));
     TSG_TRY(launch_sym_group<1>(c, bl, a));
     TSG_TRY(launch_sym_group<2>(c, bl, a));
@@ -1309,7 +1444,11 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         TSG_TRY(tsg_alloc_t(c, &v->sptr, rows_out + 1));
         Bins bl;
         int64_t set_cap = 0;
-        TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap}, bins, bl,
+        // merge tier only when the compressed rows are sorted by set (row-sorted
+        // B -> compact compression) and there is no partial row to fold in
+        const int64_t *merge_arp = (cb->sorted_sets && partial == nullptr) ? a->rp : nullptr;
+        TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off},
+                                     bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
         TSG_TRY(tsg_free(c, scap));
@@ -1577,7 +1716,7 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
     TSG_TRY(launch_num_group<4>(c, bl, na));
     TSG_TRY(launch_num_group<5>(c, bl, na));
     TSG_TRY(launch_num_group<6>(c, bl, na));
-    int64_t nbig = bl.off[NBINS] - bl.off[7];
+    int64_t nbig = bl.off[BIN_GLOBAL + 1] - bl.off[7];
     int32_t *scol = nullptr;
     double *sval = nullptr;
     if (nbig > 0) {

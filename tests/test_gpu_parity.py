@@ -61,10 +61,12 @@ def test_compress_kats():
 
 
 def test_symbolic_and_numeric_random_pairs(rng):
-    for _ in range(60):
+    for it in range(80):
         n = int(rng.integers(4, 120))
-        a = random_csr(rng, n, n, 8)
-        b = random_csr(rng, n, n, 8)
+        a = random_csr(rng, n, n, 8 if it % 3 else 40)
+        b = random_csr(rng, n, n, 8 if it % 4 else 90)
+        if it % 2:   # row-sorted B: symbolic rows with <= 32 A entries take the merge tier
+            b = canonicalize(b)
         cb = tsg.compress(b)
         counts = tsg.spgemm_symbolic(a, cb)
         want_counts = O.symbolic(a, O.compress(b))
