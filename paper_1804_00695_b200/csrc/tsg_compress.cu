@@ -331,6 +331,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
             rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;
         TSG_CK(cudaGetLastError());
         cm->sorted_sets = 1;   // one set per row
+        cm->identity_rows = (nnz == rows && b->max_row == 1) ? 1 : 0;
         *out = cm;
         return TSG_OK;
     }

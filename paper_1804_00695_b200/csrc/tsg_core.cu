@@ -685,6 +685,7 @@ int tsg_cmat_alloc(tsg_ctx *c, int64_t rows, int64_t cap, tsg_cmat **out) {
     tsg_cmat *m = new tsg_cmat();
     m->rows = rows;
     m->sorted_sets = 0;
+    m->identity_rows = 0;
     m->cap = cap;
     m->start = nullptr;
     m->cnt = nullptr;

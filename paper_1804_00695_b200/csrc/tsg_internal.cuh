@@ -70,6 +70,7 @@ struct tsg_cmat {
     uint64_t *bits;
     int64_t cap;      // entries allocated in set/bits
     int sorted_sets;  // 1: every row's sets ascend (compact compression of a row-sorted B)
+    int identity_rows;  // 1: row k is exactly set k (start = iota, cnt = 1)
 };
 
 struct tsg_vec {

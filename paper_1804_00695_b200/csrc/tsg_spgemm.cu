@@ -55,6 +55,7 @@ struct SymArgs {
     int32_t *oset;
     uint64_t *obits;
     const int *maxcb;    // device max sets per compressed B row (<= 1: unit path)
+    int unit_dense;      // compressed row k is entry k (every B row holds exactly one set)
 };
 
 constexpr int SETS_WRITTEN = 1 << 30;
@@ -95,6 +96,7 @@ struct NumArgs {
     int32_t *plen_out;
     const int *unit_b;   // device flag: every B row has <= 1 entry (read if unit_known < 0)
     int unit_known;      // 1 / 0: known on the host (uploaded B), -1: read *unit_b
+    int unit_dense;      // B row k is entry k (every row exactly one entry): no row_ptr gather
 };
 
 __device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
@@ -324,10 +326,18 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                 }
                 int64_t ss[UB];
                 bool has[UB];
+                if (a.unit_dense) {
 #pragma unroll
-                for (int u = 0; u < UB; ++u) {
-                    ss[u] = kk[u] >= 0 ? a.cbstart[kk[u]] : 0;
-                    has[u] = kk[u] >= 0 && a.cbcnt[kk[u]] > 0;
+                    for (int u = 0; u < UB; ++u) {
+                        ss[u] = kk[u] >= 0 ? kk[u] : 0;
+                        has[u] = kk[u] >= 0;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                        ss[u] = kk[u] >= 0 ? a.cbstart[kk[u]] : 0;
+                        has[u] = kk[u] >= 0 && a.cbcnt[kk[u]] > 0;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
@@ -661,12 +671,21 @@ __device__ __forceinline__ void products_unit(unsigned gm, int glane, const NumA
         }
         int64_t ss[UB];
         bool has[UB];
+        if (a.unit_dense) {   // row_ptr is the identity: one dependent load round fewer
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-            const int k = kk[u];
-            const bool in = k >= a.b_lo && k < a.b_hi;
-            ss[u] = in ? a.brp[k - a.b_lo] : 0;
-            has[u] = in && a.brp[k - a.b_lo + 1] > ss[u];
+            for (int u = 0; u < UB; ++u) {
+                const int k = kk[u];
+                has[u] = k >= a.b_lo && k < a.b_hi;
+                ss[u] = has[u] ? k - a.b_lo : 0;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int k = kk[u];
+                const bool in = k >= a.b_lo && k < a.b_hi;
+                ss[u] = in ? a.brp[k - a.b_lo] : 0;
+                has[u] = in && a.brp[k - a.b_lo + 1] > ss[u];
+            }
         }
         int cc[UB];
         double pp[UB];
@@ -1474,6 +1493,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.oset = v->sset;
         sa.obits = v->sbits;
         sa.maxcb = maxcb;
+        sa.unit_dense = cb->identity_rows;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
@@ -1597,6 +1617,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.sptr = counts->sptr;
         na.sset = counts->sset;
         na.sbits = counts->sbits;
+        na.unit_dense = (b->max_row == 1 && b->nnz == b->rows) ? 1 : 0;
         if (b->max_row >= 0) {   // known since upload: no device check
             na.unit_known = b->max_row <= 1 ? 1 : 0;
             na.unit_b = nullptr;
