@@ -4,21 +4,21 @@
 // order.  The output is COMPACT (start[r] .. start[r+1]) and built by
 // entry-parallel, fully coalesced passes -- no per-row serial loops, no
 // scattered narrow stores:
-//   P0  row-start bitmap (one bit per entry)                      rows
-//   P1  head flags: entry t opens a set if it starts its row or its set
-//       differs from entry t-1's; per-warp head words, per-block counts;
-//       a set that goes DOWN inside a row flags the matrix unsorted    nnz
-//   P2  exclusive scan of the block counts                          nnz/256
-//   P3  each head ORs its run of bits and writes (set, mask) at its
-//       global rank (consecutive heads -> consecutive addresses)       nnz
-//   P4  start[r] = rank of the first entry of row r                   rows
+//   P0  row-start bitmap (one bit per entry)                          rows
+//   P1  one pass per 8192-entry tile: head flags (an entry opens a set if
+//       it starts its row or its set differs from entry t-1's; a set that
+//       goes DOWN inside a row flags the matrix unsorted), block scan,
+//       decoupled look-back for the tile's global rank, then every head ORs
+//       its run of bits and the tile's (set, mask) pairs are written
+//       coalesced at consecutive ranks                                 nnz
+//   P2  start[r] = rank of the first entry of row r                    rows
 // For a row-sorted matrix (every generator here, and any CsrMatrix built
 // with from_coo) the first set of a run is its first touch, so this equals
-// the reference's dict order.  If P1 saw an unsorted row, P3/P4 exit and the
-// first-occurrence fallback (F1 count, scan, F2 write: entry t heads its set
-// iff no EARLIER entry of the row has the same set) rebuilds the whole
-// matrix.  The fallback kernels are launched unconditionally and exit at
-// once on sorted input, so compression never synchronises the host.
+// the reference's dict order.  Matrices not known to be row-sorted also get
+// the first-occurrence fallback (F1 count, scan, F2 write: entry t heads its
+// set iff no EARLIER entry of the row has the same set), whose kernels exit
+// at once unless P1 flagged an unsorted row; compression never synchronises
+// the host.
 #include "tsg_internal.cuh"
 
 namespace {
@@ -77,64 +77,6 @@ __device__ __forceinline__ void word_from_smem(const int4 *__restrict__ sm, int 
     }
 }
 
-// P1: head mask of each word (an entry opens a set if its row starts there or
-// its set differs from the previous entry's), block-relative word prefixes,
-// block totals; a set that goes down inside a row flags the matrix unsorted.
-__global__ void __launch_bounds__(CT) k_heads(int64_t nnz, const int32_t *__restrict__ col,
-                                             const uint32_t *__restrict__ rsbits,
-                                             uint32_t *__restrict__ hbits,
-                                             uint16_t *__restrict__ wpre,
-                                             int64_t *__restrict__ bcnt, int *unsorted) {
-    __shared__ int4 s_col[PB / 4];
-    __shared__ int s_w[CT / 32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
-    const int64_t t0 = word * 32;
-    stage_cols(col, nnz, (int64_t)blockIdx.x * PB, s_col);
-    __syncthreads();
-    int n = 0;
-    uint32_t hw = 0;
-    bool bad = false;
-    if (t0 < nnz) {
-        int c[32];
-        word_from_smem(s_col, c);
-        const uint32_t rs = rsbits[word];
-        int prev;
-        if (threadIdx.x > 0) {
-            const int pw = threadIdx.x - 1;
-            prev = reinterpret_cast<const int *>(s_col)[(pw * 8 + (7 ^ (pw & 7))) * 4 + 3] >> 6;
-        } else {
-            prev = t0 > 0 ? (__ldg(col + t0 - 1) >> 6) : -1;
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const int sv = c[q] >> 6;
-            const bool valid = t0 + q < nnz;
-            const bool start = (rs >> q) & 1u;
-            const bool head = valid && (start || t0 + q == 0 || sv != prev);
-            bad |= valid && !start && t0 + q > 0 && sv < prev;
-            hw |= (uint32_t)head << q;
-            prev = sv;
-        }
-        hbits[word] = hw;
-        n = __popc(hw);
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
-    // block-relative exclusive prefix of the words' head counts
-    int x = n;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += o;
-    }
-    if (lane == 31) s_w[w] = x;
-    __syncthreads();
-    int woff = 0;
-    for (int j = 0; j < w; ++j) woff += s_w[j];
-    if (t0 < nnz) wpre[word] = (uint16_t)(woff + x - n);
-    if (threadIdx.x == CT - 1) bcnt[blockIdx.x] = woff + x;
-}
-
 // P3: each thread walks its word's runs in registers and emits every run it
 // owns; a run that started in an earlier word belongs to that word's thread,
 // which reads ahead until the next head.  The block's runs form one
@@ -149,31 +91,127 @@ constexpr int EMIT_CAP = 4096;   // staged runs per block (~50 KB); more -> dire
 constexpr int EMIT_PAD = EMIT_CAP + EMIT_CAP / 32;
 constexpr size_t EMIT_SMEM = (size_t)EMIT_PAD * 12 > (size_t)PB * 4 ? (size_t)EMIT_PAD * 12 : (size_t)PB * 4;
 
-__global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__restrict__ col,
-                                                 const uint32_t *__restrict__ hbits,
-                                                 const uint16_t *__restrict__ wpre,
-                                                 const int64_t *__restrict__ boff,
-                                                 int32_t *__restrict__ oset,
-                                                 uint64_t *__restrict__ obits,
-                                                 const int *unsorted) {
-    if (*unsorted) return;
+// P1+P2+P3 in one pass (single launch, columns read once): each tile finds
+// its heads, scans them block-wide, obtains its global run offset by a
+// decoupled look-back over the tiles before it (tile ids from an atomic
+// counter, state words pack (prefix << 2 | flag)), publishes hbits / wpre /
+// boff for k_set_starts and emits its runs.  A run that continues past the
+// word is extended by reading columns directly (row-start bitmap + set
+// compare), so no tile waits on another tile's head bitmap.
+__device__ __forceinline__ unsigned long long lb_ld(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void lb_st(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(CT) k_compress_onepass(
+    int64_t nnz, const int32_t *__restrict__ col, const uint32_t *__restrict__ rsbits,
+    uint32_t *__restrict__ hbits, uint16_t *__restrict__ wpre, int64_t *__restrict__ boff,
+    int64_t nblocks, unsigned long long *state, unsigned *counter, int32_t *__restrict__ oset,
+    uint64_t *__restrict__ obits, int *unsorted) {
     extern __shared__ int4 esm[];
+    __shared__ int s_w[CT / 32];
+    __shared__ int64_t s_b0;
+    __shared__ unsigned s_tile;
     uint32_t *s_lo = reinterpret_cast<uint32_t *>(esm);
     uint32_t *s_hi = s_lo + EMIT_PAD;
     int32_t *s_set = reinterpret_cast<int32_t *>(s_hi + EMIT_PAD);
-    const int64_t word = (int64_t)blockIdx.x * CT + threadIdx.x;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t word = tile * CT + threadIdx.x;
     const int64_t t0 = word * 32;
-    const int64_t b0 = boff[blockIdx.x];
-    const int nrun = (int)(boff[blockIdx.x + 1] - b0);
-    const bool staged = nrun <= EMIT_CAP;
-    const uint32_t hw = t0 < nnz ? hbits[word] : 0u;
-    stage_cols(col, nnz, (int64_t)blockIdx.x * PB, esm);
+    stage_cols(col, nnz, tile * PB, esm);
     __syncthreads();
     int c[32];
     word_from_smem(esm, c);
+    int prev;
+    if (threadIdx.x > 0) {
+        const int pw = threadIdx.x - 1;
+        prev = reinterpret_cast<const int *>(esm)[(pw * 8 + (7 ^ (pw & 7))) * 4 + 3] >> 6;
+    } else {
+        prev = t0 > 0 && t0 < nnz + 1 ? (__ldg(col + t0 - 1) >> 6) : -1;
+    }
     __syncthreads();   // the column stage is reused for the output below
+    uint32_t hw = 0, rs = 0;
+    bool bad = false;
+    if (t0 < nnz) {
+        rs = rsbits[word];
+        int pv = prev;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const int sv = c[q] >> 6;
+            const bool valid = t0 + q < nnz;
+            const bool start = (rs >> q) & 1u;
+            const bool head = valid && (start || t0 + q == 0 || sv != pv);
+            bad |= valid && !start && t0 + q > 0 && sv < pv;
+            hw |= (uint32_t)head << q;
+            pv = sv;
+        }
+        hbits[word] = hw;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
+    const int n = __popc(hw);
+    int x = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    int woff = 0, agg = 0;
+#pragma unroll
+    for (int j = 0; j < CT / 32; ++j) {
+        woff += j < w ? s_w[j] : 0;
+        agg += s_w[j];
+    }
+    const int r0 = woff + x - n;   // block-relative rank of this word's first head
+    if (t0 < nnz) wpre[word] = (uint16_t)r0;
+    // decoupled look-back for the tile's global offset
+    if (w == 0) {
+        if (tile == 0) {
+            if (lane == 0) {
+                lb_st(&state[0], ((unsigned long long)agg << 2) | 2ull);
+                s_b0 = 0;
+            }
+        } else {
+            if (lane == 0) lb_st(&state[tile], ((unsigned long long)agg << 2) | 1ull);
+            int64_t excl = 0;
+            int64_t pred = tile - 1 - lane;
+            for (;;) {
+                const unsigned long long sv = pred >= 0 ? lb_ld(&state[pred]) : 2ull;
+                const unsigned flag = (unsigned)(sv & 3ull);
+                if (__any_sync(0xffffffffu, flag == 0)) continue;
+                const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+                int64_t val = (int64_t)(sv >> 2);
+                if (incl && lane > __ffs(incl) - 1) val = 0;
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+                excl += val;
+                if (incl) break;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                lb_st(&state[tile], ((unsigned long long)(excl + agg) << 2) | 2ull);
+                s_b0 = excl;
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t b0 = s_b0;
+    if (threadIdx.x == 0) {
+        boff[tile] = b0;
+        if (tile == nblocks - 1) boff[nblocks] = b0 + agg;
+    }
+    const bool staged = agg <= EMIT_CAP;
     if (hw) {
-        int r = wpre[word];   // block-relative rank of this word's first head
+        int r = r0;
         int set = -1;
         uint64_t bits = 0;
         auto put = [&](int rr, int st, uint64_t bb) {
@@ -202,18 +240,21 @@ __global__ void __launch_bounds__(CT) k_emit_sets(int64_t nnz, const int32_t *__
                 bits |= b;
             }
         }
-        for (int64_t g = t0 + 32; g < nnz; ++g) {   // the last run may continue
-            if ((hbits[g >> 5] >> (g & 31)) & 1u) break;
-            bits |= 1ull << (__ldg(col + g) & 63);
+        // the last run may continue into the next words: same row, same set
+        for (int64_t g = t0 + 32; g < nnz; ++g) {
+            if ((__ldg(rsbits + (g >> 5)) >> (g & 31)) & 1u) break;
+            const int cg = __ldg(col + g);
+            if ((cg >> 6) != set) break;
+            bits |= 1ull << (cg & 63);
         }
         put(r, set, bits);
     }
     if (!staged) return;   // block-uniform
     __syncthreads();
-    for (int x = threadIdx.x; x < nrun; x += CT) {
-        const int px = x + (x >> 5);
-        oset[b0 + x] = s_set[px];
-        obits[b0 + x] = (uint64_t)s_lo[px] | ((uint64_t)s_hi[px] << 32);
+    for (int xx = threadIdx.x; xx < agg; xx += CT) {
+        const int px = xx + (xx >> 5);
+        oset[b0 + xx] = s_set[px];
+        obits[b0 + xx] = (uint64_t)s_lo[px] | ((uint64_t)s_hi[px] << 32);
     }
 }
 
@@ -359,12 +400,14 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_CK(cudaMemsetAsync(unsorted, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(rows + 1, 256, c->num_sms * 16);
     k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits); ++c->launches;
-    k_heads<<<(unsigned)nblocks, CT, 0, s>>>(nnz, b->col, rsbits, hbits, wpre, bcnt, unsorted); ++c->launches;
-    TSG_TRY(tsg_exclusive_scan_i64(c, bcnt, bcnt, nblocks));
+    unsigned long long *lbstate = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
+    TSG_CK(cudaMemsetAsync(lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
     const size_t esmem = EMIT_SMEM;
-    TSG_TRY(tsg_func_smem((const void *)k_emit_sets, esmem));
-    k_emit_sets<<<(unsigned)nblocks, CT, esmem, s>>>(nnz, b->col, hbits, wpre, bcnt, cm->set, cm->bits,
-                                                     unsorted); ++c->launches;
+    TSG_TRY(tsg_func_smem((const void *)k_compress_onepass, esmem));
+    k_compress_onepass<<<(unsigned)nblocks, CT, esmem, s>>>(
+        nnz, b->col, rsbits, hbits, wpre, bcnt, nblocks, lbstate,
+        reinterpret_cast<unsigned *>(lbstate + nblocks), cm->set, cm->bits, unsorted); ++c->launches;
     k_set_starts<<<rgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
                                        unsorted); ++c->launches;
     // first-occurrence fallback for input not known to be row-sorted: every
@@ -381,6 +424,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_free(c, hbits);
     tsg_free(c, wpre);
     tsg_free(c, bcnt);
+    tsg_free(c, lbstate);
     tsg_free(c, fcnt);
     tsg_free(c, fstart);
     cm->sorted_sets = b->sorted;   // first-touch order of a row-sorted B ascends
