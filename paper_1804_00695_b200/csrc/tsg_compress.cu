@@ -173,16 +173,14 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
     }
     const int r0 = woff + x - n;   // block-relative rank of this word's first head
     if (t0 < nnz) wpre[word] = (uint16_t)r0;
-    // decoupled look-back for the tile's global offset
-    if (w == 0) {
-        if (tile == 0) {
-            if (lane == 0) {
-                lb_st(&state[0], ((unsigned long long)agg << 2) | 2ull);
-                s_b0 = 0;
-            }
-        } else {
-            if (lane == 0) lb_st(&state[tile], ((unsigned long long)agg << 2) | 1ull);
-            int64_t excl = 0;
+    // publish the tile aggregate at once; the look-back for the tile's
+    // global rank runs after this warp's runs are staged, so its wait
+    // overlaps the emission work of the whole block
+    if (threadIdx.x == 0)
+        lb_st(&state[tile], ((unsigned long long)agg << 2) | (tile == 0 ? 2ull : 1ull));
+    auto look_back = [&]() {   // warp 0 only
+        int64_t excl = 0;
+        if (tile > 0) {
             int64_t pred = tile - 1 - lane;
             for (;;) {
                 const unsigned long long sv = pred >= 0 ? lb_ld(&state[pred]) : 2ull;
@@ -197,20 +195,21 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
                 if (incl) break;
                 pred -= 32;
             }
-            if (lane == 0) {
-                lb_st(&state[tile], ((unsigned long long)(excl + agg) << 2) | 2ull);
-                s_b0 = excl;
-            }
+            if (lane == 0) lb_st(&state[tile], ((unsigned long long)(excl + agg) << 2) | 2ull);
         }
+        if (lane == 0) {
+            s_b0 = excl;
+            boff[tile] = excl;
+            if (tile == nblocks - 1) boff[nblocks] = excl + agg;
+        }
+    };
+    const bool staged = agg <= EMIT_CAP;   // block-uniform
+    if (!staged) {   // rare (dense tiles): global rank first, then direct stores
+        if (w == 0) look_back();
+        __syncthreads();
     }
-    __syncthreads();
-    const int64_t b0 = s_b0;
-    if (threadIdx.x == 0) {
-        boff[tile] = b0;
-        if (tile == nblocks - 1) boff[nblocks] = b0 + agg;
-    }
-    const bool staged = agg <= EMIT_CAP;
     if (hw) {
+        const int64_t b0 = staged ? 0 : s_b0;
         int r = r0;
         int set = -1;
         uint64_t bits = 0;
@@ -249,8 +248,10 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
         }
         put(r, set, bits);
     }
-    if (!staged) return;   // block-uniform
+    if (!staged) return;
+    if (w == 0) look_back();
     __syncthreads();
+    const int64_t b0 = s_b0;
     for (int xx = threadIdx.x; xx < agg; xx += CT) {
         const int px = xx + (xx >> 5);
         oset[b0 + xx] = s_set[px];
