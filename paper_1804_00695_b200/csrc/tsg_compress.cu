@@ -378,8 +378,8 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         return TSG_OK;
     }
     if (nnz == 0) {
-        TSG_CK(cudaMemsetAsync(cm->start, 0, (rows + 1) * sizeof(int64_t), c->stream));
-        TSG_CK(cudaMemsetAsync(cm->cnt, 0, (rows + 1) * sizeof(int32_t), c->stream));
+        TSG_TRY(tsg_fill(c, cm->start, 0, (rows + 1) * sizeof(int64_t), c->stream));
+        TSG_TRY(tsg_fill(c, cm->cnt, 0, (rows + 1) * sizeof(int32_t), c->stream));
         cm->sorted_sets = 1;
         *out = cm;
         return TSG_OK;
@@ -397,13 +397,13 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_alloc_t(c, &fstart, rows + 1));
     int *unsorted = reinterpret_cast<int *>(c->d_small + 8);
     cudaStream_t s = c->stream;
-    TSG_CK(cudaMemsetAsync(rsbits, 0, nwords * sizeof(uint32_t), s));
-    TSG_CK(cudaMemsetAsync(unsorted, 0, sizeof(int), s));
+    TSG_TRY(tsg_fill(c, rsbits, 0, nwords * sizeof(uint32_t), s));
+    TSG_TRY(tsg_fill(c, unsorted, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(rows + 1, 256, c->num_sms * 16);
     k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits); ++c->launches;
     unsigned long long *lbstate = nullptr;
     TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
-    TSG_CK(cudaMemsetAsync(lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
+    TSG_TRY(tsg_fill(c, lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
     const size_t esmem = EMIT_SMEM;
     TSG_TRY(tsg_func_smem((const void *)k_compress_onepass, esmem));
     k_compress_onepass<<<(unsigned)nblocks, CT, esmem, s>>>(
@@ -432,3 +432,5 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     *out = cm;
     return TSG_OK;
 }
+
+const void *tsg_kernel_compress() { return (const void *)k_row_starts; }

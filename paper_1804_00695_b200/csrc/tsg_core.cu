@@ -11,6 +11,9 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <cuda.h>
+#include <vector>
+
 #include "tsg_internal.cuh"
 
 static thread_local char g_err[1024] = "";
@@ -70,7 +73,8 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaMalloc(&c->d_err, 4 * sizeof(int)));
     TSG_CK(cudaMemset(c->d_err, 0, 4 * sizeof(int)));
     TSG_CK(cudaMalloc(&c->d_small, 64 * sizeof(int64_t)));
-    TSG_CK(cudaMallocHost(&c->h_small, 64 * sizeof(int64_t)));
+    TSG_CK(cudaHostAlloc(&c->h_small, 64 * sizeof(int64_t), cudaHostAllocMapped));
+    TSG_CK(cudaHostGetDevicePointer(&c->hd_small, c->h_small, 0));
     int init_err[2] = {0, 0x7fffffff};
     TSG_CK(cudaMemcpy(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice));
     for (int i = 0; i < 8; i++) TSG_CK(cudaEventCreate(&c->ev[i]));
@@ -85,6 +89,13 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     c->pending = nullptr;
     c->phase_n = c->phase_total = c->phase_dirty = 0;
     c->timing = 0;
+    // every kernel loaded now, not at its first launch (see tsg_preload_module_of)
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_core()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_compress()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_spgemm()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_masked()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_chunk()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_graph()));
     *out = c;
     return TSG_OK;
 }
@@ -222,6 +233,12 @@ int tsg_trace_enabled() {
         on = (e && *e && *e != '0') ? 1 : 0;
     }
     return on;
+}
+
+void tsg_trace_host(const char *what) {
+    static int on = -1;
+    if (on < 0) on = getenv("TSG_CHUNK_TIMELINE") != nullptr;
+    if (on) fprintf(stderr, "[tsg host abs] %.1f us %s\n", now_us(), what);
 }
 
 void tsg_trace(tsg_ctx *c, const char *what, int64_t arg) {
@@ -421,6 +438,96 @@ int tsg_launch_check(const char *kernel, int bin, unsigned grid, int block, size
     return TSG_ECUDA;
 }
 
+namespace {
+__global__ void k_put_small(const int64_t *__restrict__ src, int64_t *__restrict__ dst, int n) {
+    if (threadIdx.x < n) dst[threadIdx.x] = src[threadIdx.x];
+}
+}  // namespace
+
+namespace {
+__global__ void k_fill(uint8_t *__restrict__ p, uint32_t word, size_t bytes) {
+    // 16-byte body (p is at least 16-byte aligned for arena blocks; the
+    // generic head / tail loops cover any other pointer)
+    const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+    const size_t h = head < bytes ? head : bytes;
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t nth = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < h; i += nth) p[i] = (uint8_t)word;
+    uint4 *q = reinterpret_cast<uint4 *>(p + h);
+    const size_t nv = (bytes - h) / 16;
+    const uint4 v = make_uint4(word, word, word, word);
+    for (size_t i = tid; i < nv; i += nth) q[i] = v;
+    for (size_t i = h + nv * 16 + tid; i < bytes; i += nth) p[i] = (uint8_t)word;
+}
+}  // namespace
+
+const void *tsg_kernel_core() { return (const void *)k_fill; }
+
+int tsg_fill(tsg_ctx *c, void *p, int byte, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return TSG_OK;
+    const uint32_t b = (uint32_t)(byte & 0xff);
+    const uint32_t word = b | (b << 8) | (b << 16) | (b << 24);
+    size_t blocks = (bytes / 16 + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    const size_t cap = (size_t)c->num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    k_fill<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<uint8_t *>(p), word, bytes); ++c->launches;
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+int tsg_preload_module_of(const void *kernel) {
+    typedef CUresult (*FnGetModule)(CUmodule *, CUfunction);
+    typedef CUresult (*FnCount)(unsigned int *, CUmodule);
+    typedef CUresult (*FnEnum)(CUfunction *, unsigned int, CUmodule);
+    typedef CUresult (*FnLoad)(CUfunction);
+    static FnGetModule get_module = nullptr;
+    static FnCount count_fns = nullptr;
+    static FnEnum enum_fns = nullptr;
+    static FnLoad load_fn = nullptr;
+    if (!load_fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuFuncGetModule", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return TSG_OK;   // older driver: keep lazy loading
+        get_module = (FnGetModule)p;
+        if (cudaGetDriverEntryPoint("cuModuleGetFunctionCount", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return TSG_OK;
+        count_fns = (FnCount)p;
+        if (cudaGetDriverEntryPoint("cuModuleEnumerateFunctions", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return TSG_OK;
+        enum_fns = (FnEnum)p;
+        if (cudaGetDriverEntryPoint("cuFuncLoad", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return TSG_OK;
+        load_fn = (FnLoad)p;
+    }
+    cudaFunction_t f = nullptr;
+    TSG_CK(cudaGetFuncBySymbol(&f, kernel));
+    CUmodule mod = nullptr;
+    unsigned n = 0;
+    if (get_module((CUmodule *)&mod, (CUfunction)f) != CUDA_SUCCESS || count_fns(&n, mod) != CUDA_SUCCESS)
+        return TSG_OK;
+    std::vector<CUfunction> fs(n);
+    if (n && enum_fns(fs.data(), n, mod) == CUDA_SUCCESS)
+        for (CUfunction g : fs) load_fn(g);
+    return TSG_OK;
+}
+
+int tsg_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    constexpr size_t PIECE = (size_t)256 << 20;
+    for (size_t o = 0; o < bytes; o += PIECE) {
+        const size_t n = bytes - o < PIECE ? bytes - o : PIECE;
+        TSG_CK(cudaMemcpyAsync(static_cast<char *>(dst) + o, static_cast<const char *>(src) + o, n, kind, s));
+    }
+    return TSG_OK;
+}
+
+int tsg_put_small(tsg_ctx *c, const int64_t *src, int n, int slot) {
+    k_put_small<<<1, 32, 0, c->stream>>>(src, c->hd_small + slot, n); ++c->launches;
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
 int tsg_pending_errors(tsg_ctx *c) {
     const int *h = reinterpret_cast<const int *>(c->h_small + 62);
     if (h[0] == KERR_NONE) return TSG_OK;
@@ -431,8 +538,9 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
     int h[2];
     c->pending = nullptr;
     TSG_CK(cudaGetLastError());
-    TSG_CK(cudaMemcpyAsync(h, c->d_err, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    TSG_TRY(tsg_put_small(c, reinterpret_cast<const int64_t *>(c->d_err), 1, 63));
     TSG_CK(cudaStreamSynchronize(c->stream));
+    memcpy(h, c->h_small + 63, sizeof(h));
     if (h[0] == KERR_NONE) return TSG_OK;
     int init_err[2] = {0, 0x7fffffff};
     TSG_CK(cudaMemcpyAsync(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice, c->stream));
@@ -606,7 +714,7 @@ __global__ void __launch_bounds__(1024) scan_one_block(const TI *__restrict__ in
 template <typename TI>
 int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     if (n == 0) {
-        TSG_CK(cudaMemsetAsync(out, 0, sizeof(int64_t), c->stream));
+        TSG_TRY(tsg_fill(c, out, 0, sizeof(int64_t), c->stream));
         return TSG_OK;
     }
     if (n <= SMALL_SCAN) {
@@ -617,7 +725,7 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     const int64_t tiles = (n + LB_TILE - 1) / LB_TILE;
     unsigned long long *state = nullptr;
     TSG_TRY(tsg_alloc_t(c, &state, tiles + 1));   // + the tile counter
-    TSG_CK(cudaMemsetAsync(state, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
+    TSG_TRY(tsg_fill(c, state, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
     // in-place safe: a tile reads its inputs before writing, and writes only
     // its own range (plus out[n], past every input)
     scan_lookback<TI><<<(unsigned)tiles, LB_BS, 0, c->stream>>>(
@@ -760,7 +868,7 @@ __global__ void k_rows_unsorted(int64_t rows, const int64_t *__restrict__ rp,
 int tsg_csr_check_sorted(tsg_ctx *c, tsg_csr *m) {
     int *flag = reinterpret_cast<int *>(c->d_small + 52);
     unsigned long long *ml = reinterpret_cast<unsigned long long *>(c->d_small + 53);
-    TSG_CK(cudaMemsetAsync(c->d_small + 52, 0, 2 * sizeof(int64_t), c->stream));
+    TSG_TRY(tsg_fill(c, c->d_small + 52, 0, 2 * sizeof(int64_t), c->stream));
     if (m->nnz > 0 && m->rows > 0) {
         k_rows_unsorted<<<grid_for(m->rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(
             m->rows, m->rp, m->col, flag, ml); ++c->launches;
@@ -788,17 +896,14 @@ extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nn
     }
     tsg_csr *m = nullptr;
     TSG_TRY(tsg_csr_alloc(c, rows, cols, nnz, values != nullptr, &m));
-    TSG_CK(cudaMemcpyAsync(m->rp, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                           c->stream));
+    TSG_TRY(tsg_copy(m->rp, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     if (nnz > 0) {
         int64_t *stage = nullptr;
         TSG_TRY(tsg_alloc_t(c, &stage, nnz));
-        TSG_CK(cudaMemcpyAsync(stage, col_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice,
-                               c->stream));
+        TSG_TRY(tsg_copy(stage, col_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
         cols_i64_to_i32<<<ew_grid(c, nnz), 256, 0, c->stream>>>(stage, m->col, nnz, cols, c->d_err); ++c->launches;
         if (values)
-            TSG_CK(cudaMemcpyAsync(m->val, values, nnz * sizeof(double), cudaMemcpyHostToDevice,
-                                   c->stream));
+            TSG_TRY(tsg_copy(m->val, values, nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         TSG_TRY(tsg_free(c, stage));
     }
     int s = tsg_check_kernel_errors(c, "upload");
@@ -832,19 +937,16 @@ extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
         return TSG_OK;
     }
     if (row_ptr)
-        TSG_CK(cudaMemcpyAsync(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, c->stream));
+        TSG_TRY(tsg_copy(row_ptr, m->rp, (m->rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     if (m->nnz > 0 && col_idx) {
         int64_t *stage = nullptr;
         TSG_TRY(tsg_alloc_t(c, &stage, m->nnz));
         cols_i32_to_i64<<<ew_grid(c, m->nnz), 256, 0, c->stream>>>(m->col, stage, m->nnz, 0); ++c->launches;
-        TSG_CK(cudaMemcpyAsync(col_idx, stage, m->nnz * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               c->stream));
+        TSG_TRY(tsg_copy(col_idx, stage, m->nnz * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
         TSG_TRY(tsg_free(c, stage));
     }
     if (m->nnz > 0 && values && m->val)
-        TSG_CK(cudaMemcpyAsync(values, m->val, m->nnz * sizeof(double), cudaMemcpyDeviceToHost,
-                               c->stream));
+        TSG_TRY(tsg_copy(values, m->val, m->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
     if (c->pending) return tsg_check_kernel_errors(c, c->pending);   // the producer's errors
     return TSG_OK;
@@ -980,7 +1082,7 @@ extern "C" int tsg_vec_upload(tsg_ctx *c, int64_t n, const int64_t *host, tsg_ve
     tsg_vec *v = nullptr;
     TSG_TRY(tsg_vec_alloc(c, n, false, &v));
     if (n > 0)
-        TSG_CK(cudaMemcpyAsync(v->d, host, n * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+        TSG_TRY(tsg_copy(v->d, host, n * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     *out = v;
     return TSG_OK;
 }

@@ -283,7 +283,7 @@ extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr 
     }
     if (check && nnz > 0) {
         int *flags = reinterpret_cast<int *>(c->d_small + 54);
-        TSG_CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+        TSG_TRY(tsg_fill(c, flags, 0, 2 * sizeof(int), s));
         k_graph_check<<<gw, 256, 0, s>>>(n, g->rp, gcol, flags); ++c->launches;
         int h[2] = {0, 0};
         TSG_CK(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -323,7 +323,7 @@ extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr 
     int32_t *cnt = nullptr;
     TSG_TRY(tsg_alloc_t(c, &cnt, n + 1));
     unsigned long long *ml = reinterpret_cast<unsigned long long *>(c->d_small + 56);
-    TSG_CK(cudaMemsetAsync(ml, 0, sizeof(unsigned long long), s));
+    TSG_TRY(tsg_fill(c, ml, 0, sizeof(unsigned long long), s));
     if (n > 0) {
         k_lower_count<<<gw, 256, 0, s>>>(n, g->rp, g->col, pos, cnt, ml); ++c->launches;
     }
@@ -437,7 +437,7 @@ extern "C" int tsg_rmat_graph(tsg_ctx *c, int scale, int edge_factor, uint64_t s
     k_keys_to_csr<<<grid_for(n + 1 > nnz ? n + 1 : nnz, 256, c->num_sms * 16), 256, 0, s>>>(
         n, nnz, scale, keys, g->rp, g->col); ++c->launches;
     unsigned long long *ml = reinterpret_cast<unsigned long long *>(c->d_small + 56);
-    TSG_CK(cudaMemsetAsync(ml, 0, sizeof(unsigned long long), s));
+    TSG_TRY(tsg_fill(c, ml, 0, sizeof(unsigned long long), s));
     k_row_max<<<gn, 256, 0, s>>>(n, g->rp, ml); ++c->launches;
     int64_t hml = 0;
     TSG_CK(cudaMemcpyAsync(&hml, ml, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -449,3 +449,5 @@ extern "C" int tsg_rmat_graph(tsg_ctx *c, int scale, int edge_factor, uint64_t s
     *out = g;
     return TSG_OK;
 }
+
+const void *tsg_kernel_graph() { return (const void *)k_degrees; }

@@ -29,7 +29,9 @@ struct tsg_ctx {
     cudaStream_t copy_in;     // H2D
     cudaStream_t copy_out;    // D2H
     int *d_err;               // [0] code, [1] row (lowest)
-    int64_t *h_small;         // pinned scratch for small D2H reads (64 x int64)
+    int64_t *h_small;         // pinned, device-mapped scratch for small reads (64 x int64)
+    int64_t *hd_small;        // device alias of h_small: kernels store results there
+                              // directly, so small reads never queue behind bulk D2H copies
     int64_t *d_small;         // device scratch for reductions (64 x int64)
     int timing;
     cudaEvent_t ev[8];
@@ -118,11 +120,36 @@ inline int tsg_alloc_t(tsg_ctx *ctx, T **p, size_t count) {
 }
 // Reads and clears the device error flag (synchronises the compute stream).
 int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
+// copy n int64 device words into h_small[slot..] through the mapped alias
+// (a one-thread kernel on the compute stream; the caller synchronises)
+int tsg_put_small(tsg_ctx *ctx, const int64_t *src, int n, int slot);
+// Load every kernel of the translation unit that holds `kernel` now.  With
+// CUDA's lazy module loading, the first launch of a kernel waits for copies
+// already queued on other streams (measured: a first-launched compute kernel
+// sat behind 2.5 GB of pending H2D); tsg_init preloads all libtsg modules.
+int tsg_preload_module_of(const void *kernel);
+// one representative kernel per .cu file, for tsg_preload_module_of
+const void *tsg_kernel_core();
+const void *tsg_kernel_compress();
+const void *tsg_kernel_spgemm();
+const void *tsg_kernel_masked();
+const void *tsg_kernel_chunk();
+const void *tsg_kernel_graph();
+// cudaMemsetAsync replacement as a kernel: on this platform memsets queue on
+// the copy engines, i.e. behind any bulk H2D / D2H already in flight
+int tsg_fill(tsg_ctx *ctx, void *p, int byte, size_t bytes, cudaStream_t s);
+// cudaMemcpyAsync in <= 256 MiB pieces.  Measured on the B200 box: a single
+// multi-GB host copy queued on one stream holds back kernels launched on
+// OTHER streams until it completes; split, the copy keeps its bandwidth and
+// other streams' kernels start within ~0.3 ms.
+int tsg_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s);
 // after a stream sync that also copied d_err into h_small[62]: report a
 // pending (deferred) kernel error, if any
 int tsg_pending_errors(tsg_ctx *ctx);
 
 int tsg_trace_enabled();
+// host timestamp line (no sync) when TSG_CHUNK_TIMELINE is set
+void tsg_trace_host(const char *what);
 // TSG_TRACE=1: host timestamps + GPU drain per traced step (debug only)
 void tsg_trace(tsg_ctx *c, const char *what, int64_t arg);
 

@@ -230,7 +230,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     for (int b = 0; b <= MB; b++) off[b] = bl.off[b];
 
     unsigned long long *dtot = (unsigned long long *)(c->d_small + 16);
-    TSG_CK(cudaMemsetAsync(dtot, 0, sizeof(unsigned long long), c->stream));
+    TSG_TRY(tsg_fill(c, dtot, 0, sizeof(unsigned long long), c->stream));
     MaskArgs a{l->rp, l->col, cl->start, cl->cnt, cl->set, cl->bits, dtot, c->d_err};
     TSG_TRY(launch_mask_group<0>(c, list, off, a));
     TSG_TRY(launch_mask_group<1>(c, list, off, a));
@@ -251,11 +251,10 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     int4 *slab = nullptr;
     if (n8 > 0) {
         unsigned long long *dmax = (unsigned long long *)(c->d_small + 24);
-        TSG_CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
+        TSG_TRY(tsg_fill(c, dmax, 0, sizeof(unsigned long long), c->stream));
         k_maxlen<<<grid_for(n8, 256, c->num_sms * 4), 256, 0, c->stream>>>(list + off[8], n8, l->rp,
                                                                           dmax); ++c->launches;
-        TSG_CK(cudaMemcpyAsync(&c->h_small[0], dmax, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               c->stream));
+        TSG_TRY(tsg_put_small(c, (const int64_t *)dmax, 1, 0));
         TSG_CK(cudaStreamSynchronize(c->stream));
         int64_t T = table_slots(c->h_small[0]);
         int64_t ctas = ((int64_t)2 << 30) / (T * 16);
@@ -267,7 +266,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
                                                                       (int)T); ++c->launches;
         TSG_CK(cudaGetLastError());
     }
-    TSG_CK(cudaMemcpyAsync(&c->h_small[1], dtot, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_TRY(tsg_put_small(c, (const int64_t *)dtot, 1, 1));
     int s = tsg_check_kernel_errors(c, "masked count");   // synchronises
     *total = c->h_small[1];
     tsg_free(c, slab);
@@ -359,3 +358,5 @@ extern "C" int tsg_cmat_free(tsg_ctx *c, tsg_cmat *cm) {
     delete cm;
     return TSG_OK;
 }
+
+const void *tsg_kernel_masked() { return (const void *)k_maxlen; }

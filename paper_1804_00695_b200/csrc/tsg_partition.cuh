@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
                                                       int ntiles, const int64_t *__restrict__ offs,
                                                       int32_t *__restrict__ list,
                                                       const int64_t *__restrict__ extra,
+                                                      const int *__restrict__ err,
                                                       int64_t *__restrict__ out) {
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
@@ -68,9 +69,11 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
         r0 = __shfl_sync(0xffffffffu, r0, leader);
         if (b < NB) list[offs[(int64_t)b * ntiles + blockIdx.x] + r0 + __popc(peers & lt)] = (int32_t)i;
     }
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
         if (threadIdx.x <= NB) out[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
         if (threadIdx.x == NB + 1) out[NB + 1] = extra ? *extra : 0;
+        // pending kernel errors of earlier work ride along (h_small[62])
+        if (threadIdx.x == NB + 2) out[30] = *reinterpret_cast<const int64_t *>(err);
     }
 }
 
@@ -86,7 +89,7 @@ struct NoMid {
 template <int NB, class F, class Mid = NoMid>
 int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid()) {
-    static_assert(32 + NB + 2 <= 48, "partition results overlap the d_small flags");
+    static_assert(32 + NB + 2 <= 62, "partition results overlap the error slot");
     int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
     if (ntiles < 1) ntiles = 1;
     int *tc = nullptr;
@@ -97,14 +100,11 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     k_part_bins<NB, F><<<ntiles, 256, 0, c->stream>>>(rows, f, bins, ntiles, tc); ++c->launches;
     TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NB * ntiles));
     TSG_TRY(mid());
+    // results land in mapped host memory straight from the kernel: no D2H
+    // copy that would queue behind bulk transfers on the copy engine
     k_part_scatter<NB><<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list, extra,
-                                                      c->d_small + 32); ++c->launches;
+                                                      c->d_err, c->hd_small + 32); ++c->launches;
     TSG_CK(cudaGetLastError());
-    TSG_CK(cudaMemcpyAsync(c->h_small + 32, c->d_small + 32, (NB + 2) * sizeof(int64_t),
-                           cudaMemcpyDeviceToHost, c->stream));
-    // deferred kernel errors of earlier work ride along with the same sync
-    TSG_CK(cudaMemcpyAsync(c->h_small + 62, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                           c->stream));
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));
     TSG_CK(cudaStreamSynchronize(c->stream));

@@ -1283,10 +1283,10 @@ __global__ void k_max_i64_list(const int32_t *list, int64_t n, const int64_t *v,
 
 // max over listed rows of v[] (host value)
 int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64_t &out) {
-    TSG_CK(cudaMemsetAsync(c->d_small, 0, sizeof(int64_t), c->stream));
+    TSG_TRY(tsg_fill(c, c->d_small, 0, sizeof(int64_t), c->stream));
     k_max_i64_list<<<grid_for(n, 256, c->num_sms * 4), 256, 0, c->stream>>>(
         list, n, v, (unsigned long long *)c->d_small); ++c->launches;
-    TSG_CK(cudaMemcpyAsync(c->h_small, c->d_small, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_TRY(tsg_put_small(c, c->d_small, 1, 0));
     TSG_CK(cudaStreamSynchronize(c->stream));
     out = c->h_small[0];
     return TSG_OK;
@@ -1441,7 +1441,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
     if (rows_out > 0) {
         // set bounds: partial row length + sum of selected compressed B rows
         int *maxcb = reinterpret_cast<int *>(c->d_small + 50);
-        TSG_CK(cudaMemsetAsync(maxcb, 0, sizeof(int), c->stream));
+        TSG_TRY(tsg_fill(c, maxcb, 0, sizeof(int), c->stream));
         k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
                                                                                 maxcb); ++c->launches;
         if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
@@ -1623,7 +1623,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
             na.unit_b = nullptr;
         } else {
             int *uflag = reinterpret_cast<int *>(c->d_small + 49);
-            TSG_CK(cudaMemsetAsync(uflag, 0xff, sizeof(int), c->stream));
+            TSG_TRY(tsg_fill(c, uflag, 0xff, sizeof(int), c->stream));
             k_unit_rows<<<grid_for(b->rows, 256, c->num_sms * 8), 256, 0, c->stream>>>(b->rows, b->rp, nullptr,
                                                                                      uflag); ++c->launches;
             na.unit_known = -1;
@@ -1742,8 +1742,7 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
     double *sval = nullptr;
     if (nbig > 0) {
         int64_t total = 0;
-        TSG_CK(cudaMemcpyAsync(&c->h_small[40], cptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               c->stream));
+        TSG_TRY(tsg_put_small(c, cptr + rows, 1, 40));
         TSG_CK(cudaStreamSynchronize(c->stream));
         total = c->h_small[40];
         TSG_TRY(tsg_alloc_t(c, &scol, total + 1));
@@ -1780,11 +1779,11 @@ extern "C" int tsg_count_multiplications(tsg_ctx *c, const tsg_csr *a, const tsg
                       (long long)b->rows);
         return TSG_EDIM;
     }
-    TSG_CK(cudaMemsetAsync(c->d_small, 0, sizeof(int64_t), c->stream));
+    TSG_TRY(tsg_fill(c, c->d_small, 0, sizeof(int64_t), c->stream));
     if (a->rows > 0 && a->nnz > 0)
         launch_bounds(c, a, b->rp, nullptr, nullptr, nullptr, (unsigned long long *)c->d_small);
     TSG_CK(cudaGetLastError());
-    TSG_CK(cudaMemcpyAsync(c->h_small, c->d_small, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TSG_TRY(tsg_put_small(c, c->d_small, 1, 0));
     TSG_CK(cudaStreamSynchronize(c->stream));
     *total = c->h_small[0];
     return TSG_OK;
@@ -1917,3 +1916,5 @@ extern "C" int tsg_numeric_fused(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b_
     tsg_cmat_free(c, cb);
     return s;
 }
+
+const void *tsg_kernel_spgemm() { return (const void *)k_max_i32; }
