@@ -387,7 +387,10 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     auto t0 = std::chrono::steady_clock::now();
     Job J{c, {a_rows, a_cols, a_rp, a_col, a_val}, {b_rows, b_cols, b_rp, b_col, b_val}, c_rp,
           c_col, c_val, nullptr, &local};
-    std::vector<int32_t> plen_host;
+    // host partial lengths (order 2): pinned, so their D2H stays asynchronous
+    // (a copy into pageable memory would block the host until the whole C
+    // drain ahead of it finished)
+    int32_t *plen_host = nullptr;
     constexpr int NBS = 3;   // B chunk slots: the copy two steps ahead never waits on compute
     DevRange Abuf[2], Bbuf[NBS];
     DevC Cbuf[2];
@@ -422,7 +425,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         return TSG_OK;
     };
 
-    if (algo == 0 || algo == 1) {
+    {
         const int64_t *acb = ac_bounds;
         int64_t nac = n_ac;
         int64_t whole[2] = {0, a_rows};
@@ -430,12 +433,6 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             acb = whole;
             nac = 1;
         }
-        // Flat schedule over steps s = (range r, chunk j): before step s runs,
-        // the copies of step s+2 are queued (A range when j == 0, B chunk in
-        // slot s % NBS), so the copy engine always has the next transfers
-        // queued while the host blocks inside a fused step.  C ranges are
-        // opened on the compute stream right before their first step.
-        const int64_t nsteps = nac * n_b;
         // every slot sized for the largest range / chunk before the pipeline
         // starts: a mid-run reallocation would have to wait for the slot's
         // in-flight users (and can make the pool grow under running copies)
@@ -457,7 +454,9 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 st = ensure(c, Abuf[i], ar, an, true, &fresh);
                 if (st == TSG_OK) st = ensure_c(c, Cbuf[i], cr, cn);
             }
-            for (int i = 0; i < NBS && st == TSG_OK; ++i) st = ensure(c, Bbuf[i], br, bn, true, &fresh);
+            // order 2 alternates two B slots (one if B is a single chunk)
+            const int nbs = algo == 2 ? (n_b > 1 ? 2 : 1) : (int)std::min<int64_t>(NBS, nac * n_b);
+            for (int i = 0; i < nbs && st == TSG_OK; ++i) st = ensure(c, Bbuf[i], br, bn, true, &fresh);
             // grow the driver pool once by the per-step temporaries (compressed
             // B chunk, symbolic / numeric scratch of a range): growing it later
             // maps memory while copies are in flight and stalls host and device
@@ -469,6 +468,22 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 cudaGetLastError();
             TSG_CK(cudaStreamSynchronize(c->stream));
         }
+    }
+    if (algo == 0 || algo == 1) {
+        const int64_t *acb = ac_bounds;
+        int64_t nac = n_ac;
+        int64_t whole[2] = {0, a_rows};
+        if (algo == 0) {
+            acb = whole;
+            nac = 1;
+        }
+        // Flat schedule over steps s = (range r, chunk j): before step s runs,
+        // the copies of step s+2 are queued (A range when j == 0, B chunk in
+        // slot s % NBS), so the copy engine always has the next transfers
+        // queued while the host blocks inside a fused step.  C ranges are
+        // opened on the compute stream right before their first step.
+        const int64_t nsteps = nac * n_b;
+
         auto issue = [&](int64_t s2) -> int {
             const int64_t r = s2 / n_b, j = s2 % n_b;
             if (j == 0) {   // this A slot was last read by range r-2's steps
@@ -504,8 +519,11 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             }
         }
     } else {
-        plen_host.assign((size_t)a_rows + 1, 0);
-        J.h_plen = plen_host.data();
+        void *ph = nullptr;
+        TSG_TRY(tsg_host_alloc(((size_t)a_rows + 1) * sizeof(int32_t), &ph));
+        plen_host = static_cast<int32_t *>(ph);
+        memset(plen_host, 0, ((size_t)a_rows + 1) * sizeof(int32_t));
+        J.h_plen = plen_host;
         for (int64_t j = 0; j < n_b && st == TSG_OK; ++j) {
             DevRange &B = Bbuf[j & 1];
             if ((st = stage_rows(c, J.B, b_bounds[j], b_bounds[j + 1], B, used[j & 1], local.h2d_bytes)) != TSG_OK)
@@ -516,8 +534,9 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 DevC &C = Cbuf[r & 1];
                 if ((st = stage_rows(c, J.A, lo, hi, A, used_a[r & 1], local.h2d_bytes)) != TSG_OK) break;
                 // partials come back from host after the first B sweep; the D2H
-                // of the previous sweep for this range must have landed
-                TSG_CK(cudaStreamSynchronize(c->copy_out));
+                // of the previous sweep for this range must have landed (the
+                // first sweep loads nothing, so its ranges pipeline freely)
+                if (j > 0) TSG_CK(cudaStreamSynchronize(c->copy_out));
                 if ((st = open_c(J, C, lo, hi, j > 0)) != TSG_OK) break;
                 st = fused_step(A, B, C, b_bounds[j], b_bounds[j + 1], hi - lo);
                 cudaEventRecord(used_a[r & 1], c->stream);
@@ -539,6 +558,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 break;
             }
     }
+    if (plen_host) tsg_host_free(plen_host);
     int64_t mem = c->bytes_in_use;
     for (int i = 0; i < 2; i++) {
         release(c, Abuf[i]);
