@@ -168,6 +168,9 @@ int tsg_graph_lower(tsg_ctx *ctx, const tsg_csr *g, int check, tsg_csr **L,
    CSR -- equal to the host builder entry for entry. */
 int tsg_rmat_graph(tsg_ctx *ctx, int scale, int edge_factor, uint64_t seed, double a, double b,
                    double c, tsg_csr **out);
+/* every stored entry := value (allocating the value array of a pattern CSR):
+   generators.with_unit_values on the device */
+int tsg_csr_set_values(tsg_ctx *ctx, tsg_csr *m, double value);
 
 /* ---- data placement (memory.py:193-223 PlacementPolicy; PAPER.md:600-625,
    810-829).  A CSR whose arrays live in pinned, device-mapped HOST memory:

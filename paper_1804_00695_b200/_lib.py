@@ -45,6 +45,7 @@ EXPORTS = (
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
+    "tsg_csr_set_values",
 )
 
 _P = ctypes.c_void_p
@@ -86,6 +87,7 @@ _SIGS = {
     "tsg_masked_count": ([_P, _P, _P, _PI64], ctypes.c_int),
     "tsg_graph_lower": ([_P, _P, ctypes.c_int, _PP, _P], ctypes.c_int),
     "tsg_numeric_calls": ([_P, _PI64], ctypes.c_int),
+    "tsg_csr_set_values": ([_P, _P, ctypes.c_double], ctypes.c_int),
     "tsg_numeric_ms": ([_P, _I64, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                         ctypes.c_double, ctypes.c_double, _PP], ctypes.c_int),
@@ -294,6 +296,12 @@ class DeviceCsr(_Handle):
         check(load().tsg_csr_map_host(ctx.h, m.num_rows, m.num_cols, ci.shape[0], _ptr(rp), _ptr(ci),
                                       _ptr(va), ctypes.byref(h)))
         return cls(ctx, h)
+
+    def set_values(self, value: float) -> "DeviceCsr":
+        """Every stored entry := value (a pattern matrix gets a value array)."""
+        check(load().tsg_csr_set_values(self.ctx.h, self.h, float(value)))
+        self.has_values = True
+        return self
 
     def download(self) -> CsrMatrix:
         rp = pinned_empty(self.num_rows + 1, np.int64)

@@ -362,6 +362,28 @@ extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr 
     return TSG_OK;
 }
 
+namespace {
+__global__ void k_set_values(int64_t n, double v, double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = v;
+}
+}  // namespace
+
+extern "C" int tsg_csr_set_values(tsg_ctx *c, tsg_csr *m, double value) {
+    if (m->host_mapped) {
+        tsg_set_error("tsg_csr_set_values: matrix lives in mapped host memory");
+        return TSG_EARG;
+    }
+    if (!m->val) TSG_TRY(tsg_alloc_t(c, &m->val, m->nnz > 0 ? m->nnz : 1));
+    if (m->nnz > 0) {
+        k_set_values<<<grid_for(m->nnz, 256, c->num_sms * 16), 256, 0, c->stream>>>(m->nnz, value, m->val);
+        ++c->launches;
+    }
+    TSG_CK(cudaGetLastError());
+    return TSG_OK;
+}
+
 extern "C" int tsg_rmat_graph(tsg_ctx *c, int scale, int edge_factor, uint64_t seed, double a,
                               double b, double cq, tsg_csr **out) {
     if (!c || !out || scale < 1 || scale > 30 || edge_factor < 1) {
