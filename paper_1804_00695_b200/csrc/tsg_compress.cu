@@ -368,6 +368,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_cmat *cm = nullptr;
     const int64_t rows = b->rows, nnz = b->nnz;
     TSG_TRY(tsg_cmat_alloc(c, rows, nnz > 0 ? nnz : 1, &cm));
+    cm->cols = b->cols;
     if (b->max_row >= 0 && b->max_row <= 1 && nnz > 0) {
         k_compress_unit<<<grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream>>>(
             rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;

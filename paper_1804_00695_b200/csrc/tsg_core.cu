@@ -794,6 +794,7 @@ int tsg_cmat_alloc(tsg_ctx *c, int64_t rows, int64_t cap, tsg_cmat **out) {
     m->rows = rows;
     m->sorted_sets = 0;
     m->identity_rows = 0;
+    m->cols = 0;
     m->cap = cap;
     m->start = nullptr;
     m->cnt = nullptr;

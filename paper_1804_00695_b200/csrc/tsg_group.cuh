@@ -167,6 +167,34 @@ __device__ __forceinline__ void group_enumerate_any(unsigned gm, int glane, int6
     }
 }
 
+// Block-wide exclusive scan of one int per thread (NT threads); total out.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_warp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += o;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int y = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, y, d);
+            if (lane >= d) y += o;
+        }
+        s_warp[lane] = y;
+    }
+    __syncthreads();
+    int r = x - v + (w ? s_warp[w - 1] : 0);
+    total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return r;
+}
+
 // Block-wide version for one row per CTA (NT threads, NT multiple of 32).
 // f(t, s) is called only for valid positions (no collectives inside f).
 template <int NT, class Src, class F>

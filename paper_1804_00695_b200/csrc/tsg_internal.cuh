@@ -73,6 +73,7 @@ struct tsg_cmat {
     int64_t cap;      // entries allocated in set/bits
     int sorted_sets;  // 1: every row's sets ascend (compact compression of a row-sorted B)
     int identity_rows;  // 1: row k is exactly set k (start = iota, cnt = 1)
+    int64_t cols;       // columns of the source matrix (0: unknown)
 };
 
 struct tsg_vec {

@@ -187,7 +187,7 @@ __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
 // shared memory (table + dense values).  CTA tier: one row per CTA, table in
 // shared memory.  Global tier: one row per CTA, table in a global slab.
 
-constexpr int NBINS = 13;   // 0-6 group, 7-8 CTA, 9 global, 10-12 symbolic merge tier
+constexpr int NBINS = 14;   // 0-6 group, 7-8 CTA, 9 global, 10-12 symbolic merge, 13 dense
 // bins 0..6: group tier slices (bytes) and group sizes
 __host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
 __host__ __device__ constexpr int gt_g(int b) { return b <= 1 ? 8 : (b == 2 ? 16 : 32); }
@@ -204,6 +204,13 @@ __host__ __device__ constexpr int mt_g(int m) { return 8 << m; }
 __host__ __device__ constexpr int mt_slice(int m) { return 1024 << m; }
 __host__ __device__ constexpr int mt_cap(int m) { return mt_slice(m) / 12; }   // staged (set, mask) pairs
 constexpr int BIN_MERGE = 10;
+// bin 13: dense tier for rows whose bound is a sizeable fraction of B's
+// columns (power-law hubs): one CTA per row, a shared-memory bitmap of all
+// of B's column sets (symbolic) / a per-set base + mask array (numeric).
+constexpr int BIN_DENSE = 13;
+constexpr int DENSE_MIN_SETS = 2048;           // bound (sets) from which a row goes dense
+constexpr int64_t DENSE_SMEM = 200 * 1024;     // shared-memory budget of the dense kernels
+__host__ __device__ __forceinline__ int64_t dense_words(int64_t ncols) { return (ncols + 63) / 64; }
 
 __host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
@@ -252,9 +259,14 @@ struct SymBinF {
     int64_t *scap;
     const int64_t *arp;   // non-null: merge tier allowed (row-sorted B, no partial rows)
     int64_t a_row_off;
+    int64_t ncols;        // B's columns (> 0: dense tier allowed)
     __device__ __forceinline__ int operator()(int64_t i) const {
         const int64_t sb = sbound[i];
         int b = sym_bin(sb);
+        if (ncols > 0 && sb >= DENSE_MIN_SETS && dense_words(ncols) * 8 <= DENSE_SMEM) {
+            scap[i] = sb;
+            return BIN_DENSE;
+        }
         if (arp && b != 255) {
             // few A entries, bounded staging: merge the sorted lists instead of hashing
             const int64_t alen = arp[i + a_row_off + 1] - arp[i + a_row_off];
@@ -277,10 +289,15 @@ struct NumBinF {
     const int64_t *counts;
     const int32_t *msets;
     const int64_t *sbound;
+    int64_t ncols;        // B's columns (> 0: dense tier allowed for rows with sorted sets)
     __device__ __forceinline__ int operator()(int64_t i) const {
         const int64_t n = counts[i];
         const int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
-        return num_bin(n, m);
+        const int b = num_bin(n, m);
+        if (ncols > 0 && b >= 7 && b != 255 && msets && (msets[i] & SETS_WRITTEN) &&
+            dense_words(ncols) * 12 <= DENSE_SMEM)
+            return BIN_DENSE;
+        return b;
     }
 };
 
@@ -535,6 +552,74 @@ __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ l
 
 template <int M>
 int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
+
+// Dense symbolic tier: the row's union is ORed into a shared-memory bitmap
+// of all of B's column sets (64-bit words, ORed as 32-bit halves), then the
+// nonzero words are emitted in ascending set order -- no table, no sort.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ list, int64_t nlist,
+                                                  SymArgs a, int64_t nwords) {
+    extern __shared__ int4 smem[];
+    __shared__ int s_warp[32];
+    __shared__ unsigned long long s_cnt;
+    uint64_t *bm = reinterpret_cast<uint64_t *>(smem);
+    unsigned *bm32 = reinterpret_cast<unsigned *>(smem);
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
+        if (threadIdx.x == 0) s_cnt = 0ull;
+        __syncthreads();
+        block_enumerate<NT>(
+            a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.cbstart[k];
+                    len = a.cbcnt[k];
+                }
+            },
+            [&](int64_t, int64_t sidx) {
+                const int set = a.cbset[sidx];
+                const uint64_t bits = a.cbbits[sidx];
+                if ((unsigned)bits) atomicOr(&bm32[2 * set], (unsigned)bits);
+                if ((unsigned)(bits >> 32)) atomicOr(&bm32[2 * set + 1], (unsigned)(bits >> 32));
+            });
+        __syncthreads();
+        // each thread owns a contiguous run of words: count its nonzero sets,
+        // block-scan the counts, emit its sets in order
+        const int64_t per = (nwords + NT - 1) / NT;
+        const int64_t w0 = threadIdx.x * per, w1 = w0 + per < nwords ? w0 + per : nwords;
+        int nz = 0;
+        unsigned long long pc = 0;
+        for (int64_t w = w0; w < w1; ++w) {
+            const uint64_t x = bm[w];
+            nz += x != 0ull;
+            pc += __popcll(x);
+        }
+        atomicAdd(&s_cnt, pc);
+        int tot;
+        int r = block_excl_scan<NT>(nz, tot, s_warp);
+        if (a.oset) {
+            const int64_t sp = a.sptr[i];
+            for (int64_t w = w0; w < w1; ++w) {
+                const uint64_t x = bm[w];
+                if (x) {
+                    a.oset[sp + r] = (int32_t)w;
+                    a.obits[sp + r] = x;
+                    ++r;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            a.counts[i] = (int64_t)s_cnt;
+            if (a.msets) a.msets[i] = tot | (a.oset ? SETS_WRITTEN : 0);
+        }
+        __syncthreads();
+    }
+}
 
 // ======================================================================= K4 group tier
 
@@ -951,35 +1036,81 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
     }
 }
 
-// ======================================================================= CTA / global tiers
-
-// Block-wide inclusive scan helper (NT threads).
+// Dense numeric tier: rows with sorted sets from the symbolic phase and a
+// column count far beyond the group tier.  Every set of B gets a base (output
+// offset of its first column in the row) and its mask in shared memory, so a
+// product's slot is base[c >> 6] + popcount(mask below c) -- no hashing; the
+// values accumulate with fp64 REDG adds straight into C (order-free, like the
+// CTA / global tiers).
 template <int NT>
-__device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_warp) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += o;
-    }
-    if (lane == 31) s_warp[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        int y = lane < NT / 32 ? s_warp[lane] : 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int o = __shfl_up_sync(0xffffffffu, y, d);
-            if (lane >= d) y += o;
+__global__ void __launch_bounds__(NT) k_num_dense(const int32_t *__restrict__ list, int64_t nlist,
+                                                  NumArgs a, int64_t nwords) {
+    extern __shared__ int4 smem[];
+    __shared__ int s_warp[32];
+    uint64_t *mask = reinterpret_cast<uint64_t *>(smem);
+    int32_t *base = reinterpret_cast<int32_t *>(mask + nwords);
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t n = a.counts[i];
+        const int64_t cp = a.cptr[i];
+        const int m = a.msets[i] & (SETS_WRITTEN - 1);
+        const int64_t sp = a.sptr[i];
+        // bases of the row's sets (exclusive popcount scan in set order) and
+        // the row's columns, values initialised to -0.0
+        int carry = 0;
+        for (int q0 = 0; q0 < m; q0 += NT) {
+            const int q = q0 + threadIdx.x;
+            int set = 0, pc = 0;
+            uint64_t bits = 0;
+            if (q < m) {
+                set = a.sset[sp + q];
+                bits = a.sbits[sp + q];
+                pc = __popcll(bits);
+            }
+            int tot;
+            const int b0 = carry + block_excl_scan<NT>(pc, tot, s_warp);
+            if (q < m) {
+                mask[set] = bits;
+                base[set] = b0;
+                uint64_t x = bits;
+                int64_t r = cp + b0;
+                while (x) {
+                    a.ccol[r] = set * 64 + (__ffsll((long long)x) - 1);
+                    a.cval[r++] = -0.0;
+                    x &= x - 1;
+                }
+            }
+            carry += tot;
         }
-        s_warp[lane] = y;
+        if (carry != n) {
+            if (threadIdx.x == 0) kerr(a.err, KERR_COUNT, gi);
+            __syncthreads();
+            continue;
+        }
+        __syncthreads();
+        block_enumerate<NT>(
+            a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.brp[k];
+                    len = (int)(a.brp[k + 1] - st);
+                }
+            },
+            [&](int64_t t, int64_t s) {
+                const int c = a.bcol[s];
+                const uint64_t mk = mask[c >> 6];
+                const int bit = c & 63;
+                const int pos = base[c >> 6] + __popcll(mk & ((bit ? (~0ull >> (64 - bit)) : 0ull)));
+                atomicAdd(&a.cval[cp + pos], __dmul_rn(a.aval[t], a.bval[s]));
+            });
+        __syncthreads();
     }
-    __syncthreads();
-    int r = x - v + (w ? s_warp[w - 1] : 0);
-    total = s_warp[NT / 32 - 1];
-    __syncthreads();
-    return r;
 }
+
+// ======================================================================= CTA / global tiers
 
 // Union of the row's sets into tbl (generic pointer: smem or global slab).
 template <int NT>
@@ -1357,6 +1488,30 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
+int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols) {
+    const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
+    if (n <= 0) return TSG_OK;
+    const int64_t nw = dense_words(ncols);
+    const size_t smem = (size_t)nw * 8;
+    TSG_TRY(set_smem(k_sym_dense<1024>, smem));
+    k_sym_dense<1024><<<grid_for(n, 1, c->num_sms), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
+                                                                             a, nw); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid_for(n, 1, c->num_sms), 1024, smem));
+    return TSG_OK;
+}
+
+int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols) {
+    const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
+    if (n <= 0) return TSG_OK;
+    const int64_t nw = dense_words(ncols);
+    const size_t smem = (size_t)nw * 12;
+    TSG_TRY(set_smem(k_num_dense<1024>, smem));
+    k_num_dense<1024><<<grid_for(n, 1, c->num_sms), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
+                                                                             a, nw); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_num_dense", BIN_DENSE, grid_for(n, 1, c->num_sms), 1024, smem));
+    return TSG_OK;
+}
+
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     TSG_TRY(launch_sym_merge<0>(c, bl, a));
     TSG_TRY(launch_sym_merge<1>(c, bl, a));
@@ -1466,7 +1621,9 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         // merge tier only when the compressed rows are sorted by set (row-sorted
         // B -> compact compression) and there is no partial row to fold in
         const int64_t *merge_arp = (cb->sorted_sets && partial == nullptr) ? a->rp : nullptr;
-        TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off},
+        const int64_t cb_cols = cb->cols;
+        TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off,
+                                             partial == nullptr ? cb_cols : 0},
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
@@ -1496,6 +1653,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.unit_dense = cb->identity_rows;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
+        TSG_TRY(launch_sym_dense(c, bl, sa, cb_cols));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
         TSG_TRY(tsg_free(c, bl.list));
     }
@@ -1562,7 +1720,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     Bins bl;
     int64_t nnz = 0;
     if (rows_out > 0) {
-        TSG_TRY(tsg_partition<NBINS>(c, rows_out, NumBinF{counts->d, counts->aux, sbound_in}, bins, bl,
+        TSG_TRY(tsg_partition<NBINS>(c, rows_out, NumBinF{counts->d, counts->aux, sbound_in, cb->sorted_sets ? b->cols : 0}, bins, bl,
                                      cptr + rows_out, &nnz));
     }
     tsg_csr *C = nullptr;
@@ -1638,6 +1796,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
             cudaEventRecord(c->ev_ring[2 * rk], c->stream);
         }
         TSG_TRY(run_numeric_bins(c, bl, na));
+        TSG_TRY(launch_num_dense(c, bl, na, b->cols));
         if (c->timing) {
             cudaEventRecord(c->ev_num[1], c->stream);
             cudaEventRecord(c->ev_ring[2 * rk + 1], c->stream);
@@ -1702,7 +1861,7 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
         rows, a->rp, a->col, 0, b_lo, b_hi, cb->start, cb->cnt, nullptr, sbound, plen); ++c->launches;
     TSG_CK(cudaGetLastError());
     Bins bl;
-    TSG_TRY(tsg_partition<NBINS>(c, rows, NumBinF{cap, nullptr, sbound}, bins, bl));
+    TSG_TRY(tsg_partition<NBINS>(c, rows, NumBinF{cap, nullptr, sbound, 0}, bins, bl));
     NumArgs na;
     memset(&na, 0, sizeof(na));
     na.arp = a->rp;
