@@ -65,6 +65,11 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     TSG_CK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
     TSG_CK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    for (int i = 0; i < tsg_ctx::NAUX; ++i) {
+        TSG_CK(cudaStreamCreateWithFlags(&c->aux[i], cudaStreamNonBlocking));
+        TSG_CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
+    }
+    TSG_CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     // keep freed blocks cached in the default pool: no OS round trips per call
     cudaMemPool_t pool;
     TSG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -112,6 +117,11 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->copy_in);
     cudaStreamDestroy(c->copy_out);
+    for (int i = 0; i < tsg_ctx::NAUX; ++i) {
+        cudaStreamDestroy(c->aux[i]);
+        cudaEventDestroy(c->ev_join[i]);
+    }
+    cudaEventDestroy(c->ev_fork);
     delete c;
     return TSG_OK;
 }

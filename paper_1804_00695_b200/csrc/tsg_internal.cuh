@@ -28,6 +28,11 @@ struct tsg_ctx {
     cudaStream_t stream;      // compute
     cudaStream_t copy_in;     // H2D
     cudaStream_t copy_out;    // D2H
+    // independent row tiers (bins) run concurrently on these, forked from and
+    // joined back into `stream` (tsg_spgemm.cu BinFork)
+    static constexpr int NAUX = 3;
+    cudaStream_t aux[NAUX];
+    cudaEvent_t ev_fork, ev_join[NAUX];
     int *d_err;               // [0] code, [1] row (lowest)
     int64_t *h_small;         // pinned, device-mapped scratch for small reads (64 x int64)
     int64_t *hd_small;        // device alias of h_small: kernels store results there

@@ -1512,17 +1512,59 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
     return TSG_OK;
 }
 
+// Concurrent bins: the rows of different group-tier bins are disjoint, so the
+// first nonempty bin runs on the compute stream and each further one on an
+// auxiliary stream forked from it; join() makes the compute stream wait for
+// them all.  Small bins (a few boundary rows with long dependent chains) then
+// overlap the big bin instead of adding their latency to the phase.  Only
+// kernels without per-launch allocations are forked (the arena is ordered on
+// the compute stream).
+struct BinFork {
+    tsg_ctx *c;
+    int used = 0;          // nonempty bins so far
+    bool forked = false;
+    explicit BinFork(tsg_ctx *cc) : c(cc) {}
+    template <class L>
+    int run(int64_t n, L launch) {
+        if (n <= 0) return TSG_OK;
+        if (used++ == 0) return launch();   // first bin: compute stream
+        const int k = (used - 2) % tsg_ctx::NAUX;
+        if (!forked) {
+            TSG_CK(cudaEventRecord(c->ev_fork, c->stream));
+            forked = true;
+        }
+        cudaStream_t main = c->stream;
+        TSG_CK(cudaStreamWaitEvent(c->aux[k], c->ev_fork, 0));
+        c->stream = c->aux[k];
+        const int r = launch();
+        c->stream = main;
+        return r;
+    }
+    int join() {
+        if (!forked) return TSG_OK;
+        const int naux = used - 1 < tsg_ctx::NAUX ? used - 1 : tsg_ctx::NAUX;
+        for (int k = 0; k < naux; ++k) {
+            TSG_CK(cudaEventRecord(c->ev_join[k], c->aux[k]));
+            TSG_CK(cudaStreamWaitEvent(c->stream, c->ev_join[k], 0));
+        }
+        return TSG_OK;
+    }
+};
+
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
-    TSG_TRY(launch_sym_merge<0>(c, bl, a));
-    TSG_TRY(launch_sym_merge<1>(c, bl, a));
-    TSG_TRY(launch_sym_merge<2>(c, bl, a));
-    TSG_TRY(launch_sym_group<0>(c, bl, a));
-    TSG_TRY(launch_sym_group<1>(c, bl, a));
-    TSG_TRY(launch_sym_group<2>(c, bl, a));
-    TSG_TRY(launch_sym_group<3>(c, bl, a));
-    TSG_TRY(launch_sym_group<4>(c, bl, a));
-    TSG_TRY(launch_sym_group<5>(c, bl, a));
-    TSG_TRY(launch_sym_group<6>(c, bl, a));
+    BinFork f(c);
+    auto cnt = [&](int b) { return bl.off[b + 1] - bl.off[b]; };
+    TSG_TRY(f.run(cnt(BIN_MERGE + 0), [&] { return launch_sym_merge<0>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(BIN_MERGE + 1), [&] { return launch_sym_merge<1>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(BIN_MERGE + 2), [&] { return launch_sym_merge<2>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(0), [&] { return launch_sym_group<0>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(1), [&] { return launch_sym_group<1>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(2), [&] { return launch_sym_group<2>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(3), [&] { return launch_sym_group<3>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(4), [&] { return launch_sym_group<4>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(5), [&] { return launch_sym_group<5>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(6), [&] { return launch_sym_group<6>(c, bl, a); }));
+    TSG_TRY(f.join());
     TSG_TRY(launch_sym_cta<0>(c, bl, a));
     TSG_TRY(launch_sym_cta<1>(c, bl, a));
     TSG_TRY(launch_sym_global(c, bl, a));
@@ -1530,13 +1572,16 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 }
 
 int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
-    TSG_TRY(launch_num_group<0>(c, bl, a));
-    TSG_TRY(launch_num_group<1>(c, bl, a));
-    TSG_TRY(launch_num_group<2>(c, bl, a));
-    TSG_TRY(launch_num_group<3>(c, bl, a));
-    TSG_TRY(launch_num_group<4>(c, bl, a));
-    TSG_TRY(launch_num_group<5>(c, bl, a));
-    TSG_TRY(launch_num_group<6>(c, bl, a));
+    BinFork f(c);
+    auto cnt = [&](int b) { return bl.off[b + 1] - bl.off[b]; };
+    TSG_TRY(f.run(cnt(0), [&] { return launch_num_group<0>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(1), [&] { return launch_num_group<1>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(2), [&] { return launch_num_group<2>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(3), [&] { return launch_num_group<3>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(4), [&] { return launch_num_group<4>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(5), [&] { return launch_num_group<5>(c, bl, a); }));
+    TSG_TRY(f.run(cnt(6), [&] { return launch_num_group<6>(c, bl, a); }));
+    TSG_TRY(f.join());
     TSG_TRY(launch_num_cta<0>(c, bl, a));
     TSG_TRY(launch_num_cta<1>(c, bl, a));
     TSG_TRY(launch_num_global(c, bl, a));
