@@ -350,7 +350,7 @@ def main():
     achieved = alg_bytes / (num_ms * 1e-3) / 1e9
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
             traffic = int(json.load(fh)["traffic_bytes_per_launch"])
     except Exception:
         pass
@@ -360,7 +360,7 @@ def main():
             "peak_kind": peak_kind, "algorithmic_bytes": alg_bytes,
             "device_layout_bytes": dev_bytes, "kernel_ms": num_ms,
             "note": "traffic = dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch "
-                    "from one ncu --set full capture (profiles/r01_traffic.json)"}
+                    "from one ncu --set full capture (profiles/r02_traffic.json)"}
     whole_bytes_ms = tot_ms / args.steps
 
     line = {
