@@ -201,6 +201,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--phases", action="store_true", help="print per-phase device times and exit")
+    ap.add_argument("--b-mode", default="replicated", choices=["replicated", "sharded"],
+                    help="N>1: B all-gathered once (replicated) or kept as row shards read "
+                         "from peer HBM through CUDA IPC (sharded, SURVEY.md §8e)")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off)")
@@ -247,6 +250,9 @@ def main():
     if world == 1:
         da = _lib.DeviceCsr.upload(a_loc, ctx)
         a_rows, a_nnz = a_loc.num_rows, a_loc.nnz
+    elif args.b_mode == "sharded":
+        da, setup = sharded_b(ctx, a_loc, dr, dims, world, rank, torch, dist)
+        a_rows, a_nnz = da.num_rows, da.nnz
     else:
         da, setup = replicate_b(ctx, a_loc, dims, world, rank, torch, dist)
         a_rows, a_nnz = da.num_rows, da.nnz
@@ -370,7 +376,7 @@ def main():
         "config": {"workload": "config2 R*A*P brick3d %dx%dx%d + 2x2x2 aggregation" % dims,
                    "grid": list(dims), "multiplications_per_rank": m1 + m2,
                    "nnz": {"A": a_nnz, "R": r.nnz, "RA": ra_nnz, "RAP": rap_nnz},
-                   "parallelism": "row partition of R (coarse z-slabs) x%d, B replicated" % world
+                   "parallelism": "row partition of R (coarse z-slabs) x%d, B %s" % (world, args.b_mode)
                    if world > 1 else "single GPU",
                    "l2": "A (>0.7 GB) and RA (>0.2 GB) exceed L2; 252 MiB flush between steps",
                    "timing": "CUDA events on libtsg's compute stream, max over ranks"},
@@ -414,6 +420,25 @@ def replicate_b(ctx, a_loc, dims, world, rank, torch, dist):
                                     col.data_ptr(), val.data_ptr())
     return da, {"b_allgather_s": time.perf_counter() - t0,
                 "b_bytes_per_rank": int(8 * (a_loc.num_rows + 1) + 12 * a_loc.nnz)}
+
+
+def sharded_b(ctx, a_loc, dr, dims, world, rank, torch, dist):
+    """B sharded: every rank keeps its slab of the fine operator; the slabs are
+    shared once as CUDA IPC handles and the rows this rank's R selects (its
+    slab plus one halo plane from each neighbour) are gathered by a kernel
+    reading peer HBM over NVLink.  No collective in the multiply."""
+    from paper_1804_00695_b200 import distributed as D
+    t0 = time.perf_counter()
+    plane = dims[0] * dims[1]
+    lo, hi = rank * dims[0] * plane, (rank + 1) * dims[0] * plane
+    rp = torch.from_numpy(np.asarray(a_loc.row_ptr, dtype=np.int64)).cuda()
+    col = torch.from_numpy(np.asarray(a_loc.col_idx, dtype=np.int32)).cuda()
+    val = torch.from_numpy(np.asarray(a_loc.values)).cuda()
+    shards = D.share_shards((rp, col, val), lo, hi, dist)
+    torch.cuda.synchronize()
+    db = D.gather_sharded(dr, shards, a_loc.num_cols)
+    return db, {"b_shard_gather_s": time.perf_counter() - t0, "b_mode": "sharded",
+                "b_rows_gathered_nnz": int(db.nnz)}
 
 
 def run_e2e(ctx, r, a, p, args):

@@ -168,6 +168,15 @@ int tsg_graph_lower(tsg_ctx *ctx, const tsg_csr *g, int check, tsg_csr **L,
    CSR -- equal to the host builder entry for entry. */
 int tsg_rmat_graph(tsg_ctx *ctx, int scale, int edge_factor, uint64_t seed, double a, double b,
                    double c, tsg_csr **out);
+/* ---- B sharded across GPUs --------------------------------
+   B's rows [row_lo[s], row_lo[s+1]) live on shard s as device arrays
+   (shard-local int64 row pointers from 0, int32 columns, fp64 values) --
+   typically other GPUs' memory opened through CUDA IPC (NVLink P2P loads).
+   Builds a local CSR of B in which exactly the rows selected by A's columns
+   are filled (others empty), reading them straight from the shards. */
+int tsg_gather_sharded(tsg_ctx *ctx, int n_shards, const int64_t *row_lo, const void *const *shard_rp,
+                       const void *const *shard_col, const void *const *shard_val, int64_t b_cols,
+                       const tsg_csr *a, tsg_csr **out);
 /* every stored entry := value (allocating the value array of a pattern CSR):
    generators.with_unit_values on the device */
 int tsg_csr_set_values(tsg_ctx *ctx, tsg_csr *m, double value);

@@ -45,7 +45,7 @@ EXPORTS = (
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
-    "tsg_csr_set_values",
+    "tsg_csr_set_values", "tsg_gather_sharded",
 )
 
 _P = ctypes.c_void_p
@@ -88,6 +88,7 @@ _SIGS = {
     "tsg_graph_lower": ([_P, _P, ctypes.c_int, _PP, _P], ctypes.c_int),
     "tsg_numeric_calls": ([_P, _PI64], ctypes.c_int),
     "tsg_csr_set_values": ([_P, _P, ctypes.c_double], ctypes.c_int),
+    "tsg_gather_sharded": ([_P, ctypes.c_int, _P, _P, _P, _P, _I64, _P, _PP], ctypes.c_int),
     "tsg_numeric_ms": ([_P, _I64, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                         ctypes.c_double, ctypes.c_double, _PP], ctypes.c_int),
@@ -453,3 +454,16 @@ def d_rmat_graph(scale: int, edge_factor: int, seed: int, a: float, b: float, c:
     check_(load().tsg_rmat_graph(ctx.h, int(scale), int(edge_factor), int(seed) & ((1 << 64) - 1),
                                  float(a), float(b), float(c), ctypes.byref(h)))
     return DeviceCsr(ctx, h)
+
+
+def d_gather_sharded(da, shards, b_cols: int) -> DeviceCsr:
+    """shards: [(row_lo, row_hi, rp_ptr, col_ptr, val_ptr or 0)] device
+    pointers in row order (local or peer memory)."""
+    n = len(shards)
+    lo = np.array([s[0] for s in shards] + [shards[-1][1]], dtype=np.int64)
+    arr = lambda k: (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(s[k]) or None) for s in shards])
+    h = ctypes.c_void_p()
+    vals = arr(4) if all(s[4] for s in shards) else None
+    check_(load().tsg_gather_sharded(da.ctx.h, n, _ptr(lo), arr(2), arr(3), vals, int(b_cols), da.h,
+                                     ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)

@@ -16,6 +16,7 @@
 // radix / segmented sorts from the CUDA toolkit: this is input preparation,
 // not the SpGEMM hot path.
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "tsg_internal.cuh"
 
@@ -473,3 +474,135 @@ extern "C" int tsg_rmat_graph(tsg_ctx *c, int scale, int edge_factor, uint64_t s
 }
 
 const void *tsg_kernel_graph() { return (const void *)k_degrees; }
+
+// ---- B sharded across GPUs: gather the rows of B that A's
+// columns select straight from the shards' device memory -- peer HBM over
+// NVLink when the shard pointers come from CUDA IPC handles of other GPUs,
+// local memory in the single-GPU tests.  The result is a local CSR with all
+// of B's rows, the unselected ones empty, so the multiply kernels run on it
+// unchanged.  No collective is involved.
+namespace {
+
+struct ShardTable {
+    int n;
+    const int64_t *row_lo;     // device, n + 1 global row bounds
+    const int64_t *const *rp;  // device array of n shard row-pointer arrays (shard-local, from 0)
+    const int32_t *const *col;
+    const double *const *val;
+};
+
+__device__ __forceinline__ int shard_of(const ShardTable &t, int64_t k) {
+    int lo = 0, hi = t.n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (t.row_lo[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void k_mark_rows(int64_t nnz, const int32_t *__restrict__ acol, uint8_t *__restrict__ need) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz;
+         t += (int64_t)gridDim.x * blockDim.x)
+        need[acol[t]] = 1;
+}
+
+__global__ void k_gather_lens(int64_t rows, const uint8_t *__restrict__ need, ShardTable t,
+                              int32_t *__restrict__ len) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < rows;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int32_t l = 0;
+        if (need[k]) {
+            const int s = shard_of(t, k);
+            const int64_t r = k - t.row_lo[s];
+            l = (int32_t)(t.rp[s][r + 1] - t.rp[s][r]);
+        }
+        len[k] = l;
+    }
+}
+
+__global__ void k_gather_rows(int64_t rows, const uint8_t *__restrict__ need, ShardTable t,
+                              const int64_t *__restrict__ orp, int32_t *__restrict__ ocol,
+                              double *__restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < rows; k += nw) {
+        if (!need[k]) continue;
+        const int s = shard_of(t, k);
+        const int64_t r = k - t.row_lo[s];
+        const int64_t src = t.rp[s][r], len = t.rp[s][r + 1] - src, dst = orp[k];
+        for (int64_t q = lane; q < len; q += 32) {
+            ocol[dst + q] = t.col[s][src + q];
+            if (oval) oval[dst + q] = t.val[s][src + q];
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int tsg_gather_sharded(tsg_ctx *c, int n_shards, const int64_t *row_lo_host,
+                                  const void *const *shard_rp, const void *const *shard_col,
+                                  const void *const *shard_val, int64_t b_cols, const tsg_csr *a,
+                                  tsg_csr **out) {
+    if (!c || !a || !out || n_shards < 1 || !row_lo_host) {
+        tsg_set_error("tsg_gather_sharded: bad arguments");
+        return TSG_EARG;
+    }
+    const int64_t rows = row_lo_host[n_shards];
+    if (a->cols != rows) {
+        tsg_set_error("A has %lld cols but the sharded B has %lld rows", (long long)a->cols, (long long)rows);
+        return TSG_EDIM;
+    }
+    const bool values = shard_val && shard_val[0];
+    cudaStream_t s = c->stream;
+    // device copies of the shard table
+    int64_t *d_lo = nullptr;
+    const void **d_ptrs = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &d_lo, n_shards + 1));
+    TSG_TRY(tsg_alloc(c, (void **)&d_ptrs, sizeof(void *) * 3 * n_shards));
+    std::vector<const void *> hp(3 * n_shards);
+    for (int i = 0; i < n_shards; ++i) {
+        hp[i] = shard_rp[i];
+        hp[n_shards + i] = shard_col[i];
+        hp[2 * n_shards + i] = values ? shard_val[i] : nullptr;
+    }
+    TSG_CK(cudaMemcpyAsync(d_lo, row_lo_host, (n_shards + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    TSG_CK(cudaMemcpyAsync(d_ptrs, hp.data(), sizeof(void *) * 3 * n_shards, cudaMemcpyHostToDevice, s));
+    ShardTable t{n_shards, d_lo, (const int64_t *const *)d_ptrs, (const int32_t *const *)(d_ptrs + n_shards),
+                 (const double *const *)(d_ptrs + 2 * n_shards)};
+    uint8_t *need = nullptr;
+    int32_t *len = nullptr;
+    int64_t *rp = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &need, rows + 1));
+    TSG_TRY(tsg_alloc_t(c, &len, rows + 1));
+    TSG_TRY(tsg_alloc_t(c, &rp, rows + 1));
+    TSG_TRY(tsg_fill(c, need, 0, rows + 1, s));
+    if (a->nnz > 0) {
+        k_mark_rows<<<grid_for(a->nnz, 256, c->num_sms * 16), 256, 0, s>>>(a->nnz, a->col, need);
+        ++c->launches;
+    }
+    k_gather_lens<<<grid_for(rows, 256, c->num_sms * 16), 256, 0, s>>>(rows, need, t, len); ++c->launches;
+    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, len, rp, rows));
+    TSG_TRY(tsg_put_small(c, rp + rows, 1, 0));
+    TSG_CK(cudaStreamSynchronize(s));
+    const int64_t nnz = c->h_small[0];
+    tsg_csr *B = nullptr;
+    TSG_TRY(tsg_csr_alloc(c, rows, b_cols, nnz, values, &B));
+    TSG_CK(cudaMemcpyAsync(B->rp, rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (nnz > 0) {
+        k_gather_rows<<<grid_for(rows, 8, c->num_sms * 16), 256, 0, s>>>(rows, need, t, rp, B->col,
+                                                                         values ? B->val : nullptr);
+        ++c->launches;
+    }
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_free(c, need));
+    TSG_TRY(tsg_free(c, len));
+    TSG_TRY(tsg_free(c, rp));
+    TSG_TRY(tsg_free(c, d_lo));
+    TSG_TRY(tsg_free(c, (void *)d_ptrs));
+    B->sorted = 0;   // shard rows are taken as they are
+    B->max_row = -1;
+    TSG_TRY(tsg_csr_check_sorted(c, B));
+    *out = B;
+    return TSG_OK;
+}

@@ -1,8 +1,17 @@
 """Multi-GPU row partition of A.
 
 Rows of C are independent (kernel.py:11-14), so N GPUs each compute a
-contiguous block of C's rows.  The collectives are exactly the two the north
-star allows, both over torch.distributed (NCCL on B200s, gloo in the CPU
+contiguous block of C's rows.  B reaches the ranks in one of two ways:
+
+* replicated -- one all-gather rebuilds the full B on every rank
+  (``allgather_csr``);
+* sharded -- every rank keeps only its row shard of B; shards are shared as
+  CUDA IPC handles once (``share_shards``), and each rank's kernel
+  (``gather_sharded``, csrc ``tsg_gather_sharded``) loads the B rows its A
+  rows select straight from peer HBM over NVLink.  No collective runs in the
+  multiply.
+
+The collectives, over torch.distributed (NCCL on B200s, gloo in the CPU
 tests):
 
 * ``allgather_csr`` -- B replicated: every rank holds a row shard of B and one
@@ -72,3 +81,47 @@ def allgather_csr(row_counts, cols, vals, dist, device):
     rp = torch.zeros(counts.numel() + 1, dtype=torch.int64, device=device)
     rp[1:] = torch.cumsum(counts, 0)
     return rp, _allgather_var(cols, dist, device), _allgather_var(vals, dist, device)
+
+
+def shard_bounds(row_nnz, world: int) -> np.ndarray:
+    """Contiguous row shards of B with near-equal entry counts."""
+    return flops_partition(row_nnz, world)
+
+
+def local_shard_tensors(b, lo: int, hi: int, device):
+    """(rp, col, val) torch tensors of B's rows [lo, hi) on `device`, row
+    pointers rebased to 0, int32 columns -- the layout tsg_gather_sharded reads."""
+    import torch
+    rp = np.asarray(b.row_ptr[lo:hi + 1], dtype=np.int64)
+    e0, e1 = int(rp[0]), int(rp[-1])
+    t_rp = torch.from_numpy(rp - e0).to(device)
+    t_col = torch.from_numpy(np.asarray(b.col_idx[e0:e1], dtype=np.int32)).to(device)
+    t_val = None if b.values is None else torch.from_numpy(np.asarray(b.values[e0:e1])).to(device)
+    return t_rp, t_col, t_val
+
+
+def share_shards(local, lo: int, hi: int, dist):
+    """Exchange every rank's shard as CUDA IPC handles (torch's tensor
+    reductions; opened with lazy peer access) and return, in rank order,
+    [(row_lo, row_hi, rp, col, val)] tensors -- peers' live in peer HBM."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    mine = (lo, hi) + tuple(None if t is None else reduce_tensor(t) for t in local)
+    allp = [None] * dist.get_world_size()
+    dist.all_gather_object(allp, mine)
+    out = []
+    for r, item in enumerate(allp):
+        if r == dist.get_rank():
+            out.append((lo, hi) + tuple(local))
+            continue
+        lo_r, hi_r = item[0], item[1]
+        ts = tuple(None if red is None else red[0](*red[1]) for red in item[2:])
+        out.append((lo_r, hi_r) + ts)
+    return out
+
+
+def gather_sharded(da, shards, b_cols: int):
+    """Local CSR of B (the rows A selects) from shard tensors (local or peer)."""
+    from . import _lib
+    ptrs = [(lo, hi, rp.data_ptr(), col.data_ptr(), 0 if val is None else val.data_ptr())
+            for lo, hi, rp, col, val in shards]
+    return _lib.d_gather_sharded(da, ptrs, b_cols)

@@ -94,3 +94,56 @@ def test_flops_partition_properties():
         assert b[0] == 0 and b[-1] == 500 and np.all(np.diff(b) >= 0)
         parts = [int(f[b[k]:b[k + 1]].sum()) for k in range(world)]
         assert max(parts) - min(parts) <= 2 * int(f.max())
+
+
+def _shard_worker(rank, world, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    import torch.multiprocessing as tmp
+    from paper_1804_00695_b200 import distributed as D
+    from paper_1804_00695_b200 import generators as gen
+    tmp.set_sharing_strategy("file_system")
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b = gen.stencil(gen.LAPLACE3D, (5, 5, 3 * world))
+        bounds = D.shard_bounds(np.diff(b.row_ptr), world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        local = D.local_shard_tensors(b, lo, hi, "cpu")
+        shards = D.share_shards(local, lo, hi, dist)
+        # every rank sees every shard, in row order, with the owner's contents
+        got = []
+        for lo_r, hi_r, rp, col, val in shards:
+            e0 = int(b.row_ptr[lo_r])
+            got.append((lo_r, hi_r, bool(np.array_equal(rp.numpy() + e0, b.row_ptr[lo_r:hi_r + 1])),
+                        bool(np.array_equal(col.numpy(), b.col_idx[e0:int(b.row_ptr[hi_r])])),
+                        bool(np.array_equal(val.numpy(), b.values[e0:int(b.row_ptr[hi_r])]))))
+        dist.barrier()
+        q.put((rank, got, bounds.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_b_shards_shared():
+    """B sharded (§8e): each rank publishes its row shard as tensor handles;
+    every rank can read all shards in row order (CPU tensors here, CUDA IPC
+    handles into peer HBM on GPUs)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, got, bounds in res:
+        assert bounds[0] == 0 and len(got) == world
+        assert [g[0] for g in got] == bounds[:-1] and [g[1] for g in got] == bounds[1:]
+        assert all(g[2] and g[3] and g[4] for g in got)

@@ -243,3 +243,23 @@ def test_placement_policies_same_product(rng):
         assert_same_product(tsg.multiply(a, b, placement=name), want, exact=True)
     pol = PlacementPolicy("c_pin", {"A": "fast", "B": "fast", "C": "slow"})
     assert_same_product(tsg.multiply(a, b, placement=pol), want, exact=True)
+
+
+def test_sharded_b_gather_matches_replicated(rng):
+    """B sharded (§8e): the rows A selects are gathered straight from the
+    shards' device memory (peer HBM on multi-GPU, three local shards here);
+    the product equals the one with a replicated B, bit for bit."""
+    import torch
+    from paper_1804_00695_b200 import _lib, distributed as D
+    a = random_csr(rng, 500, 900, 12)
+    a_sub = random_csr(rng, 50, 900, 3)          # selects only some of B's rows
+    b = random_csr(rng, 900, 700, 20)
+    bounds = D.shard_bounds(np.diff(b.row_ptr), 3)
+    shards = [(int(bounds[s]), int(bounds[s + 1])) +
+              D.local_shard_tensors(b, int(bounds[s]), int(bounds[s + 1]), "cuda") for s in range(3)]
+    torch.cuda.synchronize()
+    for aa in (a, a_sub):
+        da = _lib.DeviceCsr.upload(aa)
+        db = D.gather_sharded(da, shards, b.num_cols)
+        got = _lib.d_multiply(da, db).download()
+        assert_same_product(got, O.multiply(aa, b), exact=True)
