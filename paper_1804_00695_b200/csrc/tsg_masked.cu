@@ -25,10 +25,13 @@ struct MaskArgs {
     int *err;
 };
 
-constexpr int MB = 9;  // bins: 0..6 group tier (slice 512 << b), 7 CTA, 8 global
+constexpr int MB = 10;  // bins: 0..6 group tier (slice 512 << b), 7 CTA, 8 global, 9 dense
+constexpr int MASK_DENSE = 9;
+constexpr int64_t MASK_DENSE_MIN = 2048;   // row length from which the dense bitmap wins
 
-__device__ __forceinline__ int mask_bin(int64_t len) {
+__device__ __forceinline__ int mask_bin(int64_t len, bool dense_ok) {
     if (len <= 0) return 255;
+    if (dense_ok && len >= MASK_DENSE_MIN) return MASK_DENSE;
     int64_t need = 16 * (int64_t)table_slots(len);
     for (int b = 0; b < 7; b++)
         if (need <= (512 << b)) return b;
@@ -38,8 +41,57 @@ __device__ __forceinline__ int mask_bin(int64_t len) {
 
 struct MaskBinF {
     const int64_t *lrp;
-    __device__ __forceinline__ int operator()(int64_t i) const { return mask_bin(lrp[i + 1] - lrp[i]); }
+    bool dense_ok;
+    __device__ __forceinline__ int operator()(int64_t i) const {
+        return mask_bin(lrp[i + 1] - lrp[i], dense_ok);
+    }
 };
+
+// Dense tier for long rows (power-law hubs): row i's columns become bits of
+// a bitmap over ALL columns (shared memory when it fits, else a per-CTA slab
+// that stays L2-resident), so every lookup of a compressed entry of L_j is one
+// word load + AND + popcount -- no hashing, no probing.  Only the words the
+// row touched are cleared afterwards.
+template <int NT, bool SMEM>
+__global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ list, int64_t nlist,
+                                                   MaskArgs a, uint64_t *slab, int64_t nwords) {
+    extern __shared__ int4 smem[];
+    __shared__ unsigned long long s_tot;
+    uint64_t *bm = SMEM ? reinterpret_cast<uint64_t *>(smem) : slab + (int64_t)blockIdx.x * nwords;
+    unsigned *bm32 = reinterpret_cast<unsigned *>(bm);
+    if (SMEM)
+        for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+    long long mine = 0;
+    for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t r0 = a.lrp[i], r1 = a.lrp[i + 1];
+        bool lower = true;
+        for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) {
+            const int c = a.lcol[q];
+            if ((int64_t)c >= i) lower = false;
+            atomicOr(&bm32[c >> 5], 1u << (c & 31));
+        }
+        if (!lower) kerr(a.err, KERR_NOTLOWER, i);
+        __syncthreads();
+        block_enumerate<NT>(
+            r0, r1,
+            [&](int64_t t, int64_t &st, int &len) {
+                int j = a.lcol[t];
+                st = a.cstart[j];
+                len = a.ccnt[j];
+            },
+            [&](int64_t, int64_t s) { mine += __popcll(a.cbits[s] & bm[a.cset[s]]); });
+        __syncthreads();
+        for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) bm[a.lcol[q] >> 6] = 0ull;
+        __syncthreads();
+    }
+    for (int d = 16; d >= 1; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_tot, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_tot) atomicAdd(a.total, s_tot);
+}
 
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_mask_group(const int32_t *__restrict__ list, int64_t nlist,
@@ -224,7 +276,12 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     uint8_t *bins = nullptr;
     TSG_TRY(tsg_alloc_t(c, &bins, rows));
     BinLists<MB> bl;
-    TSG_TRY(tsg_partition<MB>(c, rows, MaskBinF{l->rp}, bins, bl));
+    // dense tier: bitmap over all columns, in shared memory up to 200 KB,
+    // else a per-CTA global slab (one SM's worth of CTAs, L2-resident)
+    const int64_t nwords = (l->cols + 63) / 64;
+    const bool dense_smem = nwords * 8 <= 200 * 1024;
+    const bool dense_ok = dense_smem || nwords * 8 * c->num_sms <= ((int64_t)1 << 30);
+    TSG_TRY(tsg_partition<MB>(c, rows, MaskBinF{l->rp, dense_ok}, bins, bl));
     int32_t *list = bl.list;
     int64_t off[MB + 1];
     for (int b = 0; b <= MB; b++) off[b] = bl.off[b];
@@ -245,6 +302,23 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
         TSG_TRY(tsg_func_smem((const void *)k_mask_block<512, false>, smem));
         k_mask_block<512, false><<<grid_for(n7, 1, c->num_sms * 4), 512, smem, c->stream>>>(
             list + off[7], n7, a, nullptr, 0, 8192); ++c->launches;
+        TSG_CK(cudaGetLastError());
+    }
+    const int64_t nd = off[MASK_DENSE + 1] - off[MASK_DENSE];
+    uint64_t *dslab = nullptr;
+    if (nd > 0) {
+        const unsigned ctas = (unsigned)(nd < c->num_sms ? nd : c->num_sms);
+        if (dense_smem) {
+            const size_t smem = (size_t)nwords * 8;
+            TSG_TRY(tsg_func_smem((const void *)k_mask_dense<1024, true>, smem));
+            k_mask_dense<1024, true><<<ctas, 1024, smem, c->stream>>>(list + off[MASK_DENSE], nd, a, nullptr,
+                                                                      nwords); ++c->launches;
+        } else {
+            TSG_TRY(tsg_alloc_t(c, &dslab, (size_t)ctas * nwords));
+            TSG_TRY(tsg_fill(c, dslab, 0, (size_t)ctas * nwords * 8, c->stream));
+            k_mask_dense<1024, false><<<ctas, 1024, 0, c->stream>>>(list + off[MASK_DENSE], nd, a, dslab,
+                                                                    nwords); ++c->launches;
+        }
         TSG_CK(cudaGetLastError());
     }
     int64_t n8 = off[9] - off[8];
@@ -270,6 +344,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     int s = tsg_check_kernel_errors(c, "masked count");   // synchronises
     *total = c->h_small[1];
     tsg_free(c, slab);
+    tsg_free(c, dslab);
     tsg_free(c, bins);
     tsg_free(c, list);
     return s;

@@ -263,3 +263,16 @@ def test_sharded_b_gather_matches_replicated(rng):
         db = D.gather_sharded(da, shards, b.num_cols)
         got = _lib.d_multiply(da, db).download()
         assert_same_product(got, O.multiply(aa, b), exact=True)
+
+
+def test_masked_count_dense_hub_rows(rng):
+    # hubs with thousands of lower neighbours take the dense bitmap tier
+    n = 6000
+    up = np.triu(rng.random((n, n)) < 0.002, 1)
+    up[:3, 3:] = True                      # three hubs adjacent to everyone
+    rows, cols = np.nonzero(up | up.T)
+    g = CsrMatrix.from_coo(rows, cols, None, n, n)
+    low = tsg.lower_triangle(g, tsg.degree_sort_permutation(g))
+    want = O.masked_count(low, O.compress(low), workers=8)
+    assert tsg.masked_row_intersect_count(low, tsg.compress(low)) == want
+    assert tsg.count_triangles(g) == want
