@@ -30,7 +30,8 @@ namespace {
 constexpr int CT = 256;                 // threads (= words) per block
 constexpr int PB = CT * 32;             // entries per block
 
-__global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint32_t *rsbits) {
+__global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint32_t *rsbits, int *dmax) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *dmax = 0;   // max set count, raised by P2 / F2
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t e = rp[i];
@@ -264,8 +265,9 @@ __global__ void k_set_starts(int64_t rows, int64_t nnz, const int64_t *__restric
                              const uint32_t *__restrict__ hbits, const uint16_t *__restrict__ wpre,
                              const int64_t *__restrict__ boff, int64_t nblocks,
                              int64_t *__restrict__ start, int32_t *__restrict__ cnt,
-                             const int *unsorted) {
+                             const int *unsorted, int *dmax) {
     if (*unsorted) return;
+    int mx = 0;
     auto rank_at = [&](int64_t e) -> int64_t {
         if (e >= nnz) return boff[nblocks];
         return boff[e / PB] + wpre[e >> 5] + __popc(hbits[e >> 5] & ((1u << (e & 31)) - 1u));
@@ -274,8 +276,15 @@ __global__ void k_set_starts(int64_t rows, int64_t nnz, const int64_t *__restric
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t s0 = rank_at(rp[i]);
         start[i] = s0;
-        if (i < rows) cnt[i] = (int32_t)(rank_at(rp[i + 1]) - s0);
+        if (i < rows) {
+            const int32_t n = (int32_t)(rank_at(rp[i + 1]) - s0);
+            cnt[i] = n;
+            mx = n > mx ? n : mx;
+        }
     }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(dmax, mx);
 }
 
 // ---- first-occurrence fallback for unsorted rows (warp per row)
@@ -314,7 +323,10 @@ __global__ void k_first_emit(int64_t rows, const int64_t *__restrict__ rp,
     for (int64_t i = w; i <= rows; i += nw) {
         if (lane == 0) {
             start[i] = fstart[i];
-            if (i < rows) cnt[i] = fcnt[i];
+            if (i < rows) {
+                cnt[i] = fcnt[i];
+                atomicMax(&cnt[rows + 1], fcnt[i]);   // max set count (slot rows + 1)
+            }
         }
         if (i == rows) continue;
         const int64_t r0 = rp[i], r1 = rp[i + 1];
@@ -348,6 +360,8 @@ __global__ void k_compress_unit(int64_t rows, int64_t nnz, const int64_t *__rest
                                 const int32_t *__restrict__ col, int64_t *__restrict__ start,
                                 int32_t *__restrict__ cnt, int32_t *__restrict__ oset,
                                 uint64_t *__restrict__ obits) {
+    // max set count: 1 (this path runs only for matrices with entries)
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[rows + 1] = 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = rp[i];
@@ -374,14 +388,16 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
             rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;
         TSG_CK(cudaGetLastError());
         cm->sorted_sets = 1;   // one set per row
+        cm->dmax_valid = 1;
         cm->identity_rows = (nnz == rows && b->max_row == 1) ? 1 : 0;
         *out = cm;
         return TSG_OK;
     }
     if (nnz == 0) {
         TSG_TRY(tsg_fill(c, cm->start, 0, (rows + 1) * sizeof(int64_t), c->stream));
-        TSG_TRY(tsg_fill(c, cm->cnt, 0, (rows + 1) * sizeof(int32_t), c->stream));
+        TSG_TRY(tsg_fill(c, cm->cnt, 0, (rows + 2) * sizeof(int32_t), c->stream));
         cm->sorted_sets = 1;
+        cm->dmax_valid = 1;
         *out = cm;
         return TSG_OK;
     }
@@ -401,7 +417,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_fill(c, rsbits, 0, nwords * sizeof(uint32_t), s));
     TSG_TRY(tsg_fill(c, unsorted, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(rows + 1, 256, c->num_sms * 16);
-    k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits); ++c->launches;
+    k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits, cm->cnt + rows + 1); ++c->launches;
     unsigned long long *lbstate = nullptr;
     TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
     TSG_TRY(tsg_fill(c, lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
@@ -411,7 +427,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         nnz, b->col, rsbits, hbits, wpre, bcnt, nblocks, lbstate,
         reinterpret_cast<unsigned *>(lbstate + nblocks), cm->set, cm->bits, unsorted); ++c->launches;
     k_set_starts<<<rgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
-                                       unsorted); ++c->launches;
+                                       unsorted, cm->cnt + rows + 1); ++c->launches;
     // first-occurrence fallback for input not known to be row-sorted: every
     // kernel returns at once if P1 found the rows sorted after all
     if (!b->sorted) {
@@ -430,6 +446,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_free(c, fcnt);
     tsg_free(c, fstart);
     cm->sorted_sets = b->sorted;   // first-touch order of a row-sorted B ascends
+    cm->dmax_valid = 1;
     *out = cm;
     return TSG_OK;
 }

@@ -805,13 +805,14 @@ int tsg_cmat_alloc(tsg_ctx *c, int64_t rows, int64_t cap, tsg_cmat **out) {
     m->sorted_sets = 0;
     m->identity_rows = 0;
     m->cols = 0;
+    m->dmax_valid = 0;
     m->cap = cap;
     m->start = nullptr;
     m->cnt = nullptr;
     m->set = nullptr;
     m->bits = nullptr;
     int s = tsg_alloc_t(c, &m->start, rows + 1);
-    if (s == TSG_OK) s = tsg_alloc_t(c, &m->cnt, rows + 1);
+    if (s == TSG_OK) s = tsg_alloc_t(c, &m->cnt, rows + 2);   // [rows + 1]: max count
     if (s == TSG_OK) s = tsg_alloc_t(c, &m->set, cap);
     if (s == TSG_OK) s = tsg_alloc_t(c, &m->bits, cap);
     if (s != TSG_OK) {

@@ -79,6 +79,7 @@ struct tsg_cmat {
     int sorted_sets;  // 1: every row's sets ascend (compact compression of a row-sorted B)
     int identity_rows;  // 1: row k is exactly set k (start = iota, cnt = 1)
     int64_t cols;       // columns of the source matrix (0: unknown)
+    int dmax_valid;     // 1: cnt[rows + 1] holds the largest row's set count (set by compress)
 };
 
 struct tsg_vec {

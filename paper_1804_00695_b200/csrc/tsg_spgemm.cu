@@ -164,12 +164,7 @@ __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
                              const int32_t *__restrict__ acol, const int32_t *__restrict__ cbcnt,
                              const int *maxcb, int64_t *__restrict__ sbound) {
     const int mcb = *maxcb;
-    if (mcb <= CHEAP_CB) {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
-             i += (int64_t)gridDim.x * blockDim.x)
-            sbound[i] = (arp[i + 1] - arp[i]) * (int64_t)mcb;
-        return;
-    }
+    if (mcb <= CHEAP_CB) return;   // cheap bound len x max: computed by the bin functor (SymBinF)
     const unsigned gm = group_mask<G>();
     const int glane = threadIdx.x & (G - 1);
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -253,15 +248,23 @@ __global__ void k_unit_rows(int64_t rows, const int64_t *__restrict__ rp, const 
 
 // per-row bin functors for tsg_partition (tsg_partition.cuh)
 struct SymBinF {
-    const int64_t *sbound;
+    int64_t *sbound;
     int64_t *counts;
     int32_t *msets;
     int64_t *scap;
     const int64_t *arp;   // non-null: merge tier allowed (row-sorted B, no partial rows)
     int64_t a_row_off;
     int64_t ncols;        // B's columns (> 0: dense tier allowed)
+    const int64_t *carp;  // non-null: cheap bound len(A_i) x max when *cmax <= CHEAP_CB
+    const int *cmax;
     __device__ __forceinline__ int operator()(int64_t i) const {
-        const int64_t sb = sbound[i];
+        int64_t sb;
+        if (carp && *cmax <= CHEAP_CB) {
+            sb = (carp[i + 1] - carp[i]) * (int64_t)*cmax;
+            sbound[i] = sb;
+        } else {
+            sb = sbound[i];
+        }
         int b = sym_bin(sb);
         if (ncols > 0 && sb >= DENSE_MIN_SETS && dense_words(ncols) * 8 <= DENSE_SMEM) {
             scap[i] = sb;
@@ -1640,10 +1643,14 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
     TSG_TRY(tsg_alloc_t(c, &bins, rows_out + 1));
     if (rows_out > 0) {
         // set bounds: partial row length + sum of selected compressed B rows
-        int *maxcb = reinterpret_cast<int *>(c->d_small + 50);
-        TSG_TRY(tsg_fill(c, maxcb, 0, sizeof(int), c->stream));
-        k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
-                                                                                maxcb); ++c->launches;
+        // largest compressed row: kept by compress in cnt[rows + 1], else reduced here
+        int *maxcb = cb->cnt + cb->rows + 1;
+        if (!cb->dmax_valid) {
+            maxcb = reinterpret_cast<int *>(c->d_small + 50);
+            TSG_TRY(tsg_fill(c, maxcb, 0, sizeof(int), c->stream));
+            k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
+                                                                                    maxcb); ++c->launches;
+        }
         if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
             rows_out == a->rows) {
             const unsigned g = grid_for(a->rows, 256, c->num_sms * 16);
@@ -1667,8 +1674,11 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         // B -> compact compression) and there is no partial row to fold in
         const int64_t *merge_arp = (cb->sorted_sets && partial == nullptr) ? a->rp : nullptr;
         const int64_t cb_cols = cb->cols;
+        const bool plain = a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
+                           rows_out == a->rows;
         TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off,
-                                             partial == nullptr ? cb_cols : 0},
+                                             partial == nullptr ? cb_cols : 0,
+                                             plain ? a->rp : nullptr, maxcb},
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
