@@ -93,6 +93,11 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     c->num_calls = 0;
     c->pending = nullptr;
     c->phase_n = c->phase_total = c->phase_dirty = 0;
+    c->lb_state = nullptr;
+    c->lb_cap = 0;
+    c->lb_epoch = 0;
+    c->lb_counter = nullptr;
+    c->lb_base = 0;
     c->timing = 0;
     // every kernel loaded now, not at its first launch (see tsg_preload_module_of)
     TSG_TRY(tsg_preload_module_of(tsg_kernel_core()));
@@ -109,6 +114,8 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
     if (!c) return TSG_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    tsg_free(c, c->lb_state);
+    tsg_free(c, c->lb_counter);
     tsg_arena_trim(c);
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
     cudaFree(c->d_err);
@@ -532,6 +539,37 @@ int tsg_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cuda
     return TSG_OK;
 }
 
+int tsg_lookback_state(tsg_ctx *c, int64_t tiles, unsigned long long **state, unsigned *epoch) {
+    bool clear = false;
+    if (tiles > c->lb_cap) {
+        tsg_free(c, c->lb_state);
+        c->lb_cap = tiles > 4096 ? tiles : 4096;
+        TSG_TRY(tsg_alloc_t(c, &c->lb_state, c->lb_cap));
+        clear = true;
+    }
+    if (++c->lb_epoch > 0x3fffu) {   // wrapped: words of an old call could match again
+        c->lb_epoch = 1;
+        clear = true;
+    }
+    if (clear) TSG_TRY(tsg_fill(c, c->lb_state, 0, (size_t)c->lb_cap * 8, c->stream));
+    *state = c->lb_state;
+    *epoch = c->lb_epoch;
+    return TSG_OK;
+}
+
+int tsg_lookback_counter(tsg_ctx *c, int64_t tiles, unsigned long long **counter,
+                         unsigned long long *base) {
+    if (!c->lb_counter) {
+        TSG_TRY(tsg_alloc_t(c, &c->lb_counter, 1));
+        TSG_TRY(tsg_fill(c, c->lb_counter, 0, sizeof(unsigned long long), c->stream));
+        c->lb_base = 0;
+    }
+    *counter = c->lb_counter;
+    *base = c->lb_base;
+    c->lb_base += (unsigned long long)tiles;
+    return TSG_OK;
+}
+
 int tsg_put_small(tsg_ctx *c, const int64_t *src, int n, int slot) {
     k_put_small<<<1, 32, 0, c->stream>>>(src, c->hd_small + slot, n); ++c->launches;
     TSG_CK(cudaGetLastError());
@@ -605,14 +643,13 @@ __device__ __forceinline__ void st_relaxed_gpu(unsigned long long *p, unsigned l
 template <typename TI>
 __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in, int64_t n,
                                                       int64_t *__restrict__ out,
-                                                      unsigned long long *state, unsigned *counter,
+                                                      unsigned long long *state, unsigned epoch,
                                                       unsigned ntiles) {
+    // tile = block index: blocks are dispatched in index order, so every
+    // predecessor a tile waits for is already resident
     __shared__ int64_t ws[LB_BS / 32];
     __shared__ int64_t s_excl;
-    __shared__ unsigned s_tile;
-    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
+    const unsigned tile = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t base = (int64_t)tile * LB_TILE + (int64_t)threadIdx.x * LB_IT;
     int64_t v[LB_IT];
@@ -639,19 +676,19 @@ __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in
     if (w == 0) {
         if (tile == 0) {
             if (lane == 0) {
-                st_relaxed_gpu(&state[0], ((unsigned long long)agg << 2) | 2ull);
+                st_relaxed_gpu(&state[0], lb_pack(agg, epoch, 2));
                 s_excl = 0;
             }
         } else {
-            if (lane == 0) st_relaxed_gpu(&state[tile], ((unsigned long long)agg << 2) | 1ull);
+            if (lane == 0) st_relaxed_gpu(&state[tile], lb_pack(agg, epoch, 1));
             int64_t excl = 0;
             int64_t pred = (int64_t)tile - 1 - lane;
             for (;;) {
-                const unsigned long long sv = pred >= 0 ? ld_relaxed_gpu(&state[pred]) : 2ull;
-                const unsigned flag = (unsigned)(sv & 3ull);
+                const unsigned long long sv = pred >= 0 ? ld_relaxed_gpu(&state[pred]) : lb_pack(0, epoch, 2);
+                const unsigned flag = lb_flag(sv, epoch);
                 if (__any_sync(0xffffffffu, flag == 0)) continue;   // a predecessor not published yet
                 const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
-                int64_t val = (int64_t)(sv >> 2);
+                int64_t val = lb_value(sv);
                 if (incl) {
                     const int k = __ffs(incl) - 1;   // nearest inclusive prefix
                     if (lane > k) val = 0;
@@ -663,7 +700,7 @@ __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in
                 pred -= 32;
             }
             if (lane == 0) {
-                st_relaxed_gpu(&state[tile], ((unsigned long long)(excl + agg) << 2) | 2ull);
+                st_relaxed_gpu(&state[tile], lb_pack(excl + agg, epoch, 2));
                 s_excl = excl;
             }
         }
@@ -734,14 +771,13 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     }
     const int64_t tiles = (n + LB_TILE - 1) / LB_TILE;
     unsigned long long *state = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &state, tiles + 1));   // + the tile counter
-    TSG_TRY(tsg_fill(c, state, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
+    unsigned epoch = 0;
+    TSG_TRY(tsg_lookback_state(c, tiles, &state, &epoch));
     // in-place safe: a tile reads its inputs before writing, and writes only
     // its own range (plus out[n], past every input)
-    scan_lookback<TI><<<(unsigned)tiles, LB_BS, 0, c->stream>>>(
-        in, n, out, state, reinterpret_cast<unsigned *>(state + tiles), (unsigned)tiles); ++c->launches;
+    scan_lookback<TI><<<(unsigned)tiles, LB_BS, 0, c->stream>>>(in, n, out, state, epoch, (unsigned)tiles);
+    ++c->launches;
     TSG_CK(cudaGetLastError());
-    TSG_TRY(tsg_free(c, state));
     return TSG_OK;
 }
 }  // namespace

@@ -57,6 +57,14 @@ struct tsg_ctx {
     cudaEvent_t ev_ring[2 * NRING];
     int64_t num_calls;
     int64_t ring_timed[NRING];   // call id recorded in each ring slot (-1: none)
+    // decoupled look-back tile states, shared by every single-pass scan: words
+    // carry the call's epoch, so no per-call clearing (tsg_lookback_state)
+    unsigned long long *lb_state;
+    int64_t lb_cap;
+    unsigned lb_epoch;
+    // monotone tile counter (never reset): a call's tiles are counter - base
+    unsigned long long *lb_counter;
+    unsigned long long lb_base;
 };
 
 struct tsg_csr {
@@ -130,6 +138,21 @@ int tsg_check_kernel_errors(tsg_ctx *ctx, const char *phase);
 // copy n int64 device words into h_small[slot..] through the mapped alias
 // (a one-thread kernel on the compute stream; the caller synchronises)
 int tsg_put_small(tsg_ctx *ctx, const int64_t *src, int n, int slot);
+// look-back state words for `tiles` tiles and this call's epoch (1..16383)
+int tsg_lookback_state(tsg_ctx *ctx, int64_t tiles, unsigned long long **state, unsigned *epoch);
+// dynamic tile ids for a look-back kernel of `tiles` blocks: tile =
+// atomicAdd(*counter, 1) - base (tiles are then started in id order)
+int tsg_lookback_counter(tsg_ctx *ctx, int64_t tiles, unsigned long long **counter,
+                         unsigned long long *base);
+// word = value << 16 | epoch << 2 | flag (1 aggregate, 2 inclusive prefix);
+// a word of another epoch reads as flag 0 (not yet published)
+__device__ __forceinline__ unsigned long long lb_pack(int64_t v, unsigned epoch, unsigned flag) {
+    return ((unsigned long long)v << 16) | ((unsigned long long)epoch << 2) | flag;
+}
+__device__ __forceinline__ unsigned lb_flag(unsigned long long w, unsigned epoch) {
+    return ((unsigned)(w >> 2) & 0x3fffu) == epoch ? (unsigned)(w & 3ull) : 0u;
+}
+__device__ __forceinline__ int64_t lb_value(unsigned long long w) { return (int64_t)(w >> 16); }
 // Load every kernel of the translation unit that holds `kernel` now.  With
 // CUDA's lazy module loading, the first launch of a kernel waits for copies
 // already queued on other streams (measured: a first-launched compute kernel
