@@ -276,3 +276,23 @@ def test_masked_count_dense_hub_rows(rng):
     want = O.masked_count(low, O.compress(low), workers=8)
     assert tsg.masked_row_intersect_count(low, tsg.compress(low)) == want
     assert tsg.count_triangles(g) == want
+
+
+def test_empty_and_degenerate_shapes(rng):
+    """Zero rows / columns / entries behave like the reference (empty results,
+    no device errors), through every public entry point."""
+    empty = CsrMatrix.empty
+    cases = [(empty(0, 5), random_csr(rng, 5, 7, 3)),
+             (random_csr(rng, 4, 5, 3), empty(5, 0)),
+             (empty(3, 4), empty(4, 6)),
+             (CsrMatrix.from_coo([0], [0], [2.5], 1, 1), CsrMatrix.from_coo([0], [0], [-4.0], 1, 1))]
+    for a, b in cases:
+        want = O.multiply(a, b)
+        assert_same_product(tsg.multiply(a, b), want, exact=True)
+        counts = tsg.spgemm_symbolic(a, tsg.compress(b))
+        assert np.array_equal(np.asarray(counts), np.diff(want[0]))
+        assert_same_product(tsg.spgemm_numeric(a, b, counts), want, exact=True)
+        assert tsg.count_multiplications(a, b) == O.count_multiplications(a, b)
+    z = empty(0, 0, pattern=True)
+    assert tsg.count_triangles(z) == 0
+    assert tsg.masked_row_intersect_count(empty(3, 3, pattern=True), tsg.compress(empty(3, 3, pattern=True))) == 0
