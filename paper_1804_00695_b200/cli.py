@@ -16,7 +16,9 @@ took:
 * placement modes (all_slow, b_in_fast): ``device_seconds`` of the multiply
   reading / writing the slow operands in mapped host memory over PCIe;
 * chunk mode: the physical executor's wall / kernel seconds and DMA bytes
-  (``CopyLedger.physical``).
+  (``CopyLedger.physical``);
+* ``b200_model_seconds``: the reference's linear model with the parameters
+  fitted to B200 runs (memory.estimate_kernel_time_b200, §8f row 4).
 
 ``workers`` is accepted and recorded; results do not depend on it.
 """
@@ -40,7 +42,8 @@ from .generators import (BIGSTAR2D, BRICK3D, ELASTICITY3D, LAPLACE3D, StencilSpe
 from .kernel import compress, spgemm_numeric, spgemm_symbolic
 from .matrix_market import read_matrix_market, write_matrix_market
 from .memory import (CHUNKED, MemoryModel, MemorySpaceSpec, PlacementPolicy,
-                     compute_access_stats, estimate_kernel_time, validate_placement)
+                     compute_access_stats, estimate_kernel_time, estimate_kernel_time_b200,
+                     validate_placement)
 from .triangles import count_triangles, load_graph
 
 SCHEMA_VERSION = 1
@@ -221,6 +224,9 @@ def run_experiment(spec: ExperimentSpec, ledger_capture: list | None = None) -> 
             if not ok:
                 raise VerifyError("mode %s result diverges from the plain kernel "
                                   "(max relative difference %.3e)" % (spec.mode, rel))
+        meas["b200_model_seconds"] = estimate_kernel_time_b200(
+            stats, PlacementPolicy.from_name(CHUNKED if spec.mode == "chunk" else spec.mode),
+            size_a=size_a, size_c=size_c, row_bytes_b=row_bytes_b)
         runs.append({"rep": rep, "flops": 2 * stats.accumulator_inserts,
                      "multiplications": stats.accumulator_inserts, "c_nnz": int(c.nnz),
                      "simulated_seconds": kernel_s + copy_s, "kernel_seconds": kernel_s,
