@@ -85,3 +85,25 @@ def test_reference_byte_convention():
     assert int(m.row_byte_sizes().sum()) == m.byte_size
     p = CsrMatrix(3, 4, [0, 2, 2, 3], [0, 1, 3], None)
     assert p.byte_size == 8 * 4 + 8 * 3
+
+
+REFERENCE_EXPORTS = (   # /root/reference/pkg/src/tiered_spgemm/__init__.py:10-39
+    "HashmapAccumulator MemoryPool accumulator_capacity GPU_CHUNK1_AC_IN_PLACE GPU_CHUNK2_B_IN_PLACE "
+    "KNL_CHUNK ChunkPlan RowPartition binary_search_partition copy_cost_chunk1 copy_cost_chunk2 "
+    "decide_chunking execute_plan gpu_chunk_multiply_1 gpu_chunk_multiply_2 knl_chunk_multiply "
+    "plan_for_multiply CsrMatrix canonicalize matrices_equal products_match slice_rows transpose validate "
+    "CapacityError DimensionError GraphError GridError KernelError MatrixMarketError MatrixValidationError "
+    "PlacementError TieredSpgemmError UnsplittableRowError VerifyError BIGSTAR2D BRICK3D ELASTICITY3D "
+    "LAPLACE3D STENCIL_KINDS StencilSpec generate_interpolation generate_random_rhs generate_stencil "
+    "grid_for_target_bytes stencil_byte_size stencil_nnz CompressedMatrix RowRange compress "
+    "count_multiplications masked_row_intersect_count multiply spgemm_numeric spgemm_numeric_fused "
+    "spgemm_symbolic read_matrix_market write_matrix_market AccessStats CopyLedger MemoryModel "
+    "MemorySpaceSpec PlacementPolicy compute_access_stats default_model estimate_kernel_time simulate_copy "
+    "validate_placement PortableRng count_triangles degree_sort_permutation load_graph lower_triangle "
+    "to_undirected_pattern").split()
+
+
+def test_public_surface_covers_the_reference():
+    import paper_1804_00695_b200 as tsg
+    missing = [n for n in REFERENCE_EXPORTS if not hasattr(tsg, n)]
+    assert not missing, missing
