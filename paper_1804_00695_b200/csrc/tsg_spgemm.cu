@@ -306,6 +306,8 @@ struct NumBinF {
 
 // ======================================================================= K2 group tier
 
+constexpr int SYM_OPT_T = 32;   // first table size for unit rows (up to 32 distinct sets)
+
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
@@ -321,10 +323,20 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
         const int64_t gi = i + a.a_row_off;
         int T = table_slots(a.sbound[i]);
         if (T > TMAX) T = 1 << ilog2_pow2(TMAX);
-        const int logT = ilog2_pow2(T);
+        const int Tfull = T;
+        const bool unit = a.maxcb && *a.maxcb <= 1;
+        // unit compressed rows: the bound (one set per A entry) overstates the
+        // distinct sets several-fold (RA*P rows: 64 entries, ~10 sets), so the
+        // union first runs in a small table and is redone at the bound's size
+        // only if that one overflows
+        if (unit && T > SYM_OPT_T) T = SYM_OPT_T;
+        int logT;
+        bool ok;
+        for (;;) {
+        logT = ilog2_pow2(T);
         tbl_clear(tbl, T, glane, G);
         __syncwarp(gm);
-        bool ok = true;
+        ok = true;
         if (a.prp) {
             for (int64_t q = a.prp[i] + glane; q < a.prp[i + 1]; q += G) {
                 int c = a.pcol[q];
@@ -333,7 +345,7 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                              bit >= 32 ? 1u << (bit - 32) : 0u);
             }
         }
-        if (a.maxcb && *a.maxcb <= 1) {
+        if (unit) {
             // unit compressed rows: batch the three dependent load rounds of UB chunks
             const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
             for (int64_t base = a0; base < a1; base += UB * G) {
@@ -387,6 +399,9 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
                 });
         }
         __syncwarp(gm);
+        if (T == Tfull || __all_sync(gm, ok)) break;
+        T = Tfull;   // the optimistic table overflowed: redo at the bound's size
+        }
         // compact occupied slots as sortable (key << 32 | slot) into the scratch
         // area behind the table; count columns on the way
         uint64_t *ck = reinterpret_cast<uint64_t *>(tbl + T);
