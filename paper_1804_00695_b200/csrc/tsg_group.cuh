@@ -73,9 +73,12 @@ __device__ __forceinline__ int slot_pop(const int4 &e) {
 
 // rank of column `bit` inside a 64-bit set mask (number of lower set bits)
 __device__ __forceinline__ int mask_rank(const int4 &e, int bit) {
-    unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
-    if (bit < 32) return __popc(lo & ((1u << bit) - 1u));
-    return __popc(lo) + __popc(hi & ((1u << (bit - 32)) - 1u));
+    // branch-free: pick the half, add the low half's count for high bits
+    const unsigned lo = (unsigned)e.y, hi = (unsigned)e.z;
+    const bool upper = bit >= 32;
+    const unsigned half = upper ? hi : lo;
+    const unsigned below = (1u << (bit & 31)) - 1u;
+    return (upper ? __popc(lo) : 0) + __popc(half & below);
 }
 
 // ---------------------------------------------------------------- enumerate
