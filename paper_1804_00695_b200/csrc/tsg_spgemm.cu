@@ -182,7 +182,7 @@ __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
 // shared memory (table + dense values).  CTA tier: one row per CTA, table in
 // shared memory.  Global tier: one row per CTA, table in a global slab.
 
-constexpr int NBINS = 14;   // 0-6 group, 7-8 CTA, 9 global, 10-12 symbolic merge, 13 dense
+constexpr int NBINS = 15;   // 0-6 group, 7-8 CTA, 9 global, 10-12 symbolic merge, 13 dense, 14 thread
 // bins 0..6: group tier slices (bytes) and group sizes
 __host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
 __host__ __device__ constexpr int gt_g(int b) { return b <= 1 ? 8 : (b == 2 ? 16 : 32); }
@@ -203,6 +203,13 @@ constexpr int BIN_MERGE = 10;
 // columns (power-law hubs): one CTA per row, a shared-memory bitmap of all
 // of B's column sets (symbolic) / a per-set base + mask array (numeric).
 constexpr int BIN_DENSE = 13;
+// bin 14 (symbolic): thread-per-row tier for B with exactly one entry per row
+// (aggregation operators, RA*P): each A entry adds one set, so one thread per
+// row keeps the row's sorted sets itself -- no group coordination, no table.
+// (A thread-per-row numeric measured slower than the group tier: 0.37 vs
+// 0.26 ms on config 2's RA*P -- its per-product chains are latency-bound.)
+constexpr int BIN_THREAD = 14;
+constexpr int THREAD_MAX_A = 64;
 constexpr int DENSE_MIN_SETS = 2048;           // bound (sets) from which a row goes dense
 constexpr int64_t DENSE_SMEM = 200 * 1024;     // shared-memory budget of the dense kernels
 __host__ __device__ __forceinline__ int64_t dense_words(int64_t ncols) { return (ncols + 63) / 64; }
@@ -257,7 +264,16 @@ struct SymBinF {
     int64_t ncols;        // B's columns (> 0: dense tier allowed)
     const int64_t *carp;  // non-null: cheap bound len(A_i) x max when *cmax <= CHEAP_CB
     const int *cmax;
+    const int64_t *tarp;  // non-null: thread tier allowed (B rows are exactly one entry each)
     __device__ __forceinline__ int operator()(int64_t i) const {
+        if (tarp) {
+            const int64_t alen = tarp[i + a_row_off + 1] - tarp[i + a_row_off];
+            if (alen > 0 && alen <= THREAD_MAX_A) {
+                sbound[i] = alen;
+                scap[i] = alen;
+                return BIN_THREAD;
+            }
+        }
         int64_t sb;
         if (carp && *cmax <= CHEAP_CB) {
             sb = (carp[i + 1] - carp[i]) * (int64_t)*cmax;
@@ -636,6 +652,63 @@ __global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ li
             if (a.msets) a.msets[i] = tot | (a.oset ? SETS_WRITTEN : 0);
         }
         __syncthreads();
+    }
+}
+
+// Thread tier, symbolic: one thread per row of A whose B rows are single
+// entries (compressed row k = set k).  The row's sets are kept sorted in a
+// per-thread local array (appends and hits on the last set are the common
+// case for sorted A rows; otherwise binary search + shift).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_sym_thread(const int32_t *__restrict__ list, int64_t nlist,
+                                                   SymArgs a) {
+    for (int64_t li = (int64_t)blockIdx.x * NT + threadIdx.x; li < nlist; li += (int64_t)gridDim.x * NT) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+        int key[THREAD_MAX_A];
+        uint64_t msk[THREAD_MAX_A];
+        int m = 0;
+        for (int64_t t = a0; t < a1; ++t) {
+            int k = a.acol[t];
+            if (k < a.b_lo || k >= a.b_hi) continue;
+            k -= a.b_lo;
+            const int sset = a.cbset[k];
+            const uint64_t bits = a.cbbits[k];
+            if (m > 0 && key[m - 1] == sset) {
+                msk[m - 1] |= bits;
+            } else if (m == 0 || key[m - 1] < sset) {
+                key[m] = sset;
+                msk[m] = bits;
+                ++m;
+            } else {
+                int lo = 0, hi = m - 1;   // first key >= sset
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key[mid] < sset) lo = mid + 1; else hi = mid;
+                }
+                if (key[lo] == sset) {
+                    msk[lo] |= bits;
+                } else {
+                    for (int q = m; q > lo; --q) {
+                        key[q] = key[q - 1];
+                        msk[q] = msk[q - 1];
+                    }
+                    key[lo] = sset;
+                    msk[lo] = bits;
+                    ++m;
+                }
+            }
+        }
+        const int64_t sp = a.sptr[i];
+        int cnt = 0;
+        for (int q = 0; q < m; ++q) {
+            a.oset[sp + q] = key[q];
+            a.obits[sp + q] = msk[q];
+            cnt += __popcll(msk[q]);
+        }
+        a.counts[i] = cnt;
+        if (a.msets) a.msets[i] = m | SETS_WRITTEN;
     }
 }
 
@@ -1506,6 +1579,15 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
+int launch_sym_thread(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+    const int64_t n = bl.off[BIN_THREAD + 1] - bl.off[BIN_THREAD];
+    if (n <= 0) return TSG_OK;
+    const unsigned grid = grid_for(n, 128, c->num_sms * 16);
+    k_sym_thread<128><<<grid, 128, 0, c->stream>>>(bl.list + bl.off[BIN_THREAD], n, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_thread", BIN_THREAD, grid, 128, 0));
+    return TSG_OK;
+}
+
 int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols) {
     const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
     if (n <= 0) return TSG_OK;
@@ -1572,6 +1654,7 @@ struct BinFork {
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     BinFork f(c);
     auto cnt = [&](int b) { return bl.off[b + 1] - bl.off[b]; };
+    TSG_TRY(f.run(cnt(BIN_THREAD), [&] { return launch_sym_thread(c, bl, a); }));
     TSG_TRY(f.run(cnt(BIN_MERGE + 0), [&] { return launch_sym_merge<0>(c, bl, a); }));
     TSG_TRY(f.run(cnt(BIN_MERGE + 1), [&] { return launch_sym_merge<1>(c, bl, a); }));
     TSG_TRY(f.run(cnt(BIN_MERGE + 2), [&] { return launch_sym_merge<2>(c, bl, a); }));
@@ -1693,7 +1776,8 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
                            rows_out == a->rows;
         TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off,
                                              partial == nullptr ? cb_cols : 0,
-                                             plain ? a->rp : nullptr, maxcb},
+                                             plain ? a->rp : nullptr, maxcb,
+                                             (plain && cb->identity_rows) ? a->rp : nullptr},
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
