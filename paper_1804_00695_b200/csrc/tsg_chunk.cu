@@ -156,7 +156,8 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
     bool fresh = false;
     TSG_TRY(ensure(c, d, rows, nnz, h.val != nullptr, &fresh));
-    d.m.sorted = 0;      // host rows are not inspected: compress keeps its fallback
+    d.m.sorted = 0;      // host rows not inspected here: finish_rows checks them on the device
+    d.m.distinct = 0;
     d.m.max_row = -1;
     cudaStream_t s = c->copy_in;
     // freshly allocated buffers come from the compute-stream-ordered arena:
@@ -407,7 +408,12 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi,
                           int64_t rows) -> int {
         TSG_TRY(finish_rows(c, A));
+        const bool fresh_b = B.pending;
         TSG_TRY(finish_rows(c, B));
+        // row order of a freshly staged B chunk, learnt on the device: enables
+        // the compress fast path and the lane-split numeric mode (a short host
+        // wait for the compute stream, once per staged chunk)
+        if (fresh_b) TSG_TRY(tsg_csr_check_sorted(c, &B.m));
         cudaEvent_t e0, e1;
         TSG_CK(cudaEventCreate(&e0));
         TSG_CK(cudaEventCreate(&e1));

@@ -903,12 +903,18 @@ __global__ void k_rows_unsorted(int64_t rows, const int64_t *__restrict__ rp,
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long ml = 0;
     bool bad = false;
+    bool dup = false;
     for (int64_t i = w; i < rows; i += nw) {
         const int64_t r0 = rp[i], r1 = rp[i + 1];
         if ((unsigned long long)(r1 - r0) > ml) ml = (unsigned long long)(r1 - r0);
-        for (int64_t t = r0 + 1 + lane; t < r1; t += 32) bad |= col[t] < col[t - 1];
+        for (int64_t t = r0 + 1 + lane; t < r1; t += 32) {
+            bad |= col[t] < col[t - 1];
+            dup |= col[t] == col[t - 1];
+        }
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) *flag = 1;
+    // bit 0: some row decreases; bit 1: a column repeats next to itself
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(flag, 2);
     if (lane == 0 && ml) atomicMax(maxlen, ml);
 }
 }  // namespace
@@ -924,7 +930,10 @@ int tsg_csr_check_sorted(tsg_ctx *c, tsg_csr *m) {
     int64_t h[2] = {0, 0};
     TSG_CK(cudaMemcpyAsync(h, c->d_small + 52, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     TSG_CK(cudaStreamSynchronize(c->stream));
-    m->sorted = ((int)h[0]) ? 0 : 1;
+    m->sorted = ((int)h[0] & 1) ? 0 : 1;
+    // distinct is only certain for sorted rows (an unsorted row could repeat a
+    // column non-adjacently)
+    m->distinct = m->sorted && !((int)h[0] & 2);
     m->max_row = h[1];
     return TSG_OK;
 }
@@ -1023,6 +1032,7 @@ extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, i
     }
     TSG_CK(cudaGetLastError());
     s->sorted = m->sorted;
+    s->distinct = m->distinct;
     s->max_row = m->max_row;
     *out = s;
     return TSG_OK;
@@ -1076,6 +1086,20 @@ extern "C" int tsg_csr_map_host(tsg_ctx *c, int64_t rows, int64_t cols, int64_t 
         m->col[i] = (int32_t)v;
     }
     if (values) memcpy(m->val, values, nnz * sizeof(double));
+    // row order facts on the host copy (compress fast path, lane-split numeric)
+    bool sorted = true, distinct = true;
+    int64_t mx = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+        const int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+        mx = hi - lo > mx ? hi - lo : mx;
+        for (int64_t t = lo + 1; t < hi; ++t) {
+            sorted &= m->col[t] >= m->col[t - 1];
+            distinct &= m->col[t] != m->col[t - 1];
+        }
+    }
+    m->sorted = sorted ? 1 : 0;
+    m->distinct = (sorted && distinct) ? 1 : 0;
+    m->max_row = mx;
     *out = m;
     return TSG_OK;
 }

@@ -358,6 +358,7 @@ extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr 
     tsg_free(c, pos);
     TSG_CK(cudaGetLastError());
     L->sorted = 1;
+    L->distinct = 0;   // duplicates of the input graph survive the relabelling
     L->max_row = h2[1];
     *out = L;
     return TSG_OK;
@@ -468,6 +469,7 @@ extern "C" int tsg_rmat_graph(tsg_ctx *c, int scale, int edge_factor, uint64_t s
     TSG_CK(cudaGetLastError());
     tsg_free(c, keys);
     g->sorted = 1;
+    g->distinct = 1;   // de-duplicated keys
     g->max_row = hml;
     *out = g;
     return TSG_OK;
@@ -600,7 +602,7 @@ extern "C" int tsg_gather_sharded(tsg_ctx *c, int n_shards, const int64_t *row_l
     TSG_TRY(tsg_free(c, rp));
     TSG_TRY(tsg_free(c, d_lo));
     TSG_TRY(tsg_free(c, (void *)d_ptrs));
-    B->sorted = 0;   // shard rows are taken as they are
+    B->sorted = 0;   // shard rows are taken as they are (tsg_csr_check_sorted below)
     B->max_row = -1;
     TSG_TRY(tsg_csr_check_sorted(c, B));
     *out = B;

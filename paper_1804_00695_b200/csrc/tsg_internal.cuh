@@ -74,6 +74,7 @@ struct tsg_csr {
     double *val;
     int host_mapped;   // arrays live in pinned, device-mapped host memory (placement)
     int sorted;        // 1: every row's columns are non-decreasing (compress needs no fallback)
+    int distinct;      // 1: no column repeats within a row (lane-split numeric mode is race-free)
     int64_t max_row;   // longest row, or -1 if unknown
 };
 

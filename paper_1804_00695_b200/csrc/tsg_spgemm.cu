@@ -1925,7 +1925,8 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         na.ccol = C->col;
         na.cval = C->val;
         na.err = c->d_err;
-        na.seq = b->rows > 0 ? (int)(b->nnz / b->rows) : 0;
+        na.seq = (b->distinct && b->rows > 0) ? (int)(b->nnz / b->rows) : 0;   // lanes split a B row
+        // only when its columns are known distinct (a repeated column would race)
         na.sptr = counts->sptr;
         na.sset = counts->sset;
         na.sbits = counts->sbits;
@@ -1971,6 +1972,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     int s = TSG_OK;
     if (C->host_mapped) tsg_free(c, cptr);
     C->sorted = 1;   // every emitted row lists its columns in ascending order
+    C->distinct = 1;
     if (s != TSG_OK) {
         tsg_csr_free(c, C);
         return s;
@@ -2037,7 +2039,8 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
     na.ccol = ccol;
     na.cval = cval;
     na.err = c->d_err;
-    na.seq = b->rows > 0 ? (int)(b->nnz / b->rows) : 0;
+    na.seq = (b->distinct && b->rows > 0) ? (int)(b->nnz / b->rows) : 0;   // lanes split a B row
+        // only when its columns are known distinct (a repeated column would race)
     na.pcol = ccol;            // in place
     na.pval = cval;
     na.pstart = cptr;

@@ -296,3 +296,19 @@ def test_empty_and_degenerate_shapes(rng):
     z = empty(0, 0, pattern=True)
     assert tsg.count_triangles(z) == 0
     assert tsg.masked_row_intersect_count(empty(3, 3, pattern=True), tsg.compress(empty(3, 3, pattern=True))) == 0
+
+
+def test_duplicate_columns_in_b_rows(rng):
+    """Repeated columns inside a B row (legal in the reference: compress ORs
+    them, numeric sums them in order) must not race in the lane-split mode."""
+    a = random_csr(rng, 200, 300, 10)
+    base = canonicalize(random_csr(rng, 300, 400, 30))
+    rows = np.repeat(np.arange(300), np.diff(base.row_ptr))
+    dup_r = np.concatenate([rows, rows[::3]])
+    dup_c = np.concatenate([base.col_idx, base.col_idx[::3]])
+    dup_v = np.concatenate([base.values, base.values[::3] * 0.5])
+    b = CsrMatrix.from_coo(dup_r, dup_c, dup_v, 300, 400)   # sorted rows with adjacent repeats
+    want = O.multiply(a, b)
+    assert_same_product(tsg.multiply(a, b), want, exact=True)
+    counts = tsg.spgemm_symbolic(a, tsg.compress(b))
+    assert_same_product(tsg.spgemm_numeric(a, b, counts), want, exact=True)
