@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--phases", action="store_true", help="print per-phase device times and exit")
+    ap.add_argument("--base", type=int, default=128,
+                    help="config 2 fine grid edge per GPU (BASELINE config 2: 128)")
     ap.add_argument("--b-mode", default="replicated", choices=["replicated", "sharded"],
                     help="N>1: B all-gathered once (replicated) or kept as row shards read "
                          "from peer HBM through CUDA IPC (sharded, SURVEY.md §8e)")
@@ -243,7 +245,7 @@ def main():
     ctx = _lib.Context.get(local)
     ctx.set_timing(True)
 
-    dims, a_loc, r, p = build_problem(world, rank)
+    dims, a_loc, r, p = build_problem(world, rank, args.base)
     dr = _lib.DeviceCsr.upload(r, ctx)
     dp = _lib.DeviceCsr.upload(p, ctx)
     setup = {}
