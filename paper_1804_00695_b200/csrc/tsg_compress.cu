@@ -92,6 +92,61 @@ constexpr int EMIT_CAP = 4096;   // staged runs per block (~50 KB); more -> dire
 constexpr int EMIT_PAD = EMIT_CAP + EMIT_CAP / 32;
 constexpr size_t EMIT_SMEM = (size_t)EMIT_PAD * 12 > (size_t)PB * 4 ? (size_t)EMIT_PAD * 12 : (size_t)PB * 4;
 
+// Head flags of one 32-entry word: entry q opens a (row, set) run if it
+// starts a row or its set differs from entry q-1's (pv = set of the entry
+// before the word, -1 at the matrix start).  A set that goes DOWN inside a
+// row marks the matrix unsorted.  FULL: all 32 entries valid.
+template <bool FULL>
+__device__ __forceinline__ uint32_t word_heads(const int (&c)[32], uint32_t rs, int pv, int64_t left,
+                                               bool &bad) {
+    uint32_t hw = 0;
+    bool b = false;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        const int sv = c[q] >> 6;
+        const bool valid = FULL || q < left;
+        const bool start = (rs >> q) & 1u;
+        if (valid) {
+            hw |= (uint32_t)(start || sv != pv) << q;
+            b |= !start && sv < pv;
+        }
+        pv = sv;
+    }
+    bad = b;
+    return hw;
+}
+
+// Emit the word's runs walking BACKWARD: acc collects the bits of the run
+// being walked (seeded with the read-ahead bits of the last run), and at its
+// head the run is complete and stored at rank r (block-relative when staged,
+// else at b0 + r in global memory).  Entries before the word's first head
+// belong to the previous word's last run and are skipped (r < r0 there).
+template <bool FULL>
+__device__ __forceinline__ void emit_runs(const int (&c)[32], uint32_t hw, int r, uint64_t acc, int64_t left,
+                                          bool staged, int64_t b0, int32_t *s_set, uint32_t *s_lo,
+                                          uint32_t *s_hi, int32_t *__restrict__ oset,
+                                          uint64_t *__restrict__ obits) {
+#pragma unroll
+    for (int q = 31; q >= 0; --q) {
+        if (FULL || q < left) {
+            acc |= 1ull << (c[q] & 63);
+            if ((hw >> q) & 1u) {
+                if (staged) {
+                    const int pr = r + (r >> 5);
+                    s_set[pr] = c[q] >> 6;
+                    s_lo[pr] = (uint32_t)acc;
+                    s_hi[pr] = (uint32_t)(acc >> 32);
+                } else {
+                    oset[b0 + r] = c[q] >> 6;
+                    obits[b0 + r] = acc;
+                }
+                --r;
+                acc = 0;
+            }
+        }
+    }
+}
+
 // P1+P2+P3 in one pass (single launch, columns read once): each tile finds
 // its heads, scans them block-wide, obtains its global run offset by a
 // decoupled look-back over the tiles before it (tile ids from an atomic
@@ -139,21 +194,13 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
         prev = t0 > 0 && t0 < nnz + 1 ? (__ldg(col + t0 - 1) >> 6) : -1;
     }
     __syncthreads();   // the column stage is reused for the output below
-    uint32_t hw = 0, rs = 0;
+    uint32_t hw = 0;
     bool bad = false;
-    if (t0 < nnz) {
-        rs = rsbits[word];
-        int pv = prev;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const int sv = c[q] >> 6;
-            const bool valid = t0 + q < nnz;
-            const bool start = (rs >> q) & 1u;
-            const bool head = valid && (start || t0 + q == 0 || sv != pv);
-            bad |= valid && !start && t0 + q > 0 && sv < pv;
-            hw |= (uint32_t)head << q;
-            pv = sv;
-        }
+    if (t0 + 32 <= nnz) {
+        hw = word_heads<true>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
+        hbits[word] = hw;
+    } else if (t0 < nnz) {
+        hw = word_heads<false>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
         hbits[word] = hw;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
@@ -210,44 +257,24 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
         __syncthreads();
     }
     if (hw) {
+        // the last run may continue into the next words (same row, same set):
+        // its owner reads ahead until the next head
+        uint64_t acc = 0;
+        if (t0 + 32 < nnz) {
+            const int lset = c[31] >> 6;   // entry 31 belongs to the word's last run
+            for (int64_t g = t0 + 32; g < nnz; ++g) {
+                if ((__ldg(rsbits + (g >> 5)) >> (g & 31)) & 1u) break;
+                const int cg = __ldg(col + g);
+                if ((cg >> 6) != lset) break;
+                acc |= 1ull << (cg & 63);
+            }
+        }
         const int64_t b0 = staged ? 0 : s_b0;
-        int r = r0;
-        int set = -1;
-        uint64_t bits = 0;
-        auto put = [&](int rr, int st, uint64_t bb) {
-            if (staged) {
-                const int pr = rr + (rr >> 5);
-                s_set[pr] = st;
-                s_lo[pr] = (uint32_t)bb;
-                s_hi[pr] = (uint32_t)(bb >> 32);
-            } else {
-                oset[b0 + rr] = st;
-                obits[b0 + rr] = bb;
-            }
-        };
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const bool valid = t0 + q < nnz;
-            const uint64_t b = 1ull << (c[q] & 63);
-            if (valid && ((hw >> q) & 1u)) {
-                if (set >= 0) {
-                    put(r, set, bits);
-                    ++r;
-                }
-                set = c[q] >> 6;
-                bits = b;
-            } else if (valid && set >= 0) {
-                bits |= b;
-            }
-        }
-        // the last run may continue into the next words: same row, same set
-        for (int64_t g = t0 + 32; g < nnz; ++g) {
-            if ((__ldg(rsbits + (g >> 5)) >> (g & 31)) & 1u) break;
-            const int cg = __ldg(col + g);
-            if ((cg >> 6) != set) break;
-            bits |= 1ull << (cg & 63);
-        }
-        put(r, set, bits);
+        const int rlast = r0 + __popc(hw) - 1;
+        if (t0 + 32 <= nnz)
+            emit_runs<true>(c, hw, rlast, acc, nnz - t0, staged, b0, s_set, s_lo, s_hi, oset, obits);
+        else
+            emit_runs<false>(c, hw, rlast, acc, nnz - t0, staged, b0, s_set, s_lo, s_hi, oset, obits);
     }
     if (!staged) return;
     if (w == 0) look_back();

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "tsg_internal.cuh"
+#include <atomic>
 
 static thread_local char g_err[1024] = "";
 
@@ -80,6 +81,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaMalloc(&c->d_small, 64 * sizeof(int64_t)));
     TSG_CK(cudaHostAlloc(&c->h_small, 64 * sizeof(int64_t), cudaHostAllocMapped));
     TSG_CK(cudaHostGetDevicePointer(&c->hd_small, c->h_small, 0));
+    memset(c->h_small, 0, 64 * sizeof(int64_t));   // sequence words start below any issued seq
     int init_err[2] = {0, 0x7fffffff};
     TSG_CK(cudaMemcpy(c->d_err, init_err, sizeof(init_err), cudaMemcpyHostToDevice));
     for (int i = 0; i < 8; i++) TSG_CK(cudaEventCreate(&c->ev[i]));
@@ -576,6 +578,23 @@ int tsg_put_small(tsg_ctx *c, const int64_t *src, int n, int slot) {
     return TSG_OK;
 }
 
+int tsg_wait_mapped(tsg_ctx *c, int slot, int64_t seq) {
+    volatile int64_t *w = c->h_small + slot;
+    for (unsigned spin = 1;; ++spin) {
+        if (*w == seq) break;
+        if ((spin & 4095u) == 0) {
+            const cudaError_t q = cudaStreamQuery(c->stream);
+            if (q == cudaErrorNotReady) continue;
+            if (*w == seq) break;
+            TSG_CK(q);
+            tsg_set_error("mapped result word %d never arrived (expected %lld)", slot, (long long)seq);
+            return TSG_ECUDA;
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return TSG_OK;
+}
+
 int tsg_pending_errors(tsg_ctx *c) {
     const int *h = reinterpret_cast<const int *>(c->h_small + 62);
     if (h[0] == KERR_NONE) return TSG_OK;
@@ -617,7 +636,7 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
 
 // ------------------------------------------------------------------ scan
 // Exclusive scans of non-negative counts (row lengths, set counts), result
-// total in out[n].  Up to SMALL_SCAN elements: one 1024-thread block.  Above:
+// total in out[n].  Up to SMALL_SCAN elements: one 256-thread block.  Above:
 // ONE single-pass launch with decoupled look-back -- tiles take their index
 // from an atomic counter (so a tile only ever waits on tiles that are already
 // running), publish their aggregate, and warp 0 walks back over a 32-tile
@@ -627,7 +646,7 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
 
 namespace {
 constexpr int LB_BS = 256;
-constexpr int LB_IT = 16;
+constexpr int LB_IT = 4;   // elements per thread: 1024-element tiles, many CTAs in flight
 constexpr int LB_TILE = LB_BS * LB_IT;
 
 __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long *p) {
@@ -638,6 +657,49 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long
 
 __device__ __forceinline__ void st_relaxed_gpu(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// LB_IT consecutive inputs of one thread: 16-byte vector loads when the
+// tile is full and aligned (a warp then reads one contiguous span)
+template <typename TI>
+__device__ __forceinline__ void load_run(const TI *__restrict__ in, int64_t n, int64_t base, bool vec,
+                                         int64_t (&v)[LB_IT]) {
+    if (vec) {
+        if constexpr (sizeof(TI) == 8) {
+            const longlong2 *p = reinterpret_cast<const longlong2 *>(in + base);
+#pragma unroll
+            for (int k = 0; k < LB_IT / 2; k++) {
+                const longlong2 q = __ldg(p + k);
+                v[2 * k] = q.x;
+                v[2 * k + 1] = q.y;
+            }
+        } else {
+            const int4 q = __ldg(reinterpret_cast<const int4 *>(in + base));
+            v[0] = q.x;
+            v[1] = q.y;
+            v[2] = q.z;
+            v[3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < LB_IT; k++) v[k] = base + k < n ? (int64_t)in[base + k] : 0;
+    }
+}
+
+__device__ __forceinline__ void store_run(int64_t *__restrict__ out, int64_t n, int64_t base, bool vec,
+                                          int64_t run, const int64_t (&v)[LB_IT]) {
+    if (vec) {
+        longlong2 *p = reinterpret_cast<longlong2 *>(out + base);
+        const int64_t r1 = run + v[0], r2 = r1 + v[1], r3 = r2 + v[2];
+        p[0] = make_longlong2(run, r1);
+        p[1] = make_longlong2(r2, r3);
+    } else {
+#pragma unroll
+        for (int k = 0; k < LB_IT; k++) {
+            if (base + k < n) out[base + k] = run;
+            run += v[k];
+        }
+    }
 }
 
 template <typename TI>
@@ -652,13 +714,13 @@ __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in
     const unsigned tile = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t base = (int64_t)tile * LB_TILE + (int64_t)threadIdx.x * LB_IT;
+    const bool vec = (int64_t)(tile + 1) * LB_TILE <= n &&
+                     ((((uintptr_t)in) | ((uintptr_t)out)) & 15) == 0;   // block-uniform
     int64_t v[LB_IT];
+    load_run<TI>(in, n, base, vec, v);
     int64_t s = 0;
 #pragma unroll
-    for (int k = 0; k < LB_IT; k++) {
-        v[k] = base + k < n ? (int64_t)in[base + k] : 0;
-        s += v[k];
-    }
+    for (int k = 0; k < LB_IT; k++) s += v[k];
     int64_t x = s;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -706,56 +768,41 @@ __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in
         }
     }
     __syncthreads();
-    int64_t run = s_excl + woff + x - s;
-#pragma unroll
-    for (int k = 0; k < LB_IT; k++) {
-        if (base + k < n) out[base + k] = run;
-        run += v[k];
-    }
+    store_run(out, n, base, vec, s_excl + woff + x - s, v);
     if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_excl + agg;
 }
 
-// Inputs up to SMALL_SCAN elements: one 1024-thread block, one launch.
-constexpr int64_t SMALL_SCAN = 1024 * 16;
+// Inputs up to SMALL_SCAN elements: one block, one launch, no look-back state.
+constexpr int64_t SMALL_SCAN = LB_TILE;
 
 template <typename TI>
-__global__ void __launch_bounds__(1024) scan_one_block(const TI *__restrict__ in, int64_t n,
-                                                       int64_t *__restrict__ out) {
-    __shared__ int64_t ws[32];
-    constexpr int IT = 16;
+__global__ void __launch_bounds__(LB_BS) scan_one_block(const TI *__restrict__ in, int64_t n,
+                                                        int64_t *__restrict__ out) {
+    __shared__ int64_t ws[LB_BS / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t base = (int64_t)threadIdx.x * IT;
-    int64_t v[IT];
+    const int64_t base = (int64_t)threadIdx.x * LB_IT;
+    int64_t v[LB_IT];
+    load_run<TI>(in, n, base, false, v);
     int64_t s = 0;
 #pragma unroll
-    for (int k = 0; k < IT; k++) {
-        v[k] = base + k < n ? (int64_t)in[base + k] : 0;
-        s += v[k];
-    }
+    for (int k = 0; k < LB_IT; k++) s += v[k];
     int64_t x = s;
+#pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         int64_t o = __shfl_up_sync(0xffffffffu, x, d);
         if (lane >= d) x += o;
     }
     if (lane == 31) ws[w] = x;
     __syncthreads();
-    if (w == 0) {
-        int64_t y = ws[lane];
-        for (int d = 1; d < 32; d <<= 1) {
-            int64_t o = __shfl_up_sync(0xffffffffu, y, d);
-            if (lane >= d) y += o;
-        }
-        ws[lane] = y;
-    }
-    __syncthreads();
-    int64_t run = x - s + (w ? ws[w - 1] : 0);
-    __syncthreads();   // in place: every thread has read its inputs
+    int64_t woff = 0, agg = 0;
 #pragma unroll
-    for (int k = 0; k < IT; k++) {
-        if (base + k < n) out[base + k] = run;
-        run += v[k];
+    for (int j = 0; j < LB_BS / 32; j++) {
+        woff += j < w ? ws[j] : 0;
+        agg += ws[j];
     }
-    if (threadIdx.x == 1023) out[n] = run;
+    __syncthreads();   // in place: every thread has read its inputs
+    store_run(out, n, base, false, woff + x - s, v);
+    if (threadIdx.x == 0) out[n] = agg;
 }
 
 template <typename TI>
@@ -765,7 +812,7 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
         return TSG_OK;
     }
     if (n <= SMALL_SCAN) {
-        scan_one_block<TI><<<1, 1024, 0, c->stream>>>(in, n, out); ++c->launches;
+        scan_one_block<TI><<<1, LB_BS, 0, c->stream>>>(in, n, out); ++c->launches;
         TSG_CK(cudaGetLastError());
         return TSG_OK;
     }

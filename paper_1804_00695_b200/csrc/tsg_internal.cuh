@@ -36,6 +36,7 @@ struct tsg_ctx {
     int *d_err;               // [0] code, [1] row (lowest)
     int64_t *h_small;         // pinned, device-mapped scratch for small reads (64 x int64)
     int64_t *hd_small;        // device alias of h_small: kernels store results there
+    int64_t part_seq;         // last sequence word a partition kernel publishes (h_small[61])
                               // directly, so small reads never queue behind bulk D2H copies
     int64_t *d_small;         // device scratch for reductions (64 x int64)
     int timing;
@@ -174,6 +175,11 @@ int tsg_fill(tsg_ctx *ctx, void *p, int byte, size_t bytes, cudaStream_t s);
 // OTHER streams until it completes; split, the copy keeps its bandwidth and
 // other streams' kernels start within ~0.3 ms.
 int tsg_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s);
+// wait until a kernel on c->stream has stored `seq` into h_small[slot]
+// (stores before it made visible with __threadfence_system).  Polls the
+// mapped word; checks the stream every few thousand polls so a failed kernel
+// returns its error instead of spinning.
+int tsg_wait_mapped(tsg_ctx *ctx, int slot, int64_t seq);
 // after a stream sync that also copied d_err into h_small[62]: report a
 // pending (deferred) kernel error, if any
 int tsg_pending_errors(tsg_ctx *ctx);

@@ -1,13 +1,16 @@
 // tsg_partition.cuh -- row partition by tier ("bin"), shared by the symbolic,
 // numeric, fused and masked-count phases.
 //
-// Three launches and one D2H copy + stream sync per partition:
+// Three launches and one host wait per partition:
 //   k_part_bins     the phase's bin functor per row (it may also write
 //                   per-row side outputs), warp-aggregated tile histogram
 //   scan            exclusive scan of the NB x ntiles tile counts
 //   k_part_scatter  row ids into per-bin lists (tile order kept, order inside
 //                   a tile not), block 0 also gathers the bin starts and one
-//                   optional extra device value (e.g. nnz(C)) for the D2H
+//                   optional extra device value (e.g. nnz(C)) into mapped
+//                   host memory as soon as it starts, then a sequence word;
+//                   the host polls that word instead of synchronising the
+//                   stream, so the next launches overlap the scatter
 // Rows are ranked with __match_any_sync peers so a block does one shared
 // atomic per distinct bin per warp, not one per row (a single dominant bin
 // otherwise serialises 1024 atomics on one address).
@@ -51,9 +54,20 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
                                                       int32_t *__restrict__ list,
                                                       const int64_t *__restrict__ extra,
                                                       const int *__restrict__ err,
-                                                      int64_t *__restrict__ out) {
+                                                      int64_t *__restrict__ out, int64_t seq) {
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
+    if (blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
+        if (threadIdx.x <= NB) out[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
+        if (threadIdx.x == NB + 1) out[NB + 1] = extra ? *extra : 0;
+        // pending kernel errors of earlier work ride along (h_small[62])
+        if (threadIdx.x == NB + 2) out[30] = *reinterpret_cast<const int64_t *>(err);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            *reinterpret_cast<volatile int64_t *>(out + 29) = seq;   // h_small[61]
+        }
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -69,12 +83,6 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
         r0 = __shfl_sync(0xffffffffu, r0, leader);
         if (b < NB) list[offs[(int64_t)b * ntiles + blockIdx.x] + r0 + __popc(peers & lt)] = (int32_t)i;
     }
-    if (blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
-        if (threadIdx.x <= NB) out[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
-        if (threadIdx.x == NB + 1) out[NB + 1] = extra ? *extra : 0;
-        // pending kernel errors of earlier work ride along (h_small[62])
-        if (threadIdx.x == NB + 2) out[30] = *reinterpret_cast<const int64_t *>(err);
-    }
 }
 
 // Partition rows [0, rows) by f(i) (values >= NB: row skipped).  `bins` is
@@ -89,7 +97,7 @@ struct NoMid {
 template <int NB, class F, class Mid = NoMid>
 int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid()) {
-    static_assert(32 + NB + 2 <= 62, "partition results overlap the error slot");
+    static_assert(32 + NB + 2 <= 61, "partition results overlap the sequence / error slots");
     int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
     if (ntiles < 1) ntiles = 1;
     int *tc = nullptr;
@@ -103,11 +111,11 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     // results land in mapped host memory straight from the kernel: no D2H
     // copy that would queue behind bulk transfers on the copy engine
     k_part_scatter<NB><<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list, extra,
-                                                      c->d_err, c->hd_small + 32); ++c->launches;
+                                                      c->d_err, c->hd_small + 32, ++c->part_seq); ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));
-    TSG_CK(cudaStreamSynchronize(c->stream));
+    TSG_TRY(tsg_wait_mapped(c, 61, c->part_seq));
     TSG_TRY(tsg_pending_errors(c));
     for (int b = 0; b <= NB; b++) out.off[b] = c->h_small[32 + b];
     if (extra_out) *extra_out = c->h_small[32 + NB + 1];

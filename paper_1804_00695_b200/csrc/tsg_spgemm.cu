@@ -885,6 +885,82 @@ __device__ __forceinline__ void products_unit(unsigned gm, int glane, const NumA
     }
 }
 
+// Product phase for unit B rows when the host knows B is unit (uploaded or
+// generated operands): the window of UB*G A entries first stages each
+// product's output position and value in shared memory, then every lane
+// folds, in storage order, the products whose position it owns (pos = glane
+// mod G).  Same sequence of `payload += value` per position as ordered_add,
+// without match / vote / shuffle rounds per chunk.
+constexpr int UWIN_B = 12;   // staged bytes per product (int pos + double value)
+
+template <int G>
+__device__ __forceinline__ void products_unit_owned(unsigned gm, int glane, const NumArgs &a, int64_t a0,
+                                                    int64_t a1, const int4 *tbl, int T, int logT,
+                                                    double *vals, int *spos, double *sprod) {
+    constexpr int W = UB * G;
+    for (int64_t base = a0; base < a1; base += W) {
+        int kk[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int64_t t = base + u * G + glane;
+            kk[u] = t < a1 ? a.acol[t] : -1;
+        }
+        int64_t ss[UB];
+        bool has[UB];
+        if (a.unit_dense) {
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int k = kk[u];
+                has[u] = k >= a.b_lo && k < a.b_hi;
+                ss[u] = has[u] ? k - a.b_lo : 0;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int k = kk[u];
+                const bool in = k >= a.b_lo && k < a.b_hi;
+                ss[u] = in ? a.brp[k - a.b_lo] : 0;
+                has[u] = in && a.brp[k - a.b_lo + 1] > ss[u];
+            }
+        }
+        int cc[UB];
+        double pp[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int64_t t = base + u * G + glane;
+            cc[u] = has[u] ? a.bcol[ss[u]] : 0;
+            pp[u] = has[u] ? __dmul_rn(a.aval[t], a.bval[ss[u]]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            int pos = -1;
+            if (has[u]) {
+                int4 e;
+                tbl_find(tbl, T, logT, cc[u] >> 6, e);
+                pos = e.w + mask_rank(e, cc[u] & 63);
+            }
+            spos[u * G + glane] = pos;
+            sprod[u * G + glane] = pp[u];
+        }
+        __syncwarp(gm);
+        const int w = (int)((a1 - base) < W ? (a1 - base) : W);
+        const int4 *sp4 = reinterpret_cast<const int4 *>(spos);
+        for (int q = 0; q < ((w + 3) >> 2); ++q) {
+            const int4 p4 = sp4[q];
+            // owner test: non-negative and pos = glane (mod G)
+            if (((p4.x ^ glane) & (int)(0x80000000u | (G - 1))) == 0)
+                vals[p4.x] = __dadd_rn(vals[p4.x], sprod[4 * q]);
+            if (((p4.y ^ glane) & (int)(0x80000000u | (G - 1))) == 0)
+                vals[p4.y] = __dadd_rn(vals[p4.y], sprod[4 * q + 1]);
+            if (((p4.z ^ glane) & (int)(0x80000000u | (G - 1))) == 0)
+                vals[p4.z] = __dadd_rn(vals[p4.z], sprod[4 * q + 2]);
+            if (((p4.w ^ glane) & (int)(0x80000000u | (G - 1))) == 0)
+                vals[p4.w] = __dadd_rn(vals[p4.w], sprod[4 * q + 3]);
+        }
+        __syncwarp(gm);
+    }
+}
+
 struct NumRowHdr {
     int64_t i = 0, cp = 0, a0 = 0, a1 = 0, sp = 0, sb = 0;
     int n = 0, mflag = 0;
@@ -906,7 +982,15 @@ __device__ __forceinline__ NumRowHdr num_row_hdr(const NumArgs &a, int64_t i) {
 
 constexpr int NUM_SKEW = 64;
 
-template <int G, int SLICE, bool SEQ>
+// bytes of the per-group value slices of a k_num_group block (with skew)
+template <int G, int SLICE>
+__host__ __device__ constexpr size_t num_slices_bytes(int gpb) {
+    return (size_t)gpb * SLICE + (G == 8 ? (size_t)(gpb / 2) * NUM_SKEW : 0);
+}
+
+// MODE 0: generic / unit B known on the device; 1: lane-split B rows (SEQ);
+// 2: unit B known on the host (products_unit_owned, staging after the slices)
+template <int G, int SLICE, int MODE>
 __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
     extern __shared__ int4 smem[];
@@ -1075,8 +1159,13 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
             vals[e.w + mask_rank(e, c & 63)] = a.pval[q];
         }
         __syncwarp(gm);
-        if constexpr (SEQ) {
+        if constexpr (MODE == 1) {
             products_seq<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
+        } else if constexpr (MODE == 2) {
+            char *stage = reinterpret_cast<char *>(smem) + num_slices_bytes<G, SLICE>(gpb) +
+                          (size_t)(threadIdx.x / G) * (UB * G * UWIN_B);
+            products_unit_owned<G>(gm, glane, a, a0, a1, tbl, T, logT, vals, reinterpret_cast<int *>(stage),
+                                   reinterpret_cast<double *>(stage + UB * G * 4));
         } else if (a.unit_known > 0 || (a.unit_known < 0 && *a.unit_b)) {
             products_unit<G>(gm, glane, a, a0, a1, tbl, T, logT, vals);
         } else {
@@ -1440,14 +1529,14 @@ int launch_sym_group(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     return TSG_OK;
 }
 
-template <int B, bool SEQ>
+template <int B, int MODE>
 int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
-    size_t smem = (size_t)(BS / G) * SL + (G == 8 ? (size_t)(BS / G / 2) * NUM_SKEW : 0);
-    TSG_TRY(set_smem(k_num_group<G, SL, SEQ>, smem));
+    size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * UB * G * UWIN_B : 0);
+    TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
     unsigned grid = group_grid(c, n, BS / G);
-    k_num_group<G, SL, SEQ><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    k_num_group<G, SL, MODE><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_num_group", B, grid, BS, smem));
     return TSG_OK;
 }
@@ -1456,8 +1545,9 @@ template <int B>
 int launch_num_group(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     if (bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
     // lane-per-B-entry mode pays off once B rows fill at least half a group
-    if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, true>(c, bl, a);
-    return launch_num_group_m<B, false>(c, bl, a);
+    if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, 1>(c, bl, a);
+    if (a.unit_known > 0) return launch_num_group_m<B, 2>(c, bl, a);
+    return launch_num_group_m<B, 0>(c, bl, a);
 }
 
 template <int CB>

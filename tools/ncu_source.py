@@ -2,7 +2,7 @@
 usage: python tools_ncu_source.py REPORT LAUNCH_INDEX [TOP]"""
 import csv, os, subprocess, sys
 
-SRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), 'paper_1804_00695_b200', 'csrc')
+SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 'paper_1804_00695_b200', 'csrc')
 
 
 def num(x):
