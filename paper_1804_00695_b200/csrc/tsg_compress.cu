@@ -88,7 +88,7 @@ __device__ __forceinline__ void word_from_smem(const int4 *__restrict__ sm, int 
 // that open a run in the same iteration ranks exactly 32 apart (a 27-point
 // stencil row has 9 runs of 3 -> a head every third entry, ranks 32k + c),
 // which unpadded would put all of them on one bank.
-constexpr int EMIT_CAP = 4096;   // staged runs per block (~50 KB); more -> direct stores
+constexpr int EMIT_CAP = 3584;   // staged runs per block (~50 KB); more -> direct stores
 constexpr int EMIT_PAD = EMIT_CAP + EMIT_CAP / 32;
 constexpr size_t EMIT_SMEM = (size_t)EMIT_PAD * 12 > (size_t)PB * 4 ? (size_t)EMIT_PAD * 12 : (size_t)PB * 4;
 
@@ -96,7 +96,7 @@ constexpr size_t EMIT_SMEM = (size_t)EMIT_PAD * 12 > (size_t)PB * 4 ? (size_t)EM
 // starts a row or its set differs from entry q-1's (pv = set of the entry
 // before the word, -1 at the matrix start).  A set that goes DOWN inside a
 // row marks the matrix unsorted.  FULL: all 32 entries valid.
-template <bool FULL>
+template <bool FULL, bool CHECK>
 __device__ __forceinline__ uint32_t word_heads(const int (&c)[32], uint32_t rs, int pv, int64_t left,
                                                bool &bad) {
     uint32_t hw = 0;
@@ -108,7 +108,7 @@ __device__ __forceinline__ uint32_t word_heads(const int (&c)[32], uint32_t rs, 
         const bool start = (rs >> q) & 1u;
         if (valid) {
             hw |= (uint32_t)(start || sv != pv) << q;
-            b |= !start && sv < pv;
+            if (CHECK) b |= !start && sv < pv;
         }
         pv = sv;
     }
@@ -164,7 +164,9 @@ __device__ __forceinline__ void lb_st(unsigned long long *p, unsigned long long 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(CT) k_compress_onepass(
+// CHECK: also flag rows whose sets go down (input not known to be row-sorted)
+template <bool CHECK>
+__global__ void __launch_bounds__(CT, 5) k_compress_onepass(
     int64_t nnz, const int32_t *__restrict__ col, const uint32_t *__restrict__ rsbits,
     uint32_t *__restrict__ hbits, uint16_t *__restrict__ wpre, int64_t *__restrict__ boff,
     int64_t nblocks, unsigned long long *state, unsigned *counter, int32_t *__restrict__ oset,
@@ -197,13 +199,13 @@ __global__ void __launch_bounds__(CT) k_compress_onepass(
     uint32_t hw = 0;
     bool bad = false;
     if (t0 + 32 <= nnz) {
-        hw = word_heads<true>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
+        hw = word_heads<true, CHECK>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
         hbits[word] = hw;
     } else if (t0 < nnz) {
-        hw = word_heads<false>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
+        hw = word_heads<false, CHECK>(c, rsbits[word], t0 == 0 ? -1 : prev, nnz - t0, bad);
         hbits[word] = hw;
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
+    if (CHECK && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1);
     const int n = __popc(hw);
     int x = n;
 #pragma unroll
@@ -449,8 +451,9 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
     TSG_TRY(tsg_fill(c, lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
     const size_t esmem = EMIT_SMEM;
-    TSG_TRY(tsg_func_smem((const void *)k_compress_onepass, esmem));
-    k_compress_onepass<<<(unsigned)nblocks, CT, esmem, s>>>(
+    auto kern = b->sorted ? k_compress_onepass<false> : k_compress_onepass<true>;
+    TSG_TRY(tsg_func_smem((const void *)kern, esmem));
+    kern<<<(unsigned)nblocks, CT, esmem, s>>>(
         nnz, b->col, rsbits, hbits, wpre, bcnt, nblocks, lbstate,
         reinterpret_cast<unsigned *>(lbstate + nblocks), cm->set, cm->bits, unsorted); ++c->launches;
     k_set_starts<<<rgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
