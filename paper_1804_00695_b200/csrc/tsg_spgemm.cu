@@ -544,26 +544,19 @@ __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ l
         const int64_t sp = a.sptr[i];
         int m = 0, total = 0;
         for (;;) {
-            // one butterfly carries (head, mask): the smaller head wins, equal
-            // heads OR their masks -> every lane ends with (min, OR of its holders)
+            // group minimum head (min butterfly), then the OR of the masks of
+            // the lanes holding it (OR butterfly): no compare-select chains
             int mn = hs;
-            unsigned lo = (unsigned)hb, hi = (unsigned)(hb >> 32);
 #pragma unroll
-            for (int d = G / 2; d >= 1; d >>= 1) {
-                const int ok = __shfl_xor_sync(gm, mn, d, G);
-                const unsigned olo = __shfl_xor_sync(gm, lo, d, G);
-                const unsigned ohi = __shfl_xor_sync(gm, hi, d, G);
-                if (ok < mn) {
-                    mn = ok;
-                    lo = olo;
-                    hi = ohi;
-                } else if (ok == mn) {
-                    lo |= olo;
-                    hi |= ohi;
-                }
-            }
+            for (int d = G / 2; d >= 1; d >>= 1) mn = min(mn, __shfl_xor_sync(gm, mn, d, G));
             if (mn == INT32_MAX) break;
             const bool mine = hs == mn;
+            unsigned lo = mine ? (unsigned)hb : 0u, hi = mine ? (unsigned)(hb >> 32) : 0u;
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) {
+                lo |= __shfl_xor_sync(gm, lo, d, G);
+                hi |= __shfl_xor_sync(gm, hi, d, G);
+            }
             if (glane == 0) {
                 a.oset[sp + m] = mn;
                 a.obits[sp + m] = ((uint64_t)hi << 32) | lo;
@@ -656,9 +649,14 @@ __global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ li
 }
 
 // Thread tier, symbolic: one thread per row of A whose B rows are single
-// entries (compressed row k = set k).  The row's sets are kept sorted in a
-// per-thread local array (appends and hits on the last set are the common
-// case for sorted A rows; otherwise binary search + shift).
+// entries (compressed row k = set k).  The row's sets are kept sorted: the
+// largest set so far lives in registers (appends and hits on it are the
+// common case for sorted A rows), the finished ones in a per-thread array
+// (binary search + shift for an out-of-order set).  A entries are taken
+// TSYM_BATCH at a time with all their loads issued together, so a row costs
+// two dependent load rounds per batch instead of two per entry.
+constexpr int TSYM_BATCH = 8;
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sym_thread(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
@@ -668,37 +666,62 @@ __global__ void __launch_bounds__(NT) k_sym_thread(const int32_t *__restrict__ l
         const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
         int key[THREAD_MAX_A];
         uint64_t msk[THREAD_MAX_A];
-        int m = 0;
-        for (int64_t t = a0; t < a1; ++t) {
-            int k = a.acol[t];
-            if (k < a.b_lo || k >= a.b_hi) continue;
-            k -= a.b_lo;
-            const int sset = a.cbset[k];
-            const uint64_t bits = a.cbbits[k];
-            if (m > 0 && key[m - 1] == sset) {
-                msk[m - 1] |= bits;
-            } else if (m == 0 || key[m - 1] < sset) {
-                key[m] = sset;
-                msk[m] = bits;
-                ++m;
-            } else {
-                int lo = 0, hi = m - 1;   // first key >= sset
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (key[mid] < sset) lo = mid + 1; else hi = mid;
-                }
-                if (key[lo] == sset) {
-                    msk[lo] |= bits;
-                } else {
-                    for (int q = m; q > lo; --q) {
-                        key[q] = key[q - 1];
-                        msk[q] = msk[q - 1];
+        int m = 0;             // finished sets in key/msk (all below lastk)
+        int lastk = -1;        // largest set so far (-1: none)
+        uint64_t lastm = 0;
+        for (int64_t t0 = a0; t0 < a1; t0 += TSYM_BATCH) {
+            int kk[TSYM_BATCH];
+#pragma unroll
+            for (int u = 0; u < TSYM_BATCH; ++u) {
+                int k = t0 + u < a1 ? a.acol[t0 + u] : -1;
+                kk[u] = (k >= a.b_lo && k < a.b_hi) ? k - a.b_lo : -1;
+            }
+            int sv[TSYM_BATCH];
+            uint64_t bv[TSYM_BATCH];
+#pragma unroll
+            for (int u = 0; u < TSYM_BATCH; ++u) {
+                sv[u] = kk[u] >= 0 ? a.cbset[kk[u]] : -1;
+                bv[u] = kk[u] >= 0 ? a.cbbits[kk[u]] : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < TSYM_BATCH; ++u) {
+                const int sset = sv[u];
+                if (sset < 0) continue;
+                const uint64_t bits = bv[u];
+                if (sset == lastk) {
+                    lastm |= bits;
+                } else if (sset > lastk) {
+                    if (lastk >= 0) {
+                        key[m] = lastk;
+                        msk[m] = lastm;
+                        ++m;
                     }
-                    key[lo] = sset;
-                    msk[lo] = bits;
-                    ++m;
+                    lastk = sset;
+                    lastm = bits;
+                } else {
+                    int lo = 0, hi = m;   // first finished key >= sset (m: none)
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (key[mid] < sset) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo < m && key[lo] == sset) {
+                        msk[lo] |= bits;
+                    } else {
+                        for (int q = m; q > lo; --q) {
+                            key[q] = key[q - 1];
+                            msk[q] = msk[q - 1];
+                        }
+                        key[lo] = sset;
+                        msk[lo] = bits;
+                        ++m;
+                    }
                 }
             }
+        }
+        if (lastk >= 0) {
+            key[m] = lastk;
+            msk[m] = lastm;
+            ++m;
         }
         const int64_t sp = a.sptr[i];
         int cnt = 0;
