@@ -158,6 +158,7 @@ __global__ void k_max_i32(int64_t n, const int32_t *__restrict__ v, int *out) {
 // for aggregation operators, within ~10 % for stencils); skewed B falls back
 // to the exact sum of the selected compressed rows.
 constexpr int CHEAP_CB = 16;
+constexpr int INLINE_BOUND_A = 16;   // A rows up to this long: exact bound in the bin functor
 
 template <int G>
 __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
@@ -265,6 +266,8 @@ struct SymBinF {
     const int64_t *carp;  // non-null: cheap bound len(A_i) x max when *cmax <= CHEAP_CB
     const int *cmax;
     const int64_t *tarp;  // non-null: thread tier allowed (B rows are exactly one entry each)
+    const int32_t *ecol;  // non-null (with carp): short A rows, exact bound summed here
+    const int32_t *ecnt;  //   over ecnt[ecol[t]] instead of by k_sym_bounds
     __device__ __forceinline__ int operator()(int64_t i) const {
         if (tarp) {
             const int64_t alen = tarp[i + a_row_off + 1] - tarp[i + a_row_off];
@@ -277,6 +280,10 @@ struct SymBinF {
         int64_t sb;
         if (carp && *cmax <= CHEAP_CB) {
             sb = (carp[i + 1] - carp[i]) * (int64_t)*cmax;
+            sbound[i] = sb;
+        } else if (carp && ecol) {
+            sb = 0;
+            for (int64_t t = carp[i]; t < carp[i + 1]; ++t) sb += ecnt[ecol[t]];
             sbound[i] = sb;
         } else {
             sb = sbound[i];
@@ -1862,16 +1869,20 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
             k_max_i32<<<grid_for(cb->rows, 256, c->num_sms * 4), 256, 0, c->stream>>>(cb->rows, cb->cnt,
                                                                                     maxcb); ++c->launches;
         }
+        // short A rows (known at upload): the bin functor sums the exact bound
+        const bool inline_bounds = a->max_row >= 0 && a->max_row <= INLINE_BOUND_A;
         if (a_row_off == 0 && b_lo == 0 && b_hi == 0x7fffffff && partial == nullptr &&
             rows_out == a->rows) {
             const unsigned g = grid_for(a->rows, 256, c->num_sms * 16);
-            switch (pick_g(a->nnz, a->rows)) {
-            case 4: k_sym_bounds<4><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-            case 8: k_sym_bounds<8><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-            case 16: k_sym_bounds<16><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-            default: k_sym_bounds<32><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+            if (!inline_bounds) {
+                switch (pick_g(a->nnz, a->rows)) {
+                case 4: k_sym_bounds<4><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+                case 8: k_sym_bounds<8><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+                case 16: k_sym_bounds<16><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+                default: k_sym_bounds<32><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+                }
+                ++c->launches;
             }
-            ++c->launches;
         } else {
             TSG_TRY(tsg_fused_bounds(c, rows_out, a, a_row_off, b_lo, b_hi, cb->start, cb->cnt,
                                      partial ? partial->rp : nullptr, sbound));
@@ -1890,7 +1901,8 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         TSG_TRY(tsg_partition<NBINS>(c, rows_out, SymBinF{sbound, v->d, v->aux, scap, merge_arp, a_row_off,
                                              partial == nullptr ? cb_cols : 0,
                                              plain ? a->rp : nullptr, maxcb,
-                                             (plain && cb->identity_rows) ? a->rp : nullptr},
+                                             (plain && cb->identity_rows) ? a->rp : nullptr,
+                                             (plain && inline_bounds) ? a->col : nullptr, cb->cnt},
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
