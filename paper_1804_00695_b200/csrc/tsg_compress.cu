@@ -301,14 +301,23 @@ __global__ void k_set_starts(int64_t rows, int64_t nnz, const int64_t *__restric
         if (e >= nnz) return boff[nblocks];
         return boff[e / PB] + wpre[e >> 5] + __popc(hbits[e >> 5] & ((1u << (e & 31)) - 1u));
     };   // PB entries per block, wpre block-relative
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t s0 = rank_at(rp[i]);
-        start[i] = s0;
-        if (i < rows) {
-            const int32_t n = (int32_t)(rank_at(rp[i + 1]) - s0);
-            cnt[i] = n;
-            mx = n > mx ? n : mx;
+    // row i's end rank is row i+1's start rank: taken from the next lane
+    // (lane 31 computes its own), so each rank is gathered once
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t lim = (rows + 1 + 31) / 32 * 32;   // whole warps stay in the loop
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
+        const bool live = i <= rows;
+        const int64_t s0 = live ? rank_at(rp[i]) : 0;
+        int64_t s1 = __shfl_down_sync(0xffffffffu, s0, 1);
+        if (live) {
+            start[i] = s0;
+            if (i < rows) {
+                if (lane == 31) s1 = rank_at(rp[i + 1]);
+                const int32_t n = (int32_t)(s1 - s0);
+                cnt[i] = n;
+                mx = n > mx ? n : mx;
+            }
         }
     }
 #pragma unroll
