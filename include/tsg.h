@@ -181,6 +181,26 @@ int tsg_gather_sharded(tsg_ctx *ctx, int n_shards, const int64_t *row_lo, const 
    generators.with_unit_values on the device */
 int tsg_csr_set_values(tsg_ctx *ctx, tsg_csr *m, double value);
 
+/* ---- input builders on the device -------------------
+   Same arrays as the host builders: generators.stencil / stencil_rows
+   (reference generators.py:98-142, flat index first axis fastest, columns
+   ascending, centre weight = number of neighbours, elasticity3d = 3x3 blocks
+   w * (I + 0.5)), generators.aggregation (P: fine point -> aggregate, 1.0;
+   R = P^T, generators.py:204-230 restated for plain aggregation) and
+   csr.transpose (csr.py:134-142: stable by column, rows ascending). */
+#define TSG_STENCIL_LAPLACE2D 0
+#define TSG_STENCIL_LAPLACE3D 1
+#define TSG_STENCIL_BIGSTAR2D 2
+#define TSG_STENCIL_BRICK3D 3
+#define TSG_STENCIL_ELASTICITY3D 4
+/* rows [row_lo, row_hi) of the operator (row_lo < 0: all rows; elasticity3d:
+   all rows only); columns span the whole grid */
+int tsg_stencil(tsg_ctx *ctx, int kind, const int64_t *dims, int ndims, int64_t row_lo, int64_t row_hi,
+                tsg_csr **out);
+int tsg_aggregation(tsg_ctx *ctx, const int64_t *dims, int ndims, int factor, tsg_csr **p_out,
+                    tsg_csr **r_out);
+int tsg_transpose(tsg_ctx *ctx, const tsg_csr *a, tsg_csr **out);
+
 /* ---- data placement (memory.py:193-223 PlacementPolicy; PAPER.md:600-625,
    810-829).  A CSR whose arrays live in pinned, device-mapped HOST memory:
    kernels read it in place over PCIe (the paper's "pinned" columns).  Columns

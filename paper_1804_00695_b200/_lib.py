@@ -15,7 +15,7 @@ import weakref
 import numpy as np
 
 from .csr import CsrMatrix
-from .errors import (CapacityError, DimensionError, KernelError,
+from .errors import (CapacityError, DimensionError, GridError, KernelError,
                      MatrixValidationError, UnsplittableRowError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -45,7 +45,7 @@ EXPORTS = (
     "tsg_csr_from_device", "tsg_csr_device_ptrs", "tsg_host_alloc", "tsg_host_free",
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
-    "tsg_csr_set_values", "tsg_gather_sharded",
+    "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
 )
 
 _P = ctypes.c_void_p
@@ -88,6 +88,9 @@ _SIGS = {
     "tsg_graph_lower": ([_P, _P, ctypes.c_int, _PP, _P], ctypes.c_int),
     "tsg_numeric_calls": ([_P, _PI64], ctypes.c_int),
     "tsg_csr_set_values": ([_P, _P, ctypes.c_double], ctypes.c_int),
+    "tsg_stencil": ([_P, ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _PP], ctypes.c_int),
+    "tsg_aggregation": ([_P, _P, ctypes.c_int, ctypes.c_int, _PP, _PP], ctypes.c_int),
+    "tsg_transpose": ([_P, _P, _PP], ctypes.c_int),
     "tsg_gather_sharded": ([_P, ctypes.c_int, _P, _P, _P, _P, _I64, _P, _PP], ctypes.c_int),
     "tsg_numeric_ms": ([_P, _I64, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
@@ -454,6 +457,34 @@ def d_rmat_graph(scale: int, edge_factor: int, seed: int, a: float, b: float, c:
     check_(load().tsg_rmat_graph(ctx.h, int(scale), int(edge_factor), int(seed) & ((1 << 64) - 1),
                                  float(a), float(b), float(c), ctypes.byref(h)))
     return DeviceCsr(ctx, h)
+
+
+STENCIL_CODES = {"laplace2d": 0, "laplace3d": 1, "bigstar2d": 2, "brick3d": 3, "elasticity3d": 4}
+
+
+def d_stencil(kind: str, dims, row_lo: int = -1, row_hi: int = -1, ctx=None) -> DeviceCsr:
+    ctx = ctx or Context.get()
+    if kind not in STENCIL_CODES:
+        raise GridError("unknown stencil kind %r" % (kind,))
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    h = ctypes.c_void_p()
+    check_(load().tsg_stencil(ctx.h, STENCIL_CODES[kind], _ptr(d), int(d.size), int(row_lo), int(row_hi),
+                              ctypes.byref(h)))
+    return DeviceCsr(ctx, h)
+
+
+def d_aggregation(dims, factor: int = 2, ctx=None):
+    ctx = ctx or Context.get()
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    hp, hr = ctypes.c_void_p(), ctypes.c_void_p()
+    check_(load().tsg_aggregation(ctx.h, _ptr(d), int(d.size), int(factor), ctypes.byref(hp), ctypes.byref(hr)))
+    return DeviceCsr(ctx, hp), DeviceCsr(ctx, hr)
+
+
+def d_transpose(da) -> DeviceCsr:
+    h = ctypes.c_void_p()
+    check_(load().tsg_transpose(da.ctx.h, da.h, ctypes.byref(h)))
+    return DeviceCsr(da.ctx, h)
 
 
 def d_gather_sharded(da, shards, b_cols: int) -> DeviceCsr:

@@ -108,6 +108,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_TRY(tsg_preload_module_of(tsg_kernel_masked()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_chunk()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_graph()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_build()));
     *out = c;
     return TSG_OK;
 }

@@ -96,7 +96,7 @@ def local_shard_tensors(b, lo: int, hi: int, device):
     e0, e1 = int(rp[0]), int(rp[-1])
     t_rp = torch.from_numpy(rp - e0).to(device)
     t_col = torch.from_numpy(np.asarray(b.col_idx[e0:e1], dtype=np.int32)).to(device)
-    t_val = None if b.values is None else torch.from_numpy(np.asarray(b.values[e0:e1])).to(device)
+    t_val = None if b.values is None else torch.from_numpy(np.array(b.values[e0:e1])).to(device)
     return t_rp, t_col, t_val
 
 

@@ -198,6 +198,29 @@ def rmat_graph_device(scale: int, edge_factor: int = 16, seed: int = 22,
     return _lib.d_rmat_graph(scale, edge_factor, seed, a, b, c)
 
 
+def stencil_device(kind: str, dims, lo: int = None, hi: int = None):
+    """``stencil`` (or ``stencil_rows`` for a row range) built in HBM
+    (csrc/tsg_build.cu): the same rows, columns and values as the host
+    builder, as a DeviceCsr."""
+    from . import _lib
+    dims = _check_dims(kind, dims)
+    if kind not in STENCIL_KINDS:
+        raise GridError("unknown stencil kind %r" % (kind,))
+    if lo is None:
+        return _lib.d_stencil(kind, dims)
+    return _lib.d_stencil(kind, dims, int(lo), int(hi))
+
+
+def aggregation_device(dims, factor: int = 2):
+    """``aggregation`` built in HBM: (P, R) as DeviceCsr, R = P^T assembled
+    directly (each aggregate lists its fine points in ascending order)."""
+    from . import _lib
+    dims = tuple(int(d) for d in dims)
+    if any(d <= 0 for d in dims):
+        raise GridError("grid dims must be positive")
+    return _lib.d_aggregation(dims, factor)
+
+
 def with_unit_values(g: CsrMatrix) -> CsrMatrix:
     return CsrMatrix._adopt(g.num_rows, g.num_cols, g.row_ptr, g.col_idx, np.ones(g.nnz))
 

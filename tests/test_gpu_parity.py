@@ -312,3 +312,70 @@ def test_duplicate_columns_in_b_rows(rng):
     assert_same_product(tsg.multiply(a, b), want, exact=True)
     counts = tsg.spgemm_symbolic(a, tsg.compress(b))
     assert_same_product(tsg.spgemm_numeric(a, b, counts), want, exact=True)
+
+
+# ---------------------------------------------------------------- input builders on the device
+
+def _same_csr(got, want):
+    assert (got.num_rows, got.num_cols) == (want.num_rows, want.num_cols)
+    assert np.array_equal(got.row_ptr, want.row_ptr)
+    assert np.array_equal(got.col_idx, want.col_idx)
+    if want.values is None:
+        assert got.values is None
+    else:
+        assert np.array_equal(got.values, want.values)
+
+
+@pytest.mark.parametrize("kind,dims", [
+    (gen.LAPLACE2D, (7, 5)), (gen.LAPLACE3D, (4, 5, 3)), (gen.BIGSTAR2D, (6, 7)),
+    (gen.BRICK3D, (5, 4, 3)), (gen.BRICK3D, (1, 1, 1)), (gen.ELASTICITY3D, (3, 4, 2)),
+    (gen.BIGSTAR2D, (2, 1))])
+def test_device_stencil_equals_host_builder(kind, dims):
+    _same_csr(gen.stencil_device(kind, dims).download(), gen.stencil(kind, dims))
+
+
+def test_device_stencil_row_range_equals_stencil_rows():
+    dims = (6, 5, 4)
+    for lo, hi in ((17, 83), (0, 120), (119, 120), (40, 40)):
+        _same_csr(gen.stencil_device(gen.BRICK3D, dims, lo, hi).download(),
+                  gen.stencil_rows(gen.BRICK3D, dims, lo, hi))
+
+
+def test_device_stencil_bad_dims_raise_like_host():
+    with pytest.raises(tsg.GridError):
+        gen.stencil_device(gen.BRICK3D, (4, 4))
+    with pytest.raises(tsg.GridError):
+        gen.stencil_device(gen.LAPLACE2D, (0, 3))
+
+
+@pytest.mark.parametrize("dims,factor", [((5, 4, 3), 2), ((8, 8, 8), 2), ((5, 7), 3), ((9,), 4)])
+def test_device_aggregation_equals_host_builder(dims, factor):
+    p_want, r_want = gen.aggregation(dims, factor)
+    dp, dr = gen.aggregation_device(dims, factor)
+    _same_csr(dp.download(), p_want)
+    _same_csr(dr.download(), r_want)
+
+
+def test_device_transpose_equals_host():
+    from paper_1804_00695_b200._lib import DeviceCsr
+    from paper_1804_00695_b200.csr import transpose, transpose_device
+    rng = np.random.default_rng(11)
+    for rows, cols, delta in ((50, 40, 9), (300, 1000, 30), (1, 5, 5), (7, 3, 0)):
+        m = random_csr(rng, rows, cols, delta)
+        _same_csr(transpose_device(DeviceCsr.upload(m)).download(), transpose(m))
+    pat = random_csr(rng, 60, 70, 8, values=False)
+    _same_csr(transpose_device(DeviceCsr.upload(pat)).download(), transpose(pat))
+
+
+def test_device_built_galerkin_product_matches_host_built():
+    """R*A*P from operands built in HBM equals the product of the host-built ones."""
+    from paper_1804_00695_b200 import kernel
+    dims = (9, 8, 7)
+    a = gen.stencil(gen.BRICK3D, dims)
+    p, r = gen.aggregation(dims)
+    want = kernel.multiply(kernel.multiply(r, a), p)
+    da = gen.stencil_device(gen.BRICK3D, dims)
+    dp, dr = gen.aggregation_device(dims)
+    got = kernel.multiply_device(kernel.multiply_device(dr, da), dp).download()
+    _same_csr(canonicalize(got), canonicalize(want))
+    assert np.array_equal(got.values, want.values)   # same first-touch order, bit-exact
