@@ -201,6 +201,17 @@ int tsg_aggregation(tsg_ctx *ctx, const int64_t *dims, int ndims, int factor, ts
                     tsg_csr **r_out);
 int tsg_transpose(tsg_ctx *ctx, const tsg_csr *a, tsg_csr **out);
 
+/* ---- fused Galerkin triple product C = R * A * P (
+   the reference runs multiply(multiply(R, A), P), kernel.py:343-346).
+   mode 0: the two multiplies; mode 1: one symbolic + one numeric pass with
+   RA's rows kept in shared memory (never written to HBM), falling back to
+   the two multiplies when A or P lacks sorted distinct rows or a row of RA /
+   C exceeds the per-row slices.  *fused (may be NULL) reports which ran.
+   The fused result is bit-identical to the two-multiply result of this
+   library when that one keeps its rows in the group tier. */
+int tsg_rap(tsg_ctx *ctx, const tsg_csr *r, const tsg_csr *a, const tsg_csr *p, int mode, tsg_csr **out,
+            int *fused);
+
 /* ---- data placement (memory.py:193-223 PlacementPolicy; PAPER.md:600-625,
    810-829).  A CSR whose arrays live in pinned, device-mapped HOST memory:
    kernels read it in place over PCIe (the paper's "pinned" columns).  Columns

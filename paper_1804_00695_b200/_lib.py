@@ -46,6 +46,7 @@ EXPORTS = (
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
+    "tsg_rap",
 )
 
 _P = ctypes.c_void_p
@@ -91,6 +92,7 @@ _SIGS = {
     "tsg_stencil": ([_P, ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _PP], ctypes.c_int),
     "tsg_aggregation": ([_P, _P, ctypes.c_int, ctypes.c_int, _PP, _PP], ctypes.c_int),
     "tsg_transpose": ([_P, _P, _PP], ctypes.c_int),
+    "tsg_rap": ([_P, _P, _P, _P, ctypes.c_int, _PP, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tsg_gather_sharded": ([_P, ctypes.c_int, _P, _P, _P, _P, _I64, _P, _PP], ctypes.c_int),
     "tsg_numeric_ms": ([_P, _I64, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "tsg_rmat_graph": ([_P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
@@ -485,6 +487,14 @@ def d_transpose(da) -> DeviceCsr:
     h = ctypes.c_void_p()
     check_(load().tsg_transpose(da.ctx.h, da.h, ctypes.byref(h)))
     return DeviceCsr(da.ctx, h)
+
+
+def d_rap(dr, da, dp, fused: bool = True):
+    """(C, fused_ran): C = R * A * P in HBM (csrc/tsg_rap.cu)."""
+    h = ctypes.c_void_p()
+    f = ctypes.c_int(0)
+    check_(load().tsg_rap(da.ctx.h, dr.h, da.h, dp.h, 1 if fused else 0, ctypes.byref(h), ctypes.byref(f)))
+    return DeviceCsr(da.ctx, h), bool(f.value)
 
 
 def d_gather_sharded(da, shards, b_cols: int) -> DeviceCsr:

@@ -109,6 +109,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_TRY(tsg_preload_module_of(tsg_kernel_chunk()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_graph()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_build()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_rap()));
     *out = c;
     return TSG_OK;
 }

@@ -163,6 +163,7 @@ int tsg_preload_module_of(const void *kernel);
 // one representative kernel per .cu file, for tsg_preload_module_of
 const void *tsg_kernel_core();
 const void *tsg_kernel_build();
+const void *tsg_kernel_rap();
 const void *tsg_kernel_compress();
 const void *tsg_kernel_spgemm();
 const void *tsg_kernel_masked();

@@ -272,6 +272,26 @@ def masked_row_intersect_count(l, cl, workers: int = 1) -> int:
 
 # ---- device-resident entry points (no host round trips) ------------------------
 
+def rap(r, a, p, fused: bool = True, workers: int = 1) -> CsrMatrix:
+    """Galerkin triple product R * A * P.  The reference
+    computes it as multiply(multiply(r, a), p) (kernel.py:343-346); with
+    ``fused`` the device keeps each row of R * A in shared memory and never
+    writes RA to HBM (csrc/tsg_rap.cu), falling back to the two multiplies
+    when a row does not fit.  ``workers`` is accepted and ignored."""
+    del workers
+    r, a, p = as_csr(r), as_csr(a), as_csr(p)
+    if r.num_cols != a.num_rows or a.num_cols != p.num_rows:
+        raise DimensionError("R is %dx%d, A %dx%d, P %dx%d: inner dimensions differ"
+                             % (r.num_rows, r.num_cols, a.num_rows, a.num_cols, p.num_rows, p.num_cols))
+    c, _ = rap_device(upload(r), upload(a), upload(p), fused)
+    return c.download()
+
+
+def rap_device(dr, da, dp, fused: bool = True):
+    """(C, fused_ran) for operands already in HBM; C is a DeviceCsr."""
+    return _lib.d_rap(dr, da, dp, fused)
+
+
 def multiply_device(da, db):
     """A * B for operands already in HBM; returns a DeviceCsr."""
     return _lib.d_multiply(da, db)

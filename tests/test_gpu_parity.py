@@ -379,3 +379,54 @@ def test_device_built_galerkin_product_matches_host_built():
     got = kernel.multiply_device(kernel.multiply_device(dr, da), dp).download()
     _same_csr(canonicalize(got), canonicalize(want))
     assert np.array_equal(got.values, want.values)   # same first-touch order, bit-exact
+
+
+# ---------------------------------------------------------------- fused R*A*P
+
+@pytest.mark.parametrize("dims", [(10, 9, 8), (7, 5, 3), (16, 16, 16)])
+def test_fused_rap_bit_identical_to_two_multiplies(dims):
+    from paper_1804_00695_b200 import kernel
+    a = gen.stencil(gen.BRICK3D, dims)
+    p, r = gen.aggregation(dims)
+    want = kernel.multiply(kernel.multiply(r, a), p)
+    dr, da, dp = kernel.upload(r), kernel.upload(a), kernel.upload(p)
+    got, fused = kernel.rap_device(dr, da, dp)
+    assert fused
+    _same_csr(got.download(), want)
+    # against the oracle restatement of the reference's two multiplies
+    ra = O.multiply(r, a)
+    ra_m = CsrMatrix(ra[0].shape[0] - 1, a.num_cols, ra[0], ra[1], ra[2])
+    assert_same_product(canonicalize(got.download()), O.multiply(ra_m, p), exact=False)
+
+
+def test_fused_rap_general_operands():
+    from paper_1804_00695_b200 import kernel
+    rng = np.random.default_rng(5)
+    r = canonicalize(random_csr(rng, 40, 60, 5))
+    a = canonicalize(random_csr(rng, 60, 70, 6))
+    p = canonicalize(random_csr(rng, 70, 30, 3))
+    want = kernel.multiply(kernel.multiply(r, a), p)
+    got, fused = kernel.rap_device(kernel.upload(r), kernel.upload(a), kernel.upload(p))
+    assert fused
+    g = got.download()
+    assert np.array_equal(g.row_ptr, want.row_ptr) and np.array_equal(g.col_idx, want.col_idx)
+    np.testing.assert_allclose(g.values, want.values, rtol=1e-12, atol=0)
+
+
+def test_fused_rap_falls_back_when_rows_do_not_fit():
+    from paper_1804_00695_b200 import kernel
+    rng = np.random.default_rng(6)
+    r = canonicalize(random_csr(rng, 20, 300, 40, exact_delta=True))
+    a = canonicalize(random_csr(rng, 300, 400, 60, exact_delta=True))
+    p = canonicalize(random_csr(rng, 400, 500, 4))
+    want = kernel.multiply(kernel.multiply(r, a), p)
+    got, fused = kernel.rap_device(kernel.upload(r), kernel.upload(a), kernel.upload(p))
+    assert not fused
+    _same_csr(got.download(), want)
+    # explicit two-multiply mode and the host entry point
+    got2, fused2 = kernel.rap_device(kernel.upload(r), kernel.upload(a), kernel.upload(p), fused=False)
+    assert not fused2
+    _same_csr(got2.download(), want)
+    _same_csr(kernel.rap(r, a, p), want)
+    with pytest.raises(tsg.DimensionError):
+        kernel.rap(r, p, a)
