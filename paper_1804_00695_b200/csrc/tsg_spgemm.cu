@@ -2171,6 +2171,10 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
     na.pstart = cptr;
     na.plen_in = plen;
     na.plen_out = plen;
+    if (b->max_row >= 0 && b->max_row <= 1) {   // unit B chunk: owner-folded products
+        na.unit_known = 1;
+        na.unit_dense = (b->max_row == 1 && b->nnz == b->rows) ? 1 : 0;
+    }
     TSG_TRY(launch_num_group<0>(c, bl, na));
     TSG_TRY(launch_num_group<1>(c, bl, na));
     TSG_TRY(launch_num_group<2>(c, bl, na));
