@@ -584,6 +584,109 @@ __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ l
     }
 }
 
+// Merge tier with two lists per lane: G lanes own a row of at most 2G A
+// entries, lane j merges the compressed rows of entries j and j + G on the
+// fly (its head = the smaller of its two list heads, equal heads ORed), and
+// the group combines the G lane heads as above.  Half the lanes per row
+// means half the shuffles per output set per row: the 8-list merge was
+// bound by the shuffle (MIO) pipe.
+template <int G, int SLICE>
+__global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ list, int64_t nlist,
+                                                    SymArgs a) {
+    extern __shared__ int4 smem[];
+    constexpr int CAP = SLICE / 12;
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    const int g = threadIdx.x / G;
+    uint64_t *lbits = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + (size_t)g * SLICE);
+    int32_t *lset = reinterpret_cast<int32_t *>(lbits + CAP);
+    for (int64_t li = (int64_t)blockIdx.x * gpb + g; li < nlist; li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+        int64_t st[2] = {0, 0};
+        int cnt[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (a0 + glane + u * G < a1) {
+                int k = a.acol[a0 + glane + u * G];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st[u] = a.cbstart[k];
+                    cnt[u] = a.cbcnt[k];
+                }
+            }
+        }
+        const int tot = cnt[0] + cnt[1];
+        const int incl = group_incl_scan<G, int>(gm, tot, glane);
+        const int off0 = incl - tot, off1 = off0 + cnt[0];
+        // stage both lists (independent loads, four in flight per lane)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int off = u ? off1 : off0;
+            for (int q0 = 0; q0 < cnt[u]; q0 += 4) {
+                int sv[4];
+                uint64_t bv[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int q = q0 + v < cnt[u] ? q0 + v : cnt[u] - 1;
+                    sv[v] = a.cbset[st[u] + q];
+                    bv[v] = a.cbbits[st[u] + q];
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    if (q0 + v < cnt[u]) {
+                        lset[off + q0 + v] = sv[v];
+                        lbits[off + q0 + v] = bv[v];
+                    }
+            }
+        }
+        __syncwarp(gm);
+        int pa = off0, pb = off1;
+        const int ea = off0 + cnt[0], eb = off1 + cnt[1];
+        int ha = pa < ea ? lset[pa] : INT32_MAX, hb = pb < eb ? lset[pb] : INT32_MAX;
+        uint64_t ma = pa < ea ? lbits[pa] : 0ull, mb = pb < eb ? lbits[pb] : 0ull;
+        const int64_t sp = a.sptr[i];
+        int m = 0, total = 0;
+        for (;;) {
+            const int hs = min(ha, hb);
+            int mn = hs;
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) mn = min(mn, __shfl_xor_sync(gm, mn, d, G));
+            if (mn == INT32_MAX) break;
+            const uint64_t hm = (ha == mn ? ma : 0ull) | (hb == mn ? mb : 0ull);
+            unsigned lo = (unsigned)hm, hi = (unsigned)(hm >> 32);
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) {
+                lo |= __shfl_xor_sync(gm, lo, d, G);
+                hi |= __shfl_xor_sync(gm, hi, d, G);
+            }
+            if (glane == 0) {
+                a.oset[sp + m] = mn;
+                a.obits[sp + m] = ((uint64_t)hi << 32) | lo;
+            }
+            total += __popc(lo) + __popc(hi);
+            ++m;
+            if (ha == mn) {
+                ++pa;
+                ha = pa < ea ? lset[pa] : INT32_MAX;
+                ma = pa < ea ? lbits[pa] : 0ull;
+            }
+            if (hb == mn) {
+                ++pb;
+                hb = pb < eb ? lset[pb] : INT32_MAX;
+                mb = pb < eb ? lbits[pb] : 0ull;
+            }
+        }
+        if (glane == 0) {
+            a.counts[i] = total;
+            if (a.msets) a.msets[i] = m | SETS_WRITTEN;
+        }
+        __syncwarp(gm);
+    }
+}
+
 template <int M>
 int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 
@@ -1691,6 +1794,15 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     const int B = BIN_MERGE + M;
     const int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
+    if constexpr (M == 0) {   // <= 8 A entries: two lists per lane, 4 lanes per row
+        constexpr int G2 = G / 2;
+        const size_t smem = (size_t)(BS / G2) * SL;
+        TSG_TRY(set_smem(k_sym_merge2<G2, SL>, smem));
+        const unsigned grid = group_grid(c, n, BS / G2);
+        k_sym_merge2<G2, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+        TSG_TRY(tsg_launch_check("k_sym_merge2", B, grid, BS, smem));
+        return TSG_OK;
+    }
     const size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_sym_merge<G, SL>, smem));
     const unsigned grid = group_grid(c, n, BS / G);
