@@ -584,13 +584,13 @@ __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ l
     }
 }
 
-// Merge tier with two lists per lane: G lanes own a row of at most 2G A
-// entries, lane j merges the compressed rows of entries j and j + G on the
-// fly (its head = the smaller of its two list heads, equal heads ORed), and
-// the group combines the G lane heads as above.  Half the lanes per row
-// means half the shuffles per output set per row: the 8-list merge was
-// bound by the shuffle (MIO) pipe.
-template <int G, int SLICE>
+// Merge tier with K lists per lane: G lanes own a row of at most K*G A
+// entries, lane j merges the compressed rows of entries j, j + G, ... on the
+// fly (its head = the smallest of its list heads, equal heads ORed), and the
+// group combines the G lane heads as above.  Fewer lanes per row means fewer
+// shuffles per output set per row: the 8-list merge was bound by the
+// shuffle (MIO) pipe.
+template <int G, int K, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ list, int64_t nlist,
                                                     SymArgs a) {
     extern __shared__ int4 smem[];
@@ -605,10 +605,12 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
         const int64_t i = list[li];
         const int64_t gi = i + a.a_row_off;
         const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
-        int64_t st[2] = {0, 0};
-        int cnt[2] = {0, 0};
+        int64_t st[K];
+        int cnt[K];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < K; ++u) {
+            st[u] = 0;
+            cnt[u] = 0;
             if (a0 + glane + u * G < a1) {
                 int k = a.acol[a0 + glane + u * G];
                 if (k >= a.b_lo && k < a.b_hi) {
@@ -618,13 +620,23 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
                 }
             }
         }
-        const int tot = cnt[0] + cnt[1];
-        const int incl = group_incl_scan<G, int>(gm, tot, glane);
-        const int off0 = incl - tot, off1 = off0 + cnt[0];
-        // stage both lists (independent loads, four in flight per lane)
+        int tot = 0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int off = u ? off1 : off0;
+        for (int u = 0; u < K; ++u) tot += cnt[u];
+        const int incl = group_incl_scan<G, int>(gm, tot, glane);
+        int p[K], e[K];
+        {
+            int off = incl - tot;
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                p[u] = off;
+                off += cnt[u];
+                e[u] = off;
+            }
+        }
+        // stage the lists (independent loads, four in flight per lane)
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
             for (int q0 = 0; q0 < cnt[u]; q0 += 4) {
                 int sv[4];
                 uint64_t bv[4];
@@ -637,25 +649,31 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
                     if (q0 + v < cnt[u]) {
-                        lset[off + q0 + v] = sv[v];
-                        lbits[off + q0 + v] = bv[v];
+                        lset[p[u] + q0 + v] = sv[v];
+                        lbits[p[u] + q0 + v] = bv[v];
                     }
             }
         }
         __syncwarp(gm);
-        int pa = off0, pb = off1;
-        const int ea = off0 + cnt[0], eb = off1 + cnt[1];
-        int ha = pa < ea ? lset[pa] : INT32_MAX, hb = pb < eb ? lset[pb] : INT32_MAX;
-        uint64_t ma = pa < ea ? lbits[pa] : 0ull, mb = pb < eb ? lbits[pb] : 0ull;
+        int h[K];
+        uint64_t mk[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            h[u] = p[u] < e[u] ? lset[p[u]] : INT32_MAX;
+            mk[u] = p[u] < e[u] ? lbits[p[u]] : 0ull;
+        }
         const int64_t sp = a.sptr[i];
         int m = 0, total = 0;
         for (;;) {
-            const int hs = min(ha, hb);
-            int mn = hs;
+            int mn = h[0];
+#pragma unroll
+            for (int u = 1; u < K; ++u) mn = min(mn, h[u]);
 #pragma unroll
             for (int d = G / 2; d >= 1; d >>= 1) mn = min(mn, __shfl_xor_sync(gm, mn, d, G));
             if (mn == INT32_MAX) break;
-            const uint64_t hm = (ha == mn ? ma : 0ull) | (hb == mn ? mb : 0ull);
+            uint64_t hm = 0ull;
+#pragma unroll
+            for (int u = 0; u < K; ++u) hm |= h[u] == mn ? mk[u] : 0ull;
             unsigned lo = (unsigned)hm, hi = (unsigned)(hm >> 32);
 #pragma unroll
             for (int d = G / 2; d >= 1; d >>= 1) {
@@ -668,15 +686,13 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
             }
             total += __popc(lo) + __popc(hi);
             ++m;
-            if (ha == mn) {
-                ++pa;
-                ha = pa < ea ? lset[pa] : INT32_MAX;
-                ma = pa < ea ? lbits[pa] : 0ull;
-            }
-            if (hb == mn) {
-                ++pb;
-                hb = pb < eb ? lset[pb] : INT32_MAX;
-                mb = pb < eb ? lbits[pb] : 0ull;
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                if (h[u] == mn) {
+                    ++p[u];
+                    h[u] = p[u] < e[u] ? lset[p[u]] : INT32_MAX;
+                    mk[u] = p[u] < e[u] ? lbits[p[u]] : 0ull;
+                }
             }
         }
         if (glane == 0) {
@@ -687,6 +703,9 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
     }
 }
 
+#ifndef MERGE_LISTS_PER_LANE
+#define MERGE_LISTS_PER_LANE 2
+#endif
 template <int M>
 int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 
@@ -1795,11 +1814,11 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     const int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
     if constexpr (M == 0) {   // <= 8 A entries: two lists per lane, 4 lanes per row
-        constexpr int G2 = G / 2;
+        constexpr int K = MERGE_LISTS_PER_LANE, G2 = G / K;
         const size_t smem = (size_t)(BS / G2) * SL;
-        TSG_TRY(set_smem(k_sym_merge2<G2, SL>, smem));
+        TSG_TRY(set_smem(k_sym_merge2<G2, K, SL>, smem));
         const unsigned grid = group_grid(c, n, BS / G2);
-        k_sym_merge2<G2, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+        k_sym_merge2<G2, K, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
         TSG_TRY(tsg_launch_check("k_sym_merge2", B, grid, BS, smem));
         return TSG_OK;
     }
