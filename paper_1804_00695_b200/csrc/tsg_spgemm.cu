@@ -1813,7 +1813,7 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     const int B = BIN_MERGE + M;
     const int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
-    if constexpr (M == 0) {   // <= 8 A entries: two lists per lane, 4 lanes per row
+    if constexpr (MERGE_LISTS_PER_LANE > 1) {   // K lists per lane, G / K lanes per row
         constexpr int K = MERGE_LISTS_PER_LANE, G2 = G / K;
         const size_t smem = (size_t)(BS / G2) * SL;
         TSG_TRY(set_smem(k_sym_merge2<G2, K, SL>, smem));
