@@ -892,16 +892,22 @@ __device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, 
 
 // One A entry's B-row batch for products_seq: the first BB_UF*G entries of
 // the row, loaded together so their DRAM latencies overlap.
-constexpr int BB_UF = 4;
-struct BBatch {
-    int c[BB_UF];
-    double v[BB_UF];
+template <int G>
+__host__ __device__ constexpr int bb_uf() { return G < 8 ? 8 : 4; }   // >= 32 entries per batch
+template <int UF>
+struct BBatchT {
+    int c[UF];
+    double v[UF];
 };
 
 template <int G>
-__device__ __forceinline__ BBatch bbatch_issue(unsigned gm, int glane, const NumArgs &a, int64_t st,
-                                               int len, int j, int cnt) {
-    BBatch b;
+using BBatch = BBatchT<bb_uf<G>()>;
+
+template <int G>
+__device__ __forceinline__ BBatch<G> bbatch_issue(unsigned gm, int glane, const NumArgs &a, int64_t st,
+                                                  int len, int j, int cnt) {
+    constexpr int BB_UF = bb_uf<G>();
+    BBatch<G> b;
     const int jj = j < cnt ? j : 0;
     const int64_t sj = __shfl_sync(gm, st, jj, G);
     const int lj = j < cnt ? __shfl_sync(gm, len, jj, G) : 0;
@@ -916,8 +922,9 @@ __device__ __forceinline__ BBatch bbatch_issue(unsigned gm, int glane, const Num
 
 template <int G>
 __device__ __forceinline__ void bbatch_accumulate(unsigned gm, int glane, const NumArgs &a, int64_t st,
-                                                  int len, double av, int j, const BBatch &b,
+                                                  int len, double av, int j, const BBatch<G> &b,
                                                   const int4 *tbl, int T, int logT, double *vals) {
+    constexpr int BB_UF = bb_uf<G>();
     const int64_t sj = __shfl_sync(gm, st, j, G);
     const int lj = __shfl_sync(gm, len, j, G);
     const double aj = __shfl_sync(gm, av, j, G);
@@ -971,9 +978,9 @@ __device__ __forceinline__ void products_seq(unsigned gm, int glane, const NumAr
         // are loaded in one batch, and entry j+1's batch is issued before entry
         // j is accumulated, so a row costs ~1 DRAM round trip per A chunk
         // instead of one per (entry, G-slice).
-        BBatch bx = bbatch_issue<G>(gm, glane, a, st, len, 0, cnt);
+        BBatch<G> bx = bbatch_issue<G>(gm, glane, a, st, len, 0, cnt);
         for (int j = 0; j < cnt; j += 2) {
-            BBatch by = bbatch_issue<G>(gm, glane, a, st, len, j + 1, cnt);
+            BBatch<G> by = bbatch_issue<G>(gm, glane, a, st, len, j + 1, cnt);
             bbatch_accumulate<G>(gm, glane, a, st, len, av, j, bx, tbl, T, logT, vals);
             bx = bbatch_issue<G>(gm, glane, a, st, len, j + 2, cnt);
             if (j + 1 < cnt) bbatch_accumulate<G>(gm, glane, a, st, len, av, j + 1, by, tbl, T, logT, vals);
@@ -1132,12 +1139,11 @@ __device__ __forceinline__ NumRowHdr num_row_hdr(const NumArgs &a, int64_t i) {
     return h;
 }
 
-constexpr int NUM_SKEW = 64;
 
 // bytes of the per-group value slices of a k_num_group block (with skew)
 template <int G, int SLICE>
 __host__ __device__ constexpr size_t num_slices_bytes(int gpb) {
-    return (size_t)gpb * SLICE + (G == 8 ? (size_t)(gpb / 2) * NUM_SKEW : 0);
+    return (size_t)gpb * SLICE + (G <= 8 ? (size_t)gpb * 8 * G : 0);
 }
 
 // MODE 0: generic / unit B known on the device; 1: lane-split B rows (SEQ);
@@ -1150,12 +1156,12 @@ __global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ l
     const int glane = threadIdx.x & (G - 1);
     const unsigned lt = lanemask_lt();
     const int gpb = blockDim.x / G;
-    // 8-lane groups: a half-warp 64-bit shared access spans two groups, whose
-    // equally aligned slices would put equal value positions on one bank;
-    // each odd group starts 64 B (16 banks) later than its even partner
-    // (cumulative, so slices never overlap)
+    // groups of <= 8 lanes: a half-warp 64-bit shared access spans 16 / G
+    // groups whose equally aligned slices would put equal value positions
+    // on one bank; group g starts g * 8G bytes later (8-lane groups: odd
+    // groups 64 B = 16 banks after their even partner; 4-lane: 32 B steps)
     char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE +
-                  (G == 8 ? (size_t)(((threadIdx.x / G) + 1) >> 1) * NUM_SKEW : 0);
+                  (G <= 8 ? (size_t)(threadIdx.x / G) * 8 * G : 0);
     for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
          li += (int64_t)gridDim.x * gpb) {
         const NumRowHdr h = num_row_hdr(a, list[li]);
@@ -1683,7 +1689,10 @@ int launch_sym_group(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 
 template <int B, int MODE>
 int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
-    constexpr int G = gt_g(B), SL = gt_slice(B), BS = gt_block(B);
+    // unit-B rows (owner-folded products) of the two smallest bins: 4 lanes
+    // per row, twice the rows in flight (measured: RA*P 241 -> 182 us; the
+    // lane-split SEQ mode stays at 8 lanes, where 4 was slower)
+    constexpr int G = (MODE == 2 && B <= 1) ? 4 : gt_g(B), SL = gt_slice(B), BS = gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
     size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * UB * G * UWIN_B : 0);
     TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
