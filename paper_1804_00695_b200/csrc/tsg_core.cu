@@ -79,6 +79,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaMalloc(&c->d_err, 4 * sizeof(int)));
     TSG_CK(cudaMemset(c->d_err, 0, 4 * sizeof(int)));
     TSG_CK(cudaMalloc(&c->d_small, 64 * sizeof(int64_t)));
+    TSG_CK(cudaMemset(c->d_small, 0, 64 * sizeof(int64_t)));   // counters (e.g. slot 60) start at 0
     TSG_CK(cudaHostAlloc(&c->h_small, 64 * sizeof(int64_t), cudaHostAllocMapped));
     TSG_CK(cudaHostGetDevicePointer(&c->hd_small, c->h_small, 0));
     memset(c->h_small, 0, 64 * sizeof(int64_t));   // sequence words start below any issued seq

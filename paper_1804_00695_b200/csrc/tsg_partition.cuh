@@ -25,9 +25,13 @@ struct BinLists {
     int64_t off[NB + 1] = {0};
 };
 
+// tile counts up to this many are scanned by the last k_part_bins block
+constexpr int PART_FUSED_SCAN = 16384;
+
 template <int NB, class F>
 __global__ void __launch_bounds__(256) k_part_bins(int64_t rows, F f, uint8_t *__restrict__ bins,
-                                                   int ntiles, int *__restrict__ tc) {
+                                                   int ntiles, int *__restrict__ tc,
+                                                   unsigned *__restrict__ done, int64_t *__restrict__ offs) {
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
     __syncthreads();
@@ -46,6 +50,48 @@ __global__ void __launch_bounds__(256) k_part_bins(int64_t rows, F f, uint8_t *_
     }
     __syncthreads();
     if (threadIdx.x < NB) tc[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+    if (!done) return;
+    // the last block to finish scans the NB x ntiles tile counts (no
+    // separate scan launch); the counter is left at 0 for the next partition
+    __shared__ bool s_last;
+    __shared__ int64_t s_warp[8];
+    __shared__ int64_t s_carry;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == (unsigned)ntiles - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int n = NB * ntiles;
+    if (threadIdx.x == 0) {
+        s_carry = 0;
+        *done = 0;
+    }
+    __syncthreads();
+    for (int b0 = 0; b0 < n; b0 += 256) {
+        const int q = b0 + threadIdx.x;
+        const int64_t v = q < n ? (int64_t)(*(volatile int *)&tc[q]) : 0;
+        int64_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        const int w = threadIdx.x >> 5;
+        if (lane == 31) s_warp[w] = x;
+        __syncthreads();
+        int64_t woff = 0, agg = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            woff += j < w ? s_warp[j] : 0;
+            agg += s_warp[j];
+        }
+        if (q < n) offs[q] = s_carry + woff + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offs[n] = s_carry;
 }
 
 template <int NB>
@@ -105,8 +151,10 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_TRY(tsg_alloc_t(c, &tc, (size_t)NB * ntiles));
     TSG_TRY(tsg_alloc_t(c, &offs, (size_t)NB * ntiles + 1));
     TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
-    k_part_bins<NB, F><<<ntiles, 256, 0, c->stream>>>(rows, f, bins, ntiles, tc); ++c->launches;
-    TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NB * ntiles));
+    const bool fused_scan = (int64_t)NB * ntiles <= PART_FUSED_SCAN;
+    unsigned *done = fused_scan ? reinterpret_cast<unsigned *>(c->d_small + 60) : nullptr;
+    k_part_bins<NB, F><<<ntiles, 256, 0, c->stream>>>(rows, f, bins, ntiles, tc, done, offs); ++c->launches;
+    if (!fused_scan) TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NB * ntiles));
     TSG_TRY(mid());
     // results land in mapped host memory straight from the kernel: no D2H
     // copy that would queue behind bulk transfers on the copy engine
