@@ -19,7 +19,8 @@ from .errors import (CapacityError, DimensionError, GridError, KernelError,
                      MatrixValidationError, UnsplittableRowError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsg.so")
+# TSG_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("TSG_LIB") or os.path.join(_HERE, "libtsg.so")
 
 TSG_OK, TSG_EDIM, TSG_EVALID, TSG_EKERNEL, TSG_ECAPACITY, TSG_EUNSPLIT, TSG_ECUDA, TSG_EARG = range(8)
 

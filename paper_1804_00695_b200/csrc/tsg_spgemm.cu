@@ -983,7 +983,8 @@ __device__ __forceinline__ void products_seq(unsigned gm, int glane, const NumAr
             BBatch<G> by = bbatch_issue<G>(gm, glane, a, st, len, j + 1, cnt);
             bbatch_accumulate<G>(gm, glane, a, st, len, av, j, bx, tbl, T, logT, vals);
             bx = bbatch_issue<G>(gm, glane, a, st, len, j + 2, cnt);
-            if (j + 1 < cnt) bbatch_accumulate<G>(gm, glane, a, st, len, av, j + 1, by, tbl, T, logT, vals);
+            if (j + 1 < cnt)
+                bbatch_accumulate<G>(gm, glane, a, st, len, av, j + 1, by, tbl, T, logT, vals);
         }
     }
 }
@@ -1148,8 +1149,38 @@ __host__ __device__ constexpr size_t num_slices_bytes(int gpb) {
 
 // MODE 0: generic / unit B known on the device; 1: lane-split B rows (SEQ);
 // 2: unit B known on the host (products_unit_owned, staging after the slices)
+// Block size and minimum resident blocks of the numeric group kernels.  The
+// two dominant config-2 instances are latency-bound, so occupancy is worth
+// a few spilled registers (measured, R*A numeric: 256 threads at 80
+// registers = 24 warps/SM 0.400 ms; 128 x 8 blocks at 64 registers = 32
+// warps 0.370 ms).
+#ifndef TSG_NUM8_BS
+#define TSG_NUM8_BS 128
+#endif
+#ifndef TSG_NUM8_MINB
+#define TSG_NUM8_MINB 8
+#endif
+#ifndef TSG_NUM4_BS
+#define TSG_NUM4_BS 256
+#endif
+#ifndef TSG_NUM4_MINB
+#define TSG_NUM4_MINB 4
+#endif
+template <int G, int MODE>
+__host__ __device__ constexpr int num_bs() {
+    return (G == 8 && MODE == 1) ? TSG_NUM8_BS : (G == 4 && MODE == 2) ? TSG_NUM4_BS : 256;
+}
+template <int G, int MODE>
+__host__ __device__ constexpr int num_minb() {
+    // the rest: the register budgets ptxas picks for a bare 256-thread bound
+    return (G == 8 && MODE == 1) ? TSG_NUM8_MINB
+           : (G == 4 && MODE == 2) ? TSG_NUM4_MINB
+           : MODE == 1             ? 3
+                                   : 4;
+}
+
 template <int G, int SLICE, int MODE>
-__global__ void __launch_bounds__(256) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
+__global__ void __launch_bounds__(num_bs<G, MODE>(), num_minb<G, MODE>()) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
     extern __shared__ int4 smem[];
     const unsigned gm = group_mask<G>();
@@ -1692,7 +1723,8 @@ int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     // unit-B rows (owner-folded products) of the two smallest bins: 4 lanes
     // per row, twice the rows in flight (measured: RA*P 241 -> 182 us; the
     // lane-split SEQ mode stays at 8 lanes, where 4 was slower)
-    constexpr int G = (MODE == 2 && B <= 1) ? 4 : gt_g(B), SL = gt_slice(B), BS = gt_block(B);
+    constexpr int G = (MODE == 2 && B <= 1) ? 4 : gt_g(B), SL = gt_slice(B);
+    constexpr int BS = num_bs<G, MODE>() < gt_block(B) ? num_bs<G, MODE>() : gt_block(B);
     int64_t n = bl.off[B + 1] - bl.off[B];
     size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * UB * G * UWIN_B : 0);
     TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
@@ -1887,12 +1919,15 @@ struct BinFork {
     template <class L>
     int run(int64_t n, L launch) {
         if (n <= 0) return TSG_OK;
-        if (used++ == 0) return launch();   // first bin: compute stream
-        const int k = (used - 2) % tsg_ctx::NAUX;
-        if (!forked) {
+        if (used++ == 0) {
+            // the fork point precedes the first bin, so the later bins do
+            // not wait for it (a 16-row bin 0 otherwise serialised ~20 us
+            // of dependent-load latency ahead of the big bin)
             TSG_CK(cudaEventRecord(c->ev_fork, c->stream));
-            forked = true;
+            return launch();   // first bin: compute stream
         }
+        const int k = (used - 2) % tsg_ctx::NAUX;
+        forked = true;
         cudaStream_t main = c->stream;
         TSG_CK(cudaStreamWaitEvent(c->aux[k], c->ev_fork, 0));
         c->stream = c->aux[k];
