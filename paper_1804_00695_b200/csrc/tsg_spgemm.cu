@@ -634,6 +634,30 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
                 e[u] = off;
             }
         }
+#ifndef MERGE_CP_ASYNC
+#define MERGE_CP_ASYNC 1
+#endif
+#if MERGE_CP_ASYNC
+        // stage the lists with asynchronous global->shared copies: every
+        // entry of the lane's K lists is in flight at once and the lane
+        // waits a single round trip (the register-staged form waited one
+        // per 4-entry batch, ~6 per row)
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const unsigned ds = (unsigned)__cvta_generic_to_shared(lset + p[u]);
+            const unsigned db = (unsigned)__cvta_generic_to_shared(lbits + p[u]);
+            const int32_t *gs = a.cbset + st[u];
+            const uint64_t *gb = a.cbbits + st[u];
+#pragma unroll 4
+            for (int q = 0; q < cnt[u]; ++q) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ds + 4u * q), "l"(gs + q)
+                             : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(db + 8u * q), "l"(gb + q)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#else
         // stage the lists (independent loads, four in flight per lane)
 #pragma unroll
         for (int u = 0; u < K; ++u) {
@@ -654,6 +678,7 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
                     }
             }
         }
+#endif
         __syncwarp(gm);
         int h[K];
         uint64_t mk[K];
