@@ -823,12 +823,43 @@ __global__ void __launch_bounds__(NT) k_sym_thread(const int32_t *__restrict__ l
         int m = 0;             // finished sets in key/msk (all below lastk)
         int lastk = -1;        // largest set so far (-1: none)
         uint64_t lastm = 0;
-        for (int64_t t0 = a0; t0 < a1; t0 += TSYM_BATCH) {
+#ifndef TSYM_VEC
+#define TSYM_VEC 1
+#endif
+        // A's columns in 16-byte loads from the aligned position at or below
+        // a0 (a thread reads its own row, so scalar loads cost one L1
+        // wavefront per entry and warp); entries outside [a0, a1) masked
+        const bool vec = TSYM_VEC && ((reinterpret_cast<uintptr_t>(a.acol) & 15) == 0);
+        for (int64_t t0 = vec ? (a0 & ~(int64_t)3) : a0; t0 < a1; t0 += TSYM_BATCH) {
             int kk[TSYM_BATCH];
+            if (vec) {
 #pragma unroll
-            for (int u = 0; u < TSYM_BATCH; ++u) {
-                int k = t0 + u < a1 ? a.acol[t0 + u] : -1;
-                kk[u] = (k >= a.b_lo && k < a.b_hi) ? k - a.b_lo : -1;
+                for (int v = 0; v < TSYM_BATCH; v += 4) {
+                    int4 c4;
+                    if (t0 + v + 4 <= a1) {
+                        c4 = __ldg(reinterpret_cast<const int4 *>(a.acol + t0 + v));
+                    } else {
+                        c4.x = t0 + v < a1 ? a.acol[t0 + v] : -1;
+                        c4.y = t0 + v + 1 < a1 ? a.acol[t0 + v + 1] : -1;
+                        c4.z = t0 + v + 2 < a1 ? a.acol[t0 + v + 2] : -1;
+                        c4.w = -1;
+                    }
+                    kk[v] = c4.x;
+                    kk[v + 1] = c4.y;
+                    kk[v + 2] = c4.z;
+                    kk[v + 3] = c4.w;
+                }
+#pragma unroll
+                for (int u = 0; u < TSYM_BATCH; ++u) {
+                    const int k = (t0 + u >= a0 && t0 + u < a1) ? kk[u] : -1;
+                    kk[u] = (k >= a.b_lo && k < a.b_hi) ? k - a.b_lo : -1;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < TSYM_BATCH; ++u) {
+                    int k = t0 + u < a1 ? a.acol[t0 + u] : -1;
+                    kk[u] = (k >= a.b_lo && k < a.b_hi) ? k - a.b_lo : -1;
+                }
             }
             int sv[TSYM_BATCH];
             uint64_t bv[TSYM_BATCH];
