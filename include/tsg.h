@@ -58,6 +58,13 @@ int tsg_destroy(tsg_ctx *ctx);
 int tsg_sync(tsg_ctx *ctx);
 /* Bytes of device memory currently held by the context's allocations. */
 int tsg_mem_in_use(tsg_ctx *ctx, int64_t *bytes);
+/* Shared-memory hash-table conflict counters of the symbolic / numeric group
+ * tiers since the last reset: out = {lookups, extra lookup probes, inserts,
+ * extra insert probes}.  Diagnostic builds only (-DTSG_PROBE_STATS=1); the
+ * product build returns TSG_EARG.  No reference counterpart (the reference's
+ * HashmapAccumulator, accumulator.py:95-127, probes the same way but keeps no
+ * statistics). */
+int tsg_probe_stats(tsg_ctx *ctx, int64_t out[4], int reset);
 /* Bytes the device's stream-ordered pool has reserved from the driver. */
 int tsg_pool_reserved(tsg_ctx *ctx, int64_t *bytes);
 /* Per-phase device times (ms) of the last tsg_multiply (timing enabled):

@@ -37,7 +37,7 @@ _ERRORS = {
 # every symbol include/tsg.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "tsg_last_error", "tsg_abi_version", "tsg_device_count", "tsg_init", "tsg_destroy",
-    "tsg_sync", "tsg_mem_in_use", "tsg_pool_reserved", "tsg_last_phase_ms", "tsg_set_timing", "tsg_get_stats",
+    "tsg_sync", "tsg_mem_in_use", "tsg_probe_stats", "tsg_pool_reserved", "tsg_last_phase_ms", "tsg_set_timing", "tsg_get_stats",
     "tsg_csr_upload", "tsg_csr_info", "tsg_csr_download", "tsg_csr_slice_rows", "tsg_csr_free",
     "tsg_compress", "tsg_cmat_info", "tsg_cmat_download", "tsg_cmat_upload", "tsg_cmat_free",
     "tsg_vec_upload", "tsg_vec_download", "tsg_vec_len", "tsg_vec_free",
@@ -57,6 +57,7 @@ _PP = ctypes.POINTER(ctypes.c_void_p)
 
 _SIGS = {
     "tsg_last_error": ([], ctypes.c_char_p),
+    "tsg_probe_stats": ([_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_int], ctypes.c_int),
     "tsg_abi_version": ([], ctypes.c_int),
     "tsg_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tsg_init": ([ctypes.c_int, _PP], ctypes.c_int),

@@ -18,6 +18,26 @@
 // ---------------------------------------------------------------- tables
 // slot = int4 {key, mask_lo, mask_hi, base}; key TSG_EMPTY when free.
 
+// Hash-conflict counters (diagnostic builds, -DTSG_PROBE_STATS=1): lookups,
+// extra probes of lookups, inserts, extra probes of inserts.  One copy per
+// translation unit; tsg_probe_stats() reads tsg_spgemm.cu's (the symbolic and
+// numeric group tiers).  Compiled out of the product build.
+#ifndef TSG_PROBE_STATS
+#define TSG_PROBE_STATS 0
+#endif
+#if TSG_PROBE_STATS
+static __device__ unsigned long long g_tsg_probe[4];
+#define TSG_PROBE_COUNT(which, extra)                           \
+    do {                                                        \
+        atomicAdd(&g_tsg_probe[which], 1ull);                   \
+        if (extra) atomicAdd(&g_tsg_probe[(which) + 1], (unsigned long long)(extra)); \
+    } while (0)
+#else
+#define TSG_PROBE_COUNT(which, extra) \
+    do {                              \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void tbl_clear(int4 *tbl, int T, int from, int step) {
     for (int s = from; s < T; s += step) tbl[s] = make_int4(TSG_EMPTY, 0, 0, 0);
 }
@@ -35,6 +55,7 @@ __device__ __forceinline__ bool tbl_or(int4 *tbl, int T, int logT, int key, unsi
         if (k == key) {
             if (lo) atomicOr((unsigned *)&tbl[h].y, lo);
             if (hi) atomicOr((unsigned *)&tbl[h].z, hi);
+            TSG_PROBE_COUNT(2, n);
             return true;
         }
         h = (h + 1) & (unsigned)(T - 1);
@@ -46,7 +67,10 @@ __device__ __forceinline__ bool tbl_or(int4 *tbl, int T, int logT, int key, unsi
 __device__ __forceinline__ int tbl_claim(int4 *tbl, int T, int logT, int key) {
     unsigned h = hash_slot(key, logT);
     for (int n = 0; n < T; ++n) {
-        if (atomicCAS(&tbl[h].x, TSG_EMPTY, key) == TSG_EMPTY) return (int)h;
+        if (atomicCAS(&tbl[h].x, TSG_EMPTY, key) == TSG_EMPTY) {
+            TSG_PROBE_COUNT(2, n);
+            return (int)h;
+        }
         h = (h + 1) & (unsigned)(T - 1);
     }
     return -1;
@@ -59,6 +83,7 @@ __device__ __forceinline__ int tbl_find(const int4 *tbl, int T, int logT, int ke
         int4 e = tbl[h];
         if (e.x == key) {
             out = e;
+            TSG_PROBE_COUNT(0, n);
             return (int)h;
         }
         if (e.x == TSG_EMPTY) return -1;

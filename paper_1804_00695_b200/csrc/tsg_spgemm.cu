@@ -2451,6 +2451,26 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
 
 // ======================================================================= C ABI
 
+extern "C" int tsg_probe_stats(tsg_ctx *c, int64_t out[4], int reset) {
+    (void)c;
+    for (int k = 0; k < 4; ++k) out[k] = 0;
+#if TSG_PROBE_STATS
+    unsigned long long h[4];
+    TSG_CK(cudaDeviceSynchronize());
+    TSG_CK(cudaMemcpyFromSymbol(h, g_tsg_probe, sizeof(h)));
+    for (int k = 0; k < 4; ++k) out[k] = (int64_t)h[k];
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        TSG_CK(cudaMemcpyToSymbol(g_tsg_probe, z, sizeof(z)));
+    }
+    return TSG_OK;
+#else
+    (void)reset;
+    tsg_set_error("tsg_probe_stats: library built without -DTSG_PROBE_STATS=1");
+    return TSG_EARG;
+#endif
+}
+
 extern "C" int tsg_compress(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_compress_impl(c, b, out));
     return tsg_check_kernel_errors(c, "compress");
