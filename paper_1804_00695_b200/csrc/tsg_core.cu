@@ -66,8 +66,13 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     TSG_CK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
     TSG_CK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    TSG_CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     for (int i = 0; i < tsg_ctx::NAUX; ++i) {
-        TSG_CK(cudaStreamCreateWithFlags(&c->aux[i], cudaStreamNonBlocking));
+        // forked bins (BinFork) run at the highest priority: the block
+        // scheduler then dispatches a small bin's blocks as soon as the big
+        // bin's first blocks retire instead of after all of them
+        TSG_CK(cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, prio_hi));
         TSG_CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
     }
     TSG_CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
