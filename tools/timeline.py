@@ -34,6 +34,10 @@ def main():
     if not ks:
         print("no kernel records")
         return
+    # a kernel left over from before the profiled step (the profiler's own
+    # start-up fill) can precede the step by milliseconds: drop it
+    while len(ks) > 1 and ks[1][0] - ks[0][1] > 500.0:
+        ks = ks[1:]
     t0 = ks[0][0]
     busy_end = t0
     idle = 0.0
