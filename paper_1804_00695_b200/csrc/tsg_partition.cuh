@@ -170,7 +170,9 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));
+    tsg_trace_host("partition: wait");
     TSG_TRY(tsg_wait_mapped(c, 61, c->part_seq));
+    tsg_trace_host("partition: results");
     TSG_TRY(tsg_pending_errors(c));
     for (int b = 0; b <= NB; b++) out.off[b] = c->h_small[32 + b];
     if (extra_out) *extra_out = c->h_small[32 + NB + 1];

@@ -2035,7 +2035,11 @@ struct BinJob {
 int run_bins_largest_first(tsg_ctx *c, BinJob *jobs, int njobs) {
     std::stable_sort(jobs, jobs + njobs, [](const BinJob &x, const BinJob &y) { return x.n > y.n; });
     BinFork f(c);
-    for (int k = 0; k < njobs; ++k) TSG_TRY(f.run(jobs[k].n, jobs[k].launch));
+    tsg_trace_host("bins: first launch");
+    for (int k = 0; k < njobs; ++k) {
+        TSG_TRY(f.run(jobs[k].n, jobs[k].launch));
+        if (k == 0) tsg_trace_host("bins: first launched");
+    }
     return f.join();
 }
 
