@@ -31,6 +31,7 @@ constexpr int CT = 256;                 // threads (= words) per block
 constexpr int PB = CT * 32;             // entries per block
 
 __global__ void k_row_starts(int64_t rows, const int64_t *__restrict__ rp, uint32_t *rsbits, int *dmax) {
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *dmax = 0;   // max set count, raised by P2 / F2
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(CT, 5) k_compress_onepass(
     uint32_t *__restrict__ hbits, uint16_t *__restrict__ wpre, int64_t *__restrict__ boff,
     int64_t nblocks, unsigned long long *state, unsigned *counter, int32_t *__restrict__ oset,
     uint64_t *__restrict__ obits, int *unsorted, int64_t pf) {
+    pdl_wait();
     extern __shared__ int4 esm[];
     __shared__ int s_w[CT / 32];
     __shared__ int64_t s_b0;
@@ -307,6 +309,7 @@ __global__ void k_set_starts(int64_t rows, int64_t nnz, const int64_t *__restric
                              const int64_t *__restrict__ boff, int64_t nblocks,
                              int64_t *__restrict__ start, int32_t *__restrict__ cnt,
                              const int *unsorted, int *dmax) {
+    pdl_wait();
     if (*unsorted) return;
     int mx = 0;
     auto rank_at = [&](int64_t e) -> int64_t {
@@ -480,22 +483,26 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_fill(c, rsbits, 0, nwords * sizeof(uint32_t), s));
     TSG_TRY(tsg_fill(c, unsorted, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(rows + 1, 256, c->num_sms * 16);
-    k_row_starts<<<rgrid, 256, 0, s>>>(rows, b->rp, rsbits, cm->cnt + rows + 1); ++c->launches;
+    TSG_CK(launch_pdl(k_row_starts, rgrid, 256, 0, s, rows, (const int64_t *)b->rp, rsbits, cm->cnt + rows + 1));
+    ++c->launches;
     unsigned long long *lbstate = nullptr;
     TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
     TSG_TRY(tsg_fill(c, lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
     const size_t esmem = EMIT_SMEM;
     auto kern = b->sorted ? k_compress_onepass<false> : k_compress_onepass<true>;
     TSG_TRY(tsg_func_smem((const void *)kern, esmem));
-    kern<<<(unsigned)nblocks, CT, esmem, s>>>(
-        nnz, b->col, rsbits, hbits, wpre, bcnt, nblocks, lbstate,
-        reinterpret_cast<unsigned *>(lbstate + nblocks), cm->set, cm->bits, unsorted,
-        (int64_t)c->num_sms * TSG_CPF); ++c->launches;
+    TSG_CK(launch_pdl(kern, (unsigned)nblocks, CT, esmem, s, nnz, (const int32_t *)b->col,
+                      (const uint32_t *)rsbits, hbits, wpre, bcnt, nblocks, lbstate,
+                      reinterpret_cast<unsigned *>(lbstate + nblocks), cm->set, cm->bits, unsorted,
+                      (int64_t)c->num_sms * TSG_CPF));
+    ++c->launches;
     // (one row per thread measured slower than this grid-stride loop:
     // 34 vs 27 us at 2 M rows)
     const unsigned sgrid = rgrid;
-    k_set_starts<<<sgrid, 256, 0, s>>>(rows, nnz, b->rp, hbits, wpre, bcnt, nblocks, cm->start, cm->cnt,
-                                       unsorted, cm->cnt + rows + 1); ++c->launches;
+    TSG_CK(launch_pdl(k_set_starts, sgrid, 256, 0, s, rows, nnz, (const int64_t *)b->rp,
+                      (const uint32_t *)hbits, (const uint16_t *)wpre, (const int64_t *)bcnt, nblocks,
+                      cm->start, cm->cnt, (const int *)unsorted, cm->cnt + rows + 1));
+    ++c->launches;
     // first-occurrence fallback for input not known to be row-sorted: every
     // kernel returns at once if P1 found the rows sorted after all
     if (!b->sorted) {

@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in
                                                       int64_t *__restrict__ out,
                                                       unsigned long long *state, unsigned epoch,
                                                       unsigned ntiles) {
+    pdl_wait();
     // tile = block index: blocks are dispatched in index order, so every
     // predecessor a tile waits for is already resident
     __shared__ int64_t ws[LB_BS / 32];
@@ -830,7 +831,8 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     TSG_TRY(tsg_lookback_state(c, tiles, &state, &epoch));
     // in-place safe: a tile reads its inputs before writing, and writes only
     // its own range (plus out[n], past every input)
-    scan_lookback<TI><<<(unsigned)tiles, LB_BS, 0, c->stream>>>(in, n, out, state, epoch, (unsigned)tiles);
+    TSG_CK(launch_pdl(scan_lookback<TI>, (unsigned)tiles, LB_BS, 0, c->stream, in, n, out, state, epoch,
+                      (unsigned)tiles));
     ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;

@@ -12,6 +12,7 @@
 // native 32-bit ATOMS.OR halves (a 64-bit shared-memory OR is a CAS loop on
 // sm_100a).  One 128-bit LDS fetches a whole slot during lookups.
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -227,6 +228,43 @@ struct PhaseTimer {
     }
     void finish(int total_slot);
 };
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The short kernels of a phase's chain (compress, partition, scan) are
+// launched with programmatic stream serialisation: the next kernel is
+// scheduled while its predecessor drains, and pdl_wait() -- the first
+// statement of each such kernel -- holds it until the predecessor's memory is
+// visible.  Saves the ~1-2 us launch gap per boundary.  TSG_PDL=0 builds
+// plain launches (pdl_wait is then a no-op).
+#ifndef TSG_PDL
+#define TSG_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if TSG_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+#if TSG_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+#else
+    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+#endif
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ unsigned hash_slot(int key, int logT) {

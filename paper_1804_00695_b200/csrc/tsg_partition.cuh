@@ -32,6 +32,7 @@ template <int NB, class F>
 __global__ void __launch_bounds__(256) k_part_bins(int64_t rows, F f, uint8_t *__restrict__ bins,
                                                    int ntiles, int *__restrict__ tc,
                                                    unsigned *__restrict__ done, int64_t *__restrict__ offs) {
+    pdl_wait();
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
     __syncthreads();
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
                                                       const int64_t *__restrict__ extra,
                                                       const int *__restrict__ err,
                                                       int64_t *__restrict__ out, int64_t seq) {
+    pdl_wait();
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
     if (blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
@@ -160,13 +162,16 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_TRY(tsg_alloc_t(c, &out.list, rows > 0 ? rows : 1));
     const bool fused_scan = (int64_t)NB * ntiles <= PART_FUSED_SCAN;
     unsigned *done = fused_scan ? reinterpret_cast<unsigned *>(c->d_small + 60) : nullptr;
-    k_part_bins<NB, F><<<ntiles, 256, 0, c->stream>>>(rows, f, bins, ntiles, tc, done, offs); ++c->launches;
+    TSG_CK(launch_pdl(k_part_bins<NB, F>, ntiles, 256, 0, c->stream, rows, f, bins, ntiles, tc, done, offs));
+    ++c->launches;
     if (!fused_scan) TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, tc, offs, (int64_t)NB * ntiles));
     TSG_TRY(mid());
     // results land in mapped host memory straight from the kernel: no D2H
     // copy that would queue behind bulk transfers on the copy engine
-    k_part_scatter<NB><<<ntiles, 256, 0, c->stream>>>(rows, bins, ntiles, offs, out.list, extra,
-                                                      c->d_err, c->hd_small + 32, ++c->part_seq); ++c->launches;
+    TSG_CK(launch_pdl(k_part_scatter<NB>, ntiles, 256, 0, c->stream, rows, (const uint8_t *)bins, ntiles,
+                      (const int64_t *)offs, out.list, extra, (const int *)c->d_err, c->hd_small + 32,
+                      ++c->part_seq));
+    ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, tc));
     TSG_TRY(tsg_free(c, offs));
