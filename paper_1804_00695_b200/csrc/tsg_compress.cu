@@ -426,6 +426,7 @@ __global__ void k_compress_unit(int64_t rows, int64_t nnz, const int64_t *__rest
                                 const int32_t *__restrict__ col, int64_t *__restrict__ start,
                                 int32_t *__restrict__ cnt, int32_t *__restrict__ oset,
                                 uint64_t *__restrict__ obits) {
+    pdl_wait();
     // max set count: 1 (this path runs only for matrices with entries)
     if (blockIdx.x == 0 && threadIdx.x == 0) cnt[rows + 1] = 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
@@ -450,9 +451,10 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_TRY(tsg_cmat_alloc(c, rows, nnz > 0 ? nnz : 1, &cm));
     cm->cols = b->cols;
     if (b->max_row >= 0 && b->max_row <= 1 && nnz > 0) {
-        k_compress_unit<<<grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-            rows, nnz, b->rp, b->col, cm->start, cm->cnt, cm->set, cm->bits); ++c->launches;
-        TSG_CK(cudaGetLastError());
+        TSG_CK(launch_pdl(k_compress_unit, grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream, rows,
+                          nnz, (const int64_t *)b->rp, (const int32_t *)b->col, cm->start, cm->cnt, cm->set,
+                          cm->bits));
+        ++c->launches;
         cm->sorted_sets = 1;   // one set per row
         cm->dmax_valid = 1;
         cm->identity_rows = (nnz == rows && b->max_row == 1) ? 1 : 0;

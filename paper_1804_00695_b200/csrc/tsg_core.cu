@@ -473,6 +473,7 @@ __global__ void k_put_small(const int64_t *__restrict__ src, int64_t *__restrict
 
 namespace {
 __global__ void k_fill(uint8_t *__restrict__ p, uint32_t word, size_t bytes) {
+    pdl_wait();
     // 16-byte body (p is at least 16-byte aligned for arena blocks; the
     // generic head / tail loops cover any other pointer)
     const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
@@ -498,7 +499,8 @@ int tsg_fill(tsg_ctx *c, void *p, int byte, size_t bytes, cudaStream_t s) {
     if (blocks < 1) blocks = 1;
     const size_t cap = (size_t)c->num_sms * 8;
     if (blocks > cap) blocks = cap;
-    k_fill<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<uint8_t *>(p), word, bytes); ++c->launches;
+    TSG_CK(launch_pdl(k_fill, (unsigned)blocks, 256, 0, s, reinterpret_cast<uint8_t *>(p), word, bytes));
+    ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;
 }

@@ -165,6 +165,7 @@ template <int G>
 __global__ void k_sym_bounds(int64_t rows, const int64_t *__restrict__ arp,
                              const int32_t *__restrict__ acol, const int32_t *__restrict__ cbcnt,
                              const int *maxcb, int64_t *__restrict__ sbound) {
+    pdl_wait();
     const int mcb = *maxcb;
     if (mcb <= CHEAP_CB) return;   // cheap bound len x max: computed by the bin functor (SymBinF)
     const unsigned gm = group_mask<G>();
@@ -2150,10 +2151,10 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
             const unsigned g = grid_for(a->rows, 256, c->num_sms * 16);
             if (!inline_bounds) {
                 switch (pick_g(a->nnz, a->rows)) {
-                case 4: k_sym_bounds<4><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-                case 8: k_sym_bounds<8><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-                case 16: k_sym_bounds<16><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
-                default: k_sym_bounds<32><<<g, 256, 0, c->stream>>>(a->rows, a->rp, a->col, cb->cnt, maxcb, sbound); break;
+                case 4: TSG_CK(launch_pdl(k_sym_bounds<4>, g, 256, 0, c->stream, a->rows, (const int64_t *)a->rp, (const int32_t *)a->col, (const int32_t *)cb->cnt, maxcb, sbound)); break;
+                case 8: TSG_CK(launch_pdl(k_sym_bounds<8>, g, 256, 0, c->stream, a->rows, (const int64_t *)a->rp, (const int32_t *)a->col, (const int32_t *)cb->cnt, maxcb, sbound)); break;
+                case 16: TSG_CK(launch_pdl(k_sym_bounds<16>, g, 256, 0, c->stream, a->rows, (const int64_t *)a->rp, (const int32_t *)a->col, (const int32_t *)cb->cnt, maxcb, sbound)); break;
+                default: TSG_CK(launch_pdl(k_sym_bounds<32>, g, 256, 0, c->stream, a->rows, (const int64_t *)a->rp, (const int32_t *)a->col, (const int32_t *)cb->cnt, maxcb, sbound)); break;
                 }
                 ++c->launches;
             }
