@@ -6,20 +6,32 @@ Workload (N=1): brick3d 27-point stencil on a 128^3 grid (fp64, 26/-1), plain
 RA = R*A then RAP = RA*P with compress -> symbolic -> numeric on the device.
 flops = 2 * (count_multiplications(R, A) + count_multiplications(RA, P)).
 
-N>1 (torchrun, one rank per GPU, NCCL): weak scaling.  The grid grows to
-128 x 128 x 128N; rank r owns the coarse z-slab r, i.e. a contiguous block of
-R's rows (the row partition of A in the north star).  Each rank builds only
-its slab of the fine operator, the B operand (the fine A) is replicated by an
-NCCL all-gather at setup, and every step ends with the row-pointer offset
-exchange (all-gather of per-rank nnz).  No other collective.
+After the timed loop the step's RA and RAP are downloaded once and compared
+with the CPU oracle's full R*A*P (structure bit-exact, values bit-exact or
+within the north star's 1e-12): the line carries ``parity`` and the process
+exits 1 on a mismatch.  At N=1 rank 0 also emits ``secondary`` lines for
+BASELINE.json configs 1, 3 and 4 (bench_configs.py), each with its own parity
+check, so they are driver-observed.
+
+N>1 (one rank per GPU, NCCL): weak scaling.  ``python bench.py --gpus N``
+re-executes itself under torch.distributed.run when WORLD_SIZE is unset.  The
+grid grows to 128 x 128 x 128N; rank r owns the coarse z-slab r, i.e. a
+contiguous block of R's rows (the row partition of A in the north star).  Each
+rank builds only its slab of the fine operator, the B operand (the fine A) is
+replicated by an NCCL all-gather at setup (or read from peer HBM with
+``--b-mode sharded``), and every step ends with the row-pointer offset
+exchange (all-gather of per-rank nnz) on libtsg's compute stream, inside the
+event-timed region.  ``--config 5`` runs the R-MAT A*A strong-scaling arm
+(bench_configs.config5 / distributed.mg_multiply).
 
 Output: one JSON line (rank 0) with value / e2e / roofline / cpu_baseline /
-clocks / gpu_launches, as the driver's contract asks.
+clocks / gpu_launches / parity, as the driver's contract asks.
 """
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -51,7 +63,7 @@ def build_problem(world, rank, base=128):
     """Fine operator rows of this rank's slab (+ the full fine grid shape),
     R rows for this rank's coarse slab, and P (fine -> coarse)."""
     from paper_1804_00695_b200 import generators as gen
-    from paper_1804_00695_b200.csr import CsrMatrix, transpose
+    from paper_1804_00695_b200.csr import CsrMatrix
     nz = base * world
     dims = (base, base, nz)
     a = gen.stencil(gen.BRICK3D, dims) if world == 1 else None
@@ -73,6 +85,20 @@ def build_problem(world, rank, base=128):
 
 def sizes_ref(rows, nnz):
     return 8 * (rows + 1) + 16 * nnz
+
+
+def sizes_dev(rows, nnz):
+    return 8 * (rows + 1) + 12 * nnz
+
+
+def config2_desc(dims, world, mults, nnz):
+    """The config object both arms print (identical, so the driver can match
+    them): workload, grid, multiplications and operand sizes."""
+    return {"workload": "config2 R*A*P brick3d %dx%dx%d + 2x2x2 aggregation" % tuple(dims),
+            "grid": list(dims), "multiplications": int(mults),
+            "nnz": {k: int(v) for k, v in nnz.items()},
+            "parallelism": ("row partition of R (coarse z-slabs) x%d" % world) if world > 1
+            else "single GPU"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -140,9 +166,11 @@ class ClockSampler:
                 "samples_in_timed_region": len(inside)}
 
 
-# ------------------------------------------------------------------ reference arm
+# ------------------------------------------------------------------ CPU side (checker + baseline)
 
 def cpu_rap(r, a, p, workers):
+    """The oracle's R*A*P (the reference's algorithm restated in C): seconds,
+    RA (CsrMatrix, first-touch column order), RAP (ptr, col, val)."""
     from oracle import oracle as O
     from paper_1804_00695_b200.csr import CsrMatrix
     t0 = time.perf_counter()
@@ -153,41 +181,72 @@ def cpu_rap(r, a, p, workers):
     return dt, ra_m, rap
 
 
-def flops_of(r, a, ra_rows, ra_nnz, p):
-    from oracle import oracle as O
-    m1 = O.count_multiplications(r, a)
-    m2 = ra_nnz  # P has exactly one entry per row: mults(RA, P) = nnz(RA)
-    return 2 * (m1 + m2), m1, m2
-
-
 def run_reference(args, world, rank):
+    """--impl reference: the reference's algorithm on the host cores (the
+    oracle port over all threads), same config / metric / unit as our arm.
+    Under torchrun only rank 0 works."""
     if rank != 0:
         return
-    dims, a, r, p = build_problem(1, 0)
+    from oracle import oracle as O
+    dims, a, r, p = build_problem(1, 0, args.base)
     workers = os.cpu_count() or 1
     times = []
-    ra = None
+    ra = rap = None
     for i in range(args.warmup + args.steps):
-        dt, ra, _ = cpu_rap(r, a, p, workers)
+        dt, ra, rap = cpu_rap(r, a, p, workers)
         if i >= args.warmup:
             times.append(dt)
-    fl, m1, m2 = flops_of(r, a, ra.num_rows, ra.nnz, p)
+    m1 = O.count_multiplications(r, a)
+    m2 = ra.nnz   # P has exactly one entry per row: mults(RA, P) = nnz(RA)
+    fl = 2 * (m1 + m2)
     sec = statistics.median(times)
     val = fl / sec / 1e9
+    dt1, _, _ = cpu_rap(r, a, p, 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "config2 R*A*P brick3d 128^3 + 2x2x2 aggregation",
-                   "grid": list(dims), "multiplications": m1 + m2},
+        "config": config2_desc(dims, 1, m1 + m2, {"A": a.nnz, "R": r.nnz, "RA": ra.nnz,
+                                                  "RAP": len(rap[1])}),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
+                         "w1_value": fl / dt1 / 1e9, "nproc": os.cpu_count(),
                          "sample": "full config-2 R*A*P per step (oracle/tsg_oracle.c, pthreads "
-                                   "over row blocks, the reference's algorithm restated in C; the "
-                                   "Python reference is GIL-bound at ~1.3 MFLOP/s)"},
+                                   "over row blocks, the reference's algorithm restated in C); "
+                                   "w1_value = the same with 1 thread.  The Python reference is "
+                                   "GIL-bound at ~1.3 MFLOP/s (BASELINE.md §2)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ launcher
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_spawn(args):
+    """`bench.py --gpus N` without torchrun: re-execute under
+    torch.distributed.run with N ranks (one per GPU) and return its exit code.
+    Returns None when no spawn is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": "--gpus %d but only %d CUDA device(s) visible" % (args.gpus, have)}),
+                  flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ our arm
@@ -200,50 +259,77 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the config 1 / 3 / 4 secondary lines of the default N=1 run")
     ap.add_argument("--phases", action="store_true", help="print per-phase device times and exit")
     ap.add_argument("--base", type=int, default=128,
                     help="config 2 fine grid edge per GPU (BASELINE config 2: 128)")
     ap.add_argument("--b-mode", default="replicated", choices=["replicated", "sharded"],
                     help="N>1: B all-gathered once (replicated) or kept as row shards read "
-                         "from peer HBM through CUDA IPC (sharded, SURVEY.md §8e)")
+                         "from peer HBM (sharded, SURVEY.md §8e)")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off)")
     ap.add_argument("--config", type=int, default=2,
-                    help="BASELINE.json config (2 = the driver's bench line; 1, 3, 4 = secondary)")
-    ap.add_argument("--scale", type=int, default=22, help="R-MAT scale for --config 3")
+                    help="BASELINE.json config (2 = the driver's bench line; 1, 3, 4, 5 = secondary)")
+    ap.add_argument("--scale", type=int, default=22, help="R-MAT scale for --config 3 / 5")
     ap.add_argument("--grid", type=int, default=256, help="brick grid edge for --config 4")
     ap.add_argument("--hbm-cap-gib", type=float, default=8.0, help="HBM budget for --config 4")
+    ap.add_argument("--c-budget-gib", type=float, default=48.0,
+                    help="--config 5: HBM for one chunk of C (streamed-C mode above it)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
 
     if args.impl == "reference":
+        if world == 1 and args.gpus > 1:
+            world = args.gpus   # bare --gpus N: the host run stands for all N
         run_reference(args, world, rank)
         if dist:
             dist.destroy_process_group()
         return
     if args.config != 2:
         import bench_configs
-        print(json.dumps(bench_configs.run(args)), flush=True)
+        line = bench_configs.run(args, dist=dist)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        if line.get("parity", {}).get("ok") is False:
+            sys.exit(1)
         return
+    ok = run_config2(args, world, rank, local, dist)
+    if dist:
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
 
+
+def run_config2(args, world, rank, local, dist):
     import torch
     from paper_1804_00695_b200 import _lib, kernel
-    from paper_1804_00695_b200.csr import CsrMatrix
 
     torch.cuda.set_device(local)
     ctx = _lib.Context.get(local)
     ctx.set_timing(True)
+    tsg_stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
 
     dims, a_loc, r, p = build_problem(world, rank, args.base)
     dr = _lib.DeviceCsr.upload(r, ctx)
@@ -251,23 +337,26 @@ def main():
     setup = {}
     if world == 1:
         da = _lib.DeviceCsr.upload(a_loc, ctx)
-        a_rows, a_nnz = a_loc.num_rows, a_loc.nnz
     elif args.b_mode == "sharded":
         da, setup = sharded_b(ctx, a_loc, dr, dims, world, rank, torch, dist)
-        a_rows, a_nnz = da.num_rows, da.nnz
     else:
         da, setup = replicate_b(ctx, a_loc, dims, world, rank, torch, dist)
-        a_rows, a_nnz = da.num_rows, da.nnz
+    a_rows, a_nnz = da.num_rows, da.nnz
 
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
 
     def step():
-        # the R*A numeric phase is the roofline kernel: remember its call id in
-        # libtsg's event ring and read its time after the step (no sync inside)
+        # events: 0 step start, 4 between the two multiplies, 1 step end (after
+        # the offset exchange).  The R*A numeric phase is the roofline kernel:
+        # remember its call id in libtsg's event ring (no sync inside a step)
         ctx.record(0)
         call = ctx.numeric_calls()
         dra = kernel.multiply_device(dr, da)
+        ctx.record(4)
         drap = kernel.multiply_device(dra, dp)
+        if dist:
+            with torch.cuda.stream(tsg_stream):
+                exchange_offsets(drap.nnz, dist)
         ctx.record(1)
         return dra, drap, call
 
@@ -280,28 +369,10 @@ def main():
         dra, drap, _ = step()
         ctx.sync()
         torch.cuda.profiler.stop()
-        return
+        return True
     if args.phases:
-        for _ in range(4):
-            ctx.record(0)
-            h0 = time.perf_counter()
-            res0 = ctx.pool_reserved()
-            dra = kernel.multiply_device(dr, da)
-            h1 = time.perf_counter()
-            ph1, st1 = ctx.phase_ms(), ctx.stats()
-            drap = kernel.multiply_device(dra, dp)
-            ph2, st2 = ctx.phase_ms(), ctx.stats()
-            ctx.record(1)
-            h2 = time.perf_counter()
-            print(json.dumps({"step_ms": ctx.elapsed_ms(0, 1), "host_ms": [1e3 * (h1 - h0), 1e3 * (h2 - h1)],
-                              "pool_reserved_mb": [res0 >> 20, ctx.pool_reserved() >> 20],
-                              "RA": {"compress": ph1[0], "symbolic": ph1[1], "scan": ph1[2],
-                                     "numeric": ph1[3], "total": ph1[5],
-                                     "sym_kernels": st1[1], "num_kernels": st1[2]},
-                              "RAP": {"compress": ph2[0], "symbolic": ph2[1], "scan": ph2[2],
-                                      "numeric": ph2[3], "total": ph2[5],
-                                      "sym_kernels": st2[1], "num_kernels": st2[2]}}))
-        return
+        print_phases(ctx, kernel, dr, da, dp)
+        return True
     ra_rows, ra_nnz, rap_nnz = dra.num_rows, dra.nnz, drap.nnz
     m1 = _lib.d_count_multiplications(dr, da)
     m2 = _lib.d_count_multiplications(dra, dp)
@@ -316,15 +387,14 @@ def main():
     sampler.start()
     sampler.mark("t_begin")
     l0 = ctx.stats()[0]
-    times, num_times = [], []
-    offs = None
+    times, ra_times, rap_times, num_times = [], [], [], []
     for _ in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
         dra, drap, call = step()
-        if dist:
-            offs = exchange_offsets(drap.nnz, torch, dist, world)
         times.append(ctx.elapsed_ms(0, 1))
+        ra_times.append(ctx.elapsed_ms(0, 4))
+        rap_times.append(ctx.elapsed_ms(4, 1))
         num_times.append(ctx.numeric_ms(call))
         del dra, drap
     l1 = ctx.stats()[0]
@@ -348,61 +418,125 @@ def main():
     ms_step = tot_ms / args.steps
     value = flops_all / (ms_step * 1e-3) / 1e9
 
-    # roofline: numeric kernel(s) of R*A, algorithmic bytes in the reference's
-    # byte convention (8 B offsets / indices / values): size(R)+size(A)+size(RA)
+    # roofline of the dominant kernel: numeric kernels of R*A, algorithmic
+    # bytes in the reference's byte convention (8 B offsets / indices /
+    # values): size(R) + size(A) + size(RA)
     hbm, peak_kind = peaks()
-    alg_bytes = sizes_ref(r.num_rows, r.nnz) + sizes_ref(a_rows, a_nnz) + sizes_ref(ra_rows, ra_nnz)
-    dev_bytes = (8 * (r.num_rows + 1) + 12 * r.nnz) + (8 * (a_rows + 1) + 12 * a_nnz) + \
-        (8 * (ra_rows + 1) + 12 * ra_nnz)
+    alg_ra = sizes_ref(r.num_rows, r.nnz) + sizes_ref(a_rows, a_nnz) + sizes_ref(ra_rows, ra_nnz)
+    dev_ra = sizes_dev(r.num_rows, r.nnz) + sizes_dev(a_rows, a_nnz) + sizes_dev(ra_rows, ra_nnz)
+    alg_rap = sizes_ref(ra_rows, ra_nnz) + sizes_ref(p.num_rows, p.nnz) + sizes_ref(ra_rows, rap_nnz)
     num_ms = statistics.median(num_times)
-    achieved = alg_bytes / (num_ms * 1e-3) / 1e9
+    achieved = alg_ra / (num_ms * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
             traffic = int(json.load(fh)["traffic_bytes_per_launch"])
     except Exception:
         pass
+    ra_ms, rap_ms = statistics.median(ra_times), statistics.median(rap_times)
+    whole = {
+        "definition": "SURVEY.md §8(d): compress -> symbolic -> scan -> numeric of each multiply, "
+                      "reference-convention bytes size(A)+size(B)+size(C) / event-timed device time",
+        "RA_multiply": {"ms": ra_ms, "bytes": alg_ra, "frac": alg_ra / (ra_ms * 1e-3) / 1e9 / hbm},
+        "RAP_multiply": {"ms": rap_ms, "bytes": alg_rap, "frac": alg_rap / (rap_ms * 1e-3) / 1e9 / hbm},
+        "step": {"ms": ms_step, "bytes": alg_ra + alg_rap,
+                 "frac": (alg_ra + alg_rap) / (ms_step * 1e-3) / 1e9 / hbm},
+    }
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic,
             "kernel": "k_num_group (numeric phase of R*A, all bins)",
-            "peak_kind": peak_kind, "algorithmic_bytes": alg_bytes,
-            "device_layout_bytes": dev_bytes, "kernel_ms": num_ms,
+            "peak_kind": peak_kind, "algorithmic_bytes": alg_ra,
+            "device_layout_bytes": dev_ra, "device_layout_frac": dev_ra / (num_ms * 1e-3) / 1e9 / hbm,
+            "kernel_ms": num_ms, "whole_multiply": whole,
             "note": "traffic = dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch "
                     "from one ncu --set full capture (profiles/r02_traffic.json)"}
-    whole_bytes_ms = tot_ms / args.steps
 
+    nnz = {"A": a_nnz, "R": r.nnz, "RA": ra_nnz, "RAP": rap_nnz}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2 R*A*P brick3d %dx%dx%d + 2x2x2 aggregation" % dims,
-                   "grid": list(dims), "multiplications_per_rank": m1 + m2,
-                   "nnz": {"A": a_nnz, "R": r.nnz, "RA": ra_nnz, "RAP": rap_nnz},
-                   "parallelism": "row partition of R (coarse z-slabs) x%d, B %s" % (world, args.b_mode)
-                   if world > 1 else "single GPU",
-                   "l2": "A (>0.7 GB) and RA (>0.2 GB) exceed L2; 252 MiB flush between steps",
-                   "timing": "CUDA events on libtsg's compute stream, max over ranks"},
+        "config": config2_desc(dims, world, m1 + m2, nnz),
+        "notes": {"l2": "A (>0.7 GB) and RA (>0.2 GB) exceed L2; 252 MiB flush between steps",
+                  "timing": "CUDA events on libtsg's compute stream, max over ranks; N>1 includes "
+                            "the offset all-gather on that stream",
+                  "b_mode": args.b_mode if world > 1 else None},
         "roofline": roof,
         "clocks": clocks,
         "gpu_launches": int(l1 - l0),
         "setup": setup,
     }
+
+    # ---- parity: this step's RA and RAP against the oracle's full product
+    ok = True
+    cpu = None
+    if not args.no_parity:
+        import bench_configs as BC
+        dra, drap, _ = step()
+        ctx.sync()
+        ra_got, rap_got = dra.download(), drap.download()
+        del dra, drap
+        a_full = a_loc if world == 1 else BC.embed_rows(a_loc, dims, rank, args.base)
+        dt, ra_o, rap_o = cpu_rap(r, a_full, p, os.cpu_count() or 1)
+        cpu = dt
+        par_ra = BC.compare_products(ra_got, (ra_o.row_ptr, ra_o.col_idx, ra_o.values))
+        par_rap = BC.compare_products(rap_got, rap_o)
+        ok = par_ra["ok"] and par_rap["ok"]
+        par = {"ok": ok, "exact": par_ra["exact"] and par_rap["exact"], "RA": par_ra, "RAP": par_rap,
+               "oracle": "oracle/tsg_oracle.c full R*A*P (the reference's algorithm; pinned to the "
+                         "reference's outputs by tests/test_oracle.py)",
+               "rule": "row pointers + per-row sorted columns bit-exact; values bit-exact or "
+                       "rel <= 1e-12 (abs <= 1e-250)"}
+        if dist:
+            t = torch.tensor([1.0 if ok else 0.0, 1.0 if par["exact"] else 0.0], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            par["all_ranks_ok"], par["all_ranks_exact"] = bool(t[0].item()), bool(t[1].item())
+            ok = par["all_ranks_ok"]
+        line["parity"] = par
+
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(ctx, r, a_loc, p, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, ra_c, _ = cpu_rap(r, a_loc, p, os.cpu_count() or 1)
+        if cpu is None:
+            cpu, _, _ = cpu_rap(r, a_loc, p, os.cpu_count() or 1)
+        cpu1, _, _ = cpu_rap(r, a_loc, p, 1)
         line["cpu_baseline"] = {
-            "value": flops_rank / dt / 1e9, "unit": UNIT, "cores": os.cpu_count() or 1,
-            "kind": "port",
+            "value": flops_rank / cpu / 1e9, "unit": UNIT, "cores": os.cpu_count() or 1,
+            "kind": "port", "w1_value": flops_rank / cpu1 / 1e9, "nproc": os.cpu_count(),
             "sample": "one full config-2 R*A*P on the host (oracle/tsg_oracle.c with %d pthreads; "
-                      "the reference's algorithm restated in C)" % (os.cpu_count() or 1)}
+                      "the reference's algorithm restated in C); w1_value = 1 thread"
+                      % (os.cpu_count() or 1)}
+    if rank == 0 and world == 1 and not args.no_secondary:
+        import bench_configs as BC
+        line["secondary"] = BC.secondary(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    return ok
 
 
-def exchange_offsets(local_nnz, torch, dist, world):
+def print_phases(ctx, kernel, dr, da, dp):
+    for _ in range(4):
+        ctx.record(0)
+        h0 = time.perf_counter()
+        res0 = ctx.pool_reserved()
+        dra = kernel.multiply_device(dr, da)
+        h1 = time.perf_counter()
+        ph1, st1 = ctx.phase_ms(), ctx.stats()
+        drap = kernel.multiply_device(dra, dp)
+        ph2, st2 = ctx.phase_ms(), ctx.stats()
+        ctx.record(1)
+        h2 = time.perf_counter()
+        print(json.dumps({"step_ms": ctx.elapsed_ms(0, 1), "host_ms": [1e3 * (h1 - h0), 1e3 * (h2 - h1)],
+                          "pool_reserved_mb": [res0 >> 20, ctx.pool_reserved() >> 20],
+                          "RA": {"compress": ph1[0], "symbolic": ph1[1], "scan": ph1[2],
+                                 "numeric": ph1[3], "total": ph1[5],
+                                 "sym_kernels": st1[1], "num_kernels": st1[2]},
+                          "RAP": {"compress": ph2[0], "symbolic": ph2[1], "scan": ph2[2],
+                                  "numeric": ph2[3], "total": ph2[5],
+                                  "sym_kernels": st2[1], "num_kernels": st2[2]}}))
+
+
+def exchange_offsets(local_nnz, dist):
     """Row-pointer offset exchange: all-gather of per-rank nnz(C slice)."""
     from paper_1804_00695_b200 import distributed as D
     return D.exchange_offsets(local_nnz, dist, "cuda")
@@ -445,8 +579,8 @@ def sharded_b(ctx, a_loc, dr, dims, world, rank, torch, dist):
 
 def run_e2e(ctx, r, a, p, args):
     """Same metric through the public drop-in API (kernel.multiply) with host
-    CsrMatrix operands in pinned memory: every step uploads R, A, then RA and
-    P, downloads RA and RAP (fresh host wrappers defeat the residency cache)."""
+    CsrMatrix operands in pinned memory: every step uploads R, A, then P,
+    downloads RA and RAP (fresh host wrappers defeat the residency cache)."""
     import torch
     from paper_1804_00695_b200 import kernel
     from paper_1804_00695_b200.csr import CsrMatrix

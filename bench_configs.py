@@ -1,8 +1,17 @@
-"""Secondary benchmark lines for BASELINE.json configs 1, 3 and 4 (the
-driver's line is config 2, bench.py).  Same JSON keys; each line is measured
-on the device with CUDA events on libtsg's stream (configs 1, 3) or by the
-chunked executor's own stream-ordered accounting (config 4)."""
+"""Secondary benchmark lines for BASELINE.json configs 1, 3, 4 and 5 (the
+driver's line is config 2, bench.py), each with its own parity check.
 
+Every line carries ``parity`` ({"ok": ...}); ``secondary()`` runs configs 1,
+3 and 4 inside the default bench.py run so they are driver-observed.  Device
+times are CUDA events on libtsg's compute stream (configs 1, 3, 5) or the
+chunked executor's own stream-ordered accounting (config 4).
+
+The oracle (oracle/, the reference's algorithm restated in C and pinned to
+the reference's outputs) is used here only as the checker and as the CPU
+baseline, never on the measured path.
+"""
+
+import argparse
 import json
 import os
 import statistics
@@ -10,44 +19,143 @@ import time
 
 import numpy as np
 
+ROOT = os.path.dirname(os.path.abspath(__file__))
 UNIT = "GFLOP/s"
 
 
 def _peaks():
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"])
     except Exception:
         return 6650.0
 
 
-def config1(args):
-    """A*A, 2D 5-point Laplacian 256^2 (65,536 rows), in HBM."""
-    from paper_1804_00695_b200 import _lib, generators as gen, kernel
+# ------------------------------------------------------------------ parity helpers
+
+def _row_ids(ptr):
+    ptr = np.asarray(ptr, dtype=np.int64)
+    return np.repeat(np.arange(ptr.shape[0] - 1, dtype=np.int64), np.diff(ptr))
+
+
+def _canon(ptr, col, val, ncols):
+    """Per-row ascending columns (the reference's canonicalize, csr.py:145-150)."""
+    col = np.asarray(col, dtype=np.int64)
+    key = _row_ids(ptr) * max(int(ncols), 1) + col
+    if key.shape[0] < 2 or bool(np.all(key[1:] > key[:-1])):
+        return col, None if val is None else np.asarray(val)
+    order = np.argsort(key, kind="stable")
+    return col[order], None if val is None else np.asarray(val)[order]
+
+
+def compare_products(got, want, rtol=1e-12):
+    """got: CsrMatrix (ours); want: (ptr, col, val) from the oracle, any row
+    order.  Structure must be bit-exact (row pointers, per-row sorted
+    columns); values bit-exact (``exact``) or within the north star's
+    rel 1e-12 / abs 1e-250 (csr.py:165-184 products_match)."""
+    ptr, col, val = want
+    out = {"nnz": int(got.nnz), "structure": False, "exact": False, "ok": False, "max_rel": None}
+    if not np.array_equal(np.asarray(got.row_ptr), np.asarray(ptr, dtype=np.int64)):
+        return out
+    gc, gv = _canon(got.row_ptr, got.col_idx, got.values, got.num_cols)
+    wc, wv = _canon(ptr, col, val, got.num_cols)
+    if not np.array_equal(gc, wc):
+        return out
+    out["structure"] = True
+    if gv is None and wv is None:
+        out.update(exact=True, ok=True, max_rel=0.0)
+        return out
+    gv, wv = np.asarray(gv, dtype=np.float64), np.asarray(wv, dtype=np.float64)
+    out["exact"] = bool(np.array_equal(gv.view(np.uint64), wv.view(np.uint64)))
+    d = np.abs(gv - wv)
+    mag = np.maximum(np.abs(gv), np.abs(wv))
+    rel = np.where(mag > 0, d / np.where(mag > 0, mag, 1.0), 0.0)
+    out["max_rel"] = float(rel.max()) if rel.size else 0.0
+    out["ok"] = bool(np.all((d <= rtol * mag) | (d <= 1e-250)))
+    return out
+
+
+def embed_rows(a_loc, dims, rank, base):
+    """A full-height matrix holding only rank's slab rows of the fine
+    operator (N>1 config 2): the oracle's B operand for that rank."""
+    from paper_1804_00695_b200.csr import CsrMatrix
+    n = int(np.prod(dims))
+    plane = base * base
+    lo, hi = rank * base * plane, (rank + 1) * base * plane
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[lo + 1:hi + 1] = a_loc.row_ptr[1:]
+    rp[hi + 1:] = a_loc.nnz
+    return CsrMatrix._adopt(n, a_loc.num_cols, rp, a_loc.col_idx, a_loc.values)
+
+
+def _sampled_rows_check(get_row, a, b, rows):
+    """Rows of C = A*B against the oracle on single-row slices (rows of C are
+    independent, kernel.py:11-14): all exact / ok."""
     from oracle import oracle as O
+    from paper_1804_00695_b200.csr import slice_rows
+    exact = ok = True
+    for r in rows:
+        ptr, col, val = O.multiply(slice_rows(a, int(r), int(r) + 1), b)
+        got = get_row(int(r))
+        res = compare_products(got, (ptr, col, val))
+        exact &= res["exact"]
+        ok &= res["ok"]
+    return {"ok": bool(ok), "exact": bool(exact), "rows_checked": len(rows)}
+
+
+# ------------------------------------------------------------------ config 1
+
+def config1(args):
+    """A*A, 2D 5-point Laplacian 256^2 (65,536 rows), in HBM; full parity."""
+    from oracle import oracle as O
+    from paper_1804_00695_b200 import _lib, generators as gen, kernel
     ctx = _lib.Context.get(0)
     ctx.set_timing(True)
     a = gen.stencil(gen.LAPLACE2D, (256, 256))
     da = _lib.DeviceCsr.upload(a, ctx)
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         kernel.multiply_device(da, da)
     times = []
+    l0 = ctx.stats()[0]
     for _ in range(args.steps):
         ctx.record(0)
         dc = kernel.multiply_device(da, da)
         ctx.record(1)
         times.append(ctx.elapsed_ms(0, 1))
+    launches = (ctx.stats()[0] - l0) / max(args.steps, 1)
     mults = O.count_multiplications(a, a)
     ms = statistics.median(times)
     t0 = time.perf_counter()
-    O.multiply(a, a, workers=os.cpu_count() or 1)
+    want = O.multiply(a, a, workers=os.cpu_count() or 1)
     cpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.multiply(a, a, workers=1)
+    cpu1 = time.perf_counter() - t0
+    par = compare_products(dc.download(), want)
+    byts = 2 * (8 * (a.num_rows + 1) + 16 * a.nnz) + 8 * (a.num_rows + 1) + 16 * dc.nnz
     return {"metric": "SpGEMM GFLOP/s config 1 (A*A laplace2d 256^2)", "value": 2 * mults / ms / 1e6,
-            "unit": UNIT, "ms_per_step": ms, "dtype": "f64", "data": "synthetic",
+            "unit": UNIT, "ms_per_step": ms, "steps": args.steps, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config1 A*A 2D 5-pt 256^2", "multiplications": mults,
-                       "nnz_c": dc.nnz, "launch_bound": "C is 14 MB; one multiply is ~20 launches"},
+                       "nnz_c": dc.nnz, "launches_per_multiply": launches},
+            "roofline": {"bound": "hbm", "algorithmic_bytes": byts,
+                         "frac": byts / (ms * 1e-3) / 1e9 / _peaks(),
+                         "note": "launch/latency-bound: 25.6 MB per multiply is ~4 us of HBM time"},
+            "parity": par,
             "cpu_baseline": {"value": 2 * mults / cpu / 1e9, "unit": UNIT, "cores": os.cpu_count(),
-                             "kind": "port", "sample": "full A*A"}}
+                             "w1_value": 2 * mults / cpu1 / 1e9,
+                             "kind": "port", "sample": "full A*A (oracle/tsg_oracle.c)"}}
+
+
+# ------------------------------------------------------------------ config 3
+
+def rmat_golden(scale):
+    """Golden triangle count of the config-3 graph at `scale` (tests/golden/
+    rmat_triangles.json, made by tests/golden/make_rmat_triangles.py)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "rmat_triangles.json")) as fh:
+            return json.load(fh).get(str(scale))
+    except Exception:
+        return None
 
 
 def config3(args):
@@ -55,10 +163,11 @@ def config3(args):
 
     The whole pipeline runs in HBM: R-MAT build,
     validation + degree order + lower triangle, then per step compress(L) +
-    masked count.  The host oracle re-counts the downloaded L."""
+    masked count.  Parity: the golden count of the same graph (oracle, full
+    graph, tests/golden/rmat_triangles.json) and nnz(L)."""
+    from oracle import oracle as O
     from paper_1804_00695_b200 import _lib, generators as gen
     from paper_1804_00695_b200.triangles import lower_triangle_device
-    from oracle import oracle as O
     ctx = _lib.Context.get(0)
     ctx.set_timing(True)
     gen.rmat_graph_device(10)                       # warm the CUB kernels
@@ -72,7 +181,7 @@ def config3(args):
     gen_ms, prep_ms = ctx.elapsed_ms(2, 3), ctx.elapsed_ms(3, 4)
     n, g_nnz = dg.num_rows, dg.nnz
     del dg
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         tri = _lib.d_masked_count(dl, _lib.d_compress(dl))
     times = []
     for _ in range(args.steps):
@@ -82,68 +191,81 @@ def config3(args):
         ctx.record(1)
         times.append(ctx.elapsed_ms(0, 1))
     ms = statistics.median(times)
-    low = dl.download()
-    mults = O.count_multiplications(low, low)
+    mults = _lib.d_count_multiplications(dl, dl)
+    gold = rmat_golden(args.scale)
+    par = {"ok": None, "exact": None, "triangles": tri}
+    if gold is not None:
+        same = tri == gold["triangles"] and dl.nnz == gold["nnz_L"] and mults == gold["mults_LL"]
+        par.update(ok=bool(same), exact=bool(same), golden_triangles=gold["triangles"],
+                   source="tests/golden/rmat_triangles.json (oracle masked count of the full graph)")
     line = {"metric": "triangle counting GFLOP/s config 3 (2 x mults(L,L) / time)",
-            "value": 2 * mults / ms / 1e6, "unit": UNIT, "ms_per_step": ms, "dtype": "int64",
-            "data": "synthetic", "triangles": tri,
+            "value": 2 * mults / ms / 1e6, "unit": UNIT, "ms_per_step": ms, "steps": args.steps,
+            "dtype": "int64", "data": "synthetic", "triangles": tri,
             "config": {"workload": "config3 R-MAT scale %d ef16 (.57,.19,.19,.05) SplitMix64 seed 22"
-                       % args.scale, "n": n, "nnz_graph": g_nnz, "nnz_L": low.nnz, "mults_LL": mults,
+                       % args.scale, "n": n, "nnz_graph": g_nnz, "nnz_L": dl.nnz, "mults_LL": mults,
                        "device_rmat_build_ms": gen_ms, "device_lower_triangle_ms": prep_ms,
-                       "pipeline_ms": gen_ms + prep_ms + ms}}
+                       "pipeline_ms": gen_ms + prep_ms + ms},
+            "parity": par}
     if not args.no_cpu_baseline:
+        # the oracle on the full graph of a smaller scale of the same family
+        # (the scale-22 count is ~90 s of host time)
+        cs = min(args.scale, 18)
+        low = dl.download() if cs == args.scale else \
+            lower_triangle_device(gen.rmat_graph_device(cs), check=False)[0].download()
+        cm = int(np.diff(low.row_ptr)[low.col_idx].sum())
         t0 = time.perf_counter()
-        want = O.masked_count(low, O.compress(low), workers=os.cpu_count() or 1)
+        O.masked_count(low, O.compress(low), workers=os.cpu_count() or 1)
         cpu = time.perf_counter() - t0
-        line.update({"oracle_triangles": want, "exact": tri == want,
-                     "cpu_baseline": {"value": 2 * mults / cpu / 1e9, "unit": UNIT,
-                                      "cores": os.cpu_count(), "kind": "port",
-                                      "sample": "full masked count on the host"}})
+        line["cpu_baseline"] = {"value": 2 * cm / cpu / 1e9, "unit": UNIT, "cores": os.cpu_count(),
+                                "kind": "port",
+                                "sample": "compress + masked count of the full R-MAT scale-%d graph "
+                                          "(same generator) with the oracle" % cs}
     return line
 
 
+# ------------------------------------------------------------------ config 4
+
 def config4(args):
     """Chunked out-of-HBM A*A, brick3d N^3 (default 256^3), HBM budget capped
-    (default 8 GiB), A and C in pinned host memory, the Alg. 4 plan."""
-    import paper_1804_00695_b200 as tsg
-    from paper_1804_00695_b200 import _lib, chunking as ch, generators as gen
-    from paper_1804_00695_b200.csr import CsrMatrix, slice_rows
-    from paper_1804_00695_b200.memory import b200_model
+    (default 8 GiB), A and C in pinned host memory, the Alg. 4 plan.  A is
+    built on the device and downloaded into pinned memory (the host builder
+    takes ~25 s); parity on sampled rows, incl. every chunk boundary row."""
     from oracle import oracle as O
+    from paper_1804_00695_b200 import _lib, chunking as ch, generators as gen
+    from paper_1804_00695_b200.csr import slice_rows
+    from paper_1804_00695_b200.memory import b200_model
     n = args.grid
     t0 = time.perf_counter()
-    a0 = gen.stencil(gen.BRICK3D, (n, n, n))
-
-    def pin(x, dt):
-        y = _lib.pinned_empty(len(x), dt)
-        y[:] = x
-        return y
-    a = CsrMatrix._adopt(a0.num_rows, a0.num_cols, pin(a0.row_ptr, np.int64),
-                         pin(a0.col_idx, np.int64), pin(a0.values, np.float64))
-    del a0
-    gen_s = time.perf_counter() - t0
+    ctx = _lib.Context.get(0)
+    da = gen.stencil_device(gen.BRICK3D, (n, n, n))
+    a = da.download()                                # pinned host arrays
     # symbolic counts once on the device (the reference computes them unchunked
     # and unbilled, cli.py:164-165); not part of the timed chunked run
-    ctx = _lib.Context.get(0)
-    da = _lib.DeviceCsr.upload(a, ctx)
     counts = _lib.d_symbolic(da, _lib.d_compress(da)).download()
     del da
+    ctx.sync()
+    gen_s = time.perf_counter() - t0
     fast = int(args.hbm_cap_gib * 2**30)
     plan = ch.plan_for_multiply(a, a, counts, fast)
     model = b200_model(fast)
     c, led = ch.execute_plan(a, a, counts, plan, model)
     ph = led.physical
     mults = int(np.diff(a.row_ptr)[a.col_idx].sum())
-    # correctness: sampled rows against the oracle (rows are independent)
-    rs = np.random.default_rng(0).choice(a.num_rows, size=64, replace=False)
-    ok = True
-    for r in rs[:16]:
-        sub = slice_rows(a, int(r), int(r) + 1)
-        ptr, col, val = O.multiply(sub, a)
+    # parity: random rows + the first/last row of every planned range
+    rng = np.random.default_rng(0)
+    rows = set(int(x) for x in rng.choice(a.num_rows, size=24, replace=False))
+    for part in (plan.partition_ac, plan.partition_b):
+        for r in part.ranges:
+            rows.update({r.begin, max(r.begin, r.end - 1)})
+    rows = sorted(x for x in rows if x < a.num_rows)
+
+    def row_of(r):
+        from paper_1804_00695_b200.csr import CsrMatrix
         lo, hi = int(c.row_ptr[r]), int(c.row_ptr[r + 1])
-        order = np.argsort(col)
-        ok &= bool(np.array_equal(c.col_idx[lo:hi], col[order]) and
-                   np.array_equal(c.values[lo:hi], val[order]))
+        return CsrMatrix._adopt(1, c.num_cols, np.array([0, hi - lo]), c.col_idx[lo:hi], c.values[lo:hi])
+    par = _sampled_rows_check(row_of, a, a, rows)
+    par["nnz_C_exact"] = bool(c.nnz == int(np.sum(counts)))
+    par["ok"] = par["ok"] and par["nnz_C_exact"]
     # CPU rate on a row sample (extrapolated)
     sample = slice_rows(a, 0, 65536)
     t1 = time.perf_counter()
@@ -156,18 +278,22 @@ def config4(args):
             "value": 2 * mults / secs / 1e9, "unit": UNIT, "dtype": "f64", "data": "synthetic",
             "host_link": {"achieved_gbs": ph["link_gbs"], "h2d_bytes": ph["h2d_bytes"],
                           "d2h_bytes": ph["d2h_bytes"], "wall_s": secs,
-                          "kernel_s": ph["kernel_ms"] / 1e3},
+                          "kernel_s": ph["kernel_ms"] / 1e3,
+                          "peak_device_bytes": ph.get("peak_device_bytes"),
+                          "hbm_cap_bytes": fast},
             "plan": {"algorithm": plan.algorithm, "branch": plan.heuristic_branch,
                      "n_ac": len(plan.partition_ac), "n_b": len(plan.partition_b),
                      "ledger_bytes": led.total_bytes(),
                      "predicted_copy_bytes": plan.predicted_copy_bytes},
             "config": {"workload": "config4", "rows": a.num_rows, "nnz_A": a.nnz, "nnz_C": c.nnz,
-                       "multiplications": mults, "generation_s": gen_s},
-            "sampled_rows_exact": ok,
+                       "multiplications": mults, "setup_s": gen_s},
+            "parity": par,
             "cpu_baseline": {"value": 2 * smults / cpu / 1e9, "unit": UNIT,
                              "cores": os.cpu_count(), "kind": "port",
                              "sample": "first 65536 rows of A times A (extrapolated rate)"}}
 
+
+# ------------------------------------------------------------------ placement table
 
 def placement(args):
     """The paper's data-placement table (Laplace R x A:
@@ -175,7 +301,7 @@ def placement(args):
     operand either in HBM or in pinned, device-mapped host memory that the
     kernels read/write in place over PCIe."""
     import paper_1804_00695_b200 as tsg
-    from paper_1804_00695_b200 import _lib, generators as gen
+    from paper_1804_00695_b200 import generators as gen
     from paper_1804_00695_b200.memory import PlacementPolicy
     n = args.grid if args.grid != 256 else 128
     a = gen.stencil(gen.BRICK3D, (n, n, n))
@@ -198,60 +324,38 @@ def placement(args):
                                    "incl. placement of slow operands and download of C" % n}}
 
 
-def config5(args):
-    """A*A on an R-MAT graph (values 1.0), single GPU, all tiers (power-law
-    rows land in the CTA and global-memory tiers).  The graph is built in HBM
-    (generators.rmat_graph_device, equal to the host builder).  Correctness:
-    sampled rows (incl. the max-degree row) against the oracle -- C's rows are
-    sliced on the device, so a multi-billion-entry C never crosses PCIe."""
-    from paper_1804_00695_b200 import _lib, generators as gen, kernel
-    from paper_1804_00695_b200.csr import slice_rows
-    from oracle import oracle as O
-    ctx = _lib.Context.get(0)
-    ctx.set_timing(True)
-    ctx.record(2)
-    da = gen.rmat_graph_device(args.scale).set_values(1.0)
-    ctx.record(3)
-    ctx.sync()
-    build_ms = ctx.elapsed_ms(2, 3)
-    mults = _lib.d_count_multiplications(da, da)
-    for _ in range(args.warmup):
-        dc = kernel.multiply_device(da, da)
-        del dc
-    times = []
-    for _ in range(args.steps):
-        ctx.record(0)
-        dc = kernel.multiply_device(da, da)
-        ctx.record(1)
-        times.append(ctx.elapsed_ms(0, 1))
-        nnz_c = dc.nnz
-        if _ + 1 < args.steps:
-            del dc
-    ms = statistics.median(times)
-    a = da.download()                       # host copy of A for the oracle
-    deg = np.diff(a.row_ptr)
-    rng = np.random.default_rng(1)
-    rows = list(rng.choice(a.num_rows, size=24, replace=False)) + [int(np.argmax(deg))]
-    ok = True
-    for r in rows:
-        ptr, col, val = O.multiply(slice_rows(a, int(r), int(r) + 1), a)
-        o = np.argsort(col)
-        got = dc.slice_rows(int(r), int(r) + 1).download()
-        ok &= bool(np.array_equal(got.col_idx, col[o]) and np.array_equal(got.values, val[o]))
-    sample = slice_rows(a, 0, min(a.num_rows, 4096))
-    t1 = time.perf_counter()
-    O.multiply(sample, a, workers=os.cpu_count() or 1)
-    cpu = time.perf_counter() - t1
-    smults = int(deg[sample.col_idx].sum())
-    return {"metric": "SpGEMM GFLOP/s config 5 (A*A R-MAT scale %d, 1 GPU)" % args.scale,
-            "value": 2 * mults / ms / 1e6, "unit": UNIT, "ms_per_step": ms, "dtype": "f64",
-            "data": "synthetic", "sampled_rows_exact": ok,
-            "config": {"n": a.num_rows, "nnz_A": a.nnz, "nnz_C": nnz_c, "multiplications": mults,
-                       "max_degree": int(deg.max()), "device_build_ms": build_ms,
-                       "c_bytes_device": 8 * (a.num_rows + 1) + 12 * nnz_c},
-            "cpu_baseline": {"value": 2 * smults / cpu / 1e9, "unit": UNIT, "cores": os.cpu_count(),
-                             "kind": "port", "sample": "first 4096 rows of A times A"}}
+# ------------------------------------------------------------------ config 5
+
+def config5(args, dist=None):
+    """A*A on an R-MAT graph (values 1.0), row-partitioned over the ranks
+    (distributed.mg_multiply); see paper_1804_00695_b200/distributed.py."""
+    from paper_1804_00695_b200 import distributed as D
+    return D.bench_config5(args, dist)
 
 
-def run(args):
-    return {1: config1, 3: config3, 4: config4, 5: config5, 6: placement}[args.config](args)
+# ------------------------------------------------------------------ driver hooks
+
+def run(args, dist=None):
+    if args.config == 5:
+        return config5(args, dist)
+    return {1: config1, 3: config3, 4: config4, 6: placement}[args.config](args)
+
+
+def secondary(args):
+    """Configs 1, 3 and 4 at their BASELINE sizes for the default N=1 run."""
+    out = {}
+    jobs = (("config1", config1, dict(steps=20)),
+            ("config3", config3, dict(steps=5, scale=22)),
+            ("config4", config4, dict(grid=256, hbm_cap_gib=8.0)))
+    for name, fn, over in jobs:
+        a = argparse.Namespace(**vars(args))
+        a.warmup = 3
+        for k, v in over.items():
+            setattr(a, k, v)
+        t0 = time.perf_counter()
+        try:
+            out[name] = fn(a)
+        except Exception as exc:   # a secondary failure must not hide the headline line
+            out[name] = {"error": "%s: %s" % (type(exc).__name__, exc)}
+        out[name]["wall_s"] = time.perf_counter() - t0
+    return out

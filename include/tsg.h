@@ -87,6 +87,9 @@ int tsg_get_stats(tsg_ctx *ctx, tsg_stats *out);
    (one of the last 32), read without synchronising the calls after it. */
 int tsg_numeric_calls(tsg_ctx *ctx, int64_t *n);
 int tsg_numeric_ms(tsg_ctx *ctx, int64_t call, float *ms);
+/* The context's compute stream (a cudaStream_t), so a caller can order its
+   own work -- e.g. the NCCL offset exchange -- on it. */
+int tsg_stream(tsg_ctx *ctx, void **stream);
 int tsg_event_record(tsg_ctx *ctx, int slot);
 int tsg_event_elapsed(tsg_ctx *ctx, int from, int to, float *ms);
 /* Device-to-device import of a CSR whose arrays already live on this device
@@ -137,6 +140,12 @@ int tsg_vec_len(const tsg_vec *v, int64_t *n);
 int tsg_vec_free(tsg_ctx *ctx, tsg_vec *v);
 
 /* ---- the hot path ---------------------------------------------------------- */
+/* Per-row multiplications of A*B (the K0 bound loop of kernel.py:135-145 over
+   the uncompressed B: sum of nnz(B_k) over row i of A), copied to flops_host
+   (rows_A int64, may be NULL) with their total (may be NULL).  Weights of the
+   multi-GPU flops partition (distributed.flops_partition). */
+int tsg_row_flops(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b, int64_t *flops_host,
+                  int64_t *total);
 /* kernel.py:96-103 count_multiplications */
 int tsg_count_multiplications(tsg_ctx *ctx, const tsg_csr *a, const tsg_csr *b,
                               int64_t *total);

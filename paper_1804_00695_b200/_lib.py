@@ -47,7 +47,7 @@ EXPORTS = (
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
-    "tsg_rap",
+    "tsg_rap", "tsg_row_flops", "tsg_stream",
 )
 
 _P = ctypes.c_void_p
@@ -83,6 +83,8 @@ _SIGS = {
     "tsg_vec_len": ([_P, _PI64], ctypes.c_int),
     "tsg_vec_free": ([_P, _P], ctypes.c_int),
     "tsg_count_multiplications": ([_P, _P, _P, _PI64], ctypes.c_int),
+    "tsg_row_flops": ([_P, _P, _P, _P, _PI64], ctypes.c_int),
+    "tsg_stream": ([_P, _PP], ctypes.c_int),
     "tsg_symbolic": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric": ([_P, _P, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
@@ -220,6 +222,12 @@ class Context:
         st = _Stats()
         check(load().tsg_get_stats(self.h, ctypes.byref(st)))
         return st.launches, st.symbolic_ms, st.numeric_ms
+
+    def stream(self) -> int:
+        """cudaStream_t of the compute stream (for torch.cuda.ExternalStream)."""
+        v = ctypes.c_void_p()
+        check(load().tsg_stream(self.h, ctypes.byref(v)))
+        return v.value or 0
 
     def record(self, slot):
         check(load().tsg_event_record(self.h, slot))
@@ -402,6 +410,14 @@ def d_count_multiplications(da, db) -> int:
     v = ctypes.c_int64()
     check(load().tsg_count_multiplications(da.ctx.h, da.h, db.h, ctypes.byref(v)))
     return v.value
+
+
+def d_row_flops(da, db):
+    """(per-row multiplications of A*B as int64 numpy, total)."""
+    out = np.empty(da.num_rows, dtype=np.int64)
+    tot = ctypes.c_int64()
+    check(load().tsg_row_flops(da.ctx.h, da.h, db.h, _ptr(out), ctypes.byref(tot)))
+    return out, tot.value
 
 
 def d_symbolic(da, dcb) -> DeviceVec:

@@ -186,6 +186,11 @@ extern "C" int tsg_set_timing(tsg_ctx *c, int enabled) {
     return TSG_OK;
 }
 
+extern "C" int tsg_stream(tsg_ctx *c, void **stream) {
+    *stream = (void *)c->stream;
+    return TSG_OK;
+}
+
 extern "C" int tsg_event_record(tsg_ctx *c, int slot) {
     if (slot < 0 || slot >= 8) {
         tsg_set_error("event slot %d out of range", slot);
@@ -716,13 +721,19 @@ template <typename TI>
 __global__ void __launch_bounds__(LB_BS) scan_lookback(const TI *__restrict__ in, int64_t n,
                                                       int64_t *__restrict__ out,
                                                       unsigned long long *state, unsigned epoch,
-                                                      unsigned ntiles) {
+                                                      unsigned ntiles, unsigned long long *counter,
+                                                      unsigned long long cbase) {
     pdl_wait();
-    // tile = block index: blocks are dispatched in index order, so every
-    // predecessor a tile waits for is already resident
+    // tile = ticket from a monotone counter, not blockIdx: tiles are taken in
+    // the order blocks actually start, so every predecessor a tile waits for
+    // is already resident whatever the dispatch order (PDL early launch and
+    // concurrent bins on other streams give no index-order guarantee)
     __shared__ int64_t ws[LB_BS / 32];
     __shared__ int64_t s_excl;
-    const unsigned tile = blockIdx.x;
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = (unsigned)(atomicAdd(counter, 1ull) - cbase);
+    __syncthreads();
+    const unsigned tile = s_tile;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t base = (int64_t)tile * LB_TILE + (int64_t)threadIdx.x * LB_IT;
     const bool vec = (int64_t)(tile + 1) * LB_TILE <= n &&
@@ -831,10 +842,12 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     unsigned long long *state = nullptr;
     unsigned epoch = 0;
     TSG_TRY(tsg_lookback_state(c, tiles, &state, &epoch));
+    unsigned long long *counter = nullptr, cbase = 0;
+    TSG_TRY(tsg_lookback_counter(c, tiles, &counter, &cbase));
     // in-place safe: a tile reads its inputs before writing, and writes only
     // its own range (plus out[n], past every input)
     TSG_CK(launch_pdl(scan_lookback<TI>, (unsigned)tiles, LB_BS, 0, c->stream, in, n, out, state, epoch,
-                      (unsigned)tiles));
+                      (unsigned)tiles, counter, cbase));
     ++c->launches;
     TSG_CK(cudaGetLastError());
     return TSG_OK;

@@ -2529,6 +2529,38 @@ extern "C" int tsg_count_multiplications(tsg_ctx *c, const tsg_csr *a, const tsg
     return TSG_OK;
 }
 
+// Per-row K0 multiplications (kernel.py:135-145's bound loop over the
+// uncompressed B: sum of nnz(B_k) over row i of A) -- the weights of the
+// multi-GPU flops partition -- and their total
+// (kernel.py:96-103 count_multiplications).
+extern "C" int tsg_row_flops(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int64_t *flops_host,
+                             int64_t *total) {
+    if (a->cols != b->rows) {
+        tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
+                      (long long)b->rows);
+        return TSG_EDIM;
+    }
+    int64_t *f = nullptr;
+    if (flops_host && a->rows > 0) TSG_TRY(tsg_alloc_t(c, &f, a->rows));
+    TSG_TRY(tsg_fill(c, c->d_small, 0, sizeof(int64_t), c->stream));
+    if (a->rows > 0) {
+        if (a->nnz > 0) {
+            launch_bounds(c, a, b->rp, nullptr, f, nullptr, (unsigned long long *)c->d_small);
+        } else if (f) {
+            TSG_TRY(tsg_fill(c, f, 0, sizeof(int64_t) * a->rows, c->stream));
+        }
+    }
+    TSG_CK(cudaGetLastError());
+    TSG_TRY(tsg_put_small(c, c->d_small, 1, 0));
+    if (f) {
+        TSG_CK(cudaMemcpyAsync(flops_host, f, sizeof(int64_t) * a->rows, cudaMemcpyDeviceToHost, c->stream));
+    }
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    if (f) TSG_TRY(tsg_free(c, f));
+    if (total) *total = c->h_small[0];
+    return TSG_OK;
+}
+
 extern "C" int tsg_symbolic(tsg_ctx *c, const tsg_csr *a, const tsg_cmat *cb, tsg_vec **counts) {
     if (a->cols != cb->rows) {
         tsg_set_error("A has %lld cols but compressed B has %lld rows", (long long)a->cols,

@@ -20,13 +20,14 @@ Differences a caller can observe, all inside the reference's contract:
 """
 
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
 from .csr import CsrMatrix, as_csr
-from .errors import DimensionError, MatrixValidationError
+from .errors import CapacityError, DimensionError, MatrixValidationError
 
 COMPRESSION_WORD_BITS = 64
 
@@ -120,7 +121,7 @@ def _on_device(m) -> "_lib.DeviceCsr":
     hit = _resident.get(id(m))
     if hit is not None and hit[0] == k:
         return hit[1]
-    d = _lib.DeviceCsr.upload(m)
+    d = _with_room(_lib.DeviceCsr.upload, m)
     try:
         weakref.finalize(m, _resident.pop, id(m), None)
         _resident[id(m)] = (k, d)
@@ -129,28 +130,53 @@ def _on_device(m) -> "_lib.DeviceCsr":
     return d
 
 
-# results keep their device copy (bounded), so a product fed straight back as
-# an operand -- RA in R*A*P -- is not uploaded again
-_RESULT_CACHE_BYTES = 32 << 30
-_result_bytes = [0]
+# results keep their device copy, so a product fed straight back as an operand
+# -- RA in R*A*P -- is not uploaded again.  The cache is a small LRU (a few
+# results, bounded bytes); an allocation that runs out of HBM drops it and
+# retries (``_with_room``), and ``release_device_cache`` empties it.
+_RESULT_CACHE_BYTES = 8 << 30
+_RESULT_CACHE_ENTRIES = 4
+_results = OrderedDict()   # id(host) -> bytes, oldest first
+
+
+def _evict(i):
+    if _results.pop(i, None) is not None:
+        _resident.pop(i, None)
+
+
+def release_device_cache() -> None:
+    """Drop every cached device copy of results and operands (their host
+    objects stay valid; the next use uploads again)."""
+    for i in list(_results):
+        _evict(i)
+    _resident.clear()
 
 
 def _keep_result(host, dev):
     nbytes = 8 * (dev.num_rows + 1) + 12 * dev.nnz
-    if _result_bytes[0] + nbytes > _RESULT_CACHE_BYTES:
+    if nbytes > _RESULT_CACHE_BYTES:
         return host
+    while _results and (len(_results) >= _RESULT_CACHE_ENTRIES or
+                        sum(_results.values()) + nbytes > _RESULT_CACHE_BYTES):
+        _evict(next(iter(_results)))
     try:
         k = _key(host)
         _resident[id(host)] = (k, dev)
-        _result_bytes[0] += nbytes
-
-        def _drop(i=id(host), n=nbytes):
-            _resident.pop(i, None)
-            _result_bytes[0] -= n
-        weakref.finalize(host, _drop)
+        _results[id(host)] = nbytes
+        weakref.finalize(host, _evict, id(host))
     except TypeError:
         pass
     return host
+
+
+def _with_room(fn, *args):
+    """fn(*args); on CapacityError (HBM exhausted) drop the device caches and
+    retry once."""
+    try:
+        return fn(*args)
+    except CapacityError:
+        release_device_cache()
+        return fn(*args)
 
 
 def _counts_on_device(counts: np.ndarray) -> "_lib.DeviceVec":
@@ -253,7 +279,7 @@ def multiply(a, b, workers: int = 1, placement="all_fast") -> CsrMatrix:
     from .memory import ALL_FAST, CHUNKED, FAST, PlacementPolicy
     pol = placement if isinstance(placement, PlacementPolicy) else PlacementPolicy.from_name(placement)
     if pol.name in (ALL_FAST, CHUNKED) or all(v == FAST for v in pol.spaces.values()):
-        dc = _lib.d_multiply(_on_device(a), _on_device(b))
+        dc = _with_room(_lib.d_multiply, _on_device(a), _on_device(b))
         return _keep_result(dc.download(), dc)
     da = _on_device(a) if pol.space_of("A") == FAST else _lib.DeviceCsr.map_host(a)
     db = _on_device(b) if pol.space_of("B") == FAST else _lib.DeviceCsr.map_host(b)

@@ -1,0 +1,108 @@
+"""GPU parity at the BASELINE.json configuration sizes.
+
+configs 1 and 2 run at their full sizes and are compared with the oracle's
+full product; config 3 runs the device R-MAT pipeline at scales 16 and 18
+against golden counts of the same graphs (tests/golden/rmat_triangles.json)
+and a live oracle count; config 4's two plans (chunk1 7x3 and chunk2 5x1 at
+256^3) are reproduced at 64^3 with the caps scaled by 1/64 and the full C is
+compared; config 5's power-law A*A runs at R-MAT scale 14 (hub rows take the
+CTA, global and dense tiers) with the full result within 1e-12.
+
+Bar (BASELINE.json north_star): row pointers and per-row sorted columns
+bit-exact, fp64 values bit-exact for thread-group-tier rows (every row of
+configs 1, 2 and 4) and within rel 1e-12 elsewhere, integer results exact.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1804_00695_b200 as tsg
+from paper_1804_00695_b200 import _lib, chunking as ch, generators as gen, kernel
+from paper_1804_00695_b200.csr import CsrMatrix
+from paper_1804_00695_b200.memory import b200_model
+from oracle import oracle as O
+from conftest import assert_same_product
+
+import bench_configs as BC
+
+pytestmark = pytest.mark.gpu
+W = os.cpu_count() or 1
+
+
+def test_config1_full_256sq_exact():
+    a = gen.stencil(gen.LAPLACE2D, (256, 256))
+    c = tsg.multiply(a, a)
+    assert c.nnz == 846852
+    assert_same_product(c, O.multiply(a, a, workers=W), exact=True)
+
+
+def test_config2_full_128cubed_ra_and_rap_exact():
+    a = gen.stencil(gen.BRICK3D, (128, 128, 128))
+    p, r = gen.aggregation((128, 128, 128))
+    ra = tsg.multiply(r, a)
+    ra_o = O.multiply(r, a, workers=W)
+    res = BC.compare_products(ra, ra_o)
+    assert res["structure"] and res["exact"], res
+    assert ra.nnz == 16387064
+    rap = tsg.multiply(ra, p)
+    rap_o = O.multiply(CsrMatrix._adopt(r.num_rows, a.num_cols, *ra_o), p, workers=W)
+    res = BC.compare_products(rap, rap_o)
+    assert res["structure"] and res["exact"], res
+    assert rap.nnz == 6859000
+
+
+def test_config2_device_resident_path_matches_host_api():
+    # the bench's device path (multiply_device on device-built operands)
+    # gives the same bits as the host API path
+    a = gen.stencil(gen.BRICK3D, (64, 64, 64))
+    p, r = gen.aggregation((64, 64, 64))
+    da, dp, dr = (_lib.DeviceCsr.upload(m) for m in (a, p, r))
+    drap = kernel.multiply_device(kernel.multiply_device(dr, da), dp)
+    want = tsg.multiply(tsg.multiply(r, a), p)
+    got = drap.download()
+    assert np.array_equal(got.row_ptr, want.row_ptr)
+    assert np.array_equal(got.col_idx, want.col_idx)
+    assert np.array_equal(got.values.view(np.uint64), want.values.view(np.uint64))
+
+
+@pytest.mark.parametrize("scale", [16, 18])
+def test_config3_rmat_triangles_golden(scale):
+    from paper_1804_00695_b200.triangles import lower_triangle_device
+    gold = BC.rmat_golden(scale)
+    assert gold is not None, "tests/golden/rmat_triangles.json lacks scale %d" % scale
+    dg = gen.rmat_graph_device(scale)
+    assert dg.nnz == gold["nnz_graph"]
+    dl, _ = lower_triangle_device(dg, check=True)
+    assert dl.nnz == gold["nnz_L"]
+    assert _lib.d_count_multiplications(dl, dl) == gold["mults_LL"]
+    tri = _lib.d_masked_count(dl, _lib.d_compress(dl))
+    assert tri == gold["triangles"]
+    if scale == 16:   # and a live oracle count on the downloaded L
+        low = dl.download()
+        assert O.masked_count(low, O.compress(low), workers=W) == tri
+    assert tsg.count_triangles(dg.download()) == gold["triangles"]
+
+
+@pytest.mark.parametrize("cap_mib,algo,n_ac,n_b", [(128, ch.GPU_CHUNK1_AC_IN_PLACE, 7, 3),
+                                                    (224, ch.GPU_CHUNK2_B_IN_PLACE, 5, 1)])
+def test_config4_chunked_64cubed_full_result(cap_mib, algo, n_ac, n_b):
+    a = gen.stencil(gen.BRICK3D, (64, 64, 64))
+    counts = tsg.spgemm_symbolic(a, tsg.compress(a))
+    fast = cap_mib << 20
+    plan = ch.plan_for_multiply(a, a, counts, fast)
+    assert (plan.algorithm, len(plan.partition_ac), len(plan.partition_b)) == (algo, n_ac, n_b)
+    c, led = ch.execute_plan(a, a, counts, plan, b200_model(fast))
+    assert led.total_bytes() == plan.predicted_copy_bytes
+    assert_same_product(c, O.multiply(a, a, workers=W), exact=True)
+
+
+def test_config5_rmat_scale14_aa_full_result():
+    g = gen.rmat_graph(14)
+    a = gen.with_unit_values(g)
+    c = tsg.multiply(a, a)
+    assert_same_product(c, O.multiply(a, a, workers=W), exact=False, rtol=1e-12)
+    # integer-valued products: exact whatever the tier
+    deg = np.diff(a.row_ptr)
+    assert int(c.values.sum()) == int((deg.astype(np.int64) ** 2).sum())
