@@ -88,19 +88,42 @@ def embed_rows(a_loc, dims, rank, base):
     return CsrMatrix._adopt(n, a_loc.num_cols, rp, a_loc.col_idx, a_loc.values)
 
 
-def _sampled_rows_check(get_row, a, b, rows):
-    """Rows of C = A*B against the oracle on single-row slices (rows of C are
-    independent, kernel.py:11-14): all exact / ok."""
-    from oracle import oracle as O
-    from paper_1804_00695_b200.csr import slice_rows
-    exact = ok = True
-    for r in rows:
-        ptr, col, val = O.multiply(slice_rows(a, int(r), int(r) + 1), b)
-        got = get_row(int(r))
-        res = compare_products(got, (ptr, col, val))
-        exact &= res["exact"]
-        ok &= res["ok"]
-    return {"ok": bool(ok), "exact": bool(exact), "rows_checked": len(rows)}
+def link_peaks(gib=1.0, reps=3):
+    """Pinned host <-> HBM copy bandwidth on this box (the roofline of the
+    chunked executors): H2D alone, D2H alone, both directions at once (GB/s)."""
+    import torch
+    n = int(gib * 2**30)
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name + "_gbs"] = reps * n / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s1):
+        for _ in range(reps):
+            d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2):
+        for _ in range(reps):
+            h2.copy_(d2, non_blocking=True)
+    s1.synchronize()
+    s2.synchronize()
+    out["bidir_total_gbs"] = 2 * reps * n / (time.perf_counter() - t0) / 1e9
+    del h, h2, d, d2
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ config 1
@@ -227,70 +250,100 @@ def config3(args):
 
 def config4(args):
     """Chunked out-of-HBM A*A, brick3d N^3 (default 256^3), HBM budget capped
-    (default 8 GiB), A and C in pinned host memory, the Alg. 4 plan.  A is
-    built on the device and downloaded into pinned memory (the host builder
-    takes ~25 s); parity on sampled rows, incl. every chunk boundary row."""
+    (default 8 GiB, plus every cap in ``args.extra_caps_gib``), A and C in
+    pinned host memory, the Alg. 4 plan.  A is built on the device and
+    downloaded into pinned memory (the host builder takes ~25 s); the symbolic
+    counts are computed inside the same budget (chunking.symbolic_within_budget);
+    parity on sampled rows, incl. the first / last row of every planned range."""
     from oracle import oracle as O
     from paper_1804_00695_b200 import _lib, chunking as ch, generators as gen
-    from paper_1804_00695_b200.csr import slice_rows
+    from paper_1804_00695_b200.csr import CsrMatrix, slice_rows
     from paper_1804_00695_b200.memory import b200_model
     n = args.grid
     t0 = time.perf_counter()
     ctx = _lib.Context.get(0)
     da = gen.stencil_device(gen.BRICK3D, (n, n, n))
     a = da.download()                                # pinned host arrays
-    # symbolic counts once on the device (the reference computes them unchunked
-    # and unbilled, cli.py:164-165); not part of the timed chunked run
-    counts = _lib.d_symbolic(da, _lib.d_compress(da)).download()
     del da
     ctx.sync()
     gen_s = time.perf_counter() - t0
-    fast = int(args.hbm_cap_gib * 2**30)
-    plan = ch.plan_for_multiply(a, a, counts, fast)
-    model = b200_model(fast)
-    c, led = ch.execute_plan(a, a, counts, plan, model)
-    ph = led.physical
     mults = int(np.diff(a.row_ptr)[a.col_idx].sum())
-    # parity: random rows + the first/last row of every planned range
-    rng = np.random.default_rng(0)
-    rows = set(int(x) for x in rng.choice(a.num_rows, size=24, replace=False))
-    for part in (plan.partition_ac, plan.partition_b):
-        for r in part.ranges:
-            rows.update({r.begin, max(r.begin, r.end - 1)})
-    rows = sorted(x for x in rows if x < a.num_rows)
-
-    def row_of(r):
-        from paper_1804_00695_b200.csr import CsrMatrix
-        lo, hi = int(c.row_ptr[r]), int(c.row_ptr[r + 1])
-        return CsrMatrix._adopt(1, c.num_cols, np.array([0, hi - lo]), c.col_idx[lo:hi], c.values[lo:hi])
-    par = _sampled_rows_check(row_of, a, a, rows)
-    par["nnz_C_exact"] = bool(c.nnz == int(np.sum(counts)))
-    par["ok"] = par["ok"] and par["nnz_C_exact"]
-    # CPU rate on a row sample (extrapolated)
-    sample = slice_rows(a, 0, 65536)
-    t1 = time.perf_counter()
-    O.multiply(sample, a, workers=os.cpu_count() or 1)
-    cpu = time.perf_counter() - t1
-    smults = int(np.diff(a.row_ptr)[sample.col_idx].sum())
-    secs = ph["wall_ms"] / 1e3
-    return {"metric": "chunked SpGEMM GFLOP/s config 4 (A*A brick3d %d^3, HBM cap %.1f GiB)"
-                      % (n, args.hbm_cap_gib),
-            "value": 2 * mults / secs / 1e9, "unit": UNIT, "dtype": "f64", "data": "synthetic",
+    caps = [args.hbm_cap_gib] + list(getattr(args, "extra_caps_gib", []) or [])
+    link = link_peaks()
+    runs = []
+    cb_o = None
+    for cap in caps:
+        fast = int(cap * 2**30)
+        counts, sym = ch.symbolic_within_budget(a, a, fast)
+        plan = ch.plan_for_multiply(a, a, counts, fast)
+        model = b200_model(fast)
+        c, led = ch.execute_plan(a, a, counts, plan, model)
+        ph = led.physical
+        # parity: random rows + the first/last row of every planned range,
+        # through the oracle with B compressed once
+        rng = np.random.default_rng(0)
+        rows = set(int(x) for x in rng.choice(a.num_rows, size=24, replace=False))
+        for part in (plan.partition_ac, plan.partition_b):
+            for r in part.ranges:
+                rows.update({r.begin, max(r.begin, r.end - 1)})
+        rows = sorted(x for x in rows if x < a.num_rows)
+        if cb_o is None:
+            cb_o = O.compress(a)
+        exact = ok = True
+        for r in rows:
+            sub = slice_rows(a, r, r + 1)
+            want = O.numeric(sub, a, O.symbolic(sub, cb_o))
+            lo, hi = int(c.row_ptr[r]), int(c.row_ptr[r + 1])
+            got = CsrMatrix._adopt(1, c.num_cols, np.array([0, hi - lo]), c.col_idx[lo:hi], c.values[lo:hi])
+            res = compare_products(got, want)
+            exact &= res["exact"]
+            ok &= res["ok"]
+        nnz_ok = bool(c.nnz == int(np.sum(counts)))
+        secs = ph["wall_ms"] / 1e3
+        runs.append({
+            "hbm_cap_gib": cap, "value": 2 * mults / secs / 1e9, "unit": UNIT,
             "host_link": {"achieved_gbs": ph["link_gbs"], "h2d_bytes": ph["h2d_bytes"],
                           "d2h_bytes": ph["d2h_bytes"], "wall_s": secs,
                           "kernel_s": ph["kernel_ms"] / 1e3,
-                          "peak_device_bytes": ph.get("peak_device_bytes"),
-                          "hbm_cap_bytes": fast},
+                          "link_peak": link,
+                          "frac_of_bidir_peak": ph["link_gbs"] / link["bidir_total_gbs"],
+                          "h2d_engine_frac": ph["h2d_bytes"] / secs / 1e9 / link["h2d_gbs"]},
+            "hbm": {"cap_bytes": fast, "peak_device_bytes": ph["peak_device_bytes"],
+                    "layout_bytes": ph["layout_bytes"], "slots": ph["slots"], "split": ph["split"],
+                    "symbolic_peak_device_bytes": sym["peak_device_bytes"],
+                    "symbolic_wall_s": sym["wall_ms"] / 1e3},
             "plan": {"algorithm": plan.algorithm, "branch": plan.heuristic_branch,
                      "n_ac": len(plan.partition_ac), "n_b": len(plan.partition_b),
                      "ledger_bytes": led.total_bytes(),
                      "predicted_copy_bytes": plan.predicted_copy_bytes},
-            "config": {"workload": "config4", "rows": a.num_rows, "nnz_A": a.nnz, "nnz_C": c.nnz,
+            "nnz_C": c.nnz,
+            "parity": {"ok": bool(ok and nnz_ok), "exact": bool(exact), "rows_checked": len(rows),
+                       "nnz_C_exact": nnz_ok}})
+        del c
+    # CPU rate of the oracle, extrapolated: compress of the whole B once plus
+    # symbolic + numeric on a row sample scaled by its share of the multiplications
+    sample = slice_rows(a, 0, 65536)
+    smults = int(np.diff(a.row_ptr)[sample.col_idx].sum())
+    W = os.cpu_count() or 1
+    t1 = time.perf_counter()
+    cb2 = O.compress(a)
+    tc = time.perf_counter() - t1
+    t1 = time.perf_counter()
+    O.numeric(sample, a, O.symbolic(sample, cb2, W), W)
+    ts = time.perf_counter() - t1
+    cpu_s = tc + ts * mults / smults
+    main = runs[0]
+    return {"metric": "chunked SpGEMM GFLOP/s config 4 (A*A brick3d %d^3, HBM cap %.1f GiB)"
+                      % (n, args.hbm_cap_gib),
+            "value": main["value"], "unit": UNIT, "dtype": "f64", "data": "synthetic",
+            "host_link": main["host_link"], "hbm": main["hbm"], "plan": main["plan"],
+            "parity": main["parity"], "runs": runs,
+            "config": {"workload": "config4", "rows": a.num_rows, "nnz_A": a.nnz, "nnz_C": main["nnz_C"],
                        "multiplications": mults, "setup_s": gen_s},
-            "parity": par,
-            "cpu_baseline": {"value": 2 * smults / cpu / 1e9, "unit": UNIT,
-                             "cores": os.cpu_count(), "kind": "port",
-                             "sample": "first 65536 rows of A times A (extrapolated rate)"}}
+            "cpu_baseline": {"value": 2 * mults / cpu_s / 1e9, "unit": UNIT,
+                             "cores": W, "kind": "port",
+                             "sample": "oracle compress of the whole B + symbolic/numeric of the "
+                                       "first 65536 rows, extrapolated by multiplications"}}
 
 
 # ------------------------------------------------------------------ placement table
@@ -346,7 +399,7 @@ def secondary(args):
     out = {}
     jobs = (("config1", config1, dict(steps=20)),
             ("config3", config3, dict(steps=5, scale=22)),
-            ("config4", config4, dict(grid=256, hbm_cap_gib=8.0)))
+            ("config4", config4, dict(grid=256, hbm_cap_gib=8.0, extra_caps_gib=[16.0])))
     for name, fn, over in jobs:
         a = argparse.Namespace(**vars(args))
         a.warmup = 3

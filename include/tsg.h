@@ -253,14 +253,32 @@ typedef struct {
     int64_t d2h_bytes;          /* bytes actually copied device -> host     */
     double kernel_ms;           /* device time of compress + fused kernels   */
     double wall_ms;             /* host wall time of the whole call          */
-    int64_t peak_device_bytes;  /* device bytes held at the end of the plan  */
+    int64_t peak_device_bytes;  /* high-water mark of the call's HBM allocations */
+    int64_t budget_bytes;       /* the budget passed in (0: unlimited)       */
+    int64_t layout_bytes;       /* modelled footprint of the chosen layout   */
+    int32_t a_slots, c_slots, b_slots;  /* buffering chosen for A / C / B    */
+    int32_t ac_split, b_split;  /* physical sub-ranges per planned range / chunk */
 } tsg_chunk_stats;
+/* budget_bytes > 0: every device allocation of the call (slots, staging,
+   per-step scratch) stays within it -- the executor double-buffers what fits
+   and splits planned ranges / chunks physically where needed (traffic-neutral
+   splits first); TSG_ECAPACITY if no layout fits or the measured high-water
+   mark exceeds it (memory.py:103-111 residency check). */
 int tsg_chunk_multiply(tsg_ctx *ctx, int algo, int64_t a_rows, int64_t a_cols,
                        const int64_t *a_row_ptr, const int64_t *a_col, const double *a_val,
                        int64_t b_rows, int64_t b_cols, const int64_t *b_row_ptr,
                        const int64_t *b_col, const double *b_val, const int64_t *c_row_ptr,
                        int64_t *c_col, double *c_val, int64_t n_ac, const int64_t *ac_bounds,
-                       int64_t n_b, const int64_t *b_bounds, tsg_chunk_stats *stats);
+                       int64_t n_b, const int64_t *b_bounds, int64_t budget_bytes,
+                       tsg_chunk_stats *stats);
+/* spgemm_symbolic (kernel.py:124-168) through the same budget: B compressed
+   chunk by chunk into one resident compressed B, then A row ranges streamed
+   past it; counts (a_rows int64) written to host.  TSG_ECAPACITY when the
+   compressed B alone does not fit. */
+int tsg_chunk_symbolic(tsg_ctx *ctx, int64_t a_rows, int64_t a_cols, const int64_t *a_row_ptr,
+                       const int64_t *a_col, int64_t b_rows, int64_t b_cols, const int64_t *b_row_ptr,
+                       const int64_t *b_col, int64_t budget_bytes, int64_t *counts,
+                       tsg_chunk_stats *stats);
 
 #ifdef __cplusplus
 }

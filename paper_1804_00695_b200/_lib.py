@@ -47,7 +47,7 @@ EXPORTS = (
     "tsg_chunk_multiply", "tsg_csr_map_host", "tsg_multiply_placed",
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
-    "tsg_rap", "tsg_row_flops", "tsg_stream",
+    "tsg_rap", "tsg_row_flops", "tsg_stream", "tsg_chunk_symbolic",
 )
 
 _P = ctypes.c_void_p
@@ -111,7 +111,8 @@ _SIGS = {
     "tsg_csr_map_host": ([_P, _I64, _I64, _I64, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_multiply_placed": ([_P, _P, _P, ctypes.c_int, _PP], ctypes.c_int),
     "tsg_chunk_multiply": ([_P, ctypes.c_int, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
-                            _P, _P, _P, _I64, _P, _I64, _P, _P], ctypes.c_int),
+                            _P, _P, _P, _I64, _P, _I64, _P, _I64, _P], ctypes.c_int),
+    "tsg_chunk_symbolic": ([_P, _I64, _I64, _P, _P, _I64, _I64, _P, _P, _I64, _P, _P], ctypes.c_int),
 }
 
 _lib = None

@@ -244,15 +244,25 @@ def _check_partition(p: RowPartition, num_rows: int, what: str) -> None:
 class _ChunkStats(ctypes.Structure):
     _fields_ = [("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("kernel_ms", ctypes.c_double), ("wall_ms", ctypes.c_double),
-                ("peak_device_bytes", ctypes.c_int64)]
+                ("peak_device_bytes", ctypes.c_int64), ("budget_bytes", ctypes.c_int64),
+                ("layout_bytes", ctypes.c_int64), ("a_slots", ctypes.c_int32),
+                ("c_slots", ctypes.c_int32), ("b_slots", ctypes.c_int32),
+                ("ac_split", ctypes.c_int32), ("b_split", ctypes.c_int32)]
 
 
 def _c_array(x, dt):
     return np.ascontiguousarray(np.asarray(x), dtype=dt)
 
 
-def _physical(algo: str, a, b, c_counts, ac_bounds, b_bounds, ledger) -> CsrMatrix:
-    """Run the plan on the device; fills ledger.physical; returns C."""
+def _budget(model) -> int:
+    cap = getattr(getattr(model, "fast", None), "capacity", None)
+    return 0 if cap is None else int(cap)
+
+
+def _physical(algo: str, a, b, c_counts, ac_bounds, b_bounds, ledger, budget: int) -> CsrMatrix:
+    """Run the plan on the device inside `budget` bytes of HBM (0: no cap);
+    fills ledger.physical (DMA bytes, times, the measured allocation peak and
+    the buffering / splitting the executor chose); returns C."""
     lib = _lib.load()
     ctx = _lib.Context.get()
     counts = _c_array(c_counts, np.int64)
@@ -274,12 +284,36 @@ def _physical(algo: str, a, b, c_counts, ac_bounds, b_bounds, ledger) -> CsrMatr
     _lib.check(lib.tsg_chunk_multiply(
         ctx.h, _ALGO_ID[algo], a.num_rows, a.num_cols, P(arrs[0]), P(arrs[1]), P(arrs[2]),
         b.num_rows, b.num_cols, P(arrs[3]), P(arrs[4]), P(arrs[5]), P(c_rp), P(c_col), P(c_val),
-        len(acb) - 1, P(acb), len(bb) - 1, P(bb), ctypes.byref(st)))
+        len(acb) - 1, P(acb), len(bb) - 1, P(bb), int(budget), ctypes.byref(st)))
     ledger.physical = {"h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
                        "kernel_ms": st.kernel_ms, "wall_ms": st.wall_ms,
                        "link_gbs": (st.h2d_bytes + st.d2h_bytes) / max(st.wall_ms, 1e-9) / 1e6,
-                       "algorithm": algo}
+                       "algorithm": algo, "peak_device_bytes": st.peak_device_bytes,
+                       "budget_bytes": st.budget_bytes, "layout_bytes": st.layout_bytes,
+                       "slots": {"A": st.a_slots, "C": st.c_slots, "B": st.b_slots},
+                       "split": {"ac": st.ac_split, "b": st.b_split}}
     return CsrMatrix._adopt(a.num_rows, b.num_cols, c_rp, c_col, c_val)
+
+
+def symbolic_within_budget(a, b, fast_size: int):
+    """spgemm_symbolic (kernel.py:124-168) inside `fast_size` bytes of HBM:
+    B is compressed chunk by chunk into one resident compressed B, then A row
+    ranges stream past it (csrc/tsg_chunk.cu tsg_chunk_symbolic).  Returns
+    (counts, physical stats).  CapacityError when the compressed B alone does
+    not fit."""
+    if a.num_cols != b.num_rows:
+        raise DimensionError("A has %d cols but B has %d rows" % (a.num_cols, b.num_rows))
+    lib = _lib.load()
+    ctx = _lib.Context.get()
+    arrs = [_c_array(x, np.int64) for x in (a.row_ptr, a.col_idx, b.row_ptr, b.col_idx)]
+    counts = np.empty(a.num_rows, dtype=np.int64)
+    st = _ChunkStats()
+    P = _lib._ptr
+    _lib.check(lib.tsg_chunk_symbolic(ctx.h, a.num_rows, a.num_cols, P(arrs[0]), P(arrs[1]),
+                                      b.num_rows, b.num_cols, P(arrs[2]), P(arrs[3]),
+                                      int(fast_size), P(counts), ctypes.byref(st)))
+    return counts, {"h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes, "wall_ms": st.wall_ms,
+                    "peak_device_bytes": st.peak_device_bytes, "budget_bytes": st.budget_bytes}
 
 
 def knl_chunk_multiply(a, b, c_counts, fast_size: int, model: MemoryModel, workers: int = 1):
@@ -301,7 +335,7 @@ def knl_chunk_multiply(a, b, c_counts, fast_size: int, model: MemoryModel, worke
         ledger.alloc(FAST, nb)
         ledger.record(nb, SLOW, FAST, tag="B")
         ledger.free(FAST, nb)
-    c = _physical(KNL_CHUNK, a, b, c_counts, [0, a.num_rows], p_b.bounds(), ledger)
+    c = _physical(KNL_CHUNK, a, b, c_counts, [0, a.num_rows], p_b.bounds(), ledger, fast_size)
     return c, ledger
 
 
@@ -330,7 +364,8 @@ def gpu_chunk_multiply_1(a, b, c_counts, p_ac: RowPartition, p_b: RowPartition,
             ledger.free(FAST, nb)
         ledger.record(c_entries, FAST, SLOW, tag="C_out")
         ledger.free(FAST, a_bytes + c_full)
-    c = _physical(GPU_CHUNK1_AC_IN_PLACE, a, b, counts, p_ac.bounds(), p_b.bounds(), ledger)
+    c = _physical(GPU_CHUNK1_AC_IN_PLACE, a, b, counts, p_ac.bounds(), p_b.bounds(), ledger,
+                  _budget(model))
     return c, ledger
 
 
@@ -357,7 +392,8 @@ def gpu_chunk_multiply_2(a, b, c_counts, p_ac: RowPartition, p_b: RowPartition,
             ledger.record(0, FAST, SLOW, tag="C_out")
             ledger.free(FAST, a_bytes + c_full)
         ledger.free(FAST, nb)
-    c = _physical(GPU_CHUNK2_B_IN_PLACE, a, b, c_counts, p_ac.bounds(), p_b.bounds(), ledger)
+    c = _physical(GPU_CHUNK2_B_IN_PLACE, a, b, c_counts, p_ac.bounds(), p_b.bounds(), ledger,
+                  _budget(model))
     return c, ledger
 
 

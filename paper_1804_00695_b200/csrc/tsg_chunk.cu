@@ -10,20 +10,37 @@
 //   order 2 (gpu chunk2, B in place): per B chunk (resident), every A/C range
 //     streams past it; C partials round-trip through host memory.
 //   order 0 (KNL): B chunks stream past the whole of A/C (order 1 with one
-//     A/C range).
+//     A/C range, split physically as the budget requires).
 // Every chunk step is the fused multiply-add (kernel.py:235-340) run IN
 // PLACE: C rows keep their final capacity and the running partial occupies a
 // prefix whose length is tracked per row, so no C copy is ever made on the
-// device.  B chunks and A ranges are double-buffered: the next one's H2D runs
-// on the copy-in stream while the current one computes; C ranges drain D2H on
-// the copy-out stream while the next range computes.  Host formats are the
-// reference's (int64 indices): columns travel as int64 and are narrowed /
-// widened on the device, so physical PCIe bytes equal the ledger's byte
-// convention (csr.py:65-67).
+// device.  Host formats are the reference's (int64 indices): columns travel
+// as int64 and are narrowed / widened on the device, so physical PCIe bytes
+// equal the ledger's byte convention (csr.py:65-67).
+//
+// The HBM budget (the planner's fast_size, chunking.py:21-22) is honoured
+// PHYSICALLY, like the reference's residency checks (memory.py:103-111):
+// before the run the executor sizes every slot it will hold -- A ranges
+// (double-buffered when they fit), C ranges (double-buffered when they fit,
+// so a range drains while the next computes), B chunks (up to three slots,
+// the copy two steps ahead), the per-step scratch (compressed B chunk,
+// partition, bounds) -- and picks the buffering / splitting that fits:
+//   * B chunks of order 0/1 are split into sub-chunks (traffic-neutral; only
+//     when every A row is column-sorted, so each C entry still accumulates in
+//     the reference's order),
+//   * A/C ranges of order 2 into sub-ranges (traffic-neutral: A/C stream per
+//     B chunk anyway), and as a last resort those of order 0/1 (B then
+//     streams once per sub-range: more PCIe bytes, reported as such).
+// Columns are converted in place of the value buffers (int64 columns land in
+// the slot's fp64 array, are narrowed on the convert stream, then the values
+// follow), so no full-size staging array exists.  The context's allocation
+// high-water mark during the call is reported as peak_device_bytes and must
+// not exceed the budget (TSG_ECAPACITY otherwise).
 #include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "tsg_internal.cuh"
@@ -33,6 +50,9 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out);
 int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, const tsg_csr *b,
                       const tsg_cmat *cb, const int64_t *cptr, const int64_t *cap, int32_t *ccol,
                       double *cval, int32_t *plen, int64_t rows);
+int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_row_off, int32_t b_lo,
+                      int32_t b_hi, const tsg_cmat *cb, const tsg_csr *partial, tsg_vec **out,
+                      int64_t **sbound_out);
 
 namespace {
 
@@ -75,17 +95,152 @@ __global__ void k_caps(const int64_t *__restrict__ cptr, int64_t *__restrict__ c
         cap[i] = cptr[i + 1] - cptr[i];
 }
 
+// ---------------------------------------------------------------- host-side row facts
+
+struct HostCsr {
+    int64_t rows, cols;
+    const int64_t *rp;
+    const int64_t *col;
+    const double *val;
+};
+
+// Whether every row's columns ascend (sorted) and never repeat (distinct):
+// one pass over the host columns on a few threads.  Decides whether B chunks
+// may be split (A sorted) and the lane-split numeric mode (B distinct).
+void host_row_order(const HostCsr &h, bool *sorted, bool *distinct) {
+    const int64_t rows = h.rows;
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (h.rp[rows] < ((int64_t)1 << 22)) nt = 1;
+    std::vector<int> uns(nt, 0), dup(nt, 0);
+    auto work = [&](unsigned t) {
+        const int64_t lo = rows * t / nt, hi = rows * (t + 1) / nt;
+        int u = 0, d = 0;
+        for (int64_t i = lo; i < hi && !u; ++i)
+            for (int64_t e = h.rp[i] + 1; e < h.rp[i + 1]; ++e) {
+                if (h.col[e] < h.col[e - 1]) { u = 1; break; }
+                if (h.col[e] == h.col[e - 1]) d = 1;
+            }
+        uns[t] = u;
+        dup[t] = d;
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto &x : th) x.join();
+    bool u = false, d = false;
+    for (unsigned t = 0; t < nt; ++t) {
+        u |= uns[t] != 0;
+        d |= dup[t] != 0;
+    }
+    *sorted = !u;
+    *distinct = !u && !d;
+}
+
+int64_t host_max_row(const int64_t *rp, int64_t lo, int64_t hi) {
+    int64_t m = 0;
+    for (int64_t i = lo; i < hi; ++i) m = std::max(m, rp[i + 1] - rp[i]);
+    return m;
+}
+
+// Split each range of `bounds` into `k` sub-ranges of near-equal entries
+// (by the host row pointers); empty pieces are dropped.
+std::vector<int64_t> refine(const int64_t *bounds, int64_t n, int k, const int64_t *rp) {
+    std::vector<int64_t> out{bounds[0]};
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t lo = bounds[r], hi = bounds[r + 1];
+        for (int p = 1; p <= k; ++p) {
+            int64_t cut;
+            if (p == k) {
+                cut = hi;
+            } else {
+                const int64_t target = rp[lo] + (rp[hi] - rp[lo]) * p / k;
+                cut = std::lower_bound(rp + lo, rp + hi + 1, target) - rp;
+                cut = std::max(cut, out.back());
+                cut = std::min(cut, hi);
+            }
+            if (cut > out.back()) out.push_back(cut);
+        }
+        if (out.back() != hi) out.push_back(hi);
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------- device slots
+
 // A row range [lo, hi) of a host CSR staged in HBM (rebased row pointers).
 struct DevRange {
-    tsg_csr m{};          // device view (rp rebased, int32 cols)
-    int64_t *stage = nullptr;      // int64 column staging
-    int64_t *stage_rp = nullptr;   // int64 row pointer staging
+    tsg_csr m{};                   // device view (rp rebased, int32 cols, fp64 vals)
+    int64_t *stage_rp = nullptr;   // int64 host row pointers of the range
     int64_t cap_rows = 0, cap_nnz = 0;
-    cudaEvent_t ready{};           // host data landed (copy-in stream)
-    // rebasing / narrowing still owed on the compute stream (see finish_rows)
-    bool pending = false;
-    int64_t pend_rows = 0, pend_nnz = 0, pend_base = 0, pend_cols = 0;
+    cudaEvent_t cols_in{}, conv{}, ready{};
 };
+
+// the arena's size class of an allocation (tsg_core.cu size_class)
+int64_t rnd(int64_t bytes) {
+    if (bytes <= 4096) return 4096;
+    if (bytes <= ((int64_t)1 << 20)) {
+        int64_t p = 4096;
+        while (p < bytes) p <<= 1;
+        return p;
+    }
+    return (bytes + ((int64_t)1 << 20) - 1) & ~(((int64_t)1 << 20) - 1);
+}
+
+int64_t slot_ab_bytes(int64_t rows, int64_t nnz) {
+    return rnd(8 * (rows + 2)) + rnd(4 * (nnz + 1)) + rnd(8 * (nnz + 1)) + rnd(8 * (rows + 2));
+}
+
+int64_t slot_c_bytes(int64_t rows, int64_t nnz) {
+    return rnd(8 * (rows + 2)) + rnd(8 * (rows + 1)) + rnd(4 * (nnz + 1)) + rnd(8 * (nnz + 1)) +
+           rnd(4 * (rows + 1));
+}
+
+// per-step temporaries: compressed B chunk (tsg_compress_impl: 12 B per
+// entry + 12 B per row output, head / prefix bit words, per-row fallback
+// arrays) and the fused step's bounds / bins / row lists
+int64_t step_scratch_bytes(int64_t ac_rows, int64_t b_rows, int64_t b_nnz) {
+    const int64_t compress = rnd(8 * (b_rows + 1)) + rnd(4 * (b_rows + 2)) + rnd(4 * (b_nnz + 1)) +
+                             rnd(8 * (b_nnz + 1)) + 3 * rnd(4 * (b_nnz / 32 + 1)) +
+                             rnd(8 * (b_nnz / 8192 + 2)) * 2 + rnd(4 * (b_rows + 1)) + rnd(8 * (b_rows + 1));
+    const int64_t fused = rnd(8 * (ac_rows + 1)) + rnd(ac_rows + 1) + rnd(4 * (ac_rows + 1)) +
+                          rnd(4 * (ac_rows / 1024 + 1) * 16) * 2;
+    return compress + fused + ((int64_t)4 << 20);
+}
+
+int ensure(tsg_ctx *c, DevRange &d, int64_t rows, int64_t nnz) {
+    if (rows > d.cap_rows || nnz > d.cap_nnz) {
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        tsg_free(c, d.m.rp);
+        tsg_free(c, d.m.col);
+        tsg_free(c, d.m.val);
+        tsg_free(c, d.stage_rp);
+        d.cap_rows = std::max(rows, d.cap_rows);
+        d.cap_nnz = std::max(nnz, d.cap_nnz);
+        TSG_TRY(tsg_alloc_t(c, &d.m.rp, d.cap_rows + 2));
+        TSG_TRY(tsg_alloc_t(c, &d.m.col, d.cap_nnz + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.m.val, d.cap_nnz + 1));
+        TSG_TRY(tsg_alloc_t(c, &d.stage_rp, d.cap_rows + 2));
+    }
+    if (!d.ready) {
+        TSG_CK(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&d.cols_in, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&d.conv, cudaEventDisableTiming));
+    }
+    return TSG_OK;
+}
+
+void release(tsg_ctx *c, DevRange &d) {
+    tsg_free(c, d.m.rp);
+    tsg_free(c, d.m.col);
+    tsg_free(c, d.m.val);
+    tsg_free(c, d.stage_rp);
+    if (d.ready) {
+        cudaEventDestroy(d.ready);
+        cudaEventDestroy(d.cols_in);
+        cudaEventDestroy(d.conv);
+    }
+    d = DevRange();
+}
 
 // Optional timeline (TSG_CHUNK_TIMELINE=1): events around every H2D stage,
 // D2H drain and fused step, printed relative to the call's start.
@@ -93,11 +248,10 @@ struct Timeline {
     bool on = false;
     cudaEvent_t base{};
     std::vector<std::pair<char, std::pair<cudaEvent_t, cudaEvent_t>>> iv;
-    void begin(char kind, cudaStream_t s, cudaEvent_t &e0) {
+    void begin(cudaStream_t s, cudaEvent_t &e0) {
         if (!on) return;
         cudaEventCreate(&e0);
         cudaEventRecord(e0, s);
-        (void)kind;
     }
     void end(char kind, cudaStream_t s, cudaEvent_t e0) {
         if (!on) return;
@@ -109,110 +263,44 @@ struct Timeline {
 };
 Timeline g_tl;
 
-struct HostCsr {
-    int64_t rows, cols;
-    const int64_t *rp;
-    const int64_t *col;
-    const double *val;
-};
-
-int ensure(tsg_ctx *c, DevRange &d, int64_t rows, int64_t nnz, bool values, bool *fresh) {
-    *fresh = false;
-    if (rows > d.cap_rows || nnz > d.cap_nnz) {
-        *fresh = true;
-        tsg_free(c, d.m.rp);
-        tsg_free(c, d.m.col);
-        tsg_free(c, d.m.val);
-        tsg_free(c, d.stage);
-        tsg_free(c, d.stage_rp);
-        d.cap_rows = rows > d.cap_rows ? rows : d.cap_rows;
-        d.cap_nnz = nnz > d.cap_nnz ? nnz : d.cap_nnz;
-        TSG_TRY(tsg_alloc_t(c, &d.m.rp, d.cap_rows + 2));
-        TSG_TRY(tsg_alloc_t(c, &d.m.col, d.cap_nnz + 1));
-        if (values) TSG_TRY(tsg_alloc_t(c, &d.m.val, d.cap_nnz + 1));
-        TSG_TRY(tsg_alloc_t(c, &d.stage, d.cap_nnz + 2));
-        TSG_TRY(tsg_alloc_t(c, &d.stage_rp, d.cap_rows + 2));
-    }
-    if (!d.ready) TSG_CK(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
-    return TSG_OK;
-}
-
-void release(tsg_ctx *c, DevRange &d) {
-    tsg_free(c, d.m.rp);
-    tsg_free(c, d.m.col);
-    tsg_free(c, d.m.val);
-    tsg_free(c, d.stage);
-    tsg_free(c, d.stage_rp);
-    if (d.ready) cudaEventDestroy(d.ready);
-    d = DevRange();
-}
-
-// H2D of host rows [lo, hi) on the copy-in stream -- copies only: a kernel
-// queued behind a bulk copy on one stream was measured to hold back kernels
-// of other streams until that copy finished, so the rebasing / narrowing is
-// owed to the compute stream (finish_rows, right before the first use).
-int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d,
-               cudaEvent_t wait_free, int64_t &bytes) {
+// H2D of host rows [lo, hi) on the copy-in stream.  The int64 columns land in
+// the slot's value array, the convert stream narrows them into the int32
+// column array (and rebases the row pointers), then the values overwrite the
+// staging.  No kernel is ever queued on the copy stream (a kernel queued
+// behind a bulk copy was measured to hold back kernels of other streams).
+int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d, cudaEvent_t wait_free,
+               bool sorted, bool distinct, int64_t &bytes) {
     const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
-    bool fresh = false;
-    TSG_TRY(ensure(c, d, rows, nnz, h.val != nullptr, &fresh));
-    d.m.sorted = 0;      // host rows not inspected here: finish_rows checks them on the device
-    d.m.distinct = 0;
-    d.m.max_row = -1;
-    cudaStream_t s = c->copy_in;
-    // freshly allocated buffers come from the compute-stream-ordered arena:
-    // order the copy stream after the compute stream's current position
-    // (steady state reuses the slot's buffers and waits only for `wait_free`)
-    if (fresh) {
-        TSG_CK(cudaEventRecord(d.ready, c->stream));
-        TSG_CK(cudaStreamWaitEvent(s, d.ready, 0));
-    }
+    TSG_TRY(ensure(c, d, rows, nnz));
+    d.m.sorted = sorted ? 1 : 0;
+    d.m.distinct = distinct ? 1 : 0;
+    d.m.max_row = host_max_row(h.rp, lo, hi);
+    cudaStream_t s = c->copy_in, cs = c->convert;
     if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
     cudaEvent_t tl0{};
-    g_tl.begin('H', s, tl0);
+    g_tl.begin(s, tl0);
     TSG_TRY(tsg_copy(d.stage_rp, h.rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    int64_t *col64 = reinterpret_cast<int64_t *>(d.m.val);
+    if (nnz > 0) TSG_TRY(tsg_copy(col64, h.col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    TSG_CK(cudaEventRecord(d.cols_in, s));
+    TSG_CK(cudaStreamWaitEvent(cs, d.cols_in, 0));
+    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, cs>>>(d.stage_rp, d.m.rp, rows + 1, e0);
+    ++c->launches;
     if (nnz > 0) {
-        TSG_TRY(tsg_copy(d.stage, h.col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        if (h.val)
-            TSG_TRY(tsg_copy(d.m.val, h.val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, cs>>>(col64, d.m.col, nnz, h.cols, c->d_err);
+        ++c->launches;
     }
+    TSG_CK(cudaGetLastError());
+    TSG_CK(cudaEventRecord(d.conv, cs));
+    TSG_CK(cudaStreamWaitEvent(s, d.conv, 0));
+    if (nnz > 0 && h.val)
+        TSG_TRY(tsg_copy(d.m.val, h.val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
     g_tl.end('H', s, tl0);
     TSG_CK(cudaEventRecord(d.ready, s));
-    d.pending = true;
-    d.pend_rows = rows;
-    d.pend_nnz = nnz;
-    d.pend_base = e0;
-    d.pend_cols = h.cols;
     d.m.rows = rows;
     d.m.cols = h.cols;
     d.m.nnz = nnz;
     bytes += (rows + 1) * 8 + nnz * (h.val ? 16 : 8);
-    return TSG_OK;
-}
-
-// On the compute stream: wait for the staged copies, rebase the row pointers
-// and narrow the columns (range-checked) into the device view.
-int finish_rows(tsg_ctx *c, DevRange &d) {
-    if (!d.pending) return TSG_OK;
-    cudaStream_t s = c->stream;
-    TSG_CK(cudaStreamWaitEvent(s, d.ready, 0));
-    k_rebase<<<grid_for(d.pend_rows + 1, 256, c->num_sms * 8), 256, 0, s>>>(d.stage_rp, d.m.rp,
-                                                                           d.pend_rows + 1, d.pend_base);
-    ++c->launches;
-    if (d.pend_nnz > 0) {
-        k_narrow<<<grid_for(d.pend_nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.m.col, d.pend_nnz,
-                                                                             d.pend_cols, c->d_err);
-        ++c->launches;
-    }
-    TSG_CK(cudaGetLastError());
-    d.pending = false;
-    if (tsg_trace_enabled()) {
-        cudaStreamSynchronize(s);
-        int eh[2];
-        cudaMemcpy(eh, c->d_err, sizeof(eh), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "[tsg chunk] staged %lld rows nnz %lld ncols %lld err %d/%d\n",
-                (long long)d.pend_rows, (long long)d.pend_nnz, (long long)d.pend_cols, eh[0], eh[1]);
-    }
     return TSG_OK;
 }
 
@@ -221,53 +309,36 @@ struct DevC {
     int64_t *cptr = nullptr;   // rebased final row pointers (rows + 1)
     int64_t *cap = nullptr;    // capacities (rows)
     int32_t *col = nullptr;
-    double *val = nullptr;
+    double *val = nullptr;     // also the int64 column staging of transfers
     int32_t *plen = nullptr;   // running partial lengths
-    int64_t *stage = nullptr;  // int64 column staging for transfers
-    int64_t *rp_stage = nullptr;   // host row pointers of the range (copy-in stream)
     int64_t cap_rows = 0, cap_nnz = 0;
     cudaEvent_t drained{};     // D2H of this buffer finished
-    cudaEvent_t rp_ready{};    // rp_stage landed
+    cudaEvent_t done{}, vals_out{}, widened{};
 };
 
 int ensure_c(tsg_ctx *c, DevC &d, int64_t rows, int64_t nnz) {
     if (rows > d.cap_rows || nnz > d.cap_nnz) {
-        // the old buffers may still be read by this slot's previous D2H
         if (d.drained) TSG_CK(cudaEventSynchronize(d.drained));
         TSG_CK(cudaStreamSynchronize(c->stream));
-        tsg_free(c, d.rp_stage);
         tsg_free(c, d.cptr);
         tsg_free(c, d.cap);
         tsg_free(c, d.col);
         tsg_free(c, d.val);
         tsg_free(c, d.plen);
-        tsg_free(c, d.stage);
-        d.cap_rows = rows > d.cap_rows ? rows : d.cap_rows;
-        d.cap_nnz = nnz > d.cap_nnz ? nnz : d.cap_nnz;
+        d.cap_rows = std::max(rows, d.cap_rows);
+        d.cap_nnz = std::max(nnz, d.cap_nnz);
         TSG_TRY(tsg_alloc_t(c, &d.cptr, d.cap_rows + 2));
         TSG_TRY(tsg_alloc_t(c, &d.cap, d.cap_rows + 1));
         TSG_TRY(tsg_alloc_t(c, &d.col, d.cap_nnz + 1));
         TSG_TRY(tsg_alloc_t(c, &d.val, d.cap_nnz + 1));
         TSG_TRY(tsg_alloc_t(c, &d.plen, d.cap_rows + 1));
-        TSG_TRY(tsg_alloc_t(c, &d.stage, d.cap_nnz + d.cap_rows + 2));
-        TSG_TRY(tsg_alloc_t(c, &d.rp_stage, d.cap_rows + 2));
     }
-    if (!d.drained) TSG_CK(cudaEventCreateWithFlags(&d.drained, cudaEventDisableTiming));
-    if (!d.rp_ready) TSG_CK(cudaEventCreateWithFlags(&d.rp_ready, cudaEventDisableTiming));
-    return TSG_OK;
-}
-
-// Row pointers of a C range staged early on the copy-in stream, so opening
-// the range later does not queue a small H2D behind the bulk chunk copies.
-int stage_c_rows(tsg_ctx *c, const int64_t *c_rp, DevC &d, int64_t lo, int64_t hi, int64_t &bytes) {
-    const int64_t rows = hi - lo, nnz = c_rp[hi] - c_rp[lo];
-    TSG_TRY(ensure_c(c, d, rows, nnz));
-    // rp_stage of this slot was last read by open_c of range r-2 on the
-    // compute stream; the caller's preceding A stage already made copy-in
-    // wait for that range's steps (used_a)
-    TSG_TRY(tsg_copy(d.rp_stage, c_rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->copy_in));
-    TSG_CK(cudaEventRecord(d.rp_ready, c->copy_in));
-    bytes += (rows + 1) * 8;
+    if (!d.drained) {
+        TSG_CK(cudaEventCreateWithFlags(&d.drained, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&d.vals_out, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&d.widened, cudaEventDisableTiming));
+    }
     return TSG_OK;
 }
 
@@ -277,11 +348,32 @@ void release_c(tsg_ctx *c, DevC &d) {
     tsg_free(c, d.col);
     tsg_free(c, d.val);
     tsg_free(c, d.plen);
-    tsg_free(c, d.stage);
-    tsg_free(c, d.rp_stage);
-    if (d.drained) cudaEventDestroy(d.drained);
-    if (d.rp_ready) cudaEventDestroy(d.rp_ready);
+    if (d.drained) {
+        cudaEventDestroy(d.drained);
+        cudaEventDestroy(d.done);
+        cudaEventDestroy(d.vals_out);
+        cudaEventDestroy(d.widened);
+    }
     d = DevC();
+}
+
+// Row pointers of a C range, staged early on the copy-in stream (two small
+// buffers, independent of the C slots) so opening the range later does not
+// queue a small H2D behind the bulk chunk copies.
+struct CRows {
+    int64_t *rp = nullptr;
+    int64_t cap_rows = 0;
+    cudaEvent_t ready{}, used{};
+};
+
+int stage_c_rows(tsg_ctx *c, const int64_t *c_rp, CRows &d, int64_t lo, int64_t hi, int64_t &bytes) {
+    const int64_t rows = hi - lo;
+    // this buffer was last read by open_c two ranges ago (compute stream)
+    TSG_CK(cudaStreamWaitEvent(c->copy_in, d.used, 0));
+    TSG_TRY(tsg_copy(d.rp, c_rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->copy_in));
+    TSG_CK(cudaEventRecord(d.ready, c->copy_in));
+    bytes += (rows + 1) * 8;
+    return TSG_OK;
 }
 
 struct Job {
@@ -295,28 +387,31 @@ struct Job {
 };
 
 // C range setup on the compute stream: row pointers (rebased) + capacities;
-// optionally load a partial (order 2) from host.
-int open_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool load_partial, bool rp_staged = false) {
+// optionally load a partial (order 2) from host.  `staged`: the row pointers
+// were queued on the copy-in stream by stage_c_rows; else they are copied
+// here on the compute stream into the same buffer.
+int open_c(Job &J, DevC &d, CRows &cr, bool staged, int64_t lo, int64_t hi, bool load_partial) {
     tsg_ctx *c = J.c;
     const int64_t rows = hi - lo, e0 = J.c_rp[lo], nnz = J.c_rp[hi] - e0;
     cudaStream_t s = c->stream;
-    if (rp_staged) {
-        TSG_CK(cudaStreamWaitEvent(s, d.rp_ready, 0));
+    TSG_CK(cudaStreamWaitEvent(s, d.drained, 0));   // previous D2H of this buffer
+    if (staged) {
+        TSG_CK(cudaStreamWaitEvent(s, cr.ready, 0));
     } else {
-        TSG_TRY(ensure_c(c, d, rows, nnz));
-        TSG_TRY(tsg_copy(d.rp_stage, J.c_rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        TSG_TRY(tsg_copy(cr.rp, J.c_rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
         J.st->h2d_bytes += (rows + 1) * 8;
     }
-    TSG_CK(cudaStreamWaitEvent(s, d.drained, 0));   // previous D2H of this buffer
-    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, s>>>(d.rp_stage, d.cptr, rows + 1, e0); ++c->launches;
+    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, s>>>(cr.rp, d.cptr, rows + 1, e0); ++c->launches;
     k_caps<<<grid_for(rows, 256, c->num_sms * 8), 256, 0, s>>>(d.cptr, d.cap, rows); ++c->launches;
+    TSG_CK(cudaEventRecord(cr.used, s));
     if (load_partial) {
         TSG_TRY(tsg_copy(d.plen, J.h_plen + lo, rows * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         if (nnz > 0) {
-            TSG_TRY(tsg_copy(d.stage, J.c_col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            int64_t *col64 = reinterpret_cast<int64_t *>(d.val);
+            TSG_TRY(tsg_copy(col64, J.c_col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
             // only each row's partial prefix (plen) is meaningful; the capacity
             // tail is stale host memory and is never read, so no range check
-            k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(d.stage, d.col, nnz, -1,
+            k_narrow<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, s>>>(col64, d.col, nnz, -1,
                                                                          c->d_err); ++c->launches;
             TSG_TRY(tsg_copy(d.val, J.c_val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
         }
@@ -328,31 +423,114 @@ int open_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool load_partial, bool rp_s
     return TSG_OK;
 }
 
-// D2H of a C range (columns widened to int64) on the copy-out stream.
+// D2H of a C range: values first (copy-out stream), then the convert stream
+// widens the columns into the value array and the copy-out stream drains them
+// as int64.  `drained` fires when the slot is free again.
 int drain_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool with_plen) {
     tsg_ctx *c = J.c;
     const int64_t rows = hi - lo, e0 = J.c_rp[lo], nnz = J.c_rp[hi] - e0;
-    cudaEvent_t done;
-    TSG_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    if (nnz > 0) {
-        k_widen<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, c->stream>>>(d.col, d.stage, nnz); ++c->launches;
-    }
-    TSG_CK(cudaEventRecord(done, c->stream));
-    cudaStream_t s = c->copy_out;
-    TSG_CK(cudaStreamWaitEvent(s, done, 0));
+    cudaStream_t s = c->copy_out, cs = c->convert;
+    TSG_CK(cudaEventRecord(d.done, c->stream));
+    TSG_CK(cudaStreamWaitEvent(s, d.done, 0));
     cudaEvent_t tl0{};
-    g_tl.begin('D', s, tl0);
-    if (nnz > 0) {
-        TSG_TRY(tsg_copy(J.c_col + e0, d.stage, nnz * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        TSG_TRY(tsg_copy(J.c_val + e0, d.val, nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
-    }
+    g_tl.begin(s, tl0);
+    if (nnz > 0) TSG_TRY(tsg_copy(J.c_val + e0, d.val, nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (with_plen)
         TSG_TRY(tsg_copy(J.h_plen + lo, d.plen, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (nnz > 0) {
+        TSG_CK(cudaEventRecord(d.vals_out, s));
+        TSG_CK(cudaStreamWaitEvent(cs, d.vals_out, 0));
+        int64_t *col64 = reinterpret_cast<int64_t *>(d.val);
+        k_widen<<<grid_for(nnz, 256, c->num_sms * 16), 256, 0, cs>>>(d.col, col64, nnz); ++c->launches;
+        TSG_CK(cudaGetLastError());
+        TSG_CK(cudaEventRecord(d.widened, cs));
+        TSG_CK(cudaStreamWaitEvent(s, d.widened, 0));
+        TSG_TRY(tsg_copy(J.c_col + e0, col64, nnz * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
     g_tl.end('D', s, tl0);
     TSG_CK(cudaEventRecord(d.drained, s));
-    TSG_CK(cudaEventDestroy(done));
     J.st->d2h_bytes += nnz * 16 + (with_plen ? rows * 4 : 0);
     return TSG_OK;
+}
+
+// ---------------------------------------------------------------- physical layout choice
+
+struct Layout {
+    int a_slots = 2, c_slots = 2, b_slots = 3;
+    int ac_split = 1, b_split = 1;
+    int64_t bytes = 0;
+    std::vector<int64_t> acb, bb;   // physical range / chunk bounds
+};
+
+struct MaxDims {
+    int64_t a_rows = 0, a_nnz = 0, c_nnz = 0, b_rows = 0, b_nnz = 0;
+};
+
+MaxDims max_dims(const Job &J, const std::vector<int64_t> &acb, const std::vector<int64_t> &bb) {
+    MaxDims m;
+    for (size_t r = 0; r + 1 < acb.size(); ++r) {
+        const int64_t lo = acb[r], hi = acb[r + 1];
+        m.a_rows = std::max(m.a_rows, hi - lo);
+        m.a_nnz = std::max(m.a_nnz, J.A.rp[hi] - J.A.rp[lo]);
+        m.c_nnz = std::max(m.c_nnz, J.c_rp[hi] - J.c_rp[lo]);
+    }
+    for (size_t j = 0; j + 1 < bb.size(); ++j) {
+        m.b_rows = std::max(m.b_rows, bb[j + 1] - bb[j]);
+        m.b_nnz = std::max(m.b_nnz, J.B.rp[bb[j + 1]] - J.B.rp[bb[j]]);
+    }
+    return m;
+}
+
+int64_t layout_bytes(const MaxDims &m, int a_slots, int c_slots, int b_slots) {
+    return a_slots * slot_ab_bytes(m.a_rows, m.a_nnz) + c_slots * slot_c_bytes(m.a_rows, m.c_nnz) +
+           2 * rnd(8 * (m.a_rows + 2)) + b_slots * slot_ab_bytes(m.b_rows, m.b_nnz) +
+           step_scratch_bytes(m.a_rows, m.b_rows, m.b_nnz);
+}
+
+// Pick buffering and splitting that fit `budget` (0: unlimited), preferring
+// layouts that move no extra PCIe bytes and keep every stage overlapped.
+int choose_layout(const Job &J, int algo, const int64_t *acb0, int64_t nac, const int64_t *bb0, int64_t nb,
+                  bool a_sorted, int64_t budget, Layout &out) {
+    const int splits[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+    // order 0/1: B streams (split B chunks, neutral when A rows are sorted);
+    // order 2: A/C stream (split A/C ranges, neutral)
+    const bool streamed_b = algo != 2;
+    const int nb_slots_full = streamed_b ? (int)std::min<int64_t>(3, nac * nb) : (nb > 1 ? 2 : 1);
+    for (int extra = 1; extra <= 32; extra = extra < 2 ? 2 : extra * 2) {   // traffic-raising split
+        for (int cs = 2; cs >= 1; --cs)
+            for (int as = 2; as >= 1; --as)
+                for (int bs = nb_slots_full; bs >= 1; --bs)
+                    for (int sp : splits) {
+                        if (streamed_b && sp > 1 && !a_sorted) break;
+                        Layout L;
+                        L.a_slots = as;
+                        L.c_slots = cs;
+                        L.b_slots = bs;
+                        if (streamed_b) {
+                            L.b_split = sp;
+                            L.ac_split = extra;
+                        } else {
+                            L.ac_split = sp * extra;
+                            L.b_split = 1;
+                            if (extra > 1) break;   // order 2 never needs a traffic-raising split
+                        }
+                        L.acb = refine(acb0, nac, L.ac_split, J.A.rp);
+                        L.bb = refine(bb0, nb, L.b_split, J.B.rp);
+                        if (streamed_b && L.b_slots > (int64_t)(L.acb.size() - 1) * (int64_t)(L.bb.size() - 1))
+                            continue;
+                        const MaxDims m = max_dims(J, L.acb, L.bb);
+                        L.bytes = layout_bytes(m, as, cs, bs);
+                        if (budget <= 0 || L.bytes <= budget) {
+                            out = L;
+                            return TSG_OK;
+                        }
+                        if (budget <= 0) break;
+                    }
+        if (!streamed_b) break;
+    }
+    tsg_set_error("chunk plan does not fit in the HBM budget of %lld bytes even fully split "
+                  "(the largest A/C row range or B chunk row is too big)", (long long)budget);
+    return TSG_ECAPACITY;
 }
 
 }  // namespace
@@ -363,7 +541,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                                   const int64_t *b_col, const double *b_val, const int64_t *c_rp,
                                   int64_t *c_col, double *c_val, int64_t n_ac,
                                   const int64_t *ac_bounds, int64_t n_b, const int64_t *b_bounds,
-                                  tsg_chunk_stats *stats) {
+                                  int64_t budget_bytes, tsg_chunk_stats *stats) {
     if (a_cols != b_rows) {
         tsg_set_error("A has %lld cols but B has %lld rows", (long long)a_cols, (long long)b_rows);
         return TSG_EDIM;
@@ -386,34 +564,47 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         cudaEventRecord(g_tl.base, c->stream);
     }
     auto t0 = std::chrono::steady_clock::now();
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    // cached blocks could serve a slot with up to 25 % slack: start from an
+    // empty cache so the footprint is the modelled one
+    tsg_arena_trim(c);
+    const int64_t mem0 = c->bytes_in_use;
+    c->bytes_peak = mem0;
     Job J{c, {a_rows, a_cols, a_rp, a_col, a_val}, {b_rows, b_cols, b_rp, b_col, b_val}, c_rp,
           c_col, c_val, nullptr, &local};
+
+    bool a_sorted = false, a_distinct = false, b_sorted = false, b_distinct = false;
+    host_row_order(J.A, &a_sorted, &a_distinct);
+    host_row_order(J.B, &b_sorted, &b_distinct);
+    int64_t whole[2] = {0, a_rows};
+    const int64_t *acb0 = algo == 0 ? whole : ac_bounds;
+    const int64_t nac0 = algo == 0 ? 1 : n_ac;
+    Layout L;
+    TSG_TRY(choose_layout(J, algo, acb0, nac0, b_bounds, n_b, a_sorted, budget_bytes, L));
+    const int64_t nac = (int64_t)L.acb.size() - 1, nb = (int64_t)L.bb.size() - 1;
+    const int64_t *acb = L.acb.data(), *bb = L.bb.data();
+
     // host partial lengths (order 2): pinned, so their D2H stays asynchronous
-    // (a copy into pageable memory would block the host until the whole C
-    // drain ahead of it finished)
     int32_t *plen_host = nullptr;
-    constexpr int NBS = 3;   // B chunk slots: the copy two steps ahead never waits on compute
+    constexpr int NBS = 3;
     DevRange Abuf[2], Bbuf[NBS];
     DevC Cbuf[2];
-    cudaEvent_t used[NBS] = {nullptr, nullptr, nullptr};   // compute finished with a Bbuf slot
+    CRows crow[2];
+    cudaEvent_t used[NBS], used_a[2];   // compute finished with a B / A slot
     for (int i = 0; i < NBS; i++) TSG_CK(cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming));
-    cudaEvent_t used_a[2] = {nullptr, nullptr};   // compute finished with Abuf slot
-    for (int i = 0; i < 2; i++) TSG_CK(cudaEventCreateWithFlags(&used_a[i], cudaEventDisableTiming));
-    // per-step kernel timing events, read once at the end: the host never
-    // waits for a fused step, so the next chunks' copies queue behind it
+    for (int i = 0; i < 2; i++) {
+        TSG_CK(cudaEventCreateWithFlags(&used_a[i], cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&crow[i].ready, cudaEventDisableTiming));
+        TSG_CK(cudaEventCreateWithFlags(&crow[i].used, cudaEventDisableTiming));
+    }
+    // per-step kernel timing events, read once at the end
     std::vector<cudaEvent_t> kev;
     float kernel_ms = 0.f;
     int st = TSG_OK;
 
-    auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi,
-                          int64_t rows) -> int {
-        TSG_TRY(finish_rows(c, A));
-        const bool fresh_b = B.pending;
-        TSG_TRY(finish_rows(c, B));
-        // row order of a freshly staged B chunk, learnt on the device: enables
-        // the compress fast path and the lane-split numeric mode (a short host
-        // wait for the compute stream, once per staged chunk)
-        if (fresh_b) TSG_TRY(tsg_csr_check_sorted(c, &B.m));
+    auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi, int64_t rows) -> int {
+        TSG_CK(cudaStreamWaitEvent(c->stream, A.ready, 0));
+        TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
         cudaEvent_t e0, e1;
         TSG_CK(cudaEventCreate(&e0));
         TSG_CK(cudaEventCreate(&e1));
@@ -422,137 +613,123 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         TSG_CK(cudaEventRecord(e0, c->stream));
         tsg_cmat *cb = nullptr;
         TSG_TRY(tsg_compress_impl(c, &B.m, &cb));
-        int s2 = tsg_fused_inplace(c, &A.m, (int32_t)blo, (int32_t)bhi, &B.m, cb, C.cptr, C.cap, C.col,
-                                   C.val, C.plen, rows);
-
+        int s2 = tsg_fused_inplace(c, &A.m, (int32_t)blo, (int32_t)bhi, &B.m, cb, C.cptr, C.cap, C.col, C.val,
+                                   C.plen, rows);
         tsg_cmat_free(c, cb);
         TSG_TRY(s2);
         TSG_CK(cudaEventRecord(e1, c->stream));
         return TSG_OK;
     };
 
+    // every slot sized for the largest range / chunk before the pipeline
+    // starts (a mid-run reallocation would wait for the slot's in-flight users)
     {
-        const int64_t *acb = ac_bounds;
-        int64_t nac = n_ac;
-        int64_t whole[2] = {0, a_rows};
-        if (algo == 0) {
-            acb = whole;
-            nac = 1;
+        const MaxDims m = max_dims(J, L.acb, L.bb);
+        for (int i = 0; i < L.a_slots && st == TSG_OK; ++i) st = ensure(c, Abuf[i], m.a_rows, m.a_nnz);
+        for (int i = 0; i < L.c_slots && st == TSG_OK; ++i) st = ensure_c(c, Cbuf[i], m.a_rows, m.c_nnz);
+        for (int i = 0; i < 2 && st == TSG_OK; ++i) {
+            st = tsg_alloc_t(c, &crow[i].rp, m.a_rows + 2);
+            crow[i].cap_rows = m.a_rows;
         }
-        // every slot sized for the largest range / chunk before the pipeline
-        // starts: a mid-run reallocation would have to wait for the slot's
-        // in-flight users (and can make the pool grow under running copies)
-        {
-            int64_t ar = 0, an = 0, cr = 0, cn = 0, br = 0, bn = 0;
-            for (int64_t r = 0; r < nac; ++r) {
-                const int64_t lo = acb[r], hi = acb[r + 1];
-                ar = std::max(ar, hi - lo);
-                an = std::max(an, a_rp[hi] - a_rp[lo]);
-                cn = std::max(cn, c_rp[hi] - c_rp[lo]);
-            }
-            cr = ar;
-            for (int64_t j = 0; j < n_b; ++j) {
-                br = std::max(br, b_bounds[j + 1] - b_bounds[j]);
-                bn = std::max(bn, b_rp[b_bounds[j + 1]] - b_rp[b_bounds[j]]);
-            }
-            bool fresh = false;
-            for (int i = 0; i < 2 && st == TSG_OK; ++i) {
-                st = ensure(c, Abuf[i], ar, an, true, &fresh);
-                if (st == TSG_OK) st = ensure_c(c, Cbuf[i], cr, cn);
-            }
-            // order 2 alternates two B slots (one if B is a single chunk)
-            const int nbs = algo == 2 ? (n_b > 1 ? 2 : 1) : (int)std::min<int64_t>(NBS, nac * n_b);
-            for (int i = 0; i < nbs && st == TSG_OK; ++i) st = ensure(c, Bbuf[i], br, bn, true, &fresh);
-            // grow the driver pool once by the per-step temporaries (compressed
-            // B chunk, symbolic / numeric scratch of a range): growing it later
-            // maps memory while copies are in flight and stalls host and device
-            const size_t grow = (size_t)(bn * 16 + br * 16 + ar * 96) + ((size_t)256 << 20);
-            void *tmp = nullptr;
-            if (st == TSG_OK && cudaMallocAsync(&tmp, grow, c->stream) == cudaSuccess)
-                cudaFreeAsync(tmp, c->stream);
-            else
-                cudaGetLastError();
-            TSG_CK(cudaStreamSynchronize(c->stream));
-        }
+        for (int i = 0; i < L.b_slots && st == TSG_OK; ++i) st = ensure(c, Bbuf[i], m.b_rows, m.b_nnz);
+        // grow the driver pool once by the per-step temporaries: growing it
+        // later maps memory while copies are in flight and stalls host and device
+        const size_t grow = (size_t)step_scratch_bytes(m.a_rows, m.b_rows, m.b_nnz);
+        void *tmp = nullptr;
+        if (st == TSG_OK && cudaMallocAsync(&tmp, grow, c->stream) == cudaSuccess)
+            cudaFreeAsync(tmp, c->stream);
+        else
+            cudaGetLastError();
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < 2; i++) TSG_CK(cudaEventRecord(crow[i].used, c->stream));
     }
-    if (algo == 0 || algo == 1) {
-        const int64_t *acb = ac_bounds;
-        int64_t nac = n_ac;
-        int64_t whole[2] = {0, a_rows};
-        if (algo == 0) {
-            acb = whole;
-            nac = 1;
-        }
-        // Flat schedule over steps s = (range r, chunk j): before step s runs,
-        // the copies of step s+2 are queued (A range when j == 0, B chunk in
-        // slot s % NBS), so the copy engine always has the next transfers
-        // queued while the host blocks inside a fused step.  C ranges are
-        // opened on the compute stream right before their first step.
-        const int64_t nsteps = nac * n_b;
+    local.budget_bytes = budget_bytes;
+    local.a_slots = L.a_slots;
+    local.c_slots = L.c_slots;
+    local.b_slots = L.b_slots;
+    local.ac_split = L.ac_split;
+    local.b_split = L.b_split;
+    local.layout_bytes = L.bytes;
 
-        auto issue = [&](int64_t s2) -> int {
-            const int64_t r = s2 / n_b, j = s2 % n_b;
-            if (j == 0) {   // this A slot was last read by range r-2's steps
-                TSG_TRY(stage_rows(c, J.A, acb[r], acb[r + 1], Abuf[r & 1], used_a[r & 1],
-                                   local.h2d_bytes));
-                TSG_TRY(stage_c_rows(c, J.c_rp, Cbuf[r & 1], acb[r], acb[r + 1], local.h2d_bytes));
+    if (st == TSG_OK && algo != 2) {
+        // Flat schedule over steps s = (range r, chunk j): before step s runs,
+        // the copies of step s+ahead are queued (A range when j == 0, B chunk
+        // in slot s % b_slots), so the copy engine always has the next
+        // transfers queued while the host blocks inside a fused step.  C
+        // ranges are opened on the compute stream right before their first step.
+        const int64_t nsteps = nac * nb;
+        const int ahead = std::min(2, L.b_slots - 1);
+        // A range r' (and its C row pointers) may be staged once range
+        // r' - a_slots has released its A slot (used_a recorded): staging
+        // earlier would wait on a stale event and overwrite a slot in use
+        int64_t a_next = 0, finished = 0;
+        auto stage_a = [&]() -> int {
+            while (a_next < nac && a_next - L.a_slots < finished) {
+                const int64_t r = a_next++;
+                TSG_TRY(stage_rows(c, J.A, acb[r], acb[r + 1], Abuf[r % L.a_slots], used_a[r % L.a_slots],
+                                   a_sorted, a_distinct, local.h2d_bytes));
+                TSG_TRY(stage_c_rows(c, J.c_rp, crow[r & 1], acb[r], acb[r + 1], local.h2d_bytes));
             }
-            return stage_rows(c, J.B, b_bounds[j], b_bounds[j + 1], Bbuf[s2 % NBS], used[s2 % NBS],
-                              local.h2d_bytes);
+            return TSG_OK;
         };
-        for (int64_t s2 = 0; s2 < 2 && s2 < nsteps && st == TSG_OK; ++s2) st = issue(s2);
-        auto hnow = [&]() {
-            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        auto issue_b = [&](int64_t s2) -> int {
+            const int64_t j = s2 % nb;
+            return stage_rows(c, J.B, bb[j], bb[j + 1], Bbuf[s2 % L.b_slots], used[s2 % L.b_slots], b_sorted,
+                              b_distinct, local.h2d_bytes);
         };
+        st = stage_a();
+        for (int64_t s2 = 0; s2 <= ahead && s2 < nsteps && st == TSG_OK; ++s2) st = issue_b(s2);
         for (int64_t s2 = 0; s2 < nsteps && st == TSG_OK; ++s2) {
-            const int64_t r = s2 / n_b, j = s2 % n_b;
+            const int64_t r = s2 / nb, j = s2 % nb;
             const int64_t lo = acb[r], hi = acb[r + 1];
-            DevC &C = Cbuf[r & 1];
-            const double h0 = hnow();
-            if (j == 0 && (st = open_c(J, C, lo, hi, false, true)) != TSG_OK) break;
-            if (s2 + 2 < nsteps && (st = issue(s2 + 2)) != TSG_OK) break;
-            const double h1 = hnow();
-            st = fused_step(Abuf[r & 1], Bbuf[s2 % NBS], C, b_bounds[j], b_bounds[j + 1], hi - lo);
-            if (g_tl.on)
-                fprintf(stderr, "[tsg host] step %lld issue %.3f-%.3f fused %.3f-%.3f\n", (long long)s2, h0, h1,
-                        h1, hnow());
-            cudaEventRecord(used[s2 % NBS], c->stream);
-            if (st == TSG_OK && j == n_b - 1) {
-                cudaEventRecord(used_a[r & 1], c->stream);
+            DevC &C = Cbuf[r % L.c_slots];
+            if (j == 0 && (st = open_c(J, C, crow[r & 1], true, lo, hi, false)) != TSG_OK) break;
+            st = fused_step(Abuf[r % L.a_slots], Bbuf[s2 % L.b_slots], C, bb[j], bb[j + 1], hi - lo);
+            if (st != TSG_OK) break;
+            TSG_CK(cudaEventRecord(used[s2 % L.b_slots], c->stream));
+            if (j == nb - 1) {
+                TSG_CK(cudaEventRecord(used_a[r % L.a_slots], c->stream));
                 k_check_full<<<grid_for(hi - lo, 256, c->num_sms * 8), 256, 0, c->stream>>>(
                     C.plen, C.cap, hi - lo, lo, c->d_err); ++c->launches;
                 st = drain_c(J, C, lo, hi, false);
+                finished = r + 1;
+                if (st == TSG_OK) st = stage_a();
             }
+            if (st == TSG_OK && s2 + ahead + 1 < nsteps) st = issue_b(s2 + ahead + 1);
         }
-    } else {
+    } else if (st == TSG_OK) {
         void *ph = nullptr;
         TSG_TRY(tsg_host_alloc(((size_t)a_rows + 1) * sizeof(int32_t), &ph));
         plen_host = static_cast<int32_t *>(ph);
         memset(plen_host, 0, ((size_t)a_rows + 1) * sizeof(int32_t));
         J.h_plen = plen_host;
-        for (int64_t j = 0; j < n_b && st == TSG_OK; ++j) {
-            DevRange &B = Bbuf[j & 1];
-            if ((st = stage_rows(c, J.B, b_bounds[j], b_bounds[j + 1], B, used[j & 1], local.h2d_bytes)) != TSG_OK)
+        for (int64_t j = 0; j < nb && st == TSG_OK; ++j) {
+            DevRange &B = Bbuf[j % L.b_slots];
+            if ((st = stage_rows(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], b_sorted, b_distinct,
+                                 local.h2d_bytes)) != TSG_OK)
                 break;
-            for (int64_t r = 0; r < n_ac && st == TSG_OK; ++r) {
-                const int64_t lo = ac_bounds[r], hi = ac_bounds[r + 1];
-                DevRange &A = Abuf[r & 1];
-                DevC &C = Cbuf[r & 1];
-                if ((st = stage_rows(c, J.A, lo, hi, A, used_a[r & 1], local.h2d_bytes)) != TSG_OK) break;
+            for (int64_t r = 0; r < nac && st == TSG_OK; ++r) {
+                const int64_t lo = acb[r], hi = acb[r + 1];
+                DevRange &A = Abuf[r % L.a_slots];
+                DevC &C = Cbuf[r % L.c_slots];
+                if ((st = stage_rows(c, J.A, lo, hi, A, used_a[r % L.a_slots], a_sorted, a_distinct,
+                                     local.h2d_bytes)) != TSG_OK)
+                    break;
                 // partials come back from host after the first B sweep; the D2H
                 // of the previous sweep for this range must have landed (the
                 // first sweep loads nothing, so its ranges pipeline freely)
                 if (j > 0) TSG_CK(cudaStreamSynchronize(c->copy_out));
-                if ((st = open_c(J, C, lo, hi, j > 0)) != TSG_OK) break;
-                st = fused_step(A, B, C, b_bounds[j], b_bounds[j + 1], hi - lo);
-                cudaEventRecord(used_a[r & 1], c->stream);
+                if ((st = open_c(J, C, crow[r & 1], false, lo, hi, j > 0)) != TSG_OK) break;
+                st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo);
+                TSG_CK(cudaEventRecord(used_a[r % L.a_slots], c->stream));
                 if (st == TSG_OK) st = drain_c(J, C, lo, hi, true);
             }
-            cudaEventRecord(used[j & 1], c->stream);
+            TSG_CK(cudaEventRecord(used[j % L.b_slots], c->stream));
         }
     }
     cudaStreamSynchronize(c->copy_in);
     cudaStreamSynchronize(c->copy_out);
+    cudaStreamSynchronize(c->convert);
     cudaStreamSynchronize(c->stream);
     if (st == TSG_OK) st = tsg_check_kernel_errors(c, "chunked multiply");
     if (st == TSG_OK && algo == 2) {
@@ -565,14 +742,18 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             }
     }
     if (plen_host) tsg_host_free(plen_host);
-    int64_t mem = c->bytes_in_use;
+    const int64_t peak = c->bytes_peak - mem0;
     for (int i = 0; i < 2; i++) {
         release(c, Abuf[i]);
-        release(c, Bbuf[i]);
-        if (i == 1) release(c, Bbuf[2]);
         release_c(c, Cbuf[i]);
+        tsg_free(c, crow[i].rp);
+        cudaEventDestroy(crow[i].ready);
+        cudaEventDestroy(crow[i].used);
+        cudaEventDestroy(used_a[i]);
+    }
+    for (int i = 0; i < NBS; i++) {
+        release(c, Bbuf[i]);
         cudaEventDestroy(used[i]);
-        if (i == 1) cudaEventDestroy(used[2]);
     }
     for (size_t k = 0; k + 1 < kev.size(); k += 2) {
         float ms = 0.f;
@@ -595,12 +776,184 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         g_tl = Timeline();
     }
     for (cudaEvent_t e : kev) cudaEventDestroy(e);
-    for (int i = 0; i < 2; i++) cudaEventDestroy(used_a[i]);
     cudaStreamSynchronize(c->stream);
     local.kernel_ms = kernel_ms;
     local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    local.peak_device_bytes = mem;
+    local.peak_device_bytes = peak;
     if (stats) *stats = local;
+    if (st == TSG_OK && budget_bytes > 0 && peak > budget_bytes) {
+        tsg_set_error("chunked multiply held %lld bytes of HBM, above the budget of %lld",
+                      (long long)peak, (long long)budget_bytes);
+        st = TSG_ECAPACITY;
+    }
+    return st;
+}
+
+// Symbolic counts through the same budget (the
+// reference runs spgemm_symbolic unchunked, cli.py:164-165): B's rows are
+// compressed chunk by chunk (rows compress independently, kernel.py:73-93)
+// into one resident compressed B, then A row ranges stream past it.  Peak
+// HBM = compressed B + one A range (double-buffered when it fits) + scratch;
+// TSG_ECAPACITY if the compressed B alone does not fit.
+namespace {
+__global__ void k_append_cmat(int64_t rows, const int64_t *__restrict__ start, const int32_t *__restrict__ cnt,
+                              const int32_t *__restrict__ set, const uint64_t *__restrict__ bits,
+                              const int64_t *__restrict__ out_start, int32_t *__restrict__ out_cnt,
+                              int32_t *__restrict__ out_set, uint64_t *__restrict__ out_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < rows; i += nw) {
+        const int64_t s0 = start[i], o0 = out_start[i];
+        const int n = cnt[i];
+        for (int k = lane; k < n; k += 32) {
+            out_set[o0 + k] = set[s0 + k];
+            out_bits[o0 + k] = bits[s0 + k];
+        }
+        if (lane == 0) out_cnt[i] = n;
+    }
+}
+
+__global__ void k_add_base(int64_t *__restrict__ v, int64_t n, const int64_t *__restrict__ base) {
+    const int64_t b = *base;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[i] += b;
+}
+}  // namespace
+
+extern "C" int tsg_chunk_symbolic(tsg_ctx *c, int64_t a_rows, int64_t a_cols, const int64_t *a_rp,
+                                  const int64_t *a_col, int64_t b_rows, int64_t b_cols, const int64_t *b_rp,
+                                  const int64_t *b_col, int64_t budget_bytes, int64_t *counts,
+                                  tsg_chunk_stats *stats) {
+    if (a_cols != b_rows) {
+        tsg_set_error("A has %lld cols but B has %lld rows", (long long)a_cols, (long long)b_rows);
+        return TSG_EDIM;
+    }
+    tsg_chunk_stats local;
+    memset(&local, 0, sizeof(local));
+    auto t0 = std::chrono::steady_clock::now();
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    tsg_arena_trim(c);
+    const int64_t mem0 = c->bytes_in_use;
+    c->bytes_peak = mem0;
+    HostCsr HA{a_rows, a_cols, a_rp, a_col, nullptr}, HB{b_rows, b_cols, b_rp, b_col, nullptr};
+    bool a_sorted, a_distinct, b_sorted, b_distinct;
+    host_row_order(HA, &a_sorted, &a_distinct);
+    host_row_order(HB, &b_sorted, &b_distinct);
+    const int64_t b_nnz = b_rp[b_rows];
+    // compressed B capacity: one set per entry at most
+    const int64_t cb_bytes = rnd(8 * (b_rows + 1)) + rnd(4 * (b_rows + 2)) + rnd(4 * (b_nnz + 1)) +
+                             rnd(8 * (b_nnz + 1));
+    const int64_t budget = budget_bytes > 0 ? budget_bytes : ((int64_t)1 << 62);
+    if (cb_bytes >= budget) {
+        tsg_set_error("compressed B (%lld bytes) does not fit in the HBM budget of %lld", (long long)cb_bytes,
+                      (long long)budget_bytes);
+        return TSG_ECAPACITY;
+    }
+    int st = TSG_OK;
+    tsg_cmat *cb = nullptr;
+    TSG_TRY(tsg_cmat_alloc(c, b_rows, b_nnz > 0 ? b_nnz : 1, &cb));
+    cb->cols = b_cols;
+    cb->sorted_sets = 1;
+    int64_t *dcnt64 = nullptr;
+    // B in chunks of rows that fit next to the compressed B: slot + its compression scratch
+    const int64_t room = budget - cb_bytes - ((int64_t)64 << 20);
+    int64_t chunk_nnz = std::max<int64_t>(room / 40, 1 << 20);   // ~12 slot + ~25 compress scratch B/entry
+    std::vector<int64_t> bb{0};
+    for (int64_t r = 0; r < b_rows;) {
+        const int64_t target = b_rp[r] + chunk_nnz;
+        int64_t e = std::upper_bound(b_rp + r, b_rp + b_rows + 1, target) - b_rp - 1;
+        e = std::max(e, r + 1);
+        e = std::min(e, b_rows);
+        bb.push_back(e);
+        r = e;
+    }
+    DevRange slot;
+    int64_t *base_dev = nullptr;
+    TSG_TRY(tsg_alloc_t(c, &base_dev, 2));
+    TSG_TRY(tsg_fill(c, base_dev, 0, 2 * sizeof(int64_t), c->stream));
+    int max_cnt_all = 0;
+    for (size_t j = 0; j + 1 < bb.size() && st == TSG_OK; ++j) {
+        const int64_t lo = bb[j], hi = bb[j + 1];
+        st = stage_rows(c, HB, lo, hi, slot, nullptr, b_sorted, b_distinct, local.h2d_bytes);
+        if (st != TSG_OK) break;
+        TSG_CK(cudaStreamWaitEvent(c->stream, slot.ready, 0));
+        tsg_cmat *part = nullptr;
+        st = tsg_compress_impl(c, &slot.m, &part);
+        if (st != TSG_OK) break;
+        if (!part->sorted_sets) cb->sorted_sets = 0;
+        // compact starts of this chunk = global offset + exclusive scan of counts
+        const int64_t rows = hi - lo;
+        st = tsg_exclusive_scan_i32_to_i64(c, part->cnt, cb->start + lo, rows);
+        if (st == TSG_OK) {
+            k_add_base<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, c->stream>>>(cb->start + lo, rows + 1,
+                                                                                       base_dev);
+            ++c->launches;
+            k_append_cmat<<<grid_for(rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(
+                rows, part->start, part->cnt, part->set, part->bits, cb->start + lo, cb->cnt + lo, cb->set,
+                cb->bits);
+            ++c->launches;
+            TSG_CK(cudaMemcpyAsync(base_dev, cb->start + hi, sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream));
+            int mc = 0;
+            TSG_CK(cudaMemcpyAsync(&mc, part->cnt + rows + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            TSG_CK(cudaStreamSynchronize(c->stream));
+            max_cnt_all = std::max(max_cnt_all, mc);
+        }
+        tsg_cmat_free(c, part);
+        TSG_CK(cudaStreamSynchronize(c->stream));
+    }
+    release(c, slot);
+    if (st == TSG_OK) {
+        TSG_CK(cudaMemcpyAsync(cb->cnt + b_rows + 1, &max_cnt_all, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        cb->dmax_valid = 1;
+    }
+    // A row ranges streamed past the resident compressed B
+    if (st == TSG_OK && a_rows > 0) {
+        const int64_t room_a = budget - (c->bytes_peak - mem0) - ((int64_t)64 << 20);
+        int64_t nsets = 0;
+        TSG_CK(cudaMemcpy(&nsets, cb->start + b_rows, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        // per A row: slot 16 B + 12 B/entry; symbolic: counts, set counts,
+        // bounds, bins, lists (~64 B) and the sorted set lists (12 B per set
+        // of the row's bound = its entries x the mean compressed B row)
+        const double avg = (double)a_rp[a_rows] / (double)std::max<int64_t>(a_rows, 1);
+        const double avg_cb = (double)nsets / (double)std::max<int64_t>(b_rows, 1);
+        const int64_t per_row = (int64_t)(16 + 12 * avg + 96 + 12 * 1.25 * avg * avg_cb) + 1;
+        int64_t range_rows = std::max<int64_t>(room_a / per_row, 1024);
+        TSG_TRY(tsg_alloc_t(c, &dcnt64, 1));
+        for (int64_t lo = 0; lo < a_rows && st == TSG_OK; lo += range_rows) {
+            const int64_t hi = std::min(a_rows, lo + range_rows);
+            st = stage_rows(c, HA, lo, hi, slot, nullptr, a_sorted, a_distinct, local.h2d_bytes);
+            if (st != TSG_OK) break;
+            TSG_CK(cudaStreamWaitEvent(c->stream, slot.ready, 0));
+            tsg_vec *v = nullptr;
+            st = tsg_symbolic_impl(c, hi - lo, &slot.m, 0, 0, 0x7fffffff, cb, nullptr, &v, nullptr);
+            if (st != TSG_OK) break;
+            TSG_CK(cudaMemcpyAsync(counts + lo, v->d, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+            local.d2h_bytes += (hi - lo) * 8;
+            TSG_CK(cudaStreamSynchronize(c->stream));
+            tsg_vec_free(c, v);
+        }
+        release(c, slot);
+    }
+    tsg_free(c, dcnt64);
+    tsg_free(c, base_dev);
+    tsg_cmat_free(c, cb);
+    cudaStreamSynchronize(c->copy_in);
+    cudaStreamSynchronize(c->convert);
+    cudaStreamSynchronize(c->stream);
+    if (st == TSG_OK) st = tsg_check_kernel_errors(c, "chunked symbolic");
+    const int64_t peak = c->bytes_peak - mem0;
+    local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    local.peak_device_bytes = peak;
+    local.budget_bytes = budget_bytes;
+    if (stats) *stats = local;
+    if (st == TSG_OK && budget_bytes > 0 && peak > budget_bytes) {
+        tsg_set_error("chunked symbolic held %lld bytes of HBM, above the budget of %lld", (long long)peak,
+                      (long long)budget_bytes);
+        st = TSG_ECAPACITY;
+    }
     return st;
 }
 

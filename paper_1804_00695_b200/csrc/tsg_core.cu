@@ -76,6 +76,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
         TSG_CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
     }
     TSG_CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    TSG_CK(cudaStreamCreateWithPriority(&c->convert, cudaStreamNonBlocking, prio_hi));
     // keep freed blocks cached in the default pool: no OS round trips per call
     cudaMemPool_t pool;
     TSG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -139,6 +140,7 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
         cudaEventDestroy(c->ev_join[i]);
     }
     cudaEventDestroy(c->ev_fork);
+    cudaStreamDestroy(c->convert);
     delete c;
     return TSG_OK;
 }
@@ -333,6 +335,7 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
             A->cached -= got;
             A->live[*p] = got;
             c->bytes_in_use += (int64_t)got;
+            if (c->bytes_in_use > c->bytes_peak) c->bytes_peak = c->bytes_in_use;
             return TSG_OK;
         }
     }
@@ -352,6 +355,7 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
     std::lock_guard<std::mutex> g(A->mu);
     A->live[raw] = cls;
     c->bytes_in_use += (int64_t)cls;
+    if (c->bytes_in_use > c->bytes_peak) c->bytes_peak = c->bytes_in_use;
     *p = raw;
     return TSG_OK;
 }

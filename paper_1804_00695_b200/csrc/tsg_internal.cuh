@@ -44,6 +44,8 @@ struct tsg_ctx {
     cudaEvent_t ev[8];
     float phase_ms[8];
     int64_t bytes_in_use;
+    int64_t bytes_peak;       // high-water mark of bytes_in_use (the chunked executors reset it)
+    cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
     int64_t launches;         // kernels launched by this context (all entry points)
     cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply

@@ -96,6 +96,34 @@ def test_config4_chunked_64cubed_full_result(cap_mib, algo, n_ac, n_b):
     c, led = ch.execute_plan(a, a, counts, plan, b200_model(fast))
     assert led.total_bytes() == plan.predicted_copy_bytes
     assert_same_product(c, O.multiply(a, a, workers=W), exact=True)
+    # the budget holds physically: the call's allocation high-water mark
+    peak = led.physical["peak_device_bytes"]
+    assert 0 < peak <= fast, (peak, fast, led.physical)
+    assert led.physical["layout_bytes"] <= fast
+
+
+@pytest.mark.parametrize("cap_mib", [128, 224])
+def test_config4_symbolic_within_budget(cap_mib):
+    a = gen.stencil(gen.BRICK3D, (64, 64, 64))
+    want = tsg.spgemm_symbolic(a, tsg.compress(a))
+    counts, st = ch.symbolic_within_budget(a, a, cap_mib << 20)
+    assert np.array_equal(counts, want)
+    assert 0 < st["peak_device_bytes"] <= cap_mib << 20, st
+
+
+def test_chunked_budget_too_small_raises_capacity_error():
+    a = gen.stencil(gen.BRICK3D, (24, 24, 24))
+    counts = tsg.spgemm_symbolic(a, tsg.compress(a))
+    fast = 1 << 20
+    plan = ch.plan_for_multiply(a, a, counts, 64 << 20)
+    with pytest.raises(tsg.CapacityError):   # the reference's simulated residency check
+        ch.execute_plan(a, a, counts, plan, b200_model(fast))
+    from paper_1804_00695_b200.memory import CopyLedger
+    with pytest.raises(tsg.CapacityError):   # the physical executor refuses the layout
+        ch._physical(ch.GPU_CHUNK1_AC_IN_PLACE, a, a, counts, plan.partition_ac.bounds(),
+                     plan.partition_b.bounds(), CopyLedger(b200_model(64 << 20)), fast)
+    with pytest.raises(tsg.CapacityError):
+        ch.symbolic_within_budget(a, a, fast)
 
 
 def test_config5_rmat_scale14_aa_full_result():
