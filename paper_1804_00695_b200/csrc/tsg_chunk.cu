@@ -602,7 +602,10 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     float kernel_ms = 0.f;
     int st = TSG_OK;
 
-    auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi, int64_t rows) -> int {
+    // one fused step; `cb_keep`: B's compressed form shared by the steps of a
+    // resident B chunk (order 2), else compressed here and freed after
+    auto fused_step = [&](DevRange &A, DevRange &B, DevC &C, int64_t blo, int64_t bhi, int64_t rows,
+                          tsg_cmat *cb_keep) -> int {
         TSG_CK(cudaStreamWaitEvent(c->stream, A.ready, 0));
         TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
         cudaEvent_t e0, e1;
@@ -611,11 +614,11 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         kev.push_back(e0);
         kev.push_back(e1);
         TSG_CK(cudaEventRecord(e0, c->stream));
-        tsg_cmat *cb = nullptr;
-        TSG_TRY(tsg_compress_impl(c, &B.m, &cb));
+        tsg_cmat *cb = cb_keep;
+        if (!cb) TSG_TRY(tsg_compress_impl(c, &B.m, &cb));
         int s2 = tsg_fused_inplace(c, &A.m, (int32_t)blo, (int32_t)bhi, &B.m, cb, C.cptr, C.cap, C.col, C.val,
                                    C.plen, rows);
-        tsg_cmat_free(c, cb);
+        if (!cb_keep) tsg_cmat_free(c, cb);
         TSG_TRY(s2);
         TSG_CK(cudaEventRecord(e1, c->stream));
         return TSG_OK;
@@ -684,7 +687,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             const int64_t lo = acb[r], hi = acb[r + 1];
             DevC &C = Cbuf[r % L.c_slots];
             if (j == 0 && (st = open_c(J, C, crow[r & 1], true, lo, hi, false)) != TSG_OK) break;
-            st = fused_step(Abuf[r % L.a_slots], Bbuf[s2 % L.b_slots], C, bb[j], bb[j + 1], hi - lo);
+            st = fused_step(Abuf[r % L.a_slots], Bbuf[s2 % L.b_slots], C, bb[j], bb[j + 1], hi - lo, nullptr);
             if (st != TSG_OK) break;
             TSG_CK(cudaEventRecord(used[s2 % L.b_slots], c->stream));
             if (j == nb - 1) {
@@ -708,6 +711,10 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             if ((st = stage_rows(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], b_sorted, b_distinct,
                                  local.h2d_bytes)) != TSG_OK)
                 break;
+            // the resident chunk is compressed once for all A/C ranges
+            tsg_cmat *cbj = nullptr;
+            TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
+            if ((st = tsg_compress_impl(c, &B.m, &cbj)) != TSG_OK) break;
             for (int64_t r = 0; r < nac && st == TSG_OK; ++r) {
                 const int64_t lo = acb[r], hi = acb[r + 1];
                 DevRange &A = Abuf[r % L.a_slots];
@@ -720,10 +727,11 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 // first sweep loads nothing, so its ranges pipeline freely)
                 if (j > 0) TSG_CK(cudaStreamSynchronize(c->copy_out));
                 if ((st = open_c(J, C, crow[r & 1], false, lo, hi, j > 0)) != TSG_OK) break;
-                st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo);
+                st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo, cbj);
                 TSG_CK(cudaEventRecord(used_a[r % L.a_slots], c->stream));
                 if (st == TSG_OK) st = drain_c(J, C, lo, hi, true);
             }
+            tsg_cmat_free(c, cbj);
             TSG_CK(cudaEventRecord(used[j % L.b_slots], c->stream));
         }
     }

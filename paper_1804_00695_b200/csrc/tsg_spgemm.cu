@@ -327,7 +327,9 @@ struct NumBinF {
     const int32_t *msets;
     const int64_t *sbound;
     int64_t ncols;        // B's columns (> 0: dense tier allowed for rows with sorted sets)
+    int skip_idle = 0;    // in-place fused step: rows with no product in the chunk keep their partial
     __device__ __forceinline__ int operator()(int64_t i) const {
+        if (skip_idle && sbound[i] == 0) return 255;
         const int64_t n = counts[i];
         const int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
         const int b = num_bin(n, m);
@@ -2237,7 +2239,9 @@ __global__ void k_fused_bounds(int64_t rows_out, const int64_t *__restrict__ arp
             if (k >= b_lo && k < b_hi) s += cbcnt[k - b_lo];
         }
         for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-        if (lane == 0) sbound[i] = s + (prp ? prp[i + 1] - prp[i] : 0) + (plen ? plen[i] : 0);
+        // in place (plen): a row with no product in this chunk is left as it
+        // is (bound 0 = skipped by the bin functor)
+        if (lane == 0) sbound[i] = (plen && s == 0) ? 0 : s + (prp ? prp[i + 1] - prp[i] : 0) + (plen ? plen[i] : 0);
     }
 }
 }  // namespace
@@ -2417,7 +2421,7 @@ int tsg_fused_inplace(tsg_ctx *c, const tsg_csr *a, int32_t b_lo, int32_t b_hi, 
         rows, a->rp, a->col, 0, b_lo, b_hi, cb->start, cb->cnt, nullptr, sbound, plen); ++c->launches;
     TSG_CK(cudaGetLastError());
     Bins bl;
-    TSG_TRY(tsg_partition<NBINS>(c, rows, NumBinF{cap, nullptr, sbound, 0}, bins, bl));
+    TSG_TRY(tsg_partition<NBINS>(c, rows, NumBinF{cap, nullptr, sbound, 0, 1}, bins, bl));
     NumArgs na;
     memset(&na, 0, sizeof(na));
     na.arp = a->rp;
