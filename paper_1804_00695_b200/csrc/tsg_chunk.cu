@@ -488,14 +488,26 @@ int64_t layout_bytes(const MaxDims &m, int a_slots, int c_slots, int b_slots) {
 }
 
 // Pick buffering and splitting that fit `budget` (0: unlimited), preferring
-// layouts that move no extra PCIe bytes and keep every stage overlapped.
+// layouts that move no extra PCIe bytes and keep every stage overlapped.  For
+// streamed B (orders 0/1) the smallest split giving three B slots is taken,
+// then the slots are deepened (up to MAX_BS) while they fit: the bytes queued
+// ahead on the copy engine, not the piece size, hide the host's per-step work.
+constexpr int MAX_BS = 8;
+
 int choose_layout(const Job &J, int algo, const int64_t *acb0, int64_t nac, const int64_t *bb0, int64_t nb,
                   bool a_sorted, int64_t budget, Layout &out) {
     const int splits[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
     // order 0/1: B streams (split B chunks, neutral when A rows are sorted);
     // order 2: A/C stream (split A/C ranges, neutral)
     const bool streamed_b = algo != 2;
-    const int nb_slots_full = streamed_b ? (int)std::min<int64_t>(3, nac * nb) : (nb > 1 ? 2 : 1);
+    const int nb_slots_full = streamed_b ? 3 : (nb > 1 ? 2 : 1);
+    auto fits = [&](Layout &L) {
+        L.acb = refine(acb0, nac, L.ac_split, J.A.rp);
+        L.bb = refine(bb0, nb, L.b_split, J.B.rp);
+        const MaxDims m = max_dims(J, L.acb, L.bb);
+        L.bytes = layout_bytes(m, L.a_slots, L.c_slots, L.b_slots);
+        return budget <= 0 || L.bytes <= budget;
+    };
     for (int extra = 1; extra <= 32; extra = extra < 2 ? 2 : extra * 2) {   // traffic-raising split
         for (int cs = 2; cs >= 1; --cs)
             for (int as = 2; as >= 1; --as)
@@ -506,25 +518,23 @@ int choose_layout(const Job &J, int algo, const int64_t *acb0, int64_t nac, cons
                         L.a_slots = as;
                         L.c_slots = cs;
                         L.b_slots = bs;
+                        L.ac_split = streamed_b ? extra : sp;
+                        L.b_split = streamed_b ? sp : 1;
+                        if (!fits(L)) continue;
                         if (streamed_b) {
-                            L.b_split = sp;
-                            L.ac_split = extra;
-                        } else {
-                            L.ac_split = sp * extra;
-                            L.b_split = 1;
-                            if (extra > 1) break;   // order 2 never needs a traffic-raising split
+                            const int64_t steps = (int64_t)(L.acb.size() - 1) * (int64_t)(L.bb.size() - 1);
+                            L.b_slots = (int)std::min<int64_t>(L.b_slots, steps);
+                            while (L.b_slots < MAX_BS && L.b_slots < steps && budget > 0) {
+                                Layout D = L;
+                                D.b_slots = L.b_slots + 1;
+                                if (!fits(D)) break;
+                                L = D;
+                            }
+                            if (budget <= 0) L.b_slots = (int)std::min<int64_t>(3, steps);
+                            fits(L);
                         }
-                        L.acb = refine(acb0, nac, L.ac_split, J.A.rp);
-                        L.bb = refine(bb0, nb, L.b_split, J.B.rp);
-                        if (streamed_b && L.b_slots > (int64_t)(L.acb.size() - 1) * (int64_t)(L.bb.size() - 1))
-                            continue;
-                        const MaxDims m = max_dims(J, L.acb, L.bb);
-                        L.bytes = layout_bytes(m, as, cs, bs);
-                        if (budget <= 0 || L.bytes <= budget) {
-                            out = L;
-                            return TSG_OK;
-                        }
-                        if (budget <= 0) break;
+                        out = L;
+                        return TSG_OK;
                     }
         if (!streamed_b) break;
     }
@@ -586,7 +596,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
 
     // host partial lengths (order 2): pinned, so their D2H stays asynchronous
     int32_t *plen_host = nullptr;
-    constexpr int NBS = 3;
+    constexpr int NBS = MAX_BS;
     DevRange Abuf[2], Bbuf[NBS];
     DevC Cbuf[2];
     CRows crow[2];
@@ -661,7 +671,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         // transfers queued while the host blocks inside a fused step.  C
         // ranges are opened on the compute stream right before their first step.
         const int64_t nsteps = nac * nb;
-        const int ahead = std::min(2, L.b_slots - 1);
+        const int ahead = L.b_slots - 1;
         // A range r' (and its C row pointers) may be staged once range
         // r' - a_slots has released its A slot (used_a recorded): staging
         // earlier would wait on a stale event and overwrite a slot in use
