@@ -193,6 +193,49 @@ int tsg_rmat_graph(tsg_ctx *ctx, int scale, int edge_factor, uint64_t seed, doub
 int tsg_gather_sharded(tsg_ctx *ctx, int n_shards, const int64_t *row_lo, const void *const *shard_rp,
                        const void *const *shard_col, const void *const *shard_val, int64_t b_cols,
                        const tsg_csr *a, tsg_csr **out);
+/* ---- multi-GPU row partition (rows of C are independent,
+   kernel.py:11-14).  One process per GPU; the collectives (B all-gather,
+   row-pointer offset exchange) run over NCCL in the host layer
+   (paper_1804_00695_b200/distributed.py).
+
+   B sharded in peer HBM: every GPU owns one element range of B's column and
+   value arrays as a CUDA VMM physical allocation exported as a POSIX file
+   descriptor; each GPU maps every shard, in order, into ONE reserved virtual
+   range (tsg_shard_map), so B's arrays look contiguous to the kernels while
+   remote pages are read from peer HBM over NVLink.  Shard sizes are multiples
+   of tsg_shard_granularity. */
+typedef struct tsg_shard tsg_shard;  /* this GPU's exported physical shard    */
+typedef struct tsg_vmap tsg_vmap;    /* all shards mapped into one VA range   */
+int tsg_shard_granularity(tsg_ctx *ctx, size_t *bytes);
+/* Physical allocation of >= bytes on the context's GPU, mapped locally at
+   *dev_ptr (to fill it), exported as *fd (owned by the shard; dup before
+   sending if the shard may be freed first). */
+int tsg_shard_alloc(tsg_ctx *ctx, size_t bytes, tsg_shard **out, void **dev_ptr, int *fd, size_t *size);
+int tsg_shard_free(tsg_ctx *ctx, tsg_shard *s);
+/* Import n shard descriptors (this process's own or received from peers)
+   and map them back to back at *va (sum of sizes). */
+int tsg_shard_map(tsg_ctx *ctx, int n, const int *fds, const size_t *sizes, tsg_vmap **out, void **va);
+int tsg_vmap_free(tsg_ctx *ctx, tsg_vmap *m);
+/* A CSR over device arrays the caller owns (e.g. B's columns / values in a
+   tsg_shard_map range): freeing the view leaves the arrays alone.  sorted:
+   every row ascending and distinct; max_row: longest row (-1 unknown). */
+int tsg_csr_view(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t *d_row_ptr,
+                 const int32_t *d_col, const double *d_values, int sorted, int64_t max_row,
+                 tsg_csr **out);
+/* One GPU's block of C = A_block * B (kernel.py:343-346 per row block).
+   c_budget_bytes == 0: C materialised in *c (may be NULL to drop it);
+   > 0: streamed-C mode -- row sub-blocks whose C fits the budget are
+   multiplied, reduced (nnz, sum, sum of squares) and released, for products
+   whose C exceeds HBM; *c stays NULL.  B is compressed once per call. */
+typedef struct {
+    int64_t nnz;            /* entries of this block of C                    */
+    int64_t blocks;         /* sub-blocks multiplied                        */
+    int64_t max_block_nnz;  /* largest sub-block of C held at once           */
+    double value_sum;       /* sum of C's values (fp64)                      */
+    double value_sumsq;     /* sum of their squares                          */
+} tsg_mg_stats;
+int tsg_mg_multiply(tsg_ctx *ctx, const tsg_csr *a_block, const tsg_csr *b, int64_t c_budget_bytes,
+                    tsg_csr **c, tsg_mg_stats *stats);
 /* every stored entry := value (allocating the value array of a pattern CSR):
    generators.with_unit_values on the device */
 int tsg_csr_set_values(tsg_ctx *ctx, tsg_csr *m, double value);

@@ -48,6 +48,8 @@ EXPORTS = (
     "tsg_graph_lower", "tsg_rmat_graph", "tsg_numeric_calls", "tsg_numeric_ms",
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
     "tsg_rap", "tsg_row_flops", "tsg_stream", "tsg_chunk_symbolic",
+    "tsg_shard_granularity", "tsg_shard_alloc", "tsg_shard_free", "tsg_shard_map", "tsg_vmap_free",
+    "tsg_csr_view", "tsg_mg_multiply",
 )
 
 _P = ctypes.c_void_p
@@ -85,6 +87,14 @@ _SIGS = {
     "tsg_count_multiplications": ([_P, _P, _P, _PI64], ctypes.c_int),
     "tsg_row_flops": ([_P, _P, _P, _P, _PI64], ctypes.c_int),
     "tsg_stream": ([_P, _PP], ctypes.c_int),
+    "tsg_shard_granularity": ([_P, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tsg_shard_alloc": ([_P, ctypes.c_size_t, _PP, _PP, ctypes.POINTER(ctypes.c_int),
+                         ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tsg_shard_free": ([_P, _P], ctypes.c_int),
+    "tsg_shard_map": ([_P, ctypes.c_int, _P, _P, _PP, _PP], ctypes.c_int),
+    "tsg_vmap_free": ([_P, _P], ctypes.c_int),
+    "tsg_csr_view": ([_P, _I64, _I64, _I64, _P, _P, _P, ctypes.c_int, _I64, _PP], ctypes.c_int),
+    "tsg_mg_multiply": ([_P, _P, _P, _I64, _PP, _P], ctypes.c_int),
     "tsg_symbolic": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric": ([_P, _P, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
@@ -419,6 +429,72 @@ def d_row_flops(da, db):
     tot = ctypes.c_int64()
     check(load().tsg_row_flops(da.ctx.h, da.h, db.h, _ptr(out), ctypes.byref(tot)))
     return out, tot.value
+
+
+class MgStats(ctypes.Structure):
+    _fields_ = [("nnz", ctypes.c_int64), ("blocks", ctypes.c_int64), ("max_block_nnz", ctypes.c_int64),
+                ("value_sum", ctypes.c_double), ("value_sumsq", ctypes.c_double)]
+
+
+def d_mg_multiply(da, db, c_budget_bytes: int = 0, keep_c: bool = True):
+    """(C block or None, stats dict): one GPU's row block of A * B
+    (tsg_mg_multiply); c_budget_bytes > 0 streams C through that budget."""
+    h = ctypes.c_void_p()
+    st = MgStats()
+    check(load().tsg_mg_multiply(da.ctx.h, da.h, db.h, int(c_budget_bytes),
+                                 ctypes.byref(h) if keep_c else None, ctypes.byref(st)))
+    c = DeviceCsr(da.ctx, h) if (keep_c and h.value) else None
+    return c, {"nnz": st.nnz, "blocks": st.blocks, "max_block_nnz": st.max_block_nnz,
+               "value_sum": st.value_sum, "value_sumsq": st.value_sumsq}
+
+
+class Shard(_Handle):
+    """This GPU's exported VMM physical shard (tsg_shard_alloc)."""
+
+    _free_fn = "tsg_shard_free"
+
+    def __init__(self, ctx, nbytes):
+        h, p = ctypes.c_void_p(), ctypes.c_void_p()
+        fd, size = ctypes.c_int(-1), ctypes.c_size_t(0)
+        check(load().tsg_shard_alloc(ctx.h, int(nbytes), ctypes.byref(h), ctypes.byref(p),
+                                     ctypes.byref(fd), ctypes.byref(size)))
+        super().__init__(ctx, h)
+        self.ptr, self.fd, self.size = p.value, fd.value, size.value
+
+
+class VMap(_Handle):
+    """Shards (own + peers', by file descriptor) mapped into one VA range."""
+
+    _free_fn = "tsg_vmap_free"
+
+    def __init__(self, ctx, fds, sizes):
+        n = len(fds)
+        fa = (ctypes.c_int * n)(*[int(x) for x in fds])
+        sa = (ctypes.c_size_t * n)(*[int(x) for x in sizes])
+        h, va = ctypes.c_void_p(), ctypes.c_void_p()
+        check(load().tsg_shard_map(ctx.h, n, fa, sa, ctypes.byref(h), ctypes.byref(va)))
+        super().__init__(ctx, h)
+        self.va = va.value
+        self.total = sum(int(x) for x in sizes)
+
+
+def shard_granularity(ctx) -> int:
+    g = ctypes.c_size_t(0)
+    check(load().tsg_shard_granularity(ctx.h, ctypes.byref(g)))
+    return g.value
+
+
+def d_csr_view(ctx, rows, cols, nnz, rp_ptr, col_ptr, val_ptr, sorted_rows=False, max_row=-1,
+               owners=()) -> DeviceCsr:
+    """DeviceCsr over caller-owned device arrays; `owners` are kept alive
+    for as long as the view."""
+    h = ctypes.c_void_p()
+    check(load().tsg_csr_view(ctx.h, int(rows), int(cols), int(nnz), ctypes.c_void_p(rp_ptr),
+                              ctypes.c_void_p(col_ptr), ctypes.c_void_p(val_ptr) if val_ptr else None,
+                              1 if sorted_rows else 0, int(max_row), ctypes.byref(h)))
+    v = DeviceCsr(ctx, h)
+    v._owners = tuple(owners)
+    return v
 
 
 def d_symbolic(da, dcb) -> DeviceVec:

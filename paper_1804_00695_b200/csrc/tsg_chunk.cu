@@ -275,7 +275,10 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     d.m.sorted = sorted ? 1 : 0;
     d.m.distinct = distinct ? 1 : 0;
     d.m.max_row = host_max_row(h.rp, lo, hi);
-    cudaStream_t s = c->copy_in, cs = c->convert;
+    // alternate the two H2D streams: while this piece's values wait for the
+    // column conversion, the next piece's columns are already on the link
+    static thread_local unsigned flip = 0;
+    cudaStream_t s = (flip++ & 1) ? c->copy_in2 : c->copy_in, cs = c->convert;
     if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
     cudaEvent_t tl0{};
     g_tl.begin(s, tl0);
@@ -746,6 +749,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         }
     }
     cudaStreamSynchronize(c->copy_in);
+    cudaStreamSynchronize(c->copy_in2);
     cudaStreamSynchronize(c->copy_out);
     cudaStreamSynchronize(c->convert);
     cudaStreamSynchronize(c->stream);
@@ -959,6 +963,7 @@ extern "C" int tsg_chunk_symbolic(tsg_ctx *c, int64_t a_rows, int64_t a_cols, co
     tsg_free(c, base_dev);
     tsg_cmat_free(c, cb);
     cudaStreamSynchronize(c->copy_in);
+    cudaStreamSynchronize(c->copy_in2);
     cudaStreamSynchronize(c->convert);
     cudaStreamSynchronize(c->stream);
     if (st == TSG_OK) st = tsg_check_kernel_errors(c, "chunked symbolic");

@@ -77,6 +77,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     }
     TSG_CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     TSG_CK(cudaStreamCreateWithPriority(&c->convert, cudaStreamNonBlocking, prio_hi));
+    TSG_CK(cudaStreamCreateWithFlags(&c->copy_in2, cudaStreamNonBlocking));
     // keep freed blocks cached in the default pool: no OS round trips per call
     cudaMemPool_t pool;
     TSG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -117,6 +118,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_TRY(tsg_preload_module_of(tsg_kernel_graph()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_build()));
     TSG_TRY(tsg_preload_module_of(tsg_kernel_rap()));
+    TSG_TRY(tsg_preload_module_of(tsg_kernel_mg()));
     *out = c;
     return TSG_OK;
 }
@@ -141,6 +143,7 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
     }
     cudaEventDestroy(c->ev_fork);
     cudaStreamDestroy(c->convert);
+    cudaStreamDestroy(c->copy_in2);
     delete c;
     return TSG_OK;
 }
@@ -1217,9 +1220,11 @@ extern "C" int tsg_csr_free(tsg_ctx *c, tsg_csr *m) {
         delete m;
         return TSG_OK;
     }
-    tsg_free(c, m->rp);
-    tsg_free(c, m->col);
-    tsg_free(c, m->val);
+    if (!m->borrowed) {
+        tsg_free(c, m->rp);
+        tsg_free(c, m->col);
+        tsg_free(c, m->val);
+    }
     delete m;
     return TSG_OK;
 }

@@ -46,6 +46,8 @@ struct tsg_ctx {
     int64_t bytes_in_use;
     int64_t bytes_peak;       // high-water mark of bytes_in_use (the chunked executors reset it)
     cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
+    cudaStream_t copy_in2;    // second H2D stream: a piece's column copy queues while the
+                              // previous piece waits for its conversion (chunked)
     int64_t launches;         // kernels launched by this context (all entry points)
     cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
@@ -80,6 +82,7 @@ struct tsg_csr {
     int sorted;        // 1: every row's columns are non-decreasing (compress needs no fallback)
     int distinct;      // 1: no column repeats within a row (lane-split numeric mode is race-free)
     int64_t max_row;   // longest row, or -1 if unknown
+    int borrowed;      // arrays owned by the caller (tsg_csr_view): free releases only the handle
 };
 
 struct tsg_cmat {
@@ -171,6 +174,9 @@ const void *tsg_kernel_compress();
 const void *tsg_kernel_spgemm();
 const void *tsg_kernel_masked();
 const void *tsg_kernel_chunk();
+const void *tsg_kernel_mg();
+// per-row multiplications of A * B (K0 over B's row pointers) into flops[rows]
+void tsg_launch_row_flops(tsg_ctx *ctx, const tsg_csr *a, const int64_t *brp, int64_t *flops);
 const void *tsg_kernel_graph();
 // cudaMemsetAsync replacement as a kernel: on this platform memsets queue on
 // the copy engines, i.e. behind any bulk H2D / D2H already in flight

@@ -2123,6 +2123,11 @@ int tsg_fused_bounds(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_r
                      int32_t b_lo, int32_t b_hi, const int64_t *cbstart, const int32_t *cbcnt,
                      const int64_t *prp, int64_t *sbound);
 
+void tsg_launch_row_flops(tsg_ctx *c, const tsg_csr *a, const int64_t *brp, int64_t *flops) {
+    if (a->rows > 0 && a->nnz > 0) launch_bounds(c, a, brp, nullptr, flops, nullptr, nullptr);
+    else if (a->rows > 0) tsg_fill(c, flops, 0, sizeof(int64_t) * a->rows, c->stream);
+}
+
 int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out);   // tsg_compress.cu
 
 // counts (+ msets) of A * B for output rows [0, rows_out); fused mode when
