@@ -280,13 +280,15 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     static thread_local unsigned flip = 0;
     cudaStream_t s = (flip++ & 1) ? c->copy_in2 : c->copy_in, cs = c->convert;
     if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
-    cudaEvent_t tl0{};
+    cudaEvent_t tl0{}, tl1{}, tl2{};
     g_tl.begin(s, tl0);
     TSG_TRY(tsg_copy(d.stage_rp, h.rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     int64_t *col64 = reinterpret_cast<int64_t *>(d.m.val);
     if (nnz > 0) TSG_TRY(tsg_copy(col64, h.col + e0, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    g_tl.end('c', s, tl0);
     TSG_CK(cudaEventRecord(d.cols_in, s));
     TSG_CK(cudaStreamWaitEvent(cs, d.cols_in, 0));
+    g_tl.begin(cs, tl1);
     k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, cs>>>(d.stage_rp, d.m.rp, rows + 1, e0);
     ++c->launches;
     if (nnz > 0) {
@@ -294,11 +296,13 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
         ++c->launches;
     }
     TSG_CK(cudaGetLastError());
+    g_tl.end('n', cs, tl1);
     TSG_CK(cudaEventRecord(d.conv, cs));
     TSG_CK(cudaStreamWaitEvent(s, d.conv, 0));
+    g_tl.begin(s, tl2);
     if (nnz > 0 && h.val)
         TSG_TRY(tsg_copy(d.m.val, h.val + e0, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
-    g_tl.end('H', s, tl0);
+    g_tl.end('v', s, tl2);
     TSG_CK(cudaEventRecord(d.ready, s));
     d.m.rows = rows;
     d.m.cols = h.cols;
@@ -432,12 +436,14 @@ int open_c(Job &J, DevC &d, CRows &cr, bool staged, int64_t lo, int64_t hi, bool
 int drain_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool with_plen) {
     tsg_ctx *c = J.c;
     const int64_t rows = hi - lo, e0 = J.c_rp[lo], nnz = J.c_rp[hi] - e0;
-    cudaStream_t s = c->copy_out, cs = c->convert;
+    cudaStream_t s = c->copy_out, cs = c->widen;
     TSG_CK(cudaEventRecord(d.done, c->stream));
     TSG_CK(cudaStreamWaitEvent(s, d.done, 0));
-    cudaEvent_t tl0{};
+    cudaEvent_t tl0{}, tl1{};
     g_tl.begin(s, tl0);
     if (nnz > 0) TSG_TRY(tsg_copy(J.c_val + e0, d.val, nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+    g_tl.end('D', s, tl0);
+    g_tl.begin(s, tl1);
     if (with_plen)
         TSG_TRY(tsg_copy(J.h_plen + lo, d.plen, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (nnz > 0) {
@@ -450,7 +456,7 @@ int drain_c(Job &J, DevC &d, int64_t lo, int64_t hi, bool with_plen) {
         TSG_CK(cudaStreamWaitEvent(s, d.widened, 0));
         TSG_TRY(tsg_copy(J.c_col + e0, col64, nnz * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     }
-    g_tl.end('D', s, tl0);
+    g_tl.end('d', s, tl1);
     TSG_CK(cudaEventRecord(d.drained, s));
     J.st->d2h_bytes += nnz * 16 + (with_plen ? rows * 4 : 0);
     return TSG_OK;
@@ -581,19 +587,31 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     // cached blocks could serve a slot with up to 25 % slack: start from an
     // empty cache so the footprint is the modelled one
     tsg_arena_trim(c);
+    if (g_tl.on) fprintf(stderr, "[tsg host] trimmed %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     const int64_t mem0 = c->bytes_in_use;
     c->bytes_peak = mem0;
     Job J{c, {a_rows, a_cols, a_rp, a_col, a_val}, {b_rows, b_cols, b_rp, b_col, b_val}, c_rp,
           c_col, c_val, nullptr, &local};
 
     bool a_sorted = false, a_distinct = false, b_sorted = false, b_distinct = false;
+    auto hms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
     host_row_order(J.A, &a_sorted, &a_distinct);
-    host_row_order(J.B, &b_sorted, &b_distinct);
+    if (J.B.rp == J.A.rp && J.B.col == J.A.col && J.B.rows == J.A.rows) {   // A * A: one pass
+        b_sorted = a_sorted;
+        b_distinct = a_distinct;
+    } else {
+        host_row_order(J.B, &b_sorted, &b_distinct);
+    }
+    if (g_tl.on) fprintf(stderr, "[tsg host] row order %.1f ms\n", hms());
     int64_t whole[2] = {0, a_rows};
     const int64_t *acb0 = algo == 0 ? whole : ac_bounds;
     const int64_t nac0 = algo == 0 ? 1 : n_ac;
     Layout L;
     TSG_TRY(choose_layout(J, algo, acb0, nac0, b_bounds, n_b, a_sorted, budget_bytes, L));
+    if (g_tl.on) fprintf(stderr, "[tsg host] layout %.1f ms\n", hms());
     const int64_t nac = (int64_t)L.acb.size() - 1, nb = (int64_t)L.bb.size() - 1;
     const int64_t *acb = L.acb.data(), *bb = L.bb.data();
 
@@ -659,6 +677,7 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         TSG_CK(cudaStreamSynchronize(c->stream));
         for (int i = 0; i < 2; i++) TSG_CK(cudaEventRecord(crow[i].used, c->stream));
     }
+    if (g_tl.on) fprintf(stderr, "[tsg host] slots allocated %.1f ms\n", hms());
     local.budget_bytes = budget_bytes;
     local.a_slots = L.a_slots;
     local.c_slots = L.c_slots;
@@ -714,16 +733,22 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             if (st == TSG_OK && s2 + ahead + 1 < nsteps) st = issue_b(s2 + ahead + 1);
         }
     } else if (st == TSG_OK) {
-        void *ph = nullptr;
-        TSG_TRY(tsg_host_alloc(((size_t)a_rows + 1) * sizeof(int32_t), &ph));
-        plen_host = static_cast<int32_t *>(ph);
-        memset(plen_host, 0, ((size_t)a_rows + 1) * sizeof(int32_t));
-        J.h_plen = plen_host;
+        // partial lengths round-trip through pinned host memory only when a
+        // later B chunk reloads them; a single resident chunk finishes every
+        // range in one step, checked on the device like order 1
+        const bool partials = nb > 1;
         for (int64_t j = 0; j < nb && st == TSG_OK; ++j) {
             DevRange &B = Bbuf[j % L.b_slots];
             if ((st = stage_rows(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], b_sorted, b_distinct,
                                  local.h2d_bytes)) != TSG_OK)
                 break;
+            if (j == 0 && partials) {   // allocated while the first chunk is on the link
+                void *ph = nullptr;
+                TSG_TRY(tsg_host_alloc(((size_t)a_rows + 1) * sizeof(int32_t), &ph));
+                plen_host = static_cast<int32_t *>(ph);
+                memset(plen_host, 0, ((size_t)a_rows + 1) * sizeof(int32_t));
+                J.h_plen = plen_host;
+            }
             // the resident chunk is compressed once for all A/C ranges
             tsg_cmat *cbj = nullptr;
             TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
@@ -742,7 +767,11 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 if ((st = open_c(J, C, crow[r & 1], false, lo, hi, j > 0)) != TSG_OK) break;
                 st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo, cbj);
                 TSG_CK(cudaEventRecord(used_a[r % L.a_slots], c->stream));
-                if (st == TSG_OK) st = drain_c(J, C, lo, hi, true);
+                if (st == TSG_OK && !partials) {
+                    k_check_full<<<grid_for(hi - lo, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+                        C.plen, C.cap, hi - lo, lo, c->d_err); ++c->launches;
+                }
+                if (st == TSG_OK) st = drain_c(J, C, lo, hi, partials);
             }
             tsg_cmat_free(c, cbj);
             TSG_CK(cudaEventRecord(used[j % L.b_slots], c->stream));
@@ -752,9 +781,10 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     cudaStreamSynchronize(c->copy_in2);
     cudaStreamSynchronize(c->copy_out);
     cudaStreamSynchronize(c->convert);
+    cudaStreamSynchronize(c->widen);
     cudaStreamSynchronize(c->stream);
     if (st == TSG_OK) st = tsg_check_kernel_errors(c, "chunked multiply");
-    if (st == TSG_OK && algo == 2) {
+    if (st == TSG_OK && algo == 2 && plen_host) {
         for (int64_t i = 0; i < a_rows; ++i)
             if (plen_host[i] != c_rp[i + 1] - c_rp[i]) {
                 tsg_set_error("chunked result rows disagree with symbolic counts (row %lld: %d vs %lld)",

@@ -78,6 +78,7 @@ extern "C" int tsg_init(int device, tsg_ctx **out) {
     TSG_CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     TSG_CK(cudaStreamCreateWithPriority(&c->convert, cudaStreamNonBlocking, prio_hi));
     TSG_CK(cudaStreamCreateWithFlags(&c->copy_in2, cudaStreamNonBlocking));
+    TSG_CK(cudaStreamCreateWithPriority(&c->widen, cudaStreamNonBlocking, prio_hi));
     // keep freed blocks cached in the default pool: no OS round trips per call
     cudaMemPool_t pool;
     TSG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -144,6 +145,7 @@ extern "C" int tsg_destroy(tsg_ctx *c) {
     cudaEventDestroy(c->ev_fork);
     cudaStreamDestroy(c->convert);
     cudaStreamDestroy(c->copy_in2);
+    cudaStreamDestroy(c->widen);
     delete c;
     return TSG_OK;
 }

@@ -46,6 +46,8 @@ struct tsg_ctx {
     int64_t bytes_in_use;
     int64_t bytes_peak;       // high-water mark of bytes_in_use (the chunked executors reset it)
     cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
+    cudaStream_t widen;       // int32 -> int64 widening of drained C ranges (own stream, so a
+                              // narrow for an H2D piece never queues behind a C drain)
     cudaStream_t copy_in2;    // second H2D stream: a piece's column copy queues while the
                               // previous piece waits for its conversion (chunked)
     int64_t launches;         // kernels launched by this context (all entry points)

@@ -1,5 +1,7 @@
 """Summarise TSG_CHUNK_TIMELINE=1 output of one chunked run: busy fractions of
-the H2D engine (H), the D2H engine (D) and the compute stream (K), and the
+the H2D engine (c = int64 columns, v = values),
+the narrowing kernels (n), the D2H engine (D values, d columns) and the
+compute stream (K), and the
 largest H2D gaps.  Usage: python tools/chunk_timeline.py < stderr.log"""
 import sys
 
@@ -16,7 +18,7 @@ def union(iv):
 
 
 def main():
-    ev = {"H": [], "D": [], "K": []}
+    ev = {"c": [], "n": [], "v": [], "D": [], "d": [], "K": []}
     for ln in sys.stdin:
         if ln.startswith("[tsg timeline]"):
             _, _, k, a, b = ln.split()
@@ -26,7 +28,7 @@ def main():
         u = union(v)
         busy = sum(b - a for a, b in u)
         print("%s: %d intervals, busy %.1f ms of %.1f (%.0f %%)" % (k, len(v), busy, end, 100 * busy / end))
-    u = union(ev["H"])
+    u = union(ev["c"] + ev["v"])
     gaps = sorted(((u[i + 1][0] - u[i][1], u[i][1]) for i in range(len(u) - 1)), reverse=True)[:15]
     print("largest H2D gaps (ms, at):", [("%.2f" % g, "%.1f" % t) for g, t in gaps])
 
