@@ -506,9 +506,14 @@ def run_config2(args, world, rank, local, dist):
             "sample": "one full config-2 R*A*P on the host (oracle/tsg_oracle.c with %d pthreads; "
                       "the reference's algorithm restated in C); w1_value = 1 thread"
                       % (os.cpu_count() or 1)}
-    if rank == 0 and world == 1 and not args.no_secondary:
+    if not args.no_secondary:
         import bench_configs as BC
-        line["secondary"] = BC.secondary(args)
+        if world == 1:
+            line["secondary"] = BC.secondary(args)
+        else:   # config 5 strong scaling over the same ranks (every rank takes part)
+            ns = argparse.Namespace(**vars(args))
+            ns.scale, ns.steps, ns.warmup, ns.no_parity = 20, 2, 1, False
+            line["secondary"] = {"config5": BC.config5(ns, dist)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return ok

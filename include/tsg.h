@@ -216,6 +216,9 @@ int tsg_shard_free(tsg_ctx *ctx, tsg_shard *s);
    and map them back to back at *va (sum of sizes). */
 int tsg_shard_map(tsg_ctx *ctx, int n, const int *fds, const size_t *sizes, tsg_vmap **out, void **va);
 int tsg_vmap_free(tsg_ctx *ctx, tsg_vmap *m);
+/* Synchronous copy on the context's compute stream between any addresses the
+   GPU reaches (device memory, VMM ranges, pinned host). */
+int tsg_memcpy(tsg_ctx *ctx, void *dst, const void *src, size_t bytes);
 /* A CSR over device arrays the caller owns (e.g. B's columns / values in a
    tsg_shard_map range): freeing the view leaves the arrays alone.  sorted:
    every row ascending and distinct; max_row: longest row (-1 unknown). */

@@ -49,7 +49,7 @@ EXPORTS = (
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
     "tsg_rap", "tsg_row_flops", "tsg_stream", "tsg_chunk_symbolic",
     "tsg_shard_granularity", "tsg_shard_alloc", "tsg_shard_free", "tsg_shard_map", "tsg_vmap_free",
-    "tsg_csr_view", "tsg_mg_multiply",
+    "tsg_csr_view", "tsg_mg_multiply", "tsg_memcpy",
 )
 
 _P = ctypes.c_void_p
@@ -95,6 +95,7 @@ _SIGS = {
     "tsg_vmap_free": ([_P, _P], ctypes.c_int),
     "tsg_csr_view": ([_P, _I64, _I64, _I64, _P, _P, _P, ctypes.c_int, _I64, _PP], ctypes.c_int),
     "tsg_mg_multiply": ([_P, _P, _P, _I64, _PP, _P], ctypes.c_int),
+    "tsg_memcpy": ([_P, _P, _P, ctypes.c_size_t], ctypes.c_int),
     "tsg_symbolic": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric": ([_P, _P, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
@@ -476,6 +477,11 @@ class VMap(_Handle):
         super().__init__(ctx, h)
         self.va = va.value
         self.total = sum(int(x) for x in sizes)
+
+
+def memcpy(ctx, dst: int, src: int, nbytes: int) -> None:
+    """Synchronous copy between device-reachable addresses (tsg_memcpy)."""
+    check(load().tsg_memcpy(ctx.h, ctypes.c_void_p(dst), ctypes.c_void_p(src), int(nbytes)))
 
 
 def shard_granularity(ctx) -> int:

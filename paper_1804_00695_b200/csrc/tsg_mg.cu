@@ -256,6 +256,15 @@ extern "C" int tsg_vmap_free(tsg_ctx *c, tsg_vmap *m) {
     return TSG_OK;
 }
 
+// Synchronous copy on the compute stream between any two addresses the
+// device can reach (device, mapped host, VMM ranges).
+extern "C" int tsg_memcpy(tsg_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes == 0) return TSG_OK;
+    TSG_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    return TSG_OK;
+}
+
 // A CSR over arrays the caller owns (e.g. B's columns / values in a VMM range
 // spanning peer shards); freeing the view leaves the arrays alone.
 extern "C" int tsg_csr_view(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz, const int64_t *d_rp,

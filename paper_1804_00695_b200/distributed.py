@@ -1,33 +1,42 @@
 """Multi-GPU row partition of A.
 
-Rows of C are independent (kernel.py:11-14), so N GPUs each compute a
-contiguous block of C's rows.  B reaches the ranks in one of two ways:
+Rows of C are independent (kernel.py:11-14), so N GPUs -- one process each --
+compute contiguous blocks of C's rows.  The blocks are balanced by the K0
+per-row multiplications (``flops_partition``: prefix + binary search, the
+idea of chunking.py:80-128 applied to flops instead of bytes), which keeps
+power-law rows (R-MAT hubs) from piling up on one GPU.  B reaches the GPUs in
+one of the two ways §8e names:
 
-* replicated -- one all-gather rebuilds the full B on every rank
-  (``allgather_csr``);
-* sharded -- every rank keeps only its row shard of B; shards are shared as
-  CUDA IPC handles once (``share_shards``), and each rank's kernel
-  (``gather_sharded``, csrc ``tsg_gather_sharded``) loads the B rows its A
-  rows select straight from peer HBM over NVLink.  No collective runs in the
-  multiply.
+* **replicated** -- every rank holds a row shard of B and one all-gather
+  (row lengths, columns, values) rebuilds the full B on every rank
+  (``allgather_csr`` / ``replicate_b``);
+* **sharded** -- every rank keeps one element range of B's column and value
+  arrays in its own HBM as a CUDA VMM allocation; the ranks swap the
+  allocations' file descriptors once (``exchange_fds``, a Unix socket per
+  rank) and every rank maps all shards back to back into one virtual range
+  (``shard_b``), so the unchanged kernels read remote parts of B straight
+  from peer HBM over NVLink.  No collective runs in the multiply.
 
-The collectives, over torch.distributed (NCCL on B200s, gloo in the CPU
-tests):
-
-* ``allgather_csr`` -- B replicated: every rank holds a row shard of B and one
-  all-gather (counts, columns, values) rebuilds the full B on every rank;
-* ``exchange_offsets`` -- the row-pointer offset exchange: an all-gather of
-  each rank's nnz(C slice) whose exclusive prefix places the slice in the
-  global C.
-
-``flops_partition`` balances the row blocks by the K0 per-row flops
-(prefix + binary search, the same idea as chunking.py:80-128 over flops
-instead of bytes), which is what keeps power-law rows (R-MAT) from piling up
-on one rank.  All helpers are device-agnostic torch code.
+Per step each rank multiplies its block (``tsg_mg_multiply``, optionally in
+streamed-C mode for products whose C exceeds HBM) and the ranks exchange
+their block sizes (``exchange_offsets``: all-gather of nnz, exclusive prefix
+= the block's offset in the global row pointer).  Those two all-gathers are
+the only collectives.  With NCCL they run on GPU tensors; with gloo (the CPU
+tests, or two processes sharing one GPU) on host tensors.
 """
+
+import json
+import os
+import secrets
+import socket
+import statistics
+import threading
+import time
 
 import numpy as np
 
+
+# ---------------------------------------------------------------- host logic
 
 def flops_partition(row_flops, world: int) -> np.ndarray:
     """Boundaries b[0..world] (b[0]=0, b[world]=rows) of contiguous row blocks
@@ -45,9 +54,32 @@ def flops_partition(row_flops, world: int) -> np.ndarray:
     return np.maximum.accumulate(np.minimum(b, n))
 
 
-def exchange_offsets(local_nnz: int, dist, device) -> "tuple[int, int]":
-    """(offset of this rank's C slice in the global C, global nnz)."""
+def shard_bounds(row_nnz, world: int) -> np.ndarray:
+    """Contiguous row shards of B with near-equal entry counts."""
+    return flops_partition(row_nnz, world)
+
+
+def element_shards(nnz: int, world: int, granularity: int) -> int:
+    """Entries per shard of B's arrays: the smallest E >= nnz / world such
+    that E int32 columns (and so E fp64 values) fill whole VMM granules."""
+    per = max(1, granularity // 4)
+    e = -(-max(int(nnz), 1) // world)
+    return -(-e // per) * per
+
+
+def _coll_device(dist):
+    try:
+        return "cuda" if dist.get_backend() == "nccl" else "cpu"
+    except Exception:
+        return "cpu"
+
+
+# ---------------------------------------------------------------- collectives
+
+def exchange_offsets(local_nnz: int, dist, device=None) -> "tuple[int, int]":
+    """(offset of this rank's C block in the global C, global nnz)."""
     import torch
+    device = device or _coll_device(dist)
     world = dist.get_world_size()
     t = torch.tensor([int(local_nnz)], dtype=torch.int64, device=device)
     outs = [torch.empty_like(t) for _ in range(world)]
@@ -67,7 +99,7 @@ def _allgather_var(x, dist, device):
     lens = [int(v.item()) for v in ns]
     cap = max(lens) if lens else 0
     pad = torch.zeros(cap, dtype=x.dtype, device=device)
-    pad[:x.numel()] = x
+    pad[:x.numel()] = x.to(device)
     outs = [torch.empty(cap, dtype=x.dtype, device=device) for _ in range(world)]
     dist.all_gather(outs, pad)
     return torch.cat([o[:l] for o, l in zip(outs, lens)])
@@ -83,10 +115,115 @@ def allgather_csr(row_counts, cols, vals, dist, device):
     return rp, _allgather_var(cols, dist, device), _allgather_var(vals, dist, device)
 
 
-def shard_bounds(row_nnz, world: int) -> np.ndarray:
-    """Contiguous row shards of B with near-equal entry counts."""
-    return flops_partition(row_nnz, world)
+def exchange_fds(my_fds, dist):
+    """Give every rank every other rank's file descriptors (CUDA VMM shard
+    handles): each rank serves its descriptors on an abstract Unix socket
+    (SCM_RIGHTS) and connects to every peer's.  Returns, in rank order, the
+    list of descriptors valid in this process (this rank's own as given)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    token = [secrets.token_hex(8) if rank == 0 else None]
+    dist.broadcast_object_list(token, src=0)
+    name = lambda r: "\0tsg-%s-%d" % (token[0], r)
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(name(rank))
+    srv.listen(world)
 
+    def serve():
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            with conn:
+                socket.send_fds(conn, [b"f"], list(my_fds))
+
+    th = threading.Thread(target=serve, daemon=True)
+    th.start()
+    dist.barrier()
+    out = []
+    for r in range(world):
+        if r == rank:
+            out.append(list(my_fds))
+            continue
+        cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        for _ in range(200):
+            try:
+                cli.connect(name(r))
+                break
+            except (FileNotFoundError, ConnectionRefusedError):
+                time.sleep(0.01)
+        with cli:
+            _, fds, _, _ = socket.recv_fds(cli, 16, len(my_fds))
+        out.append(list(fds))
+    th.join()
+    srv.close()
+    dist.barrier()
+    return out
+
+
+# ---------------------------------------------------------------- B on the ranks
+
+def replicate_b(ctx, db_rows, b_rows: int, b_cols: int, dist):
+    """B replicated: this rank holds B's rows as ``db_rows`` (a DeviceCsr of
+    its row shard, global columns); one all-gather of (row lengths, int32
+    columns, fp64 values) rebuilds the full B in this GPU's HBM."""
+    import torch
+    from . import _lib
+    dev = _coll_device(dist)
+    rp_p, col_p, val_p = db_rows.device_ptrs()
+    n, nnz = db_rows.num_rows, db_rows.nnz
+    rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    val = torch.empty(max(nnz, 1), dtype=torch.float64, device="cuda")
+    _lib.memcpy(ctx, rp.data_ptr(), rp_p, 8 * (n + 1))
+    _lib.memcpy(ctx, col.data_ptr(), col_p, 4 * nnz)
+    _lib.memcpy(ctx, val.data_ptr(), val_p, 8 * nnz)
+    rpf, colf, valf = allgather_csr(torch.diff(rp).to(dev), col[:nnz].to(dev), val[:nnz].to(dev), dist, dev)
+    rpf, colf, valf = rpf.cuda(), colf.cuda(), valf.cuda()
+    if rpf.numel() - 1 != b_rows:
+        raise ValueError("gathered %d rows, expected %d" % (rpf.numel() - 1, b_rows))
+    torch.cuda.synchronize()
+    return _lib.DeviceCsr.from_device(ctx, b_rows, b_cols, int(colf.numel()), rpf.data_ptr(),
+                                      colf.data_ptr(), valf.data_ptr())
+
+
+def shard_b(ctx, db_full, dist, sorted_rows=True, max_row=-1):
+    """B sharded in peer HBM.  Every rank exports one element range of B's
+    columns and values as VMM physical allocations, the descriptors are
+    exchanged once, and every rank maps all ranges back to back into one
+    virtual range: a DeviceCsr view whose remote pages are read over NVLink.
+    ``db_full`` (this rank's copy of B, from a deterministic builder) is only
+    read for this rank's range and for the replicated row pointers; drop it
+    afterwards.  Returns (view, info)."""
+    import torch
+    from . import _lib
+    world, rank = dist.get_world_size(), dist.get_rank()
+    gran = _lib.shard_granularity(ctx)
+    nnz = db_full.nnz
+    e = element_shards(nnz, world, gran)
+    rp_p, col_p, val_p = db_full.device_ptrs()
+    lo, hi = min(rank * e, nnz), min((rank + 1) * e, nnz)
+    sc = _lib.Shard(ctx, 4 * e)
+    sv = _lib.Shard(ctx, 8 * e)
+    _lib.memcpy(ctx, sc.ptr, col_p + 4 * lo, 4 * (hi - lo))
+    _lib.memcpy(ctx, sv.ptr, val_p + 8 * lo, 8 * (hi - lo))
+    rp = torch.empty(db_full.num_rows + 1, dtype=torch.int64, device="cuda")
+    _lib.memcpy(ctx, rp.data_ptr(), rp_p, 8 * (db_full.num_rows + 1))
+    fds = exchange_fds([sc.fd, sv.fd], dist)
+    vc = _lib.VMap(ctx, [f[0] for f in fds], [sc.size] * world)
+    vv = _lib.VMap(ctx, [f[1] for f in fds], [sv.size] * world)
+    for r, f in enumerate(fds):   # imported handles keep the memory; close our copies
+        if r != rank:
+            for x in f:
+                os.close(x)
+    view = _lib.d_csr_view(ctx, db_full.num_rows, db_full.num_cols, nnz, rp.data_ptr(), vc.va, vv.va,
+                           sorted_rows, max_row, owners=(rp, vc, vv, sc, sv))
+    dist.barrier()
+    return view, {"entries_per_shard": e, "granularity": gran, "local_bytes": sc.size + sv.size,
+                  "mapped_bytes": vc.total + vv.total}
+
+
+# Config 2's slabs (bench.py --b-mode sharded at N>1): every rank owns the
+# fine operator's rows of its z-slab; the B rows a rank's R selects (its slab
+# plus a halo plane each side) are gathered by a kernel that reads the peers'
+# slabs through CUDA IPC (tsg_gather_sharded).
 
 def local_shard_tensors(b, lo: int, hi: int, device):
     """(rp, col, val) torch tensors of B's rows [lo, hi) on `device`, row
@@ -125,3 +262,144 @@ def gather_sharded(da, shards, b_cols: int):
     ptrs = [(lo, hi, rp.data_ptr(), col.data_ptr(), 0 if val is None else val.data_ptr())
             for lo, hi, rp, col, val in shards]
     return _lib.d_gather_sharded(da, ptrs, b_cols)
+
+
+# ---------------------------------------------------------------- one rank's block
+
+def mg_multiply(da_block, db, c_budget_bytes: int = 0, keep_c: bool = False):
+    """This rank's block of C = A_block * B (C ABI ``tsg_mg_multiply``)."""
+    from . import _lib
+    return _lib.d_mg_multiply(da_block, db, c_budget_bytes, keep_c)
+
+
+# ---------------------------------------------------------------- config 5 bench arm
+
+def bench_config5(args, dist=None):
+    """BASELINE.json config 5: A*A on an R-MAT graph (Graph500 parameters,
+    SplitMix64 seed 22, unit values), rows partitioned over the ranks by K0
+    flops, B replicated (NCCL all-gather) or sharded in peer HBM
+    (``--b-mode``), C streamed through ``--c-budget-gib`` when it does not fit.
+    Strong scaling: the graph is fixed, every rank takes 1/N of the flops.
+    Timing: CUDA events on each rank's libtsg stream around the block
+    multiply + offset exchange, max over ranks.  Parity: every rank's sum of
+    C's values equals its multiplications exactly (unit values: C_ij counts
+    paths, so the sum over a block is its K0 flops), the global nnz is
+    all-reduced, and sampled rows (incl. the hub) match the oracle."""
+    import torch
+    from . import _lib, generators as gen
+    from .csr import CsrMatrix
+    world = dist.get_world_size() if dist else 1
+    rank = dist.get_rank() if dist else 0
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    ctx = _lib.Context.get(local)
+    ctx.set_timing(True)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    t_setup = time.perf_counter()
+    da = gen.rmat_graph_device(args.scale).set_values(1.0)
+    n = da.num_rows
+    row_flops, total = _lib.d_row_flops(da, da)
+    bounds = flops_partition(row_flops, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    a_blk = da.slice_rows(lo, hi)
+    mode = getattr(args, "b_mode", "replicated") if world > 1 else "local"
+    info = {}
+    t_b = time.perf_counter()
+    if world == 1:
+        db = da
+    elif mode == "sharded":
+        db, info = shard_b(ctx, da, dist, sorted_rows=True)
+    else:
+        sb = shard_bounds(np.diff(_rp_host(ctx, da)), world)
+        shard = da.slice_rows(int(sb[rank]), int(sb[rank + 1]))
+        db = replicate_b(ctx, shard, n, n, dist)
+        del shard
+    b_setup_s = time.perf_counter() - t_b
+    host_a = da.download() if rank == 0 or not getattr(args, "no_parity", False) else None
+    if world > 1:
+        del da
+    budget = int(getattr(args, "c_budget_gib", 48.0) * 2**30)
+    mults = int(row_flops[lo:hi].sum())
+    est_c_bytes = 12 * mults   # nnz(C) <= multiplications
+    c_budget = budget if est_c_bytes > budget else 0
+    setup_s = time.perf_counter() - t_setup
+
+    def step():
+        ctx.record(0)
+        _, st = mg_multiply(a_blk, db, c_budget, keep_c=False)
+        if dist:
+            with torch.cuda.stream(stream):
+                off, tot = exchange_offsets(st["nnz"], dist)
+        else:
+            off, tot = 0, st["nnz"]
+        ctx.record(1)
+        return st, off, tot
+
+    for _ in range(max(1, args.warmup)):
+        st, off, tot = step()
+    if dist:
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        st, off, tot = step()
+        times.append(ctx.elapsed_ms(0, 1))
+    my_ms = statistics.median(times)
+    ms = my_ms
+    flops_all = 2 * total
+    sums_ok = bool(st["value_sum"] == float(mults))
+    if dist:
+        dev = _coll_device(dist)
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        ok = torch.tensor([1.0 if sums_ok else 0.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        sums_ok = bool(ok.item() > 0.5)
+    # sampled rows of this block (incl. its largest-flops row) against the oracle
+    par = {"block_value_sum_equals_mults": sums_ok, "nnz_C": tot}
+    if not getattr(args, "no_parity", False):
+        from oracle import oracle as O
+        cb = O.compress(host_a)
+        rng = np.random.default_rng(rank)
+        rows = sorted(set([lo + int(np.argmax(row_flops[lo:hi]))] +
+                          [int(x) for x in rng.integers(lo, hi, size=min(6, hi - lo))])) if hi > lo else []
+        exact = ok = True
+        from bench_configs import compare_products
+        for r in rows:
+            sub = CsrMatrix._adopt(1, n, np.array([0, host_a.row_ptr[r + 1] - host_a.row_ptr[r]]),
+                                   host_a.col_idx[host_a.row_ptr[r]:host_a.row_ptr[r + 1]],
+                                   host_a.values[host_a.row_ptr[r]:host_a.row_ptr[r + 1]])
+            want = O.numeric(sub, host_a, O.symbolic(sub, cb))
+            c1, _ = mg_multiply(a_blk.slice_rows(r - lo, r - lo + 1), db, 0, keep_c=True)
+            res = compare_products(c1.download(), want)
+            exact &= res["exact"]
+            ok &= res["ok"]
+        if dist:
+            dev = _coll_device(dist)
+            t = torch.tensor([1.0 if ok else 0.0, 1.0 if exact else 0.0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok, exact = bool(t[0].item() > 0.5), bool(t[1].item() > 0.5)
+        par.update(sampled_rows_ok=ok, sampled_rows_exact=exact, rows_per_rank=len(rows))
+    par["ok"] = bool(sums_ok and par.get("sampled_rows_ok", True))
+    line = {"metric": "SpGEMM GFLOP/s config 5 (A*A R-MAT scale %d, %d GPU, B %s)" % (args.scale, world, mode),
+            "value": flops_all / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+            "ms_per_step": ms, "steps": args.steps, "warmup": args.warmup, "scaling": "strong",
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5 A*A R-MAT scale %d ef16 (.57,.19,.19,.05) SplitMix64 seed 22"
+                                   % args.scale, "n": n, "multiplications": total,
+                       "b_mode": mode, "partition": "K0 flops, contiguous row blocks",
+                       "c_mode": "streamed (budget %d GiB per GPU)" % (budget >> 30) if c_budget else
+                                 "materialised per GPU", "rank0_block_rows": hi - lo},
+            "per_rank": {"ms": my_ms, "blocks": st["blocks"], "max_block_nnz": st["max_block_nnz"],
+                         "mults": mults},
+            "setup": {"total_s": setup_s, "b_setup_s": b_setup_s, **info},
+            "parity": par}
+    return line
+
+
+def _rp_host(ctx, d):
+    from . import _lib
+    rp = np.empty(d.num_rows + 1, dtype=np.int64)
+    rp_p, _, _ = d.device_ptrs()
+    _lib.memcpy(ctx, rp.ctypes.data, rp_p, rp.nbytes)
+    return rp

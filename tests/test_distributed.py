@@ -147,3 +147,130 @@ def test_two_rank_b_shards_shared():
         assert bounds[0] == 0 and len(got) == world
         assert [g[0] for g in got] == bounds[:-1] and [g[1] for g in got] == bounds[1:]
         assert all(g[2] and g[3] and g[4] for g in got)
+
+
+def test_element_shards_fill_whole_granules():
+    from paper_1804_00695_b200 import distributed as D
+    g = 2 << 20
+    for nnz in (1, 1000, 524288, 524289, 10**9 + 7):
+        for world in (1, 2, 3, 8):
+            e = D.element_shards(nnz, world, g)
+            assert (4 * e) % g == 0 and (8 * e) % g == 0
+            assert e * world >= nnz and (e - g // 4) * world < max(nnz, 1) + world * (g // 4)
+
+
+def _fd_worker(rank, world, port, q):
+    """exchange_fds on CPU: each rank shares a memfd holding its rank; every
+    rank reads every peer's file through the received descriptor."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    from paper_1804_00695_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fd = os.memfd_create("shard%d" % rank)
+        os.write(fd, ("rank-%d" % rank).encode())
+        got = D.exchange_fds([fd], dist)
+        seen = [os.pread(f[0], 16, 0).decode() for f in got]
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_fd_exchange():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, seen in res:
+        assert seen == ["rank-%d" % r for r in range(world)]
+
+
+def _mg_worker(rank, world, port, q, mode, scale):
+    """One rank of the config-5 path on the product kernels: R-MAT built on
+    the device, K0-flops row partition, B replicated (gloo all-gather) or
+    sharded (VMM shards mapped into one VA, descriptors over Unix sockets),
+    block multiply materialised and streamed, offset exchange."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    from paper_1804_00695_b200 import _lib, distributed as D, generators as gen
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        ctx = _lib.Context.get(0)
+        da = gen.rmat_graph_device(scale).set_values(1.0)
+        n = da.num_rows
+        row_flops, total = _lib.d_row_flops(da, da)
+        bounds = D.flops_partition(row_flops, world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        a_blk = da.slice_rows(lo, hi)
+        if mode == "sharded":
+            db, info = D.shard_b(ctx, da, dist)
+        else:
+            rp = np.empty(n + 1, dtype=np.int64)
+            _lib.memcpy(ctx, rp.ctypes.data, da.device_ptrs()[0], rp.nbytes)
+            sb = D.shard_bounds(np.diff(rp), world)
+            db = D.replicate_b(ctx, da.slice_rows(int(sb[rank]), int(sb[rank + 1])), n, n, dist)
+        c, st = D.mg_multiply(a_blk, db, 0, keep_c=True)
+        _, st2 = D.mg_multiply(a_blk, db, 1 << 20, keep_c=False)   # streamed in small blocks
+        off, tot = D.exchange_offsets(st["nnz"], dist)
+        h = c.download()
+        q.put((rank, lo, hi, off, tot, h.row_ptr.copy(), h.col_idx.copy(), h.values.copy(), st, st2,
+               int(row_flops[lo:hi].sum()), bounds.tolist()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["replicated", "sharded"])
+def test_two_process_config5_on_product_kernels(mode):
+    """Two processes (gloo; both on GPU 0 -- their kernels never wait on each
+    other) run the multi-GPU path end to end; the gathered blocks equal the
+    oracle's A*A, the streamed-C statistics equal the materialised ones, and
+    every block's value sum equals its multiplications."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_1804_00695_b200 import generators as gen
+    from paper_1804_00695_b200.csr import CsrMatrix
+    from oracle import oracle as O
+    from conftest import assert_same_product
+    world, scale = 2, 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mg_worker, args=(r, world, port, q, mode, scale)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    a = gen.with_unit_values(gen.rmat_graph(scale))
+    rp, cols, vals = [np.zeros(1, np.int64)], [], []
+    for rank, lo, hi, off, tot, prp, pcol, pval, st, st2, mults, bounds in res:
+        assert off == int(sum(x[9]["nnz"] for x in res[:rank]))
+        assert tot == sum(x[8]["nnz"] for x in res)
+        assert st["nnz"] == st2["nnz"] == len(pcol) and st2["blocks"] > 1
+        assert st["value_sum"] == st2["value_sum"] == float(mults)
+        rp.append(prp[1:] + rp[-1][-1])
+        cols.append(pcol)
+        vals.append(pval)
+    got = CsrMatrix(a.num_rows, a.num_cols, np.concatenate(rp), np.concatenate(cols), np.concatenate(vals))
+    assert_same_product(got, O.multiply(a, a, workers=os.cpu_count() or 1), exact=False, rtol=1e-12)
