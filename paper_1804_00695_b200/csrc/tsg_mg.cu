@@ -340,11 +340,17 @@ extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, i
             TSG_CK(cudaStreamSynchronize(c->stream));
         }
         tsg_free(c, flops);
+        // C entries per block <= budget / 16 (12 B of C + symbolic / numeric
+        // scratch).  nnz(C_i) <= mults_i, but hashing merges most products
+        // (R-MAT A*A: ~3 per entry): each block is sized by the largest
+        // entries-per-multiplication ratio seen so far (x 1.25), starting at 1
         const int64_t cap_entries = std::max<int64_t>(c_budget_bytes / 16, 1);
+        double ratio = 1.0;
         int64_t lo = 0;
         while (lo < a->rows && st_ == TSG_OK) {
+            const double cap_mults = (double)cap_entries / std::min(1.0, 1.25 * ratio);
             int64_t hi = lo, acc = 0;
-            while (hi < a->rows && (hi == lo || acc + hf[hi] <= cap_entries)) acc += hf[hi++];
+            while (hi < a->rows && (hi == lo || (double)(acc + hf[hi]) <= cap_mults)) acc += hf[hi++];
             tsg_csr *as = nullptr;
             st_ = tsg_csr_slice_rows(c, a, lo, hi, &as);
             if (st_ != TSG_OK) break;
@@ -366,6 +372,7 @@ extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, i
                     ++c->launches;
                 }
                 local.max_block_nnz = std::max(local.max_block_nnz, C->nnz);
+                if (acc > 0) ratio = std::max(local.blocks ? ratio : 0.0, (double)C->nnz / (double)acc);
                 tsg_csr_free(c, C);
             }
             tsg_csr_free(c, as);
