@@ -111,8 +111,12 @@ int tsg_host_free(void *p);
 int tsg_csr_upload(tsg_ctx *ctx, int64_t rows, int64_t cols, int64_t nnz,
                    const int64_t *row_ptr, const int64_t *col_idx,
                    const double *values, tsg_csr **out);
+/* nnz of a product is resolved on first request: tsg_multiply may return
+   before the device has counted C's entries (its device-driven path never
+   waits), so asking for nnz can synchronise; tsg_csr_dims never does. */
 int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int64_t *nnz,
                  int *has_values);
+int tsg_csr_dims(const tsg_csr *m, int64_t *rows, int64_t *cols, int *has_values);
 /* Host buffers sized rows+1 / nnz / nnz (values may be NULL to skip). */
 int tsg_csr_download(tsg_ctx *ctx, const tsg_csr *m, int64_t *row_ptr,
                      int64_t *col_idx, double *values);

@@ -49,7 +49,7 @@ EXPORTS = (
     "tsg_csr_set_values", "tsg_gather_sharded", "tsg_stencil", "tsg_aggregation", "tsg_transpose",
     "tsg_rap", "tsg_row_flops", "tsg_stream", "tsg_chunk_symbolic",
     "tsg_shard_granularity", "tsg_shard_alloc", "tsg_shard_free", "tsg_shard_map", "tsg_vmap_free",
-    "tsg_csr_view", "tsg_mg_multiply", "tsg_memcpy",
+    "tsg_csr_view", "tsg_mg_multiply", "tsg_memcpy", "tsg_csr_dims",
 )
 
 _P = ctypes.c_void_p
@@ -96,6 +96,7 @@ _SIGS = {
     "tsg_csr_view": ([_P, _I64, _I64, _I64, _P, _P, _P, ctypes.c_int, _I64, _PP], ctypes.c_int),
     "tsg_mg_multiply": ([_P, _P, _P, _I64, _PP, _P], ctypes.c_int),
     "tsg_memcpy": ([_P, _P, _P, ctypes.c_size_t], ctypes.c_int),
+    "tsg_csr_dims": ([_P, _PI64, _PI64, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tsg_symbolic": ([_P, _P, _P, _PP], ctypes.c_int),
     "tsg_numeric": ([_P, _P, _P, _P, _P, _PP], ctypes.c_int),
     "tsg_multiply": ([_P, _P, _P, _PP], ctypes.c_int),
@@ -296,9 +297,20 @@ class DeviceCsr(_Handle):
 
     def __init__(self, ctx, h):
         super().__init__(ctx, h)
-        r, c, n, hv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
-        check(load().tsg_csr_info(h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(n), ctypes.byref(hv)))
-        self.num_rows, self.num_cols, self.nnz, self.has_values = r.value, c.value, n.value, bool(hv.value)
+        r, c, hv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        check(load().tsg_csr_dims(h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(hv)))
+        self.num_rows, self.num_cols, self.has_values = r.value, c.value, bool(hv.value)
+        self._nnz = None
+
+    @property
+    def nnz(self) -> int:
+        """Entries (a product's count is read from the device on first use:
+        the multiply that made it did not wait for the device)."""
+        if self._nnz is None:
+            n = ctypes.c_int64()
+            check(load().tsg_csr_info(self.h, None, None, ctypes.byref(n), None))
+            self._nnz = n.value
+        return self._nnz
 
     @classmethod
     def upload(cls, m, ctx=None):

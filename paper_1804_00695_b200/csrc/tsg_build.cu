@@ -408,6 +408,7 @@ extern "C" int tsg_aggregation(tsg_ctx *c, const int64_t *dims, int ndims, int f
 }
 
 extern "C" int tsg_transpose(tsg_ctx *c, const tsg_csr *a, tsg_csr **out) {
+    TSG_RESOLVE(c, a);
     if (!c || !a || !out) {
         tsg_set_error("tsg_transpose: bad arguments");
         return TSG_EARG;

@@ -1054,8 +1054,27 @@ extern "C" int tsg_csr_upload(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nn
     return TSG_OK;
 }
 
+int tsg_csr_resolve(tsg_ctx *c, tsg_csr *m) {
+    if (!m || !m->lazy_nnz) return TSG_OK;
+    tsg_ctx *o = m->owner ? m->owner : c;
+    TSG_TRY(tsg_put_small(o, m->rp + m->rows, 1, 20));
+    TSG_CK(cudaStreamSynchronize(o->stream));
+    m->nnz = o->h_small[20];
+    m->lazy_nnz = 0;
+    if (o->pending) return tsg_check_kernel_errors(o, o->pending);   // the producer's errors
+    return TSG_OK;
+}
+
+extern "C" int tsg_csr_dims(const tsg_csr *m, int64_t *rows, int64_t *cols, int *has_values) {
+    if (rows) *rows = m->rows;
+    if (cols) *cols = m->cols;
+    if (has_values) *has_values = m->val != nullptr;
+    return TSG_OK;
+}
+
 extern "C" int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int64_t *nnz,
                             int *has_values) {
+    if (nnz && m->lazy_nnz) TSG_TRY(tsg_csr_resolve(m->owner, const_cast<tsg_csr *>(m)));
     if (rows) *rows = m->rows;
     if (cols) *cols = m->cols;
     if (nnz) *nnz = m->nnz;
@@ -1065,6 +1084,7 @@ extern "C" int tsg_csr_info(const tsg_csr *m, int64_t *rows, int64_t *cols, int6
 
 extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
                                 int64_t *col_idx, double *values) {
+    TSG_RESOLVE(c, m);
     if (m->host_mapped) {   // already in host memory: widen on the host
         TSG_CK(cudaStreamSynchronize(c->stream));
         if (c->pending) TSG_TRY(tsg_check_kernel_errors(c, c->pending));
@@ -1092,6 +1112,7 @@ extern "C" int tsg_csr_download(tsg_ctx *c, const tsg_csr *m, int64_t *row_ptr,
 
 extern "C" int tsg_csr_slice_rows(tsg_ctx *c, const tsg_csr *m, int64_t begin, int64_t end,
                                   tsg_csr **out) {
+    TSG_RESOLVE(c, m);
     if (!(0 <= begin && begin <= end && end <= m->rows)) {
         tsg_set_error("row slice [%lld, %lld) out of range", (long long)begin, (long long)end);
         return TSG_EDIM;

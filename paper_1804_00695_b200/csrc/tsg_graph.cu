@@ -256,6 +256,7 @@ int sort_rows(tsg_ctx *c, Temp &tmp, int64_t rows, int64_t nnz, const int64_t *r
 
 extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr **out,
                                int64_t *perm_host) {
+    TSG_RESOLVE(c, g);
     if (!c || !g || !out) {
         tsg_set_error("tsg_graph_lower: null argument");
         return TSG_EARG;
@@ -373,6 +374,7 @@ __global__ void k_set_values(int64_t n, double v, double *__restrict__ out) {
 }  // namespace
 
 extern "C" int tsg_csr_set_values(tsg_ctx *c, tsg_csr *m, double value) {
+    TSG_RESOLVE(c, m);
     if (m->host_mapped) {
         tsg_set_error("tsg_csr_set_values: matrix lives in mapped host memory");
         return TSG_EARG;
@@ -546,6 +548,7 @@ extern "C" int tsg_gather_sharded(tsg_ctx *c, int n_shards, const int64_t *row_l
                                   const void *const *shard_rp, const void *const *shard_col,
                                   const void *const *shard_val, int64_t b_cols, const tsg_csr *a,
                                   tsg_csr **out) {
+    TSG_RESOLVE(c, a);
     if (!c || !a || !out || n_shards < 1 || !row_lo_host) {
         tsg_set_error("tsg_gather_sharded: bad arguments");
         return TSG_EARG;

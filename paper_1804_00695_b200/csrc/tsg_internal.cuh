@@ -45,6 +45,12 @@ struct tsg_ctx {
     float phase_ms[8];
     int64_t bytes_in_use;
     int64_t bytes_peak;       // high-water mark of bytes_in_use (the chunked executors reset it)
+    // device-driven multiply (tsg_multiply's fast path): the partitions do not
+    // wait for the host, bins launch on the host's bounds, and allocations
+    // take these bounds instead of read-back sizes
+    int nowait;
+    uint32_t sym_possible, num_possible;
+    int64_t set_cap_bound, nnz_bound, c_row_bound;
     cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
     cudaStream_t widen;       // int32 -> int64 widening of drained C ranges (own stream, so a
                               // narrow for an H2D piece never queues behind a C drain)
@@ -85,7 +91,17 @@ struct tsg_csr {
     int distinct;      // 1: no column repeats within a row (lane-split numeric mode is race-free)
     int64_t max_row;   // longest row, or -1 if unknown
     int borrowed;      // arrays owned by the caller (tsg_csr_view): free releases only the handle
+    // A product of a device-driven multiply: the host never waited for it,
+    // so `nnz` is the allocation bound and the exact count is rp[rows] on the
+    // device, read on first need (tsg_csr_resolve).  max_row_bound (> 0) is
+    // an upper bound on its row lengths, for the next multiply's planning.
+    int lazy_nnz;
+    tsg_ctx *owner;
+    int64_t max_row_bound;
 };
+// exact nnz of a product whose count is still on the device (no-op otherwise)
+int tsg_csr_resolve(tsg_ctx *ctx, tsg_csr *m);
+#define TSG_RESOLVE(ctx, m) TSG_TRY(tsg_csr_resolve((ctx), const_cast<tsg_csr *>(m)))
 
 struct tsg_cmat {
     int64_t rows;

@@ -266,6 +266,7 @@ __global__ void k_i64_to_i32(const int64_t *in, int32_t *out, int64_t n) {
 }  // namespace
 
 extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl, int64_t *total) {
+    TSG_RESOLVE(c, l);
     if (l->rows != cl->rows) {
         tsg_set_error("matrix and compressed form disagree on row count");
         return TSG_EDIM;

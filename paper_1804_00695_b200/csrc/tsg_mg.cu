@@ -291,6 +291,8 @@ extern "C" int tsg_csr_view(tsg_ctx *c, int64_t rows, int64_t cols, int64_t nnz,
 // reduced and released; *c_out stays NULL).
 extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int64_t c_budget_bytes,
                                tsg_csr **c_out, tsg_mg_stats *st) {
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, b);
     if (a->cols != b->rows) {
         tsg_set_error("A has %lld cols but B has %lld rows", (long long)a->cols, (long long)b->rows);
         return TSG_EDIM;

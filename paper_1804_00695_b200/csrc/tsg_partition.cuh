@@ -23,6 +23,13 @@ template <int NB>
 struct BinLists {
     int32_t *list = nullptr;
     int64_t off[NB + 1] = {0};
+    // device-driven mode (tsg_partition with nowait): the bin starts live
+    // only in device memory (dstart[0 .. NB]); off[] holds no counts and
+    // `rows` bounds every bin
+    int64_t *dstart = nullptr;
+    bool device = false;
+    int64_t rows = 0;
+    uint32_t possible = 0xffffffffu;   // device mode: bins the host's bounds allow
 };
 
 // tile counts up to this many are scanned by the last k_part_bins block
@@ -108,11 +115,13 @@ __global__ void __launch_bounds__(256) k_part_scatter(int64_t rows, const uint8_
                                                       int32_t *__restrict__ list,
                                                       const int64_t *__restrict__ extra,
                                                       const int *__restrict__ err,
-                                                      int64_t *__restrict__ out, int64_t seq) {
+                                                      int64_t *__restrict__ out, int64_t seq,
+                                                      int64_t *__restrict__ dstart) {
     pdl_wait();
     __shared__ int h[NB];
     if (threadIdx.x < NB) h[threadIdx.x] = 0;
-    if (blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
+    if (dstart && blockIdx.x == 0 && threadIdx.x <= NB) dstart[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
+    if (out && blockIdx.x == 0) {   // `out` is the mapped host scratch (h_small[32 ..])
         if (threadIdx.x <= NB) out[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles];
         if (threadIdx.x == NB + 1) out[NB + 1] = extra ? *extra : 0;
         // pending kernel errors of earlier work ride along (h_small[62])
@@ -151,7 +160,8 @@ struct NoMid {
 
 template <int NB, class F, class Mid = NoMid>
 int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
-                  const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid()) {
+                  const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid(),
+                  bool nowait = false) {
     static_assert(32 + NB + 2 <= 61, "partition results overlap the sequence / error slots");
     int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
     if (ntiles < 1) ntiles = 1;
@@ -168,9 +178,25 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_TRY(mid());
     // results land in mapped host memory straight from the kernel: no D2H
     // copy that would queue behind bulk transfers on the copy engine
+    if (nowait) {
+        // device-driven: the bin kernels read their ranges from dstart; the
+        // host learns nothing and waits for nothing
+        TSG_TRY(tsg_alloc_t(c, &out.dstart, NB + 1));
+        out.device = true;
+        out.rows = rows;
+        TSG_CK(launch_pdl(k_part_scatter<NB>, ntiles, 256, 0, c->stream, rows, (const uint8_t *)bins, ntiles,
+                          (const int64_t *)offs, out.list, extra, (const int *)c->d_err, (int64_t *)nullptr,
+                          (int64_t)0, out.dstart));
+        ++c->launches;
+        TSG_CK(cudaGetLastError());
+        TSG_TRY(tsg_free(c, tc));
+        TSG_TRY(tsg_free(c, offs));
+        for (int b = 0; b <= NB; b++) out.off[b] = -1;
+        return TSG_OK;
+    }
     TSG_CK(launch_pdl(k_part_scatter<NB>, ntiles, 256, 0, c->stream, rows, (const uint8_t *)bins, ntiles,
                       (const int64_t *)offs, out.list, extra, (const int *)c->d_err, c->hd_small + 32,
-                      ++c->part_seq));
+                      ++c->part_seq, (int64_t *)nullptr));
     ++c->launches;
     TSG_CK(cudaGetLastError());
     TSG_TRY(tsg_free(c, tc));

@@ -375,6 +375,9 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out);
 
 extern "C" int tsg_rap(tsg_ctx *c, const tsg_csr *r, const tsg_csr *a, const tsg_csr *p, int mode,
                        tsg_csr **out, int *fused) {
+    TSG_RESOLVE(c, r);
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, p);
     if (!c || !r || !a || !p || !out) {
         tsg_set_error("tsg_rap: bad arguments");
         return TSG_EARG;

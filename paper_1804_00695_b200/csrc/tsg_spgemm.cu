@@ -26,6 +26,8 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <map>
+#include <mutex>
 
 #include "tsg_group.cuh"
 #include <functional>
@@ -57,9 +59,24 @@ struct SymArgs {
     uint64_t *obits;
     const int *maxcb;    // device max sets per compressed B row (<= 1: unit path)
     int unit_dense;      // compressed row k is entry k (every B row holds exactly one set)
+    // device-driven bins (no host read-back): the launch covers bin `bin`
+    // whose rows are list[dbins[bin] .. dbins[bin + 1]) (see bin_range)
+    const int64_t *dbins;
+    int bin;
 };
 
 constexpr int SETS_WRITTEN = 1 << 30;
+
+// A bin kernel launched without the host knowing the bin's size takes its
+// row range from the partition's device-side bin starts.
+template <class Args, class P>
+__device__ __forceinline__ void bin_range(const Args &a, P &list, int64_t &nlist) {
+    if (a.dbins) {
+        const int64_t b0 = a.dbins[a.bin];
+        nlist = a.dbins[a.bin + 1] - b0;
+        list += b0;
+    }
+}
 constexpr int UB = 4;   // A chunks whose loads are batched on the unit-row paths
 
 struct NumArgs {
@@ -98,6 +115,8 @@ struct NumArgs {
     const int *unit_b;   // device flag: every B row has <= 1 entry (read if unit_known < 0)
     int unit_known;      // 1 / 0: known on the host (uploaded B), -1: read *unit_b
     int unit_dense;      // B row k is entry k (every row exactly one entry): no row_ptr gather
+    const int64_t *dbins;   // device-driven bins, as in SymArgs
+    int bin;
 };
 
 __device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
@@ -220,7 +239,7 @@ __host__ __device__ __forceinline__ int64_t dense_words(int64_t ncols) { return 
 __host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
 // symbolic: table only (16 B/slot)
-__device__ __forceinline__ int sym_bin(int64_t sbound) {
+__host__ __device__ __forceinline__ int sym_bin(int64_t sbound) {
     if (sbound <= 0) return 255;
     int64_t T = table_slots(sbound);
     int64_t need = 24 * T;
@@ -232,7 +251,7 @@ __device__ __forceinline__ int sym_bin(int64_t sbound) {
 }
 
 // numeric: table + dense fp64 values for the group tier; table for CTA tier
-__device__ __forceinline__ int num_bin(int64_t n, int64_t m) {
+__host__ __device__ __forceinline__ int num_bin(int64_t n, int64_t m) {
     if (n <= 0) return 255;
     int64_t T = table_slots(m);
     int64_t need = round16(8 * n) + 16 * T;
@@ -347,6 +366,7 @@ constexpr int SYM_OPT_T = 32;   // first table size for unit rows (up to 32 dist
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
+    bin_range(a, list, nlist);
     extern __shared__ int4 smem[];
     constexpr int TMAX = SLICE / 24;   // 16 B table slot + 8 B sort key per slot
     const unsigned gm = group_mask<G>();
@@ -515,6 +535,7 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
 template <int G, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
+    bin_range(a, list, nlist);
     extern __shared__ int4 smem[];
     constexpr int CAP = SLICE / 12;
     const unsigned gm = group_mask<G>();
@@ -606,6 +627,7 @@ __global__ void __launch_bounds__(256) k_sym_merge(const int32_t *__restrict__ l
 template <int G, int K, int SLICE>
 __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ list, int64_t nlist,
                                                     SymArgs a) {
+    bin_range(a, list, nlist);
     extern __shared__ int4 smem[];
     constexpr int CAP = SLICE / 12;
     const unsigned gm = group_mask<G>();
@@ -827,6 +849,7 @@ constexpr int TSYM_BATCH = 8;
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sym_thread(const int32_t *__restrict__ list, int64_t nlist,
                                                    SymArgs a) {
+    bin_range(a, list, nlist);
     for (int64_t li = (int64_t)blockIdx.x * NT + threadIdx.x; li < nlist; li += (int64_t)gridDim.x * NT) {
         const int64_t i = list[li];
         const int64_t gi = i + a.a_row_off;
@@ -961,8 +984,11 @@ __device__ __forceinline__ void ordered_add(unsigned gm, double *vals, int pos, 
 
 // One A entry's B-row batch for products_seq: the first BB_UF*G entries of
 // the row, loaded together so their DRAM latencies overlap.
+#ifndef TSG_BBUF8
+#define TSG_BBUF8 4
+#endif
 template <int G>
-__host__ __device__ constexpr int bb_uf() { return G < 8 ? 8 : 4; }   // >= 32 entries per batch
+__host__ __device__ constexpr int bb_uf() { return G < 8 ? 8 : (G == 8 ? TSG_BBUF8 : 4); }   // >= 32 entries per batch
 template <int UF>
 struct BBatchT {
     int c[UF];
@@ -1259,6 +1285,7 @@ __host__ __device__ constexpr int num_minb() {
 template <int G, int SLICE, int MODE>
 __global__ void __launch_bounds__(num_bs<G, MODE>(), num_minb<G, MODE>()) k_num_group(const int32_t *__restrict__ list, int64_t nlist,
                                                    NumArgs a) {
+    bin_range(a, list, nlist);
     extern __shared__ int4 smem[];
     const unsigned gm = group_mask<G>();
     const int glane = threadIdx.x & (G - 1);
@@ -1779,41 +1806,99 @@ unsigned group_grid(tsg_ctx *c, int64_t nrows, int groups_per_block) {
     return grid_for(nrows, groups_per_block, c->num_sms * 64);
 }
 
+// Device-driven bins: a bin's size is unknown to the host, so its kernel is
+// launched with one resident wave (grid-stride loops cover any size) and
+// takes its rows from the partition's device-side bin starts.
+template <class K>
+unsigned resident_grid(tsg_ctx *c, K kernel, int bs, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, size_t>, int> cache;
+    const auto key = std::make_pair((const void *)kernel, smem);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    int nb;
+    if (it != cache.end()) {
+        nb = it->second;
+    } else {
+        nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, bs, smem) != cudaSuccess) {
+            cudaGetLastError();
+            nb = 1;
+        }
+        if (nb < 1) nb = 1;
+        cache[key] = nb;
+    }
+    return (unsigned)(nb * c->num_sms);
+}
+
+// The rows of bin B for a launch: (list, n) from the host offsets, or -- in
+// device-driven mode -- the whole list with the bin id in the kernel
+// arguments (bin_range) and n = an upper bound for grid sizing.  False:
+// nothing to launch (empty, or impossible by the host's bounds).
+template <class Args>
+bool bin_select(const Bins &bl, int B, Args &a, const int32_t *&list, int64_t &n) {
+    if (bl.device) {
+        if (!((bl.possible >> B) & 1u)) return false;
+        a.dbins = bl.dstart;
+        a.bin = B;
+        list = bl.list;
+        n = bl.rows;
+        return n > 0;
+    }
+    n = bl.off[B + 1] - bl.off[B];
+    if (n <= 0) return false;
+    a.dbins = nullptr;
+    list = bl.list + bl.off[B];
+    return true;
+}
+
+template <class K>
+unsigned bin_grid(tsg_ctx *c, const Bins &bl, unsigned grid, K kernel, int bs, size_t smem) {
+    if (!bl.device) return grid;
+    const unsigned r = resident_grid(c, kernel, bs, smem);
+    return grid < r ? grid : r;
+}
+
 // global-tier slab sizing: T slots per CTA, bounded by a memory budget
 constexpr int64_t GLOBAL_SLAB_BUDGET = (int64_t)2 << 30;
 
 template <int B>
-int launch_sym_group(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+int launch_sym_group(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
     constexpr int G = gt_g_sym(B), SL = gt_slice(B), BS = gt_block(B);
-    int64_t n = bl.off[B + 1] - bl.off[B];
-    if (n <= 0) return TSG_OK;
+    SymArgs a = a0;
+    const int32_t *lst;
+    int64_t n;
+    if (!bin_select(bl, B, a, lst, n)) return TSG_OK;
     size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_sym_group<G, SL>, smem));
-    unsigned grid = group_grid(c, n, BS / G);
-    k_sym_group<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    unsigned grid = bin_grid(c, bl, group_grid(c, n, BS / G), k_sym_group<G, SL>, BS, smem);
+    k_sym_group<G, SL><<<grid, BS, smem, c->stream>>>(lst, n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_sym_group", B, grid, BS, smem));
     return TSG_OK;
 }
 
 template <int B, int MODE>
-int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
+int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a0) {
     // unit-B rows (owner-folded products) of the two smallest bins: 4 lanes
     // per row, twice the rows in flight (measured: RA*P 241 -> 182 us; the
     // lane-split SEQ mode stays at 8 lanes, where 4 was slower)
     constexpr int G = (MODE == 2 && B <= 1) ? 4 : gt_g(B), SL = gt_slice(B);
     constexpr int BS = num_bs<G, MODE>() < gt_block(B) ? num_bs<G, MODE>() : gt_block(B);
-    int64_t n = bl.off[B + 1] - bl.off[B];
+    NumArgs a = a0;
+    const int32_t *lst;
+    int64_t n;
+    if (!bin_select(bl, B, a, lst, n)) return TSG_OK;
     size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * ustage_bytes<G>() : 0);
     TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
-    unsigned grid = group_grid(c, n, BS / G);
-    k_num_group<G, SL, MODE><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    unsigned grid = bin_grid(c, bl, group_grid(c, n, BS / G), k_num_group<G, SL, MODE>, BS, smem);
+    k_num_group<G, SL, MODE><<<grid, BS, smem, c->stream>>>(lst, n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_num_group", B, grid, BS, smem));
     return TSG_OK;
 }
 
 template <int B>
 int launch_num_group(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
-    if (bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
+    if (bl.device ? !((bl.possible >> B) & 1u) : bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
     // lane-per-B-entry mode pays off once B rows fill at least half a group
     if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, 1>(c, bl, a);
     if (a.unit_known > 0) return launch_num_group_m<B, 2>(c, bl, a);
@@ -1822,6 +1907,7 @@ int launch_num_group(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
 
 template <int CB>
 int launch_sym_cta(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
     const int B = 7 + CB;
     int64_t n = bl.off[B + 1] - bl.off[B];
@@ -1836,6 +1922,7 @@ int launch_sym_cta(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 
 template <int CB>
 int launch_num_cta(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     constexpr int NT = ct_nt(CB), TS = ct_slots(CB);
     const int B = 7 + CB;
     int64_t n = bl.off[B + 1] - bl.off[B];
@@ -1875,6 +1962,7 @@ int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64
 }
 
 int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
@@ -1899,6 +1987,7 @@ int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 }
 
 int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
@@ -1926,38 +2015,43 @@ int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
 }
 
 template <int M>
-int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
+int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
     constexpr int G = mt_g(M), SL = mt_slice(M), BS = 256;
     const int B = BIN_MERGE + M;
-    const int64_t n = bl.off[B + 1] - bl.off[B];
-    if (n <= 0) return TSG_OK;
+    SymArgs a = a0;
+    const int32_t *lst;
+    int64_t n;
+    if (!bin_select(bl, B, a, lst, n)) return TSG_OK;
     if constexpr (MERGE_LISTS_PER_LANE > 1) {   // K lists per lane, G / K lanes per row
         constexpr int K = MERGE_LISTS_PER_LANE, G2 = G / K;
         const size_t smem = (size_t)(BS / G2) * SL;
         TSG_TRY(set_smem(k_sym_merge2<G2, K, SL>, smem));
-        const unsigned grid = group_grid(c, n, BS / G2);
-        k_sym_merge2<G2, K, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+        const unsigned grid = bin_grid(c, bl, group_grid(c, n, BS / G2), k_sym_merge2<G2, K, SL>, BS, smem);
+        k_sym_merge2<G2, K, SL><<<grid, BS, smem, c->stream>>>(lst, n, a); ++c->launches;
         TSG_TRY(tsg_launch_check("k_sym_merge2", B, grid, BS, smem));
         return TSG_OK;
     }
     const size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_sym_merge<G, SL>, smem));
-    const unsigned grid = group_grid(c, n, BS / G);
-    k_sym_merge<G, SL><<<grid, BS, smem, c->stream>>>(bl.list + bl.off[B], n, a); ++c->launches;
+    const unsigned grid = bin_grid(c, bl, group_grid(c, n, BS / G), k_sym_merge<G, SL>, BS, smem);
+    k_sym_merge<G, SL><<<grid, BS, smem, c->stream>>>(lst, n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_sym_merge", B, grid, BS, smem));
     return TSG_OK;
 }
 
-int launch_sym_thread(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
-    const int64_t n = bl.off[BIN_THREAD + 1] - bl.off[BIN_THREAD];
-    if (n <= 0) return TSG_OK;
-    const unsigned grid = grid_for(n, 128, c->num_sms * 16);
-    k_sym_thread<128><<<grid, 128, 0, c->stream>>>(bl.list + bl.off[BIN_THREAD], n, a); ++c->launches;
+int launch_sym_thread(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
+    SymArgs a = a0;
+    const int32_t *lst;
+    int64_t n;
+    if (!bin_select(bl, BIN_THREAD, a, lst, n)) return TSG_OK;
+    const unsigned grid = bin_grid(c, bl, grid_for(n, 128, c->num_sms * 16), k_sym_thread<128>, 128, 0);
+    k_sym_thread<128><<<grid, 128, 0, c->stream>>>(lst, n, a); ++c->launches;
     TSG_TRY(tsg_launch_check("k_sym_thread", BIN_THREAD, grid, 128, 0));
     return TSG_OK;
 }
 
 int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
     if (n <= 0) return TSG_OK;
     const int64_t nw = dense_words(ncols);
@@ -1970,6 +2064,7 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
 }
 
 int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
     if (n <= 0) return TSG_OK;
     const int64_t nw = dense_words(ncols);
@@ -2047,7 +2142,9 @@ int run_bins_largest_first(tsg_ctx *c, BinJob *jobs, int njobs) {
 }
 
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
-    auto cnt = [&](int b) { return bl.off[b + 1] - bl.off[b]; };
+    auto cnt = [&](int b) -> int64_t {
+        return bl.device ? (int64_t)((bl.possible >> b) & 1u) : bl.off[b + 1] - bl.off[b];
+    };
     BinJob jobs[] = {
         {cnt(BIN_THREAD), [&] { return launch_sym_thread(c, bl, a); }},
         {cnt(BIN_MERGE + 0), [&] { return launch_sym_merge<0>(c, bl, a); }},
@@ -2069,7 +2166,9 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 }
 
 int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
-    auto cnt = [&](int b) { return bl.off[b + 1] - bl.off[b]; };
+    auto cnt = [&](int b) -> int64_t {
+        return bl.device ? (int64_t)((bl.possible >> b) & 1u) : bl.off[b + 1] - bl.off[b];
+    };
     BinJob jobs[] = {
         {cnt(0), [&] { return launch_num_group<0>(c, bl, a); }},
         {cnt(1), [&] { return launch_num_group<1>(c, bl, a); }},
@@ -2187,11 +2286,16 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
                                              (plain && inline_bounds) ? a->col : nullptr, cb->cnt},
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
-                                     [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); }));
+                                     [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); },
+                                     c->nowait != 0));
+        if (bl.device) {   // device-driven: host bounds instead of read-back sizes
+            bl.possible = c->sym_possible;
+            set_cap = c->set_cap_bound;
+        }
         TSG_TRY(tsg_free(c, scap));
         TSG_TRY(tsg_alloc_t(c, &v->sset, set_cap > 0 ? set_cap : 1));
         TSG_TRY(tsg_alloc_t(c, &v->sbits, set_cap > 0 ? set_cap : 1));
-        SymArgs sa;
+        SymArgs sa{};
         sa.arp = a->rp;
         sa.acol = a->col;
         sa.a_row_off = a_row_off;
@@ -2217,6 +2321,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         TSG_TRY(launch_sym_dense(c, bl, sa, cb_cols));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
         TSG_TRY(tsg_free(c, bl.list));
+        TSG_TRY(tsg_free(c, bl.dstart));
     }
     TSG_TRY(tsg_free(c, bins));
     if (sbound_out)
@@ -2284,7 +2389,11 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     int64_t nnz = 0;
     if (rows_out > 0) {
         TSG_TRY(tsg_partition<NBINS>(c, rows_out, NumBinF{counts->d, counts->aux, sbound_in, cb->sorted_sets ? b->cols : 0}, bins, bl,
-                                     cptr + rows_out, &nnz));
+                                     cptr + rows_out, &nnz, NoMid(), c->nowait != 0));
+        if (bl.device) {
+            bl.possible = c->num_possible;
+            nnz = c->nnz_bound;   // capacity; the exact count stays on the device
+        }
     }
     tsg_csr *C = nullptr;
     if (c->c_host_out) {
@@ -2299,6 +2408,11 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         C->rows = rows_out;
         C->cols = cols_out;
         C->nnz = nnz;
+        if (bl.device) {
+            C->lazy_nnz = 1;
+            C->owner = c;
+            C->max_row_bound = c->c_row_bound;
+        }
         C->rp = cptr;
         C->col = nullptr;
         C->val = nullptr;
@@ -2310,7 +2424,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         }
     }
     if (rows_out > 0 && nnz > 0) {
-        NumArgs na;
+        NumArgs na{};
         na.arp = a->rp;
         na.acol = a->col;
         na.aval = a->val;
@@ -2370,6 +2484,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         }
     }
     if (bl.list) TSG_TRY(tsg_free(c, bl.list));
+    TSG_TRY(tsg_free(c, bl.dstart));
     TSG_TRY(tsg_free(c, bins));
     TSG_TRY(tsg_free(c, sbound));
     if (pt) pt->mark();
@@ -2517,12 +2632,15 @@ extern "C" int tsg_probe_stats(tsg_ctx *c, int64_t out[4], int reset) {
 }
 
 extern "C" int tsg_compress(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
+    TSG_RESOLVE(c, b);
     TSG_TRY(tsg_compress_impl(c, b, out));
     return tsg_check_kernel_errors(c, "compress");
 }
 
 extern "C" int tsg_count_multiplications(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b,
                                          int64_t *total) {
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, b);
     if (a->cols != b->rows) {
         tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
                       (long long)b->rows);
@@ -2544,6 +2662,8 @@ extern "C" int tsg_count_multiplications(tsg_ctx *c, const tsg_csr *a, const tsg
 // (kernel.py:96-103 count_multiplications).
 extern "C" int tsg_row_flops(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int64_t *flops_host,
                              int64_t *total) {
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, b);
     if (a->cols != b->rows) {
         tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
                       (long long)b->rows);
@@ -2571,6 +2691,7 @@ extern "C" int tsg_row_flops(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int
 }
 
 extern "C" int tsg_symbolic(tsg_ctx *c, const tsg_csr *a, const tsg_cmat *cb, tsg_vec **counts) {
+    TSG_RESOLVE(c, a);
     if (a->cols != cb->rows) {
         tsg_set_error("A has %lld cols but compressed B has %lld rows", (long long)a->cols,
                       (long long)cb->rows);
@@ -2589,6 +2710,8 @@ extern "C" int tsg_symbolic(tsg_ctx *c, const tsg_csr *a, const tsg_cmat *cb, ts
 
 extern "C" int tsg_numeric(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, const tsg_cmat *cb,
                            const tsg_vec *counts, tsg_csr **out) {
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, b);
     if (a->cols != b->rows) {
         tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
                       (long long)b->rows);
@@ -2613,7 +2736,42 @@ extern "C" int tsg_numeric(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, const
     return s;
 }
 
+// Host bounds for a device-driven multiply (see tsg_multiply): per-row set
+// and entry bounds from the operands' known row lengths decide which bins can
+// be non-empty; anything that could need the CTA, global or dense tiers (or a
+// pool sized from device data) takes the read-back path.
+static void plan_device_bins(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b) {
+    c->nowait = 0;
+    if (c->c_host_out || getenv("TSG_NO_DEVICE_BINS")) return;
+    const int64_t amax = a->max_row >= 0 ? a->max_row : (a->max_row_bound > 0 ? a->max_row_bound : -1);
+    const int64_t bmax = b->max_row;
+    if (amax <= 0 || bmax <= 0 || a->rows <= 0 || b->rows <= 0) return;
+    const int64_t sbmax = amax * bmax;              // sets per row <= entries of its B rows
+    const int64_t nmax = std::min<int64_t>(sbmax, b->cols);
+    if (sbmax >= DENSE_MIN_SETS || sym_bin(sbmax) >= 7 || num_bin(nmax, nmax) >= 7) return;
+    const int64_t anz = a->nnz;                     // a bound when `a` is itself lazy
+    const int64_t bound = anz * bmax;
+    const int64_t nnz_bound = std::min<int64_t>(bound, a->rows * b->cols);
+    if (12 * (bound + nnz_bound) > ((int64_t)12 << 30)) return;
+    uint32_t sym = 0, num = 0;
+    for (int k = 0; k <= sym_bin(sbmax); ++k) sym |= 1u << k;
+    for (int k = 0; k <= num_bin(nmax, nmax); ++k) num |= 1u << k;
+    // merge tier (row-sorted B): bin m holds rows with <= mt_g(m) entries
+    // whose bound <= mt_cap(m) that no smaller m took
+    sym |= 1u << BIN_MERGE;
+    if (amax > mt_g(0) || sbmax > mt_cap(0)) sym |= 1u << (BIN_MERGE + 1);
+    if (amax > mt_g(1) || sbmax > mt_cap(1)) sym |= 1u << (BIN_MERGE + 2);
+    if (bmax <= 1) sym |= 1u << BIN_THREAD;         // unit B: thread tier
+    c->sym_possible = sym;
+    c->num_possible = num;
+    c->set_cap_bound = std::max<int64_t>(bound, 1);
+    c->nnz_bound = nnz_bound;
+    c->c_row_bound = nmax;
+    c->nowait = 1;
+}
+
 extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_csr **out) {
+    TSG_RESOLVE(c, b);
     if (a->cols != b->rows) {
         tsg_set_error("A is %lldx%lld but B has %lld rows", (long long)a->rows, (long long)a->cols,
                       (long long)b->rows);
@@ -2623,6 +2781,11 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
         tsg_set_error("numeric multiply requires values on both operands");
         return TSG_EVALID;
     }
+    // Device-driven path: when the host's row-length bounds keep every row in
+    // the group / merge / thread tiers and the bounded allocations are small,
+    // the multiply never waits for the device (no partition read-backs, C's
+    // nnz left on the device) -- back-to-back multiplies queue without gaps.
+    plan_device_bins(c, a, b);
     PhaseTimer pt(c);
     pt.mark();
     tsg_trace(c, "multiply:start", a->rows);
@@ -2638,6 +2801,7 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
     if (s == TSG_OK)
         s = tsg_numeric_impl(c, a->rows, b->cols, a, 0, 0, 0x7fffffff, b, cb, nullptr, counts, sbound,
                              out, &pt);
+    c->nowait = 0;
     pt.finish(5);
     // phase slots: [0] compress [1] symbolic [2] scan [3] numeric [5] total
     tsg_free(c, sbound);
@@ -2657,6 +2821,9 @@ extern "C" int tsg_multiply_placed(tsg_ctx *c, const tsg_csr *a, const tsg_csr *
 extern "C" int tsg_numeric_fused(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b_chunk,
                                  const tsg_csr *c_partial, int64_t a_lo, int64_t a_hi,
                                  int64_t b_lo, int64_t b_hi, tsg_csr **out) {
+    TSG_RESOLVE(c, a);
+    TSG_RESOLVE(c, b_chunk);
+    TSG_RESOLVE(c, c_partial);
     if (a_hi > a->rows || a_lo < 0 || a_lo > a_hi) {
         tsg_set_error("a_rows exceeds A's row count");
         return TSG_EDIM;
