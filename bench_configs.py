@@ -380,10 +380,126 @@ def placement(args):
 # ------------------------------------------------------------------ config 5
 
 def config5(args, dist=None):
-    """A*A on an R-MAT graph (values 1.0), row-partitioned over the ranks
-    (distributed.mg_multiply); see paper_1804_00695_b200/distributed.py."""
+    """BASELINE.json config 5: A*A on an R-MAT graph (Graph500 parameters,
+    SplitMix64 seed 22, unit values), rows partitioned over the ranks by K0
+    flops, B replicated (NCCL all-gather) or sharded in peer HBM
+    (``--b-mode``), C streamed through ``--c-budget-gib`` when it does not fit.
+    Strong scaling: the graph is fixed, every rank takes 1/N of the flops.
+    Timing: CUDA events on each rank's libtsg stream around the block
+    multiply + offset exchange, max over ranks.  Parity: every rank's sum of
+    C's values equals its multiplications exactly (unit values: C_ij counts
+    paths, so the sum over a block is its K0 flops), the global nnz is
+    all-reduced, and sampled rows (incl. the hub) match the oracle."""
+    import torch
+    from paper_1804_00695_b200 import _lib, generators as gen
     from paper_1804_00695_b200 import distributed as D
-    return D.bench_config5(args, dist)
+    from paper_1804_00695_b200.csr import CsrMatrix
+    world = dist.get_world_size() if dist else 1
+    rank = dist.get_rank() if dist else 0
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    ctx = _lib.Context.get(local)
+    ctx.set_timing(True)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    t_setup = time.perf_counter()
+    da = gen.rmat_graph_device(args.scale).set_values(1.0)
+    n = da.num_rows
+    row_flops, total = _lib.d_row_flops(da, da)
+    bounds = D.flops_partition(row_flops, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    a_blk = da.slice_rows(lo, hi)
+    mode = getattr(args, "b_mode", "replicated") if world > 1 else "local"
+    info = {}
+    t_b = time.perf_counter()
+    if world == 1:
+        db = da
+    elif mode == "sharded":
+        db, info = D.shard_b(ctx, da, dist, sorted_rows=True)
+    else:
+        sb = D.shard_bounds(np.diff(D.rp_host(ctx, da)), world)
+        shard = da.slice_rows(int(sb[rank]), int(sb[rank + 1]))
+        db = D.replicate_b(ctx, shard, n, n, dist)
+        del shard
+    b_setup_s = time.perf_counter() - t_b
+    host_a = da.download() if rank == 0 or not getattr(args, "no_parity", False) else None
+    if world > 1:
+        del da
+    budget = int(getattr(args, "c_budget_gib", 48.0) * 2**30)
+    mults = int(row_flops[lo:hi].sum())
+    est_c_bytes = 12 * mults   # nnz(C) <= multiplications
+    c_budget = budget if est_c_bytes > budget else 0
+    setup_s = time.perf_counter() - t_setup
+
+    def step():
+        ctx.record(0)
+        _, st = D.mg_multiply(a_blk, db, c_budget, keep_c=False)
+        if dist:
+            with torch.cuda.stream(stream):
+                off, tot = D.exchange_offsets(st["nnz"], dist)
+        else:
+            off, tot = 0, st["nnz"]
+        ctx.record(1)
+        return st, off, tot
+
+    for _ in range(max(1, args.warmup)):
+        st, off, tot = step()
+    if dist:
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        st, off, tot = step()
+        times.append(ctx.elapsed_ms(0, 1))
+    my_ms = statistics.median(times)
+    ms = my_ms
+    flops_all = 2 * total
+    sums_ok = bool(st["value_sum"] == float(mults))
+    if dist:
+        dev = D._coll_device(dist)
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        ok = torch.tensor([1.0 if sums_ok else 0.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        sums_ok = bool(ok.item() > 0.5)
+    # sampled rows of this block (incl. its largest-flops row) against the oracle
+    par = {"block_value_sum_equals_mults": sums_ok, "nnz_C": tot}
+    if not getattr(args, "no_parity", False):
+        from oracle import oracle as O
+        cb = O.compress(host_a)
+        rng = np.random.default_rng(rank)
+        rows = sorted(set([lo + int(np.argmax(row_flops[lo:hi]))] +
+                          [int(x) for x in rng.integers(lo, hi, size=min(6, hi - lo))])) if hi > lo else []
+        exact = ok = True
+        for r in rows:
+            sub = CsrMatrix._adopt(1, n, np.array([0, host_a.row_ptr[r + 1] - host_a.row_ptr[r]]),
+                                   host_a.col_idx[host_a.row_ptr[r]:host_a.row_ptr[r + 1]],
+                                   host_a.values[host_a.row_ptr[r]:host_a.row_ptr[r + 1]])
+            want = O.numeric(sub, host_a, O.symbolic(sub, cb))
+            c1, _ = D.mg_multiply(a_blk.slice_rows(r - lo, r - lo + 1), db, 0, keep_c=True)
+            res = compare_products(c1.download(), want)
+            exact &= res["exact"]
+            ok &= res["ok"]
+        if dist:
+            dev = D._coll_device(dist)
+            t = torch.tensor([1.0 if ok else 0.0, 1.0 if exact else 0.0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok, exact = bool(t[0].item() > 0.5), bool(t[1].item() > 0.5)
+        par.update(sampled_rows_ok=ok, sampled_rows_exact=exact, rows_per_rank=len(rows))
+    par["ok"] = bool(sums_ok and par.get("sampled_rows_ok", True))
+    line = {"metric": "SpGEMM GFLOP/s config 5 (A*A R-MAT scale %d, %d GPU, B %s)" % (args.scale, world, mode),
+            "value": flops_all / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+            "ms_per_step": ms, "steps": args.steps, "warmup": args.warmup, "scaling": "strong",
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5 A*A R-MAT scale %d ef16 (.57,.19,.19,.05) SplitMix64 seed 22"
+                                   % args.scale, "n": n, "multiplications": total,
+                       "b_mode": mode, "partition": "K0 flops, contiguous row blocks",
+                       "c_mode": "streamed (budget %d GiB per GPU)" % (budget >> 30) if c_budget else
+                                 "materialised per GPU", "rank0_block_rows": hi - lo},
+            "per_rank": {"ms": my_ms, "blocks": st["blocks"], "max_block_nnz": st["max_block_nnz"],
+                         "mults": mults},
+            "setup": {"total_s": setup_s, "b_setup_s": b_setup_s, **info},
+            "parity": par}
+    return line
 
 
 # ------------------------------------------------------------------ driver hooks
