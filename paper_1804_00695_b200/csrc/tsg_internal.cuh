@@ -51,6 +51,11 @@ struct tsg_ctx {
     int nowait;
     uint32_t sym_possible, num_possible;
     int64_t set_cap_bound, nnz_bound, c_row_bound;
+    // bin-size hints of this operand shape (pinned, device-mapped; written by
+    // the partitions of the previous multiply of the same shape, read by the
+    // host only to order launches and size grids)
+    int64_t *hint_sym, *hint_num;     // host views (nullptr: none)
+    int64_t *hintd_sym, *hintd_num;   // device aliases
     cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
     cudaStream_t widen;       // int32 -> int64 widening of drained C ranges (own stream, so a
                               // narrow for an H2D piece never queues behind a C drain)

@@ -30,6 +30,7 @@ struct BinLists {
     bool device = false;
     int64_t rows = 0;
     uint32_t possible = 0xffffffffu;   // device mode: bins the host's bounds allow
+    int64_t hint[NB + 1] = {0};        // device mode: bin starts of the last same-shape call
 };
 
 // tile counts up to this many are scanned by the last k_part_bins block
@@ -161,7 +162,7 @@ struct NoMid {
 template <int NB, class F, class Mid = NoMid>
 int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &out,
                   const int64_t *extra = nullptr, int64_t *extra_out = nullptr, Mid mid = Mid(),
-                  bool nowait = false) {
+                  bool nowait = false, int64_t *hint_host = nullptr, int64_t *hint_dev = nullptr) {
     static_assert(32 + NB + 2 <= 61, "partition results overlap the sequence / error slots");
     int ntiles = (int)((rows + PART_TILE - 1) / PART_TILE);
     if (ntiles < 1) ntiles = 1;
@@ -180,12 +181,15 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     // copy that would queue behind bulk transfers on the copy engine
     if (nowait) {
         // device-driven: the bin kernels read their ranges from dstart; the
-        // host learns nothing and waits for nothing
+        // host waits for nothing.  The starts also land in this shape's hint
+        // buffer (read by the host at the next same-shape call, never now)
         TSG_TRY(tsg_alloc_t(c, &out.dstart, NB + 1));
         out.device = true;
         out.rows = rows;
+        if (hint_host)
+            for (int b = 0; b <= NB; b++) out.hint[b] = hint_host[b];
         TSG_CK(launch_pdl(k_part_scatter<NB>, ntiles, 256, 0, c->stream, rows, (const uint8_t *)bins, ntiles,
-                          (const int64_t *)offs, out.list, extra, (const int *)c->d_err, (int64_t *)nullptr,
+                          (const int64_t *)offs, out.list, extra, (const int *)c->d_err, hint_dev,
                           (int64_t)0, out.dstart));
         ++c->launches;
         TSG_CK(cudaGetLastError());
@@ -207,5 +211,7 @@ int tsg_partition(tsg_ctx *c, int64_t rows, F f, uint8_t *bins, BinLists<NB> &ou
     TSG_TRY(tsg_pending_errors(c));
     for (int b = 0; b <= NB; b++) out.off[b] = c->h_small[32 + b];
     if (extra_out) *extra_out = c->h_small[32 + NB + 1];
+    if (hint_host)
+        for (int b = 0; b <= NB; b++) hint_host[b] = out.off[b];
     return TSG_OK;
 }

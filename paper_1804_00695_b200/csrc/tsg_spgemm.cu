@@ -28,6 +28,7 @@
 #include <vector>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 #include "tsg_group.cuh"
 #include <functional>
@@ -1842,8 +1843,13 @@ bool bin_select(const Bins &bl, int B, Args &a, const int32_t *&list, int64_t &n
         a.dbins = bl.dstart;
         a.bin = B;
         list = bl.list;
-        n = bl.rows;
-        return n > 0;
+        // grid from the last same-shape call's bin size (a hint: the kernel
+        // covers whatever the device partition holds); a bin that was empty
+        // gets a token grid, which stays correct -- only slower -- if the
+        // structure changed under the same shape
+        const int64_t h = bl.hint[B + 1] - bl.hint[B];
+        n = h > 0 && h <= bl.rows ? h : 1;
+        return bl.rows > 0;
     }
     n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return false;
@@ -1854,9 +1860,8 @@ bool bin_select(const Bins &bl, int B, Args &a, const int32_t *&list, int64_t &n
 
 template <class K>
 unsigned bin_grid(tsg_ctx *c, const Bins &bl, unsigned grid, K kernel, int bs, size_t smem) {
-    if (!bl.device) return grid;
-    const unsigned r = resident_grid(c, kernel, bs, smem);
-    return grid < r ? grid : r;
+    (void)c; (void)bl; (void)kernel; (void)bs; (void)smem;
+    return grid;
 }
 
 // global-tier slab sizing: T slots per CTA, bounded by a memory budget
@@ -2143,7 +2148,9 @@ int run_bins_largest_first(tsg_ctx *c, BinJob *jobs, int njobs) {
 
 int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     auto cnt = [&](int b) -> int64_t {
-        return bl.device ? (int64_t)((bl.possible >> b) & 1u) : bl.off[b + 1] - bl.off[b];
+        if (!bl.device) return bl.off[b + 1] - bl.off[b];
+        if (!((bl.possible >> b) & 1u)) return 0;
+        return 1 + (bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0);   // largest first
     };
     BinJob jobs[] = {
         {cnt(BIN_THREAD), [&] { return launch_sym_thread(c, bl, a); }},
@@ -2167,7 +2174,9 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
 
 int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     auto cnt = [&](int b) -> int64_t {
-        return bl.device ? (int64_t)((bl.possible >> b) & 1u) : bl.off[b + 1] - bl.off[b];
+        if (!bl.device) return bl.off[b + 1] - bl.off[b];
+        if (!((bl.possible >> b) & 1u)) return 0;
+        return 1 + (bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0);   // largest first
     };
     BinJob jobs[] = {
         {cnt(0), [&] { return launch_num_group<0>(c, bl, a); }},
@@ -2287,7 +2296,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
                                      bins, bl,
                                      v->sptr + rows_out, &set_cap,
                                      [&]() { return tsg_exclusive_scan_i64(c, scap, v->sptr, rows_out); },
-                                     c->nowait != 0));
+                                     c->nowait != 0, c->hint_sym, c->hintd_sym));
         if (bl.device) {   // device-driven: host bounds instead of read-back sizes
             bl.possible = c->sym_possible;
             set_cap = c->set_cap_bound;
@@ -2389,7 +2398,7 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
     int64_t nnz = 0;
     if (rows_out > 0) {
         TSG_TRY(tsg_partition<NBINS>(c, rows_out, NumBinF{counts->d, counts->aux, sbound_in, cb->sorted_sets ? b->cols : 0}, bins, bl,
-                                     cptr + rows_out, &nnz, NoMid(), c->nowait != 0));
+                                     cptr + rows_out, &nnz, NoMid(), c->nowait != 0, c->hint_num, c->hintd_num));
         if (bl.device) {
             bl.possible = c->num_possible;
             nnz = c->nnz_bound;   // capacity; the exact count stays on the device
@@ -2408,10 +2417,10 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         C->rows = rows_out;
         C->cols = cols_out;
         C->nnz = nnz;
+        C->max_row_bound = c->c_row_bound;   // 0 unless tsg_multiply planned bounds
         if (bl.device) {
             C->lazy_nnz = 1;
             C->owner = c;
-            C->max_row_bound = c->c_row_bound;
         }
         C->rp = cptr;
         C->col = nullptr;
@@ -2740,8 +2749,41 @@ extern "C" int tsg_numeric(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, const
 // and entry bounds from the operands' known row lengths decide which bins can
 // be non-empty; anything that could need the CTA, global or dense tiers (or a
 // pool sized from device data) takes the read-back path.
+struct HintKey {
+    const tsg_ctx *c;
+    int64_t ar, ac, an, br, bc, bn;
+    bool operator<(const HintKey &o) const {
+        return std::tie(c, ar, ac, an, br, bc, bn) < std::tie(o.c, o.ar, o.ac, o.an, o.br, o.bc, o.bn);
+    }
+};
+struct HintBufs {
+    int64_t *h = nullptr, *d = nullptr;   // 64 int64: [0, 32) symbolic, [32, 64) numeric
+};
+static std::mutex g_hint_mu;
+static std::map<HintKey, HintBufs> g_hints;
+
+// pinned, mapped bin-start buffers of an operand shape (slot 31 of each half
+// = 1 once a read-back multiply has recorded the starts)
+static HintBufs *hint_bufs(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b) {
+    std::lock_guard<std::mutex> g(g_hint_mu);
+    const HintKey k{c, a->rows, a->cols, a->nnz, b->rows, b->cols, b->nnz};
+    auto it = g_hints.find(k);
+    if (it != g_hints.end()) return &it->second;
+    if (g_hints.size() >= 256) return nullptr;
+    HintBufs hb;
+    if (cudaHostAlloc(&hb.h, 64 * sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&hb.d, hb.h, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    memset(hb.h, 0, 64 * sizeof(int64_t));
+    return &(g_hints[k] = hb);
+}
+
 static void plan_device_bins(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b) {
     c->nowait = 0;
+    c->c_row_bound = 0;
+    c->hint_sym = c->hint_num = c->hintd_sym = c->hintd_num = nullptr;
     if (c->c_host_out || getenv("TSG_NO_DEVICE_BINS")) return;
     const int64_t amax = a->max_row >= 0 ? a->max_row : (a->max_row_bound > 0 ? a->max_row_bound : -1);
     const int64_t bmax = b->max_row;
@@ -2767,7 +2809,19 @@ static void plan_device_bins(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b) {
     c->set_cap_bound = std::max<int64_t>(bound, 1);
     c->nnz_bound = nnz_bound;
     c->c_row_bound = nmax;
-    c->nowait = 1;
+    // the first multiply of a shape reads its bin sizes back (and records
+    // them); later ones run device-driven with those sizes as launch hints
+    HintBufs *hb = hint_bufs(c, a, b);
+    if (!hb) return;
+    c->hint_sym = hb->h;
+    c->hintd_sym = hb->d;
+    c->hint_num = hb->h + 32;
+    c->hintd_num = hb->d + 32;
+    if (hb->h[31] == 1 && hb->h[63] == 1) {
+        c->nowait = 1;
+    } else {
+        hb->h[31] = hb->h[63] = 1;   // the read-back partitions below fill the starts
+    }
 }
 
 extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_csr **out) {
@@ -2802,6 +2856,8 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
         s = tsg_numeric_impl(c, a->rows, b->cols, a, 0, 0, 0x7fffffff, b, cb, nullptr, counts, sbound,
                              out, &pt);
     c->nowait = 0;
+    c->c_row_bound = 0;
+    c->hint_sym = c->hint_num = c->hintd_sym = c->hintd_num = nullptr;
     pt.finish(5);
     // phase slots: [0] compress [1] symbolic [2] scan [3] numeric [5] total
     tsg_free(c, sbound);
