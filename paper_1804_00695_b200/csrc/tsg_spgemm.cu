@@ -63,16 +63,41 @@ struct SymArgs {
     // device-driven bins (no host read-back): the launch covers bin `bin`
     // whose rows are list[dbins[bin] .. dbins[bin + 1]) (see bin_range)
     const int64_t *dbins;
-    int bin;
+    int bin;             // -1: leftover launch over every bin in binmask
+    uint32_t binmask;
 };
 
 constexpr int SETS_WRITTEN = 1 << 30;
 
+// pass `pass` of a kernel's bin loop: (list, n) of the pass-th bin of a
+// leftover launch's mask; false when the mask is exhausted.  A normal launch
+// has exactly one pass over its own (list, nlist).
+template <class Args, class P>
+__device__ __forceinline__ bool leftover_range(const Args &a, int pass, P base, int64_t nbase, P &lst,
+                                               int64_t &n) {
+    if (!(a.dbins && a.bin < 0)) {
+        lst = base;
+        n = nbase;
+        return pass == 0;
+    }
+    uint32_t m = a.binmask;
+    for (int k = 0; k < pass && m; ++k) m &= m - 1;
+    if (!m) return false;
+    const int b = __ffs(m) - 1;
+    lst = base + a.dbins[b];
+    n = a.dbins[b + 1] - a.dbins[b];
+    return true;
+}
+
 // A bin kernel launched without the host knowing the bin's size takes its
-// row range from the partition's device-side bin starts.
+// row range from the partition's device-side bin starts.  A "leftover"
+// launch (bin = -1) of the most general group kernel walks every bin in
+// binmask in turn: the bins the last same-shape call left empty, so they need
+// no launch of their own (leftover_range / the loops of k_sym_group and
+// k_num_group).
 template <class Args, class P>
 __device__ __forceinline__ void bin_range(const Args &a, P &list, int64_t &nlist) {
-    if (a.dbins) {
+    if (a.dbins && a.bin >= 0) {
         const int64_t b0 = a.dbins[a.bin];
         nlist = a.dbins[a.bin + 1] - b0;
         list += b0;
@@ -118,6 +143,7 @@ struct NumArgs {
     int unit_dense;      // B row k is entry k (every row exactly one entry): no row_ptr gather
     const int64_t *dbins;   // device-driven bins, as in SymArgs
     int bin;
+    uint32_t binmask;
 };
 
 __device__ __forceinline__ void partial_range(const NumArgs &a, int64_t i, int64_t &p0, int64_t &p1) {
@@ -374,9 +400,13 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
     const int glane = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     int4 *tbl = reinterpret_cast<int4 *>(reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE);
-    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
+    for (int pass_ = 0;; ++pass_) {
+    const int32_t *lst_;
+    int64_t nl_;
+    if (!leftover_range(a, pass_, list, nlist, lst_, nl_)) break;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nl_;
          li += (int64_t)gridDim.x * gpb) {
-        const int64_t i = list[li];
+        const int64_t i = lst_[li];
         const int64_t gi = i + a.a_row_off;
         int T = table_slots(a.sbound[i]);
         if (T > TMAX) T = 1 << ilog2_pow2(TMAX);
@@ -524,6 +554,7 @@ __global__ void __launch_bounds__(256) k_sym_group(const int32_t *__restrict__ l
             if (a.msets) a.msets[i] = m | (emit ? SETS_WRITTEN : 0);
         }
         __syncwarp(gm);
+    }
     }
 }
 
@@ -1298,9 +1329,13 @@ __global__ void __launch_bounds__(num_bs<G, MODE>(), num_minb<G, MODE>()) k_num_
     // groups 64 B = 16 banks after their even partner; 4-lane: 32 B steps)
     char *slice = reinterpret_cast<char *>(smem) + (size_t)(threadIdx.x / G) * SLICE +
                   (G <= 8 ? (size_t)(threadIdx.x / G) * 8 * G : 0);
-    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nlist;
+    for (int pass_ = 0;; ++pass_) {
+    const int32_t *lst_;
+    int64_t nl_;
+    if (!leftover_range(a, pass_, list, nlist, lst_, nl_)) break;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + threadIdx.x / G; li < nl_;
          li += (int64_t)gridDim.x * gpb) {
-        const NumRowHdr h = num_row_hdr(a, list[li]);
+        const NumRowHdr h = num_row_hdr(a, lst_[li]);
         const int64_t i = h.i;
         const int64_t gi = i + a.a_row_off;
         const int n = h.n;
@@ -1507,6 +1542,7 @@ __global__ void __launch_bounds__(num_bs<G, MODE>(), num_minb<G, MODE>()) k_num_
         for (int q = glane; q < rowlen; q += G) a.cval[cp + q] = vals[q];
         if (cap_mode && glane == 0) a.plen_out[i] = rowlen;
         __syncwarp(gm);
+    }
     }
 }
 
@@ -1840,16 +1876,16 @@ template <class Args>
 bool bin_select(const Bins &bl, int B, Args &a, const int32_t *&list, int64_t &n) {
     if (bl.device) {
         if (!((bl.possible >> B) & 1u)) return false;
+        // only bins the last same-shape call filled get their own launch,
+        // sized by that call's count (a hint: the kernel covers whatever the
+        // device partition holds); the others go to the leftover launch
+        const int64_t h = bl.hint[B + 1] - bl.hint[B];
+        if (h <= 0) return false;
         a.dbins = bl.dstart;
         a.bin = B;
         list = bl.list;
-        // grid from the last same-shape call's bin size (a hint: the kernel
-        // covers whatever the device partition holds); a bin that was empty
-        // gets a token grid, which stays correct -- only slower -- if the
-        // structure changed under the same shape
-        const int64_t h = bl.hint[B + 1] - bl.hint[B];
-        n = h > 0 && h <= bl.rows ? h : 1;
-        return bl.rows > 0;
+        n = h < bl.rows ? h : bl.rows;
+        return true;
     }
     n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return false;
@@ -1903,7 +1939,9 @@ int launch_num_group_m(tsg_ctx *c, const Bins &bl, const NumArgs &a0) {
 
 template <int B>
 int launch_num_group(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
-    if (bl.device ? !((bl.possible >> B) & 1u) : bl.off[B + 1] - bl.off[B] <= 0) return TSG_OK;
+    if (bl.device ? !((bl.possible >> B) & 1u) || bl.hint[B + 1] - bl.hint[B] <= 0
+                  : bl.off[B + 1] - bl.off[B] <= 0)
+        return TSG_OK;
     // lane-per-B-entry mode pays off once B rows fill at least half a group
     if (a.seq >= gt_g(B) / 2) return launch_num_group_m<B, 1>(c, bl, a);
     if (a.unit_known > 0) return launch_num_group_m<B, 2>(c, bl, a);
@@ -2135,6 +2173,56 @@ struct BinJob {
     std::function<int()> launch;
 };
 
+// Device-driven mode: every possible bin the hint left empty, in one launch
+// of the most general group kernel (bin 6: any row of the group / merge /
+// thread tiers fits its slice), one CTA per SM.
+uint32_t leftover_mask(const Bins &bl) {
+    uint32_t m = 0;
+    for (int b = 0; b < NBINS; ++b)
+        if (((bl.possible >> b) & 1u) && bl.hint[b + 1] - bl.hint[b] <= 0) m |= 1u << b;
+    return m;
+}
+
+int launch_sym_leftover(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
+    if (!bl.device) return TSG_OK;
+    const uint32_t m = leftover_mask(bl);
+    if (!m) return TSG_OK;
+    constexpr int G = gt_g_sym(6), SL = gt_slice(6), BS = gt_block(6);
+    SymArgs a = a0;
+    a.dbins = bl.dstart;
+    a.bin = -1;
+    a.binmask = m;
+    const size_t smem = (size_t)(BS / G) * SL;
+    TSG_TRY(set_smem(k_sym_group<G, SL>, smem));
+    k_sym_group<G, SL><<<c->num_sms, BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_group(leftover)", 6, c->num_sms, BS, smem));
+    return TSG_OK;
+}
+
+template <int MODE>
+int launch_num_leftover_m(tsg_ctx *c, const Bins &bl, const NumArgs &a0, uint32_t m) {
+    constexpr int G = gt_g(6), SL = gt_slice(6);
+    constexpr int BS = num_bs<G, MODE>() < gt_block(6) ? num_bs<G, MODE>() : gt_block(6);
+    NumArgs a = a0;
+    a.dbins = bl.dstart;
+    a.bin = -1;
+    a.binmask = m;
+    const size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * ustage_bytes<G>() : 0);
+    TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
+    k_num_group<G, SL, MODE><<<c->num_sms, BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_num_group(leftover)", 6, c->num_sms, BS, smem));
+    return TSG_OK;
+}
+
+int launch_num_leftover(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
+    if (!bl.device) return TSG_OK;
+    const uint32_t m = leftover_mask(bl);
+    if (!m) return TSG_OK;
+    if (a.seq >= gt_g(6) / 2) return launch_num_leftover_m<1>(c, bl, a, m);
+    if (a.unit_known > 0) return launch_num_leftover_m<2>(c, bl, a, m);
+    return launch_num_leftover_m<0>(c, bl, a, m);
+}
+
 int run_bins_largest_first(tsg_ctx *c, BinJob *jobs, int njobs) {
     std::stable_sort(jobs, jobs + njobs, [](const BinJob &x, const BinJob &y) { return x.n > y.n; });
     BinFork f(c);
@@ -2150,7 +2238,7 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     auto cnt = [&](int b) -> int64_t {
         if (!bl.device) return bl.off[b + 1] - bl.off[b];
         if (!((bl.possible >> b) & 1u)) return 0;
-        return 1 + (bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0);   // largest first
+        return bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0;   // largest first
     };
     BinJob jobs[] = {
         {cnt(BIN_THREAD), [&] { return launch_sym_thread(c, bl, a); }},
@@ -2164,6 +2252,7 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
         {cnt(4), [&] { return launch_sym_group<4>(c, bl, a); }},
         {cnt(5), [&] { return launch_sym_group<5>(c, bl, a); }},
         {cnt(6), [&] { return launch_sym_group<6>(c, bl, a); }},
+        {bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_sym_leftover(c, bl, a); }},
     };
     TSG_TRY(run_bins_largest_first(c, jobs, (int)(sizeof(jobs) / sizeof(jobs[0]))));
     TSG_TRY(launch_sym_cta<0>(c, bl, a));
@@ -2176,7 +2265,7 @@ int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     auto cnt = [&](int b) -> int64_t {
         if (!bl.device) return bl.off[b + 1] - bl.off[b];
         if (!((bl.possible >> b) & 1u)) return 0;
-        return 1 + (bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0);   // largest first
+        return bl.hint[b + 1] - bl.hint[b] > 0 ? bl.hint[b + 1] - bl.hint[b] : 0;   // largest first
     };
     BinJob jobs[] = {
         {cnt(0), [&] { return launch_num_group<0>(c, bl, a); }},
@@ -2186,6 +2275,7 @@ int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
         {cnt(4), [&] { return launch_num_group<4>(c, bl, a); }},
         {cnt(5), [&] { return launch_num_group<5>(c, bl, a); }},
         {cnt(6), [&] { return launch_num_group<6>(c, bl, a); }},
+        {bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_num_leftover(c, bl, a); }},
     };
     TSG_TRY(run_bins_largest_first(c, jobs, (int)(sizeof(jobs) / sizeof(jobs[0]))));
     TSG_TRY(launch_num_cta<0>(c, bl, a));
