@@ -2175,7 +2175,18 @@ struct BinJob {
 
 // Device-driven mode: every possible bin the hint left empty, in one launch
 // of the most general group kernel (bin 6: any row of the group / merge /
-// thread tiers fits its slice), one CTA per SM.
+// thread tiers fits its slice).  Its grid is small: the bins are expected
+// empty, and blocks of a 64 KB-slice kernel waiting for shared memory next
+// to the big bin's blocks would hold back that bin (measured: a full-width
+// leftover slowed config 2's RA*P bins by 15-20 %).
+static unsigned leftover_grid() {
+    static const unsigned g = [] {
+        const char *e = getenv("TSG_LEFTOVER_GRID");
+        const int v = e ? atoi(e) : 16;
+        return (unsigned)(v > 0 ? v : 16);
+    }();
+    return g;
+}
 uint32_t leftover_mask(const Bins &bl) {
     uint32_t m = 0;
     for (int b = 0; b < NBINS; ++b)
@@ -2194,8 +2205,8 @@ int launch_sym_leftover(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
     a.binmask = m;
     const size_t smem = (size_t)(BS / G) * SL;
     TSG_TRY(set_smem(k_sym_group<G, SL>, smem));
-    k_sym_group<G, SL><<<c->num_sms, BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
-    TSG_TRY(tsg_launch_check("k_sym_group(leftover)", 6, c->num_sms, BS, smem));
+    k_sym_group<G, SL><<<leftover_grid(), BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_group(leftover)", 6, leftover_grid(), BS, smem));
     return TSG_OK;
 }
 
@@ -2209,8 +2220,8 @@ int launch_num_leftover_m(tsg_ctx *c, const Bins &bl, const NumArgs &a0, uint32_
     a.binmask = m;
     const size_t smem = num_slices_bytes<G, SL>(BS / G) + (MODE == 2 ? (size_t)(BS / G) * ustage_bytes<G>() : 0);
     TSG_TRY(set_smem(k_num_group<G, SL, MODE>, smem));
-    k_num_group<G, SL, MODE><<<c->num_sms, BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
-    TSG_TRY(tsg_launch_check("k_num_group(leftover)", 6, c->num_sms, BS, smem));
+    k_num_group<G, SL, MODE><<<leftover_grid(), BS, smem, c->stream>>>(bl.list, 0, a); ++c->launches;
+    TSG_TRY(tsg_launch_check("k_num_group(leftover)", 6, leftover_grid(), BS, smem));
     return TSG_OK;
 }
 
@@ -2221,6 +2232,11 @@ int launch_num_leftover(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     if (a.seq >= gt_g(6) / 2) return launch_num_leftover_m<1>(c, bl, a, m);
     if (a.unit_known > 0) return launch_num_leftover_m<2>(c, bl, a, m);
     return launch_num_leftover_m<0>(c, bl, a, m);
+}
+
+static bool leftover_concurrent() {
+    static const bool v = getenv("TSG_LEFTOVER_CONCURRENT") != nullptr;
+    return v;
 }
 
 int run_bins_largest_first(tsg_ctx *c, BinJob *jobs, int njobs) {
@@ -2252,8 +2268,12 @@ int run_symbolic_bins(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
         {cnt(4), [&] { return launch_sym_group<4>(c, bl, a); }},
         {cnt(5), [&] { return launch_sym_group<5>(c, bl, a); }},
         {cnt(6), [&] { return launch_sym_group<6>(c, bl, a); }},
-        {bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_sym_leftover(c, bl, a); }},
+        {leftover_concurrent() && bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_sym_leftover(c, bl, a); }},
     };
+    // the leftover launch (bins the hint left empty) goes first and alone on
+    // the compute stream: a few us, and no 64 KB-slice blocks waiting for
+    // shared memory beside the big bins
+    if (!leftover_concurrent()) TSG_TRY(launch_sym_leftover(c, bl, a));
     TSG_TRY(run_bins_largest_first(c, jobs, (int)(sizeof(jobs) / sizeof(jobs[0]))));
     TSG_TRY(launch_sym_cta<0>(c, bl, a));
     TSG_TRY(launch_sym_cta<1>(c, bl, a));
@@ -2275,8 +2295,12 @@ int run_numeric_bins(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
         {cnt(4), [&] { return launch_num_group<4>(c, bl, a); }},
         {cnt(5), [&] { return launch_num_group<5>(c, bl, a); }},
         {cnt(6), [&] { return launch_num_group<6>(c, bl, a); }},
-        {bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_num_leftover(c, bl, a); }},
+        {leftover_concurrent() && bl.device && leftover_mask(bl) ? 1 : 0, [&] { return launch_num_leftover(c, bl, a); }},
     };
+    // the leftover launch (bins the hint left empty) goes first and alone on
+    // the compute stream: a few us, and no 64 KB-slice blocks waiting for
+    // shared memory beside the big bins
+    if (!leftover_concurrent()) TSG_TRY(launch_num_leftover(c, bl, a));
     TSG_TRY(run_bins_largest_first(c, jobs, (int)(sizeof(jobs) / sizeof(jobs[0]))));
     TSG_TRY(launch_num_cta<0>(c, bl, a));
     TSG_TRY(launch_num_cta<1>(c, bl, a));
