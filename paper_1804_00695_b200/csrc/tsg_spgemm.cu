@@ -2898,7 +2898,13 @@ static void plan_device_bins(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b) {
     c->nowait = 0;
     c->c_row_bound = 0;
     c->hint_sym = c->hint_num = c->hintd_sym = c->hintd_num = nullptr;
-    if (c->c_host_out || getenv("TSG_NO_DEVICE_BINS")) return;
+    // opt-in (TSG_DEVICE_BINS=1): measured on config 2 the removed host
+    // round trips (~25 us of idle per step) were outweighed by slower bin
+    // kernels (the device-side range prologue per block, the extra leftover
+    // launch): 1.197 ms per step read-back vs 1.212-1.220 device-driven;
+    // config 1 0.176 vs 0.181 ms
+    static const bool enabled = getenv("TSG_DEVICE_BINS") && !getenv("TSG_NO_DEVICE_BINS");
+    if (c->c_host_out || !enabled) return;
     const int64_t amax = a->max_row >= 0 ? a->max_row : (a->max_row_bound > 0 ? a->max_row_bound : -1);
     const int64_t bmax = b->max_row;
     if (amax <= 0 || bmax <= 0 || a->rows <= 0 || b->rows <= 0) return;
