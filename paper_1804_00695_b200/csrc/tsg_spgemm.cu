@@ -795,6 +795,95 @@ __global__ void __launch_bounds__(256) k_sym_merge2(const int32_t *__restrict__ 
     }
 }
 
+// Merge tier without shared memory: each lane keeps its K list heads AND the
+// next entry of each list in registers (the next-next entry is loaded as a
+// head advances, one iteration ahead of its use), so no staging, no shared
+// memory bank conflicts and no shared-memory occupancy cap.  Lists are short
+// (compressed rows of a stencil: ~9 pairs), contiguous, and L1-resident after
+// their first sector.
+template <int G, int K>
+__global__ void __launch_bounds__(256) k_sym_merge3(const int32_t *__restrict__ list, int64_t nlist,
+                                                    SymArgs a) {
+    bin_range(a, list, nlist);
+    const unsigned gm = group_mask<G>();
+    const int glane = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    const int g = threadIdx.x / G;
+    for (int64_t li = (int64_t)blockIdx.x * gpb + g; li < nlist; li += (int64_t)gridDim.x * gpb) {
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+        int64_t p[K], e[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            p[u] = 0;
+            e[u] = 0;
+            const int64_t t = a0 + glane + u * G;
+            if (t < a1) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    p[u] = a.cbstart[k];
+                    e[u] = p[u] + a.cbcnt[k];
+                }
+            }
+        }
+        int h[K], hn[K];
+        uint64_t mk[K], mkn[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const bool v0 = p[u] < e[u], v1 = p[u] + 1 < e[u];
+            h[u] = v0 ? __ldg(a.cbset + p[u]) : INT32_MAX;
+            mk[u] = v0 ? __ldg(a.cbbits + p[u]) : 0ull;
+            hn[u] = v1 ? __ldg(a.cbset + p[u] + 1) : INT32_MAX;
+            mkn[u] = v1 ? __ldg(a.cbbits + p[u] + 1) : 0ull;
+        }
+        const int64_t sp = a.sptr[i];
+        int m = 0, total = 0;
+        for (;;) {
+            int mn = h[0];
+#pragma unroll
+            for (int u = 1; u < K; ++u) mn = min(mn, h[u]);
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) mn = min(mn, __shfl_xor_sync(gm, mn, d, G));
+            if (mn == INT32_MAX) break;
+            uint64_t hm = 0ull;
+#pragma unroll
+            for (int u = 0; u < K; ++u) hm |= h[u] == mn ? mk[u] : 0ull;
+            unsigned lo = (unsigned)hm, hi = (unsigned)(hm >> 32);
+#pragma unroll
+            for (int d = G / 2; d >= 1; d >>= 1) {
+                lo |= __shfl_xor_sync(gm, lo, d, G);
+                hi |= __shfl_xor_sync(gm, hi, d, G);
+            }
+            if (glane == 0) {
+                a.oset[sp + m] = mn;
+                a.obits[sp + m] = ((uint64_t)hi << 32) | lo;
+            }
+            total += __popc(lo) + __popc(hi);
+            ++m;
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                if (h[u] == mn) {
+                    ++p[u];
+                    h[u] = hn[u];
+                    mk[u] = mkn[u];
+                    const bool v1 = p[u] + 1 < e[u];
+                    hn[u] = v1 ? __ldg(a.cbset + p[u] + 1) : INT32_MAX;
+                    mkn[u] = v1 ? __ldg(a.cbbits + p[u] + 1) : 0ull;
+                }
+            }
+        }
+        if (glane == 0) {
+            a.counts[i] = total;
+            if (a.msets) a.msets[i] = m | SETS_WRITTEN;
+        }
+    }
+}
+
+#ifndef MERGE_IMPL
+#define MERGE_IMPL 3   // 2: lists staged in shared memory (k_sym_merge2), 3: in registers (k_sym_merge3)
+#endif
 #ifndef MERGE_LISTS_PER_LANE
 #define MERGE_LISTS_PER_LANE 2
 #endif
@@ -2065,6 +2154,13 @@ int launch_sym_merge(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
     const int32_t *lst;
     int64_t n;
     if (!bin_select(bl, B, a, lst, n)) return TSG_OK;
+    if constexpr (MERGE_IMPL == 3) {
+        constexpr int K = MERGE_LISTS_PER_LANE, G2 = G / K;
+        const unsigned grid = group_grid(c, n, BS / G2);
+        k_sym_merge3<G2, K><<<grid, BS, 0, c->stream>>>(lst, n, a); ++c->launches;
+        TSG_TRY(tsg_launch_check("k_sym_merge3", B, grid, BS, 0));
+        return TSG_OK;
+    }
     if constexpr (MERGE_LISTS_PER_LANE > 1) {   // K lists per lane, G / K lanes per row
         constexpr int K = MERGE_LISTS_PER_LANE, G2 = G / K;
         const size_t smem = (size_t)(BS / G2) * SL;
