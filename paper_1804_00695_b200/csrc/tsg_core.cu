@@ -670,7 +670,11 @@ int tsg_check_kernel_errors(tsg_ctx *c, const char *phase) {
 
 namespace {
 constexpr int LB_BS = 256;
-constexpr int LB_IT = 4;   // elements per thread: 1024-element tiles, many CTAs in flight
+#ifndef TSG_LB_IT
+#define TSG_LB_IT 4
+#endif
+static_assert(TSG_LB_IT % 4 == 0, "scan tiles load 16-byte vectors");
+constexpr int LB_IT = TSG_LB_IT;   // elements per thread: 1024-element tiles, many CTAs in flight
 constexpr int LB_TILE = LB_BS * LB_IT;
 
 __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long *p) {
@@ -698,11 +702,14 @@ __device__ __forceinline__ void load_run(const TI *__restrict__ in, int64_t n, i
                 v[2 * k + 1] = q.y;
             }
         } else {
-            const int4 q = __ldg(reinterpret_cast<const int4 *>(in + base));
-            v[0] = q.x;
-            v[1] = q.y;
-            v[2] = q.z;
-            v[3] = q.w;
+#pragma unroll
+            for (int k = 0; k < LB_IT / 4; k++) {
+                const int4 q = __ldg(reinterpret_cast<const int4 *>(in + base) + k);
+                v[4 * k] = q.x;
+                v[4 * k + 1] = q.y;
+                v[4 * k + 2] = q.z;
+                v[4 * k + 3] = q.w;
+            }
         }
     } else {
 #pragma unroll
@@ -714,9 +721,13 @@ __device__ __forceinline__ void store_run(int64_t *__restrict__ out, int64_t n, 
                                           int64_t run, const int64_t (&v)[LB_IT]) {
     if (vec) {
         longlong2 *p = reinterpret_cast<longlong2 *>(out + base);
-        const int64_t r1 = run + v[0], r2 = r1 + v[1], r3 = r2 + v[2];
-        p[0] = make_longlong2(run, r1);
-        p[1] = make_longlong2(r2, r3);
+#pragma unroll
+        for (int k = 0; k < LB_IT / 2; k++) {
+            const int64_t r0 = run;
+            run += v[2 * k];
+            p[k] = make_longlong2(r0, run);
+            run += v[2 * k + 1];
+        }
     } else {
 #pragma unroll
         for (int k = 0; k < LB_IT; k++) {

@@ -17,7 +17,10 @@
 #pragma once
 #include "tsg_internal.cuh"
 
-constexpr int PART_TILE = 1024;   // rows per tile = one 256-thread block
+#ifndef TSG_PART_TILE
+#define TSG_PART_TILE 1024
+#endif
+constexpr int PART_TILE = TSG_PART_TILE;   // rows per tile = one 256-thread block
 
 template <int NB>
 struct BinLists {
