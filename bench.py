@@ -432,7 +432,7 @@ def run_config2(args, world, rank, local, dist):
     achieved = alg_ra / (num_ms * 1e-3) / 1e9
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r03_traffic.json")) as fh:
             traffic = int(json.load(fh)["traffic_bytes_per_launch"])
     except Exception:
         pass
@@ -452,7 +452,7 @@ def run_config2(args, world, rank, local, dist):
             "device_layout_bytes": dev_ra, "device_layout_frac": dev_ra / (num_ms * 1e-3) / 1e9 / hbm,
             "kernel_ms": num_ms, "whole_multiply": whole,
             "note": "traffic = dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch "
-                    "from one ncu --set full capture (profiles/r02_traffic.json)"}
+                    "from the ncu launch list of one warm step (profiles/r03_traffic.json)"}
 
     nnz = {"A": a_nnz, "R": r.nnz, "RA": ra_nnz, "RAP": rap_nnz}
     line = {
