@@ -27,7 +27,16 @@ struct MaskArgs {
 
 constexpr int MB = 10;  // bins: 0..6 group tier (slice 512 << b), 7 CTA, 8 global, 9 dense
 constexpr int MASK_DENSE = 9;
-constexpr int64_t MASK_DENSE_MIN = 2048;   // row length from which the dense bitmap wins
+#ifndef TSG_MASK_DENSE_MIN
+#define TSG_MASK_DENSE_MIN 128
+#endif
+// row length from which the dense bitmap wins (measured at R-MAT scale 22:
+// 2048 -> 140 ms, 512 -> 82, 256 -> 74, 128 -> 68, 64 -> 72 ms per count once
+// the dense tier enumerates a warp per entry)
+constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
+#ifndef DENSE_WARP_ENTRY
+#define DENSE_WARP_ENTRY 1
+#endif
 
 __device__ __forceinline__ int mask_bin(int64_t len, bool dense_ok) {
     if (len <= 0) return 255;
@@ -75,14 +84,27 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
         }
         if (!lower) kerr(a.err, KERR_NOTLOWER, i);
         __syncthreads();
-        block_enumerate<NT>(
-            r0, r1,
-            [&](int64_t t, int64_t &st, int &len) {
-                int j = a.lcol[t];
-                st = a.cstart[j];
-                len = a.ccnt[j];
-            },
-            [&](int64_t, int64_t s) { mine += __popcll(a.cbits[s] & bm[a.cset[s]]); });
+        if (DENSE_WARP_ENTRY) {
+            // a warp per entry j of the row, its lanes striding over L_j's
+            // compressed sets: coalesced loads, no per-element search (the
+            // flattened block enumeration spent ~10 shared-memory binary-search
+            // steps per compressed entry)
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            for (int64_t t = r0 + wid; t < r1; t += NT / 32) {
+                const int j = a.lcol[t];
+                const int64_t st = a.cstart[j], en = st + a.ccnt[j];
+                for (int64_t q = st + lane; q < en; q += 32) mine += __popcll(a.cbits[q] & bm[a.cset[q]]);
+            }
+        } else {
+            block_enumerate<NT>(
+                r0, r1,
+                [&](int64_t t, int64_t &st, int &len) {
+                    int j = a.lcol[t];
+                    st = a.cstart[j];
+                    len = a.ccnt[j];
+                },
+                [&](int64_t, int64_t s) { mine += __popcll(a.cbits[s] & bm[a.cset[s]]); });
+        }
         __syncthreads();
         for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) bm[a.lcol[q] >> 6] = 0ull;
         __syncthreads();
