@@ -223,6 +223,23 @@ __device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_warp) {
     return r;
 }
 
+// Block-wide enumeration with a warp per entry: warps take the entries t of
+// [a0, a1) in turn and their lanes stride over [st, st + len).  Every
+// compressed / B entry costs one coalesced load and no search (the flattened
+// block_enumerate below spends ~log2(NT) shared-memory steps per element to
+// find its entry); the price is imbalance when one entry's list is much
+// longer than the rest.  f(t, s) as in block_enumerate.
+template <int NT, class Src, class F>
+__device__ __forceinline__ void block_warp_enumerate(int64_t a0, int64_t a1, Src src, F f) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t = a0 + wid; t < a1; t += NT / 32) {
+        int64_t st = 0;
+        int len = 0;
+        src(t, st, len);
+        for (int q = lane; q < len; q += 32) f(t, st + q);
+    }
+}
+
 // Block-wide version for one row per CTA (NT threads, NT multiple of 32).
 // f(t, s) is called only for valid positions (no collectives inside f).
 template <int NT, class Src, class F>

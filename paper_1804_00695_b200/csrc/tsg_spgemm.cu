@@ -890,6 +890,14 @@ __global__ void __launch_bounds__(256) k_sym_merge3(const int32_t *__restrict__ 
 template <int M>
 int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 
+// The dense symbolic tier enumerates a warp per A entry (R-MAT scale 18:
+// 80 -> 72 ms; the masked count's dense tier: 146 -> 54 ms at scale 22).  The
+// dense numeric tier keeps the flattened enumeration: a warp per entry
+// pointed its fp64 atomics at neighbouring positions (112 -> 179 ms)
+#ifndef DENSE_ENUM
+#define DENSE_ENUM block_warp_enumerate
+#endif
+
 // Dense symbolic tier: the row's union is ORed into a shared-memory bitmap
 // of all of B's column sets (64-bit words, ORed as 32-bit halves), then the
 // nonzero words are emitted in ascending set order -- no table, no sort.
@@ -907,7 +915,7 @@ __global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ li
         for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
         if (threadIdx.x == 0) s_cnt = 0ull;
         __syncthreads();
-        block_enumerate<NT>(
+        DENSE_ENUM<NT>(
             a.arp[gi], a.arp[gi + 1],
             [&](int64_t t, int64_t &st, int &len) {
                 int k = a.acol[t];
