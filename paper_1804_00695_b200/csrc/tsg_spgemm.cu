@@ -2197,6 +2197,17 @@ int launch_sym_thread(tsg_ctx *c, const Bins &bl, const SymArgs &a0) {
     return TSG_OK;
 }
 
+// resident CTAs per SM of the 1024-thread dense symbolic kernel with `smem`
+// bytes (two fit when the bitmap does: one CTA per SM was 50 % occupancy;
+// R-MAT scale 18: 74 -> 48 ms).  The dense numeric kernel stays at one per
+// SM: twice the CTAs doubled its fp64 atomic traffic in flight (110 -> 154 ms).
+static int dense_ctas_per_sm(size_t smem) {
+    static const int cap = getenv("TSG_DENSE_CTAS") ? atoi(getenv("TSG_DENSE_CTAS")) : 2;
+    int k = (int)((220 * 1024) / (smem + 1024));
+    if (k > cap) k = cap;
+    return k < 1 ? 1 : k;
+}
+
 int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols) {
     if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
@@ -2204,9 +2215,9 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
     const int64_t nw = dense_words(ncols);
     const size_t smem = (size_t)nw * 8;
     TSG_TRY(set_smem(k_sym_dense<1024>, smem));
-    k_sym_dense<1024><<<grid_for(n, 1, c->num_sms), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
+    k_sym_dense<1024><<<grid_for(n, 1, c->num_sms * dense_ctas_per_sm(smem)), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
                                                                              a, nw); ++c->launches;
-    TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid_for(n, 1, c->num_sms), 1024, smem));
+    TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid_for(n, 1, c->num_sms * dense_ctas_per_sm(smem)), 1024, smem));
     return TSG_OK;
 }
 
