@@ -341,10 +341,28 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
             A->live[*p] = got;
             c->bytes_in_use += (int64_t)got;
             if (c->bytes_in_use > c->bytes_peak) c->bytes_peak = c->bytes_in_use;
+            if (c->capture_owned) c->capture_owned->push_back(*p);
             return TSG_OK;
         }
     }
     void *raw = nullptr;
+    if (c->capture_owned) {
+        // inside a graph capture no stream-ordered allocation may be issued:
+        // a plain cudaMalloc (a block the plan keeps for its lifetime)
+        cudaError_t e2 = cudaMalloc(&raw, cls);
+        if (e2 != cudaSuccess) {
+            cudaGetLastError();
+            c->capture_failed = 1;
+            tsg_set_error("device allocation of %zu bytes failed during capture", bytes);
+            return TSG_ECAPACITY;
+        }
+        std::lock_guard<std::mutex> g(A->mu);
+        A->live[raw] = cls;
+        c->bytes_in_use += (int64_t)cls;
+        c->capture_owned->push_back(raw);
+        *p = raw;
+        return TSG_OK;
+    }
     cudaError_t e = cudaMallocAsync(&raw, cls, c->stream);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
@@ -367,6 +385,10 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
 
 int tsg_free(tsg_ctx *c, void *p) {
     if (!p) return TSG_OK;
+    if (c->capture_owned) {   // the capturing plan keeps every block it touched
+        c->capture_owned->push_back(p);
+        return TSG_OK;
+    }
     Arena *A = arena_of(c);
     std::lock_guard<std::mutex> g(A->mu);
     auto it = A->live.find(p);
@@ -384,6 +406,12 @@ int tsg_free(tsg_ctx *c, void *p) {
     A->free_blocks.emplace(cls, p);
     A->cached += cls;
     return TSG_OK;
+}
+
+// Blocks a destroyed plan owned go back to the arena (after the device is
+// done with them: the caller synchronises).
+void tsg_arena_return(tsg_ctx *c, const std::vector<void *> &blocks) {
+    for (void *p : blocks) tsg_free(c, p);
 }
 
 // ---- pinned host pool: result arrays handed to the caller live here, so the
@@ -861,9 +889,19 @@ int scan_impl(tsg_ctx *c, const TI *in, int64_t *out, int64_t n) {
     const int64_t tiles = (n + LB_TILE - 1) / LB_TILE;
     unsigned long long *state = nullptr;
     unsigned epoch = 0;
-    TSG_TRY(tsg_lookback_state(c, tiles, &state, &epoch));
     unsigned long long *counter = nullptr, cbase = 0;
-    TSG_TRY(tsg_lookback_counter(c, tiles, &counter, &cbase));
+    if (c->capture_owned) {
+        // a captured scan replays with the epoch and ticket base it was
+        // captured with: give it its own state and counter, cleared by the
+        // graph itself on every replay
+        TSG_TRY(tsg_alloc_t(c, &state, tiles + 1));
+        TSG_TRY(tsg_fill(c, state, 0, (size_t)(tiles + 1) * 8, c->stream));
+        counter = state + tiles;
+        epoch = 1;
+    } else {
+        TSG_TRY(tsg_lookback_state(c, tiles, &state, &epoch));
+        TSG_TRY(tsg_lookback_counter(c, tiles, &counter, &cbase));
+    }
     // in-place safe: a tile reads its inputs before writing, and writes only
     // its own range (plus out[n], past every input)
     TSG_CK(launch_pdl(scan_lookback<TI>, (unsigned)tiles, LB_BS, 0, c->stream, in, n, out, state, epoch,
@@ -1246,6 +1284,12 @@ extern "C" int tsg_csr_device_ptrs(const tsg_csr *m, int64_t **rp, int32_t **col
 
 extern "C" int tsg_csr_free(tsg_ctx *c, tsg_csr *m) {
     if (!m) return TSG_OK;
+    tsg_plans_forget(c, m);
+    if (m->plan) {   // a captured plan's output: its arrays stay with the plan
+        tsg_plan_release_slot(m->plan, m->plan_slot);
+        delete m;
+        return TSG_OK;
+    }
     if (m->host_mapped) {
         cudaStreamSynchronize(c->stream);
         cudaFreeHost(m->rp);

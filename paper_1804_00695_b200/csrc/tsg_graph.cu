@@ -375,6 +375,7 @@ __global__ void k_set_values(int64_t n, double v, double *__restrict__ out) {
 
 extern "C" int tsg_csr_set_values(tsg_ctx *c, tsg_csr *m, double value) {
     TSG_RESOLVE(c, m);
+    tsg_plans_forget(c, m);   // a captured multiply may hold its value pointer
     if (m->host_mapped) {
         tsg_set_error("tsg_csr_set_values: matrix lives in mapped host memory");
         return TSG_EARG;

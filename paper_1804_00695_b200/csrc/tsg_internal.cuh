@@ -12,6 +12,8 @@
 // native 32-bit ATOMS.OR halves (a 64-bit shared-memory OR is a CAS loop on
 // sm_100a).  One 128-bit LDS fetches a whole slot during lookups.
 #pragma once
+#include <cstdlib>
+#include <vector>
 #include <utility>
 
 #include <cuda_runtime.h>
@@ -56,6 +58,13 @@ struct tsg_ctx {
     // host only to order launches and size grids)
     int64_t *hint_sym, *hint_num;     // host views (nullptr: none)
     int64_t *hintd_sym, *hintd_num;   // device aliases
+    // CUDA-graph capture of a multiply (tsg_spgemm.cu plans): while set, the
+    // arena hands out blocks without stream-ordered calls, and every block
+    // allocated -- freed inside the capture or not -- is owned by the plan
+    std::vector<void *> *capture_owned;
+    int capture_failed;
+    int capture_timing;    // record the numeric ring events as external (replayed) nodes
+    int capture_rk;        // ring slot a capture recorded into
     cudaStream_t convert;     // int64 <-> int32 column conversion between copy stages (chunked)
     cudaStream_t widen;       // int32 -> int64 widening of drained C ranges (own stream, so a
                               // narrow for an H2D piece never queues behind a C drain)
@@ -103,7 +112,15 @@ struct tsg_csr {
     int lazy_nnz;
     tsg_ctx *owner;
     int64_t max_row_bound;
+    // output of a captured multiply plan (arrays owned by the plan): freeing
+    // it hands the plan's output slot back
+    void *plan;
+    int plan_slot;
 };
+// a plan whose graphs read `m` is dropped when m is freed or changed
+void tsg_plans_forget(tsg_ctx *ctx, const tsg_csr *m);
+void tsg_arena_return(tsg_ctx *ctx, const std::vector<void *> &blocks);
+void tsg_plan_release_slot(void *plan, int slot);
 // exact nnz of a product whose count is still on the device (no-op otherwise)
 int tsg_csr_resolve(tsg_ctx *ctx, tsg_csr *m);
 #define TSG_RESOLVE(ctx, m) TSG_TRY(tsg_csr_resolve((ctx), const_cast<tsg_csr *>(m)))
