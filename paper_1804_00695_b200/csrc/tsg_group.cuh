@@ -240,6 +240,64 @@ __device__ __forceinline__ void block_warp_enumerate(int64_t a0, int64_t a1, Src
     }
 }
 
+// Block-wide enumeration balanced by units, for rows whose entries' lists
+// are power-law long (hub rows).  EB entries at a time: src(t, st, len, w)
+// for all of them in flight together, each list cut into units of CH
+// consecutive elements, warps take units round-robin.  A unit's lanes cover
+// consecutive elements of ONE list (so an add / OR instruction never sees two
+// lanes on one target from different lists), and each lane issues its CH/32
+// loads ld(s) before any apply ap(w, v).  (A warp per whole entry left 31
+// warps at the barrier behind the one on a hub's list.)
+template <int NT, int EB, int CH, class V, class Src, class Ld, class Ap>
+__device__ __forceinline__ void block_unit_enumerate(int64_t a0, int64_t a1, Src src, Ld ld, Ap ap,
+                                                     int *s_warp) {
+    static_assert(EB <= NT && EB % 32 == 0 && EB <= 1024 && CH % 32 == 0, "unit enumeration shape");
+    __shared__ int64_t s_s0[EB];
+    __shared__ double s_w[EB];
+    __shared__ int s_uinc[EB];
+    __shared__ int s_len[EB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t tb = a0; tb < a1; tb += EB) {
+        const int64_t t = tb + threadIdx.x;
+        int64_t st = 0;
+        int ln = 0;
+        double w = 0.0;
+        if (threadIdx.x < EB && t < a1) src(t, st, ln, w);
+        const int nch = (ln + CH - 1) / CH;
+        int utot;
+        const int ux = block_excl_scan<NT>(nch, utot, s_warp);
+        if (threadIdx.x < EB) {
+            s_uinc[threadIdx.x] = ux + nch;
+            s_len[threadIdx.x] = ln;
+            s_s0[threadIdx.x] = st;
+            s_w[threadIdx.x] = w;
+        }
+        __syncthreads();
+        for (int u = wid; u < utot; u += NT / 32) {
+            // first entry with s_uinc > u: two ballot rounds over EB / 32
+            // groups (a 9-step binary search was a quarter of the instructions)
+            constexpr int G = EB / 32;
+            const unsigned g1 = __ballot_sync(0xffffffffu, s_uinc[lane * G + G - 1] <= u);
+            const int grp = __popc(g1);
+            const unsigned g2 = __ballot_sync(0xffffffffu, lane < G && s_uinc[grp * G + (lane < G ? lane : 0)] <= u);
+            const int lo = grp * G + __popc(g2);
+            const int le = s_len[lo];
+            const int q0 = (u - (s_uinc[lo] - (le + CH - 1) / CH)) * CH;
+            const int64_t sb = s_s0[lo] + q0;
+            const int cnt = le - q0 < CH ? le - q0 : CH;
+            const double we = s_w[lo];
+            V v[CH / 32];
+#pragma unroll
+            for (int r = 0; r < CH / 32; ++r)
+                if (r * 32 + lane < cnt) v[r] = ld(sb + r * 32 + lane);
+#pragma unroll
+            for (int r = 0; r < CH / 32; ++r)
+                if (r * 32 + lane < cnt) ap(we, v[r]);
+        }
+        __syncthreads();
+    }
+}
+
 // Block-wide version for one row per CTA (NT threads, NT multiple of 32).
 // f(t, s) is called only for valid positions (no collectives inside f).
 template <int NT, class Src, class F>

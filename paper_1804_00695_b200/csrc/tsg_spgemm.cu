@@ -897,24 +897,56 @@ int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 #ifndef DENSE_ENUM
 #define DENSE_ENUM block_warp_enumerate
 #endif
+#ifndef DENSE_SYM_UNITS
+#define DENSE_SYM_UNITS 1
+#endif
+#ifndef DENSE_EB
+#define DENSE_EB 512   // A entries per enumeration round (block_unit_enumerate)
+#endif
+#ifndef DENSE_CH
+#define DENSE_CH 128   // elements per warp unit
+#endif
 
 // Dense symbolic tier: the row's union is ORed into a shared-memory bitmap
 // of all of B's column sets (64-bit words, ORed as 32-bit halves), then the
 // nonzero words are emitted in ascending set order -- no table, no sort.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ list, int64_t nlist,
+__global__ void __launch_bounds__(NT, 2048 / NT) k_sym_dense(const int32_t *__restrict__ list, int64_t nlist,
                                                   SymArgs a, int64_t nwords) {
     extern __shared__ int4 smem[];
     __shared__ int s_warp[32];
-    __shared__ unsigned long long s_cnt;
+    __shared__ unsigned s_cnt;
     uint64_t *bm = reinterpret_cast<uint64_t *>(smem);
     unsigned *bm32 = reinterpret_cast<unsigned *>(smem);
     for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
         const int64_t i = list[li];
         const int64_t gi = i + a.a_row_off;
         for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
-        if (threadIdx.x == 0) s_cnt = 0ull;
+        if (threadIdx.x == 0) s_cnt = 0u;
         __syncthreads();
+#if DENSE_SYM_UNITS
+        struct SB {
+            int set;
+            uint64_t bits;
+        };
+        block_unit_enumerate<NT, DENSE_EB, DENSE_CH, SB>(
+            a.arp[gi], a.arp[gi + 1],
+            [&](int64_t t, int64_t &st, int &len, double &) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    st = a.cbstart[k];
+                    len = a.cbcnt[k];
+                }
+            },
+            [&](int64_t sidx) { return SB{a.cbset[sidx], a.cbbits[sidx]}; },
+            [&](double, const SB &x) {
+                if ((unsigned)x.bits) atomicOr(&bm32[2 * x.set], (unsigned)x.bits);
+                if ((unsigned)(x.bits >> 32)) atomicOr(&bm32[2 * x.set + 1], (unsigned)(x.bits >> 32));
+            },
+            s_warp);
+        __syncthreads();
+#else
         DENSE_ENUM<NT>(
             a.arp[gi], a.arp[gi + 1],
             [&](int64_t t, int64_t &st, int &len) {
@@ -931,19 +963,24 @@ __global__ void __launch_bounds__(NT) k_sym_dense(const int32_t *__restrict__ li
                 if ((unsigned)bits) atomicOr(&bm32[2 * set], (unsigned)bits);
                 if ((unsigned)(bits >> 32)) atomicOr(&bm32[2 * set + 1], (unsigned)(bits >> 32));
             });
+#endif
         __syncthreads();
         // each thread owns a contiguous run of words: count its nonzero sets,
         // block-scan the counts, emit its sets in order
         const int64_t per = (nwords + NT - 1) / NT;
         const int64_t w0 = threadIdx.x * per, w1 = w0 + per < nwords ? w0 + per : nwords;
         int nz = 0;
-        unsigned long long pc = 0;
+        unsigned pc = 0;
         for (int64_t w = w0; w < w1; ++w) {
             const uint64_t x = bm[w];
             nz += x != 0ull;
             pc += __popcll(x);
         }
-        atomicAdd(&s_cnt, pc);
+        // one native 32-bit add per warp (a 64-bit add per thread was a CAS
+        // spin on one word: half of the kernel's stall samples)
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, d);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, pc);
         int tot;
         int r = block_excl_scan<NT>(nz, tot, s_warp);
         if (a.oset) {
@@ -1717,6 +1754,258 @@ __global__ void __launch_bounds__(NT) k_num_dense(const int32_t *__restrict__ li
     }
 }
 
+// Dense numeric tier, windowed (default).  The flattened REDG form above is
+// bound by its enumeration (a ~10-step shared-memory search per product) and
+// by fp64 atomics in L2 (R-MAT scale 18: 108 ms).  Here a row's sorted sets
+// are cut into windows and every (row, window) pair is a work item taken from
+// an atomic counter by persistent CTAs:
+//   k_num_dense_prep  one CTA per row: window starts.  A window is a run of
+//                     the row's sets with one block of DW_SETS column sets
+//                     (so its (mask, base) map is direct-mapped in shared
+//                     memory) and set bases in one block of W positions (so
+//                     its values fit a W + 63 shared fp64 window)
+//   k_num_dense_win   per item: the window's map in shared memory, its
+//                     columns into C; a warp per A entry adds the entry's
+//                     products into the shared window (CAS adds: neighbouring
+//                     positions of one warp hit distinct banks, no L2
+//                     atomics); one coalesced store of the values.  Rows of
+//                     several windows cut every B row to the window's column
+//                     range by binary search (the dense tier requires
+//                     row-sorted B), so each product is read once.
+// Hub rows thereby spread over all SMs instead of one CTA each.
+struct DenseWin {
+    int W;        // positions per window block
+    int sets;     // column sets (64-column words) per window block
+    int maxw;     // window-start slots per row
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_num_dense_prep(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
+                                                       DenseWin dw, int32_t *__restrict__ nwin,
+                                                       int2 *__restrict__ wst) {
+    __shared__ int s_warp[32];
+    for (int64_t li = blockIdx.x; li < nb; li += gridDim.x) {
+        const int64_t i = list[li];
+        const int64_t n = a.counts[i];
+        const int m = a.msets[i] & (SETS_WRITTEN - 1);
+        const int64_t sp = a.sptr[i];
+        int2 *ws = wst + li * dw.maxw;
+        int carry = 0, nstart = 0;
+        for (int q0 = 0; q0 < m; q0 += NT) {
+            const int q = q0 + threadIdx.x;
+            int set = 0, pc = 0;
+            if (q < m) {
+                set = a.sset[sp + q];
+                pc = __popcll(a.sbits[sp + q]);
+            }
+            int tot;
+            const int b = carry + block_excl_scan<NT>(pc, tot, s_warp);
+            bool start = false;
+            if (q < m) {
+                if (q == 0) {
+                    start = true;
+                } else {
+                    const int ps = a.sset[sp + q - 1];
+                    const int pb = b - __popcll(a.sbits[sp + q - 1]);
+                    start = ps / dw.sets != set / dw.sets || pb / dw.W != b / dw.W;
+                }
+            }
+            __syncthreads();   // s_warp reuse
+            int ns;
+            const int r = nstart + block_excl_scan<NT>(start ? 1 : 0, ns, s_warp);
+            if (start && r < dw.maxw) ws[r] = make_int2(q, b);
+            nstart += ns;
+            carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const bool ok = carry == n && nstart <= dw.maxw;
+            if (!ok) kerr(a.err, KERR_COUNT, i + a.a_row_off);
+            nwin[li] = ok ? nstart : 0;
+        }
+        __syncthreads();
+    }
+}
+
+// first s in [s0, s1) with col[s] >= c (col ascending)
+__device__ __forceinline__ int64_t lower_col(const int32_t *__restrict__ col, int64_t s0, int64_t s1, int c) {
+    while (s0 < s1) {
+        const int64_t mid = (s0 + s1) >> 1;
+        if (col[mid] < c) s0 = mid + 1;
+        else s1 = mid;
+    }
+    return s0;
+}
+
+#ifndef DENSE_U
+#define DENSE_U 4
+#endif
+#ifndef DENSE_FLATTEN
+#define DENSE_FLATTEN 0
+#endif
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
+                                                      DenseWin dw, const int64_t *__restrict__ woff,
+                                                      const int2 *__restrict__ wst,
+                                                      unsigned long long *__restrict__ counter) {
+    extern __shared__ int4 smem[];
+    uint64_t *smask = reinterpret_cast<uint64_t *>(smem);
+    int32_t *sbase = reinterpret_cast<int32_t *>(smask + dw.sets);
+    double *acc = reinterpret_cast<double *>(sbase + dw.sets + (dw.sets & 1));
+    __shared__ int64_t s_item;
+    __shared__ int s_warp[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t total = woff[nb];
+    for (;;) {
+        if (threadIdx.x == 0) s_item = (int64_t)atomicAdd(counter, 1ull);
+        __syncthreads();
+        const int64_t x = s_item;
+        if (x >= total) break;
+        int64_t lo = 0, hi = nb - 1;   // last row with woff <= x
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (woff[mid] <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t li = lo;
+        const int nw = (int)(woff[li + 1] - woff[li]);
+        const int j = (int)(x - woff[li]);
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t cp = a.cptr[i];
+        const int64_t sp = a.sptr[i];
+        const int2 w0 = wst[li * dw.maxw + j];
+        int2 w1;
+        if (j + 1 < nw) w1 = wst[li * dw.maxw + j + 1];
+        else w1 = make_int2(a.msets[i] & (SETS_WRITTEN - 1), (int)a.counts[i]);
+        const int P0 = w0.y, len = w1.y - w0.y;
+        const int blk = a.sset[sp + w0.x] / dw.sets * dw.sets;
+        const int c_lo = nw > 1 ? a.sset[sp + w0.x] * 64 : INT_MIN;
+        const int c_hi = j + 1 < nw ? a.sset[sp + w1.x] * 64 : INT_MAX;
+        // the window's (mask, base) map and columns
+        int carry = P0;
+        for (int q0 = w0.x; q0 < w1.x; q0 += NT) {
+            const int q = q0 + threadIdx.x;
+            int set = 0, pc = 0;
+            uint64_t bits = 0;
+            if (q < w1.x) {
+                set = a.sset[sp + q];
+                bits = a.sbits[sp + q];
+                pc = __popcll(bits);
+            }
+            int tot;
+            const int b = carry + block_excl_scan<NT>(pc, tot, s_warp);
+            if (q < w1.x) {
+                smask[set - blk] = bits;
+                sbase[set - blk] = b - P0;
+                uint64_t y = bits;
+                int64_t r = cp + b;
+                while (y) {
+                    a.ccol[r++] = set * 64 + (__ffsll((long long)y) - 1);
+                    y &= y - 1;
+                }
+            }
+            carry += tot;
+            __syncthreads();
+        }
+        for (int q = threadIdx.x; q < len; q += NT) acc[q] = -0.0;
+        __syncthreads();
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+#if DENSE_FLATTEN
+        // a warp takes 32 A entries at a time (their row / range lookups in
+        // flight together), then walks their flattened products DENSE_U per
+        // lane per round with every B load issued before the adds
+        for (int64_t tb = a0 + wid * 32; tb < a1; tb += NT) {
+            const int64_t t = tb + lane;
+            int64_t s0 = 0;
+            int ln = 0;
+            double av = 0.0;
+            if (t < a1) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    s0 = a.brp[k];
+                    int64_t s1 = a.brp[k + 1];
+                    if (nw > 1) {
+                        s0 = lower_col(a.bcol, s0, s1, c_lo);
+                        s1 = lower_col(a.bcol, s0, s1, c_hi);
+                    }
+                    ln = (int)(s1 - s0);
+                    av = a.aval[t];
+                }
+            }
+            int incl = ln;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int64_t sx = s0 - (incl - ln);   // s of product p of this entry = sx + p
+            for (int p0 = 0; p0 < total; p0 += 32 * DENSE_U) {
+                int cc[DENSE_U];
+                double pv[DENSE_U];
+#pragma unroll
+                for (int u = 0; u < DENSE_U; ++u) {
+                    const int p = p0 + u * 32 + lane;
+                    int e = 0;   // entry of product p: lanes with incl <= p
+#pragma unroll
+                    for (int st = 16; st >= 1; st >>= 1)
+                        if (__shfl_sync(0xffffffffu, incl, e + st - 1) <= p) e += st;
+                    const int64_t s = __shfl_sync(0xffffffffu, sx, e & 31) + p;
+                    const double ae = __shfl_sync(0xffffffffu, av, e & 31);
+                    cc[u] = p < total ? a.bcol[s] : -1;
+                    pv[u] = p < total ? __dmul_rn(ae, a.bval[s]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < DENSE_U; ++u) {
+                    if (cc[u] < 0) continue;
+                    const int c = cc[u];
+                    const int w = (c >> 6) - blk;
+                    const int bit = c & 63;
+                    const int pos = sbase[w] + __popcll(smask[w] & ((1ull << bit) - 1ull));
+                    atomicAdd(&acc[pos], pv[u]);
+                }
+            }
+        }
+#else
+        // products in units of DENSE_CH of one B row (block_unit_enumerate)
+        struct BV {
+            int c;
+            double v;
+        };
+        block_unit_enumerate<NT, DENSE_EB, DENSE_CH, BV>(
+            a0, a1,
+            [&](int64_t t, int64_t &st, int &ln, double &w) {
+                int k = a.acol[t];
+                if (k >= a.b_lo && k < a.b_hi) {
+                    k -= a.b_lo;
+                    int64_t s0 = a.brp[k], s1 = a.brp[k + 1];
+                    if (nw > 1) {
+                        s0 = lower_col(a.bcol, s0, s1, c_lo);
+                        s1 = lower_col(a.bcol, s0, s1, c_hi);
+                    }
+                    st = s0;
+                    ln = (int)(s1 - s0);
+                    w = a.aval[t];
+                }
+            },
+            [&](int64_t s) { return BV{a.bcol[s], a.bval[s]}; },
+            [&](double av, const BV &x) {
+                const int w = (x.c >> 6) - blk;
+                const int bit = x.c & 63;
+                const int pos = sbase[w] + __popcll(smask[w] & ((1ull << bit) - 1ull));
+                atomicAdd(&acc[pos], __dmul_rn(av, x.v));
+            },
+            s_warp);
+#endif
+        __syncthreads();
+        for (int q = threadIdx.x; q < len; q += NT) a.cval[cp + P0 + q] = acc[q];
+        __syncthreads();
+    }
+}
+
 // ======================================================================= CTA / global tiers
 
 // Union of the row's sets into tbl (generic pointer: smem or global slab).
@@ -2101,28 +2390,83 @@ int list_max(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int64
     return TSG_OK;
 }
 
+// Global tier rows split into classes of table size (<= 2^15, 2^17, 2^19,
+// 2^21 slots, above) before launching: the slab budget per launch then bounds
+// the CTAs by the class's own largest table instead of the bin's largest row
+// (one 4 M-column hub row used to leave ~10 CTAs for all of an R-MAT scale-22
+// bin's rows).  One small read-back of the class sizes replaces the max.
+constexpr int GCLASSES = 5;
+__host__ __device__ __forceinline__ int gclass_of(int64_t T) {
+    int k = 0;
+    while (k < GCLASSES - 1 && T > ((int64_t)1 << (15 + 2 * k))) ++k;
+    return k;
+}
+
+__global__ void k_gclass_count(const int32_t *__restrict__ list, int64_t n, const int64_t *__restrict__ v,
+                               unsigned long long *cnt) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[gclass_of(table_slots(v[list[x]]))], 1ull);
+}
+
+__global__ void k_gclass_scatter(const int32_t *__restrict__ list, int64_t n, const int64_t *__restrict__ v,
+                                 unsigned long long *cursor, int32_t *__restrict__ out) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = list[x];
+        out[atomicAdd(&cursor[gclass_of(table_slots(v[r]))], 1ull)] = r;
+    }
+}
+
+// rows of `list` regrouped by class (out: n entries, off: GCLASSES + 1 starts)
+static int global_classes(tsg_ctx *c, const int32_t *list, int64_t n, const int64_t *v, int32_t **out,
+                          int64_t off[GCLASSES + 1]) {
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(c->d_small + 24);
+    TSG_TRY(tsg_fill(c, cnt, 0, GCLASSES * sizeof(unsigned long long), c->stream));
+    k_gclass_count<<<grid_for(n, 256, c->num_sms * 4), 256, 0, c->stream>>>(list, n, v, cnt); ++c->launches;
+    TSG_TRY(tsg_put_small(c, reinterpret_cast<const int64_t *>(cnt), GCLASSES, 2));
+    TSG_CK(cudaStreamSynchronize(c->stream));
+    off[0] = 0;
+    for (int k = 0; k < GCLASSES; ++k) off[k + 1] = off[k] + c->h_small[2 + k];
+    TSG_TRY(tsg_alloc_t(c, out, n));
+    unsigned long long *cur = reinterpret_cast<unsigned long long *>(c->d_small + 24);
+    unsigned long long h[GCLASSES];
+    for (int k = 0; k < GCLASSES; ++k) h[k] = (unsigned long long)off[k];
+    TSG_CK(cudaMemcpyAsync(cur, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    k_gclass_scatter<<<grid_for(n, 256, c->num_sms * 4), 256, 0, c->stream>>>(list, n, v, cur, *out);
+    ++c->launches;
+    TSG_CK(cudaStreamSynchronize(c->stream));   // `h` is pageable host memory
+    return TSG_OK;
+}
+
 int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
-    int64_t maxb = 0;
-    TSG_TRY(list_max(c, bl.list + bl.off[B], n, a.sbound, maxb));
-    int64_t T = table_slots(maxb);
-    if (T > (1ll << 30)) {
-        tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
-        return TSG_ECAPACITY;
+    int32_t *cl = nullptr;
+    int64_t off[GCLASSES + 1];
+    TSG_TRY(global_classes(c, bl.list + bl.off[B], n, a.sbound, &cl, off));
+    for (int k = GCLASSES - 1; k >= 0; --k) {
+        const int64_t nk = off[k + 1] - off[k];
+        if (nk <= 0) continue;
+        int64_t maxb = 0;
+        TSG_TRY(list_max(c, cl + off[k], nk, a.sbound, maxb));
+        int64_t T = table_slots(maxb);
+        if (T > (1ll << 30)) {
+            tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
+            return TSG_ECAPACITY;
+        }
+        int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 16);
+        if (ctas < 1) ctas = 1;
+        if (ctas > nk) ctas = nk;
+        if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
+        int4 *slab = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
+        k_sym_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(cl + off[k], nk, a, slab, T, (int)T);
+        ++c->launches;
+        TSG_CK(cudaGetLastError());
+        TSG_TRY(tsg_free(c, slab));
     }
-    int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 16);
-    if (ctas < 1) ctas = 1;
-    if (ctas > n) ctas = n;
-    if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
-    int4 *slab = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
-    k_sym_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab, T,
-                                                                   (int)T); ++c->launches;
-    TSG_CK(cudaGetLastError());
-    TSG_TRY(tsg_free(c, slab));
+    TSG_TRY(tsg_free(c, cl));
     return TSG_OK;
 }
 
@@ -2131,26 +2475,36 @@ int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     const int B = BIN_GLOBAL;
     int64_t n = bl.off[B + 1] - bl.off[B];
     if (n <= 0) return TSG_OK;
-    int64_t maxm = 0;   // distinct sets <= columns: size the slab by the largest count
-    TSG_TRY(list_max(c, bl.list + bl.off[B], n, a.counts, maxm));
-    int64_t T = table_slots(maxm);
-    if (T > (1ll << 30)) {
-        tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
-        return TSG_ECAPACITY;
+    // distinct sets <= columns: classes (and slabs) by the rows' counts
+    int32_t *cl = nullptr;
+    int64_t off[GCLASSES + 1];
+    TSG_TRY(global_classes(c, bl.list + bl.off[B], n, a.counts, &cl, off));
+    for (int k = GCLASSES - 1; k >= 0; --k) {
+        const int64_t nk = off[k + 1] - off[k];
+        if (nk <= 0) continue;
+        int64_t maxm = 0;
+        TSG_TRY(list_max(c, cl + off[k], nk, a.counts, maxm));
+        int64_t T = table_slots(maxm);
+        if (T > (1ll << 30)) {
+            tsg_set_error("row accumulator of %lld slots exceeds the global tier", (long long)T);
+            return TSG_ECAPACITY;
+        }
+        int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 24);
+        if (ctas < 1) ctas = 1;
+        if (ctas > nk) ctas = nk;
+        if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
+        int4 *slab = nullptr;
+        uint64_t *sortslab = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
+        TSG_TRY(tsg_alloc_t(c, &sortslab, (size_t)(ctas * T)));
+        k_num_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(cl + off[k], nk, a, slab, sortslab, T,
+                                                                       (int)T);
+        ++c->launches;
+        TSG_CK(cudaGetLastError());
+        TSG_TRY(tsg_free(c, slab));
+        TSG_TRY(tsg_free(c, sortslab));
     }
-    int64_t ctas = GLOBAL_SLAB_BUDGET / (T * 24);
-    if (ctas < 1) ctas = 1;
-    if (ctas > n) ctas = n;
-    if (ctas > 2 * c->num_sms) ctas = 2 * c->num_sms;
-    int4 *slab = nullptr;
-    uint64_t *sortslab = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &slab, (size_t)(ctas * T)));
-    TSG_TRY(tsg_alloc_t(c, &sortslab, (size_t)(ctas * T)));
-    k_num_block<512, true><<<(unsigned)ctas, 512, 0, c->stream>>>(bl.list + bl.off[B], n, a, slab,
-                                                                   sortslab, T, (int)T); ++c->launches;
-    TSG_CK(cudaGetLastError());
-    TSG_TRY(tsg_free(c, slab));
-    TSG_TRY(tsg_free(c, sortslab));
+    TSG_TRY(tsg_free(c, cl));
     return TSG_OK;
 }
 
@@ -2221,10 +2575,56 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
     return TSG_OK;
 }
 
+// windowed dense numeric: positions per window, CTAs per SM, map budget
+static int dense_win_param(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols) {
     if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
     if (n <= 0) return TSG_OK;
+    static const int per_sm = dense_win_param("TSG_DENSE_WIN_CTAS", 1);
+    static const int W = dense_win_param("TSG_DENSE_WIN", per_sm > 1 ? 8192 : 19456);
+    static const int WS = dense_win_param("TSG_DENSE_WIN_SETS", per_sm > 1 ? 2048 : 4096);
+    static const int old = dense_win_param("TSG_DENSE_FLAT", 0);
+    if (!old) {
+        const int64_t nw = dense_words(ncols);
+        DenseWin dw;
+        dw.W = W;
+        dw.sets = WS;
+        dw.maxw = (int)((ncols + W - 1) / W + (nw + WS - 1) / WS + 2);
+        int64_t batch = ((int64_t)64 << 20) / (dw.maxw * 8);
+        if (batch < 1) batch = 1;
+        if (batch > n) batch = n;
+        int32_t *nwin = nullptr;
+        int64_t *woff = nullptr;
+        int2 *wst = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &nwin, (size_t)batch));
+        TSG_TRY(tsg_alloc_t(c, &woff, (size_t)batch + 1));
+        TSG_TRY(tsg_alloc_t(c, &wst, (size_t)(batch * dw.maxw)));
+        unsigned long long *counter = reinterpret_cast<unsigned long long *>(c->d_small + 30);
+        const size_t smem = (size_t)WS * 12 + 8 + (size_t)(W + 64) * 8;
+        TSG_TRY(set_smem(k_num_dense_win<1024>, smem));
+        for (int64_t b0 = 0; b0 < n; b0 += batch) {
+            const int64_t nb = n - b0 < batch ? n - b0 : batch;
+            const int32_t *lst = bl.list + bl.off[BIN_DENSE] + b0;
+            k_num_dense_prep<1024><<<grid_for(nb, 1, c->num_sms * 2), 1024, 0, c->stream>>>(lst, nb, a, dw, nwin,
+                                                                                             wst);
+            ++c->launches;
+            TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nwin, woff, nb));
+            TSG_TRY(tsg_fill(c, counter, 0, sizeof(unsigned long long), c->stream));
+            k_num_dense_win<1024><<<c->num_sms * per_sm, 1024, smem, c->stream>>>(lst, nb, a, dw, woff, wst,
+                                                                                  counter);
+            ++c->launches;
+            TSG_TRY(tsg_launch_check("k_num_dense_win", BIN_DENSE, c->num_sms * per_sm, 1024, smem));
+        }
+        TSG_TRY(tsg_free(c, nwin));
+        TSG_TRY(tsg_free(c, woff));
+        TSG_TRY(tsg_free(c, wst));
+        return TSG_OK;
+    }
     const int64_t nw = dense_words(ncols);
     const size_t smem = (size_t)nw * 12;
     TSG_TRY(set_smem(k_num_dense<1024>, smem));

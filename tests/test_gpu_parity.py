@@ -430,3 +430,35 @@ def test_fused_rap_falls_back_when_rows_do_not_fit():
     _same_csr(kernel.rap(r, a, p), want)
     with pytest.raises(tsg.DimensionError):
         kernel.rap(r, p, a)
+
+
+def test_dense_numeric_small_windows():
+    # the windowed dense numeric tier with 777-position windows (env read once
+    # per process, so in a child): many window boundaries inside set words,
+    # every B row cut by binary search; compared with the oracle
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "import paper_1804_00695_b200 as tsg\n"
+        "from paper_1804_00695_b200.csr import CsrMatrix, canonicalize\n"
+        "from oracle import oracle as O\n"
+        "from conftest import assert_same_product, random_csr\n"
+        "rng = np.random.default_rng(7)\n"
+        "n = 6000\n"
+        "rows = [rng.choice(n, size=k, replace=False) for k in (3, 40, 400, 2500, 5000)]\n"
+        "r = np.concatenate([np.full(len(x), i) for i, x in enumerate(rows)])\n"
+        "a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.uniform(0.1, 1, len(r)), len(rows), n)\n"
+        "b = canonicalize(random_csr(rng, n, 150000, 60))\n"
+        "assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=False, rtol=1e-12)\n"
+        "bi = CsrMatrix(b.num_rows, b.num_cols, b.row_ptr, b.col_idx, np.round(b.values * 8))\n"
+        "ai = CsrMatrix(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, np.ones(a.nnz))\n"
+        "assert_same_product(tsg.multiply(ai, bi), O.multiply(ai, bi), exact=True)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_DENSE_WIN="777",
+               PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
