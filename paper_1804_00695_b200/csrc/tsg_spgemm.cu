@@ -1733,23 +1733,29 @@ __global__ void __launch_bounds__(NT) k_num_dense(const int32_t *__restrict__ li
             continue;
         }
         __syncthreads();
-        block_enumerate<NT>(
+        struct BV {
+            int c;
+            double v;
+        };
+        block_unit_enumerate<NT, DENSE_EB, DENSE_CH, BV>(
             a.arp[gi], a.arp[gi + 1],
-            [&](int64_t t, int64_t &st, int &len) {
+            [&](int64_t t, int64_t &st, int &len, double &w) {
                 int k = a.acol[t];
                 if (k >= a.b_lo && k < a.b_hi) {
                     k -= a.b_lo;
                     st = a.brp[k];
                     len = (int)(a.brp[k + 1] - st);
+                    w = a.aval[t];
                 }
             },
-            [&](int64_t t, int64_t s) {
-                const int c = a.bcol[s];
-                const uint64_t mk = mask[c >> 6];
-                const int bit = c & 63;
-                const int pos = base[c >> 6] + __popcll(mk & ((bit ? (~0ull >> (64 - bit)) : 0ull)));
-                atomicAdd(&a.cval[cp + pos], __dmul_rn(a.aval[t], a.bval[s]));
-            });
+            [&](int64_t s) { return BV{a.bcol[s], a.bval[s]}; },
+            [&](double av, const BV &x) {
+                const uint64_t mk = mask[x.c >> 6];
+                const int bit = x.c & 63;
+                const int pos = base[x.c >> 6] + __popcll(mk & ((1ull << bit) - 1ull));
+                atomicAdd(&a.cval[cp + pos], __dmul_rn(av, x.v));
+            },
+            s_warp);
         __syncthreads();
     }
 }
@@ -1773,6 +1779,16 @@ __global__ void __launch_bounds__(NT) k_num_dense(const int32_t *__restrict__ li
 //                     range by binary search (the dense tier requires
 //                     row-sorted B), so each product is read once.
 // Hub rows thereby spread over all SMs instead of one CTA each.
+// first s in [s0, s1) with col[s] >= c (col ascending)
+__device__ __forceinline__ int64_t lower_col(const int32_t *__restrict__ col, int64_t s0, int64_t s1, int c) {
+    while (s0 < s1) {
+        const int64_t mid = (s0 + s1) >> 1;
+        if (col[mid] < c) s0 = mid + 1;
+        else s1 = mid;
+    }
+    return s0;
+}
+
 struct DenseWin {
     int W;        // positions per window block
     int sets;     // column sets (64-column words) per window block
@@ -1782,7 +1798,8 @@ struct DenseWin {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_num_dense_prep(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
                                                        DenseWin dw, int32_t *__restrict__ nwin,
-                                                       int2 *__restrict__ wst) {
+                                                       int2 *__restrict__ wst, int32_t *__restrict__ ncut_e,
+                                                       int32_t *__restrict__ ncut) {
     __shared__ int s_warp[32];
     for (int64_t li = blockIdx.x; li < nb; li += gridDim.x) {
         const int64_t i = list[li];
@@ -1822,19 +1839,64 @@ __global__ void __launch_bounds__(NT) k_num_dense_prep(const int32_t *__restrict
             const bool ok = carry == n && nstart <= dw.maxw;
             if (!ok) kerr(a.err, KERR_COUNT, i + a.a_row_off);
             nwin[li] = ok ? nstart : 0;
+            const int64_t gi = i + a.a_row_off;
+            const int alen = (int)(a.arp[gi + 1] - a.arp[gi]);
+            ncut_e[li] = ok && nstart > 1 ? alen : 0;
+            ncut[li] = ok && nstart > 1 ? alen * (nstart - 1) : 0;
         }
         __syncthreads();
     }
 }
 
-// first s in [s0, s1) with col[s] >= c (col ascending)
-__device__ __forceinline__ int64_t lower_col(const int32_t *__restrict__ col, int64_t s0, int64_t s1, int c) {
-    while (s0 < s1) {
-        const int64_t mid = (s0 + s1) >> 1;
-        if (col[mid] < c) s0 = mid + 1;
-        else s1 = mid;
+// Cut points of multi-window rows: for every A entry of such a row, the
+// offsets into its B row where each later window's columns start (window-major,
+// coalesced for the window kernel).  A thread per entry gallops from one cut
+// to the next; thousands of independent searches replace the dependent
+// binary searches that stalled the window kernel's enumeration (18 ms of
+// barrier waits at R-MAT scale 18).
+__global__ void __launch_bounds__(256) k_num_dense_cut(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
+                                                       DenseWin dw, const int64_t *__restrict__ woff,
+                                                       const int2 *__restrict__ wst,
+                                                       const int64_t *__restrict__ eoff,
+                                                       const int64_t *__restrict__ coff,
+                                                       int32_t *__restrict__ cut) {
+    const int64_t tot = eoff[nb];
+    for (int64_t x = (int64_t)blockIdx.x * 256 + threadIdx.x; x < tot; x += (int64_t)gridDim.x * 256) {
+        int64_t lo = 0, hi = nb - 1;   // last row with eoff <= x
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (eoff[mid] <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t li = lo;
+        const int e = (int)(x - eoff[li]);
+        const int alen = (int)(eoff[li + 1] - eoff[li]);
+        const int nw = (int)(woff[li + 1] - woff[li]);
+        const int64_t i = list[li];
+        const int64_t gi = i + a.a_row_off;
+        const int64_t sp = a.sptr[i];
+        int32_t *cr = cut + coff[li] + e;
+        int k = a.acol[a.arp[gi] + e];
+        if (k < a.b_lo || k >= a.b_hi) {
+            for (int j = 1; j < nw; ++j) cr[(int64_t)(j - 1) * alen] = 0;
+            continue;
+        }
+        k -= a.b_lo;
+        const int64_t b0 = a.brp[k], b1 = a.brp[k + 1];
+        int64_t cur = b0;
+        for (int j = 1; j < nw; ++j) {
+            const int c = a.sset[sp + wst[li * dw.maxw + j].x] * 64;
+            // gallop: first s >= cur with col[s] >= c
+            int64_t step = 1, lo2 = cur, hi2 = cur;
+            while (hi2 < b1 && a.bcol[hi2] < c) {
+                lo2 = hi2 + 1;
+                hi2 += step;
+                step <<= 1;
+            }
+            cur = lower_col(a.bcol, lo2, hi2 < b1 ? hi2 : b1, c);
+            cr[(int64_t)(j - 1) * alen] = (int32_t)(cur - b0);
+        }
     }
-    return s0;
 }
 
 #ifndef DENSE_U
@@ -1843,11 +1905,22 @@ __device__ __forceinline__ int64_t lower_col(const int32_t *__restrict__ col, in
 #ifndef DENSE_FLATTEN
 #define DENSE_FLATTEN 0
 #endif
+#ifndef DENSE_NO_CCOL
+#define DENSE_NO_CCOL 0   // timing experiments only
+#endif
+#ifndef DENSE_CCOL_WARP
+#define DENSE_CCOL_WARP 0   // 1: warp per set (R-MAT 18: 68 -> 90 ms)
+#endif
+#ifndef DENSE_NO_ACC
+#define DENSE_NO_ACC 0    // timing experiments only
+#endif
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
                                                       DenseWin dw, const int64_t *__restrict__ woff,
                                                       const int2 *__restrict__ wst,
+                                                      const int64_t *__restrict__ coff,
+                                                      const int32_t *__restrict__ cut,
                                                       unsigned long long *__restrict__ counter) {
     extern __shared__ int4 smem[];
     uint64_t *smask = reinterpret_cast<uint64_t *>(smem);
@@ -1899,17 +1972,34 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
             if (q < w1.x) {
                 smask[set - blk] = bits;
                 sbase[set - blk] = b - P0;
+#if !DENSE_NO_CCOL && !DENSE_CCOL_WARP
                 uint64_t y = bits;
                 int64_t r = cp + b;
                 while (y) {
                     a.ccol[r++] = set * 64 + (__ffsll((long long)y) - 1);
                     y &= y - 1;
                 }
+#endif
             }
             carry += tot;
             __syncthreads();
         }
         for (int q = threadIdx.x; q < len; q += NT) acc[q] = -0.0;
+#if DENSE_CCOL_WARP
+        // the window's columns: a warp per set, a lane per bit (coalesced
+        // stores; a thread per set looped over its bits with scattered stores)
+        for (int q = w0.x + wid; q < w1.x; q += NT / 32) {
+            const int set = a.sset[sp + q];
+            const uint64_t mk = smask[set - blk];
+            const int bs = sbase[set - blk];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int bit = h * 32 + lane;
+                if ((mk >> bit) & 1ull)
+                    a.ccol[cp + P0 + bs + __popcll(mk & ((1ull << bit) - 1ull))] = set * 64 + bit;
+            }
+        }
+#endif
         __syncthreads();
         const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
 #if DENSE_FLATTEN
@@ -1983,8 +2073,11 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
                     k -= a.b_lo;
                     int64_t s0 = a.brp[k], s1 = a.brp[k + 1];
                     if (nw > 1) {
-                        s0 = lower_col(a.bcol, s0, s1, c_lo);
-                        s1 = lower_col(a.bcol, s0, s1, c_hi);
+                        const int64_t e = t - a0;
+                        const int32_t *cr = cut + coff[li] + e;
+                        const int64_t bb = s0;
+                        if (j > 0) s0 = bb + cr[(int64_t)(j - 1) * (a1 - a0)];
+                        if (j + 1 < nw) s1 = bb + cr[(int64_t)j * (a1 - a0)];
                     }
                     st = s0;
                     ln = (int)(s1 - s0);
@@ -1996,7 +2089,11 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
                 const int w = (x.c >> 6) - blk;
                 const int bit = x.c & 63;
                 const int pos = sbase[w] + __popcll(smask[w] & ((1ull << bit) - 1ull));
+#if DENSE_NO_ACC
+                if (__dmul_rn(av, x.v) == 12345.678) acc[pos] = 1.0;
+#else
                 atomicAdd(&acc[pos], __dmul_rn(av, x.v));
+#endif
             },
             s_warp);
 #endif
@@ -2598,11 +2695,15 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
         int64_t batch = ((int64_t)64 << 20) / (dw.maxw * 8);
         if (batch < 1) batch = 1;
         if (batch > n) batch = n;
-        int32_t *nwin = nullptr;
-        int64_t *woff = nullptr;
+        int32_t *nwin = nullptr, *ncut_e = nullptr, *ncut = nullptr;
+        int64_t *woff = nullptr, *eoff = nullptr, *coff = nullptr;
         int2 *wst = nullptr;
         TSG_TRY(tsg_alloc_t(c, &nwin, (size_t)batch));
+        TSG_TRY(tsg_alloc_t(c, &ncut_e, (size_t)batch));
+        TSG_TRY(tsg_alloc_t(c, &ncut, (size_t)batch));
         TSG_TRY(tsg_alloc_t(c, &woff, (size_t)batch + 1));
+        TSG_TRY(tsg_alloc_t(c, &eoff, (size_t)batch + 1));
+        TSG_TRY(tsg_alloc_t(c, &coff, (size_t)batch + 1));
         TSG_TRY(tsg_alloc_t(c, &wst, (size_t)(batch * dw.maxw)));
         unsigned long long *counter = reinterpret_cast<unsigned long long *>(c->d_small + 30);
         const size_t smem = (size_t)WS * 12 + 8 + (size_t)(W + 64) * 8;
@@ -2611,15 +2712,33 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
             const int64_t nb = n - b0 < batch ? n - b0 : batch;
             const int32_t *lst = bl.list + bl.off[BIN_DENSE] + b0;
             k_num_dense_prep<1024><<<grid_for(nb, 1, c->num_sms * 2), 1024, 0, c->stream>>>(lst, nb, a, dw, nwin,
-                                                                                             wst);
+                                                                                             wst, ncut_e, ncut);
             ++c->launches;
             TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nwin, woff, nb));
+            TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut_e, eoff, nb));
+            TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut, coff, nb));
+            TSG_TRY(tsg_put_small(c, coff + nb, 1, 2));
+            TSG_TRY(tsg_put_small(c, eoff + nb, 1, 3));
+            TSG_CK(cudaStreamSynchronize(c->stream));
+            const int64_t ncuts = c->h_small[2], nents = c->h_small[3];
+            int32_t *cut = nullptr;
+            if (ncuts > 0) {
+                TSG_TRY(tsg_alloc_t(c, &cut, (size_t)ncuts));
+                k_num_dense_cut<<<grid_for(nents, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+                    lst, nb, a, dw, woff, wst, eoff, coff, cut);
+                ++c->launches;
+            }
             TSG_TRY(tsg_fill(c, counter, 0, sizeof(unsigned long long), c->stream));
             k_num_dense_win<1024><<<c->num_sms * per_sm, 1024, smem, c->stream>>>(lst, nb, a, dw, woff, wst,
-                                                                                  counter);
+                                                                                  coff, cut, counter);
             ++c->launches;
             TSG_TRY(tsg_launch_check("k_num_dense_win", BIN_DENSE, c->num_sms * per_sm, 1024, smem));
+            if (cut) TSG_TRY(tsg_free(c, cut));
         }
+        TSG_TRY(tsg_free(c, ncut_e));
+        TSG_TRY(tsg_free(c, ncut));
+        TSG_TRY(tsg_free(c, eoff));
+        TSG_TRY(tsg_free(c, coff));
         TSG_TRY(tsg_free(c, nwin));
         TSG_TRY(tsg_free(c, woff));
         TSG_TRY(tsg_free(c, wst));
@@ -2628,7 +2747,8 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
     const int64_t nw = dense_words(ncols);
     const size_t smem = (size_t)nw * 12;
     TSG_TRY(set_smem(k_num_dense<1024>, smem));
-    k_num_dense<1024><<<grid_for(n, 1, c->num_sms), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
+    static const int flat_ctas = dense_win_param("TSG_DENSE_FLAT_CTAS", 1);
+    k_num_dense<1024><<<grid_for(n, 1, c->num_sms * flat_ctas), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
                                                                              a, nw); ++c->launches;
     TSG_TRY(tsg_launch_check("k_num_dense", BIN_DENSE, grid_for(n, 1, c->num_sms), 1024, smem));
     return TSG_OK;
