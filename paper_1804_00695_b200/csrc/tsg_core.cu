@@ -333,7 +333,11 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
     {
         std::lock_guard<std::mutex> g(A->mu);
         auto it = A->free_blocks.lower_bound(cls);
-        if (it != A->free_blocks.end() && it->first <= cls + cls / 4) {   // best fit, <= 25% slack
+        // best fit, <= 25% slack; blocks of >= 256 MiB take up to 2x (a
+        // streamed multiply's C blocks vary in size: a miss there re-maps
+        // tens of GB after an out-of-memory trim, ~0.25 s per block)
+        const size_t slack = cls >= ((size_t)256 << 20) ? cls : cls / 4;
+        if (it != A->free_blocks.end() && it->first <= cls + slack) {
             *p = it->second;
             size_t got = it->first;
             A->free_blocks.erase(it);

@@ -71,6 +71,7 @@ struct tsg_ctx {
     cudaStream_t copy_in2;    // second H2D stream: a piece's column copy queues while the
                               // previous piece waits for its conversion (chunked)
     int64_t launches;         // kernels launched by this context (all entry points)
+    double mg_ratio = 0.0;    // streamed tsg_mg_multiply: last C entries per multiplication
     cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
     cudaEvent_t ev_user[8];   // tsg_event_record slots

@@ -347,7 +347,9 @@ extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, i
         // (R-MAT A*A: ~3 per entry): each block is sized by the largest
         // entries-per-multiplication ratio seen so far (x 1.25), starting at 1
         const int64_t cap_entries = std::max<int64_t>(c_budget_bytes / 16, 1);
-        double ratio = 1.0;
+        // the last call's ratio (same B, similar A blocks): the first block
+        // is sized like the rest, so the arena reuses its C blocks
+        double ratio = c->mg_ratio > 0 ? c->mg_ratio : 1.0;
         int64_t lo = 0;
         while (lo < a->rows && st_ == TSG_OK) {
             const double cap_mults = (double)cap_entries / std::min(1.0, 1.25 * ratio);
@@ -375,6 +377,7 @@ extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, i
                 }
                 local.max_block_nnz = std::max(local.max_block_nnz, C->nnz);
                 if (acc > 0) ratio = std::max(local.blocks ? ratio : 0.0, (double)C->nnz / (double)acc);
+                c->mg_ratio = ratio;
                 tsg_csr_free(c, C);
             }
             tsg_csr_free(c, as);
