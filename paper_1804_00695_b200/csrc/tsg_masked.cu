@@ -37,6 +37,9 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef DENSE_WARP_ENTRY
 #define DENSE_WARP_ENTRY 1
 #endif
+#ifndef DENSE_UNITS
+#define DENSE_UNITS 1
+#endif
 
 __device__ __forceinline__ int mask_bin(int64_t len, bool dense_ok) {
     if (len <= 0) return 255;
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
                                                    MaskArgs a, uint64_t *slab, int64_t nwords) {
     extern __shared__ int4 smem[];
     __shared__ unsigned long long s_tot;
+    __shared__ int s_warp[32];
     uint64_t *bm = SMEM ? reinterpret_cast<uint64_t *>(smem) : slab + (int64_t)blockIdx.x * nwords;
     unsigned *bm32 = reinterpret_cast<unsigned *>(bm);
     if (SMEM)
@@ -84,7 +88,24 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
         }
         if (!lower) kerr(a.err, KERR_NOTLOWER, i);
         __syncthreads();
-        if (DENSE_WARP_ENTRY) {
+        if (DENSE_UNITS) {
+            // units of DENSE_CH compressed sets of one L_j, balanced over the
+            // warps (a warp per whole entry left the block waiting on the one
+            // walking a hub's row), CH/32 loads per lane in flight
+            struct CS {
+                int set;
+                uint64_t bits;
+            };
+            block_unit_enumerate<NT, 512, 128, CS>(
+                r0, r1,
+                [&](int64_t t, int64_t &st, int &len, double &) {
+                    const int j = a.lcol[t];
+                    st = a.cstart[j];
+                    len = a.ccnt[j];
+                },
+                [&](int64_t s) { return CS{a.cset[s], a.cbits[s]}; },
+                [&](double, const CS &x) { mine += __popcll(x.bits & bm[x.set]); }, s_warp);
+        } else if (DENSE_WARP_ENTRY) {
             // a warp per entry j of the row, its lanes striding over L_j's
             // compressed sets: coalesced loads, no per-element search (the
             // flattened block enumeration spent ~10 shared-memory binary-search
