@@ -9,6 +9,8 @@
 // binned by table size exactly like the symbolic phase, and the int64 total
 // is reduced warp -> CTA (shared atomic) -> one global atomic per CTA, so the
 // integer result is exact and launch-order independent.
+#include <algorithm>
+
 #include "tsg_group.cuh"
 #include "tsg_partition.cuh"
 
@@ -66,74 +68,155 @@ struct MaskBinF {
 // row touched are cleared afterwards.
 template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ list, int64_t nlist,
-                                                   MaskArgs a, uint64_t *slab, int64_t nwords) {
+                                                   MaskArgs a, uint64_t *slab, int64_t nwords, int64_t wwords,
+                                                   const int64_t *__restrict__ coff, int64_t cut_base,
+                                                   const int32_t *__restrict__ cut) {
     extern __shared__ int4 smem[];
     __shared__ unsigned long long s_tot;
     __shared__ int s_warp[32];
     uint64_t *bm = SMEM ? reinterpret_cast<uint64_t *>(smem) : slab + (int64_t)blockIdx.x * nwords;
     unsigned *bm32 = reinterpret_cast<unsigned *>(bm);
-    if (SMEM)
-        for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
+    if (!SMEM) wwords = nwords;
+    for (int64_t w = threadIdx.x; w < wwords; w += NT) bm[w] = 0ull;
     if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
     long long mine = 0;
     for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
         const int64_t i = list[li];
         const int64_t r0 = a.lrp[i], r1 = a.lrp[i + 1];
-        bool lower = true;
-        for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) {
-            const int c = a.lcol[q];
-            if ((int64_t)c >= i) lower = false;
-            atomicOr(&bm32[c >> 5], 1u << (c & 31));
-        }
-        if (!lower) kerr(a.err, KERR_NOTLOWER, i);
-        __syncthreads();
-        if (DENSE_UNITS) {
-            // units of DENSE_CH compressed sets of one L_j, balanced over the
-            // warps (a warp per whole entry left the block waiting on the one
-            // walking a hub's row), CH/32 loads per lane in flight
-            struct CS {
-                int set;
-                uint64_t bits;
-            };
-            block_unit_enumerate<NT, 512, 128, CS>(
-                r0, r1,
-                [&](int64_t t, int64_t &st, int &len, double &) {
-                    const int j = a.lcol[t];
-                    st = a.cstart[j];
-                    len = a.ccnt[j];
-                },
-                [&](int64_t s) { return CS{a.cset[s], a.cbits[s]}; },
-                [&](double, const CS &x) { mine += __popcll(x.bits & bm[x.set]); }, s_warp);
-        } else if (DENSE_WARP_ENTRY) {
-            // a warp per entry j of the row, its lanes striding over L_j's
-            // compressed sets: coalesced loads, no per-element search (the
-            // flattened block enumeration spent ~10 shared-memory binary-search
-            // steps per compressed entry)
-            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-            for (int64_t t = r0 + wid; t < r1; t += NT / 32) {
-                const int j = a.lcol[t];
-                const int64_t st = a.cstart[j], en = st + a.ccnt[j];
-                for (int64_t q = st + lane; q < en; q += 32) mine += __popcll(a.cbits[q] & bm[a.cset[q]]);
+        // column windows of wwords sets: row i's columns (and every L_j's) lie
+        // below i, so rows below the first window's end take one pass; the
+        // windowed bitmap stays in shared memory at any graph size
+        const int64_t used = (i + 63) / 64 < nwords ? (i + 63) / 64 : nwords;
+        const int nwin = used <= wwords ? 1 : (int)((used + wwords - 1) / wwords);
+        for (int win = 0; win < nwin; ++win) {
+            const int64_t lo = (int64_t)win * wwords, hi = lo + wwords;
+            bool lower = true;
+            for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) {
+                const int c = a.lcol[q];
+                if ((int64_t)c >= i) lower = false;
+                const int64_t cw = c >> 6;
+                if (cw >= lo && cw < hi) atomicOr(&bm32[(c - lo * 64) >> 5], 1u << (c & 31));
             }
-        } else {
-            block_enumerate<NT>(
-                r0, r1,
-                [&](int64_t t, int64_t &st, int &len) {
-                    int j = a.lcol[t];
-                    st = a.cstart[j];
-                    len = a.ccnt[j];
-                },
-                [&](int64_t, int64_t s) { mine += __popcll(a.cbits[s] & bm[a.cset[s]]); });
+            if (win == 0 && !lower) kerr(a.err, KERR_NOTLOWER, i);
+            __syncthreads();
+            if (DENSE_UNITS) {
+                // units of DENSE_CH compressed sets of one L_j, balanced over
+                // the warps (a warp per whole entry left the block waiting on
+                // the one walking a hub's row), CH/32 loads per lane in flight
+                struct CS {
+                    int set;
+                    uint64_t bits;
+                };
+                block_unit_enumerate<NT, 512, 128, CS>(
+                    r0, r1,
+                    [&](int64_t t, int64_t &st, int &len, double &) {
+                        const int j = a.lcol[t];
+                        if (j > 0 && ((int64_t)(j - 1) >> 6) >= lo) {   // L_j's sets lie below j / 64
+                            st = a.cstart[j];
+                            len = a.ccnt[j];
+                            if (nwin > 1) {   // the window's sets: precomputed cuts (k_mask_cut)
+                                const int64_t alen = r1 - r0;
+                                const int32_t *cr = cut + (coff[li] - cut_base) + (t - r0);
+                                const int c0 = win > 0 ? cr[(win - 1) * alen] : 0;
+                                const int c1 = win + 1 < nwin ? cr[win * alen] : len;
+                                st += c0;
+                                len = c1 - c0;
+                            }
+                        }
+                    },
+                    [&](int64_t s) { return CS{a.cset[s], a.cbits[s]}; },
+                    [&](double, const CS &x) { mine += __popcll(x.bits & bm[x.set - lo]); },
+                    s_warp);
+            } else {
+                const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                for (int64_t t = r0 + wid; t < r1; t += NT / 32) {
+                    const int j = a.lcol[t];
+                    const int64_t st = a.cstart[j], en = st + a.ccnt[j];
+                    for (int64_t q = st + lane; q < en; q += 32) {
+                        const int set = a.cset[q];
+                        if (set >= lo && set < hi) mine += __popcll(a.cbits[q] & bm[set - lo]);
+                    }
+                }
+            }
+            __syncthreads();
+            for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) {
+                const int64_t cw = a.lcol[q] >> 6;
+                if (cw >= lo && cw < hi) bm[cw - lo] = 0ull;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        for (int64_t q = r0 + threadIdx.x; q < r1; q += NT) bm[a.lcol[q] >> 6] = 0ull;
-        __syncthreads();
     }
     for (int d = 16; d >= 1; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_tot, (unsigned long long)mine);
     __syncthreads();
     if (threadIdx.x == 0 && s_tot) atomicAdd(a.total, s_tot);
+}
+
+// Dense rows of several windows: per row the entries needing cut points (its
+// length) and the number of cuts (length x (windows - 1)).
+__device__ __forceinline__ int mask_windows(int64_t i, int64_t nwords, int64_t wwords) {
+    const int64_t used = (i + 63) / 64 < nwords ? (i + 63) / 64 : nwords;
+    return used <= wwords ? 1 : (int)((used + wwords - 1) / wwords);
+}
+
+__global__ void k_mask_wcount(const int32_t *__restrict__ list, int64_t nd, const int64_t *__restrict__ lrp,
+                              int64_t nwords, int64_t wwords, int32_t *__restrict__ ncut_e,
+                              int32_t *__restrict__ ncut) {
+    for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < nd; li += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = list[li];
+        const int nwin = mask_windows(i, nwords, wwords);
+        const int alen = (int)(lrp[i + 1] - lrp[i]);
+        ncut_e[li] = nwin > 1 ? alen : 0;
+        ncut[li] = nwin > 1 ? alen * (nwin - 1) : 0;
+    }
+}
+
+// Cut points: for entry j of a multi-window row, the offset into L_j's
+// (ascending) compressed sets of the first set of each later window.  A
+// thread per entry gallops window to window; independent threads hide the
+// dependent loads that a search inside the dense kernel's enumeration would
+// put in front of a block barrier.
+__global__ void __launch_bounds__(256) k_mask_cut(const int32_t *__restrict__ list, int64_t nd, MaskArgs a,
+                                                  int64_t nwords, int64_t wwords,
+                                                  const int64_t *__restrict__ eoff,
+                                                  const int64_t *__restrict__ coff, int64_t cut_base,
+                                                  int32_t *__restrict__ cut) {
+    const int64_t e0 = eoff[0], tot = eoff[nd] - e0;
+    for (int64_t x = (int64_t)blockIdx.x * 256 + threadIdx.x; x < tot; x += (int64_t)gridDim.x * 256) {
+        int64_t lo = 0, hi = nd - 1;   // last row with eoff - e0 <= x
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (eoff[mid] - e0 <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t li = lo;
+        const int64_t e = x - (eoff[li] - e0);
+        const int64_t alen = eoff[li + 1] - eoff[li];
+        const int64_t i = list[li];
+        const int nwin = mask_windows(i, nwords, wwords);
+        const int j = a.lcol[a.lrp[i] + e];
+        const int64_t st = a.cstart[j], en = st + a.ccnt[j];
+        int32_t *cr = cut + (coff[li] - cut_base) + e;
+        int64_t cur = st;
+        for (int w = 1; w < nwin; ++w) {
+            const int64_t lw = (int64_t)w * wwords;
+            int64_t step = 1, l2 = cur, h2 = cur;
+            while (h2 < en && a.cset[h2] < lw) {
+                l2 = h2 + 1;
+                h2 += step;
+                step <<= 1;
+            }
+            int64_t r = h2 < en ? h2 : en;
+            while (l2 < r) {
+                const int64_t mid = (l2 + r) >> 1;
+                if (a.cset[mid] < lw) l2 = mid + 1;
+                else r = mid;
+            }
+            cur = l2;
+            cr[(int64_t)(w - 1) * alen] = (int32_t)(cur - st);
+        }
+    }
 }
 
 template <int G, int SLICE>
@@ -323,7 +406,17 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     // dense tier: bitmap over all columns, in shared memory up to 200 KB,
     // else a per-CTA global slab (one SM's worth of CTAs, L2-resident)
     const int64_t nwords = (l->cols + 63) / 64;
-    const bool dense_smem = nwords * 8 <= 200 * 1024;
+    // shared-memory bitmap windows of up to 24576 sets (192 KB, 1.57 M
+    // columns); larger graphs take several windows per long row
+    // Windowed shared-memory bitmaps (TSG_MASK_WIN_WORDS sets per window,
+    // cut points from k_mask_cut) are opt-in: at R-MAT scale 22 three 192 KB
+    // windows ran 62.8 + 1.9 ms against 54.6 ms for the L2-resident per-CTA
+    // bitmap -- the tier is bound by re-reading the compressed L_j rows from
+    // DRAM, not by the bitmap lookups.
+    static const int64_t wcap = getenv("TSG_MASK_WIN_WORDS") ? atoll(getenv("TSG_MASK_WIN_WORDS")) : 0;
+    const int64_t wwords = wcap > 0 && nwords > wcap ? wcap : nwords;
+    // several windows need ascending compressed sets (row-sorted L)
+    const bool dense_smem = wwords * 8 <= 200 * 1024 && (wwords == nwords || cl->sorted_sets);
     const bool dense_ok = dense_smem || nwords * 8 * c->num_sms <= ((int64_t)1 << 30);
     TSG_TRY(tsg_partition<MB>(c, rows, MaskBinF{l->rp, dense_ok}, bins, bl));
     int32_t *list = bl.list;
@@ -353,15 +446,63 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
     if (nd > 0) {
         const unsigned ctas = (unsigned)(nd < c->num_sms ? nd : c->num_sms);
         if (dense_smem) {
-            const size_t smem = (size_t)nwords * 8;
+            const size_t smem = (size_t)wwords * 8;
             TSG_TRY(tsg_func_smem((const void *)k_mask_dense<1024, true>, smem));
-            k_mask_dense<1024, true><<<ctas, 1024, smem, c->stream>>>(list + off[MASK_DENSE], nd, a, nullptr,
-                                                                      nwords); ++c->launches;
+            const int32_t *dl = list + off[MASK_DENSE];
+            if (wwords == nwords) {
+                k_mask_dense<1024, true><<<ctas, 1024, smem, c->stream>>>(dl, nd, a, nullptr, nwords, wwords,
+                                                                          nullptr, 0, nullptr);
+                ++c->launches;
+            } else {
+                int32_t *ncut_e = nullptr, *ncut = nullptr;
+                int64_t *eoff = nullptr, *coff = nullptr;
+                TSG_TRY(tsg_alloc_t(c, &ncut_e, (size_t)nd));
+                TSG_TRY(tsg_alloc_t(c, &ncut, (size_t)nd));
+                TSG_TRY(tsg_alloc_t(c, &eoff, (size_t)nd + 1));
+                TSG_TRY(tsg_alloc_t(c, &coff, (size_t)nd + 1));
+                k_mask_wcount<<<grid_for(nd, 256, c->num_sms * 8), 256, 0, c->stream>>>(dl, nd, l->rp, nwords,
+                                                                                        wwords, ncut_e, ncut);
+                ++c->launches;
+                TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut_e, eoff, nd));
+                TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut, coff, nd));
+                // batches of rows whose cut points fit CUT_MAX entries
+                std::vector<int64_t> hc((size_t)nd + 1);
+                TSG_CK(cudaMemcpyAsync(hc.data(), coff, (nd + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                       c->stream));
+                TSG_CK(cudaStreamSynchronize(c->stream));
+                const int64_t CUT_MAX = (int64_t)256 << 20;
+                int32_t *cut = nullptr;
+                const int64_t cap = std::min<int64_t>(CUT_MAX, std::max<int64_t>(hc[nd], 1));
+                int64_t maxrow = 0;
+                for (int64_t r = 0; r < nd; ++r) maxrow = std::max(maxrow, hc[r + 1] - hc[r]);
+                TSG_TRY(tsg_alloc_t(c, &cut, (size_t)std::max(cap, maxrow)));
+                for (int64_t b0 = 0; b0 < nd;) {
+                    int64_t b1 = b0 + 1;
+                    while (b1 < nd && hc[b1 + 1] - hc[b0] <= cap) ++b1;
+                    const int64_t nb = b1 - b0;
+                    if (hc[b1] > hc[b0]) {
+                        k_mask_cut<<<grid_for(nb * 64, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+                            dl + b0, nb, a, nwords, wwords, eoff + b0, coff + b0, hc[b0], cut);
+                        ++c->launches;
+                    }
+                    k_mask_dense<1024, true><<<(unsigned)std::min<int64_t>(nb, c->num_sms), 1024, smem,
+                                               c->stream>>>(dl + b0, nb, a, nullptr, nwords, wwords, coff + b0,
+                                                            hc[b0], cut);
+                    ++c->launches;
+                    b0 = b1;
+                }
+                TSG_TRY(tsg_free(c, cut));
+                TSG_TRY(tsg_free(c, ncut_e));
+                TSG_TRY(tsg_free(c, ncut));
+                TSG_TRY(tsg_free(c, eoff));
+                TSG_TRY(tsg_free(c, coff));
+            }
         } else {
             TSG_TRY(tsg_alloc_t(c, &dslab, (size_t)ctas * nwords));
             TSG_TRY(tsg_fill(c, dslab, 0, (size_t)ctas * nwords * 8, c->stream));
             k_mask_dense<1024, false><<<ctas, 1024, 0, c->stream>>>(list + off[MASK_DENSE], nd, a, dslab,
-                                                                    nwords); ++c->launches;
+                                                                    nwords, nwords, nullptr, 0, nullptr);
+            ++c->launches;
         }
         TSG_CK(cudaGetLastError());
     }

@@ -129,3 +129,22 @@ def test_chunked_budget_physical_floor_and_capacity_error():
     # the reference's simulated residency check still raises for tiny budgets
     with pytest.raises(tsg.CapacityError):
         ch.execute_plan(a, a, counts, plan, b200_model(1 << 20))
+
+
+def test_config3_masked_count_small_windows():
+    # the dense tier's shared-memory bitmap in windows of 5 sets (320
+    # columns; env read once per process, so in a child): hub rows take
+    # dozens of windows; the count must still equal the golden one
+    import subprocess
+    import sys
+    code = ("import bench_configs as BC\n"
+            "from paper_1804_00695_b200 import _lib, generators as gen\n"
+            "from paper_1804_00695_b200.triangles import lower_triangle_device\n"
+            "dl, _ = lower_triangle_device(gen.rmat_graph_device(16))\n"
+            "assert _lib.d_masked_count(dl, _lib.d_compress(dl)) == BC.rmat_golden(16)['triangles']\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_MASK_WIN_WORDS="5", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
