@@ -262,6 +262,14 @@ constexpr int THREAD_MAX_A = 64;
 constexpr int DENSE_MIN_SETS = 2048;           // bound (sets) from which a row goes dense
 constexpr int64_t DENSE_SMEM = 200 * 1024;     // shared-memory budget of the dense kernels
 __host__ __device__ __forceinline__ int64_t dense_words(int64_t ncols) { return (ncols + 63) / 64; }
+// set bound from which a row takes the dense tier: 2048 while B's column-set
+// bitmap fits shared memory; beyond that the symbolic bitmap is an L2-resident
+// per-CTA slab whose emission scans all of B's sets, so rows must be long
+// enough to amortise that (R-MAT scale 21 without it: 132 s in the global tier)
+__host__ __device__ __forceinline__ int64_t dense_min_sets(int64_t ncols) {
+    const int64_t nw = dense_words(ncols);
+    return nw * 8 <= DENSE_SMEM ? DENSE_MIN_SETS : (nw / 8 > DENSE_MIN_SETS ? nw / 8 : DENSE_MIN_SETS);
+}
 
 __host__ __device__ __forceinline__ int64_t round16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
@@ -346,7 +354,7 @@ struct SymBinF {
             sb = sbound[i];
         }
         int b = sym_bin(sb);
-        if (ncols > 0 && sb >= DENSE_MIN_SETS && dense_words(ncols) * 8 <= DENSE_SMEM) {
+        if (ncols > 0 && sb >= dense_min_sets(ncols)) {
             scap[i] = sb;
             return BIN_DENSE;
         }
@@ -379,8 +387,7 @@ struct NumBinF {
         const int64_t n = counts[i];
         const int64_t m = msets ? (int64_t)(msets[i] & (SETS_WRITTEN - 1)) : (sbound[i] < n ? sbound[i] : n);
         const int b = num_bin(n, m);
-        if (ncols > 0 && b >= 7 && b != 255 && msets && (msets[i] & SETS_WRITTEN) &&
-            dense_words(ncols) * 12 <= DENSE_SMEM)
+        if (ncols > 0 && b >= 7 && b != 255 && msets && (msets[i] & SETS_WRITTEN))   // windowed: any B width
             return BIN_DENSE;
         return b;
     }
@@ -890,16 +897,10 @@ __global__ void __launch_bounds__(256) k_sym_merge3(const int32_t *__restrict__ 
 template <int M>
 int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 
-// The dense symbolic tier enumerates a warp per A entry (R-MAT scale 18:
-// 80 -> 72 ms; the masked count's dense tier: 146 -> 54 ms at scale 22).  The
-// dense numeric tier keeps the flattened enumeration: a warp per entry
-// pointed its fp64 atomics at neighbouring positions (112 -> 179 ms)
-#ifndef DENSE_ENUM
-#define DENSE_ENUM block_warp_enumerate
-#endif
-#ifndef DENSE_SYM_UNITS
-#define DENSE_SYM_UNITS 1
-#endif
+// The dense tiers enumerate through block_unit_enumerate (tsg_group.cuh):
+// R-MAT scale 18 symbolic 48 -> 44 ms over a warp per A entry (and 16 ms with
+// the popcount total fixed below), numeric 108 -> 80 ms over the flattened
+// block enumeration.
 #ifndef DENSE_EB
 #define DENSE_EB 512   // A entries per enumeration round (block_unit_enumerate)
 #endif
@@ -910,96 +911,173 @@ int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 // Dense symbolic tier: the row's union is ORed into a shared-memory bitmap
 // of all of B's column sets (64-bit words, ORed as 32-bit halves), then the
 // nonzero words are emitted in ascending set order -- no table, no sort.
-template <int NT>
+// MODE 0: one shared bitmap of all of B's column sets.  MODE 1 (B wider
+// than shared memory, row-sorted): the sets in column windows of `wwords`,
+// one window after another per row; each entry's compressed B row is cut to
+// the window by precomputed offsets (k_sym_dense_cut) and the emitted sets
+// and counts carry across windows.  MODE 2 (unsorted B wider than shared
+// memory): an L2-resident bitmap slab per CTA (zeroed by the host once,
+// re-zeroed as emitted), ORed with fire-and-forget global atomics and read
+// with L1-bypassing loads -- L2 atomic throughput bounds it (R-MAT scale 21:
+// 2.0 s against 132 s in the global hash tier).
+template <int NT, int MODE>
 __global__ void __launch_bounds__(NT, 2048 / NT) k_sym_dense(const int32_t *__restrict__ list, int64_t nlist,
-                                                  SymArgs a, int64_t nwords) {
+                                                  SymArgs a, int64_t nwords, int64_t wwords, uint64_t *gbm,
+                                                  const int64_t *__restrict__ coff, int64_t cut_base,
+                                                  const int32_t *__restrict__ cut) {
     extern __shared__ int4 smem[];
     __shared__ int s_warp[32];
     __shared__ unsigned s_cnt;
-    uint64_t *bm = reinterpret_cast<uint64_t *>(smem);
-    unsigned *bm32 = reinterpret_cast<unsigned *>(smem);
+    __shared__ int s_nz;
+    uint64_t *bm = MODE == 2 ? gbm + (int64_t)blockIdx.x * nwords : reinterpret_cast<uint64_t *>(smem);
+    unsigned *bm32 = reinterpret_cast<unsigned *>(bm);
+    const int64_t ww = MODE == 1 ? wwords : nwords;   // words per window
+    const int nwin = MODE == 1 ? (int)((nwords + wwords - 1) / wwords) : 1;
     for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
         const int64_t i = list[li];
         const int64_t gi = i + a.a_row_off;
-        for (int64_t w = threadIdx.x; w < nwords; w += NT) bm[w] = 0ull;
-        if (threadIdx.x == 0) s_cnt = 0u;
-        __syncthreads();
-#if DENSE_SYM_UNITS
-        struct SB {
-            int set;
-            uint64_t bits;
-        };
-        block_unit_enumerate<NT, DENSE_EB, DENSE_CH, SB>(
-            a.arp[gi], a.arp[gi + 1],
-            [&](int64_t t, int64_t &st, int &len, double &) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    st = a.cbstart[k];
-                    len = a.cbcnt[k];
-                }
-            },
-            [&](int64_t sidx) { return SB{a.cbset[sidx], a.cbbits[sidx]}; },
-            [&](double, const SB &x) {
-                if ((unsigned)x.bits) atomicOr(&bm32[2 * x.set], (unsigned)x.bits);
-                if ((unsigned)(x.bits >> 32)) atomicOr(&bm32[2 * x.set + 1], (unsigned)(x.bits >> 32));
-            },
-            s_warp);
-        __syncthreads();
-#else
-        DENSE_ENUM<NT>(
-            a.arp[gi], a.arp[gi + 1],
-            [&](int64_t t, int64_t &st, int &len) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    st = a.cbstart[k];
-                    len = a.cbcnt[k];
-                }
-            },
-            [&](int64_t, int64_t sidx) {
-                const int set = a.cbset[sidx];
-                const uint64_t bits = a.cbbits[sidx];
-                if ((unsigned)bits) atomicOr(&bm32[2 * set], (unsigned)bits);
-                if ((unsigned)(bits >> 32)) atomicOr(&bm32[2 * set + 1], (unsigned)(bits >> 32));
-            });
-#endif
-        __syncthreads();
-        // each thread owns a contiguous run of words: count its nonzero sets,
-        // block-scan the counts, emit its sets in order
-        const int64_t per = (nwords + NT - 1) / NT;
-        const int64_t w0 = threadIdx.x * per, w1 = w0 + per < nwords ? w0 + per : nwords;
-        int nz = 0;
-        unsigned pc = 0;
-        for (int64_t w = w0; w < w1; ++w) {
-            const uint64_t x = bm[w];
-            nz += x != 0ull;
-            pc += __popcll(x);
+        const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
+        if (threadIdx.x == 0) {
+            s_cnt = 0u;
+            s_nz = 0;
         }
-        // one native 32-bit add per warp (a 64-bit add per thread was a CAS
-        // spin on one word: half of the kernel's stall samples)
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, d);
-        if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, pc);
-        int tot;
-        int r = block_excl_scan<NT>(nz, tot, s_warp);
-        if (a.oset) {
-            const int64_t sp = a.sptr[i];
+        const int64_t sp = a.oset ? a.sptr[i] : 0;
+        for (int win = 0; win < nwin; ++win) {
+            const int64_t lo = (int64_t)win * ww;
+            const int64_t wn = nwords - lo < ww ? nwords - lo : ww;   // words in this window
+            if (MODE != 2)
+                for (int64_t w = threadIdx.x; w < wn; w += NT) bm[w] = 0ull;
+            __syncthreads();
+            struct SB {
+                int set;
+                uint64_t bits;
+            };
+            block_unit_enumerate<NT, DENSE_EB, DENSE_CH, SB>(
+                a0, a1,
+                [&](int64_t t, int64_t &st, int &len, double &) {
+                    int k = a.acol[t];
+                    if (k >= a.b_lo && k < a.b_hi) {
+                        k -= a.b_lo;
+                        st = a.cbstart[k];
+                        len = a.cbcnt[k];
+                        if (MODE == 1) {
+                            const int64_t alen = a1 - a0;
+                            const int32_t *cr = cut + (coff[li] - cut_base) + (t - a0);
+                            const int c0 = win > 0 ? cr[(win - 1) * alen] : 0;
+                            const int c1 = win + 1 < nwin ? cr[win * alen] : len;
+                            st += c0;
+                            len = c1 - c0;
+                        }
+                    }
+                },
+                [&](int64_t sidx) { return SB{a.cbset[sidx], a.cbbits[sidx]}; },
+                [&](double, const SB &x) {
+                    const int64_t o = 2 * (x.set - lo);
+                    if ((unsigned)x.bits) atomicOr(&bm32[o], (unsigned)x.bits);
+                    if ((unsigned)(x.bits >> 32)) atomicOr(&bm32[o + 1], (unsigned)(x.bits >> 32));
+                },
+                s_warp);
+            __syncthreads();
+            // each thread owns a contiguous run of words: count its nonzero
+            // sets, block-scan the counts, emit its sets in order
+            const int64_t per = (wn + NT - 1) / NT;
+            const int64_t w0 = threadIdx.x * per, w1 = w0 + per < wn ? w0 + per : wn;
+            int nz = 0;
+            unsigned pc = 0;
             for (int64_t w = w0; w < w1; ++w) {
-                const uint64_t x = bm[w];
-                if (x) {
-                    a.oset[sp + r] = (int32_t)w;
-                    a.obits[sp + r] = x;
-                    ++r;
+                const uint64_t x = MODE == 2 ? __ldcg(bm + w) : bm[w];
+                nz += x != 0ull;
+                pc += __popcll(x);
+            }
+            // one native 32-bit add per warp (a 64-bit add per thread was a
+            // CAS spin on one word: half of the kernel's stall samples)
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, d);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, pc);
+            int tot;
+            int r = s_nz + block_excl_scan<NT>(nz, tot, s_warp);
+            if (a.oset || MODE == 2) {
+                for (int64_t w = w0; w < w1; ++w) {
+                    const uint64_t x = MODE == 2 ? __ldcg(bm + w) : bm[w];
+                    if (x) {
+                        if (a.oset) {
+                            a.oset[sp + r] = (int32_t)(lo + w);
+                            a.obits[sp + r] = x;
+                            ++r;
+                        }
+                        if (MODE == 2) __stcg(bm + w, 0ull);
+                    }
                 }
             }
+            __syncthreads();
+            if (threadIdx.x == 0) s_nz += tot;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             a.counts[i] = (int64_t)s_cnt;
-            if (a.msets) a.msets[i] = tot | (a.oset ? SETS_WRITTEN : 0);
+            if (a.msets) a.msets[i] = s_nz | (a.oset ? SETS_WRITTEN : 0);
         }
         __syncthreads();
+    }
+}
+
+// Cut points of the windowed symbolic dense tier: for every A entry of a
+// listed row, the offsets into its compressed B row (ascending sets) where
+// each later window starts (window-major per row, so the dense kernel's
+// entry lookups are coalesced).  A thread per entry gallops window to window.
+__global__ void __launch_bounds__(256) k_sym_dense_cut(const int32_t *__restrict__ list, int64_t nb, SymArgs a,
+                                                       int64_t wwords, int nwin,
+                                                       const int64_t *__restrict__ eoff,
+                                                       const int64_t *__restrict__ coff, int64_t cut_base,
+                                                       int32_t *__restrict__ cut) {
+    const int64_t e0 = eoff[0], tot = eoff[nb] - e0;
+    for (int64_t x = (int64_t)blockIdx.x * 256 + threadIdx.x; x < tot; x += (int64_t)gridDim.x * 256) {
+        int64_t lo = 0, hi = nb - 1;   // last row with eoff - e0 <= x
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (eoff[mid] - e0 <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t li = lo;
+        const int64_t e = x - (eoff[li] - e0);
+        const int64_t alen = eoff[li + 1] - eoff[li];
+        const int64_t gi = list[li] + a.a_row_off;
+        int32_t *cr = cut + (coff[li] - cut_base) + e;
+        int k = a.acol[a.arp[gi] + e];
+        if (k < a.b_lo || k >= a.b_hi) {
+            for (int w = 1; w < nwin; ++w) cr[(int64_t)(w - 1) * alen] = 0;
+            continue;
+        }
+        k -= a.b_lo;
+        const int64_t st = a.cbstart[k], en = st + a.cbcnt[k];
+        int64_t cur = st;
+        for (int w = 1; w < nwin; ++w) {
+            const int64_t lw = (int64_t)w * wwords;
+            int64_t step = 1, l2 = cur, h2 = cur;
+            while (h2 < en && a.cbset[h2] < lw) {
+                l2 = h2 + 1;
+                h2 += step;
+                step <<= 1;
+            }
+            int64_t r = h2 < en ? h2 : en;
+            while (l2 < r) {
+                const int64_t mid = (l2 + r) >> 1;
+                if (a.cbset[mid] < lw) l2 = mid + 1;
+                else r = mid;
+            }
+            cur = l2;
+            cr[(int64_t)(w - 1) * alen] = (int32_t)(cur - st);
+        }
+    }
+}
+
+__global__ void k_alen(const int32_t *__restrict__ list, int64_t n, const int64_t *__restrict__ arp,
+                       int64_t a_row_off, int mult, int32_t *__restrict__ ne, int32_t *__restrict__ nc) {
+    for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < n; li += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gi = list[li] + a_row_off;
+        const int alen = (int)(arp[gi + 1] - arp[gi]);
+        ne[li] = alen;
+        nc[li] = alen * mult;
     }
 }
 
@@ -2659,24 +2737,88 @@ static int dense_ctas_per_sm(size_t smem) {
     return k < 1 ? 1 : k;
 }
 
-int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols) {
-    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
-    const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
-    if (n <= 0) return TSG_OK;
-    const int64_t nw = dense_words(ncols);
-    const size_t smem = (size_t)nw * 8;
-    TSG_TRY(set_smem(k_sym_dense<1024>, smem));
-    k_sym_dense<1024><<<grid_for(n, 1, c->num_sms * dense_ctas_per_sm(smem)), 1024, smem, c->stream>>>(bl.list + bl.off[BIN_DENSE], n,
-                                                                             a, nw); ++c->launches;
-    TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid_for(n, 1, c->num_sms * dense_ctas_per_sm(smem)), 1024, smem));
-    return TSG_OK;
-}
-
-// windowed dense numeric: positions per window, CTAs per SM, map budget
+// dense-tier tuning knobs (environment, read once)
 static int dense_win_param(const char *name, int dflt) {
     const char *e = getenv(name);
     return e ? atoi(e) : dflt;
 }
+
+int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols, bool sorted_sets) {
+    if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
+    const int64_t n = bl.off[BIN_DENSE + 1] - bl.off[BIN_DENSE];
+    if (n <= 0) return TSG_OK;
+    const int64_t nw = dense_words(ncols);
+    const int32_t *dl = bl.list + bl.off[BIN_DENSE];
+    static const int64_t WW = dense_win_param("TSG_SYM_WIN_WORDS", 24576);
+    if (nw * 8 > DENSE_SMEM && sorted_sets && !getenv("TSG_SYM_DENSE_L2")) {
+        // windowed shared-memory bitmaps; cut points in batches of rows
+        const int64_t ww = nw < WW ? nw : WW;
+        const int nwin = (int)((nw + ww - 1) / ww);
+        const size_t smem = (size_t)ww * 8;
+        TSG_TRY(set_smem(k_sym_dense<1024, 1>, smem));
+        int32_t *ne = nullptr, *nc = nullptr;
+        int64_t *eoff = nullptr, *coff = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &ne, (size_t)n));
+        TSG_TRY(tsg_alloc_t(c, &nc, (size_t)n));
+        TSG_TRY(tsg_alloc_t(c, &eoff, (size_t)n + 1));
+        TSG_TRY(tsg_alloc_t(c, &coff, (size_t)n + 1));
+        k_alen<<<grid_for(n, 256, c->num_sms * 8), 256, 0, c->stream>>>(dl, n, a.arp, a.a_row_off, nwin - 1, ne,
+                                                                        nc);
+        ++c->launches;
+        TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ne, eoff, n));
+        TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nc, coff, n));
+        std::vector<int64_t> hc((size_t)n + 1);
+        TSG_CK(cudaMemcpyAsync(hc.data(), coff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        TSG_CK(cudaStreamSynchronize(c->stream));
+        const int64_t CUT_MAX = (int64_t)128 << 20;
+        int64_t maxrow = 1;
+        for (int64_t r = 0; r < n; ++r) maxrow = std::max(maxrow, hc[r + 1] - hc[r]);
+        const int64_t cap = std::max<int64_t>(std::min<int64_t>(CUT_MAX, hc[n]), maxrow);
+        int32_t *cut = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &cut, (size_t)cap));
+        for (int64_t b0 = 0; b0 < n;) {
+            int64_t b1 = b0 + 1;
+            while (b1 < n && hc[b1 + 1] - hc[b0] <= cap) ++b1;
+            const int64_t nb = b1 - b0;
+            k_sym_dense_cut<<<grid_for(nb * 256, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+                dl + b0, nb, a, ww, nwin, eoff + b0, coff + b0, hc[b0], cut);
+            ++c->launches;
+            const unsigned grid = (unsigned)std::min<int64_t>(nb, c->num_sms);
+            k_sym_dense<1024, 1><<<grid, 1024, smem, c->stream>>>(dl + b0, nb, a, nw, ww, nullptr, coff + b0, hc[b0],
+                                                                cut);
+            ++c->launches;
+            TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid, 1024, smem));
+            b0 = b1;
+        }
+        TSG_TRY(tsg_free(c, cut));
+        TSG_TRY(tsg_free(c, ne));
+        TSG_TRY(tsg_free(c, nc));
+        TSG_TRY(tsg_free(c, eoff));
+        TSG_TRY(tsg_free(c, coff));
+        return TSG_OK;
+    }
+    if (nw * 8 > DENSE_SMEM) {   // bitmap slabs in global memory (L2-resident)
+        int64_t ctas = 2 * c->num_sms;
+        while (ctas > c->num_sms / 2 && ctas * nw * 8 > ((int64_t)2 << 30)) ctas /= 2;
+        if (ctas > n) ctas = n;
+        uint64_t *gbm = nullptr;
+        TSG_TRY(tsg_alloc_t(c, &gbm, (size_t)(ctas * nw)));
+        TSG_TRY(tsg_fill(c, gbm, 0, (size_t)(ctas * nw) * 8, c->stream));
+        k_sym_dense<1024, 2><<<(unsigned)ctas, 1024, 0, c->stream>>>(dl, n, a, nw, nw, gbm, nullptr, 0, nullptr);
+        ++c->launches;
+        TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, (unsigned)ctas, 1024, 0));
+        TSG_TRY(tsg_free(c, gbm));
+        return TSG_OK;
+    }
+    const size_t smem = (size_t)nw * 8;
+    TSG_TRY(set_smem(k_sym_dense<1024, 0>, smem));
+    const unsigned grid = grid_for(n, 1, c->num_sms * dense_ctas_per_sm(smem));
+    k_sym_dense<1024, 0><<<grid, 1024, smem, c->stream>>>(dl, n, a, nw, nw, nullptr, nullptr, 0, nullptr);
+    ++c->launches;
+    TSG_TRY(tsg_launch_check("k_sym_dense", BIN_DENSE, grid, 1024, smem));
+    return TSG_OK;
+}
+
 
 int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols) {
     if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
@@ -2686,7 +2828,7 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
     static const int W = dense_win_param("TSG_DENSE_WIN", per_sm > 1 ? 8192 : 19456);
     static const int WS = dense_win_param("TSG_DENSE_WIN_SETS", per_sm > 1 ? 2048 : 4096);
     static const int old = dense_win_param("TSG_DENSE_FLAT", 0);
-    if (!old) {
+    if (!old || dense_words(ncols) * 12 > DENSE_SMEM) {
         const int64_t nw = dense_words(ncols);
         DenseWin dw;
         dw.W = W;
@@ -3076,7 +3218,7 @@ int tsg_symbolic_impl(tsg_ctx *c, int64_t rows_out, const tsg_csr *a, int64_t a_
         sa.unit_dense = cb->identity_rows;
         if (c->timing) cudaEventRecord(c->ev_sym[0], c->stream);
         TSG_TRY(run_symbolic_bins(c, bl, sa));
-        TSG_TRY(launch_sym_dense(c, bl, sa, cb_cols));
+        TSG_TRY(launch_sym_dense(c, bl, sa, cb_cols, cb->sorted_sets != 0));
         if (c->timing) cudaEventRecord(c->ev_sym[1], c->stream);
         TSG_TRY(tsg_free(c, bl.list));
         TSG_TRY(tsg_free(c, bl.dstart));

@@ -462,3 +462,51 @@ def test_dense_numeric_small_windows():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_dense_tiers_beyond_shared_memory(rng):
+    # B with 2.1 M columns: the symbolic bitmap (262 KB) exceeds shared memory,
+    # so hub rows take the L2-slab symbolic dense tier and the windowed numeric
+    # tier over a 33 K-set width; rows below the raised dense threshold take
+    # the CTA / global tiers
+    n, cols = 20000, 2_100_000
+    rows = [rng.choice(n, size=k, replace=False) for k in (5, 300, 2000, 6000)]
+    r = np.concatenate([np.full(len(x), i) for i, x in enumerate(rows)])
+    a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.uniform(0.1, 1, len(r)), len(rows), n)
+    bu = random_csr(rng, n, cols, 60)
+    b = canonicalize(bu)   # row-sorted: windowed shared-memory symbolic bitmaps
+    assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=False, rtol=1e-12)
+    bi = CsrMatrix(b.num_rows, b.num_cols, b.row_ptr, b.col_idx, np.round(b.values * 8))
+    ai = CsrMatrix(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, np.ones(a.nnz))
+    assert_same_product(tsg.multiply(ai, bi), O.multiply(ai, bi), exact=True)
+    # unsorted B: the L2-slab symbolic bitmap
+    assert_same_product(tsg.multiply(a, bu), O.multiply(a, bu), exact=False, rtol=1e-12)
+
+
+def test_dense_tiers_many_windows():
+    # the wide case with 3000-set symbolic windows and 1000-position numeric
+    # windows (env read once per process, so in a child): 11 symbolic windows
+    # per row, cut points at every boundary
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "import paper_1804_00695_b200 as tsg\n"
+        "from paper_1804_00695_b200.csr import CsrMatrix, canonicalize\n"
+        "from oracle import oracle as O\n"
+        "from conftest import assert_same_product, random_csr\n"
+        "rng = np.random.default_rng(11)\n"
+        "n, cols = 20000, 2_100_000\n"
+        "rows = [rng.choice(n, size=k, replace=False) for k in (5, 300, 2000, 6000)]\n"
+        "r = np.concatenate([np.full(len(x), i) for i, x in enumerate(rows)])\n"
+        "a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.uniform(0.1, 1, len(r)), len(rows), n)\n"
+        "b = canonicalize(random_csr(rng, n, cols, 60))\n"
+        "assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=False, rtol=1e-12)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_SYM_WIN_WORDS="3000", TSG_DENSE_WIN="1000",
+               PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
