@@ -313,14 +313,24 @@ static Arena *arena_of(tsg_ctx *c) {
     return a;
 }
 
-static size_t size_class(size_t bytes) {
+static size_t size_class(size_t bytes, bool coarse = false) {
     if (bytes <= 4096) return 4096;
     if (bytes <= (1u << 20)) {
         size_t p = 4096;
         while (p < bytes) p <<= 1;
         return p;
     }
-    return (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);   // 1 MiB granules
+    if (!coarse || bytes < ((size_t)1 << 30))
+        return (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);   // 1 MiB granules
+    // coarse (streamed tsg_mg_multiply), >= 1 GiB: four classes per octave
+    // (<= 25 % slack), so its varying C blocks land in a few sizes the cache
+    // reuses instead of forcing an out-of-memory trim and a multi-GB re-map
+    // (R-MAT scale 21: 17.3 -> 3.6 s).  Not for the chunked executors, whose
+    // HBM budget counts every byte.
+    size_t p = (size_t)1 << 30;
+    while (p * 2 <= bytes) p <<= 1;
+    const size_t q = p / 4;
+    return (bytes + q - 1) / q * q;
 }
 
 static const size_t ARENA_CACHE_LIMIT = (size_t)48 << 30;
@@ -329,14 +339,14 @@ int tsg_alloc(tsg_ctx *c, void **p, size_t bytes) {
     *p = nullptr;
     tsg_trace(c, "alloc", (int64_t)bytes);
     Arena *A = arena_of(c);
-    size_t cls = size_class(bytes);
+    size_t cls = size_class(bytes, c->coarse_alloc != 0);
     {
         std::lock_guard<std::mutex> g(A->mu);
         auto it = A->free_blocks.lower_bound(cls);
-        // best fit, <= 25% slack; blocks of >= 256 MiB take up to 2x (a
-        // streamed multiply's C blocks vary in size: a miss there re-maps
-        // tens of GB after an out-of-memory trim, ~0.25 s per block)
-        const size_t slack = cls >= ((size_t)256 << 20) ? cls : cls / 4;
+        // best fit, <= 25% slack; in coarse mode (streamed multiply) blocks of
+        // >= 256 MiB take up to 2x (its C blocks vary in size: a miss there
+        // re-maps tens of GB after an out-of-memory trim, ~0.25 s per block)
+        const size_t slack = c->coarse_alloc && cls >= ((size_t)256 << 20) ? cls : cls / 4;
         if (it != A->free_blocks.end() && it->first <= cls + slack) {
             *p = it->second;
             size_t got = it->first;
@@ -1304,8 +1314,10 @@ extern "C" int tsg_csr_free(tsg_ctx *c, tsg_csr *m) {
     }
     if (!m->borrowed) {
         tsg_free(c, m->rp);
-        tsg_free(c, m->col);
-        tsg_free(c, m->val);
+        if (!m->cv_borrowed) {
+            tsg_free(c, m->col);
+            tsg_free(c, m->val);
+        }
     }
     delete m;
     return TSG_OK;

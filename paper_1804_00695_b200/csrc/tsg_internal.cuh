@@ -72,6 +72,12 @@ struct tsg_ctx {
                               // previous piece waits for its conversion (chunked)
     int64_t launches;         // kernels launched by this context (all entry points)
     double mg_ratio = 0.0;    // streamed tsg_mg_multiply: last C entries per multiplication
+    int coarse_alloc = 0;     // > 0: arena size classes of >= 1 GiB are coarse (streamed multiply)
+    // streamed multiply: one col / val reservoir per call that every block's
+    // C uses when it fits (no per-block multi-GB allocations)
+    int32_t *c_res_col = nullptr;
+    double *c_res_val = nullptr;
+    int64_t c_res_cap = 0;
     cudaEvent_t ev_num[2];    // around the numeric kernels of the last multiply
     cudaEvent_t ev_sym[2];    // around the symbolic kernels of the last multiply
     cudaEvent_t ev_user[8];   // tsg_event_record slots
@@ -106,6 +112,7 @@ struct tsg_csr {
     int distinct;      // 1: no column repeats within a row (lane-split numeric mode is race-free)
     int64_t max_row;   // longest row, or -1 if unknown
     int borrowed;      // arrays owned by the caller (tsg_csr_view): free releases only the handle
+    int cv_borrowed;   // col / val are the context's C reservoir (streamed multiply): not freed
     // A product of a device-driven multiply: the host never waited for it,
     // so `nnz` is the allocation bound and the exact count is rp[rows] on the
     // device, read on first need (tsg_csr_resolve).  max_row_bound (> 0) is

@@ -347,6 +347,27 @@ extern "C" int tsg_mg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, i
         // (R-MAT A*A: ~3 per entry): each block is sized by the largest
         // entries-per-multiplication ratio seen so far (x 1.25), starting at 1
         const int64_t cap_entries = std::max<int64_t>(c_budget_bytes / 16, 1);
+        struct Coarse {   // coarse arena classes for the blocks' varying scratch sizes
+            tsg_ctx *c;
+            explicit Coarse(tsg_ctx *x) : c(x) { ++c->coarse_alloc; }
+            ~Coarse() { --c->coarse_alloc; }
+        } coarse(c);
+        // one C reservoir of cap_entries for every block (same size every
+        // call, so the arena hands the same two blocks back)
+        struct Reservoir {
+            tsg_ctx *c;
+            explicit Reservoir(tsg_ctx *x) : c(x) {}
+            ~Reservoir() {
+                tsg_free(c, c->c_res_col);
+                tsg_free(c, c->c_res_val);
+                c->c_res_col = nullptr;
+                c->c_res_val = nullptr;
+                c->c_res_cap = 0;
+            }
+        } reservoir(c);
+        if (tsg_alloc_t(c, &c->c_res_col, (size_t)cap_entries) == TSG_OK &&
+            tsg_alloc_t(c, &c->c_res_val, (size_t)cap_entries) == TSG_OK)
+            c->c_res_cap = cap_entries;
         // the last call's ratio (same B, similar A blocks): the first block
         // is sized like the rest, so the arena reuses its C blocks
         double ratio = c->mg_ratio > 0 ? c->mg_ratio : 1.0;

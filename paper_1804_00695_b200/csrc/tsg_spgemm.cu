@@ -3316,8 +3316,15 @@ int tsg_numeric_impl(tsg_ctx *c, int64_t rows_out, int64_t cols_out, const tsg_c
         C->rp = cptr;
         C->col = nullptr;
         C->val = nullptr;
-        int st = tsg_alloc_t(c, &C->col, nnz);
-        if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, nnz);
+        int st = TSG_OK;
+        if (c->c_res_col && nnz <= c->c_res_cap) {   // streamed multiply's reservoir
+            C->col = c->c_res_col;
+            C->val = c->c_res_val;
+            C->cv_borrowed = 1;
+        } else {
+            st = tsg_alloc_t(c, &C->col, nnz);
+            if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, nnz);
+        }
         if (st != TSG_OK) {
             tsg_csr_free(c, C);
             return st;
