@@ -413,9 +413,18 @@ int tsg_free(tsg_ctx *c, void *p) {
     size_t cls = it->second;
     A->live.erase(it);
     c->bytes_in_use -= (int64_t)cls;
-    if (A->cached + cls > ARENA_CACHE_LIMIT) {
+    if (cls > ARENA_CACHE_LIMIT) {
         TSG_CK(cudaFreeAsync(p, c->stream));
         return TSG_OK;
+    }
+    // over the limit: evict the largest cached blocks, keep the one just
+    // freed (a workload's own blocks come back next call; stale ones from an
+    // earlier workload otherwise pin the cache and force re-maps)
+    while (A->cached + cls > ARENA_CACHE_LIMIT && !A->free_blocks.empty()) {
+        auto last = std::prev(A->free_blocks.end());
+        TSG_CK(cudaFreeAsync(last->second, c->stream));
+        A->cached -= last->first;
+        A->free_blocks.erase(last);
     }
     A->free_blocks.emplace(cls, p);
     A->cached += cls;
