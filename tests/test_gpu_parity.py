@@ -510,3 +510,15 @@ def test_dense_tiers_many_windows():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_global_tier_size_classes(rng):
+    # B 134 M columns wide: the dense threshold rises to B's words / 8 (262 K
+    # sets), so rows of 12 K .. 100 K sets take the global-memory tier, split
+    # into table-size classes (2^15, 2^17, 2^19 slots) with their own slabs
+    n, cols = 20000, 1 << 27
+    rows = [rng.choice(n, size=k, replace=False) for k in (3, 400, 1700, 3400)]
+    r = np.concatenate([np.full(len(x), i) for i, x in enumerate(rows)])
+    a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.uniform(0.1, 1, len(r)), len(rows), n)
+    b = random_csr(rng, n, cols, 60)
+    assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=False, rtol=1e-12)
