@@ -42,6 +42,9 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef DENSE_UNITS
 #define DENSE_UNITS 1
 #endif
+#ifndef MASK_RAW
+#define MASK_RAW 1
+#endif
 
 __device__ __forceinline__ int mask_bin(int64_t len, bool dense_ok) {
     if (len <= 0) return 255;
@@ -100,7 +103,23 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
             }
             if (win == 0 && !lower) kerr(a.err, KERR_NOTLOWER, i);
             __syncthreads();
-            if (DENSE_UNITS) {
+            if (MASK_RAW && nwin == 1) {
+                // L_j's raw columns (4 B each) tested against the bitmap
+                // instead of its compressed sets (12 B each, 0.64 sets per
+                // column at R-MAT scale 20): the tier is bound by re-reading
+                // L_j rows from DRAM, and the sum of bit(c) over a row's
+                // distinct columns equals the sum of popcount(bits & word)
+                block_unit_enumerate<NT, 512, 128, int>(
+                    r0, r1,
+                    [&](int64_t t, int64_t &st, int &len, double &) {
+                        const int j = a.lcol[t];
+                        st = a.lrp[j];
+                        len = (int)(a.lrp[j + 1] - st);
+                    },
+                    [&](int64_t s) { return a.lcol[s]; },
+                    [&](double, const int &c) { mine += (long long)((bm[c >> 6] >> (c & 63)) & 1ull); },
+                    s_warp);
+            } else if (DENSE_UNITS) {
                 // units of DENSE_CH compressed sets of one L_j, balanced over
                 // the warps (a warp per whole entry left the block waiting on
                 // the one walking a hub's row), CH/32 loads per lane in flight
