@@ -1075,12 +1075,12 @@ __global__ void __launch_bounds__(256) k_sym_dense_cut(const int32_t *__restrict
 }
 
 __global__ void k_alen(const int32_t *__restrict__ list, int64_t n, const int64_t *__restrict__ arp,
-                       int64_t a_row_off, int mult, int32_t *__restrict__ ne, int32_t *__restrict__ nc) {
+                       int64_t a_row_off, int mult, int32_t *__restrict__ ne, int64_t *__restrict__ nc) {
     for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < n; li += (int64_t)gridDim.x * blockDim.x) {
         const int64_t gi = list[li] + a_row_off;
         const int alen = (int)(arp[gi + 1] - arp[gi]);
         ne[li] = alen;
-        nc[li] = alen * mult;
+        nc[li] = (int64_t)alen * mult;
     }
 }
 
@@ -1880,7 +1880,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_num_dense_prep(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
                                                        DenseWin dw, int32_t *__restrict__ nwin,
                                                        int2 *__restrict__ wst, int32_t *__restrict__ ncut_e,
-                                                       int32_t *__restrict__ ncut) {
+                                                       int64_t *__restrict__ ncut) {
     __shared__ int s_warp[32];
     for (int64_t li = blockIdx.x; li < nb; li += gridDim.x) {
         const int64_t i = list[li];
@@ -1923,7 +1923,7 @@ __global__ void __launch_bounds__(NT) k_num_dense_prep(const int32_t *__restrict
             const int64_t gi = i + a.a_row_off;
             const int alen = (int)(a.arp[gi + 1] - a.arp[gi]);
             ncut_e[li] = ok && nstart > 1 ? alen : 0;
-            ncut[li] = ok && nstart > 1 ? alen * (nstart - 1) : 0;
+            ncut[li] = ok && nstart > 1 ? (int64_t)alen * (nstart - 1) : 0;
         }
         __syncthreads();
     }
@@ -2759,7 +2759,8 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
         const int nwin = (int)((nw + ww - 1) / ww);
         const size_t smem = (size_t)ww * 8;
         TSG_TRY(set_smem(k_sym_dense<1024, 1>, smem));
-        int32_t *ne = nullptr, *nc = nullptr;
+        int32_t *ne = nullptr;
+        int64_t *nc = nullptr;
         int64_t *eoff = nullptr, *coff = nullptr;
         TSG_TRY(tsg_alloc_t(c, &ne, (size_t)n));
         TSG_TRY(tsg_alloc_t(c, &nc, (size_t)n));
@@ -2769,7 +2770,7 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
                                                                         nc);
         ++c->launches;
         TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ne, eoff, n));
-        TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nc, coff, n));
+        TSG_TRY(tsg_exclusive_scan_i64(c, nc, coff, n));
         std::vector<int64_t> hc((size_t)n + 1);
         TSG_CK(cudaMemcpyAsync(hc.data(), coff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
         TSG_CK(cudaStreamSynchronize(c->stream));
@@ -2840,7 +2841,8 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
         int64_t batch = ((int64_t)64 << 20) / (dw.maxw * 8);
         if (batch < 1) batch = 1;
         if (batch > n) batch = n;
-        int32_t *nwin = nullptr, *ncut_e = nullptr, *ncut = nullptr;
+        int32_t *nwin = nullptr, *ncut_e = nullptr;
+        int64_t *ncut = nullptr;
         int64_t *woff = nullptr, *eoff = nullptr, *coff = nullptr;
         int2 *wst = nullptr;
         TSG_TRY(tsg_alloc_t(c, &nwin, (size_t)batch));
@@ -2861,7 +2863,7 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
             ++c->launches;
             TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nwin, woff, nb));
             TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut_e, eoff, nb));
-            TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, ncut, coff, nb));
+            TSG_TRY(tsg_exclusive_scan_i64(c, ncut, coff, nb));
             TSG_TRY(tsg_put_small(c, coff + nb, 1, 2));
             TSG_TRY(tsg_put_small(c, eoff + nb, 1, 3));
             TSG_CK(cudaStreamSynchronize(c->stream));
