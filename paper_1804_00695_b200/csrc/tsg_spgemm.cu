@@ -1980,22 +1980,6 @@ __global__ void __launch_bounds__(256) k_num_dense_cut(const int32_t *__restrict
     }
 }
 
-#ifndef DENSE_U
-#define DENSE_U 4
-#endif
-#ifndef DENSE_FLATTEN
-#define DENSE_FLATTEN 0
-#endif
-#ifndef DENSE_NO_CCOL
-#define DENSE_NO_CCOL 0   // timing experiments only
-#endif
-#ifndef DENSE_CCOL_WARP
-#define DENSE_CCOL_WARP 0   // 1: warp per set (R-MAT 18: 68 -> 90 ms)
-#endif
-#ifndef DENSE_NO_ACC
-#define DENSE_NO_ACC 0    // timing experiments only
-#endif
-
 template <int NT>
 __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict__ list, int64_t nb, NumArgs a,
                                                       DenseWin dw, const int64_t *__restrict__ woff,
@@ -2009,7 +1993,6 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
     double *acc = reinterpret_cast<double *>(sbase + dw.sets + (dw.sets & 1));
     __shared__ int64_t s_item;
     __shared__ int s_warp[32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t total = woff[nb];
     for (;;) {
         if (threadIdx.x == 0) s_item = (int64_t)atomicAdd(counter, 1ull);
@@ -2035,8 +2018,6 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
         else w1 = make_int2(a.msets[i] & (SETS_WRITTEN - 1), (int)a.counts[i]);
         const int P0 = w0.y, len = w1.y - w0.y;
         const int blk = a.sset[sp + w0.x] / dw.sets * dw.sets;
-        const int c_lo = nw > 1 ? a.sset[sp + w0.x] * 64 : INT_MIN;
-        const int c_hi = j + 1 < nw ? a.sset[sp + w1.x] * 64 : INT_MAX;
         // the window's (mask, base) map and columns
         int carry = P0;
         for (int q0 = w0.x; q0 < w1.x; q0 += NT) {
@@ -2053,94 +2034,19 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
             if (q < w1.x) {
                 smask[set - blk] = bits;
                 sbase[set - blk] = b - P0;
-#if !DENSE_NO_CCOL && !DENSE_CCOL_WARP
                 uint64_t y = bits;
                 int64_t r = cp + b;
                 while (y) {
                     a.ccol[r++] = set * 64 + (__ffsll((long long)y) - 1);
                     y &= y - 1;
                 }
-#endif
             }
             carry += tot;
             __syncthreads();
         }
         for (int q = threadIdx.x; q < len; q += NT) acc[q] = -0.0;
-#if DENSE_CCOL_WARP
-        // the window's columns: a warp per set, a lane per bit (coalesced
-        // stores; a thread per set looped over its bits with scattered stores)
-        for (int q = w0.x + wid; q < w1.x; q += NT / 32) {
-            const int set = a.sset[sp + q];
-            const uint64_t mk = smask[set - blk];
-            const int bs = sbase[set - blk];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int bit = h * 32 + lane;
-                if ((mk >> bit) & 1ull)
-                    a.ccol[cp + P0 + bs + __popcll(mk & ((1ull << bit) - 1ull))] = set * 64 + bit;
-            }
-        }
-#endif
         __syncthreads();
         const int64_t a0 = a.arp[gi], a1 = a.arp[gi + 1];
-#if DENSE_FLATTEN
-        // a warp takes 32 A entries at a time (their row / range lookups in
-        // flight together), then walks their flattened products DENSE_U per
-        // lane per round with every B load issued before the adds
-        for (int64_t tb = a0 + wid * 32; tb < a1; tb += NT) {
-            const int64_t t = tb + lane;
-            int64_t s0 = 0;
-            int ln = 0;
-            double av = 0.0;
-            if (t < a1) {
-                int k = a.acol[t];
-                if (k >= a.b_lo && k < a.b_hi) {
-                    k -= a.b_lo;
-                    s0 = a.brp[k];
-                    int64_t s1 = a.brp[k + 1];
-                    if (nw > 1) {
-                        s0 = lower_col(a.bcol, s0, s1, c_lo);
-                        s1 = lower_col(a.bcol, s0, s1, c_hi);
-                    }
-                    ln = (int)(s1 - s0);
-                    av = a.aval[t];
-                }
-            }
-            int incl = ln;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += o;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
-            const int64_t sx = s0 - (incl - ln);   // s of product p of this entry = sx + p
-            for (int p0 = 0; p0 < total; p0 += 32 * DENSE_U) {
-                int cc[DENSE_U];
-                double pv[DENSE_U];
-#pragma unroll
-                for (int u = 0; u < DENSE_U; ++u) {
-                    const int p = p0 + u * 32 + lane;
-                    int e = 0;   // entry of product p: lanes with incl <= p
-#pragma unroll
-                    for (int st = 16; st >= 1; st >>= 1)
-                        if (__shfl_sync(0xffffffffu, incl, e + st - 1) <= p) e += st;
-                    const int64_t s = __shfl_sync(0xffffffffu, sx, e & 31) + p;
-                    const double ae = __shfl_sync(0xffffffffu, av, e & 31);
-                    cc[u] = p < total ? a.bcol[s] : -1;
-                    pv[u] = p < total ? __dmul_rn(ae, a.bval[s]) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < DENSE_U; ++u) {
-                    if (cc[u] < 0) continue;
-                    const int c = cc[u];
-                    const int w = (c >> 6) - blk;
-                    const int bit = c & 63;
-                    const int pos = sbase[w] + __popcll(smask[w] & ((1ull << bit) - 1ull));
-                    atomicAdd(&acc[pos], pv[u]);
-                }
-            }
-        }
-#else
         // products in units of DENSE_CH of one B row (block_unit_enumerate)
         struct BV {
             int c;
@@ -2170,14 +2076,9 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
                 const int w = (x.c >> 6) - blk;
                 const int bit = x.c & 63;
                 const int pos = sbase[w] + __popcll(smask[w] & ((1ull << bit) - 1ull));
-#if DENSE_NO_ACC
-                if (__dmul_rn(av, x.v) == 12345.678) acc[pos] = 1.0;
-#else
                 atomicAdd(&acc[pos], __dmul_rn(av, x.v));
-#endif
             },
             s_warp);
-#endif
         __syncthreads();
         for (int q = threadIdx.x; q < len; q += NT) a.cval[cp + P0 + q] = acc[q];
         __syncthreads();
