@@ -45,6 +45,14 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef MASK_RAW
 #define MASK_RAW 1
 #endif
+// L2-slab dense tier shape, R-MAT scale 22: 1024 x 1 per SM 49.6 ms, 512 x 2
+// 64.8, 512 x 3 62.0, 256 x 4 96.7, 256 x 6 103.2
+#ifndef MASK_SLAB_NT
+#define MASK_SLAB_NT 1024
+#endif
+#ifndef MASK_SLAB_CTAS
+#define MASK_SLAB_CTAS 1
+#endif
 
 __device__ __forceinline__ int mask_bin(int64_t len, bool dense_ok) {
     if (len <= 0) return 255;
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
                 // column at R-MAT scale 20): the tier is bound by re-reading
                 // L_j rows from DRAM, and the sum of bit(c) over a row's
                 // distinct columns equals the sum of popcount(bits & word)
-                block_unit_enumerate<NT, 512, 128, int>(
+                block_unit_enumerate<NT, (NT < 512 ? NT : 512), 128, int>(
                     r0, r1,
                     [&](int64_t t, int64_t &st, int &len, double &) {
                         const int j = a.lcol[t];
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
                     int set;
                     uint64_t bits;
                 };
-                block_unit_enumerate<NT, 512, 128, CS>(
+                block_unit_enumerate<NT, (NT < 512 ? NT : 512), 128, CS>(
                     r0, r1,
                     [&](int64_t t, int64_t &st, int &len, double &) {
                         const int j = a.lcol[t];
@@ -517,10 +525,12 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
                 TSG_TRY(tsg_free(c, coff));
             }
         } else {
-            TSG_TRY(tsg_alloc_t(c, &dslab, (size_t)ctas * nwords));
-            TSG_TRY(tsg_fill(c, dslab, 0, (size_t)ctas * nwords * 8, c->stream));
-            k_mask_dense<1024, false><<<ctas, 1024, 0, c->stream>>>(list + off[MASK_DENSE], nd, a, dslab,
-                                                                    nwords, nwords, nullptr, 0, nullptr);
+            // L2-slab bitmaps: MASK_SLAB_NT threads per CTA, MASK_SLAB_CTAS per SM
+            const unsigned gs = (unsigned)std::min<int64_t>(nd, (int64_t)c->num_sms * MASK_SLAB_CTAS);
+            TSG_TRY(tsg_alloc_t(c, &dslab, (size_t)gs * nwords));
+            TSG_TRY(tsg_fill(c, dslab, 0, (size_t)gs * nwords * 8, c->stream));
+            k_mask_dense<MASK_SLAB_NT, false><<<gs, MASK_SLAB_NT, 0, c->stream>>>(
+                list + off[MASK_DENSE], nd, a, dslab, nwords, nwords, nullptr, 0, nullptr);
             ++c->launches;
         }
         TSG_CK(cudaGetLastError());
