@@ -269,7 +269,7 @@ Timeline g_tl;
 // staging.  No kernel is ever queued on the copy stream (a kernel queued
 // behind a bulk copy was measured to hold back kernels of other streams).
 int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d, cudaEvent_t wait_free,
-               bool sorted, bool distinct, int64_t &bytes) {
+               bool sorted, bool distinct, int64_t &bytes, bool one_stream = false) {
     const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
     TSG_TRY(ensure(c, d, rows, nnz));
     d.m.sorted = sorted ? 1 : 0;
@@ -278,7 +278,7 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     // alternate the two H2D streams: while this piece's values wait for the
     // column conversion, the next piece's columns are already on the link
     static thread_local unsigned flip = 0;
-    cudaStream_t s = (flip++ & 1) ? c->copy_in2 : c->copy_in, cs = c->convert;
+    cudaStream_t s = (!one_stream && (flip++ & 1)) ? c->copy_in2 : c->copy_in, cs = c->convert;
     if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
     cudaEvent_t tl0{}, tl1{}, tl2{};
     g_tl.begin(s, tl0);
@@ -308,6 +308,87 @@ int stage_rows(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d
     d.m.cols = h.cols;
     d.m.nnz = nnz;
     bytes += (rows + 1) * 8 + nnz * (h.val ? 16 : 8);
+    return TSG_OK;
+}
+
+// Resident-B upload in pieces (order 2 with one B chunk): the row pointers
+// first, then NP pieces of columns (narrowed on the convert stream) and
+// values in row order on one H2D stream, each piece's landing an event.  A/C
+// ranges whose largest column lies below a landed prefix run against that
+// prefix while the rest of B is still on the link, so the C drain (the
+// D2H-bound part of the order) starts ~1/NP of B's upload time after the
+// call instead of after all of it.  Results are identical: such a range's
+// products all come from the prefix rows, in the same order.
+struct BPieces {
+    std::vector<int64_t> q;          // piece row bounds, relative to the chunk's first row
+    std::vector<cudaEvent_t> ev;     // piece k landed (implies pieces < k)
+    int issued = 0;                  // pieces queued so far
+};
+
+int stage_b_begin(tsg_ctx *c, const HostCsr &h, int64_t lo, int64_t hi, DevRange &d, cudaEvent_t wait_free,
+                  bool sorted, bool distinct, int64_t &bytes, int np, BPieces &bp) {
+    const int64_t rows = hi - lo, e0 = h.rp[lo], e1 = h.rp[hi], nnz = e1 - e0;
+    TSG_TRY(ensure(c, d, rows, nnz));
+    d.m.sorted = sorted ? 1 : 0;
+    d.m.distinct = distinct ? 1 : 0;
+    d.m.max_row = host_max_row(h.rp, lo, hi);
+    cudaStream_t s = c->copy_in, cs = c->convert;
+    if (wait_free) TSG_CK(cudaStreamWaitEvent(s, wait_free, 0));
+    TSG_TRY(tsg_copy(d.stage_rp, h.rp + lo, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    TSG_CK(cudaEventRecord(d.cols_in, s));
+    TSG_CK(cudaStreamWaitEvent(cs, d.cols_in, 0));
+    k_rebase<<<grid_for(rows + 1, 256, c->num_sms * 8), 256, 0, cs>>>(d.stage_rp, d.m.rp, rows + 1, e0);
+    ++c->launches;
+    bp.q.assign(1, 0);
+    for (int k = 1; k < np; ++k) {   // pieces of near-equal entries, whole rows
+        const int64_t target = e0 + nnz * k / np;
+        const int64_t r = std::upper_bound(h.rp + lo, h.rp + hi + 1, target) - (h.rp + lo) - 1;
+        bp.q.push_back(std::max<int64_t>(bp.q.back(), std::min<int64_t>(r, rows)));
+    }
+    bp.q.push_back(rows);
+    bp.issued = 0;
+    d.m.rows = rows;
+    d.m.cols = h.cols;
+    d.m.nnz = nnz;
+    bytes += (rows + 1) * 8 + nnz * (h.val ? 16 : 8);
+    return TSG_OK;
+}
+
+// queue pieces up to k (in order, on the copy-in stream: the A ranges share
+// that FIFO, so each lands right after the B rows it needs)
+int stage_b_upto(tsg_ctx *c, const HostCsr &h, int64_t lo, DevRange &d, int k, BPieces &bp) {
+    const int64_t e0 = h.rp[lo];
+    cudaStream_t s = c->copy_in, cs = c->convert;
+    int64_t *col64 = reinterpret_cast<int64_t *>(d.m.val);
+    for (; bp.issued <= k; ++bp.issued) {
+        const int p = bp.issued;
+        const int64_t p0 = h.rp[lo + bp.q[p]] - e0, p1 = h.rp[lo + bp.q[p + 1]] - e0, n = p1 - p0;
+        cudaEvent_t ev;
+        TSG_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        bp.ev.push_back(ev);
+        if (n > 0) {
+            cudaEvent_t tl0{}, tl1{};
+            g_tl.begin(s, tl0);
+            TSG_TRY(tsg_copy(col64 + p0, h.col + e0 + p0, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            g_tl.end('c', s, tl0);
+            TSG_CK(cudaEventRecord(d.cols_in, s));
+            TSG_CK(cudaStreamWaitEvent(cs, d.cols_in, 0));
+            k_narrow<<<grid_for(n, 256, c->num_sms * 16), 256, 0, cs>>>(col64 + p0, d.m.col + p0, n, h.cols,
+                                                                         c->d_err);
+            ++c->launches;
+            TSG_CK(cudaGetLastError());
+            TSG_CK(cudaEventRecord(d.conv, cs));
+            TSG_CK(cudaStreamWaitEvent(s, d.conv, 0));
+            g_tl.begin(s, tl1);
+            if (h.val) TSG_TRY(tsg_copy(d.m.val + p0, h.val + e0 + p0, n * sizeof(double), cudaMemcpyHostToDevice, s));
+            g_tl.end('v', s, tl1);
+        } else {
+            TSG_CK(cudaEventRecord(d.conv, cs));   // the row pointers' rebase
+            TSG_CK(cudaStreamWaitEvent(s, d.conv, 0));
+        }
+        TSG_CK(cudaEventRecord(ev, s));
+        if (p == (int)bp.q.size() - 2) TSG_CK(cudaEventRecord(d.ready, s));
+    }
     return TSG_OK;
 }
 
@@ -598,13 +679,19 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
     auto hms = [&]() {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     };
-    host_row_order(J.A, &a_sorted, &a_distinct);
-    if (J.B.rp == J.A.rp && J.B.col == J.A.col && J.B.rows == J.A.rows) {   // A * A: one pass
-        b_sorted = a_sorted;
-        b_distinct = a_distinct;
-    } else {
-        host_row_order(J.B, &b_sorted, &b_distinct);
-    }
+    auto row_orders = [&]() {
+        host_row_order(J.A, &a_sorted, &a_distinct);
+        if (J.B.rp == J.A.rp && J.B.col == J.A.col && J.B.rows == J.A.rows) {   // A * A: one pass
+            b_sorted = a_sorted;
+            b_distinct = a_distinct;
+        } else {
+            host_row_order(J.B, &b_sorted, &b_distinct);
+        }
+    };
+    // (before any copy: in a thread beside order 2's first B pieces the scan
+    // competed with the DMA for host-memory bandwidth -- one run in three
+    // took 1.06 s instead of 0.79-0.81)
+    row_orders();
     if (g_tl.on) fprintf(stderr, "[tsg host] row order %.1f ms\n", hms());
     int64_t whole[2] = {0, a_rows};
     const int64_t *acb0 = algo == 0 ? whole : ac_bounds;
@@ -737,11 +824,30 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         // later B chunk reloads them; a single resident chunk finishes every
         // range in one step, checked on the device like order 1
         const bool partials = nb > 1;
+        // one resident B chunk and row-sorted A: B lands in pieces and the
+        // early A/C ranges start on its landed prefix (stage_b_pieces)
+        // opt-in (TSG_CHUNK_OVERLAP=1): config 4 at 16 GiB ran 0.79-0.81 s
+        // against 0.87-0.88 s, but the prefix compressions allocate blocks of
+        // a new size per prefix, and one run in four grew the pool while
+        // copies were in flight (2.69 s)
+        static const bool overlap_on = getenv("TSG_CHUNK_OVERLAP") != nullptr;
+        const bool overlap = !partials && nac > 1 && overlap_on;
+        const int NP = 8;
+        BPieces bp;
         for (int64_t j = 0; j < nb && st == TSG_OK; ++j) {
             DevRange &B = Bbuf[j % L.b_slots];
-            if ((st = stage_rows(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], b_sorted, b_distinct,
-                                 local.h2d_bytes)) != TSG_OK)
-                break;
+            if (overlap) {
+                // B's row pointers and first two pieces go on the link at once
+                st = stage_b_begin(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], false, false,
+                                   local.h2d_bytes, NP, bp);
+                if (st == TSG_OK) st = stage_b_upto(c, J.B, bb[j], B, 1, bp);
+                B.m.sorted = b_sorted ? 1 : 0;
+                B.m.distinct = b_distinct ? 1 : 0;
+            } else {
+                st = stage_rows(c, J.B, bb[j], bb[j + 1], B, used[j % L.b_slots], b_sorted, b_distinct,
+                                local.h2d_bytes);
+            }
+            if (st != TSG_OK) break;
             if (j == 0 && partials) {   // allocated while the first chunk is on the link
                 void *ph = nullptr;
                 TSG_TRY(tsg_host_alloc(((size_t)a_rows + 1) * sizeof(int32_t), &ph));
@@ -749,23 +855,63 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 memset(plen_host, 0, ((size_t)a_rows + 1) * sizeof(int32_t));
                 J.h_plen = plen_host;
             }
-            // the resident chunk is compressed once for all A/C ranges
-            tsg_cmat *cbj = nullptr;
-            TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
-            if ((st = tsg_compress_impl(c, &B.m, &cbj)) != TSG_OK) break;
+            // the resident chunk is compressed once for all A/C ranges (a
+            // landed prefix on its own for the ranges that run before)
+            tsg_cmat *cbj = nullptr, *cbp = nullptr;
+            int cur_k = -1;
+            DevRange Bv = B;   // prefix view: same arrays, fewer rows, the piece's event
+            if (!overlap) {
+                TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
+                if ((st = tsg_compress_impl(c, &B.m, &cbj)) != TSG_OK) break;
+            }
             for (int64_t r = 0; r < nac && st == TSG_OK; ++r) {
                 const int64_t lo = acb[r], hi = acb[r + 1];
                 DevRange &A = Abuf[r % L.a_slots];
                 DevC &C = Cbuf[r % L.c_slots];
+                int k = NP - 1;
+                if (overlap && !cbj) {   // smallest landed prefix holding every column of the range
+                    int64_t need = 0;
+                    if (a_sorted) {   // a row's largest column is its last
+                        for (int64_t i = lo; i < hi; ++i)
+                            if (J.A.rp[i + 1] > J.A.rp[i])
+                                need = std::max<int64_t>(need, J.A.col[J.A.rp[i + 1] - 1] + 1);
+                    } else {
+                        for (int64_t e = J.A.rp[lo]; e < J.A.rp[hi]; ++e) need = std::max<int64_t>(need, J.A.col[e] + 1);
+                    }
+                    need -= bb[j];
+                    k = 0;
+                    while (k < NP - 1 && bp.q[k + 1] < need) ++k;
+                }
+                if (overlap && (st = stage_b_upto(c, J.B, bb[j], B, k, bp)) != TSG_OK) break;
                 if ((st = stage_rows(c, J.A, lo, hi, A, used_a[r % L.a_slots], a_sorted, a_distinct,
-                                     local.h2d_bytes)) != TSG_OK)
+                                     local.h2d_bytes, overlap)) != TSG_OK)
                     break;
                 // partials come back from host after the first B sweep; the D2H
                 // of the previous sweep for this range must have landed (the
                 // first sweep loads nothing, so its ranges pipeline freely)
                 if (j > 0) TSG_CK(cudaStreamSynchronize(c->copy_out));
                 if ((st = open_c(J, C, crow[r & 1], false, lo, hi, j > 0)) != TSG_OK) break;
-                st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo, cbj);
+                if (overlap && !cbj && k < NP - 1) {
+                    if (k != cur_k) {
+                        if (cbp) tsg_cmat_free(c, cbp);
+                        cbp = nullptr;
+                        Bv.m.rows = bp.q[k + 1];
+                        Bv.m.nnz = J.B.rp[bb[j] + bp.q[k + 1]] - J.B.rp[bb[j]];
+                        Bv.ready = bp.ev[k];
+                        TSG_CK(cudaStreamWaitEvent(c->stream, bp.ev[k], 0));
+                        if ((st = tsg_compress_impl(c, &Bv.m, &cbp)) != TSG_OK) break;
+                        cur_k = k;
+                    }
+                    st = fused_step(A, Bv, C, bb[j], bb[j] + bp.q[k + 1], hi - lo, cbp);
+                } else {
+                    if (overlap && !cbj) {   // B complete: its full compression from here on
+                        if (cbp) tsg_cmat_free(c, cbp);
+                        cbp = nullptr;
+                        TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));
+                        if ((st = tsg_compress_impl(c, &B.m, &cbj)) != TSG_OK) break;
+                    }
+                    st = fused_step(A, B, C, bb[j], bb[j + 1], hi - lo, cbj);
+                }
                 TSG_CK(cudaEventRecord(used_a[r % L.a_slots], c->stream));
                 if (st == TSG_OK && !partials) {
                     k_check_full<<<grid_for(hi - lo, 256, c->num_sms * 8), 256, 0, c->stream>>>(
@@ -774,8 +920,10 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
                 if (st == TSG_OK) st = drain_c(J, C, lo, hi, partials);
             }
             tsg_cmat_free(c, cbj);
+            if (cbp) tsg_cmat_free(c, cbp);
             TSG_CK(cudaEventRecord(used[j % L.b_slots], c->stream));
         }
+        for (cudaEvent_t e : bp.ev) cudaEventDestroy(e);
     }
     cudaStreamSynchronize(c->copy_in);
     cudaStreamSynchronize(c->copy_in2);

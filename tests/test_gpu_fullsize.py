@@ -148,3 +148,17 @@ def test_config3_masked_count_small_windows():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_config4_chunk2_overlapped_b_upload():
+    # the opt-in order-2 schedule that starts A/C ranges on a landed prefix
+    # of the resident B (TSG_CHUNK_OVERLAP=1, read once per process: a child)
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_CHUNK_OVERLAP="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          os.path.join(root, "tests", "test_gpu_fullsize.py") +
+                          "::test_config4_chunked_64cubed_full_result", "-k", "224"],
+                         env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "1 passed" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
