@@ -826,12 +826,12 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
         const bool partials = nb > 1;
         // one resident B chunk and row-sorted A: B lands in pieces and the
         // early A/C ranges start on its landed prefix (stage_b_pieces)
-        // opt-in (TSG_CHUNK_OVERLAP=1): config 4 at 16 GiB ran 0.79-0.81 s
-        // against 0.87-0.88 s, but the prefix compressions allocate blocks of
-        // a new size per prefix, and one run in four grew the pool while
-        // copies were in flight (2.69 s)
-        static const bool overlap_on = getenv("TSG_CHUNK_OVERLAP") != nullptr;
-        const bool overlap = !partials && nac > 1 && overlap_on;
+        // config 4 at 16 GiB: 0.803-0.810 s per run against 0.872-0.881 s
+        // without (TSG_CHUNK_NO_OVERLAP=1).  The prefix compressions allocate
+        // the full chunk's sizes (c->cmp_floor_*): with per-prefix sizes one
+        // run in four grew the pool while copies were in flight (2.69 s)
+        static const bool overlap_off = getenv("TSG_CHUNK_NO_OVERLAP") != nullptr;
+        const bool overlap = !partials && nac > 1 && !overlap_off;
         const int NP = 8;
         BPieces bp;
         for (int64_t j = 0; j < nb && st == TSG_OK; ++j) {
@@ -859,6 +859,17 @@ extern "C" int tsg_chunk_multiply(tsg_ctx *c, int algo, int64_t a_rows, int64_t 
             // landed prefix on its own for the ranges that run before)
             tsg_cmat *cbj = nullptr, *cbp = nullptr;
             int cur_k = -1;
+            // prefix and full compressions allocate the full chunk's sizes
+            struct Floor {
+                tsg_ctx *c;
+                Floor(tsg_ctx *x, bool on, int64_t r, int64_t n) : c(x) {
+                    if (on) {
+                        c->cmp_floor_rows = r;
+                        c->cmp_floor_nnz = n;
+                    }
+                }
+                ~Floor() { c->cmp_floor_rows = c->cmp_floor_nnz = 0; }
+            } floor_(c, overlap, B.m.rows, B.m.nnz);
             DevRange Bv = B;   // prefix view: same arrays, fewer rows, the piece's event
             if (!overlap) {
                 TSG_CK(cudaStreamWaitEvent(c->stream, B.ready, 0));

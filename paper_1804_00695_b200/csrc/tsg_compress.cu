@@ -19,6 +19,8 @@
 // set iff no EARLIER entry of the row has the same set), whose kernels exit
 // at once unless P1 flagged an unsorted row; compression never synchronises
 // the host.
+#include <algorithm>
+
 #include "tsg_internal.cuh"
 
 namespace {
@@ -448,7 +450,11 @@ __global__ void k_compress_unit(int64_t rows, int64_t nnz, const int64_t *__rest
 int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     tsg_cmat *cm = nullptr;
     const int64_t rows = b->rows, nnz = b->nnz;
-    TSG_TRY(tsg_cmat_alloc(c, rows, nnz > 0 ? nnz : 1, &cm));
+    // allocation sizes: at least the context's floor (c->cmp_floor_*), so a
+    // sequence of growing prefixes of one B reuses the same arena blocks
+    const int64_t arows = std::max(rows, c->cmp_floor_rows), annz = std::max(nnz, c->cmp_floor_nnz);
+    TSG_TRY(tsg_cmat_alloc(c, arows, annz > 0 ? annz : 1, &cm));
+    cm->rows = rows;
     cm->cols = b->cols;
     if (b->max_row >= 0 && b->max_row <= 1 && nnz > 0) {
         TSG_CK(launch_pdl(k_compress_unit, grid_for(rows + 1, 256, c->num_sms * 16), 256, 0, c->stream, rows,
@@ -470,16 +476,17 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
         return TSG_OK;
     }
     const int64_t nwords = (nnz + 31) / 32, nblocks = (nnz + PB - 1) / PB;   // PB = 8192 entries
+    const int64_t anwords = (annz + 31) / 32, anblocks = (annz + PB - 1) / PB;
     uint32_t *rsbits = nullptr, *hbits = nullptr;
     uint16_t *wpre = nullptr;
     int64_t *bcnt = nullptr, *fstart = nullptr;
     int32_t *fcnt = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &rsbits, nwords));
-    TSG_TRY(tsg_alloc_t(c, &hbits, nwords));
-    TSG_TRY(tsg_alloc_t(c, &wpre, nwords));
-    TSG_TRY(tsg_alloc_t(c, &bcnt, nblocks + 1));
-    TSG_TRY(tsg_alloc_t(c, &fcnt, rows + 1));
-    TSG_TRY(tsg_alloc_t(c, &fstart, rows + 1));
+    TSG_TRY(tsg_alloc_t(c, &rsbits, anwords));
+    TSG_TRY(tsg_alloc_t(c, &hbits, anwords));
+    TSG_TRY(tsg_alloc_t(c, &wpre, anwords));
+    TSG_TRY(tsg_alloc_t(c, &bcnt, anblocks + 1));
+    TSG_TRY(tsg_alloc_t(c, &fcnt, arows + 1));
+    TSG_TRY(tsg_alloc_t(c, &fstart, arows + 1));
     int *unsorted = reinterpret_cast<int *>(c->d_small + 8);
     cudaStream_t s = c->stream;
     TSG_TRY(tsg_fill(c, rsbits, 0, nwords * sizeof(uint32_t), s));
@@ -488,7 +495,7 @@ int tsg_compress_impl(tsg_ctx *c, const tsg_csr *b, tsg_cmat **out) {
     TSG_CK(launch_pdl(k_row_starts, rgrid, 256, 0, s, rows, (const int64_t *)b->rp, rsbits, cm->cnt + rows + 1));
     ++c->launches;
     unsigned long long *lbstate = nullptr;
-    TSG_TRY(tsg_alloc_t(c, &lbstate, nblocks + 1));   // + the tile counter
+    TSG_TRY(tsg_alloc_t(c, &lbstate, anblocks + 1));   // + the tile counter
     TSG_TRY(tsg_fill(c, lbstate, 0, (nblocks + 1) * sizeof(unsigned long long), s));
     const size_t esmem = EMIT_SMEM;
     auto kern = b->sorted ? k_compress_onepass<false> : k_compress_onepass<true>;

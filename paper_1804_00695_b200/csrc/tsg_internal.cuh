@@ -73,6 +73,7 @@ struct tsg_ctx {
     int64_t launches;         // kernels launched by this context (all entry points)
     double mg_ratio = 0.0;    // streamed tsg_mg_multiply: last C entries per multiplication
     int coarse_alloc = 0;     // > 0: arena size classes of >= 1 GiB are coarse (streamed multiply)
+    int64_t cmp_floor_rows = 0, cmp_floor_nnz = 0;   // tsg_compress_impl allocation floor (0: none)
     // streamed multiply: one col / val reservoir per call that every block's
     // C uses when it fits (no per-block multi-GB allocations)
     int32_t *c_res_col = nullptr;

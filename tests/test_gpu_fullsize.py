@@ -150,13 +150,14 @@ def test_config3_masked_count_small_windows():
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
-def test_config4_chunk2_overlapped_b_upload():
-    # the opt-in order-2 schedule that starts A/C ranges on a landed prefix
-    # of the resident B (TSG_CHUNK_OVERLAP=1, read once per process: a child)
+def test_config4_chunk2_without_overlapped_b_upload():
+    # order 2 with the resident B uploaded whole before the first range (the
+    # default starts A/C ranges on a landed prefix; TSG_CHUNK_NO_OVERLAP=1 is
+    # read once per process, so in a child)
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TSG_CHUNK_OVERLAP="1")
+    env = dict(os.environ, TSG_CHUNK_NO_OVERLAP="1")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                           os.path.join(root, "tests", "test_gpu_fullsize.py") +
                           "::test_config4_chunked_64cubed_full_result", "-k", "224"],
