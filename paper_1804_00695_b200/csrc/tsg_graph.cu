@@ -359,7 +359,9 @@ extern "C" int tsg_graph_lower(tsg_ctx *c, const tsg_csr *g, int check, tsg_csr 
     tsg_free(c, pos);
     TSG_CK(cudaGetLastError());
     L->sorted = 1;
-    L->distinct = 0;   // duplicates of the input graph survive the relabelling
+    // a row-distinct graph stays row-distinct under the relabelling (a
+    // permutation); duplicates of any other graph survive it
+    L->distinct = g->distinct ? 1 : 0;
     L->max_row = h2[1];
     *out = L;
     return TSG_OK;

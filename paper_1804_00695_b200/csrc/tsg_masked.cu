@@ -81,7 +81,9 @@ template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ list, int64_t nlist,
                                                    MaskArgs a, uint64_t *slab, int64_t nwords, int64_t wwords,
                                                    const int64_t *__restrict__ coff, int64_t cut_base,
-                                                   const int32_t *__restrict__ cut) {
+                                                   const int32_t *__restrict__ cut, bool raw) {
+    // raw: L's rows are column-distinct, so testing L_j's raw columns equals
+    // the popcounts of its compressed sets
     extern __shared__ int4 smem[];
     __shared__ unsigned long long s_tot;
     __shared__ int s_warp[32];
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
             }
             if (win == 0 && !lower) kerr(a.err, KERR_NOTLOWER, i);
             __syncthreads();
-            if (MASK_RAW && nwin == 1) {
+            if (MASK_RAW && raw && nwin == 1) {
                 // L_j's raw columns (4 B each) tested against the bitmap
                 // instead of its compressed sets (12 B each, 0.64 sets per
                 // column at R-MAT scale 20): the tier is bound by re-reading
@@ -478,7 +480,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
             const int32_t *dl = list + off[MASK_DENSE];
             if (wwords == nwords) {
                 k_mask_dense<1024, true><<<ctas, 1024, smem, c->stream>>>(dl, nd, a, nullptr, nwords, wwords,
-                                                                          nullptr, 0, nullptr);
+                                                                          nullptr, 0, nullptr, l->distinct != 0);
                 ++c->launches;
             } else {
                 int32_t *ncut_e = nullptr, *ncut = nullptr;
@@ -514,7 +516,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
                     }
                     k_mask_dense<1024, true><<<(unsigned)std::min<int64_t>(nb, c->num_sms), 1024, smem,
                                                c->stream>>>(dl + b0, nb, a, nullptr, nwords, wwords, coff + b0,
-                                                            hc[b0], cut);
+                                                            hc[b0], cut, l->distinct != 0);
                     ++c->launches;
                     b0 = b1;
                 }
@@ -530,7 +532,7 @@ extern "C" int tsg_masked_count(tsg_ctx *c, const tsg_csr *l, const tsg_cmat *cl
             TSG_TRY(tsg_alloc_t(c, &dslab, (size_t)gs * nwords));
             TSG_TRY(tsg_fill(c, dslab, 0, (size_t)gs * nwords * 8, c->stream));
             k_mask_dense<MASK_SLAB_NT, false><<<gs, MASK_SLAB_NT, 0, c->stream>>>(
-                list + off[MASK_DENSE], nd, a, dslab, nwords, nwords, nullptr, 0, nullptr);
+                list + off[MASK_DENSE], nd, a, dslab, nwords, nwords, nullptr, 0, nullptr, l->distinct != 0);
             ++c->launches;
         }
         TSG_CK(cudaGetLastError());

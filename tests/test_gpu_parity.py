@@ -278,6 +278,29 @@ def test_masked_count_dense_hub_rows(rng):
     assert tsg.count_triangles(g) == want
 
 
+def test_masked_count_dense_rows_with_repeated_columns(rng):
+    # L rows that repeat a column: the reference ORs L_j's columns into sets
+    # (a repeat counts once inside L_j, but every entry of L_i counts), so the
+    # dense tier must not test L_j's raw columns here
+    n = 3000
+    up = np.triu(rng.random((n, n)) < 0.01, 1)
+    up[:2, 2:] = True
+    rows, cols = np.nonzero(up | up.T)
+    g = CsrMatrix.from_coo(rows, cols, None, n, n)
+    low = tsg.lower_triangle(g, tsg.degree_sort_permutation(g))
+    rp, ci = np.asarray(low.row_ptr), np.asarray(low.col_idx)
+    r = np.repeat(np.arange(n), np.diff(rp))
+    dup = rng.random(len(ci)) < 0.3                 # repeat 30 % of the entries
+    r2 = np.concatenate([r, r[dup]])
+    c2 = np.concatenate([ci, ci[dup]])
+    order = np.lexsort((c2, r2))
+    rp2 = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(r2, minlength=n), out=rp2[1:])
+    ld = CsrMatrix(n, n, rp2, c2[order].astype(np.int64), None)
+    want = O.masked_count(ld, O.compress(ld), workers=8)
+    assert tsg.masked_row_intersect_count(ld, tsg.compress(ld)) == want
+
+
 def test_empty_and_degenerate_shapes(rng):
     """Zero rows / columns / entries behave like the reference (empty results,
     no device errors), through every public entry point."""
