@@ -237,7 +237,10 @@ __host__ __device__ constexpr int gt_slice(int b) { return 512 << b; }
 #ifndef TSG_NUM_G1
 #define TSG_NUM_G1 8   // lanes per row of numeric bin 1 (config 2 R*A numeric: 4 -> 0.486 ms, 8 -> 0.362, 16 -> 0.547)
 #endif
-__host__ __device__ constexpr int gt_g(int b) { return b == 0 ? 8 : b == 1 ? TSG_NUM_G1 : (b == 2 ? 16 : 32); }
+#ifndef TSG_NUM_G0
+#define TSG_NUM_G0 8   // lanes per row of numeric bin 0 (config 1: 4 -> 0.167 ms, 8 -> 0.165)
+#endif
+__host__ __device__ constexpr int gt_g(int b) { return b == 0 ? TSG_NUM_G0 : b == 1 ? TSG_NUM_G1 : (b == 2 ? 16 : 32); }
 // symbolic tables are larger (bounded by compressed entries, not exact sets)
 __host__ __device__ constexpr int gt_g_sym(int b) { return b == 0 ? 8 : (b == 1 ? 16 : 32); }
 __host__ __device__ constexpr int gt_block(int b) { return b <= 4 ? 256 : (b == 5 ? 128 : 64); }
