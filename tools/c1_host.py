@@ -1,6 +1,15 @@
-import os, sys, time
-sys.path.insert(0, "/root/repo")
-from paper_1804_00695_b200 import _lib, generators as gen, kernel
+"""Config 1 (A*A, 2D Laplacian 256^2) wall time per multiply from the host:
+pipelined (the host runs ahead of the device) and synchronised after every
+multiply -- separates host launch / read-back cost from device time.
+
+    python tools/c1_host.py"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1804_00695_b200 import _lib, generators as gen, kernel  # noqa: E402
 ctx = _lib.Context.get(0)
 da = _lib.DeviceCsr.upload(gen.stencil(gen.LAPLACE2D, (256, 256)), ctx)
 for _ in range(20):
