@@ -545,3 +545,21 @@ def test_global_tier_size_classes(rng):
     a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.uniform(0.1, 1, len(r)), len(rows), n)
     b = random_csr(rng, n, cols, 60)
     assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=False, rtol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_big_row_tiers_random_battery(seed):
+    # random hub rows against random B of random width (dense tier in shared
+    # memory, windowed, L2 slab; CTA and global tiers; sorted and unsorted B)
+    # with small-integer values, so every tier must be exact
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2000, 12000))
+    cols = int(rng.choice([5000, 200_000, 2_500_000, 40_000_000]))
+    lens = [int(x) for x in rng.integers(1, 3000, size=6)] + [1, 2]
+    rows = [rng.choice(n, size=min(k, n), replace=False) for k in lens]
+    r = np.concatenate([np.full(len(x), i) for i, x in enumerate(rows)])
+    a = CsrMatrix.from_coo(r, np.concatenate(rows), rng.integers(1, 4, len(r)).astype(np.float64), len(rows), n)
+    b = random_csr(rng, n, cols, int(rng.integers(2, 80)))
+    b = CsrMatrix(b.num_rows, b.num_cols, b.row_ptr, b.col_idx, np.round(b.values * 4))
+    for bb in (b, canonicalize(b)):
+        assert_same_product(tsg.multiply(a, bb), O.multiply(a, bb), exact=True)
