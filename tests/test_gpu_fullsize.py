@@ -1,8 +1,8 @@
 """GPU parity at the BASELINE.json configuration sizes.
 
 configs 1 and 2 run at their full sizes and are compared with the oracle's
-full product; config 3 runs the device R-MAT pipeline at scales 16 and 18
-against golden counts of the same graphs (tests/golden/rmat_triangles.json)
+full product; config 3 runs the device R-MAT pipeline at scales 16, 18 and
+22 (the L2-slab dense bitmap) against golden counts of the same graphs (tests/golden/rmat_triangles.json)
 and a live oracle count; config 4's two plans (chunk1 7x3 and chunk2 5x1 at
 256^3) are reproduced at 64^3 with the caps scaled by 1/64 and the full C is
 compared; config 5's power-law A*A runs at R-MAT scale 14 (hub rows take the
@@ -67,7 +67,7 @@ def test_config2_device_resident_path_matches_host_api():
     assert np.array_equal(got.values.view(np.uint64), want.values.view(np.uint64))
 
 
-@pytest.mark.parametrize("scale", [16, 18])
+@pytest.mark.parametrize("scale", [16, 18, 22])   # 22: the L2-slab dense bitmap (4 M columns)
 def test_config3_rmat_triangles_golden(scale):
     from paper_1804_00695_b200.triangles import lower_triangle_device
     gold = BC.rmat_golden(scale)
