@@ -6,7 +6,9 @@ full product; config 3 runs the device R-MAT pipeline at scales 16, 18 and
 and a live oracle count; config 4's two plans (chunk1 7x3 and chunk2 5x1 at
 256^3) are reproduced at 64^3 with the caps scaled by 1/64 and the full C is
 compared; config 5's power-law A*A runs at R-MAT scale 14 (hub rows take the
-CTA, global and dense tiers) with the full result within 1e-12.
+CTA, global and dense tiers) with the full result exact (unit values), and at
+scale 18 through the streamed multiply (block value sums = multiplications,
+the hub row and random rows equal to the oracle's).
 
 Bar (BASELINE.json north_star): row pointers and per-row sorted columns
 bit-exact, fp64 values bit-exact for thread-group-tier rows (every row of
@@ -163,3 +165,34 @@ def test_config4_chunk2_without_overlapped_b_upload():
                           "::test_config4_chunked_64cubed_full_result", "-k", "224"],
                          env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "1 passed" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+def test_config5_rmat_scale14_full_product():
+    # power-law A*A: hub rows through the CTA, global and dense tiers; unit
+    # values, so every entry counts paths and the whole C is exact
+    a = gen.with_unit_values(gen.rmat_graph(14))
+    c = tsg.multiply(a, a)
+    assert_same_product(c, O.multiply(a, a, workers=W), exact=True)
+
+
+def test_config5_rmat_scale18_streamed():
+    # the bench's streamed mode at scale 18: C in several budget-sized blocks
+    # (one reservoir), each block's value sum = its multiplications exactly,
+    # and the hub row plus random rows equal the oracle's
+    from paper_1804_00695_b200 import distributed as D
+    da = gen.rmat_graph_device(18).set_values(1.0)
+    row_flops, total = _lib.d_row_flops(da, da)
+    _, st = D.mg_multiply(da, da, 8 << 30, keep_c=False)
+    assert st["blocks"] > 1
+    assert st["value_sum"] == float(total)
+    host = da.download()
+    cb = O.compress(host)
+    rng = np.random.default_rng(5)
+    rows = sorted({int(np.argmax(row_flops))} | {int(x) for x in rng.integers(0, host.num_rows, 6)})
+    for r in rows:
+        sub = CsrMatrix(1, host.num_cols, np.array([0, host.row_ptr[r + 1] - host.row_ptr[r]]),
+                        host.col_idx[host.row_ptr[r]:host.row_ptr[r + 1]],
+                        host.values[host.row_ptr[r]:host.row_ptr[r + 1]])
+        want = O.numeric(sub, host, O.symbolic(sub, cb))
+        c1, _ = D.mg_multiply(da.slice_rows(r, r + 1), da, 0, keep_c=True)
+        assert_same_product(c1.download(), want, exact=True)
