@@ -512,13 +512,14 @@ def run(args, dist=None):
 
 def secondary(args):
     """Configs 1, 3 and 4 at their BASELINE sizes, and config 5 at R-MAT
-    scale 20 (the scale-25 run is ``--config 5 --scale 25`` on 8 GPUs), for
-    the default N=1 run."""
+    scales 20 and 21 (the scale-25 run is ``--config 5 --scale 25`` on 8
+    GPUs), for the default N=1 run."""
     out = {}
     jobs = (("config1", config1, dict(steps=20)),
             ("config3", config3, dict(steps=5, scale=22)),
             ("config4", config4, dict(grid=256, hbm_cap_gib=8.0, extra_caps_gib=[16.0])),
-            ("config5", config5, dict(scale=20, steps=2, warmup=1, c_budget_gib=48.0)))
+            ("config5", config5, dict(scale=20, steps=2, warmup=1, c_budget_gib=48.0)),
+            ("config5_scale21", config5, dict(scale=21, steps=1, warmup=1, c_budget_gib=48.0)))
     for name, fn, over in jobs:
         a = argparse.Namespace(**vars(args))
         a.warmup = 3
