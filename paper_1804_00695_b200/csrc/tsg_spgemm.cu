@@ -2656,8 +2656,11 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
     if (n <= 0) return TSG_OK;
     const int64_t nw = dense_words(ncols);
     const int32_t *dl = bl.list + bl.off[BIN_DENSE];
-    static const int64_t WW = dense_win_param("TSG_SYM_WIN_WORDS", 24576);
-    if (nw * 8 > DENSE_SMEM && sorted_sets && !getenv("TSG_SYM_DENSE_L2")) {
+    // 64 KB windows (two CTAs per SM) once B exceeds 8192 sets: R-MAT scale
+    // 20 248 -> 205 ms, scale 21 ~880 -> 763 ms against one 128 / 192 KB
+    // window per SM; at scale 18 (4096 sets) one window stays faster
+    static const int64_t WW = dense_win_param("TSG_SYM_WIN_WORDS", 8192);
+    if ((nw * 8 > DENSE_SMEM || nw > WW) && sorted_sets && !getenv("TSG_SYM_DENSE_L2")) {
         // windowed shared-memory bitmaps; cut points in batches of rows
         const int64_t ww = nw < WW ? nw : WW;
         const int nwin = (int)((nw + ww - 1) / ww);
@@ -2691,7 +2694,7 @@ int launch_sym_dense(tsg_ctx *c, const Bins &bl, const SymArgs &a, int64_t ncols
             k_sym_dense_cut<<<grid_for(nb * 256, 256, c->num_sms * 16), 256, 0, c->stream>>>(
                 dl + b0, nb, a, ww, nwin, eoff + b0, coff + b0, hc[b0], cut);
             ++c->launches;
-            const unsigned grid = (unsigned)std::min<int64_t>(nb, c->num_sms);
+            const unsigned grid = (unsigned)std::min<int64_t>(nb, (int64_t)c->num_sms * dense_ctas_per_sm(smem));
             k_sym_dense<1024, 1><<<grid, 1024, smem, c->stream>>>(dl + b0, nb, a, nw, ww, nullptr, coff + b0, hc[b0],
                                                                 cut);
             ++c->launches;
