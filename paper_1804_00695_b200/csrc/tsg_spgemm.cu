@@ -1873,6 +1873,9 @@ __device__ __forceinline__ int64_t lower_col(const int32_t *__restrict__ col, in
     return s0;
 }
 
+#ifndef PREP_NT
+#define PREP_NT 256   // k_num_dense_prep block (R-MAT scale 20: 1024 -> 54.7 ms, 256 -> 47.7, 128 -> 48.8)
+#endif
 struct DenseWin {
     int W;        // positions per window block
     int sets;     // column sets (64-column words) per window block
@@ -2765,7 +2768,7 @@ int launch_num_dense(tsg_ctx *c, const Bins &bl, const NumArgs &a, int64_t ncols
         for (int64_t b0 = 0; b0 < n; b0 += batch) {
             const int64_t nb = n - b0 < batch ? n - b0 : batch;
             const int32_t *lst = bl.list + bl.off[BIN_DENSE] + b0;
-            k_num_dense_prep<1024><<<grid_for(nb, 1, c->num_sms * 2), 1024, 0, c->stream>>>(lst, nb, a, dw, nwin,
+            k_num_dense_prep<PREP_NT><<<grid_for(nb, 1, c->num_sms * (2048 / PREP_NT)), PREP_NT, 0, c->stream>>>(lst, nb, a, dw, nwin,
                                                                                              wst, ncut_e, ncut);
             ++c->launches;
             TSG_TRY(tsg_exclusive_scan_i32_to_i64(c, nwin, woff, nb));
