@@ -913,6 +913,9 @@ int launch_sym_merge(tsg_ctx *c, const ::BinLists<NBINS> &bl, const SymArgs &a);
 #ifndef DENSE_CH
 #define DENSE_CH 128   // elements per warp unit
 #endif
+#ifndef DENSE_CH_NUM
+#define DENSE_CH_NUM DENSE_CH   // numeric window unit (R-MAT scale 20: 64 -> 668 ms, 128 -> 649, 256 -> 664)
+#endif
 
 // Dense symbolic tier: the row's union is ORed into a shared-memory bitmap
 // of all of B's column sets (64-bit words, ORed as 32-bit halves), then the
@@ -2058,7 +2061,7 @@ __global__ void __launch_bounds__(NT) k_num_dense_win(const int32_t *__restrict_
             int c;
             double v;
         };
-        block_unit_enumerate<NT, DENSE_EB, DENSE_CH, BV>(
+        block_unit_enumerate<NT, DENSE_EB, DENSE_CH_NUM, BV>(
             a0, a1,
             [&](int64_t t, int64_t &st, int &ln, double &w) {
                 int k = a.acol[t];
