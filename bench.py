@@ -98,7 +98,9 @@ def config2_desc(dims, world, mults, nnz):
             "grid": list(dims), "multiplications": int(mults),
             "nnz": {k: int(v) for k, v in nnz.items()},
             "parallelism": ("row partition of R (coarse z-slabs) x%d" % world) if world > 1
-            else "single GPU"}
+            else "single GPU",
+            "l2_between_steps": "inputs larger than L2 (A > 0.7 GB) and a 252 MiB L2 flush before each "
+                                "timed step"}
 
 
 # ------------------------------------------------------------------ clocks
