@@ -254,7 +254,11 @@ __device__ __forceinline__ void block_unit_enumerate(int64_t a0, int64_t a1, Src
     static_assert(EB <= NT && EB % 32 == 0 && EB <= 1024 && CH % 32 == 0, "unit enumeration shape");
     __shared__ int64_t s_s0[EB];
     __shared__ double s_w[EB];
-    __shared__ int s_uinc[EB];
+    // unit prefix per entry, one pad word per G entries: the first search
+    // round reads s_uinc[lane * G + G - 1] (stride G, a 16-way bank conflict
+    // unpadded: 9 % of the dense numeric kernel's shared wavefronts)
+    constexpr int G = EB / 32;
+    __shared__ int s_uinc[EB + 32];
     __shared__ int s_len[EB];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t tb = a0; tb < a1; tb += EB) {
@@ -267,7 +271,7 @@ __device__ __forceinline__ void block_unit_enumerate(int64_t a0, int64_t a1, Src
         int utot;
         const int ux = block_excl_scan<NT>(nch, utot, s_warp);
         if (threadIdx.x < EB) {
-            s_uinc[threadIdx.x] = ux + nch;
+            s_uinc[threadIdx.x + threadIdx.x / G] = ux + nch;
             s_len[threadIdx.x] = ln;
             s_s0[threadIdx.x] = st;
             s_w[threadIdx.x] = w;
@@ -276,13 +280,13 @@ __device__ __forceinline__ void block_unit_enumerate(int64_t a0, int64_t a1, Src
         for (int u = wid; u < utot; u += NT / 32) {
             // first entry with s_uinc > u: two ballot rounds over EB / 32
             // groups (a 9-step binary search was a quarter of the instructions)
-            constexpr int G = EB / 32;
-            const unsigned g1 = __ballot_sync(0xffffffffu, s_uinc[lane * G + G - 1] <= u);
+            const unsigned g1 = __ballot_sync(0xffffffffu, s_uinc[lane * (G + 1) + G - 1] <= u);
             const int grp = __popc(g1);
-            const unsigned g2 = __ballot_sync(0xffffffffu, lane < G && s_uinc[grp * G + (lane < G ? lane : 0)] <= u);
+            const unsigned g2 =
+                __ballot_sync(0xffffffffu, lane < G && s_uinc[grp * (G + 1) + (lane < G ? lane : 0)] <= u);
             const int lo = grp * G + __popc(g2);
             const int le = s_len[lo];
-            const int q0 = (u - (s_uinc[lo] - (le + CH - 1) / CH)) * CH;
+            const int q0 = (u - (s_uinc[lo + lo / G] - (le + CH - 1) / CH)) * CH;
             const int64_t sb = s_s0[lo] + q0;
             const int cnt = le - q0 < CH ? le - q0 : CH;
             const double we = s_w[lo];
