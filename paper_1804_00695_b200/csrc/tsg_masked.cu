@@ -45,6 +45,9 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef MASK_RAW
 #define MASK_RAW 1
 #endif
+#ifndef MASK_CH
+#define MASK_CH 256   // raw columns per warp unit (R-MAT scale 22: 128 -> 49.8 ms, 256 -> 45.7, 512 -> 51.3)
+#endif
 // L2-slab dense tier shape, R-MAT scale 22: 1024 x 1 per SM 49.6 ms, 512 x 2
 // 64.8, 512 x 3 62.0, 256 x 4 96.7, 256 x 6 103.2
 #ifndef MASK_SLAB_NT
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ l
                 // column at R-MAT scale 20): the tier is bound by re-reading
                 // L_j rows from DRAM, and the sum of bit(c) over a row's
                 // distinct columns equals the sum of popcount(bits & word)
-                block_unit_enumerate<NT, (NT < 512 ? NT : 512), 128, int>(
+                block_unit_enumerate<NT, (NT < 512 ? NT : 512), MASK_CH, int>(
                     r0, r1,
                     [&](int64_t t, int64_t &st, int &len, double &) {
                         const int j = a.lcol[t];
