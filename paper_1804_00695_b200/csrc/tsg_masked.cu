@@ -45,6 +45,9 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef MASK_RAW
 #define MASK_RAW 1
 #endif
+#ifndef MASK_MINB
+#define MASK_MINB 1   // 2 (32 registers, spills, two slabs per SM): 66.6 ms against 48.4 at scale 22
+#endif
 #ifndef MASK_CH
 #define MASK_CH 256   // raw columns per warp unit (R-MAT scale 22: 128 -> 49.8 ms, 256 -> 45.7, 512 -> 51.3)
 #endif
@@ -81,7 +84,7 @@ struct MaskBinF {
 // word load + AND + popcount -- no hashing, no probing.  Only the words the
 // row touched are cleared afterwards.
 template <int NT, bool SMEM>
-__global__ void __launch_bounds__(NT) k_mask_dense(const int32_t *__restrict__ list, int64_t nlist,
+__global__ void __launch_bounds__(NT, MASK_MINB) k_mask_dense(const int32_t *__restrict__ list, int64_t nlist,
                                                    MaskArgs a, uint64_t *slab, int64_t nwords, int64_t wwords,
                                                    const int64_t *__restrict__ coff, int64_t cut_base,
                                                    const int32_t *__restrict__ cut, bool raw) {
