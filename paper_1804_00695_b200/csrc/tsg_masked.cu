@@ -45,6 +45,9 @@ constexpr int64_t MASK_DENSE_MIN = TSG_MASK_DENSE_MIN;
 #ifndef MASK_RAW
 #define MASK_RAW 1
 #endif
+#ifndef MASK_PIPE
+#define MASK_PIPE 1
+#endif
 #ifndef MASK_MINB
 #define MASK_MINB 1   // 2 (32 registers, spills, two slabs per SM): 66.6 ms against 48.4 at scale 22
 #endif
@@ -77,6 +80,72 @@ struct MaskBinF {
         return mask_bin(lrp[i + 1] - lrp[i], dense_ok);
     }
 };
+
+// Raw-column unit enumeration for the dense tier, software-pipelined: the
+// units are block_unit_enumerate's (EB entries per round, CH consecutive
+// columns of one L_j per unit, warps round-robin), but each warp issues the
+// column loads of its next unit before the bitmap lookups of the current one,
+// so the two dependent loads of a unit (column, then bitmap word) overlap
+// the next unit's first.
+template <int NT, int EB, int CH>
+__device__ __forceinline__ long long mask_raw_units(int64_t r0, int64_t r1, const MaskArgs &a,
+                                                    const uint64_t *bm, int *s_warp) {
+    constexpr int G = EB / 32, R = CH / 32;
+    __shared__ int64_t s_s0[EB];
+    __shared__ int s_uinc[EB + 32];   // one pad word per G entries (bank-distinct first search round)
+    __shared__ int s_len[EB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long mine = 0;
+    for (int64_t tb = r0; tb < r1; tb += EB) {
+        const int64_t t = tb + threadIdx.x;
+        int64_t st = 0;
+        int ln = 0;
+        if (threadIdx.x < EB && t < r1) {
+            const int j = a.lcol[t];
+            st = a.lrp[j];
+            ln = (int)(a.lrp[j + 1] - st);
+        }
+        const int nch = (ln + CH - 1) / CH;
+        int utot;
+        const int ux = block_excl_scan<NT>(nch, utot, s_warp);
+        if (threadIdx.x < EB) {
+            s_uinc[threadIdx.x + threadIdx.x / G] = ux + nch;
+            s_len[threadIdx.x] = ln;
+            s_s0[threadIdx.x] = st;
+        }
+        __syncthreads();
+        auto load_unit = [&](int u, int (&c)[R]) {
+            const unsigned g1 = __ballot_sync(0xffffffffu, s_uinc[lane * (G + 1) + G - 1] <= u);
+            const int grp = __popc(g1);
+            const unsigned g2 =
+                __ballot_sync(0xffffffffu, lane < G && s_uinc[grp * (G + 1) + (lane < G ? lane : 0)] <= u);
+            const int e = grp * G + __popc(g2);
+            const int le = s_len[e];
+            const int q0 = (u - (s_uinc[e + e / G] - (le + CH - 1) / CH)) * CH;
+            const int64_t sb = s_s0[e] + q0;
+            const int cnt = le - q0 < CH ? le - q0 : CH;
+#pragma unroll
+            for (int r = 0; r < R; ++r) c[r] = r * 32 + lane < cnt ? a.lcol[sb + r * 32 + lane] : -1;
+        };
+        int cur[R], nxt[R];
+        int u = wid;
+        if (u < utot) load_unit(u, cur);
+        for (; u < utot; u += NT / 32) {
+            const int un = u + NT / 32;
+            if (un < utot) load_unit(un, nxt);
+            uint64_t wv[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) wv[r] = cur[r] >= 0 ? bm[cur[r] >> 6] : 0ull;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (cur[r] >= 0) mine += (long long)((wv[r] >> (cur[r] & 63)) & 1ull);
+#pragma unroll
+            for (int r = 0; r < R; ++r) cur[r] = nxt[r];
+        }
+        __syncthreads();
+    }
+    return mine;
+}
 
 // Dense tier for long rows (power-law hubs): row i's columns become bits of
 // a bitmap over ALL columns (shared memory when it fits, else a per-CTA slab
@@ -125,16 +194,19 @@ __global__ void __launch_bounds__(NT, MASK_MINB) k_mask_dense(const int32_t *__r
                 // column at R-MAT scale 20): the tier is bound by re-reading
                 // L_j rows from DRAM, and the sum of bit(c) over a row's
                 // distinct columns equals the sum of popcount(bits & word)
-                block_unit_enumerate<NT, (NT < 512 ? NT : 512), MASK_CH, int>(
-                    r0, r1,
-                    [&](int64_t t, int64_t &st, int &len, double &) {
-                        const int j = a.lcol[t];
-                        st = a.lrp[j];
-                        len = (int)(a.lrp[j + 1] - st);
-                    },
-                    [&](int64_t s) { return a.lcol[s]; },
-                    [&](double, const int &c) { mine += (long long)((bm[c >> 6] >> (c & 63)) & 1ull); },
-                    s_warp);
+                if (MASK_PIPE && !SMEM)   // L2 bitmap: pipelined (scale 22: 48.0 -> 42.4 ms); shared bitmap: plain (scale 20: 6.3 vs 8.0)
+                    mine += mask_raw_units<NT, (NT < 512 ? NT : 512), MASK_CH>(r0, r1, a, bm, s_warp);
+                else
+                    block_unit_enumerate<NT, (NT < 512 ? NT : 512), MASK_CH, int>(
+                        r0, r1,
+                        [&](int64_t t, int64_t &st, int &len, double &) {
+                            const int j = a.lcol[t];
+                            st = a.lrp[j];
+                            len = (int)(a.lrp[j + 1] - st);
+                        },
+                        [&](int64_t s) { return a.lcol[s]; },
+                        [&](double, const int &c) { mine += (long long)((bm[c >> 6] >> (c & 63)) & 1ull); },
+                        s_warp);
             } else if (DENSE_UNITS) {
                 // units of DENSE_CH compressed sets of one L_j, balanced over
                 // the warps (a warp per whole entry left the block waiting on
