@@ -2525,6 +2525,14 @@ static int global_classes(tsg_ctx *c, const int32_t *list, int64_t n, const int6
     return TSG_OK;
 }
 
+// arena block released when the scope ends (stream-ordered, so after the
+// kernels queued in the scope), on error returns too
+struct ArenaGuard {
+    tsg_ctx *c;
+    void *p;
+    ~ArenaGuard() { tsg_free(c, p); }
+};
+
 int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     if (bl.device) return TSG_OK;   // excluded by the host's bounds (device_bins_ok)
     const int B = BIN_GLOBAL;
@@ -2533,6 +2541,7 @@ int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
     int32_t *cl = nullptr;
     int64_t off[GCLASSES + 1];
     TSG_TRY(global_classes(c, bl.list + bl.off[B], n, a.sbound, &cl, off));
+    ArenaGuard cl_guard{c, cl};
     for (int k = GCLASSES - 1; k >= 0; --k) {
         const int64_t nk = off[k + 1] - off[k];
         if (nk <= 0) continue;
@@ -2554,7 +2563,6 @@ int launch_sym_global(tsg_ctx *c, const Bins &bl, const SymArgs &a) {
         TSG_CK(cudaGetLastError());
         TSG_TRY(tsg_free(c, slab));
     }
-    TSG_TRY(tsg_free(c, cl));
     return TSG_OK;
 }
 
@@ -2567,6 +2575,7 @@ int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
     int32_t *cl = nullptr;
     int64_t off[GCLASSES + 1];
     TSG_TRY(global_classes(c, bl.list + bl.off[B], n, a.counts, &cl, off));
+    ArenaGuard cl_guard{c, cl};
     for (int k = GCLASSES - 1; k >= 0; --k) {
         const int64_t nk = off[k + 1] - off[k];
         if (nk <= 0) continue;
@@ -2592,7 +2601,6 @@ int launch_num_global(tsg_ctx *c, const Bins &bl, const NumArgs &a) {
         TSG_TRY(tsg_free(c, slab));
         TSG_TRY(tsg_free(c, sortslab));
     }
-    TSG_TRY(tsg_free(c, cl));
     return TSG_OK;
 }
 
