@@ -455,10 +455,12 @@ def test_fused_rap_falls_back_when_rows_do_not_fit():
         kernel.rap(r, p, a)
 
 
-def test_dense_numeric_small_windows():
+@pytest.mark.parametrize("knob", [{"TSG_DENSE_WIN": "777"}, {"TSG_DENSE_FLAT": "1"}])
+def test_dense_numeric_small_windows(knob):
     # the windowed dense numeric tier with 777-position windows (env read once
     # per process, so in a child): many window boundaries inside set words,
-    # every B row cut by binary search; compared with the oracle
+    # every B row cut at precomputed points; and the opt-in flat form (fp64
+    # REDs into C); compared with the oracle
     import os
     import subprocess
     import sys
@@ -480,7 +482,7 @@ def test_dense_numeric_small_windows():
         "assert_same_product(tsg.multiply(ai, bi), O.multiply(ai, bi), exact=True)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TSG_DENSE_WIN="777",
+    env = dict(os.environ, **knob,
                PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=600)
