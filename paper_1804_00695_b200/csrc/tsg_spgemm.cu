@@ -3728,6 +3728,7 @@ void tsg_plan_release_slot(void *plan, int slot) {
 }
 
 static int multiply_body(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_csr **out);
+static int multiply_small(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int64_t bound, tsg_csr **out);
 
 // capture slot `k` of a plan: the device-driven multiply recorded into a graph
 static int plan_capture(tsg_ctx *c, MulPlan *pl, int k) {
@@ -3850,8 +3851,98 @@ extern "C" int tsg_multiply(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_
     // the group / merge / thread tiers and the bounded allocations are small,
     // the multiply never waits for the device (no partition read-backs, C's
     // nnz left on the device) -- back-to-back multiplies queue without gaps.
+    // small products: the symbolic-free path (multiply_small), opt-in
+    // (TSG_SMALL_PATH=1): config 1's device span 0.167 -> 0.160 ms, but the
+    // host wall per multiply 141 -> 157 us synchronised, 117 -> 142 us
+    // pipelined (tools/c1_host.py) -- more host work per call than it saves
+    static const bool small_on = getenv("TSG_SMALL_PATH") != nullptr;
+    if (small_on && !c->c_host_out && !c->capture_owned && a->rows > 0 && a->rows <= ((int64_t)1 << 20) &&
+        b->max_row >= 0 && a->nnz > 0) {
+        const int64_t bound = a->nnz * std::max<int64_t>(b->max_row, 1);
+        if (bound <= ((int64_t)4 << 20)) return multiply_small(c, a, b, bound, out);
+    }
     plan_device_bins(c, a, b);
     return multiply_body(c, a, b, out);
+}
+
+// C rows from padded rows (capacity = the row's multiplications) to CSR
+__global__ void k_compact_rows(int64_t rows, const int64_t *__restrict__ pptr, const int32_t *__restrict__ plen,
+                               const int64_t *__restrict__ cptr, const int32_t *__restrict__ pcol,
+                               const double *__restrict__ pval, int32_t *__restrict__ ccol,
+                               double *__restrict__ cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < rows; i += nw) {
+        const int64_t s = pptr[i], d = cptr[i];
+        const int n = plen[i];
+        for (int q = lane; q < n; q += 32) {
+            ccol[d + q] = pcol[s + q];
+            cval[d + q] = pval[s + q];
+        }
+    }
+}
+
+// Small products (config-1 sized): no symbolic phase.  Every row of C is
+// built at a capacity of its multiplications by the fused in-place numeric
+// step (the chunked executors' kernels: same union, same ordered values, C
+// columns ascending), its length comes back per row, and one scan + copy
+// compacts the rows.  One partition read-back instead of two, no symbolic
+// kernels; C's nnz stays on the device (lazy, like the device-driven path).
+static int multiply_small(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, int64_t bound, tsg_csr **out) {
+    const int64_t rows = a->rows;
+    tsg_cmat *cb = nullptr;
+    TSG_TRY(tsg_compress_impl(c, b, &cb));
+    int64_t *flops = nullptr, *pptr = nullptr;
+    int32_t *plen = nullptr, *pcol = nullptr;
+    double *pval = nullptr;
+    int st = tsg_alloc_t(c, &flops, rows + 1);
+    if (st == TSG_OK) st = tsg_alloc_t(c, &pptr, rows + 1);
+    if (st == TSG_OK) st = tsg_alloc_t(c, &plen, rows + 1);
+    if (st == TSG_OK) st = tsg_alloc_t(c, &pcol, bound + 1);
+    if (st == TSG_OK) st = tsg_alloc_t(c, &pval, bound + 1);
+    tsg_csr *C = nullptr;
+    if (st == TSG_OK) {
+        launch_bounds(c, a, b->rp, nullptr, flops, nullptr, nullptr);
+        st = tsg_exclusive_scan_i64(c, flops, pptr, rows);
+    }
+    if (st == TSG_OK) st = tsg_fill(c, plen, 0, (rows + 1) * sizeof(int32_t), c->stream);
+    if (st == TSG_OK)
+        st = tsg_fused_inplace(c, a, 0, 0x7fffffff, b, cb, pptr, flops, pcol, pval, plen, rows);
+    if (st == TSG_OK) {
+        C = new tsg_csr();
+        C->max_row = -1;
+        C->rows = rows;
+        C->cols = b->cols;
+        C->nnz = bound;   // capacity; the exact count is rp[rows] on the device
+        C->lazy_nnz = 1;
+        C->owner = c;
+        C->sorted = 1;
+        C->distinct = 1;
+        st = tsg_alloc_t(c, &C->rp, rows + 1);
+        if (st == TSG_OK) st = tsg_alloc_t(c, &C->col, bound + 1);
+        if (st == TSG_OK) st = tsg_alloc_t(c, &C->val, bound + 1);
+        if (st == TSG_OK) st = tsg_exclusive_scan_i32_to_i64(c, plen, C->rp, rows);
+        if (st == TSG_OK) {
+            k_compact_rows<<<grid_for(rows, 8, c->num_sms * 16), 256, 0, c->stream>>>(rows, pptr, plen, C->rp, pcol,
+                                                                                   pval, C->col, C->val);
+            ++c->launches;
+            if (cudaGetLastError() != cudaSuccess) st = TSG_ECUDA;
+        }
+        if (st != TSG_OK) {
+            tsg_csr_free(c, C);
+            C = nullptr;
+        }
+    }
+    tsg_free(c, flops);
+    tsg_free(c, pptr);
+    tsg_free(c, plen);
+    tsg_free(c, pcol);
+    tsg_free(c, pval);
+    tsg_cmat_free(c, cb);
+    if (st == TSG_OK) *out = C;
+    ++c->num_calls;
+    return st;
 }
 
 static int multiply_body(tsg_ctx *c, const tsg_csr *a, const tsg_csr *b, tsg_csr **out) {

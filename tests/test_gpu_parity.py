@@ -565,3 +565,32 @@ def test_big_row_tiers_random_battery(seed):
     b = CsrMatrix(b.num_rows, b.num_cols, b.row_ptr, b.col_idx, np.round(b.values * 4))
     for bb in (b, canonicalize(b)):
         assert_same_product(tsg.multiply(a, bb), O.multiply(a, bb), exact=True)
+
+
+def test_small_product_path_against_oracle():
+    # the opt-in symbolic-free path for small products (TSG_SMALL_PATH=1,
+    # read once per process: a child) on random pairs and config 1's A*A
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "import paper_1804_00695_b200 as tsg\n"
+        "from paper_1804_00695_b200 import generators as gen\n"
+        "from oracle import oracle as O\n"
+        "from conftest import assert_same_product, random_csr\n"
+        "rng = np.random.default_rng(3)\n"
+        "for _ in range(12):\n"
+        "    m, k, n = (int(x) for x in rng.integers(1, 400, 3))\n"
+        "    a = random_csr(rng, m, k, int(rng.integers(1, 20)))\n"
+        "    b = random_csr(rng, k, n, int(rng.integers(1, 20)))\n"
+        "    assert_same_product(tsg.multiply(a, b), O.multiply(a, b), exact=True)\n"
+        "a = gen.stencil(gen.LAPLACE2D, (256, 256))\n"
+        "assert_same_product(tsg.multiply(a, a), O.multiply(a, a), exact=True)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_SMALL_PATH="1",
+               PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
